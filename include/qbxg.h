@@ -1,0 +1,261 @@
+/*
+ * qbxg.h -- C ABI of the B200-native GIGAQBX-FMM evaluation path.
+ *
+ * Drop-in boundary for the reference's in-process C++ API (namespace qbx):
+ *   - qbxg_direct_sum   replaces qbx::direct_sum
+ *                       (/root/reference/proj/include/qbx3d/kernels.hpp:39-40,
+ *                        /root/reference/proj/src/kernels.cpp:46-73)
+ *   - qbxg_plan_create  replaces build_tree + build_lists
+ *                       (declared in
+ *                        proj/CMakeLists.txt:24-25 as src/tree.cpp, src/interaction_lists.cpp)
+ *   - qbxg_create/qbxg_apply replace execute(bundle, density, FmmConfig)
+ *                       (Algorithm 4 Stages 2-9 at PAPER.md:2343-2430;
+ *                        declared as src/fmm.cpp in proj/CMakeLists.txt:27)
+ *   - qbxg_plan_ledger  replaces modeled_flops / CostLedger
+ *   - qbxg_geometry_*   procedural inputs of BASELINE.json configs 0-4;
+ *                       stands in for gen_sphere / gen_urchin
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; all arrays are host memory unless the
+ *     function name ends in _device.
+ *   - Positions are AoS double[3*N], byte-compatible with std::vector<qbx::Vec3>
+ *     (/root/reference/proj/include/qbx3d/vec3.hpp:9-10: three doubles, 24 B).
+ *   - Source weights are premultiplied (quadrature weight x density) and dipole
+ *     moments are weight x density x normal, exactly as qbx::SourceEnsemble
+ *     (/root/reference/proj/include/qbx3d/kernels.hpp:16-22).
+ *   - Target association follows qbx::TargetSet::association
+ *     (/root/reference/proj/include/qbx3d/kernels.hpp:31-35): >=0 centre id, -1 conventional.
+ *   - Potentials include the 1/(4 pi) of G, as direct_sum does
+ *     (/root/reference/proj/src/kernels.cpp:67).
+ *   - Centre coefficients are returned in the paper's normalisation, Eq. (5)/(8)
+ *     (PAPER.md:287-289, 326-330): local coefficient (L_c)_n^m for 0<=m<=n<=p_qbx,
+ *     packed n-major at index n(n+1)/2+m, interleaved (re,im); (L_c)_n^{-m} is the
+ *     complex conjugate for real densities.
+ *   - Every function returns a status code; no C++ exception crosses the ABI.
+ *     qbxg_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef QBXG_H_
+#define QBXG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirror the reference's exception classes) ---------- */
+enum {
+  QBXG_OK = 0,
+  QBXG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (kernels.cpp:28-36)   */
+  QBXG_ERR_DOMAIN = 2,           /* std::domain_error     (kernels.cpp:15,22,69) */
+  QBXG_ERR_CUDA = 3,
+  QBXG_ERR_NCCL = 4,
+  QBXG_ERR_INTERNAL = 5,
+  QBXG_ERR_NO_DEVICE = 6
+};
+
+enum {
+  QBXG_KERNEL_LAPLACE_SL = 0,    /* single layer: sum w G                     */
+  QBXG_KERNEL_LAPLACE_SL_DL = 1, /* single + double layer: sum w G + m.grad_y G */
+  QBXG_KERNEL_HELMHOLTZ_SL = 2   /* reserved: not implemented in this build    */
+};
+
+/* Interaction-list kinds (Definitions 1-8). */
+enum {
+  QBXG_LIST_U = 0,       /* List 1                 */
+  QBXG_LIST_V = 1,       /* List 2                 */
+  QBXG_LIST_W_CLOSE = 2, /* List 3 close           */
+  QBXG_LIST_W_FAR = 3,   /* List 3 far             */
+  QBXG_LIST_X_CLOSE = 4, /* List 4 close           */
+  QBXG_LIST_X_FAR = 5,   /* List 4 far             */
+  QBXG_NUM_LISTS = 6
+};
+
+/* Stages timed by qbxg_apply (CUDA events). */
+enum {
+  QBXG_T_H2D = 0,      /* density upload + permutation                 */
+  QBXG_T_P2M = 1,      /* Stage 2 leaf formation                        */
+  QBXG_T_M2M = 2,      /* Stage 2 postorder shifts                      */
+  QBXG_T_NEAR = 3,     /* Stages 3, 5a, 6a: P2QBXL + P2P over U, W_close, X_close */
+  QBXG_T_M2L = 4,      /* Stage 4                                       */
+  QBXG_T_WFAR = 5,     /* Stage 5b: M2QBXL + M2P                        */
+  QBXG_T_P2L = 6,      /* Stage 6b                                      */
+  QBXG_T_L2L = 7,      /* Stage 7                                       */
+  QBXG_T_L2QBXL = 8,   /* Stage 8                                       */
+  QBXG_T_EVAL = 9,     /* Stage 9: QBXL2P + L2P + sum                   */
+  QBXG_T_D2H = 10,     /* result download + un-permutation              */
+  QBXG_T_TOTAL = 11,
+  QBXG_NUM_TIMERS = 12
+};
+
+typedef struct {
+  int32_t p_fmm;        /* FMM order (p)                                  */
+  int32_t p_qbx;        /* QBX order (q), q <= p            */
+  double t_f;           /* target confinement factor, < 2 sqrt(3) - 2     */
+  int32_t n_max;        /* max particles (sources+centres+targets) per box */
+  int32_t kernel;       /* QBXG_KERNEL_*                                  */
+  double helmholtz_k;   /* reserved                                       */
+  int32_t w_far_demote; /* Remark 1: a List-3-far box whose
+                           subtree holds fewer than this many sources is replaced by
+                           its source leaves in List 3 close; 0 disables.  */
+  int32_t reserved;     /* must be 0 (level restriction not implemented)   */
+} qbxg_config;
+
+typedef struct {
+  int64_t n_sources;
+  const double* source_pos;    /* 3*n_sources                             */
+  int64_t n_centers;
+  const double* center_pos;    /* 3*n_centers                             */
+  const double* center_radius; /* n_centers                               */
+  int64_t n_targets;
+  const double* target_pos;    /* 3*n_targets                             */
+  const int32_t* association;  /* n_targets: centre id or -1              */
+} qbxg_geometry;
+
+/* ---- procedural inputs (BASELINE.json configs) ---------- */
+enum { QBXG_SURF_ICOSPHERE = 0, QBXG_SURF_TORUS = 1, QBXG_SURF_URCHIN = 2, QBXG_SURF_URCHIN_ARRAY = 3 };
+enum { QBXG_DENS_UNIFORM = 0, QBXG_DENS_ONES = 1, QBXG_DENS_FOURIER8 = 2, QBXG_DENS_COMPLEX_UNIFORM = 3 };
+
+typedef struct {
+  int32_t surface;        /* QBXG_SURF_*                                   */
+  int32_t level;          /* icosphere subdivision level                   */
+  int32_t nu, nv;         /* torus grid                                    */
+  int32_t nx, ny, nz;     /* urchin array dimensions                       */
+  double spacing;         /* urchin array spacing                          */
+  int32_t density;        /* QBXG_DENS_*                                   */
+  int32_t reserved;
+  int64_t n_volume_targets; /* uniform volume targets drawn before filtering */
+  double volume_halfwidth;  /* cube [-hw, hw]^3                            */
+  uint64_t seed;
+} qbxg_geometry_spec;
+
+typedef struct qbxg_generated qbxg_generated;
+
+typedef struct {
+  int64_t n_triangles;
+  int64_t n_sources;
+  const double* source_pos;    /* 3*n_sources                               */
+  const double* source_normal; /* 3*n_sources, unit normals                 */
+  const double* quad_weight;   /* n_sources (area-scaled Duffy weights)     */
+  const double* density;       /* n_sources (real) or 2*n_sources (complex) */
+  int32_t density_is_complex;
+  int64_t n_centers;
+  const double* center_pos;
+  const double* center_radius;
+  int64_t n_targets;           /* 2*n_sources on-surface + retained volume  */
+  const double* target_pos;
+  const int32_t* association;
+  int64_t n_volume_drawn;      /* volume targets drawn (before filtering)   */
+} qbxg_generated_view;
+
+int qbxg_geometry_spec_for_config(int32_t config_id, int32_t variant, uint64_t seed,
+                                  qbxg_geometry_spec* out);
+int qbxg_geometry_generate(const qbxg_geometry_spec* spec, qbxg_generated** out);
+int qbxg_geometry_view(const qbxg_generated* g, qbxg_generated_view* out);
+void qbxg_geometry_destroy(qbxg_generated* g);
+
+/* ---- host tree + interaction lists (Stage 1, stays in host C++) --------- */
+typedef struct qbxg_plan qbxg_plan;
+
+typedef struct {
+  int32_t n_boxes;
+  int32_t n_levels;
+  double root_center[3];
+  double root_radius;             /* l-inf half width |root|              */
+  const double* box_center;       /* 3*n_boxes                            */
+  const double* box_radius;       /* n_boxes (|b|)                        */
+  const int32_t* box_level;       /* n_boxes                              */
+  const int32_t* box_parent;      /* n_boxes (-1 for root)                */
+  const int32_t* child_starts;    /* n_boxes+1 (CSR into children)        */
+  const int32_t* children;
+  const int32_t* level_starts;    /* n_levels+1 (CSR into level_boxes)    */
+  const int32_t* level_boxes;
+  /* per-role ranges in the box-sorted particle arrays (DFS preorder)     */
+  const int32_t* src_own_start; const int32_t* src_own_count;
+  const int32_t* src_sub_start; const int32_t* src_sub_count;
+  const int32_t* ctr_own_start; const int32_t* ctr_own_count;
+  const int32_t* ctr_sub_start; const int32_t* ctr_sub_count;
+  const int32_t* tgt_own_start; const int32_t* tgt_own_count;  /* conventional targets */
+  const int32_t* tgt_sub_start; const int32_t* tgt_sub_count;
+  int64_t n_sources, n_centers, n_conv_targets, n_targets;
+  const int32_t* src_perm;        /* sorted pos -> original source index   */
+  const int32_t* ctr_perm;        /* sorted pos -> original centre index   */
+  const int32_t* tgt_perm;        /* sorted pos -> original target index (conventional only) */
+  const uint8_t* box_flags;       /* bit0 target box, bit1 target-ancestor, bit2 has sources in subtree, bit3 leaf */
+  const int64_t* list_starts[QBXG_NUM_LISTS]; /* n_boxes+1 each           */
+  const int32_t* list_boxes[QBXG_NUM_LISTS];
+  uint64_t list_hash[QBXG_NUM_LISTS];         /* FNV-1a over (starts, boxes) */
+  double build_seconds_tree, build_seconds_lists;
+} qbxg_plan_view;
+
+enum { QBXG_BOX_TARGET = 1, QBXG_BOX_TARGET_ANCESTOR = 2, QBXG_BOX_HAS_SOURCES = 4, QBXG_BOX_LEAF = 8 };
+
+/* Modeled operation counts, Table 3, plus pair counts. */
+typedef struct {
+  double modeled[QBXG_NUM_LISTS]; /* per list kind                         */
+  double modeled_total;
+  int64_t entries[QBXG_NUM_LISTS];/* list entries over evaluated boxes     */
+  int64_t pairs_qbx_near;         /* (source, centre) pairs, lists 1, 3c, 4c */
+  int64_t pairs_p2p_near;         /* (source, conventional target) pairs   */
+  int64_t pairs_wfar_centre;      /* (W_far box, centre) pairs             */
+  int64_t pairs_wfar_target;      /* (W_far box, conventional target) pairs */
+  int64_t pairs_xfar_source;      /* (source, X_far target box) pairs      */
+  int64_t n_m2m, n_l2l;           /* child->parent shifts                  */
+  int64_t n_p2m_sources;
+  int64_t n_l2qbxl_centres;
+  int64_t n_l2p_targets;
+  int64_t n_qbxl2p_targets;
+} qbxg_ledger;
+
+int qbxg_plan_create(const qbxg_config* cfg, const qbxg_geometry* geom, qbxg_plan** out);
+int qbxg_plan_view_get(const qbxg_plan* plan, qbxg_plan_view* out);
+int qbxg_plan_ledger(const qbxg_plan* plan, qbxg_ledger* out);
+void qbxg_plan_destroy(qbxg_plan* plan);
+
+/* ---- device evaluation (Stages 2-9 on one B200) ------------------------ */
+typedef struct qbxg_handle qbxg_handle;
+
+typedef struct {
+  double ms[QBXG_NUM_TIMERS];     /* CUDA-event times of the last apply    */
+  int32_t kernel_launches;        /* kernels launched by the last apply    */
+  int64_t h2d_bytes, d2h_bytes;
+} qbxg_timings;
+
+/* Upload geometry, box-sorted particle data, tree and lists; build operator
+ * tables.  The plan must have been created from the same cfg and geometry. */
+int qbxg_create(const qbxg_config* cfg, const qbxg_geometry* geom, const qbxg_plan* plan,
+                int32_t device, qbxg_handle** out);
+
+/* Host-buffer apply (e2e).  weights: n_sources; dipoles: 3*n_sources or NULL
+ * (required for QBXG_KERNEL_LAPLACE_SL_DL); out_target_pot: n_targets;
+ * out_center_coeffs: NULL or n_centers*2*K_q (K_q=(q+1)(q+2)/2) doubles. */
+int qbxg_apply(qbxg_handle* h, const double* weights, const double* dipoles,
+               double* out_target_pot, double* out_center_coeffs, qbxg_timings* timings);
+
+/* Device-buffer apply: same layout, pointers in device memory of the handle's
+ * GPU, original (caller) ordering; stream may be NULL (handle stream). */
+int qbxg_apply_device(qbxg_handle* h, const double* d_weights, const double* d_dipoles,
+                      double* d_out_target_pot, double* d_out_center_coeffs,
+                      void* cuda_stream, qbxg_timings* timings);
+
+int qbxg_destroy(qbxg_handle* h);
+
+/* ---- near-field P2P, the GPU counterpart of qbx::direct_sum ------------ */
+/* pot[i] = (1/4pi) sum_j [w_j/|x_i-y_j| + m_j.(x_i-y_j)/|x_i-y_j|^3].
+ * Returns QBXG_ERR_DOMAIN when a target coincides with a source (message names
+ * the pair, as kernels.cpp:69-71) and QBXG_ERR_INVALID_ARGUMENT on non-finite
+ * source data (kernels.cpp:27-38). */
+int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* weights,
+                    const double* dipoles_or_null, int64_t n_targets, const double* target_pos,
+                    double* out_pot);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char* qbxg_last_error(void);
+int qbxg_device_count(int32_t* out);
+const char* qbxg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QBXG_H_ */

@@ -1,0 +1,202 @@
+"""ORACLE -- test infrastructure only.
+
+ctypes loader for oracle/liboracle.so (CPU restatement of the QBX-FMM path)
+and oracle/_ref/libqbxref.so (the reference's own qbx::direct_sum compiled from
+/root/reference/proj/src/kernels.cpp).  Only tests/, __graft_entry__.smoke()
+and bench.py's CPU legs may import this package; the product path never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libqbxref.so")
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+_o = None
+_r = None
+
+
+def lib():
+    global _o
+    if _o is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.qbxo_last_error.restype = C.c_char_p
+        L.qbxo_sph_harm.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+        L.qbxo_form_expansion.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, C.c_int, _dp]
+        L.qbxo_eval_expansion.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _dp]
+        L.qbxo_translate.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, C.c_int, _dp]
+        L.qbxo_form_internal.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, C.c_int, _dp]
+        L.qbxo_eval_internal.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _dp]
+        L.qbxo_execute.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _i32p, _dp, _dp,
+                                   _dp, _dp, _dp]
+        L.qbxo_direct_qbx.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _i32p, C.c_int,
+                                      _dp]
+        L.qbxo_lists_brute.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int64, _i64p * 6, _i32p * 6, _i64p]
+        _o = L
+    return _o
+
+
+def ref_lib():
+    """The reference's own direct_sum (oracle/_ref).  None when not built."""
+    global _r
+    if _r is None:
+        if not os.path.exists(REF_SO):
+            try:
+                build()
+            except Exception:
+                pass
+        if not os.path.exists(REF_SO):
+            return None
+        L = C.CDLL(REF_SO)
+        L.qbxref_last_error.restype = C.c_char_p
+        L.qbxref_direct_sum.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp]
+        L.qbxref_laplace_green.argtypes = [_dp, _dp, _dp]
+        L.qbxref_laplace_dipole.argtypes = [_dp, _dp, _dp, _dp]
+        _r = L
+    return _r
+
+
+def _p(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(_dp)
+
+
+def _chk(st, L):
+    if st == 0:
+        return
+    msg = L.qbxo_last_error().decode() if L is _o else L.qbxref_last_error().decode()
+    if st == 1:
+        raise ValueError(msg)
+    if st == 2:
+        raise ArithmeticError(msg)
+    raise RuntimeError(msg)
+
+
+def sph_harm(n, m, theta, phi):
+    out = np.zeros(2)
+    _chk(lib().qbxo_sph_harm(n, m, theta, phi, out.ctypes.data_as(_dp)), _o)
+    return complex(out[0], out[1])
+
+
+def form_expansion(kind, pos, w, mu, center, p):
+    """Paper normalisation (Eq. (5)/(10)); kind 'multipole' | 'local'; full table n^2+n+m."""
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    w = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+    out = np.zeros(2 * (p + 1) ** 2)
+    _chk(lib().qbxo_form_expansion(0 if kind == "multipole" else 1, pos.shape[0], _p(pos), _p(w),
+                                   _p(None if mu is None else np.asarray(mu).reshape(-1, 3)), _p(center), p,
+                                   out.ctypes.data_as(_dp)), _o)
+    return out[0::2] + 1j * out[1::2]
+
+
+def eval_expansion(kind, coeffs, p, center, t):
+    c = np.zeros(2 * (p + 1) ** 2)
+    c[0::2] = np.real(coeffs)
+    c[1::2] = np.imag(coeffs)
+    out = np.zeros(1)
+    _chk(lib().qbxo_eval_expansion(0 if kind == "multipole" else 1, _p(c), p, _p(center), _p(t),
+                                   out.ctypes.data_as(_dp)), _o)
+    return float(out[0])
+
+
+def form_internal(kind, pos, w, mu, center, p):
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(2 * (p + 1) ** 2)
+    _chk(lib().qbxo_form_internal(0 if kind == "multipole" else 1, pos.shape[0], _p(pos), _p(w),
+                                  _p(None if mu is None else np.asarray(mu).reshape(-1, 3)), _p(center), p,
+                                  out.ctypes.data_as(_dp)), _o)
+    return out[0::2] + 1j * out[1::2]
+
+
+def eval_internal(kind, coeffs, p, center, t):
+    c = np.zeros(2 * (p + 1) ** 2)
+    c[0::2] = np.real(coeffs)
+    c[1::2] = np.imag(coeffs)
+    out = np.zeros(1)
+    _chk(lib().qbxo_eval_internal(0 if kind == "multipole" else 1, _p(c), p, _p(center), _p(t),
+                                  out.ctypes.data_as(_dp)), _o)
+    return float(out[0])
+
+
+def translate(kind, coeffs, p, c, C_, q):
+    k = {"M2M": 0, "M2L": 1, "L2L": 2}[kind]
+    a = np.zeros(2 * (p + 1) ** 2)
+    a[0::2] = np.real(coeffs)
+    a[1::2] = np.imag(coeffs)
+    out = np.zeros(2 * (q + 1) ** 2)
+    _chk(lib().qbxo_translate(k, _p(a), p, _p(c), _p(C_), q, out.ctypes.data_as(_dp)), _o)
+    return out[0::2] + 1j * out[1::2]
+
+
+def execute(plan, geom, weights, dipoles=None, want_centers=False):
+    """Stages 2-9 on the CPU over the product's host tree and lists (plan)."""
+    cfg = plan.cfg
+    pot = np.empty(geom.n_targets)
+    kq = cfg.kq
+    coeffs = np.empty(geom.n_centers * 2 * kq) if want_centers else None
+    stages = np.zeros(8)
+    keep = [np.ascontiguousarray(weights, dtype=np.float64), None if dipoles is None else
+            np.ascontiguousarray(dipoles, dtype=np.float64)]
+    _chk(lib().qbxo_execute(C.addressof(plan.view), cfg.p_fmm, cfg.p_qbx, cfg.t_f, _p(geom.source_pos),
+                            _p(geom.center_pos), _p(geom.center_radius), _p(geom.target_pos),
+                            geom.association.ctypes.data_as(_i32p), _p(keep[0]), _p(keep[1]),
+                            pot.ctypes.data_as(_dp), None if coeffs is None else coeffs.ctypes.data_as(_dp),
+                            stages.ctypes.data_as(_dp)), _o)
+    if want_centers:
+        c = coeffs.reshape(geom.n_centers, kq, 2)
+        return pot, c[..., 0] + 1j * c[..., 1], stages
+    return pot, stages
+
+
+def direct_qbx(geom, weights, dipoles, q):
+    pot = np.empty(geom.n_targets)
+    _chk(lib().qbxo_direct_qbx(geom.n_sources, _p(geom.source_pos), _p(weights), _p(dipoles), geom.n_centers,
+                               _p(geom.center_pos), _p(geom.center_radius), geom.n_targets, _p(geom.target_pos),
+                               geom.association.ctypes.data_as(_i32p), q, pot.ctypes.data_as(_dp)), _o)
+    return pot
+
+
+def lists_brute(plan):
+    """Definitional lists on the plan's tree: dict name -> (starts, boxes)."""
+    v = plan.view
+    nb = v.n_boxes
+    cap = 4 * nb * nb + 16
+    starts = [np.zeros(nb + 1, dtype=np.int64) for _ in range(6)]
+    boxes = [np.zeros(cap, dtype=np.int32) for _ in range(6)]
+    counts = np.zeros(6, dtype=np.int64)
+    sp = (_i64p * 6)(*[s.ctypes.data_as(_i64p) for s in starts])
+    bp = (_i32p * 6)(*[b.ctypes.data_as(_i32p) for b in boxes])
+    st = lib().qbxo_lists_brute(C.addressof(v), plan.cfg.t_f, plan.cfg.w_far_demote, cap, sp, bp,
+                                counts.ctypes.data_as(_i64p))
+    if st != 0:
+        raise RuntimeError("lists_brute capacity exceeded")
+    names = ("U", "V", "W_close", "W_far", "X_close", "X_far")
+    return {names[k]: (starts[k], boxes[k][:counts[k]].copy()) for k in range(6)}
+
+
+def ref_direct_sum(pos, w, mu, tpos):
+    """The reference's own qbx::direct_sum (kernels.cpp:46-73) via oracle/_ref."""
+    L = ref_lib()
+    if L is None:
+        raise RuntimeError("oracle/_ref not built")
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    tpos = np.ascontiguousarray(tpos, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(tpos.shape[0])
+    _chk(L.qbxref_direct_sum(pos.shape[0], _p(pos), _p(w), _p(mu), tpos.shape[0], _p(tpos),
+                             out.ctypes.data_as(_dp)), L)
+    return out

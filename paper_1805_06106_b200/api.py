@@ -1,0 +1,347 @@
+"""Host-side mirror of the reference's qbx:: interface, over the C ABI.
+
+Names follow the reference (/root/reference/proj/include/qbx3d/kernels.hpp and
+SPEC.md): ``SourceEnsemble``, ``TargetSet``, ``direct_sum``, ``FmmConfig``,
+``build_plan`` (build_tree + build_lists), ``execute``.  Errors are raised as
+the reference raises them: ``ValueError`` for std::invalid_argument and
+``ArithmeticError`` (``DomainError``) for std::domain_error.
+
+Every numerical call lands in libqbxg.so (CUDA for sm_100a).  There is no CPU
+fallback: without the library or a GPU the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+
+
+class DomainError(ArithmeticError):
+    """Mirror of std::domain_error (kernels.cpp:15, 22, 69-71)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(status: int):
+    if status == _abi.OK:
+        return
+    msg = _abi.lib().qbxg_last_error().decode(errors="replace")
+    if status == _abi.ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == _abi.ERR_DOMAIN:
+        raise DomainError(msg)
+    if status in (_abi.ERR_CUDA, _abi.ERR_NO_DEVICE):
+        raise CudaError(msg)
+    raise RuntimeError(f"qbxg status {status}: {msg}")
+
+
+def _ptr(a, ctype=C.c_double):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def _arr(p, n, dtype):
+    if n == 0 or not p:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(p, shape=(n,)).astype(dtype, copy=True)
+
+
+# --------------------------------------------------------------------------- inputs
+@dataclass
+class SourceEnsemble:
+    """kernels.hpp:18-29: positions (N,3), premultiplied weights (N,), optional dipole moments (N,3)."""
+    positions: np.ndarray
+    weights: np.ndarray
+    dipole_moments: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.positions = np.ascontiguousarray(self.positions, dtype=np.float64).reshape(-1, 3)
+        self.weights = np.ascontiguousarray(self.weights, dtype=np.float64).reshape(-1)
+        if self.dipole_moments is not None and np.size(self.dipole_moments) == 0:
+            self.dipole_moments = None
+        if self.dipole_moments is not None:
+            self.dipole_moments = np.ascontiguousarray(self.dipole_moments, dtype=np.float64).reshape(-1, 3)
+
+    def size(self):
+        return self.positions.shape[0]
+
+    def has_dipoles(self):
+        return self.dipole_moments is not None
+
+    def total_abs_weight(self):
+        return float(np.abs(self.weights).sum())
+
+
+@dataclass
+class TargetSet:
+    """kernels.hpp:31-37: positions (M,3) and association (centre id or -1)."""
+    positions: np.ndarray
+    association: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.positions = np.ascontiguousarray(self.positions, dtype=np.float64).reshape(-1, 3)
+        if self.association is None:
+            self.association = -np.ones(self.positions.shape[0], dtype=np.int32)
+        self.association = np.ascontiguousarray(self.association, dtype=np.int32).reshape(-1)
+
+    def size(self):
+        return self.positions.shape[0]
+
+
+@dataclass
+class FmmConfig:
+    """SPEC.md:414-417 (p_fmm, p_qbx, t_f, n_max, demotion threshold, level restriction)."""
+    p_fmm: int = 15
+    p_qbx: int = 5
+    t_f: float = 0.9
+    n_max: int = 64
+    kernel: int = _abi.KERNEL_LAPLACE_SL
+    w_far_demote: int = 0
+
+    def to_c(self):
+        return _abi.Config(self.p_fmm, self.p_qbx, self.t_f, self.n_max, self.kernel, 0.0, self.w_far_demote, 0)
+
+    @property
+    def kq(self):
+        return (self.p_qbx + 1) * (self.p_qbx + 2) // 2
+
+    @property
+    def kp(self):
+        return (self.p_fmm + 1) * (self.p_fmm + 2) // 2
+
+
+@dataclass
+class Geometry:
+    """Geometry bundle: sources, QBX centres (+radii), targets (+association)."""
+    source_pos: np.ndarray
+    center_pos: np.ndarray
+    center_radius: np.ndarray
+    target_pos: np.ndarray
+    association: np.ndarray
+    source_normal: np.ndarray | None = None
+    quad_weight: np.ndarray | None = None
+    density: np.ndarray | None = None
+    n_triangles: int = 0
+    n_volume_drawn: int = 0
+    _keep: list = field(default_factory=list, repr=False)
+
+    def __post_init__(self):
+        self.source_pos = np.ascontiguousarray(self.source_pos, dtype=np.float64).reshape(-1, 3)
+        self.center_pos = np.ascontiguousarray(self.center_pos, dtype=np.float64).reshape(-1, 3)
+        self.center_radius = np.ascontiguousarray(self.center_radius, dtype=np.float64).reshape(-1)
+        self.target_pos = np.ascontiguousarray(self.target_pos, dtype=np.float64).reshape(-1, 3)
+        self.association = np.ascontiguousarray(self.association, dtype=np.int32).reshape(-1)
+
+    @property
+    def n_sources(self):
+        return self.source_pos.shape[0]
+
+    @property
+    def n_centers(self):
+        return self.center_pos.shape[0]
+
+    @property
+    def n_targets(self):
+        return self.target_pos.shape[0]
+
+    def to_c(self):
+        return _abi.Geometry(self.n_sources, _ptr(self.source_pos), self.n_centers, _ptr(self.center_pos),
+                             _ptr(self.center_radius), self.n_targets, _ptr(self.target_pos),
+                             _ptr(self.association, C.c_int32))
+
+    def weights(self, density=None):
+        d = self.density if density is None else density
+        return np.ascontiguousarray(self.quad_weight * d)
+
+    def dipoles(self, density=None):
+        d = self.density if density is None else density
+        return np.ascontiguousarray(self.source_normal * (self.quad_weight * d)[:, None])
+
+
+def geometry_spec(config_id: int, variant: int = 0, seed: int = 0, **overrides) -> _abi.GeometrySpec:
+    spec = _abi.GeometrySpec()
+    _check(_abi.lib().qbxg_geometry_spec_for_config(config_id, variant, seed, C.byref(spec)))
+    for k, v in overrides.items():
+        setattr(spec, k, v)
+    return spec
+
+
+def generate_geometry(spec: _abi.GeometrySpec) -> Geometry:
+    L = _abi.lib()
+    h = C.c_void_p()
+    _check(L.qbxg_geometry_generate(C.byref(spec), C.byref(h)))
+    try:
+        v = _abi.GeneratedView()
+        _check(L.qbxg_geometry_view(h, C.byref(v)))
+        ns, nc, nt = v.n_sources, v.n_centers, v.n_targets
+        g = Geometry(source_pos=_arr(v.source_pos, 3 * ns, np.float64), center_pos=_arr(v.center_pos, 3 * nc, np.float64),
+                     center_radius=_arr(v.center_radius, nc, np.float64), target_pos=_arr(v.target_pos, 3 * nt, np.float64),
+                     association=_arr(v.association, nt, np.int32),
+                     source_normal=_arr(v.source_normal, 3 * ns, np.float64).reshape(-1, 3),
+                     quad_weight=_arr(v.quad_weight, ns, np.float64),
+                     density=_arr(v.density, ns * (2 if v.density_is_complex else 1), np.float64),
+                     n_triangles=v.n_triangles, n_volume_drawn=v.n_volume_drawn)
+        return g
+    finally:
+        L.qbxg_geometry_destroy(h)
+
+
+def config_geometry(config_id: int, variant: int = 0, seed: int = 0, **overrides) -> Geometry:
+    return generate_geometry(geometry_spec(config_id, variant, seed, **overrides))
+
+
+CONFIG_ORDERS = {0: (10, 3, _abi.KERNEL_LAPLACE_SL), 1: (15, 5, _abi.KERNEL_LAPLACE_SL_DL),
+                 2: (15, 5, _abi.KERNEL_LAPLACE_SL), 3: (20, 5, _abi.KERNEL_HELMHOLTZ_SL),
+                 4: (15, 5, _abi.KERNEL_LAPLACE_SL_DL)}
+
+
+def config_fmm(config_id: int, **overrides) -> FmmConfig:
+    p, q, k = CONFIG_ORDERS[config_id]
+    cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k)
+    for key, v in overrides.items():
+        setattr(cfg, key, v)
+    return cfg
+
+
+# --------------------------------------------------------------------------- plan
+class Plan:
+    """Host octree + interaction lists (Stage 1), built by libqbxg's host C++."""
+
+    def __init__(self, cfg: FmmConfig, geom: Geometry):
+        self.cfg = cfg
+        self.geom = geom
+        self._c_cfg = cfg.to_c()
+        self._c_geom = geom.to_c()
+        self.handle = C.c_void_p()
+        _check(_abi.lib().qbxg_plan_create(C.byref(self._c_cfg), C.byref(self._c_geom), C.byref(self.handle)))
+        self.view = _abi.PlanView()
+        _check(_abi.lib().qbxg_plan_view_get(self.handle, C.byref(self.view)))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _abi.lib().qbxg_plan_destroy(h)
+            self.handle = None
+
+    # numpy copies of the tree
+    def arrays(self):
+        v = self.view
+        nb = v.n_boxes
+        out = dict(n_boxes=nb, n_levels=v.n_levels, root_center=np.array(v.root_center[:]), root_radius=v.root_radius,
+                   box_center=_arr(v.box_center, 3 * nb, np.float64).reshape(-1, 3),
+                   box_radius=_arr(v.box_radius, nb, np.float64), box_level=_arr(v.box_level, nb, np.int32),
+                   box_parent=_arr(v.box_parent, nb, np.int32), child_starts=_arr(v.child_starts, nb + 1, np.int32),
+                   box_flags=_arr(v.box_flags, nb, np.uint8))
+        out["children"] = _arr(v.children, int(out["child_starts"][-1]), np.int32)
+        out["level_starts"] = _arr(v.level_starts, v.n_levels + 1, np.int32)
+        out["level_boxes"] = _arr(v.level_boxes, nb, np.int32)
+        for role in ("src", "ctr", "tgt"):
+            for kind in ("own_start", "own_count", "sub_start", "sub_count"):
+                nm = f"{role}_{kind}"
+                out[nm] = _arr(getattr(v, nm), nb, np.int32)
+        out["src_perm"] = _arr(v.src_perm, v.n_sources, np.int32)
+        out["ctr_perm"] = _arr(v.ctr_perm, v.n_centers, np.int32)
+        out["tgt_perm"] = _arr(v.tgt_perm, v.n_conv_targets, np.int32)
+        return out
+
+    def list_csr(self, k: int):
+        v = self.view
+        starts = _arr(v.list_starts[k], v.n_boxes + 1, np.int64)
+        boxes = _arr(v.list_boxes[k], int(starts[-1]), np.int32)
+        return starts, boxes
+
+    def list_hashes(self):
+        return {name: int(self.view.list_hash[k]) for k, name in enumerate(_abi.LIST_NAMES)}
+
+    def ledger(self) -> dict:
+        L = _abi.Ledger()
+        _check(_abi.lib().qbxg_plan_ledger(self.handle, C.byref(L)))
+        d = {f: getattr(L, f) for f, _ in L._fields_}
+        d["modeled"] = dict(zip(_abi.LIST_NAMES, L.modeled[:]))
+        d["entries"] = dict(zip(_abi.LIST_NAMES, L.entries[:]))
+        return d
+
+
+def build_plan(cfg: FmmConfig, geom: Geometry) -> Plan:
+    return Plan(cfg, geom)
+
+
+# --------------------------------------------------------------------------- device engine
+class FmmEngine:
+    """One GPU's QBX-FMM apply (qbxg_create / qbxg_apply)."""
+
+    def __init__(self, cfg: FmmConfig, geom: Geometry, plan: Plan | None = None, device: int = 0):
+        self.cfg = cfg
+        self.geom = geom
+        self.plan = plan if plan is not None else Plan(cfg, geom)
+        self._c_cfg = cfg.to_c()
+        self._c_geom = geom.to_c()
+        self.handle = C.c_void_p()
+        _check(_abi.lib().qbxg_create(C.byref(self._c_cfg), C.byref(self._c_geom), self.plan.handle, device,
+                                      C.byref(self.handle)))
+        self.timings = _abi.Timings()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _abi.lib().qbxg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    def apply(self, weights, dipoles=None, want_centers=False):
+        w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        m = None if dipoles is None else np.ascontiguousarray(dipoles, dtype=np.float64).reshape(-1)
+        pot = np.empty(self.geom.n_targets, dtype=np.float64)
+        coeffs = np.empty(self.geom.n_centers * 2 * self.cfg.kq, dtype=np.float64) if want_centers else None
+        _check(_abi.lib().qbxg_apply(self.handle, _ptr(w), _ptr(m), _ptr(pot), _ptr(coeffs), C.byref(self.timings)))
+        if want_centers:
+            c = coeffs.reshape(self.geom.n_centers, self.cfg.kq, 2)
+            return pot, c[..., 0] + 1j * c[..., 1]
+        return pot
+
+    def apply_device(self, d_weights: int, d_dipoles: int | None, d_pot: int, d_coeffs: int | None = None,
+                     stream: int | None = None):
+        """Device pointers (ints, e.g. torch tensor.data_ptr()) in original ordering."""
+        _check(_abi.lib().qbxg_apply_device(self.handle, C.c_void_p(d_weights), C.c_void_p(d_dipoles or 0),
+                                            C.c_void_p(d_pot), C.c_void_p(d_coeffs or 0), C.c_void_p(stream or 0),
+                                            C.byref(self.timings)))
+
+    def last_timings(self):
+        t = self.timings
+        return dict(zip(_abi.TIMER_NAMES, t.ms[:])), int(t.kernel_launches), int(t.h2d_bytes), int(t.d2h_bytes)
+
+
+def execute(geom: Geometry, weights, dipoles, cfg: FmmConfig, want_centers=False, device=0):
+    """SPEC.md:424 execute(bundle, density, FmmConfig) -> (potentials, ledger)."""
+    plan = Plan(cfg, geom)
+    eng = FmmEngine(cfg, geom, plan, device)
+    try:
+        out = eng.apply(weights, dipoles, want_centers=want_centers)
+    finally:
+        eng.close()
+    return out, plan.ledger()
+
+
+def direct_sum(sources: SourceEnsemble, targets: TargetSet) -> np.ndarray:
+    """GPU counterpart of qbx::direct_sum (kernels.cpp:46-73)."""
+    pot = np.empty(targets.size(), dtype=np.float64)
+    m = sources.dipole_moments
+    _check(_abi.lib().qbxg_direct_sum(sources.size(), _ptr(sources.positions), _ptr(sources.weights), _ptr(m),
+                                      targets.size(), _ptr(targets.positions), _ptr(pot)))
+    return pot
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    _check(_abi.lib().qbxg_device_count(C.byref(n)))
+    return n.value
