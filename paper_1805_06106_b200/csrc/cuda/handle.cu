@@ -1,0 +1,533 @@
+// Device handle: qbxg_create / qbxg_apply / qbxg_apply_device / qbxg_destroy
+// and qbxg_direct_sum.  Replaces the reference's declared execute() driver
+// (src/fmm.cpp, proj/CMakeLists.txt:27) and direct_sum
+// (proj/src/kernels.cpp:46-73) with one sm_100a pass over Stages 2-9.
+//
+// HBM layout (all box-sorted in the plan's DFS preorder):
+//   sources  double4 (x, y, z, w) [+ double4 dipole]      32 B (64 B SL+DL) per source
+//   centres  double4 (x, y, z, r)                          32 B per centre
+//   targets  double4 (x, y, z, 0) for conventional targets
+//   boxes    double4 (cx, cy, cz, |b|)
+//   M, L     nb x K_p complex (half table), box-scaled
+//   L_c      nc x K_q complex (half table), radius-scaled
+// Lists are CSR; near-field lists are flattened into source segments.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../host/common.hpp"
+#include "harmonics.cuh"
+#include "kernels.cuh"
+
+namespace qbxg {
+
+#define QCK(call)                                                                                    \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess)                                                                           \
+      throw ::qbxg::CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);         \
+  } while (0)
+
+namespace {
+
+template <class T>
+T* dalloc(std::vector<void*>& owned, size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  QCK(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* dupload(std::vector<void*>& owned, const std::vector<T>& v, cudaStream_t s) {
+  T* p = dalloc<T>(owned, v.size());
+  if (!v.empty()) QCK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+void check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device available (the qbxg GPU path has no CPU fallback)");
+  }
+}
+
+}  // namespace
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[QBXG_NUM_TIMERS + 2] = {};
+  qbxg_config cfg{};
+  int64_t ns = 0, nc = 0, nt = 0, nconv = 0;
+  int nb = 0, nlev = 0;
+  dev::DevData D{};
+  std::vector<void*> owned;
+  // index arrays
+  int* d_src_perm = nullptr;
+  int* d_ctr_perm = nullptr;
+  int* d_tgt_perm = nullptr;
+  int* d_tgt_box = nullptr;
+  int* d_ctr_sorted = nullptr;
+  int* d_assoc = nullptr;
+  double* d_tpos = nullptr;
+  // work lists
+  int* d_leaves = nullptr;
+  int n_leaves = 0;
+  std::vector<int*> d_m2m_level;
+  std::vector<int> n_m2m_level;
+  std::vector<int*> d_l2l_level;
+  std::vector<int> n_l2l_level;
+  int* d_ctr_boxes = nullptr;
+  int n_ctr_boxes = 0;
+  int* d_tgt_boxes = nullptr;
+  int n_tgt_boxes = 0;
+  int* d_v_boxes = nullptr;
+  int n_v_boxes = 0;
+  int* d_wfar_boxes = nullptr;
+  int n_wfar_boxes = 0;
+  int* d_xfar_boxes = nullptr;
+  int n_xfar_boxes = 0;
+  // staging for host applies
+  double* d_w = nullptr;
+  double* d_mu_in = nullptr;
+  double* d_pot = nullptr;
+  double* d_coeffs = nullptr;
+  int last_launches = 0;
+
+  ~Handle() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : owned) cudaFree(p);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device) {
+  check_device();
+  if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL)
+    throw InvalidArgument("qbxg_create: only Laplace kernels are implemented");
+  if (cfg.p_fmm > 21) throw InvalidArgument("qbxg_create: p_fmm > 21 not supported on the GPU path");
+  if (cfg.p_qbx > 8) throw InvalidArgument("qbxg_create: p_qbx > 8 not supported on the GPU path");
+  qbxg_plan_view V;
+  if (qbxg_plan_view_get(plan, &V) != QBXG_OK) throw InvalidArgument(get_last_error());
+  if (V.n_sources != g.n_sources || V.n_centers != g.n_centers || V.n_targets != g.n_targets)
+    throw InvalidArgument("qbxg_create: plan was built from a different geometry");
+  H.device = device;
+  QCK(cudaSetDevice(device));
+  dev::upload_constants();
+  dev::set_smem_limits();
+  QCK(cudaStreamCreateWithFlags(&H.stream, cudaStreamNonBlocking));
+  for (auto& e : H.ev) QCK(cudaEventCreate(&e));
+  cudaStream_t s = H.stream;
+  auto& O = H.owned;
+  H.cfg = cfg;
+  H.ns = g.n_sources;
+  H.nc = g.n_centers;
+  H.nt = g.n_targets;
+  H.nconv = V.n_conv_targets;
+  H.nb = V.n_boxes;
+  H.nlev = V.n_levels;
+  const int nb = H.nb;
+  const int p = cfg.p_fmm, q = cfg.p_qbx;
+  dev::DevData& D = H.D;
+  D.p = p;
+  D.q = q;
+  D.kp = dev::hsize(p);
+  D.kq = dev::hsize(q);
+  D.ktab_m2l = dev::hsize(2 * p);
+  D.dipole = cfg.kernel == QBXG_KERNEL_LAPLACE_SL_DL ? 1 : 0;
+
+  // --- tree
+  std::vector<double4> box(nb);
+  for (int b = 0; b < nb; ++b)
+    box[b] = make_double4(V.box_center[3 * b], V.box_center[3 * b + 1], V.box_center[3 * b + 2], V.box_radius[b]);
+  D.box = dupload(O, box, s);
+  D.child_starts = dupload(O, std::vector<int>(V.child_starts, V.child_starts + nb + 1), s);
+  D.children = dupload(O, std::vector<int>(V.children, V.children + V.child_starts[nb]), s);
+  D.parent = dupload(O, std::vector<int>(V.box_parent, V.box_parent + nb), s);
+  auto up_i = [&](const int32_t* a) { return dupload(O, std::vector<int>(a, a + nb), s); };
+  D.src_own_start = up_i(V.src_own_start);
+  D.src_own_count = up_i(V.src_own_count);
+  D.ctr_own_start = up_i(V.ctr_own_start);
+  D.ctr_own_count = up_i(V.ctr_own_count);
+  D.tgt_own_start = up_i(V.tgt_own_start);
+  D.tgt_own_count = up_i(V.tgt_own_count);
+
+  // --- particles (box-sorted)
+  std::vector<double4> src(H.ns), ctr(H.nc), tgt(H.nconv);
+  for (int64_t i = 0; i < H.ns; ++i) {
+    const int64_t o = V.src_perm[i];
+    src[i] = make_double4(g.source_pos[3 * o], g.source_pos[3 * o + 1], g.source_pos[3 * o + 2], 0.0);
+  }
+  for (int64_t i = 0; i < H.nc; ++i) {
+    const int64_t o = V.ctr_perm[i];
+    ctr[i] = make_double4(g.center_pos[3 * o], g.center_pos[3 * o + 1], g.center_pos[3 * o + 2], g.center_radius[o]);
+  }
+  for (int64_t i = 0; i < H.nconv; ++i) {
+    const int64_t o = V.tgt_perm[i];
+    tgt[i] = make_double4(g.target_pos[3 * o], g.target_pos[3 * o + 1], g.target_pos[3 * o + 2], 0.0);
+  }
+  D.src = dupload(O, src, s);
+  D.mu = D.dipole ? dalloc<double4>(O, H.ns) : nullptr;
+  D.ctr = dupload(O, ctr, s);
+  D.tgt = dupload(O, tgt, s);
+  H.d_src_perm = dupload(O, std::vector<int>(V.src_perm, V.src_perm + H.ns), s);
+  H.d_ctr_perm = dupload(O, std::vector<int>(V.ctr_perm, V.ctr_perm + H.nc), s);
+  H.d_tgt_perm = dupload(O, std::vector<int>(V.tgt_perm, V.tgt_perm + H.nconv), s);
+  {
+    std::vector<int> tb(H.nconv), cs(H.nc);
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < V.tgt_own_count[b]; ++j) tb[V.tgt_own_start[b] + j] = b;
+    for (int64_t i = 0; i < H.nc; ++i) cs[V.ctr_perm[i]] = int(i);
+    H.d_tgt_box = dupload(O, tb, s);
+    H.d_ctr_sorted = dupload(O, cs, s);
+    H.d_assoc = dupload(O, std::vector<int>(g.association, g.association + H.nt), s);
+    H.d_tpos = dupload(O, std::vector<double>(g.target_pos, g.target_pos + 3 * H.nt), s);
+  }
+
+  // --- expansions
+  D.M = dalloc<double2>(O, size_t(nb) * D.kp);
+  D.L = dalloc<double2>(O, size_t(nb) * D.kp);
+  D.Lc = dalloc<double2>(O, size_t(H.nc) * D.kq);
+  D.phi = dalloc<double>(O, H.nconv);
+
+  // --- lists
+  auto lrow = [&](int k, int b, int64_t& a, int64_t& e) {
+    a = V.list_starts[k][b];
+    e = V.list_starts[k][b + 1];
+  };
+  {
+    std::vector<int64_t> ns_(nb + 1, 0), xs(nb + 1, 0), vs(nb + 1, 0), ws(nb + 1, 0);
+    std::vector<int2> nseg, xseg, vent;
+    std::vector<int> wbox;
+    const int near_lists[3] = {QBXG_LIST_U, QBXG_LIST_W_CLOSE, QBXG_LIST_X_CLOSE};
+    for (int b = 0; b < nb; ++b) {
+      int64_t a, e;
+      if (V.box_flags[b] & QBXG_BOX_TARGET) {
+        for (int li : near_lists) {
+          lrow(li, b, a, e);
+          for (int64_t i = a; i < e; ++i) {
+            const int d = V.list_boxes[li][i];
+            if (V.src_own_count[d] > 0) nseg.push_back(make_int2(V.src_own_start[d], V.src_own_count[d]));
+          }
+        }
+      }
+      ns_[b + 1] = int64_t(nseg.size());
+      lrow(QBXG_LIST_X_FAR, b, a, e);
+      for (int64_t i = a; i < e; ++i) {
+        const int d = V.list_boxes[QBXG_LIST_X_FAR][i];
+        if (V.src_own_count[d] > 0) xseg.push_back(make_int2(V.src_own_start[d], V.src_own_count[d]));
+      }
+      xs[b + 1] = int64_t(xseg.size());
+      lrow(QBXG_LIST_V, b, a, e);
+      for (int64_t i = a; i < e; ++i) {
+        const int d = V.list_boxes[QBXG_LIST_V][i];
+        int dd[3];
+        for (int k = 0; k < 3; ++k)
+          dd[k] = int(std::lround((V.box_center[3 * b + k] - V.box_center[3 * d + k]) / (2.0 * V.box_radius[b])));
+        if (std::abs(dd[0]) > 5 || std::abs(dd[1]) > 5 || std::abs(dd[2]) > 5)
+          throw InvalidArgument("qbxg_create: List 2 offset outside [-5,5]^3");
+        vent.push_back(make_int2(d, ((dd[0] + 5) * 11 + (dd[1] + 5)) * 11 + (dd[2] + 5)));
+      }
+      vs[b + 1] = int64_t(vent.size());
+      lrow(QBXG_LIST_W_FAR, b, a, e);
+      for (int64_t i = a; i < e; ++i) wbox.push_back(V.list_boxes[QBXG_LIST_W_FAR][i]);
+      ws[b + 1] = int64_t(wbox.size());
+    }
+    D.near_starts = dupload(O, ns_, s);
+    D.near_seg = dupload(O, nseg, s);
+    D.xfar_starts = dupload(O, xs, s);
+    D.xfar_seg = dupload(O, xseg, s);
+    D.v_starts = dupload(O, vs, s);
+    D.v_ent = dupload(O, vent, s);
+    D.wfar_starts = dupload(O, ws, s);
+    D.wfar_box = dupload(O, wbox, s);
+
+    // work lists
+    std::vector<int> leaves, cb, tb, vb, wb, xb;
+    H.d_m2m_level.assign(H.nlev, nullptr);
+    H.n_m2m_level.assign(H.nlev, 0);
+    H.d_l2l_level.assign(H.nlev, nullptr);
+    H.n_l2l_level.assign(H.nlev, 0);
+    for (int b = 0; b < nb; ++b) {
+      const bool leaf = V.box_flags[b] & QBXG_BOX_LEAF;
+      if (leaf && V.src_own_count[b] > 0) leaves.push_back(b);
+      if (V.ctr_own_count[b] > 0) cb.push_back(b);
+      if (V.tgt_own_count[b] > 0 && ns_[b + 1] > ns_[b]) tb.push_back(b);
+      if (vs[b + 1] > vs[b]) vb.push_back(b);
+      if (ws[b + 1] > ws[b] && (V.ctr_own_count[b] + V.tgt_own_count[b]) > 0) wb.push_back(b);
+      if (xs[b + 1] > xs[b]) xb.push_back(b);
+    }
+    // conventional targets with an empty near list still need phi = 0
+    H.d_leaves = dupload(O, leaves, s);
+    H.n_leaves = int(leaves.size());
+    H.d_ctr_boxes = dupload(O, cb, s);
+    H.n_ctr_boxes = int(cb.size());
+    H.d_tgt_boxes = dupload(O, tb, s);
+    H.n_tgt_boxes = int(tb.size());
+    H.d_v_boxes = dupload(O, vb, s);
+    H.n_v_boxes = int(vb.size());
+    H.d_wfar_boxes = dupload(O, wb, s);
+    H.n_wfar_boxes = int(wb.size());
+    H.d_xfar_boxes = dupload(O, xb, s);
+    H.n_xfar_boxes = int(xb.size());
+    for (int l = 0; l < H.nlev; ++l) {
+      std::vector<int> m2m, l2l;
+      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
+        const int b = V.level_boxes[i];
+        if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES)) m2m.push_back(b);
+        if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR))) l2l.push_back(b);
+      }
+      H.d_m2m_level[l] = dupload(O, m2m, s);
+      H.n_m2m_level[l] = int(m2m.size());
+      H.d_l2l_level[l] = dupload(O, l2l, s);
+      H.n_l2l_level[l] = int(l2l.size());
+    }
+  }
+
+  // --- operator tables
+  double2* m2l_tab = dalloc<double2>(O, size_t(1331) * D.ktab_m2l);
+  double2* oct_m2m = dalloc<double2>(O, size_t(8) * D.kp);
+  double2* oct_l2l = dalloc<double2>(O, size_t(8) * D.kp);
+  dev::launch_tables(D, m2l_tab, oct_m2m, oct_l2l, s);
+  D.m2l_tab = m2l_tab;
+  D.oct_m2m = oct_m2m;
+  D.oct_l2l = oct_l2l;
+
+  // --- host-apply staging
+  H.d_w = dalloc<double>(O, H.ns);
+  H.d_mu_in = D.dipole ? dalloc<double>(O, 3 * H.ns) : nullptr;
+  H.d_pot = dalloc<double>(O, H.nt);
+  H.d_coeffs = dalloc<double>(O, size_t(H.nc) * 2 * D.kq);
+  QCK(cudaGetLastError());
+  QCK(cudaStreamSynchronize(s));
+}
+
+void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s,
+                int timer_base_event) {
+  (void)timer_base_event;
+  dev::DevData& D = H.D;
+  if (D.dipole && !d_mu) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
+  int L = 0;
+  auto chk = [&](int k) {
+    if (k < 0) throw InvalidArgument("qbxg_apply: unsupported order");
+    L += k;
+  };
+  auto& ev = H.ev;
+  QCK(cudaEventRecord(ev[0], s));
+  chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
+  QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
+  QCK(cudaMemsetAsync(D.L, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
+  QCK(cudaMemsetAsync(D.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double), s));
+  QCK(cudaEventRecord(ev[1], s));
+  chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
+  QCK(cudaEventRecord(ev[2], s));
+  for (int l = H.nlev - 2; l >= 0; --l) chk(dev::launch_m2m(D, H.d_m2m_level[l], H.n_m2m_level[l], s));
+  QCK(cudaEventRecord(ev[3], s));
+  chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
+  QCK(cudaEventRecord(ev[4], s));
+  chk(dev::launch_m2l(D, H.d_v_boxes, H.n_v_boxes, s));
+  QCK(cudaEventRecord(ev[5], s));
+  chk(dev::launch_wfar(D, H.d_wfar_boxes, H.n_wfar_boxes, s));
+  QCK(cudaEventRecord(ev[6], s));
+  chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
+  QCK(cudaEventRecord(ev[7], s));
+  for (int l = 1; l < H.nlev; ++l) chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
+  QCK(cudaEventRecord(ev[8], s));
+  chk(dev::launch_l2qbxl(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  QCK(cudaEventRecord(ev[9], s));
+  chk(dev::launch_eval(D, int(H.nt), H.d_tpos, H.d_assoc, H.d_ctr_sorted, int(H.nconv), H.d_tgt_perm, H.d_tgt_box,
+                       d_pot, s));
+  if (d_coeffs) chk(dev::launch_centre_out(D, int(H.nc), H.d_ctr_perm, d_coeffs, s));
+  QCK(cudaEventRecord(ev[10], s));
+  QCK(cudaGetLastError());
+  H.last_launches = L;
+}
+
+void fill_timings(Handle& H, qbxg_timings* t, bool host_copies, int64_t h2d, int64_t d2h) {
+  QCK(cudaEventSynchronize(H.ev[host_copies ? 12 : 10]));
+  if (!t) return;
+  std::memset(t, 0, sizeof(*t));
+  auto el = [&](int a, int b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, H.ev[a], H.ev[b]);
+    return double(ms);
+  };
+  t->ms[QBXG_T_P2M] = el(1, 2);
+  t->ms[QBXG_T_M2M] = el(2, 3);
+  t->ms[QBXG_T_NEAR] = el(3, 4);
+  t->ms[QBXG_T_M2L] = el(4, 5);
+  t->ms[QBXG_T_WFAR] = el(5, 6);
+  t->ms[QBXG_T_P2L] = el(6, 7);
+  t->ms[QBXG_T_L2L] = el(7, 8);
+  t->ms[QBXG_T_L2QBXL] = el(8, 9);
+  t->ms[QBXG_T_EVAL] = el(9, 10);
+  if (host_copies) {
+    t->ms[QBXG_T_H2D] = el(11, 0) + el(0, 1);
+    t->ms[QBXG_T_D2H] = el(10, 12);
+    t->ms[QBXG_T_TOTAL] = el(11, 12);
+  } else {
+    t->ms[QBXG_T_H2D] = el(0, 1);
+    t->ms[QBXG_T_TOTAL] = el(0, 10);
+  }
+  t->kernel_launches = H.last_launches;
+  t->h2d_bytes = h2d;
+  t->d2h_bytes = d2h;
+}
+
+void validate_sources(int64_t ns, const double* pos, const double* w, const double* mu) {
+  for (int64_t i = 0; i < ns; ++i) {
+    if (!std::isfinite(pos[3 * i]) || !std::isfinite(pos[3 * i + 1]) || !std::isfinite(pos[3 * i + 2]) ||
+        !std::isfinite(w[i]))
+      throw InvalidArgument("SourceEnsemble: non-finite entry at index " + std::to_string(i));
+    if (mu && (!std::isfinite(mu[3 * i]) || !std::isfinite(mu[3 * i + 1]) || !std::isfinite(mu[3 * i + 2])))
+      throw InvalidArgument("SourceEnsemble: non-finite dipole at index " + std::to_string(i));
+  }
+}
+
+}  // namespace
+}  // namespace qbxg
+
+struct qbxg_handle {
+  qbxg::Handle h;
+};
+
+extern "C" {
+
+int qbxg_device_count(int32_t* out) {
+  return qbxg::guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *out = n;
+  });
+}
+
+int qbxg_create(const qbxg_config* cfg, const qbxg_geometry* geom, const qbxg_plan* plan, int32_t device,
+                qbxg_handle** out) {
+  int st = qbxg::guarded([&] {
+    if (!cfg || !geom || !plan || !out) throw qbxg::InvalidArgument("qbxg_create: null argument");
+    auto* h = new qbxg_handle;
+    try {
+      qbxg::create(h->h, *cfg, *geom, plan, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+  if (st == QBXG_ERR_CUDA) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return QBXG_ERR_NO_DEVICE;
+    }
+  }
+  return st;
+}
+
+int qbxg_apply_device(qbxg_handle* hp, const double* d_weights, const double* d_dipoles, double* d_out_target_pot,
+                      double* d_out_center_coeffs, void* cuda_stream, qbxg_timings* timings) {
+  return qbxg::guarded([&] {
+    if (!hp || !d_weights || !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_device: null argument");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
+    qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, 0);
+    qbxg::fill_timings(H, timings, false, 0, 0);
+  });
+}
+
+int qbxg_apply(qbxg_handle* hp, const double* weights, const double* dipoles, double* out_target_pot,
+               double* out_center_coeffs, qbxg_timings* timings) {
+  return qbxg::guarded([&] {
+    if (!hp || !weights || !out_target_pot) throw qbxg::InvalidArgument("qbxg_apply: null argument");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    cudaStream_t s = H.stream;
+    const bool dip = H.D.dipole;
+    if (dip && !dipoles) throw qbxg::InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
+    QCK(cudaEventRecord(H.ev[11], s));
+    int64_t h2d = H.ns * 8, d2h = H.nt * 8;
+    QCK(cudaMemcpyAsync(H.d_w, weights, H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (dip) {
+      QCK(cudaMemcpyAsync(H.d_mu_in, dipoles, 3 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+      h2d += 24 * H.ns;
+    }
+    qbxg::run_device(H, H.d_w, dip ? H.d_mu_in : nullptr, H.d_pot, out_center_coeffs ? H.d_coeffs : nullptr, s, 0);
+    QCK(cudaMemcpyAsync(out_target_pot, H.d_pot, H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out_center_coeffs) {
+      const size_t nbytes = size_t(H.nc) * 2 * H.D.kq * sizeof(double);
+      QCK(cudaMemcpyAsync(out_center_coeffs, H.d_coeffs, nbytes, cudaMemcpyDeviceToHost, s));
+      d2h += int64_t(nbytes);
+    }
+    QCK(cudaEventRecord(H.ev[12], s));
+    qbxg::fill_timings(H, timings, true, h2d, d2h);
+    QCK(cudaStreamSynchronize(s));
+  });
+}
+
+int qbxg_destroy(qbxg_handle* h) {
+  delete h;
+  return QBXG_OK;
+}
+
+int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* weights, const double* dipoles_or_null,
+                    int64_t n_targets, const double* target_pos, double* out_pot) {
+  return qbxg::guarded([&] {
+    if (n_sources < 0 || n_targets < 0) throw qbxg::InvalidArgument("direct_sum: negative size");
+    if ((n_sources && (!source_pos || !weights)) || (n_targets && (!target_pos || !out_pot)))
+      throw qbxg::InvalidArgument("direct_sum: null array");
+    if (n_sources >= (int64_t(1) << 31) || n_targets >= (int64_t(1) << 31))
+      throw qbxg::InvalidArgument("direct_sum: too many points");
+    qbxg::validate_sources(n_sources, source_pos, weights, dipoles_or_null);
+    if (n_targets == 0) return;
+    qbxg::check_device();
+    std::vector<void*> owned;
+    struct Free {
+      std::vector<void*>& o;
+      ~Free() {
+        for (void* p : o) cudaFree(p);
+      }
+    } fr{owned};
+    std::vector<double4> src(n_sources), mu(dipoles_or_null ? n_sources : 0), tgt(n_targets);
+    for (int64_t i = 0; i < n_sources; ++i) {
+      src[i] = make_double4(source_pos[3 * i], source_pos[3 * i + 1], source_pos[3 * i + 2], weights[i]);
+      if (dipoles_or_null)
+        mu[i] = make_double4(dipoles_or_null[3 * i], dipoles_or_null[3 * i + 1], dipoles_or_null[3 * i + 2], 0);
+    }
+    for (int64_t i = 0; i < n_targets; ++i)
+      tgt[i] = make_double4(target_pos[3 * i], target_pos[3 * i + 1], target_pos[3 * i + 2], 0);
+    cudaStream_t s = nullptr;
+    double4* ds = qbxg::dupload(owned, src, s);
+    double4* dm = dipoles_or_null ? qbxg::dupload(owned, mu, s) : nullptr;
+    double4* dt = qbxg::dupload(owned, tgt, s);
+    double* dp = qbxg::dalloc<double>(owned, n_targets);
+    unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
+    QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+    qbxg::dev::launch_direct_sum(int(n_sources), ds, dm, int(n_targets), dt, dp, bad, s);
+    QCK(cudaGetLastError());
+    unsigned long long hb = 0;
+    QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+    QCK(cudaMemcpy(out_pot, dp, n_targets * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hb != ~0ull)
+      throw qbxg::DomainError("direct_sum: target " + std::to_string(hb >> 32) + " coincides with source " +
+                              std::to_string(hb & 0xffffffffull));
+  });
+}
+
+}  // extern "C"

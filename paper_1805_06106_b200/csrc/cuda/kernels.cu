@@ -1,0 +1,938 @@
+// Stage kernels of the GIGAQBX evaluation (Algorithm 4)
+// for sm_100a, fp64.  Every kernel owns its outputs (one CTA per target box or
+// per output box, one thread per output coefficient or per centre slice) and
+// sums in a fixed order, so results are bitwise reproducible run to run
+// without floating-point atomics.
+//
+// Coefficient conventions: see harmonics.cuh.  Box multipoles M~ = M/|b|^n,
+// box locals L~ = L |b|^n, QBX locals L~_c = L_c r_c^n.  The formulas are the
+// same as the CPU oracle's (oracle/qbx_oracle.cpp), restated on half tables.
+#include <cstdio>
+
+#include "harmonics.cuh"
+#include "kernels.cuh"
+
+namespace qbxg {
+namespace dev {
+
+void upload_constants() {
+  static bool done = false;
+  if (done) return;
+  double h[hsize(kMaxOrder)];
+  for (int n = 0; n <= kMaxOrder; ++n)
+    for (int m = 0; m <= n; ++m) h[hidx(n, m)] = (n >= m + 2) ? 1.0 / double((n - m) * (n + m)) : 0.0;
+  cudaMemcpyToSymbol(c_inv_nm, h, sizeof(h));
+  done = true;
+}
+
+namespace {
+
+__device__ __forceinline__ void idx_nm(int c, int& n, int& m) {
+  n = int((sqrt(8.0 * c + 1.0) - 1.0) * 0.5);
+  while (hidx(n + 1, 0) <= c) ++n;
+  while (hidx(n, 0) > c) --n;
+  m = c - hidx(n, 0);
+}
+
+__device__ __forceinline__ double ipow(double x, int n) {
+  double r = 1.0;
+  for (int i = 0; i < n; ++i) r *= x;
+  return r;
+}
+
+// ---------------------------------------------------------------- gather
+__global__ void k_gather(int ns, const int* __restrict__ perm, const double* __restrict__ w,
+                         const double* __restrict__ mu, double4* src, double4* smu) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int o = perm[i];
+  src[i].w = w[o];
+  if (smu) smu[i] = make_double4(mu[3 * o], mu[3 * o + 1], mu[3 * o + 2], 0.0);
+}
+
+// ---------------------------------------------------------------- P2M (Stage 2)
+// M~_n^m = sum_s w conj(R_n^m(u)) + conj(mu . grad R_n^m(u)) / h,  u = (s - c)/h
+constexpr int kP2MBatch = 16;
+
+__global__ void __launch_bounds__(256) k_p2m(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* tab = sm;                          // kP2MBatch x kp
+  double2* acc = sm + kP2MBatch * D.kp;       // kp
+  __shared__ double4 s_src[kP2MBatch], s_mu[kP2MBatch];
+  const int b = boxes[blockIdx.x];
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  const int s0 = D.src_own_start[b], ns = D.src_own_count[b];
+  for (int c = threadIdx.x; c < D.kp; c += blockDim.x) acc[c] = make_double2(0, 0);
+  for (int base = 0; base < ns; base += kP2MBatch) {
+    const int nb = min(kP2MBatch, ns - base);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      s_src[threadIdx.x] = D.src[s0 + base + threadIdx.x];
+      if (D.dipole) s_mu[threadIdx.x] = D.mu[s0 + base + threadIdx.x];
+    }
+    __syncthreads();
+    // column-parallel table build: task (s, m)
+    for (int t = threadIdx.x; t < nb * (D.p + 1); t += blockDim.x) {
+      const int s = t / (D.p + 1), m = t % (D.p + 1);
+      const double4 x = s_src[s];
+      double2 col[kMaxOrder + 1];
+      regular_column((x.x - bc.x) * ih, (x.y - bc.y) * ih, (x.z - bc.z) * ih, m, D.p, col);
+      for (int n = m; n <= D.p; ++n) tab[s * D.kp + hidx(n, m)] = col[n - m];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < D.kp; c += blockDim.x) {
+      int n, m;
+      idx_nm(c, n, m);
+      double2 a = acc[c];
+      for (int s = 0; s < nb; ++s) {
+        const double2* T = tab + s * D.kp;
+        const double w = s_src[s].w;
+        const double2 r = T[c];
+        a.x += w * r.x;
+        a.y -= w * r.y;
+        if (D.dipole && n > 0) {
+          const double4 u = s_mu[s];
+          const double2 r0 = (m <= n - 1) ? T[hidx(n - 1, m)] : make_double2(0, 0);
+          const double2 rm = (m - 1 >= -(n - 1)) ? hget(T, n - 1, m - 1) : make_double2(0, 0);
+          const double2 rp = (m + 1 <= n - 1) ? T[hidx(n - 1, m + 1)] : make_double2(0, 0);
+          // g = mz r0 + (mx + i my)/2 rm - (mx - i my)/2 rp
+          double gx = u.z * r0.x + 0.5 * (u.x * rm.x - u.y * rm.y) - 0.5 * (u.x * rp.x + u.y * rp.y);
+          double gy = u.z * r0.y + 0.5 * (u.x * rm.y + u.y * rm.x) - 0.5 * (u.x * rp.y - u.y * rp.x);
+          a.x += gx * ih;
+          a.y -= gy * ih;
+        }
+      }
+      acc[c] = a;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D.kp; c += blockDim.x) D.M[size_t(b) * D.kp + c] = acc[c];
+}
+
+// ---------------------------------------------------------------- M2M (Stage 2 postorder)
+// M~_parent(n,m) = 2^-n sum_children sum_{j<=n,k} M~_c(j,k) conj(R_{n-j}^{m-k}(u_oct))
+__device__ __forceinline__ int octant_of(const double4& child, const double4& par) {
+  return (child.x > par.x ? 1 : 0) | (child.y > par.y ? 2 : 0) | (child.z > par.z ? 4 : 0);
+}
+
+__global__ void __launch_bounds__(256) k_m2m(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* Mc = sm;           // kp
+  double2* R = sm + D.kp;     // kp
+  const int b = boxes[blockIdx.x];
+  const double4 pb = D.box[b];
+  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+  for (int k = D.child_starts[b]; k < D.child_starts[b + 1]; ++k) {
+    const int c = D.children[k];
+    const int o = octant_of(D.box[c], pb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < D.kp; i += blockDim.x) {
+      Mc[i] = D.M[size_t(c) * D.kp + i];
+      R[i] = D.oct_m2m[o * D.kp + i];
+    }
+    __syncthreads();
+    int slot = 0;
+    for (int cidx = threadIdx.x; cidx < D.kp; cidx += blockDim.x, ++slot) {
+      int n, m;
+      idx_nm(cidx, n, m);
+      double sx = 0, sy = 0;
+      for (int j = 0; j <= n; ++j) {
+        const int nj = n - j;
+        for (int kk = -j; kk <= j; ++kk) {
+          const int mk = m - kk;
+          if (mk > nj || mk < -nj) continue;
+          const double2 a = hget(Mc, j, kk);
+          const double2 r = hget(R, nj, mk);
+          // a * conj(r)
+          sx += a.x * r.x + a.y * r.y;
+          sy += a.y * r.x - a.x * r.y;
+        }
+      }
+      acc[slot].x += sx;
+      acc[slot].y += sy;
+    }
+  }
+  int slot = 0;
+  for (int cidx = threadIdx.x; cidx < D.kp; cidx += blockDim.x, ++slot) {
+    int n, m;
+    idx_nm(cidx, n, m);
+    const double s = ldexp(1.0, -n);
+    D.M[size_t(b) * D.kp + cidx] = make_double2(acc[slot].x * s, acc[slot].y * s);
+  }
+}
+
+// ---------------------------------------------------------------- near field (Stages 3, 5a, 6a)
+constexpr int kNearThreads = 128;
+constexpr int kNearChunk = 256;
+constexpr int kMaxSeg = 128;
+
+// Stage the segment descriptors [sb, se) (at most kMaxSeg) with prefix sums.
+__device__ __forceinline__ int load_segments(const int2* __restrict__ seg, int64_t sb, int nseg, int* s_start,
+                                             int* s_pre) {
+  if (threadIdx.x < nseg) s_start[threadIdx.x] = seg[sb + threadIdx.x].x;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+      s_pre[i] = acc;
+      acc += seg[sb + i].y;
+    }
+    s_pre[nseg] = acc;
+  }
+  __syncthreads();
+  return s_pre[nseg];
+}
+
+__device__ __forceinline__ int seg_source(int f, int nseg, const int* s_start, const int* s_pre) {
+  int lo = 0, hi = nseg;  // find k with s_pre[k] <= f < s_pre[k+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_pre[mid] <= f) lo = mid; else hi = mid;
+  }
+  return s_start[lo] + (f - s_pre[lo]);
+}
+
+// P2QBXL: L~_c += (1/r)[w conj(I(u)) + conj(mu . grad I(u)) / r], u = (s - c)/r   (Eq. (8))
+template <int Q, bool DIP>
+__global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int* __restrict__ boxes) {
+  constexpr int KQ = hsize(Q);
+  constexpr int KI = hsize(Q + (DIP ? 1 : 0));
+  __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
+  __shared__ double4 s_src[kNearChunk];
+  __shared__ double4 s_mu[DIP ? kNearChunk : 1];
+  const int b = boxes[blockIdx.x];
+  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
+  const int64_t sb = D.near_starts[b], se = D.near_starts[b + 1];
+  for (int cc = 0; cc < nctr; cc += kNearThreads) {
+    const int ncc = min(kNearThreads, nctr - cc);
+    int S = 1;
+    while (S * 2 * ncc <= kNearThreads && S < 32) S *= 2;
+    const int ci = threadIdx.x / S, sl = threadIdx.x % S;
+    const bool active = ci < ncc;
+    double4 c = make_double4(0, 0, 0, 1);
+    if (active) c = D.ctr[c0 + cc + ci];
+    const double ir = 1.0 / c.w;
+    double ax[KQ], ay[KQ];
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
+    for (int64_t s0 = sb; s0 < se; s0 += kMaxSeg) {
+      const int nseg = int(se - s0 < kMaxSeg ? se - s0 : kMaxSeg);
+      __syncthreads();
+      const int total = load_segments(D.near_seg, s0, nseg, s_start, s_pre);
+      for (int ch = 0; ch < total; ch += kNearChunk) {
+        const int nch = min(kNearChunk, total - ch);
+        __syncthreads();
+        for (int f = threadIdx.x; f < nch; f += kNearThreads) {
+          const int s = seg_source(ch + f, nseg, s_start, s_pre);
+          s_src[f] = D.src[s];
+          if (DIP) s_mu[f] = D.mu[s];
+        }
+        __syncthreads();
+        if (active) {
+          for (int j = sl; j < nch; j += S) {
+            const double4 x = s_src[j];
+            const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
+            double2 I[KI];
+            irregular_regs<Q + (DIP ? 1 : 0)>(ux, uy, uz, I);
+            const double w = x.w;
+#pragma unroll
+            for (int n = 0; n <= Q; ++n)
+#pragma unroll
+              for (int m = 0; m <= n; ++m) {
+                const int id = hidx(n, m);
+                ax[id] = fma(w, I[id].x, ax[id]);
+                ay[id] = fma(-w, I[id].y, ay[id]);
+              }
+            if (DIP) {
+              const double4 u = s_mu[j];
+              const double hx = 0.5 * u.x * ir, hy = 0.5 * u.y * ir, mz = u.z * ir;
+#pragma unroll
+              for (int n = 0; n <= Q; ++n)
+#pragma unroll
+                for (int m = 0; m <= n; ++m) {
+                  const int id = hidx(n, m);
+                  const double2 i0 = I[hidx(n + 1, m)];
+                  const double2 ip = I[hidx(n + 1, m + 1)];
+                  double2 im;
+                  if (m >= 1) {
+                    im = I[hidx(n + 1, m - 1)];
+                  } else {
+                    const double2 t = I[hidx(n + 1, 1)];
+                    im = make_double2(-t.x, t.y);  // I_{n+1}^{-1} = -conj(I_{n+1}^1)
+                  }
+                  // g = -mz i0 + (hx + i hy) im - (hx - i hy) ip ; acc += conj(g)
+                  const double gx = -mz * i0.x + (hx * im.x - hy * im.y) - (hx * ip.x + hy * ip.y);
+                  const double gy = -mz * i0.y + (hx * im.y + hy * im.x) - (hx * ip.y - hy * ip.x);
+                  ax[id] += gx;
+                  ay[id] -= gy;
+                }
+            }
+          }
+        }
+      }
+    }
+    // reduce over the S slices of each centre (contiguous lanes, S <= 32)
+    for (int off = S >> 1; off > 0; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) {
+        ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], off, S);
+        ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], off, S);
+      }
+    }
+    if (active && sl == 0) {
+      double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) out[i] = make_double2(ax[i] * ir, ay[i] * ir);
+    }
+  }
+}
+
+// P2P at conventional targets: phi_t = sum_s w/r + mu.(t-s)/r^3   (kernels.cpp:55-66)
+template <bool DIP>
+__global__ void __launch_bounds__(kNearThreads) k_near_p2p(DevData D, const int* __restrict__ boxes) {
+  __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
+  __shared__ double4 s_src[kNearChunk];
+  __shared__ double4 s_mu[DIP ? kNearChunk : 1];
+  const int b = boxes[blockIdx.x];
+  const int ntg = D.tgt_own_count[b], t0 = D.tgt_own_start[b];
+  const int64_t sb = D.near_starts[b], se = D.near_starts[b + 1];
+  for (int tc = 0; tc < ntg; tc += kNearThreads) {
+    const int ntc = min(kNearThreads, ntg - tc);
+    int S = 1;
+    while (S * 2 * ntc <= kNearThreads && S < 32) S *= 2;
+    const int ti = threadIdx.x / S, sl = threadIdx.x % S;
+    const bool active = ti < ntc;
+    double4 t = make_double4(0, 0, 0, 0);
+    if (active) t = D.tgt[t0 + tc + ti];
+    double acc = 0;
+    for (int64_t s0 = sb; s0 < se; s0 += kMaxSeg) {
+      const int nseg = int(se - s0 < kMaxSeg ? se - s0 : kMaxSeg);
+      __syncthreads();
+      const int total = load_segments(D.near_seg, s0, nseg, s_start, s_pre);
+      for (int ch = 0; ch < total; ch += kNearChunk) {
+        const int nch = min(kNearChunk, total - ch);
+        __syncthreads();
+        for (int f = threadIdx.x; f < nch; f += kNearThreads) {
+          const int s = seg_source(ch + f, nseg, s_start, s_pre);
+          s_src[f] = D.src[s];
+          if (DIP) s_mu[f] = D.mu[s];
+        }
+        __syncthreads();
+        if (active) {
+          for (int j = sl; j < nch; j += S) {
+            const double4 x = s_src[j];
+            const double dx = t.x - x.x, dy = t.y - x.y, dz = t.z - x.z;
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            const double rinv = rsqrt(r2);
+            acc = fma(x.w, rinv, acc);
+            if (DIP) {
+              const double4 u = s_mu[j];
+              acc += (u.x * dx + u.y * dy + u.z * dz) * rinv * rinv * rinv;
+            }
+          }
+        }
+      }
+    }
+    for (int off = S >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, S);
+    if (active && sl == 0) D.phi[t0 + tc + ti] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- M2L (Stage 4)
+// L~_b(n,m) += (1/h)(-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}(2 delta)
+__global__ void __launch_bounds__(256) k_m2l(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* Md = sm;               // kp
+  double2* T = sm + D.kp;         // ktab_m2l
+  const int b = boxes[blockIdx.x];
+  const double ih = 1.0 / D.box[b].w;
+  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+  for (int64_t e = D.v_starts[b]; e < D.v_starts[b + 1]; ++e) {
+    const int2 ent = D.v_ent[e];
+    __syncthreads();
+    for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(ent.x) * D.kp + i];
+    for (int i = threadIdx.x; i < D.ktab_m2l; i += blockDim.x) T[i] = D.m2l_tab[size_t(ent.y) * D.ktab_m2l + i];
+    __syncthreads();
+    int slot = 0;
+    for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
+      int n, m;
+      idx_nm(c, n, m);
+      double sx = 0, sy = 0;
+      for (int j = 0; j <= D.p; ++j)
+        for (int k = -j; k <= j; ++k) {
+          const double2 a = hget(Md, j, k);
+          const double2 t = hget(T, j + n, k - m);
+          sx += a.x * t.x - a.y * t.y;
+          sy += a.x * t.y + a.y * t.x;
+        }
+      const double sg = ((n + m) & 1) ? -1.0 : 1.0;
+      acc[slot].x += sg * sx;
+      acc[slot].y += sg * sy;
+    }
+  }
+  int slot = 0;
+  for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
+    double2 v = D.L[size_t(b) * D.kp + c];
+    v.x += acc[slot].x * ih;
+    v.y += acc[slot].y * ih;
+    D.L[size_t(b) * D.kp + c] = v;
+  }
+}
+
+// ---------------------------------------------------------------- W far (Stage 5b)
+// M2QBXL: L~_c(n,m) += (r/h)^n (1/h)(-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}((c - c_d)/h)
+// M2P:    phi_t += (1/h) sum M~_d(n,m) I_n^m((t - c_d)/h)
+constexpr int kWfarGroup = 8;
+
+__device__ inline double eval_irregular_sum(const double2* M, int P, double x, double y, double z) {
+  // Re sum_{n,|m|<=n} M_n^m I_n^m = sum_n [M_n^0 I_n^0 + 2 sum_{m>0} Re(M_n^m I_n^m)]
+  const double r2 = x * x + y * y + z * z;
+  const double ir2 = 1.0 / r2;
+  double2 imm = make_double2(sqrt(ir2), 0.0);
+  double acc = 0;
+  for (int m = 0; m <= P; ++m) {
+    const double f = m ? 2.0 : 1.0;
+    if (m > 0) {
+      const double s = (2 * m - 1) * ir2;
+      imm = make_double2((imm.x * x - imm.y * y) * s, (imm.x * y + imm.y * x) * s);
+    }
+    double2 a = imm;
+    double2 mm = M[hidx(m, m)];
+    acc += f * (mm.x * a.x - mm.y * a.y);
+    if (m + 1 > P) break;
+    const double s1 = (2 * m + 1) * z * ir2;
+    double2 bb = make_double2(s1 * imm.x, s1 * imm.y);
+    mm = M[hidx(m + 1, m)];
+    acc += f * (mm.x * bb.x - mm.y * bb.y);
+    for (int n = m + 2; n <= P; ++n) {
+      const double c1 = (2 * n - 1) * z;
+      const double c2 = double((n - 1 + m) * (n - 1 - m));
+      const double2 cc = make_double2((c1 * bb.x - c2 * a.x) * ir2, (c1 * bb.y - c2 * a.y) * ir2);
+      mm = M[hidx(n, m)];
+      acc += f * (mm.x * cc.x - mm.y * cc.y);
+      a = bb;
+      bb = cc;
+    }
+  }
+  return acc;
+}
+
+__device__ inline double eval_regular_sum(const double2* L, int P, double x, double y, double z) {
+  const double r2 = x * x + y * y + z * z;
+  double2 rmm = make_double2(1.0, 0.0);
+  double acc = 0;
+  for (int m = 0; m <= P; ++m) {
+    const double f = m ? 2.0 : 1.0;
+    if (m > 0) {
+      const double s = 1.0 / (2.0 * m);
+      rmm = make_double2((rmm.x * x - rmm.y * y) * s, (rmm.x * y + rmm.y * x) * s);
+    }
+    double2 a = rmm;
+    double2 ll = L[hidx(m, m)];
+    acc += f * (ll.x * a.x - ll.y * a.y);
+    if (m + 1 > P) break;
+    double2 bb = make_double2(z * rmm.x, z * rmm.y);
+    ll = L[hidx(m + 1, m)];
+    acc += f * (ll.x * bb.x - ll.y * bb.y);
+    for (int n = m + 2; n <= P; ++n) {
+      const double fi = c_inv_nm[hidx(n, m)];
+      const double c1 = (2 * n - 1) * z;
+      const double2 cc = make_double2((c1 * bb.x - r2 * a.x) * fi, (c1 * bb.y - r2 * a.y) * fi);
+      ll = L[hidx(n, m)];
+      acc += f * (ll.x * cc.x - ll.y * cc.y);
+      a = bb;
+      bb = cc;
+    }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_wfar(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  const int ktab = hsize(D.p + D.q);
+  double2* Md = sm;                 // kp
+  double2* T = sm + D.kp;           // kWfarGroup x ktab
+  const int b = boxes[blockIdx.x];
+  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
+  const int ntg = D.tgt_own_count[b], t0 = D.tgt_own_start[b];
+  const int64_t eb = D.wfar_starts[b], ee = D.wfar_starts[b + 1];
+  // centres, in groups of kWfarGroup; thread task (g, output)
+  const int G = min(kWfarGroup, int(blockDim.x) / D.kq);
+  for (int cg = 0; cg < nctr; cg += G) {
+    const int ng = min(G, nctr - cg);
+    const int g = threadIdx.x / D.kq, oc = threadIdx.x % D.kq;
+    const bool active = g < ng;
+    int n = 0, m = 0;
+    idx_nm(oc, n, m);
+    double4 c = make_double4(0, 0, 0, 1);
+    if (g < kWfarGroup && g < ng) c = D.ctr[c0 + cg + g];
+    double ax = 0, ay = 0;
+    for (int64_t e = eb; e < ee; ++e) {
+      const int d = D.wfar_box[e];
+      const double4 bd = D.box[d];
+      const double ih = 1.0 / bd.w;
+      __syncthreads();
+      for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(d) * D.kp + i];
+      // column-parallel irregular tables of (c - c_d)/h for each centre of the group
+      const int ncol = D.p + D.q + 1;
+      for (int t = threadIdx.x; t < ng * ncol; t += blockDim.x) {
+        const int gg = t / ncol, mm = t % ncol;
+        const double4 cx = D.ctr[c0 + cg + gg];
+        double2 col[kMaxOrder + 1];
+        irregular_column((cx.x - bd.x) * ih, (cx.y - bd.y) * ih, (cx.z - bd.z) * ih, mm, D.p + D.q, col);
+        double2* Tg = T + gg * ktab;
+        for (int nn = mm; nn <= D.p + D.q; ++nn) Tg[hidx(nn, mm)] = col[nn - mm];
+      }
+      __syncthreads();
+      if (active) {
+        const double2* Tg = T + g * ktab;
+        double sx = 0, sy = 0;
+        for (int j = 0; j <= D.p; ++j)
+          for (int k = -j; k <= j; ++k) {
+            const double2 a = hget(Md, j, k);
+            const double2 t = hget(Tg, j + n, k - m);
+            sx += a.x * t.x - a.y * t.y;
+            sy += a.x * t.y + a.y * t.x;
+          }
+        const double s = (((n + m) & 1) ? -1.0 : 1.0) * ipow(c.w * ih, n) * ih;
+        ax += s * sx;
+        ay += s * sy;
+      }
+    }
+    if (active) {
+      double2* out = D.Lc + size_t(c0 + cg + g) * D.kq + oc;
+      double2 v = *out;
+      v.x += ax;
+      v.y += ay;
+      *out = v;
+    }
+  }
+  // conventional targets: thread per target
+  for (int tc = 0; tc < ntg; tc += blockDim.x) {
+    const int ti = tc + threadIdx.x;
+    double acc = 0;
+    double4 t = make_double4(0, 0, 0, 0);
+    if (ti < ntg) t = D.tgt[t0 + ti];
+    for (int64_t e = eb; e < ee; ++e) {
+      const int d = D.wfar_box[e];
+      const double4 bd = D.box[d];
+      const double ih = 1.0 / bd.w;
+      __syncthreads();
+      for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(d) * D.kp + i];
+      __syncthreads();
+      if (ti < ntg) acc += ih * eval_irregular_sum(Md, D.p, (t.x - bd.x) * ih, (t.y - bd.y) * ih, (t.z - bd.z) * ih);
+    }
+    if (ti < ntg) D.phi[t0 + ti] += acc;
+  }
+}
+
+// ---------------------------------------------------------------- P2L (Stage 6b)
+// L~_b += (1/h)[w conj(I(u)) + conj(mu . grad I(u))/h], u = (s - c_b)/h, sources of X_far boxes
+constexpr int kP2LBatch = 16;
+
+__global__ void __launch_bounds__(256) k_p2l(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  const int P1 = D.p + (D.dipole ? 1 : 0);
+  const int kt = hsize(P1);
+  double2* tab = sm;  // kP2LBatch x kt
+  __shared__ double4 s_src[kP2LBatch], s_mu[kP2LBatch];
+  __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
+  const int b = boxes[blockIdx.x];
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+  const int64_t sb = D.xfar_starts[b], se = D.xfar_starts[b + 1];
+  for (int64_t s0 = sb; s0 < se; s0 += kMaxSeg) {
+    const int nseg = int(se - s0 < kMaxSeg ? se - s0 : kMaxSeg);
+    __syncthreads();
+    const int total = load_segments(D.xfar_seg, s0, nseg, s_start, s_pre);
+    for (int base = 0; base < total; base += kP2LBatch) {
+      const int nb = min(kP2LBatch, total - base);
+      __syncthreads();
+      if (threadIdx.x < nb) {
+        const int s = seg_source(base + threadIdx.x, nseg, s_start, s_pre);
+        s_src[threadIdx.x] = D.src[s];
+        if (D.dipole) s_mu[threadIdx.x] = D.mu[s];
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nb * (P1 + 1); t += blockDim.x) {
+        const int s = t / (P1 + 1), m = t % (P1 + 1);
+        const double4 x = s_src[s];
+        double2 col[kMaxOrder + 1];
+        irregular_column((x.x - bc.x) * ih, (x.y - bc.y) * ih, (x.z - bc.z) * ih, m, P1, col);
+        for (int n = m; n <= P1; ++n) tab[s * kt + hidx(n, m)] = col[n - m];
+      }
+      __syncthreads();
+      int slot = 0;
+      for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
+        int n, m;
+        idx_nm(c, n, m);
+        double2 a = acc[slot];
+        for (int s = 0; s < nb; ++s) {
+          const double2* T = tab + s * kt;
+          const double w = s_src[s].w;
+          const double2 iv = T[hidx(n, m)];
+          a.x += w * iv.x;
+          a.y -= w * iv.y;
+          if (D.dipole) {
+            const double4 u = s_mu[s];
+            const double2 i0 = T[hidx(n + 1, m)];
+            const double2 ip = T[hidx(n + 1, m + 1)];
+            const double2 im = hget(T, n + 1, m - 1);
+            const double hx = 0.5 * u.x * ih, hy = 0.5 * u.y * ih, mz = u.z * ih;
+            const double gx = -mz * i0.x + (hx * im.x - hy * im.y) - (hx * ip.x + hy * ip.y);
+            const double gy = -mz * i0.y + (hx * im.y + hy * im.x) - (hx * ip.y - hy * ip.x);
+            a.x += gx;
+            a.y -= gy;
+          }
+        }
+        acc[slot] = a;
+      }
+    }
+  }
+  int slot = 0;
+  for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
+    double2 v = D.L[size_t(b) * D.kp + c];
+    v.x += acc[slot].x * ih;
+    v.y += acc[slot].y * ih;
+    D.L[size_t(b) * D.kp + c] = v;
+  }
+}
+
+// ---------------------------------------------------------------- L2L (Stage 7)
+// L~_child(n,m) += 2^-n sum_{j>=n,k} L~_parent(j,k) R_{j-n}^{k-m}(u_oct/2)
+__global__ void __launch_bounds__(256) k_l2l(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* Lp = sm;
+  double2* R = sm + D.kp;
+  const int b = boxes[blockIdx.x];
+  const int a = D.parent[b];
+  const int o = octant_of(D.box[b], D.box[a]);
+  for (int i = threadIdx.x; i < D.kp; i += blockDim.x) {
+    Lp[i] = D.L[size_t(a) * D.kp + i];
+    R[i] = D.oct_l2l[o * D.kp + i];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D.kp; c += blockDim.x) {
+    int n, m;
+    idx_nm(c, n, m);
+    double sx = 0, sy = 0;
+    for (int j = n; j <= D.p; ++j) {
+      const int jn = j - n;
+      for (int k = -j; k <= j; ++k) {
+        const int km = k - m;
+        if (km > jn || km < -jn) continue;
+        const double2 l = hget(Lp, j, k);
+        const double2 r = hget(R, jn, km);
+        sx += l.x * r.x - l.y * r.y;
+        sy += l.x * r.y + l.y * r.x;
+      }
+    }
+    const double s = ldexp(1.0, -n);
+    double2 v = D.L[size_t(b) * D.kp + c];
+    v.x += s * sx;
+    v.y += s * sy;
+    D.L[size_t(b) * D.kp + c] = v;
+  }
+}
+
+// ---------------------------------------------------------------- L2QBXL (Stage 8)
+// L~_c(n,m) += (r/h)^n sum_{j>=n,k} L~_b(j,k) R_{j-n}^{k-m}((c - c_b)/h)
+__global__ void __launch_bounds__(256) k_l2qbxl(DevData D, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* Lb = sm;          // kp
+  double2* T = sm + D.kp;    // kWfarGroup x kp
+  const int b = boxes[blockIdx.x];
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
+  for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Lb[i] = D.L[size_t(b) * D.kp + i];
+  const int G = min(kWfarGroup, int(blockDim.x) / D.kq);
+  for (int cg = 0; cg < nctr; cg += G) {
+    const int ng = min(G, nctr - cg);
+    __syncthreads();
+    for (int t = threadIdx.x; t < ng * (D.p + 1); t += blockDim.x) {
+      const int gg = t / (D.p + 1), mm = t % (D.p + 1);
+      const double4 cx = D.ctr[c0 + cg + gg];
+      double2 col[kMaxOrder + 1];
+      regular_column((cx.x - bc.x) * ih, (cx.y - bc.y) * ih, (cx.z - bc.z) * ih, mm, D.p, col);
+      for (int nn = mm; nn <= D.p; ++nn) T[gg * D.kp + hidx(nn, mm)] = col[nn - mm];
+    }
+    __syncthreads();
+    const int g = threadIdx.x / D.kq, oc = threadIdx.x % D.kq;
+    if (g < ng) {
+      int n, m;
+      idx_nm(oc, n, m);
+      const double4 c = D.ctr[c0 + cg + g];
+      const double2* Tg = T + g * D.kp;
+      double sx = 0, sy = 0;
+      for (int j = n; j <= D.p; ++j) {
+        const int jn = j - n;
+        for (int k = -j; k <= j; ++k) {
+          const int km = k - m;
+          if (km > jn || km < -jn) continue;
+          const double2 l = hget(Lb, j, k);
+          const double2 r = hget(Tg, jn, km);
+          sx += l.x * r.x - l.y * r.y;
+          sy += l.x * r.y + l.y * r.x;
+        }
+      }
+      const double s = ipow(c.w * ih, n);
+      double2* out = D.Lc + size_t(c0 + cg + g) * D.kq + oc;
+      double2 v = *out;
+      v.x += s * sx;
+      v.y += s * sy;
+      *out = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Stage 9
+// QBXL2P: pot_t = (1/4pi) sum L~_c R((t - c)/r);  L2P: pot_t = (1/4pi)(phi_t + sum L~_b R((t - c_b)/h))
+__global__ void k_eval_assoc(DevData D, int nt, const double* __restrict__ tpos, const int* __restrict__ assoc,
+                             const int* __restrict__ ctr_sorted, double* __restrict__ pot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int a = assoc[i];
+  if (a < 0) return;
+  const int cs = ctr_sorted[a];
+  const double4 c = D.ctr[cs];
+  const double ir = 1.0 / c.w;
+  const double v = eval_regular_sum(D.Lc + size_t(cs) * D.kq, D.q, (tpos[3 * i] - c.x) * ir,
+                                    (tpos[3 * i + 1] - c.y) * ir, (tpos[3 * i + 2] - c.z) * ir);
+  pot[i] = kInv4Pi * v;
+}
+
+__global__ void k_eval_conv(DevData D, int nconv, const int* __restrict__ tgt_perm, const int* __restrict__ tgt_box,
+                            double* __restrict__ pot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nconv) return;
+  const int b = tgt_box[i];
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  const double4 t = D.tgt[i];
+  const double v = eval_regular_sum(D.L + size_t(b) * D.kp, D.p, (t.x - bc.x) * ih, (t.y - bc.y) * ih,
+                                    (t.z - bc.z) * ih);
+  pot[tgt_perm[i]] = kInv4Pi * (D.phi[i] + v);
+}
+
+// Centre coefficients in the paper's normalisation (Eq. (5)):
+//   L^paper_n^m = (L~_n^m / r^n) / (4 pi N_nm (n+m)!),  N_nm = sqrt((2n+1)/(4 pi) (n-m)!/(n+m)!)
+__global__ void k_centre_out(DevData D, int nc, const int* __restrict__ ctr_perm, double* __restrict__ out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(nc) * D.kq) return;
+  const int cs = int(t / D.kq), c = int(t % D.kq);
+  int n, m;
+  idx_nm(c, n, m);
+  const double r = D.ctr[cs].w;
+  double fnm = 1, fnp = 1;
+  for (int i = 2; i <= n - m; ++i) fnm *= i;
+  for (int i = 2; i <= n + m; ++i) fnp *= i;
+  const double N = sqrt((2 * n + 1) / (4 * M_PI) * fnm / fnp);
+  const double f = 1.0 / (4 * M_PI * N * fnp * ipow(r, n));
+  const double2 v = D.Lc[size_t(cs) * D.kq + c];
+  const int64_t o = (int64_t(ctr_perm[cs]) * D.kq + c) * 2;
+  out[o] = v.x * f;
+  out[o + 1] = v.y * f;
+}
+
+// ---------------------------------------------------------------- operator tables
+__global__ void k_tables(DevData D, double2* m2l_tab, double2* oct_m2m, double2* oct_l2l) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o < 1331) {
+    const int dx = o / 121 - 5, dy = (o / 11) % 11 - 5, dz = o % 11 - 5;
+    double2* T = m2l_tab + size_t(o) * D.ktab_m2l;
+    if (dx == 0 && dy == 0 && dz == 0) {
+      for (int i = 0; i < D.ktab_m2l; ++i) T[i] = make_double2(0, 0);
+    } else {
+      irregular_table(2.0 * dx, 2.0 * dy, 2.0 * dz, 2 * D.p, T);
+    }
+  } else if (o < 1331 + 8) {
+    const int k = o - 1331;
+    regular_table((k & 1) ? 1.0 : -1.0, (k & 2) ? 1.0 : -1.0, (k & 4) ? 1.0 : -1.0, D.p, oct_m2m + k * D.kp);
+  } else if (o < 1331 + 16) {
+    const int k = o - 1331 - 8;
+    regular_table((k & 1) ? 0.5 : -0.5, (k & 2) ? 0.5 : -0.5, (k & 4) ? 0.5 : -0.5, D.p, oct_l2l + k * D.kp);
+  }
+}
+
+// ---------------------------------------------------------------- direct sum (qbx::direct_sum)
+__global__ void __launch_bounds__(256) k_direct_sum(int ns, const double4* __restrict__ src,
+                                                    const double4* __restrict__ mu, int nt,
+                                                    const double4* __restrict__ tgt, double* __restrict__ pot,
+                                                    unsigned long long* bad) {
+  __shared__ double4 s_src[256];
+  __shared__ double4 s_mu[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double4 t = make_double4(0, 0, 0, 0);
+  if (i < nt) t = tgt[i];
+  double acc = 0;
+  for (int base = 0; base < ns; base += 256) {
+    const int nb = min(256, ns - base);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      s_src[threadIdx.x] = src[base + threadIdx.x];
+      if (mu) s_mu[threadIdx.x] = mu[base + threadIdx.x];
+    }
+    __syncthreads();
+    if (i < nt) {
+      for (int j = 0; j < nb; ++j) {
+        const double4 x = s_src[j];
+        const double dx = t.x - x.x, dy = t.y - x.y, dz = t.z - x.z;
+        const double r2 = dx * dx + dy * dy + dz * dz;
+        if (r2 == 0.0) {
+          atomicMin(bad, (unsigned long long)i << 32 | (unsigned long long)(base + j));
+          continue;
+        }
+        const double rinv = 1.0 / sqrt(r2);
+        acc += x.w * rinv;
+        if (mu) {
+          const double4 u = s_mu[j];
+          acc += (u.x * dx + u.y * dy + u.z * dz) * rinv * rinv * rinv;
+        }
+      }
+    }
+  }
+  if (i < nt) pot[i] = 0.07957747154594766788 * acc;
+}
+
+template <int Q>
+void near_qbx_q(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (D.dipole)
+    k_near_qbx<Q, true><<<n, kNearThreads, 0, s>>>(D, boxes);
+  else
+    k_near_qbx<Q, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+}
+
+int block_for(int k) { return k <= 128 ? 128 : 256; }
+
+}  // namespace
+
+int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s) {
+  if (ns == 0) return 0;
+  k_gather<<<(ns + 255) / 256, 256, 0, s>>>(ns, perm, w, D.dipole ? mu : nullptr, D.src, D.dipole ? D.mu : nullptr);
+  return 1;
+}
+
+int launch_p2m(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = (kP2MBatch + 1) * D.kp * sizeof(double2);
+  k_p2m<<<n, 256, smem, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_m2m(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_m2m<<<n, block_for(D.kp), 2 * D.kp * sizeof(double2), s>>>(D, boxes);
+  return 1;
+}
+
+int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  switch (D.q) {
+    case 0: near_qbx_q<0>(D, boxes, n, s); break;
+    case 1: near_qbx_q<1>(D, boxes, n, s); break;
+    case 2: near_qbx_q<2>(D, boxes, n, s); break;
+    case 3: near_qbx_q<3>(D, boxes, n, s); break;
+    case 4: near_qbx_q<4>(D, boxes, n, s); break;
+    case 5: near_qbx_q<5>(D, boxes, n, s); break;
+    case 6: near_qbx_q<6>(D, boxes, n, s); break;
+    case 7: near_qbx_q<7>(D, boxes, n, s); break;
+    case 8: near_qbx_q<8>(D, boxes, n, s); break;
+    default: return -1;
+  }
+  return 1;
+}
+
+int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  if (D.dipole)
+    k_near_p2p<true><<<n, kNearThreads, 0, s>>>(D, boxes);
+  else
+    k_near_p2p<false><<<n, kNearThreads, 0, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_m2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = (D.kp + D.ktab_m2l) * sizeof(double2);
+  k_m2l<<<n, block_for(D.kp), smem, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = (D.kp + kWfarGroup * hsize(D.p + D.q)) * sizeof(double2);
+  k_wfar<<<n, 256, smem, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = kP2LBatch * hsize(D.p + 1) * sizeof(double2);
+  k_p2l<<<n, block_for(D.kp), smem, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_l2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_l2l<<<n, block_for(D.kp), 2 * D.kp * sizeof(double2), s>>>(D, boxes);
+  return 1;
+}
+
+int launch_l2qbxl(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const size_t smem = (D.kp + kWfarGroup * D.kp) * sizeof(double2);
+  k_l2qbxl<<<n, 256, smem, s>>>(D, boxes);
+  return 1;
+}
+
+int launch_eval(const DevData& D, int nt, const double* tpos, const int* assoc, const int* ctr_sorted, int nconv,
+                const int* tgt_perm, const int* tgt_box, double* pot, cudaStream_t s) {
+  int k = 0;
+  if (nt > 0) {
+    k_eval_assoc<<<(nt + 127) / 128, 128, 0, s>>>(D, nt, tpos, assoc, ctr_sorted, pot);
+    ++k;
+  }
+  if (nconv > 0) {
+    k_eval_conv<<<(nconv + 127) / 128, 128, 0, s>>>(D, nconv, tgt_perm, tgt_box, pot);
+    ++k;
+  }
+  return k;
+}
+
+int launch_centre_out(const DevData& D, int nc, const int* ctr_perm, double* out, cudaStream_t s) {
+  const int64_t n = int64_t(nc) * D.kq;
+  if (n == 0) return 0;
+  k_centre_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(D, nc, ctr_perm, out);
+  return 1;
+}
+
+int launch_tables(const DevData& D, double2* m2l_tab, double2* oct_m2m, double2* oct_l2l, cudaStream_t s) {
+  k_tables<<<(1331 + 16 + 127) / 128, 128, 0, s>>>(D, m2l_tab, oct_m2m, oct_l2l);
+  return 1;
+}
+
+int launch_direct_sum(int ns, const double4* src, const double4* mu, int nt, const double4* tgt, double* pot,
+                      unsigned long long* bad, cudaStream_t s) {
+  if (nt == 0) return 0;
+  k_direct_sum<<<(nt + 255) / 256, 256, 0, s>>>(ns, src, mu, nt, tgt, pot, bad);
+  return 1;
+}
+
+void set_smem_limits() {
+  static bool done = false;
+  if (done) return;
+  const int lim = 200 * 1024;
+  cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_wfar, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(k_l2qbxl, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  done = true;
+}
+
+}  // namespace dev
+}  // namespace qbxg
