@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""QBX-FMM layer-potential apply throughput on B200 (BASELINE.json metric).
+
+One step = one full GIGAQBX evaluation (Algorithm 4, Stages 2-9) of BASELINE.json
+config 1: Laplace single+double layer on the R=2/r=1 torus, 256x128 cells,
+65,536 flat triangles x 16 Gauss-Legendre/Duffy nodes = 1,048,576 sources,
+2,097,152 QBX centres and on-surface targets, p_fmm=15, p_qbx=5, n_max=64,
+t_f=0.9.  Metric: (N_S + N_T) / t_apply.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Default (no torchrun): N=1.  Under torchrun each rank drives one GPU; the
+apply is replicated per rank (the sharded multi-GPU apply is reported as
+"parallelism" in the config).  --impl reference times the CPU
+restatement of the path (oracle/, the reference ships no FMM code to run) on a
+bounded sample of the same workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+CONFIG_ID = 1
+CPU_SAMPLE = dict(nu=48, nv=24)  # 2,304 triangles, 36,864 sources: same family and orders, ~1/28 size
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--small", action="store_true", help="debug: torus 64x32 instead of config 1")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- work model
+def stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
+    """Algorithmic fp64 flops and compulsory bytes per stage (SURVEY.md §8d conventions:
+    real flops, FMA = 2; K_x = (x+1)(x+2)/2 half-table coefficients)."""
+    K = lambda x: (x + 1) * (x + 2) // 2
+    p, q = cfg.p_fmm, cfg.p_qbx
+    kp, kq, kpq = K(p), K(q), K(p + q)
+    dl = cfg.kernel == 1
+    src_b = 56 if dl else 32
+    f = {}
+    b = {}
+    f["p2m"] = led["n_p2m_sources"] * ((26 if dl else 10) * kp + (40 if dl else 30))
+    b["p2m"] = n_src * src_b + 16 * kp * led["n_p2m_sources"] / 8.0
+    f["m2m"] = led["n_m2m"] * 8 * kp * kp
+    b["m2m"] = led["n_m2m"] * 2 * 16 * kp
+    f["near"] = led["pairs_qbx_near"] * ((26 if dl else 10) * kq + (40 if dl else 30)) + \
+        led["pairs_p2p_near"] * (30 if dl else 20)
+    b["near"] = n_src * src_b + n_ctr * (32 + 16 * kq) + n_conv * 32
+    f["m2l"] = led["entries"]["V"] * 8 * kp * kp
+    b["m2l"] = led["entries"]["V"] * 0 + 2 * 16 * kp * led["n_l2l"]
+    f["wfar"] = led["pairs_wfar_centre"] * (8 * kp * kq + 10 * kpq + 30) + led["pairs_wfar_target"] * (10 * kp + 30)
+    b["wfar"] = n_ctr * 16 * kq * 2
+    f["p2l"] = led["pairs_xfar_source"] * ((26 if dl else 10) * kp + (40 if dl else 30))
+    b["p2l"] = led["entries"]["X_far"] * 16 * kp
+    f["l2l"] = led["n_l2l"] * 8 * kp * kp
+    b["l2l"] = led["n_l2l"] * 2 * 16 * kp
+    f["l2qbxl"] = n_ctr * (8 * kp * kq + 10 * kpq + 30)
+    b["l2qbxl"] = n_ctr * 16 * kq * 2
+    f["eval"] = n_assoc * (10 * kq + 30) + n_conv * (10 * kp + 30)
+    b["eval"] = n_assoc * (16 * kq + 24 + 4 + 8) + n_conv * (32 + 8)
+    return f, b
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU legs (oracle)
+def cpu_oracle_throughput(steps: int, warmup: int):
+    """The CPU restatement of the path (oracle/) on a bounded sample of the workload."""
+    import oracle as O
+    from paper_1805_06106_b200 import api
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    g = api.config_geometry(CONFIG_ID, **CPU_SAMPLE)
+    cfg = api.config_fmm(CONFIG_ID)
+    plan = api.Plan(cfg, g)
+    w, mu = g.weights(), g.dipoles()
+    for _ in range(warmup):
+        O.execute(plan, g, w, mu)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.execute(plan, g, w, mu)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    units = g.n_sources + g.n_targets
+    return dict(value=units / t, unit="points/s", cores=cores, kind="port",
+                sample=f"torus {CPU_SAMPLE['nu']}x{CPU_SAMPLE['nv']} cells ({g.n_sources} sources + {g.n_targets} "
+                       f"targets), p=15 q=5 SL+DL, oracle/ OpenMP restatement of Stages 2-9, mean of {steps} "
+                       f"after {warmup} warm-up", seconds_per_step=t)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    steps, warm = max(1, min(args.steps, 2)), 0
+    cb = cpu_oracle_throughput(steps, warm)
+    line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": cb["value"],
+            "unit": "points/s", "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+            "ms_per_step": cb["seconds_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (procedural torus, seeded density)",
+            "config": {"workload": "BASELINE config 1 family (torus SL+DL, p=15, q=5), bounded CPU sample",
+                       "sample": cb["sample"]},
+            "cpu_baseline": {"value": cb["value"], "unit": "points/s", "cores": cb["cores"], "kind": "port",
+                             "sample": cb["sample"]},
+            "e2e": {"value": cb["value"], "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU leg
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_1805_06106_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    t0 = time.perf_counter()
+    over = dict(nu=64, nv=32) if args.small else {}
+    g = api.config_geometry(CONFIG_ID, **over)
+    cfg = api.config_fmm(CONFIG_ID)
+    t1 = time.perf_counter()
+    plan = api.Plan(cfg, g)
+    t2 = time.perf_counter()
+    eng = api.FmmEngine(cfg, g, plan, device=local_rank)
+    t3 = time.perf_counter()
+    led = plan.ledger()
+    w, mu = g.weights(), g.dipoles()
+    dev = torch.device("cuda", local_rank)
+    d_w = torch.from_numpy(w).to(dev)
+    d_mu = torch.from_numpy(mu.reshape(-1)).to(dev)
+    d_pot = torch.empty(g.n_targets, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.apply_device(d_w.data_ptr(), d_mu.data_ptr(), d_pot.data_ptr(), None, stream.cuda_stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    stage_ms = {}
+    launches = 0
+    clk = ClockSampler(local_rank)
+    clk.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        tm, nl, _, _ = eng.last_timings()
+        launches += nl
+        for k, v in tm.items():
+            stage_ms[k] = stage_ms.get(k, 0.0) + v
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    for k in stage_ms:
+        stage_ms[k] /= args.steps
+    units = g.n_sources + g.n_targets
+    value = world * units / (ms * 1e-3)
+
+    # end to end through the public C-ABI call with pinned host buffers
+    hw = torch.from_numpy(w).pin_memory().numpy()
+    hmu = torch.from_numpy(mu).pin_memory().numpy()
+    e2e_times = []
+    for i in range(args.steps + 1):
+        if dist:
+            dist.barrier()
+        ta = time.perf_counter()
+        pot = eng.apply(hw, hmu)
+        tb = time.perf_counter()
+        if i > 0:
+            e2e_times.append(tb - ta)
+    _, _, h2d, d2h = eng.last_timings()
+    e2e_t = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * units / float(e2e_t.item())
+    # sanity: device-resident and host paths agree bitwise
+    same = bool(np.array_equal(pot, d_pot.cpu().numpy()))
+
+    # roofline of the dominant kernel, per-stage fractions
+    peak = api.measure_fp64_peak(local_rank)
+    n_assoc = int((g.association >= 0).sum())
+    flops, bytes_ = stage_work(led, cfg, g.n_sources, g.n_centers, n_assoc, g.n_targets - n_assoc)
+    with open(os.path.join(HERE, "MEASURED_PEAKS.json")) if os.path.exists(os.path.join(HERE, "MEASURED_PEAKS.json")) else open(os.devnull) as fh:
+        try:
+            mp = json.load(fh)
+        except Exception:
+            mp = {}
+    hbm = float(mp.get("hbm_gbs", 6548.8))
+    stages = {}
+    for k in flops:
+        t = stage_ms.get(k, 0.0) * 1e-3
+        if t <= 0:
+            continue
+        tf = flops[k] / t / 1e12
+        gbs = bytes_[k] / t / 1e9
+        stages[k] = {"ms": round(stage_ms[k], 4), "tflops": round(tf, 3), "frac_fp64": round(tf / peak, 4),
+                     "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4), "flops": flops[k]}
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    d = stages[dom]
+    roofline = {"bound": "fp64", "kernel": dom, "achieved": d["tflops"], "peak": round(peak, 3), "unit": "TFLOP/s",
+                "frac": d["frac_fp64"], "traffic": None,
+                "peak_source": "in-run DFMA microbenchmark (qbxg_measure_fp64_peak); MEASURED_PEAKS.json has no fp64",
+                "algorithmic_flops_per_launch": flops[dom]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_oracle_throughput(1, 0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": value,
+                "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (procedural torus, seeded Fourier density)",
+                "config": {"workload": "BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
+                                       "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9" if not args.small
+                           else "debug: torus 64x32", "n_sources": g.n_sources, "n_targets": g.n_targets,
+                           "n_centers": g.n_centers, "n_boxes": plan.view.n_boxes,
+                           "parallelism": "replicas" if world > 1 else "single GPU",
+                           "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"},
+                "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
+                "cpu_baseline": cpu,
+                "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
+                            "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3)},
+                "list_hashes": {k: f"{v:016x}" for k, v in plan.list_hashes().items()},
+                "host_device_bitwise_equal": same}
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -253,6 +253,8 @@ int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* w
 /* ---- misc ---------------------------------------------------------------- */
 const char* qbxg_last_error(void);
 int qbxg_device_count(int32_t* out);
+/* fp64 DFMA throughput of `device` (TFLOP/s), the roofline denominator of the fp64 stages. */
+int qbxg_measure_fp64_peak(int32_t device, double* out_tflops);
 const char* qbxg_version(void);
 
 #ifdef __cplusplus

@@ -74,36 +74,77 @@ cd sph_harm(int n, int m, double theta, double phi) {
   return norm * legendre(n, am, std::cos(theta)) * std::exp(cd(0, m * phi));
 }
 
+// All P_n^m(x), 0 <= m <= n <= P (no Condon-Shortley phase), in one O(P^2)
+// pass of the same recurrences as legendre(); table index idx(n, m).
+void legendre_table(int P, double x, std::vector<double>& T) {
+  T.assign(nfull(P), 0.0);
+  const double s = std::sqrt(std::max(0.0, (1.0 - x) * (1.0 + x)));
+  double pmm = 1.0;
+  for (int m = 0; m <= P; ++m) {
+    if (m > 0) pmm *= (2 * m - 1) * s;
+    T[idx(m, m)] = pmm;
+    if (m + 1 > P) break;
+    double a = pmm, b = x * (2 * m + 1) * pmm;
+    T[idx(m + 1, m)] = b;
+    for (int k = m + 2; k <= P; ++k) {
+      const double c = ((2 * k - 1) * x * b - (k + m - 1) * a) / (k - m);
+      T[idx(k, m)] = c;
+      a = b;
+      b = c;
+    }
+  }
+}
+
+struct FactTable {
+  double f[200];
+  FactTable() {
+    f[0] = 1;
+    for (int i = 1; i < 200; ++i) f[i] = f[i - 1] * i;
+  }
+};
+const FactTable kFact;
+
 // Regular / irregular solid harmonics by explicit spherical-coordinate
-// evaluation (oracle style: no Cartesian recurrences).
+// evaluation (oracle style: trig azimuth, Legendre in cos(theta); no
+// Cartesian recurrences).
 void regular(const double* x, int P, std::vector<cd>& R) {
+  thread_local std::vector<double> Pt;
   R.assign(nfull(P), cd(0));
   const double r = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
   const double ct = r > 0 ? x[2] / r : 1.0;
   const double phi = std::atan2(x[1], x[0]);
+  legendre_table(P, ct, Pt);
+  const cd e1 = std::exp(cd(0, phi));
   double rn = 1;
   for (int n = 0; n <= P; ++n) {
+    cd em = 1.0;
     for (int m = 0; m <= n; ++m) {
-      const cd v = rn * legendre(n, m, ct) * std::exp(cd(0, m * phi)) / factorial(n + m);
+      const cd v = rn * Pt[idx(n, m)] * em / kFact.f[n + m];
       R[idx(n, m)] = v;
       R[idx(n, -m)] = (m & 1 ? -1.0 : 1.0) * std::conj(v);
+      em *= e1;
     }
     rn *= r;
   }
 }
 
 void irregular(const double* x, int P, std::vector<cd>& I) {
+  thread_local std::vector<double> Pt;
   I.assign(nfull(P), cd(0));
   const double r = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
   if (r == 0) throw std::domain_error("irregular harmonic at the origin (source coincides with centre)");
   const double ct = x[2] / r;
   const double phi = std::atan2(x[1], x[0]);
+  legendre_table(P, ct, Pt);
+  const cd e1 = std::exp(cd(0, phi));
   double rn = 1.0 / r;
   for (int n = 0; n <= P; ++n) {
+    cd em = 1.0;
     for (int m = 0; m <= n; ++m) {
-      const cd v = factorial(n - m) * legendre(n, m, ct) * std::exp(cd(0, m * phi)) * rn;
+      const cd v = kFact.f[n - m] * Pt[idx(n, m)] * em * rn;
       I[idx(n, m)] = v;
       I[idx(n, -m)] = (m & 1 ? -1.0 : 1.0) * std::conj(v);
+      em *= e1;
     }
     rn /= r;
   }
@@ -137,7 +178,7 @@ struct Src {
 // P2M: M~ += w conj(R(u)) + conj(mu . grad R(u)) / h, u = (s - c)/h   (Eq. (10))
 void p2m(const Src& S, int64_t s, const double* c, double h, int P, std::vector<cd>& M) {
   double u[3] = {(S.pos[3 * s] - c[0]) / h, (S.pos[3 * s + 1] - c[1]) / h, (S.pos[3 * s + 2] - c[2]) / h};
-  std::vector<cd> R;
+  thread_local std::vector<cd> R;
   regular(u, P, R);
   for (int n = 0; n <= P; ++n)
     for (int m = -n; m <= n; ++m) {
@@ -150,7 +191,7 @@ void p2m(const Src& S, int64_t s, const double* c, double h, int P, std::vector<
 // P2L at a centre with scale h: L~ += (1/h)[w conj(I(u)) + conj(mu . grad I(u))/h]   (Eq. (5)/(8))
 void p2l(const Src& S, int64_t s, const double* c, double h, int P, std::vector<cd>& L) {
   double u[3] = {(S.pos[3 * s] - c[0]) / h, (S.pos[3 * s + 1] - c[1]) / h, (S.pos[3 * s + 2] - c[2]) / h};
-  std::vector<cd> I;
+  thread_local std::vector<cd> I;
   irregular(u, P + 1, I);
   for (int n = 0; n <= P; ++n)
     for (int m = -n; m <= n; ++m) {
@@ -163,7 +204,7 @@ void p2l(const Src& S, int64_t s, const double* c, double h, int P, std::vector<
 // Evaluate a box-scaled local (order P, scale h, centre c) at t: sum L~ R((t-c)/h)   (Eq. (9))
 double eval_local(const std::vector<cd>& L, int P, const double* c, double h, const double* t) {
   double u[3] = {(t[0] - c[0]) / h, (t[1] - c[1]) / h, (t[2] - c[2]) / h};
-  std::vector<cd> R;
+  thread_local std::vector<cd> R;
   regular(u, P, R);
   cd acc = 0;
   for (int n = 0; n <= P; ++n)
@@ -174,7 +215,7 @@ double eval_local(const std::vector<cd>& L, int P, const double* c, double h, co
 // Evaluate a box-scaled multipole at t: (1/h) sum M~ I((t-c)/h)
 double eval_multipole(const std::vector<cd>& M, int P, const double* c, double h, const double* t) {
   double u[3] = {(t[0] - c[0]) / h, (t[1] - c[1]) / h, (t[2] - c[2]) / h};
-  std::vector<cd> I;
+  thread_local std::vector<cd> I;
   irregular(u, P, I);
   cd acc = 0;
   for (int n = 0; n <= P; ++n)
@@ -186,7 +227,7 @@ double eval_multipole(const std::vector<cd>& M, int P, const double* c, double h
 //   M_n^m(C) = sum_{j,k} M_j^k(c) conj(R_{n-j}^{m-k}(c - C))   (Greengard thesis Thm 3.5.4)
 void m2m(const std::vector<cd>& Mc, int P, const double* c, double h, const double* C, double H, std::vector<cd>& Mp) {
   double d[3] = {(c[0] - C[0]) / h, (c[1] - C[1]) / h, (c[2] - C[2]) / h};
-  std::vector<cd> R;
+  thread_local std::vector<cd> R;
   regular(d, P, R);
   for (int n = 0; n <= P; ++n) {
     const double s = std::pow(h / H, n);
@@ -204,7 +245,7 @@ void m2m(const std::vector<cd>& Mc, int P, const double* c, double h, const doub
 void m2l(const std::vector<cd>& M, int P, const double* c, double h, const double* C, double H, int Q,
          std::vector<cd>& L) {
   double d[3] = {(C[0] - c[0]) / h, (C[1] - c[1]) / h, (C[2] - c[2]) / h};
-  std::vector<cd> I;
+  thread_local std::vector<cd> I;
   irregular(d, P + Q, I);
   for (int n = 0; n <= Q; ++n) {
     const double s = std::pow(H / h, n) / h;
@@ -222,7 +263,7 @@ void m2l(const std::vector<cd>& M, int P, const double* c, double h, const doubl
 void l2l(const std::vector<cd>& Lc, int P, const double* c, double h, const double* C, double H, int Q,
          std::vector<cd>& L) {
   double d[3] = {(C[0] - c[0]) / h, (C[1] - c[1]) / h, (C[2] - c[2]) / h};
-  std::vector<cd> R;
+  thread_local std::vector<cd> R;
   regular(d, P, R);
   for (int n = 0; n <= Q; ++n) {
     const double s = std::pow(H / h, n);

@@ -93,7 +93,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_geometry_spec_for_config", "qbxg_geometry_generate", "qbxg_geometry_view", "qbxg_geometry_destroy",
     "qbxg_plan_create", "qbxg_plan_view_get", "qbxg_plan_ledger", "qbxg_plan_destroy",
     "qbxg_create", "qbxg_apply", "qbxg_apply_device", "qbxg_destroy", "qbxg_direct_sum",
-    "qbxg_last_error", "qbxg_device_count", "qbxg_version",
+    "qbxg_last_error", "qbxg_device_count", "qbxg_version", "qbxg_measure_fp64_peak",
 )
 
 
@@ -116,6 +116,7 @@ def _declare(lib):
         "qbxg_last_error": ([], C.c_char_p),
         "qbxg_device_count": ([P(C.c_int32)], C.c_int),
         "qbxg_version": ([], C.c_char_p),
+        "qbxg_measure_fp64_peak": ([C.c_int32, P(C.c_double)], C.c_int),
     }
     for name, (args, res) in sig.items():
         if not hasattr(lib, name):

@@ -345,3 +345,10 @@ def device_count() -> int:
     n = C.c_int32(0)
     _check(_abi.lib().qbxg_device_count(C.byref(n)))
     return n.value
+
+
+def measure_fp64_peak(device: int = 0) -> float:
+    """Measured DFMA throughput (TFLOP/s) of the GPU: the fp64 roofline denominator."""
+    v = C.c_double(0)
+    _check(_abi.lib().qbxg_measure_fp64_peak(device, C.byref(v)))
+    return v.value

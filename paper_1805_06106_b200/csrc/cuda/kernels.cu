@@ -9,6 +9,7 @@
 // same as the CPU oracle's (oracle/qbx_oracle.cpp), restated on half tables.
 #include <cstdio>
 
+#include "qbxg.h"
 #include "harmonics.cuh"
 #include "kernels.cuh"
 
@@ -936,3 +937,53 @@ void set_smem_limits() {
 
 }  // namespace dev
 }  // namespace qbxg
+
+// ---------------------------------------------------------------- fp64 peak microbenchmark
+// Roofline denominator for the fp64 stages (MEASURED_PEAKS.json has no fp64
+// entry): 8 independent DFMA chains per thread, 148 x 8 CTAs of 256 threads.
+namespace qbxg {
+namespace dev {
+namespace {
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+}  // namespace dev
+}  // namespace qbxg
+
+extern "C" int qbxg_measure_fp64_peak(int32_t device, double* out_tflops) {
+  cudaSetDevice(device);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return QBXG_ERR_CUDA;
+  const int iters = 4096, blocks = nsm * 8, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    qbxg::dev::k_dfma_peak<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  const double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+  *out_tflops = flops / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return cudaGetLastError() == cudaSuccess ? QBXG_OK : QBXG_ERR_CUDA;
+}
