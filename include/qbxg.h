@@ -255,6 +255,8 @@ const char* qbxg_last_error(void);
 int qbxg_device_count(int32_t* out);
 /* fp64 DFMA throughput of `device` (TFLOP/s), the roofline denominator of the fp64 stages. */
 int qbxg_measure_fp64_peak(int32_t device, double* out_tflops);
+/* fp64 tensor-pipe (DMMA m8n8k4) throughput of `device` (TFLOP/s). */
+int qbxg_measure_dmma_peak(int32_t device, double* out_tflops);
 const char* qbxg_version(void);
 
 #ifdef __cplusplus

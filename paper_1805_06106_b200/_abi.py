@@ -94,6 +94,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_plan_create", "qbxg_plan_view_get", "qbxg_plan_ledger", "qbxg_plan_destroy",
     "qbxg_create", "qbxg_apply", "qbxg_apply_device", "qbxg_destroy", "qbxg_direct_sum",
     "qbxg_last_error", "qbxg_device_count", "qbxg_version", "qbxg_measure_fp64_peak",
+    "qbxg_measure_dmma_peak",
 )
 
 
@@ -117,6 +118,7 @@ def _declare(lib):
         "qbxg_device_count": ([P(C.c_int32)], C.c_int),
         "qbxg_version": ([], C.c_char_p),
         "qbxg_measure_fp64_peak": ([C.c_int32, P(C.c_double)], C.c_int),
+        "qbxg_measure_dmma_peak": ([C.c_int32, P(C.c_double)], C.c_int),
     }
     for name, (args, res) in sig.items():
         if not hasattr(lib, name):

@@ -352,3 +352,10 @@ def measure_fp64_peak(device: int = 0) -> float:
     v = C.c_double(0)
     _check(_abi.lib().qbxg_measure_fp64_peak(device, C.byref(v)))
     return v.value
+
+
+def measure_dmma_peak(device: int = 0) -> float:
+    """Measured fp64 tensor-pipe (DMMA) throughput (TFLOP/s)."""
+    v = C.c_double(0)
+    _check(_abi.lib().qbxg_measure_dmma_peak(device, C.byref(v)))
+    return v.value

@@ -100,6 +100,7 @@ struct Handle {
   double* d_mu_in = nullptr;
   double* d_pot = nullptr;
   double* d_coeffs = nullptr;
+  dev::M2LPlan m2l;
   int last_launches = 0;
 
   ~Handle() {
@@ -112,6 +113,109 @@ struct Handle {
 };
 
 namespace {
+
+// Group List-2 entries by relative offset for the dense per-offset M2L GEMM
+// (m2l_gemm.cu): operator tables, chunks bounded by the staging buffer, tiles
+// of <= 64 same-offset columns.
+void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
+  auto& O = H.owned;
+  dev::M2LPlan& P = H.m2l;
+  const int p = H.cfg.p_fmm;
+  P.KR = (p + 1) * (p + 1);
+  P.KRp = (P.KR + 63) / 64 * 64;
+  std::vector<int4> rdof(P.KRp, make_int4(0, 0, 0, 0));
+  std::vector<int> rmap(P.KRp, -1);
+  {
+    int r = 0;
+    for (int n = 0; n <= p; ++n)
+      for (int m = 0; m <= n; ++m)
+        for (int part = 0; part < (m == 0 ? 1 : 2); ++part) {
+          rdof[r] = make_int4(n, m, part, 0);
+          rmap[r] = 2 * dev::hidx(n, m) + part;
+          ++r;
+        }
+  }
+  P.rmap = dupload(O, rmap, s);
+  int4* d_rdof = dupload(O, rdof, s);
+  const int nb = V.n_boxes;
+  const int64_t* vs = V.list_starts[QBXG_LIST_V];
+  const int32_t* vb = V.list_boxes[QBXG_LIST_V];
+  const int64_t nent = vs[nb];
+  // offset slot of every entry, used-slot compaction
+  std::vector<int> slot(nent);
+  std::vector<int> slot_to_op(1331, -1), used;
+  for (int b = 0; b < nb; ++b)
+    for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
+      const int d = vb[e];
+      int dd[3];
+      for (int k = 0; k < 3; ++k)
+        dd[k] = int(std::lround((V.box_center[3 * b + k] - V.box_center[3 * d + k]) / (2.0 * V.box_radius[b])));
+      const int sl = ((dd[0] + 5) * 11 + (dd[1] + 5)) * 11 + (dd[2] + 5);
+      slot[e] = sl;
+      if (slot_to_op[sl] < 0) {
+        slot_to_op[sl] = int(used.size());
+        used.push_back(sl);
+      }
+    }
+  P.n_ops = int(used.size());
+  if (P.n_ops == 0) return;
+  int* d_used = dupload(O, used, s);
+  P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
+  dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
+  QCK(cudaGetLastError());
+
+  // chunking by staging-buffer capacity
+  size_t free_b = 0, total_b = 0;
+  QCK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t row_bytes = size_t(P.KRp) * sizeof(double);
+  size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
+  int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);
+  if (const char* env = std::getenv("QBXG_M2L_CHUNK_ENTRIES")) cap = std::max<int64_t>(64, std::atoll(env));
+  int64_t max_chunk = 0;
+  int b0 = 0;
+  while (b0 < nb) {
+    // extend the chunk over whole target boxes
+    int b1 = b0;
+    while (b1 < nb && (vs[b1 + 1] - vs[b0] <= cap || b1 == b0)) ++b1;
+    const int64_t base = vs[b0], cnt = vs[b1] - vs[b0];
+    if (cnt > 0) {
+      dev::M2LChunk C;
+      C.base = base;
+      std::vector<int> boxes;
+      for (int b = b0; b < b1; ++b)
+        if (vs[b + 1] > vs[b]) boxes.push_back(b);
+      // counting sort of entries by operator, keeping CSR order inside an operator
+      std::vector<int64_t> cnt_op(P.n_ops + 1, 0);
+      for (int64_t e = base; e < base + cnt; ++e) cnt_op[slot_to_op[slot[e]] + 1]++;
+      for (int o = 0; o < P.n_ops; ++o) cnt_op[o + 1] += cnt_op[o];
+      std::vector<int> col_src(cnt), col_pos(cnt);
+      std::vector<double> col_scale(cnt);
+      std::vector<int64_t> fill(cnt_op.begin(), cnt_op.end() - 1);
+      for (int b = b0; b < b1; ++b)
+        for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
+          const int64_t i = fill[slot_to_op[slot[e]]]++;
+          col_src[i] = vb[e];
+          col_pos[i] = int(e - base);
+          col_scale[i] = 1.0 / V.box_radius[b];
+        }
+      std::vector<int4> tiles;
+      for (int o = 0; o < P.n_ops; ++o)
+        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += 64)
+          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(64, cnt_op[o + 1] - i)), 0));
+      C.n_tiles = int(tiles.size());
+      C.tiles = dupload(O, tiles, s);
+      C.col_src = dupload(O, col_src, s);
+      C.col_pos = dupload(O, col_pos, s);
+      C.col_scale = dupload(O, col_scale, s);
+      C.n_boxes = int(boxes.size());
+      C.boxes = dupload(O, boxes, s);
+      P.chunks.push_back(C);
+      max_chunk = std::max(max_chunk, cnt);
+    }
+    b0 = b1;
+  }
+  P.temp = dalloc<double>(O, size_t(max_chunk) * P.KRp);
+}
 
 void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device) {
   check_device();
@@ -310,6 +414,8 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   H.d_mu_in = D.dipole ? dalloc<double>(O, 3 * H.ns) : nullptr;
   H.d_pot = dalloc<double>(O, H.nt);
   H.d_coeffs = dalloc<double>(O, size_t(H.nc) * 2 * D.kq);
+
+  build_m2l(H, V, s);
   QCK(cudaGetLastError());
   QCK(cudaStreamSynchronize(s));
 }
@@ -338,7 +444,10 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
-  chk(dev::launch_m2l(D, H.d_v_boxes, H.n_v_boxes, s));
+  if (std::getenv("QBXG_M2L_NAIVE"))
+    chk(dev::launch_m2l(D, H.d_v_boxes, H.n_v_boxes, s));
+  else
+    chk(dev::launch_m2l_dense(H.m2l, D, s));
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::launch_wfar(D, H.d_wfar_boxes, H.n_wfar_boxes, s));
   QCK(cudaEventRecord(ev[6], s));

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -49,6 +50,29 @@ struct DevData {
   const double2* oct_m2m;  // 8 x kp: R((child-parent)/|child|)
   const double2* oct_l2l;  // 8 x kp: R((child-parent)/|parent|)
 };
+
+// Dense per-offset M2L (m2l_gemm.cu).  Work is split into chunks of target
+// boxes (contiguous in List-2 CSR order) so the staging buffer stays bounded.
+struct M2LChunk {
+  int n_tiles = 0;
+  int4* tiles = nullptr;       // (operator index, first column, column count, 0)
+  int* col_src = nullptr;      // source box of each column (offset-sorted)
+  int* col_pos = nullptr;      // List-2 CSR position (relative to base) of each column
+  double* col_scale = nullptr; // 1/|b| of the target box
+  int n_boxes = 0;
+  int* boxes = nullptr;        // target boxes of the chunk
+  int64_t base = 0;            // first CSR position of the chunk
+};
+struct M2LPlan {
+  int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64
+  int n_ops = 0;               // used offsets
+  double* ops = nullptr;       // n_ops x KRp x KRp
+  int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
+  double* temp = nullptr;      // staging: max chunk entries x KRp
+  std::vector<M2LChunk> chunks;
+};
+int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
+int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
 
 // launchers (return number of kernels launched)
 int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s);

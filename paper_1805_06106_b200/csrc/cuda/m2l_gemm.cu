@@ -1,0 +1,289 @@
+// Stage 4 (M2L over List 2) as one dense contraction per
+// relative box offset, on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64).
+//
+// With box-scaled coefficients the M2L operator depends only on the offset
+// delta = (c_b - c_d) / (2|b|) in [-5,5]^3 (11^3 - 5^3 = 1,206 used offsets,
+// PAPER.md:3622-3626), up to a 1/|b| factor:
+//   L~_b(n,m) += (1/|b|) (-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}(2 delta).
+// For real densities M_j^{-k} = (-1)^k conj(M_j^k) and M_j^0, L_n^0 are real,
+// so the map acts on (p+1)^2 real degrees of freedom ("real DOF": per degree n,
+// Re L_n^0, then Re/Im L_n^m for m = 1..n) as a real (p+1)^2 x (p+1)^2 matrix
+// T_delta (256 x 256 at p = 15).  Per offset that is a GEMM
+//   C[KR x n_pairs] = T_delta[KR x KR] * B[KR x n_pairs]
+// whose columns gather the source boxes' multipoles.  Columns of one offset
+// hit distinct target boxes; results go to a per-entry staging buffer in List-2
+// CSR order and a second kernel sums each target box's row in that order, so
+// the result is bitwise reproducible and needs no atomics.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qbxg.h"
+#include "harmonics.cuh"
+#include "kernels.cuh"
+
+namespace qbxg {
+namespace dev {
+
+namespace {
+
+constexpr int kKC = 16;          // K chunk per pipeline stage
+constexpr int kAPad = kKC + 4;   // A smem row stride (doubles): conflict-free fragment reads
+constexpr int kBN = 64;          // columns (pairs) per CTA tile
+constexpr int kBPad = kBN + 4;   // B smem row stride
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Build T_delta for each used offset: rows/cols in real-DOF order, KRp x KRp
+// row-major, zero padded.  rdof[r] = (n, m, part).
+__global__ void __launch_bounds__(256) k_m2l_ops(int p, int KR, int KRp, const int* __restrict__ used_slot,
+                                                 const int4* __restrict__ rdof, double* __restrict__ ops) {
+  extern __shared__ double2 sI[];  // hsize(2p)
+  const int o = blockIdx.x;
+  const int slot = used_slot[o];
+  const int dx = slot / 121 - 5, dy = (slot / 11) % 11 - 5, dz = slot % 11 - 5;
+  const int P2 = 2 * p;
+  if (threadIdx.x <= P2) {
+    double2 col[kMaxOrder + 1];
+    irregular_column(2.0 * dx, 2.0 * dy, 2.0 * dz, threadIdx.x, P2, col);
+    for (int n = threadIdx.x; n <= P2; ++n) sI[hidx(n, threadIdx.x)] = col[n - threadIdx.x];
+  }
+  __syncthreads();
+  double* T = ops + size_t(o) * KRp * KRp;
+  for (int idx = threadIdx.x; idx < KRp * KRp; idx += blockDim.x) {
+    const int ro = idx / KRp, ri = idx % KRp;
+    double v = 0.0;
+    if (ro < KR && ri < KR) {
+      const int4 a = rdof[ro], b = rdof[ri];
+      const int n = a.x, m = a.y, po = a.z, j = b.x, k = b.y, pi = b.z;
+      const double s = ((n + m) & 1) ? -1.0 : 1.0;
+      const double2 A = hget(sI, j + n, k - m);
+      double2 B = make_double2(0, 0);
+      if (k > 0) {
+        B = hget(sI, j + n, -k - m);
+        if (k & 1) B = make_double2(-B.x, -B.y);
+      }
+      // L = A M + B conj(M), M = x + i y:  Re: Re(A+B) x - Im(A-B) y;  Im: Im(A+B) x + Re(A-B) y
+      if (po == 0)
+        v = (pi == 0) ? (A.x + B.x) : -(A.y - B.y);
+      else
+        v = (pi == 0) ? (A.y + B.y) : (A.x - B.x);
+      v *= s;
+    }
+    T[idx] = v;
+  }
+}
+
+// One CTA: one offset, up to kBN pairs; 8 warps x (8*MT rows); full K.
+template <int MT>
+__global__ void __launch_bounds__(256) k_m2l_gemm(const double* __restrict__ ops, const int4* __restrict__ tiles,
+                                                  const int* __restrict__ col_src, const int* __restrict__ col_pos,
+                                                  const double* __restrict__ col_scale,
+                                                  const int* __restrict__ rmap, const double* __restrict__ M,
+                                                  int kp2, double* __restrict__ temp) {
+  constexpr int KRp = 64 * MT;
+  extern __shared__ double smem[];
+  double* As = smem;                              // 2 x KRp x kAPad
+  double* Bs = smem + 2 * KRp * kAPad;            // 2 x kKC x kBPad
+  __shared__ int s_src[kBN];
+  __shared__ int s_map[KRp];
+  const int4 tile = tiles[blockIdx.x];  // (op index, first column, count, -)
+  const double* T = ops + size_t(tile.x) * KRp * KRp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kBN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+  for (int i = tid; i < KRp; i += 256) s_map[i] = rmap[i];
+  __syncthreads();
+
+  auto load_stage = [&](int buf, int k0) {
+    double* A = As + buf * KRp * kAPad;
+    // A: KRp rows x kKC doubles = KRp x 8 16-byte copies
+    for (int i = tid; i < KRp * (kKC / 2); i += 256) {
+      const int r = i / (kKC / 2), c = (i % (kKC / 2)) * 2;
+      cp_async16(A + r * kAPad + c, T + size_t(r) * KRp + k0 + c);
+    }
+    double* B = Bs + buf * kKC * kBPad;
+    for (int i = tid; i < kKC * kBN; i += 256) {
+      const int kk = i / kBN, c = i % kBN;
+      const int src = s_src[c];
+      const int mo = s_map[k0 + kk];
+      if (src >= 0 && mo >= 0)
+        cp_async8(B + kk * kBPad + c, M + size_t(src) * kp2 + mo);
+      else
+        B[kk * kBPad + c] = 0.0;
+    }
+    cp_async_commit();
+  };
+
+  double acc[MT][8][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = KRp / kKC;
+  load_stage(0, 0);
+  const int row_w = warp * 8 * MT;
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      load_stage((kc + 1) & 1, (kc + 1) * kKC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* A = As + (kc & 1) * KRp * kAPad;
+    const double* B = Bs + (kc & 1) * kKC * kBPad;
+#pragma unroll
+    for (int kk = 0; kk < kKC; kk += 4) {
+      double a[MT], b[8];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = A[(row_w + i * 8 + (lane >> 2)) * kAPad + kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = B[(kk + (lane & 3)) * kBPad + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  // epilogue: temp[pos][row] = scale * acc
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = j * 8 + (lane & 3) * 2 + h;
+      if (c >= tile.z) continue;
+      const int pos = col_pos[tile.y + c];
+      const double sc = col_scale[tile.y + c];
+      double* out = temp + size_t(pos) * KRp;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) out[row_w + i * 8 + (lane >> 2)] = sc * acc[i][j][h];
+    }
+  }
+}
+
+// Sum each target box's staged rows in List-2 CSR order and add to L~_b.
+__global__ void __launch_bounds__(256) k_m2l_reduce(const int* __restrict__ boxes, const int64_t* __restrict__ v_starts,
+                                                    int64_t chunk_base, int KR, int KRp,
+                                                    const int* __restrict__ rmap, const double* __restrict__ temp,
+                                                    double* __restrict__ L, int kp2) {
+  const int b = boxes[blockIdx.x];
+  const int64_t a = v_starts[b] - chunk_base, e = v_starts[b + 1] - chunk_base;
+  for (int r = threadIdx.x; r < KR; r += blockDim.x) {
+    double s = 0.0;
+    for (int64_t pos = a; pos < e; ++pos) s += temp[pos * KRp + r];
+    L[size_t(b) * kp2 + rmap[r]] += s;
+  }
+}
+
+// DMMA throughput microbenchmark: 16 independent m8n8k4 accumulators per warp.
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
+  double acc[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 0.5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dmma(acc[i][0], acc[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i][0] + acc[i][1];
+  if (s == 1234.5) out[0] = s;
+}
+
+template <int MT>
+void gemm_mt(const M2LPlan& P, int chunk, const double* M, int kp2, cudaStream_t s) {
+  const M2LChunk& C = P.chunks[chunk];
+  const size_t smem = (2 * 64 * MT * kAPad + 2 * kKC * kBPad) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2l_gemm<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_m2l_gemm<MT><<<C.n_tiles, 256, smem, s>>>(P.ops, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap, M, kp2,
+                                              P.temp);
+}
+
+}  // namespace
+
+int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s) {
+  const size_t smem = hsize(2 * p) * sizeof(double2);
+  cudaFuncSetAttribute(k_m2l_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_m2l_ops<<<P.n_ops, 256, smem, s>>>(p, P.KR, P.KRp, used_slot, rdof, P.ops);
+  return 1;
+}
+
+int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
+  int k = 0;
+  const int kp2 = 2 * D.kp;
+  for (int c = 0; c < int(P.chunks.size()); ++c) {
+    const M2LChunk& C = P.chunks[c];
+    if (C.n_tiles == 0) continue;
+    switch (P.KRp / 64) {
+      case 1: gemm_mt<1>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 2: gemm_mt<2>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 3: gemm_mt<3>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 4: gemm_mt<4>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 5: gemm_mt<5>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 6: gemm_mt<6>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 7: gemm_mt<7>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      case 8: gemm_mt<8>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
+      default: return -1;
+    }
+    k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp,
+                                            reinterpret_cast<double*>(D.L), kp2);
+    k += 2;
+  }
+  return k;
+}
+
+}  // namespace dev
+}  // namespace qbxg
+
+extern "C" int qbxg_measure_dmma_peak(int32_t device, double* out_tflops) {
+  cudaSetDevice(device);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  if (cudaMalloc(&d, 8) != cudaSuccess) return QBXG_ERR_CUDA;
+  const int iters = 2048, blocks = nsm * 4, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    qbxg::dev::k_dmma_peak<<<blocks, threads>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  const double flops = 2.0 * 256 * 16 * double(iters) * (blocks * threads / 32);
+  *out_tflops = flops / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return cudaGetLastError() == cudaSuccess ? QBXG_OK : QBXG_ERR_CUDA;
+}
