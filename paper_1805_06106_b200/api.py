@@ -205,8 +205,11 @@ CONFIG_ORDERS = {0: (10, 3, _abi.KERNEL_LAPLACE_SL), 1: (15, 5, _abi.KERNEL_LAPL
 
 
 def config_fmm(config_id: int, **overrides) -> FmmConfig:
+    """FmmConfig of a BASELINE.json config.  List-3-far demotion (Remark 1,
+    PAPER.md:2246-2256) uses the spec's cost-balance threshold p^3/q^2
+    (SPEC.md:382); pass w_far_demote=0 to disable it."""
     p, q, k = CONFIG_ORDERS[config_id]
-    cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k)
+    cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k, w_far_demote=(p ** 3) // max(q * q, 1))
     for key, v in overrides.items():
         setattr(cfg, key, v)
     return cfg

@@ -91,10 +91,22 @@ struct Handle {
   int n_tgt_boxes = 0;
   int* d_v_boxes = nullptr;
   int n_v_boxes = 0;
-  int* d_wfar_boxes = nullptr;
+  int* d_wfar_boxes = nullptr;   // boxes with List 3 far entries and centres
   int n_wfar_boxes = 0;
+  int* d_wfar_tboxes = nullptr;  // boxes with List 3 far entries and conventional targets
+  int n_wfar_tboxes = 0;
   int* d_xfar_boxes = nullptr;
   int n_xfar_boxes = 0;
+  int2* d_items_wfar = nullptr;  // (box, centre offset) chunks for M2QBXL
+  int n_items_wfar = 0;
+  int2* d_items_ctr = nullptr;   // (box, centre offset) chunks for L2QBXL
+  int n_items_ctr = 0;
+  int* d_ctr_box = nullptr;      // owning box of each sorted centre
+  int* d_flat_all = nullptr;     // 0..nc-1
+  int* d_flat_wfar = nullptr;    // sorted centres of boxes with List 3 far entries
+  int n_flat_wfar = 0;
+  int ctr_mode = 0;              // 0 flat, 1 gemm, 2 per-box
+  dev::PairPlan wpairs;          // M2QBXL (centre, W_far box) pairs
   // staging for host applies
   double* d_w = nullptr;
   double* d_mu_in = nullptr;
@@ -359,7 +371,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     D.wfar_box = dupload(O, wbox, s);
 
     // work lists
-    std::vector<int> leaves, cb, tb, vb, wb, xb;
+    std::vector<int> leaves, cb, tb, vb, wb, wtb, xb;
     H.d_m2m_level.assign(H.nlev, nullptr);
     H.n_m2m_level.assign(H.nlev, 0);
     H.d_l2l_level.assign(H.nlev, nullptr);
@@ -370,7 +382,8 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       if (V.ctr_own_count[b] > 0) cb.push_back(b);
       if (V.tgt_own_count[b] > 0 && ns_[b + 1] > ns_[b]) tb.push_back(b);
       if (vs[b + 1] > vs[b]) vb.push_back(b);
-      if (ws[b + 1] > ws[b] && (V.ctr_own_count[b] + V.tgt_own_count[b]) > 0) wb.push_back(b);
+      if (ws[b + 1] > ws[b] && V.ctr_own_count[b] > 0) wb.push_back(b);
+      if (ws[b + 1] > ws[b] && V.tgt_own_count[b] > 0) wtb.push_back(b);
       if (xs[b + 1] > xs[b]) xb.push_back(b);
     }
     // conventional targets with an empty near list still need phi = 0
@@ -384,6 +397,64 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_v_boxes = int(vb.size());
     H.d_wfar_boxes = dupload(O, wb, s);
     H.n_wfar_boxes = int(wb.size());
+    H.d_wfar_tboxes = dupload(O, wtb, s);
+    H.n_wfar_tboxes = int(wtb.size());
+    std::vector<int2> iw, ic;
+    for (int b : wb)
+      for (int o = 0; o < V.ctr_own_count[b]; o += 16) iw.push_back(make_int2(b, o));
+    for (int b : cb)
+      for (int o = 0; o < V.ctr_own_count[b]; o += 16) ic.push_back(make_int2(b, o));
+    H.d_items_wfar = dupload(O, iw, s);
+    H.n_items_wfar = int(iw.size());
+    H.d_items_ctr = dupload(O, ic, s);
+    H.n_items_ctr = int(ic.size());
+    std::vector<int> cbox(H.nc), all(H.nc), fw;
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < V.ctr_own_count[b]; ++j) cbox[V.ctr_own_start[b] + j] = b;
+    for (int64_t i = 0; i < H.nc; ++i) all[i] = int(i);
+    for (int b : wb)
+      for (int j = 0; j < V.ctr_own_count[b]; ++j) fw.push_back(V.ctr_own_start[b] + j);
+    H.d_ctr_box = dupload(O, cbox, s);
+    H.d_flat_all = dupload(O, all, s);
+    H.d_flat_wfar = dupload(O, fw, s);
+    H.n_flat_wfar = int(fw.size());
+    if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
+    // (centre, W_far box) pairs, centre-major, chunked to bound the staging buffer
+    {
+      const int64_t cap_pairs = int64_t(1) << 24;
+      std::vector<int2> pairs;
+      std::vector<int> centres, starts;
+      int64_t total = 0, max_chunk = 0;
+      auto flush = [&]() {
+        if (centres.empty()) return;
+        dev::PairChunk C;
+        C.n_pairs = int(pairs.size());
+        C.pair_base = starts.front();
+        C.n_centres = int(centres.size());
+        starts.push_back(int(total));
+        C.pairs = dupload(O, pairs, s);
+        C.centres = dupload(O, centres, s);
+        C.starts = dupload(O, starts, s);
+        H.wpairs.chunks.push_back(C);
+        max_chunk = std::max<int64_t>(max_chunk, int64_t(pairs.size()));
+        pairs.clear();
+        centres.clear();
+        starts.clear();
+      };
+      for (int b : wb) {
+        const int64_t a = ws[b], e = ws[b + 1];
+        for (int j = 0; j < V.ctr_own_count[b]; ++j) {
+          if (int64_t(pairs.size()) + (e - a) > cap_pairs) flush();
+          const int cs = V.ctr_own_start[b] + j;
+          centres.push_back(cs);
+          starts.push_back(int(total));
+          for (int64_t i = a; i < e; ++i) pairs.push_back(make_int2(cs, wbox[i]));
+          total += e - a;
+        }
+      }
+      flush();
+      H.wpairs.temp = dalloc<double2>(O, size_t(std::max<int64_t>(max_chunk, 1)) * D.kq);
+    }
     H.d_xfar_boxes = dupload(O, xb, s);
     H.n_xfar_boxes = int(xb.size());
     for (int l = 0; l < H.nlev; ++l) {
@@ -449,13 +520,26 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   else
     chk(dev::launch_m2l_dense(H.m2l, D, s));
   QCK(cudaEventRecord(ev[5], s));
-  chk(dev::launch_wfar(D, H.d_wfar_boxes, H.n_wfar_boxes, s));
+  if (H.ctr_mode == 0) {
+    chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
+    chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
+  } else if (H.ctr_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, true)) {
+    chk(dev::launch_ctr_gemm(D, H.d_items_wfar, H.n_items_wfar, true, s));
+    chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
+  } else {
+    chk(dev::launch_wfar2(D, H.d_wfar_boxes, H.n_wfar_boxes, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
+  }
   QCK(cudaEventRecord(ev[6], s));
   chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(ev[7], s));
   for (int l = 1; l < H.nlev; ++l) chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
   QCK(cudaEventRecord(ev[8], s));
-  chk(dev::launch_l2qbxl(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  if (H.ctr_mode == 0)
+    chk(dev::launch_ctr_flat(D, H.d_flat_all, int(H.nc), H.d_ctr_box, false, s));
+  else if (H.ctr_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
+    chk(dev::launch_ctr_gemm(D, H.d_items_ctr, H.n_items_ctr, false, s));
+  else
+    chk(dev::launch_l2qbxl2(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   QCK(cudaEventRecord(ev[9], s));
   chk(dev::launch_eval(D, int(H.nt), H.d_tpos, H.d_assoc, H.d_ctr_sorted, int(H.nconv), H.d_tgt_perm, H.d_tgt_box,
                        d_pot, s));

@@ -74,6 +74,32 @@ struct M2LPlan {
 int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
 int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
 
+// Box expansion -> centre locals as DMMA GEMMs (centre_gemm.cu); items are
+// (box, first centre offset) chunks of up to 16 centres.
+bool ctr_gemm_fits(int p, int q, bool irreg);
+int launch_ctr_gemm(const DevData& D, const int2* items, int n_items, bool irreg, cudaStream_t s);
+
+// Thread-per-centre translations (centre_trans.cu)
+int launch_wfar2(const DevData& D, const int* ctr_boxes, int n_ctr, const int* tgt_boxes, int n_tgt,
+                 cudaStream_t s);
+int launch_l2qbxl2(const DevData& D, const int* boxes, int n, cudaStream_t s);
+// M2QBXL over (centre, List-3-far box) pairs, chunked by centres.
+struct PairChunk {
+  int n_pairs = 0;
+  int2* pairs = nullptr;   // (sorted centre, source box), centre-major
+  int pair_base = 0;       // index of the chunk's first pair (starts are global)
+  int n_centres = 0;
+  int* centres = nullptr;  // sorted centre ids of the chunk
+  int* starts = nullptr;   // n_centres + 1 global pair offsets
+};
+struct PairPlan {
+  double2* temp = nullptr;  // max chunk pairs x kq
+  std::vector<PairChunk> chunks;
+};
+int launch_m2qbxl_pairs(const DevData& D, const PairPlan& P, cudaStream_t s);
+// flat thread-per-centre variant: items = sorted centre indices, ctr_box = owner box
+int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s);
+
 // launchers (return number of kernels launched)
 int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s);
 int launch_p2m(const DevData& D, const int* boxes, int n, cudaStream_t s);
