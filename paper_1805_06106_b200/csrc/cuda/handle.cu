@@ -107,6 +107,10 @@ struct Handle {
   int n_flat_wfar = 0;
   int ctr_mode = 0;              // 0 flat, 1 gemm, 2 per-box
   dev::PairPlan wpairs;          // M2QBXL (centre, W_far box) pairs
+  double* ops_m2m = nullptr;     // 8 octant operators (real DOF)
+  double* ops_l2l = nullptr;
+  std::vector<dev::ShiftLevel> m2m_levels, l2l_levels;
+  int shift_mode = 0;            // 0 DMMA GEMM, 1 per-box kernels
   // staging for host applies
   double* d_w = nullptr;
   double* d_mu_in = nullptr;
@@ -170,7 +174,88 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
       }
     }
   P.n_ops = int(used.size());
-  if (P.n_ops == 0) return;
+
+  // --- tree shifts: octant operators and per-level tiles
+  int64_t max_level_rows = 1;
+  {
+    H.ops_m2m = dalloc<double>(O, size_t(8) * P.KRp * P.KRp);
+    H.ops_l2l = dalloc<double>(O, size_t(8) * P.KRp * P.KRp);
+    dev::launch_shift_ops(1, p, P.KR, P.KRp, d_rdof, H.ops_m2m, s);
+    dev::launch_shift_ops(2, p, P.KR, P.KRp, d_rdof, H.ops_l2l, s);
+    auto octant = [&](int c, int par) {
+      return (V.box_center[3 * c] > V.box_center[3 * par] ? 1 : 0) |
+             (V.box_center[3 * c + 1] > V.box_center[3 * par + 1] ? 2 : 0) |
+             (V.box_center[3 * c + 2] > V.box_center[3 * par + 2] ? 4 : 0);
+    };
+    // cols: (octant, src, pos) -> tiles of <= 64 same-octant columns
+    auto make_level = [&](const std::vector<int3>& cols, const std::vector<int>& outb,
+                          const std::vector<int2>& seg) {
+      dev::ShiftLevel L;
+      if (cols.empty()) return L;
+      std::vector<int> csrc, cpos;
+      std::vector<double> cscale;
+      std::vector<int4> tiles;
+      for (int o = 0; o < 8; ++o) {
+        const int first = int(csrc.size());
+        for (const int3& c : cols)
+          if (c.x == o) {
+            csrc.push_back(c.y);
+            cpos.push_back(c.z);
+            cscale.push_back(1.0);
+          }
+        for (int i = first; i < int(csrc.size()); i += 64)
+          tiles.push_back(make_int4(o, i, std::min(64, int(csrc.size()) - i), 0));
+      }
+      L.n_tiles = int(tiles.size());
+      L.tiles = dupload(O, tiles, s);
+      L.col_src = dupload(O, csrc, s);
+      L.col_pos = dupload(O, cpos, s);
+      L.col_scale = dupload(O, cscale, s);
+      L.n_out = int(outb.size());
+      L.out_boxes = dupload(O, outb, s);
+      L.out_seg = dupload(O, seg, s);
+      max_level_rows = std::max<int64_t>(max_level_rows, int64_t(cols.size()));
+      return L;
+    };
+    H.m2m_levels.assign(H.nlev, dev::ShiftLevel());
+    H.l2l_levels.assign(H.nlev, dev::ShiftLevel());
+    for (int l = 0; l < H.nlev; ++l) {
+      std::vector<int3> cols;
+      std::vector<int> outb;
+      std::vector<int2> seg;
+      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
+        const int b = V.level_boxes[i];
+        if ((V.box_flags[b] & QBXG_BOX_LEAF) || !(V.box_flags[b] & QBXG_BOX_HAS_SOURCES)) continue;
+        const int first = int(cols.size());
+        for (int k = V.child_starts[b]; k < V.child_starts[b + 1]; ++k) {
+          const int c = V.children[k];
+          if (V.src_sub_count[c] == 0) continue;
+          cols.push_back(make_int3(octant(c, b), c, int(cols.size())));
+        }
+        outb.push_back(b);
+        seg.push_back(make_int2(first, int(cols.size())));
+      }
+      H.m2m_levels[l] = make_level(cols, outb, seg);
+      cols.clear();
+      outb.clear();
+      seg.clear();
+      if (l == 0) continue;
+      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
+        const int b = V.level_boxes[i];
+        if (!(V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR))) continue;
+        const int par = V.box_parent[b];
+        const int pos = int(cols.size());
+        cols.push_back(make_int3(octant(b, par), par, pos));
+        outb.push_back(b);
+        seg.push_back(make_int2(pos, pos + 1));
+      }
+      H.l2l_levels[l] = make_level(cols, outb, seg);
+    }
+  }
+  if (P.n_ops == 0) {
+    P.temp = dalloc<double>(O, size_t(max_level_rows) * P.KRp);
+    return;
+  }
   int* d_used = dupload(O, used, s);
   P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
   dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
@@ -226,7 +311,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
     }
     b0 = b1;
   }
-  P.temp = dalloc<double>(O, size_t(max_chunk) * P.KRp);
+  P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.KRp);
 }
 
 void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device) {
@@ -419,6 +504,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.d_flat_wfar = dupload(O, fw, s);
     H.n_flat_wfar = int(fw.size());
     if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
+    if (const char* m = std::getenv("QBXG_SHIFT_MODE")) H.shift_mode = std::atoi(m);
     // (centre, W_far box) pairs, centre-major, chunked to bound the staging buffer
     {
       const int64_t cap_pairs = int64_t(1) << 24;
@@ -510,7 +596,12 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   QCK(cudaEventRecord(ev[1], s));
   chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
-  for (int l = H.nlev - 2; l >= 0; --l) chk(dev::launch_m2m(D, H.d_m2m_level[l], H.n_m2m_level[l], s));
+  for (int l = H.nlev - 2; l >= 0; --l) {
+    if (H.shift_mode == 0)
+      chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
+    else
+      chk(dev::launch_m2m(D, H.d_m2m_level[l], H.n_m2m_level[l], s));
+  }
   QCK(cudaEventRecord(ev[3], s));
   chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
@@ -532,7 +623,12 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   QCK(cudaEventRecord(ev[6], s));
   chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(ev[7], s));
-  for (int l = 1; l < H.nlev; ++l) chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
+  for (int l = 1; l < H.nlev; ++l) {
+    if (H.shift_mode == 0)
+      chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
+    else
+      chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
+  }
   QCK(cudaEventRecord(ev[8], s));
   if (H.ctr_mode == 0)
     chk(dev::launch_ctr_flat(D, H.d_flat_all, int(H.nc), H.d_ctr_box, false, s));

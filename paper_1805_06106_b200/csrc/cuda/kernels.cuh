@@ -72,6 +72,22 @@ struct M2LPlan {
   std::vector<M2LChunk> chunks;
 };
 int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
+
+// Tree shifts (Stage 2 M2M, Stage 7 L2L) as DMMA GEMMs over 8 octant operators:
+// one level = tiles of same-octant columns, staged rows, segmented reduce.
+struct ShiftLevel {
+  int n_tiles = 0;
+  int4* tiles = nullptr;
+  int* col_src = nullptr;       // box whose expansion is shifted
+  int* col_pos = nullptr;       // staging row
+  double* col_scale = nullptr;  // 1
+  int n_out = 0;
+  int* out_boxes = nullptr;     // receiving boxes
+  int2* out_seg = nullptr;      // staging rows [first, last) of each receiver
+};
+int launch_shift_ops(int mode, int p, int KR, int KRp, const int4* rdof, double* ops, cudaStream_t s);
+int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops, double2* X, int kp, bool accumulate,
+                       cudaStream_t s);
 int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
 
 // Box expansion -> centre locals as DMMA GEMMs (centre_gemm.cu); items are

@@ -92,6 +92,77 @@ __global__ void __launch_bounds__(256) k_m2l_ops(int p, int KR, int KRp, const i
   }
 }
 
+// Octant operators for the tree shifts in the same real-DOF form:
+//   mode 1, M2M (child -> parent), u = (c_child - c_parent)/|child| in {+-1}^3:
+//     M~_par(n,m) = 2^-n sum_{j<=n,k} M~_ch(j,k) conj(R_{n-j}^{m-k}(u))
+//   mode 2, L2L (parent -> child), u = (c_child - c_parent)/|parent| in {+-1/2}^3:
+//     L~_ch(n,m) = 2^-n sum_{j>=n,k} L~_par(j,k) R_{j-n}^{k-m}(u)
+// Written as L = A X + B conj(X) per (output, input) pair, like k_m2l_ops.
+__global__ void __launch_bounds__(256) k_shift_ops(int mode, int p, int KR, int KRp, const int4* __restrict__ rdof,
+                                                   double* __restrict__ ops) {
+  extern __shared__ double2 sR[];  // hsize(p)
+  const int o = blockIdx.x;        // octant
+  const double a = mode == 1 ? 1.0 : 0.5;
+  const double ux = (o & 1) ? a : -a, uy = (o & 2) ? a : -a, uz = (o & 4) ? a : -a;
+  if (threadIdx.x <= p) {
+    double2 col[kMaxOrder + 1];
+    regular_column(ux, uy, uz, threadIdx.x, p, col);
+    for (int n = threadIdx.x; n <= p; ++n) sR[hidx(n, threadIdx.x)] = col[n - threadIdx.x];
+  }
+  __syncthreads();
+  double* T = ops + size_t(o) * KRp * KRp;
+  for (int idx = threadIdx.x; idx < KRp * KRp; idx += blockDim.x) {
+    const int ro = idx / KRp, ri = idx % KRp;
+    double v = 0.0;
+    if (ro < KR && ri < KR) {
+      const int4 ao = rdof[ro], bi = rdof[ri];
+      const int n = ao.x, m = ao.y, po = ao.z, j = bi.x, k = bi.y, pi = bi.z;
+      const double s = ldexp(1.0, -n);
+      double2 A = make_double2(0, 0), B = make_double2(0, 0);
+      auto R = [&](int nn, int mm) {
+        if (nn < 0 || nn > p || mm > nn || mm < -nn) return make_double2(0.0, 0.0);
+        return hget(sR, nn, mm);
+      };
+      if (mode == 1) {
+        A = R(n - j, m - k);
+        A.y = -A.y;
+        if (k > 0) {
+          B = R(n - j, m + k);
+          B.y = -B.y;
+          if (k & 1) B = make_double2(-B.x, -B.y);
+        }
+      } else {
+        A = R(j - n, k - m);
+        if (k > 0) {
+          B = R(j - n, -k - m);
+          if (k & 1) B = make_double2(-B.x, -B.y);
+        }
+      }
+      if (po == 0)
+        v = (pi == 0) ? (A.x + B.x) : -(A.y - B.y);
+      else
+        v = (pi == 0) ? (A.y + B.y) : (A.x - B.x);
+      v *= s;
+    }
+    T[idx] = v;
+  }
+}
+
+// out[b] (+)= sum of staged rows seg[i] = [first, last) for box boxes[i].
+__global__ void __launch_bounds__(256) k_seg_reduce(const int* __restrict__ boxes, const int2* __restrict__ seg,
+                                                    int KR, int KRp, const int* __restrict__ rmap,
+                                                    const double* __restrict__ temp, double* __restrict__ out,
+                                                    int kp2, int accumulate) {
+  const int b = boxes[blockIdx.x];
+  const int2 sg = seg[blockIdx.x];
+  for (int r = threadIdx.x; r < KR; r += blockDim.x) {
+    double s = 0.0;
+    for (int pos = sg.x; pos < sg.y; ++pos) s += temp[size_t(pos) * KRp + r];
+    double* dst = out + size_t(b) * kp2 + rmap[r];
+    *dst = accumulate ? *dst + s : s;
+  }
+}
+
 // One CTA: one offset, up to kBN pairs; 8 warps x (8*MT rows); full K.
 template <int MT>
 __global__ void __launch_bounds__(256) k_m2l_gemm(const double* __restrict__ ops, const int4* __restrict__ tiles,
@@ -212,19 +283,52 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
 }
 
 template <int MT>
-void gemm_mt(const M2LPlan& P, int chunk, const double* M, int kp2, cudaStream_t s) {
-  const M2LChunk& C = P.chunks[chunk];
+void gemm_mt(const double* ops, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s) {
   const size_t smem = (2 * 64 * MT * kAPad + 2 * kKC * kBPad) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2l_gemm<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_m2l_gemm<MT><<<C.n_tiles, 256, smem, s>>>(P.ops, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap, M, kp2,
-                                              P.temp);
+  k_m2l_gemm<MT><<<n_tiles, 256, smem, s>>>(ops, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp);
+}
+
+int gemm_any(int KRp, const double* ops, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s) {
+  switch (KRp / 64) {
+    case 1: gemm_mt<1>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 2: gemm_mt<2>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 3: gemm_mt<3>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 4: gemm_mt<4>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 5: gemm_mt<5>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 6: gemm_mt<6>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 7: gemm_mt<7>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 8: gemm_mt<8>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    default: return -1;
+  }
+  return 1;
 }
 
 }  // namespace
+
+int launch_shift_ops(int mode, int p, int KR, int KRp, const int4* rdof, double* ops, cudaStream_t s) {
+  cudaFuncSetAttribute(k_shift_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_shift_ops<<<8, 256, hsize(p) * sizeof(double2), s>>>(mode, p, KR, KRp, rdof, ops);
+  return 1;
+}
+
+// One tree level of M2M (src = M, out = M, overwrite) or L2L (src = L, out = L, accumulate).
+int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops, double2* X, int kp, bool accumulate,
+                       cudaStream_t s) {
+  if (S.n_tiles == 0) return 0;
+  double* Xd = reinterpret_cast<double*>(X);
+  if (gemm_any(P.KRp, ops, S.n_tiles, S.tiles, S.col_src, S.col_pos, S.col_scale, P.rmap, Xd, 2 * kp, P.temp, s) < 0)
+    return -1;
+  k_seg_reduce<<<S.n_out, 256, 0, s>>>(S.out_boxes, S.out_seg, P.KR, P.KRp, P.rmap, P.temp, Xd, 2 * kp,
+                                        accumulate ? 1 : 0);
+  return 2;
+}
 
 int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s) {
   const size_t smem = hsize(2 * p) * sizeof(double2);
@@ -239,17 +343,9 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
   for (int c = 0; c < int(P.chunks.size()); ++c) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
-    switch (P.KRp / 64) {
-      case 1: gemm_mt<1>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 2: gemm_mt<2>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 3: gemm_mt<3>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 4: gemm_mt<4>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 5: gemm_mt<5>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 6: gemm_mt<6>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 7: gemm_mt<7>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      case 8: gemm_mt<8>(P, c, reinterpret_cast<const double*>(D.M), kp2, s); break;
-      default: return -1;
-    }
+    if (gemm_any(P.KRp, P.ops, C.n_tiles, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap,
+                 reinterpret_cast<const double*>(D.M), kp2, P.temp, s) < 0)
+      return -1;
     k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp,
                                             reinterpret_cast<double*>(D.L), kp2);
     k += 2;
