@@ -208,6 +208,18 @@ typedef struct {
   int64_t n_qbxl2p_targets;
 } qbxg_ledger;
 
+/* ---- multi-GPU sharding ---------------------------------
+ * Rank r owns the contiguous DFS-preorder (Morton) box range [cuts[r], cuts[r+1]),
+ * cut by a per-box cost model.  Per-box role bits for one rank: */
+enum {
+  QBXG_SHARD_OWN = 1,        /* box in the rank's range: its centres/targets are evaluated here */
+  QBXG_SHARD_SUBTREE = 2,    /* whole subtree in the range: upward pass done here              */
+  QBXG_SHARD_STRADDLE = 4,   /* subtree spans ranks: M2M recomputed by every rank after exchange */
+  QBXG_SHARD_DOWN = 8        /* in the range or an ancestor of it: M2L / P2L / L2L done here     */
+};
+/* cuts: n_ranks+1 ints; mask: n_boxes bytes (may be NULL). */
+int qbxg_plan_shard(const qbxg_plan* plan, int32_t n_ranks, int32_t rank, int32_t* cuts, uint8_t* mask);
+
 int qbxg_plan_create(const qbxg_config* cfg, const qbxg_geometry* geom, qbxg_plan** out);
 int qbxg_plan_view_get(const qbxg_plan* plan, qbxg_plan_view* out);
 int qbxg_plan_ledger(const qbxg_plan* plan, qbxg_ledger* out);
@@ -240,6 +252,27 @@ int qbxg_apply_device(qbxg_handle* h, const double* d_weights, const double* d_d
                       void* cuda_stream, qbxg_timings* timings);
 
 int qbxg_destroy(qbxg_handle* h);
+
+/* Sharded handle for rank `rank` of `n_ranks` (one process per GPU).  Work
+ * lists are restricted to the rank's boxes (qbxg_plan_shard); qbxg_apply /
+ * qbxg_apply_device then need an NCCL communicator (qbxg_nccl_attach) and
+ * return complete results on every rank.  Without NCCL, drive the phases and
+ * the multipole exchange yourself: */
+int qbxg_create_sharded(const qbxg_config* cfg, const qbxg_geometry* geom, const qbxg_plan* plan,
+                        int32_t device, int32_t n_ranks, int32_t rank, qbxg_handle** out);
+/* phase 1: gather density, P2M, M2M of owned subtrees.
+ * phase 2: M2M of straddling boxes, Stages 3-9 for owned boxes; potentials and
+ *          centre coefficients of other ranks' targets are written as 0. */
+int qbxg_apply_phase(qbxg_handle* h, int32_t phase, const double* d_weights, const double* d_dipoles,
+                     double* d_out_target_pot, double* d_out_center_coeffs, void* cuda_stream);
+/* Device multipole buffer (n_boxes rows of row_doubles, DFS order) and cuts
+ * (n_ranks+1): after phase 1, rows [cuts[r], cuts[r+1]) of rank r are final. */
+int qbxg_multipole_buffer(qbxg_handle* h, double** d_multipoles, int64_t* row_doubles, int32_t* cuts);
+/* Exchange between handles of one process (device copies), e.g. ranks emulated on one GPU. */
+int qbxg_exchange_local(qbxg_handle** handles, int32_t n_ranks);
+/* NCCL (libnccl.so.2 loaded at run time): rank 0 creates the id, all ranks attach. */
+int qbxg_nccl_unique_id(uint8_t* out128);
+int qbxg_nccl_attach(qbxg_handle* h, const uint8_t* id128);
 
 /* ---- near-field P2P, the GPU counterpart of qbx::direct_sum ------------ */
 /* pot[i] = (1/4pi) sum_j [w_j/|x_i-y_j| + m_j.(x_i-y_j)/|x_i-y_j|^3].

@@ -200,3 +200,29 @@ def ref_direct_sum(pos, w, mu, tpos):
     _chk(L.qbxref_direct_sum(pos.shape[0], _p(pos), _p(w), _p(mu), tpos.shape[0], _p(tpos),
                              out.ctypes.data_as(_dp)), L)
     return out
+
+
+def execute_phase(plan, geom, weights, dipoles, mask, phase, Mbuf, want_centers=False):
+    """Sharded oracle step (SURVEY.md §8e harness): mask from api.plan_shard,
+    phase 1 fills Mbuf (n_boxes x (p+1)^2 complex as float64 pairs), phase 2
+    consumes it.  Returns (pot, centre coefficients or None) for phase 2."""
+    L = lib()
+    if not hasattr(L, "_phase_declared"):
+        L.qbxo_execute_phase.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _i32p, _dp, _dp, _dp, _dp,
+                                         C.POINTER(C.c_uint8), C.c_int, _dp]
+        L._phase_declared = True
+    cfg = plan.cfg
+    pot = np.zeros(geom.n_targets)
+    coeffs = np.zeros(geom.n_centers * 2 * cfg.kq) if want_centers else None
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    mu = None if dipoles is None else np.ascontiguousarray(dipoles, dtype=np.float64)
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    _chk(L.qbxo_execute_phase(C.addressof(plan.view), cfg.p_fmm, cfg.p_qbx, _p(geom.source_pos), _p(geom.center_pos),
+                              _p(geom.center_radius), _p(geom.target_pos), geom.association.ctypes.data_as(_i32p),
+                              _p(w), _p(mu), pot.ctypes.data_as(_dp),
+                              None if coeffs is None else coeffs.ctypes.data_as(_dp),
+                              m.ctypes.data_as(C.POINTER(C.c_uint8)), phase, Mbuf.ctypes.data_as(_dp)), _o)
+    if coeffs is not None:
+        c = coeffs.reshape(geom.n_centers, cfg.kq, 2)
+        return pot, c[..., 0] + 1j * c[..., 1]
+    return pot, None

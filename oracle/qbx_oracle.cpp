@@ -445,11 +445,37 @@ int qbxo_eval_internal(int kind, const double* coeffs, int p, const double* cent
 // include 1/(4 pi).  out_center_coeffs (optional): n_centers x K_q complex in
 // the paper normalisation, m >= 0, index n(n+1)/2+m.
 // stage_seconds (optional, 8 entries): stage 2, 3+5a+6a, 4, 5b, 6b, 7, 8, 9.
+// Sharded variant (test harness for the multi-rank protocol):
+// mask = per-box role bits from qbxg_plan_shard (NULL: everything), phase 1 =
+// upward pass of owned leaves/subtrees into Mbuf (nb x (p+1)^2 complex, other
+// rows zero), phase 2 = straddling M2M from Mbuf then Stages 3-9 of the owned
+// boxes (other targets/centres written as 0), phase 3 = both.
+int execute_impl(const qbxg_plan_view* V, int p, int q, const double* src_pos, const double* center_pos,
+                 const double* center_radius, const double* target_pos, const int32_t* association,
+                 const double* weights, const double* dipoles, double* out_pot, double* out_center_coeffs,
+                 double* stage_seconds, const uint8_t* mask, int phase, double* Mbuf);
+
 int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double* src_pos,
                  const double* center_pos, const double* center_radius, const double* target_pos,
                  const int32_t* association, const double* weights, const double* dipoles, double* out_pot,
                  double* out_center_coeffs, double* stage_seconds) {
   (void)tf;
+  return execute_impl(V, p, q, src_pos, center_pos, center_radius, target_pos, association, weights, dipoles,
+                      out_pot, out_center_coeffs, stage_seconds, nullptr, 3, nullptr);
+}
+
+int qbxo_execute_phase(const qbxg_plan_view* V, int p, int q, const double* src_pos, const double* center_pos,
+                       const double* center_radius, const double* target_pos, const int32_t* association,
+                       const double* weights, const double* dipoles, double* out_pot, double* out_center_coeffs,
+                       const uint8_t* mask, int phase, double* Mbuf) {
+  return execute_impl(V, p, q, src_pos, center_pos, center_radius, target_pos, association, weights, dipoles,
+                      out_pot, out_center_coeffs, nullptr, mask, phase, Mbuf);
+}
+
+int execute_impl(const qbxg_plan_view* V, int p, int q, const double* src_pos, const double* center_pos,
+                 const double* center_radius, const double* target_pos, const int32_t* association,
+                 const double* weights, const double* dipoles, double* out_pot, double* out_center_coeffs,
+                 double* stage_seconds, const uint8_t* mask, int phase, double* Mbuf) {
   return guard([&] {
     const int nb = V->n_boxes;
     const int KP = nfull(p), KQ = nfull(q);
@@ -457,30 +483,48 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     auto now = [] {
       return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
+    auto has = [&](int b, uint8_t bit) { return mask ? (mask[b] & bit) != 0 : true; };
+    auto straddle = [&](int b) { return mask ? (mask[b] & QBXG_SHARD_STRADDLE) != 0 : false; };
     double t[9];
     t[0] = now();
     // box-sorted views: source s_sorted -> original index src_perm[s_sorted]
     std::vector<std::vector<cd>> M(nb, std::vector<cd>(KP, cd(0)));
     auto src_of = [&](int64_t sorted) { return int64_t(V->src_perm[sorted]); };
-
-    // Stage 2: form multipoles (leaves), then M2M in postorder (children have larger ids).
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int b = 0; b < nb; ++b) {
-      if (V->child_starts[b + 1] != V->child_starts[b]) continue;
-      for (int i = 0; i < V->src_own_count[b]; ++i)
-        p2m(S, src_of(V->src_own_start[b] + i), &V->box_center[3 * b], V->box_radius[b], p, M[b]);
-    }
-    for (int l = V->n_levels - 2; l >= 0; --l) {
+    auto m2m_level = [&](int l, bool want_straddle) {
 #pragma omp parallel for schedule(dynamic, 16)
       for (int i = V->level_starts[l]; i < V->level_starts[l + 1]; ++i) {
         const int b = V->level_boxes[i];
+        if (want_straddle ? !straddle(b) : !has(b, QBXG_SHARD_SUBTREE)) continue;
         for (int k = V->child_starts[b]; k < V->child_starts[b + 1]; ++k) {
           const int c = V->children[k];
           if (V->src_sub_count[c] == 0) continue;
           m2m(M[c], p, &V->box_center[3 * c], V->box_radius[c], &V->box_center[3 * b], V->box_radius[b], M[b]);
         }
       }
+    };
+
+    if (phase & 1) {
+      // Stage 2: form multipoles (leaves), then M2M in postorder (children have larger ids).
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int b = 0; b < nb; ++b) {
+        if (V->child_starts[b + 1] != V->child_starts[b] || !has(b, QBXG_SHARD_OWN)) continue;
+        for (int i = 0; i < V->src_own_count[b]; ++i)
+          p2m(S, src_of(V->src_own_start[b] + i), &V->box_center[3 * b], V->box_radius[b], p, M[b]);
+      }
+      for (int l = V->n_levels - 2; l >= 0; --l) m2m_level(l, false);
+      if (Mbuf)
+        for (int b = 0; b < nb; ++b)
+          for (int i = 0; i < KP; ++i) {
+            Mbuf[2 * (size_t(b) * KP + i)] = M[b][i].real();
+            Mbuf[2 * (size_t(b) * KP + i) + 1] = M[b][i].imag();
+          }
     }
+    if (!(phase & 2)) return;
+    if (!(phase & 1) && Mbuf)
+      for (int b = 0; b < nb; ++b)
+        for (int i = 0; i < KP; ++i) M[b][i] = cd(Mbuf[2 * (size_t(b) * KP + i)], Mbuf[2 * (size_t(b) * KP + i) + 1]);
+    if (mask)
+      for (int l = V->n_levels - 2; l >= 0; --l) m2m_level(l, true);
     t[1] = now();
 
     const int64_t nc = V->n_centers;
@@ -492,7 +536,7 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     const int near_lists[3] = {QBXG_LIST_U, QBXG_LIST_W_CLOSE, QBXG_LIST_X_CLOSE};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int b = 0; b < nb; ++b) {
-      if (!(V->box_flags[b] & QBXG_BOX_TARGET)) continue;
+      if (!(V->box_flags[b] & QBXG_BOX_TARGET) || !has(b, QBXG_SHARD_OWN)) continue;
       for (int li : near_lists) {
         for (int64_t e = V->list_starts[li][b]; e < V->list_starts[li][b + 1]; ++e) {
           const int d = V->list_boxes[li][e];
@@ -517,7 +561,8 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     std::vector<std::vector<cd>> Lb(nb, std::vector<cd>(KP, cd(0)));
 #pragma omp parallel for schedule(dynamic, 16)
     for (int b = 0; b < nb; ++b)
-      for (int64_t e = V->list_starts[QBXG_LIST_V][b]; e < V->list_starts[QBXG_LIST_V][b + 1]; ++e) {
+      for (int64_t e = V->list_starts[QBXG_LIST_V][b]; has(b, QBXG_SHARD_DOWN) && e < V->list_starts[QBXG_LIST_V][b + 1];
+           ++e) {
         const int d = V->list_boxes[QBXG_LIST_V][e];
         m2l(M[d], p, &V->box_center[3 * d], V->box_radius[d], &V->box_center[3 * b], V->box_radius[b], p, Lb[b]);
       }
@@ -526,7 +571,7 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     // Stage 5b: List 3 far: M2P at conventional targets, M2QBXL at centres
 #pragma omp parallel for schedule(dynamic, 4)
     for (int b = 0; b < nb; ++b) {
-      if (!(V->box_flags[b] & QBXG_BOX_TARGET)) continue;
+      if (!(V->box_flags[b] & QBXG_BOX_TARGET) || !has(b, QBXG_SHARD_OWN)) continue;
       for (int64_t e = V->list_starts[QBXG_LIST_W_FAR][b]; e < V->list_starts[QBXG_LIST_W_FAR][b + 1]; ++e) {
         const int d = V->list_boxes[QBXG_LIST_W_FAR][e];
         for (int j = 0; j < V->ctr_own_count[b]; ++j) {
@@ -546,7 +591,8 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     // Stage 6b: List 4 far: P2L into the box local
 #pragma omp parallel for schedule(dynamic, 16)
     for (int b = 0; b < nb; ++b)
-      for (int64_t e = V->list_starts[QBXG_LIST_X_FAR][b]; e < V->list_starts[QBXG_LIST_X_FAR][b + 1]; ++e) {
+      for (int64_t e = V->list_starts[QBXG_LIST_X_FAR][b];
+           has(b, QBXG_SHARD_DOWN) && e < V->list_starts[QBXG_LIST_X_FAR][b + 1]; ++e) {
         const int d = V->list_boxes[QBXG_LIST_X_FAR][e];
         for (int i = 0; i < V->src_own_count[d]; ++i)
           p2l(S, src_of(V->src_own_start[d] + i), &V->box_center[3 * b], V->box_radius[b], p, Lb[b]);
@@ -558,7 +604,7 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
 #pragma omp parallel for schedule(dynamic, 16)
       for (int i = V->level_starts[l]; i < V->level_starts[l + 1]; ++i) {
         const int b = V->level_boxes[i];
-        if (!(V->box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR))) continue;
+        if (!(V->box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) || !has(b, QBXG_SHARD_DOWN)) continue;
         const int a = V->box_parent[b];
         l2l(Lb[a], p, &V->box_center[3 * a], V->box_radius[a], &V->box_center[3 * b], V->box_radius[b], p, Lb[b]);
       }
@@ -568,7 +614,7 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     // Stage 8: L2QBXL at every centre from its owning box's local
 #pragma omp parallel for schedule(dynamic, 16)
     for (int b = 0; b < nb; ++b)
-      for (int j = 0; j < V->ctr_own_count[b]; ++j) {
+      for (int j = 0; has(b, QBXG_SHARD_OWN) && j < V->ctr_own_count[b]; ++j) {
         const int64_t cs = V->ctr_own_start[b] + j;
         const int64_t c = V->ctr_perm[cs];
         l2l(Lb[b], p, &V->box_center[3 * b], V->box_radius[b], &center_pos[3 * c], center_radius[c], q, Lc[cs]);
@@ -578,18 +624,28 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
     // Stage 9: evaluate
     std::vector<int64_t> ctr_sorted_pos(nc);
     for (int64_t cs = 0; cs < nc; ++cs) ctr_sorted_pos[V->ctr_perm[cs]] = cs;
+    std::vector<uint8_t> ctr_owned(nc, 1);
+    if (mask)
+      for (int b = 0; b < nb; ++b)
+        for (int j = 0; j < V->ctr_own_count[b]; ++j) ctr_owned[V->ctr_own_start[b] + j] = has(b, QBXG_SHARD_OWN);
     const int64_t nt = V->n_targets;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < nt; ++i) {
       const int32_t a = association[i];
       if (a >= 0) {
         const int64_t cs = ctr_sorted_pos[a];
-        out_pot[i] = kInv4Pi * eval_local(Lc[cs], q, &center_pos[3 * int64_t(a)], center_radius[a], &target_pos[3 * i]);
+        out_pot[i] = ctr_owned[cs] ? kInv4Pi * eval_local(Lc[cs], q, &center_pos[3 * int64_t(a)], center_radius[a],
+                                                          &target_pos[3 * i])
+                                   : 0.0;
       }
     }
 #pragma omp parallel for schedule(dynamic, 16)
     for (int b = 0; b < nb; ++b)
       for (int j = 0; j < V->tgt_own_count[b]; ++j) {
+        if (!has(b, QBXG_SHARD_OWN)) {
+          out_pot[V->tgt_perm[V->tgt_own_start[b] + j]] = 0.0;
+          continue;
+        }
         const int64_t ts = V->tgt_own_start[b] + j;
         const int64_t ti = V->tgt_perm[ts];
         const double lf = eval_local(Lb[b], p, &V->box_center[3 * b], V->box_radius[b], &target_pos[3 * ti]);
@@ -603,7 +659,7 @@ int qbxo_execute(const qbxg_plan_view* V, int p, int q, double tf, const double*
         const double r = center_radius[c];
         for (int n = 0; n <= q; ++n)
           for (int m = 0; m <= n; ++m) {
-            const cd v = Lc[cs][idx(n, m)] / std::pow(r, n) * paper_factor(n, m);
+            const cd v = ctr_owned[cs] ? Lc[cs][idx(n, m)] / std::pow(r, n) * paper_factor(n, m) : cd(0);
             out_center_coeffs[2 * (c * kq + n * (n + 1) / 2 + m)] = v.real();
             out_center_coeffs[2 * (c * kq + n * (n + 1) / 2 + m) + 1] = v.imag();
           }

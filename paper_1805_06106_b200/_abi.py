@@ -94,8 +94,11 @@ EXPORTED_SYMBOLS = (
     "qbxg_plan_create", "qbxg_plan_view_get", "qbxg_plan_ledger", "qbxg_plan_destroy",
     "qbxg_create", "qbxg_apply", "qbxg_apply_device", "qbxg_destroy", "qbxg_direct_sum",
     "qbxg_last_error", "qbxg_device_count", "qbxg_version", "qbxg_measure_fp64_peak",
-    "qbxg_measure_dmma_peak",
+    "qbxg_measure_dmma_peak", "qbxg_plan_shard", "qbxg_create_sharded", "qbxg_apply_phase",
+    "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
 )
+
+SHARD_OWN, SHARD_SUBTREE, SHARD_STRADDLE, SHARD_DOWN = 1, 2, 4, 8
 
 
 def _declare(lib):
@@ -119,6 +122,14 @@ def _declare(lib):
         "qbxg_version": ([], C.c_char_p),
         "qbxg_measure_fp64_peak": ([C.c_int32, P(C.c_double)], C.c_int),
         "qbxg_measure_dmma_peak": ([C.c_int32, P(C.c_double)], C.c_int),
+        "qbxg_plan_shard": ([C.c_void_p, C.c_int32, C.c_int32, _i32p, _u8p], C.c_int),
+        "qbxg_create_sharded": ([P(Config), P(Geometry), C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                 P(C.c_void_p)], C.c_int),
+        "qbxg_apply_phase": ([C.c_void_p, C.c_int32] + [C.c_void_p] * 5, C.c_int),
+        "qbxg_multipole_buffer": ([C.c_void_p, P(C.c_void_p), _i64p, _i32p], C.c_int),
+        "qbxg_exchange_local": ([P(C.c_void_p), C.c_int32], C.c_int),
+        "qbxg_nccl_unique_id": ([C.c_char_p], C.c_int),
+        "qbxg_nccl_attach": ([C.c_void_p, C.c_char_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         if not hasattr(lib, name):

@@ -282,16 +282,48 @@ def build_plan(cfg: FmmConfig, geom: Geometry) -> Plan:
 class FmmEngine:
     """One GPU's QBX-FMM apply (qbxg_create / qbxg_apply)."""
 
-    def __init__(self, cfg: FmmConfig, geom: Geometry, plan: Plan | None = None, device: int = 0):
+    def __init__(self, cfg: FmmConfig, geom: Geometry, plan: Plan | None = None, device: int = 0,
+                 shard: tuple[int, int] | None = None):
+        """shard=(n_ranks, rank): this process's part of a Morton-range sharded apply."""
         self.cfg = cfg
         self.geom = geom
         self.plan = plan if plan is not None else Plan(cfg, geom)
         self._c_cfg = cfg.to_c()
         self._c_geom = geom.to_c()
         self.handle = C.c_void_p()
-        _check(_abi.lib().qbxg_create(C.byref(self._c_cfg), C.byref(self._c_geom), self.plan.handle, device,
-                                      C.byref(self.handle)))
+        self.shard = shard
+        if shard is None:
+            _check(_abi.lib().qbxg_create(C.byref(self._c_cfg), C.byref(self._c_geom), self.plan.handle, device,
+                                          C.byref(self.handle)))
+        else:
+            _check(_abi.lib().qbxg_create_sharded(C.byref(self._c_cfg), C.byref(self._c_geom), self.plan.handle,
+                                                  device, shard[0], shard[1], C.byref(self.handle)))
         self.timings = _abi.Timings()
+
+    # ---- sharded driving (multi-GPU, SURVEY.md §8e)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_abi.lib().qbxg_nccl_unique_id(buf))
+        return buf.raw
+
+    def attach_nccl(self, uid: bytes):
+        _check(_abi.lib().qbxg_nccl_attach(self.handle, C.c_char_p(uid)))
+
+    def apply_phase(self, phase: int, d_weights: int | None, d_dipoles: int | None, d_pot: int | None,
+                    d_coeffs: int | None = None, stream: int | None = None):
+        _check(_abi.lib().qbxg_apply_phase(self.handle, phase, C.c_void_p(d_weights or 0),
+                                           C.c_void_p(d_dipoles or 0), C.c_void_p(d_pot or 0),
+                                           C.c_void_p(d_coeffs or 0), C.c_void_p(stream or 0)))
+
+    def multipole_buffer(self):
+        ptr = C.c_void_p()
+        row = C.c_int64()
+        n = self.shard[0] if self.shard else 1
+        cuts = (C.c_int32 * (n + 1))()
+        _check(_abi.lib().qbxg_multipole_buffer(self.handle, C.byref(ptr), C.byref(row), cuts))
+        return ptr.value, row.value, list(cuts)
+
 
     def close(self):
         if getattr(self, "handle", None):
@@ -323,6 +355,22 @@ class FmmEngine:
         t = self.timings
         return dict(zip(_abi.TIMER_NAMES, t.ms[:])), int(t.kernel_launches), int(t.h2d_bytes), int(t.d2h_bytes)
 
+
+
+
+def exchange_local(engines):
+    """Multipole exchange between sharded engines living in one process (device copies)."""
+    arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
+    _check(_abi.lib().qbxg_exchange_local(arr, len(engines)))
+
+
+def plan_shard(plan: "Plan", n_ranks: int, rank: int):
+    """Rank's box range cuts (n_ranks+1) and per-box role bits (_abi.SHARD_*)."""
+    cuts = np.zeros(n_ranks + 1, dtype=np.int32)
+    mask = np.zeros(plan.view.n_boxes, dtype=np.uint8)
+    _check(_abi.lib().qbxg_plan_shard(plan.handle, n_ranks, rank, cuts.ctypes.data_as(_i32p),
+                                      mask.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return cuts, mask
 
 def execute(geom: Geometry, weights, dipoles, cfg: FmmConfig, want_centers=False, device=0):
     """SPEC.md:424 execute(bundle, density, FmmConfig) -> (potentials, ledger)."""

@@ -12,6 +12,8 @@
 //   L_c      nc x K_q complex (half table), radius-scaled
 // Lists are CSR; near-field lists are flattened into source segments.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -110,6 +112,18 @@ struct Handle {
   double* ops_m2m = nullptr;     // 8 octant operators (real DOF)
   double* ops_l2l = nullptr;
   std::vector<dev::ShiftLevel> m2m_levels, l2l_levels;
+  std::vector<dev::ShiftLevel> m2m_straddle;  // per level, recomputed after the exchange
+  // sharding: rank's role bits per box and the global cuts
+  int nranks = 1, rank = 0;
+  std::vector<uint8_t> mask;
+  std::vector<int32_t> cuts;
+  int* d_eval_assoc = nullptr;   // owned associated targets (original index)
+  int n_eval_assoc = 0;
+  int* d_eval_conv = nullptr;    // owned conventional targets (sorted index)
+  int n_eval_conv = 0;
+  int* d_own_ctr = nullptr;      // owned centres (sorted index)
+  int n_own_ctr = 0;
+  void* nccl_comm = nullptr;     // ncclComm_t when attached
   int shift_mode = 0;            // 0 DMMA GEMM, 1 per-box kernels
   // staging for host applies
   double* d_w = nullptr;
@@ -121,6 +135,13 @@ struct Handle {
 
   ~Handle() {
     if (stream) cudaStreamSynchronize(stream);
+    if (nccl_comm) {
+      void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (lib) {
+        auto destroy = reinterpret_cast<ncclResult_t (*)(ncclComm_t)>(dlsym(lib, "ncclCommDestroy"));
+        if (destroy) destroy(static_cast<ncclComm_t>(nccl_comm));
+      }
+    }
     for (void* p : owned) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -133,7 +154,8 @@ namespace {
 // Group List-2 entries by relative offset for the dense per-offset M2L GEMM
 // (m2l_gemm.cu): operator tables, chunks bounded by the staging buffer, tiles
 // of <= 64 same-offset columns.
-void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
+void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& vstarts,
+               const std::vector<int2>& vent, cudaStream_t s) {
   auto& O = H.owned;
   dev::M2LPlan& P = H.m2l;
   const int p = H.cfg.p_fmm;
@@ -154,26 +176,22 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
   P.rmap = dupload(O, rmap, s);
   int4* d_rdof = dupload(O, rdof, s);
   const int nb = V.n_boxes;
-  const int64_t* vs = V.list_starts[QBXG_LIST_V];
-  const int32_t* vb = V.list_boxes[QBXG_LIST_V];
+  // the rank's (filtered) List-2 CSR: entries (source box, offset slot)
+  const int64_t* vs = vstarts.data();
   const int64_t nent = vs[nb];
-  // offset slot of every entry, used-slot compaction
-  std::vector<int> slot(nent);
+  std::vector<int> vb(nent), slot(nent);
   std::vector<int> slot_to_op(1331, -1), used;
-  for (int b = 0; b < nb; ++b)
-    for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
-      const int d = vb[e];
-      int dd[3];
-      for (int k = 0; k < 3; ++k)
-        dd[k] = int(std::lround((V.box_center[3 * b + k] - V.box_center[3 * d + k]) / (2.0 * V.box_radius[b])));
-      const int sl = ((dd[0] + 5) * 11 + (dd[1] + 5)) * 11 + (dd[2] + 5);
-      slot[e] = sl;
-      if (slot_to_op[sl] < 0) {
-        slot_to_op[sl] = int(used.size());
-        used.push_back(sl);
-      }
+  for (int64_t e = 0; e < nent; ++e) {
+    vb[e] = vent[e].x;
+    const int sl = vent[e].y;
+    slot[e] = sl;
+    if (slot_to_op[sl] < 0) {
+      slot_to_op[sl] = int(used.size());
+      used.push_back(sl);
     }
+  }
   P.n_ops = int(used.size());
+  const auto& mk = H.mask;
 
   // --- tree shifts: octant operators and per-level tiles
   int64_t max_level_rows = 1;
@@ -218,24 +236,33 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
       return L;
     };
     H.m2m_levels.assign(H.nlev, dev::ShiftLevel());
+    H.m2m_straddle.assign(H.nlev, dev::ShiftLevel());
     H.l2l_levels.assign(H.nlev, dev::ShiftLevel());
     for (int l = 0; l < H.nlev; ++l) {
       std::vector<int3> cols;
       std::vector<int> outb;
       std::vector<int2> seg;
-      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
-        const int b = V.level_boxes[i];
-        if ((V.box_flags[b] & QBXG_BOX_LEAF) || !(V.box_flags[b] & QBXG_BOX_HAS_SOURCES)) continue;
-        const int first = int(cols.size());
-        for (int k = V.child_starts[b]; k < V.child_starts[b + 1]; ++k) {
-          const int c = V.children[k];
-          if (V.src_sub_count[c] == 0) continue;
-          cols.push_back(make_int3(octant(c, b), c, int(cols.size())));
+      // upward: boxes whose subtree is the rank's (pass 0) or spans ranks (pass 1, after the exchange)
+      for (int pass = 0; pass < 2; ++pass) {
+        const uint8_t want = pass == 0 ? QBXG_SHARD_SUBTREE : QBXG_SHARD_STRADDLE;
+        cols.clear();
+        outb.clear();
+        seg.clear();
+        for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
+          const int b = V.level_boxes[i];
+          if ((V.box_flags[b] & QBXG_BOX_LEAF) || !(V.box_flags[b] & QBXG_BOX_HAS_SOURCES)) continue;
+          if (!(mk[b] & want)) continue;
+          const int first = int(cols.size());
+          for (int k = V.child_starts[b]; k < V.child_starts[b + 1]; ++k) {
+            const int c = V.children[k];
+            if (V.src_sub_count[c] == 0) continue;
+            cols.push_back(make_int3(octant(c, b), c, int(cols.size())));
+          }
+          outb.push_back(b);
+          seg.push_back(make_int2(first, int(cols.size())));
         }
-        outb.push_back(b);
-        seg.push_back(make_int2(first, int(cols.size())));
+        (pass == 0 ? H.m2m_levels : H.m2m_straddle)[l] = make_level(cols, outb, seg);
       }
-      H.m2m_levels[l] = make_level(cols, outb, seg);
       cols.clear();
       outb.clear();
       seg.clear();
@@ -243,6 +270,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
       for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
         const int b = V.level_boxes[i];
         if (!(V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR))) continue;
+        if (!(mk[b] & QBXG_SHARD_DOWN)) continue;
         const int par = V.box_parent[b];
         const int pos = int(cols.size());
         cols.push_back(make_int3(octant(b, par), par, pos));
@@ -314,8 +342,20 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, cudaStream_t s) {
   P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.KRp);
 }
 
-void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device) {
+void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device,
+            int nranks = 1, int rank = 0) {
   check_device();
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("qbxg_create: bad rank / n_ranks");
+  {
+    qbxg_plan_view V0;
+    if (qbxg_plan_view_get(plan, &V0) != QBXG_OK) throw InvalidArgument(get_last_error());
+    H.nranks = nranks;
+    H.rank = rank;
+    H.cuts.assign(nranks + 1, 0);
+    H.mask.assign(V0.n_boxes, 0);
+    if (qbxg_plan_shard(plan, nranks, rank, H.cuts.data(), H.mask.data()) != QBXG_OK)
+      throw InvalidArgument(get_last_error());
+  }
   if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL)
     throw InvalidArgument("qbxg_create: only Laplace kernels are implemented");
   if (cfg.p_fmm > 21) throw InvalidArgument("qbxg_create: p_fmm > 21 not supported on the GPU path");
@@ -408,14 +448,17 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     a = V.list_starts[k][b];
     e = V.list_starts[k][b + 1];
   };
+  std::vector<int64_t> vs(nb + 1, 0);
+  std::vector<int2> vent;
   {
-    std::vector<int64_t> ns_(nb + 1, 0), xs(nb + 1, 0), vs(nb + 1, 0), ws(nb + 1, 0);
-    std::vector<int2> nseg, xseg, vent;
+    std::vector<int64_t> ns_(nb + 1, 0), xs(nb + 1, 0), ws(nb + 1, 0);
+    std::vector<int2> nseg, xseg;
     std::vector<int> wbox;
+    const auto& mk = H.mask;
     const int near_lists[3] = {QBXG_LIST_U, QBXG_LIST_W_CLOSE, QBXG_LIST_X_CLOSE};
     for (int b = 0; b < nb; ++b) {
       int64_t a, e;
-      if (V.box_flags[b] & QBXG_BOX_TARGET) {
+      if ((V.box_flags[b] & QBXG_BOX_TARGET) && (mk[b] & QBXG_SHARD_OWN)) {
         for (int li : near_lists) {
           lrow(li, b, a, e);
           for (int64_t i = a; i < e; ++i) {
@@ -426,12 +469,14 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       }
       ns_[b + 1] = int64_t(nseg.size());
       lrow(QBXG_LIST_X_FAR, b, a, e);
+      if (!(mk[b] & QBXG_SHARD_DOWN)) e = a;
       for (int64_t i = a; i < e; ++i) {
         const int d = V.list_boxes[QBXG_LIST_X_FAR][i];
         if (V.src_own_count[d] > 0) xseg.push_back(make_int2(V.src_own_start[d], V.src_own_count[d]));
       }
       xs[b + 1] = int64_t(xseg.size());
       lrow(QBXG_LIST_V, b, a, e);
+      if (!(mk[b] & QBXG_SHARD_DOWN)) e = a;
       for (int64_t i = a; i < e; ++i) {
         const int d = V.list_boxes[QBXG_LIST_V][i];
         int dd[3];
@@ -443,6 +488,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       }
       vs[b + 1] = int64_t(vent.size());
       lrow(QBXG_LIST_W_FAR, b, a, e);
+      if (!(mk[b] & QBXG_SHARD_OWN)) e = a;
       for (int64_t i = a; i < e; ++i) wbox.push_back(V.list_boxes[QBXG_LIST_W_FAR][i]);
       ws[b + 1] = int64_t(wbox.size());
     }
@@ -463,9 +509,10 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_l2l_level.assign(H.nlev, 0);
     for (int b = 0; b < nb; ++b) {
       const bool leaf = V.box_flags[b] & QBXG_BOX_LEAF;
-      if (leaf && V.src_own_count[b] > 0) leaves.push_back(b);
-      if (V.ctr_own_count[b] > 0) cb.push_back(b);
-      if (V.tgt_own_count[b] > 0 && ns_[b + 1] > ns_[b]) tb.push_back(b);
+      const bool own = mk[b] & QBXG_SHARD_OWN;
+      if (leaf && V.src_own_count[b] > 0 && own) leaves.push_back(b);
+      if (V.ctr_own_count[b] > 0 && own) cb.push_back(b);
+      if (V.tgt_own_count[b] > 0 && ns_[b + 1] > ns_[b] && own) tb.push_back(b);
       if (vs[b + 1] > vs[b]) vb.push_back(b);
       if (ws[b + 1] > ws[b] && V.ctr_own_count[b] > 0) wb.push_back(b);
       if (ws[b + 1] > ws[b] && V.tgt_own_count[b] > 0) wtb.push_back(b);
@@ -493,10 +540,25 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_items_wfar = int(iw.size());
     H.d_items_ctr = dupload(O, ic, s);
     H.n_items_ctr = int(ic.size());
-    std::vector<int> cbox(H.nc), all(H.nc), fw;
+    std::vector<int> cbox(H.nc), all, fw, eval_assoc, eval_conv;
     for (int b = 0; b < nb; ++b)
       for (int j = 0; j < V.ctr_own_count[b]; ++j) cbox[V.ctr_own_start[b] + j] = b;
-    for (int64_t i = 0; i < H.nc; ++i) all[i] = int(i);
+    for (int b : cb)
+      for (int j = 0; j < V.ctr_own_count[b]; ++j) all.push_back(V.ctr_own_start[b] + j);
+    {
+      std::vector<int> cs_of(H.nc);
+      for (int64_t i = 0; i < H.nc; ++i) cs_of[V.ctr_perm[i]] = int(i);
+      for (int64_t t = 0; t < H.nt; ++t)
+        if (g.association[t] >= 0 && (mk[cbox[cs_of[g.association[t]]]] & QBXG_SHARD_OWN)) eval_assoc.push_back(int(t));
+      for (int b = 0; b < nb; ++b)
+        if (mk[b] & QBXG_SHARD_OWN)
+          for (int j = 0; j < V.tgt_own_count[b]; ++j) eval_conv.push_back(V.tgt_own_start[b] + j);
+    }
+    H.d_eval_assoc = dupload(O, eval_assoc, s);
+    H.n_eval_assoc = int(eval_assoc.size());
+    H.d_eval_conv = dupload(O, eval_conv, s);
+    H.n_eval_conv = int(eval_conv.size());
+    H.n_own_ctr = int(all.size());
     for (int b : wb)
       for (int j = 0; j < V.ctr_own_count[b]; ++j) fw.push_back(V.ctr_own_start[b] + j);
     H.d_ctr_box = dupload(O, cbox, s);
@@ -547,8 +609,11 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       std::vector<int> m2m, l2l;
       for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
         const int b = V.level_boxes[i];
-        if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES)) m2m.push_back(b);
-        if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR))) l2l.push_back(b);
+        if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES) &&
+            (mk[b] & QBXG_SHARD_SUBTREE))
+          m2m.push_back(b);
+        if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) && (mk[b] & QBXG_SHARD_DOWN))
+          l2l.push_back(b);
       }
       H.d_m2m_level[l] = dupload(O, m2m, s);
       H.n_m2m_level[l] = int(m2m.size());
@@ -572,22 +637,80 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   H.d_pot = dalloc<double>(O, H.nt);
   H.d_coeffs = dalloc<double>(O, size_t(H.nc) * 2 * D.kq);
 
-  build_m2l(H, V, s);
+  build_m2l(H, V, vs, vent, s);
   QCK(cudaGetLastError());
   QCK(cudaStreamSynchronize(s));
 }
 
+// ---- NCCL, loaded at run time (libnccl.so.2: torch's or the system's) ----
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    n.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (n.lib) {
+      n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(n.lib, "ncclGetUniqueId"));
+      n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(n.lib, "ncclCommInitRank"));
+      n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(n.lib, "ncclCommDestroy"));
+      n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(dlsym(n.lib, "ncclBroadcast"));
+      n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(n.lib, "ncclAllReduce"));
+      n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(n.lib, "ncclGroupStart"));
+      n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(n.lib, "ncclGroupEnd"));
+      n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(n.lib, "ncclGetErrorString"));
+    }
+  }
+  if (!n.lib || !n.GetUniqueId || !n.CommInitRank || !n.Broadcast || !n.AllReduce || !n.GroupStart || !n.GroupEnd)
+    throw NcclError("libnccl.so.2 not loadable");
+  return n;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NcclError(std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+// Multipole exchange after the owned upward pass: rank r broadcasts the rows
+// of its box range [cuts[r], cuts[r+1]) of M (in place) to every rank.
+void exchange_nccl(Handle& H, cudaStream_t s) {
+  Nccl& n = nccl();
+  auto comm = static_cast<ncclComm_t>(H.nccl_comm);
+  const size_t row = size_t(2) * H.D.kp;
+  nck(n.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < H.nranks; ++r) {
+    const size_t a = size_t(H.cuts[r]), b = size_t(H.cuts[r + 1]);
+    if (b <= a) continue;
+    double* p = reinterpret_cast<double*>(H.D.M) + a * row;
+    nck(n.Broadcast(p, p, (b - a) * row, ncclFloat64, r, comm, s), "ncclBroadcast");
+  }
+  nck(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// phase bit 1: density gather, P2M, M2M of the rank's subtrees.
+// phase bit 2: M2M of straddling boxes, then Stages 3-9 for the rank's boxes.
 void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s,
-                int timer_base_event) {
-  (void)timer_base_event;
+                int phase) {
   dev::DevData& D = H.D;
-  if (D.dipole && !d_mu) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
-  int L = 0;
+  if (D.dipole && !d_mu && (phase & 1)) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
+  int L = (phase & 1) ? 0 : H.last_launches;
   auto chk = [&](int k) {
     if (k < 0) throw InvalidArgument("qbxg_apply: unsupported order");
     L += k;
   };
   auto& ev = H.ev;
+  if (phase & 1) {
   QCK(cudaEventRecord(ev[0], s));
   chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
   QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
@@ -597,11 +720,19 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
   for (int l = H.nlev - 2; l >= 0; --l) {
-    if (H.shift_mode == 0)
+    if (H.shift_mode == 0 || H.nranks > 1)
       chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
     else
       chk(dev::launch_m2m(D, H.d_m2m_level[l], H.n_m2m_level[l], s));
   }
+  H.last_launches = L;
+  }
+  if (!(phase & 2)) return;
+  // boxes whose subtree spans ranks: recomputed identically by every rank once
+  // the owned multipoles have been exchanged (no-op for a single rank)
+  if (H.nranks > 1)
+    for (int l = H.nlev - 2; l >= 0; --l)
+      chk(dev::launch_shift_level(H.m2l, H.m2m_straddle[l], H.ops_m2m, D.M, D.kp, false, s));
   QCK(cudaEventRecord(ev[3], s));
   chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
@@ -631,18 +762,40 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   }
   QCK(cudaEventRecord(ev[8], s));
   if (H.ctr_mode == 0)
-    chk(dev::launch_ctr_flat(D, H.d_flat_all, int(H.nc), H.d_ctr_box, false, s));
+    chk(dev::launch_ctr_flat(D, H.d_flat_all, H.n_own_ctr, H.d_ctr_box, false, s));
   else if (H.ctr_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
     chk(dev::launch_ctr_gemm(D, H.d_items_ctr, H.n_items_ctr, false, s));
   else
     chk(dev::launch_l2qbxl2(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   QCK(cudaEventRecord(ev[9], s));
-  chk(dev::launch_eval(D, int(H.nt), H.d_tpos, H.d_assoc, H.d_ctr_sorted, int(H.nconv), H.d_tgt_perm, H.d_tgt_box,
-                       d_pot, s));
-  if (d_coeffs) chk(dev::launch_centre_out(D, int(H.nc), H.d_ctr_perm, d_coeffs, s));
+  if (H.nranks > 1) {  // targets / centres of other ranks stay zero (summed across ranks)
+    QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * sizeof(double), s));
+    if (d_coeffs) QCK(cudaMemsetAsync(d_coeffs, 0, size_t(std::max<int64_t>(H.nc, 1)) * 2 * D.kq * sizeof(double), s));
+  }
+  chk(dev::launch_eval(D, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_eval_conv,
+                       H.d_eval_conv, H.d_tgt_perm, H.d_tgt_box, d_pot, s));
+  if (d_coeffs) chk(dev::launch_centre_out(D, H.n_own_ctr, H.d_flat_all, H.d_ctr_perm, d_coeffs, s));
   QCK(cudaEventRecord(ev[10], s));
   QCK(cudaGetLastError());
   H.last_launches = L;
+}
+
+// One whole apply: owned upward pass, multipole exchange (NCCL) when sharded,
+// straddling M2M, downward + QBX stages, and the sum of the ranks' outputs.
+void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s) {
+  if (H.nranks > 1 && !H.nccl_comm)
+    throw InvalidArgument("sharded handle: attach NCCL (qbxg_nccl_attach) or drive qbxg_apply_phase");
+  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 1);
+  if (H.nranks > 1) exchange_nccl(H, s);
+  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 2);
+  if (H.nranks > 1) {
+    auto comm = static_cast<ncclComm_t>(H.nccl_comm);
+    Nccl& n = nccl();
+    nck(n.AllReduce(d_pot, d_pot, size_t(H.nt), ncclFloat64, ncclSum, comm, s), "ncclAllReduce(potentials)");
+    if (d_coeffs)
+      nck(n.AllReduce(d_coeffs, d_coeffs, size_t(H.nc) * 2 * H.D.kq, ncclFloat64, ncclSum, comm, s),
+          "ncclAllReduce(centre coefficients)");
+  }
 }
 
 void fill_timings(Handle& H, qbxg_timings* t, bool host_copies, int64_t h2d, int64_t d2h) {
@@ -736,8 +889,88 @@ int qbxg_apply_device(qbxg_handle* hp, const double* d_weights, const double* d_
     auto& H = hp->h;
     QCK(cudaSetDevice(H.device));
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
-    qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, 0);
+    qbxg::full_apply(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s);
     qbxg::fill_timings(H, timings, false, 0, 0);
+  });
+}
+
+int qbxg_create_sharded(const qbxg_config* cfg, const qbxg_geometry* geom, const qbxg_plan* plan, int32_t device,
+                        int32_t n_ranks, int32_t rank, qbxg_handle** out) {
+  return qbxg::guarded([&] {
+    if (!cfg || !geom || !plan || !out) throw qbxg::InvalidArgument("qbxg_create_sharded: null argument");
+    auto* h = new qbxg_handle;
+    try {
+      qbxg::create(h->h, *cfg, *geom, plan, device, n_ranks, rank);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int qbxg_apply_phase(qbxg_handle* hp, int32_t phase, const double* d_weights, const double* d_dipoles,
+                     double* d_out_target_pot, double* d_out_center_coeffs, void* cuda_stream) {
+  return qbxg::guarded([&] {
+    if (!hp || phase < 1 || phase > 2) throw qbxg::InvalidArgument("qbxg_apply_phase: bad argument");
+    if (phase == 1 && !d_weights) throw qbxg::InvalidArgument("qbxg_apply_phase: null weights");
+    if (phase == 2 && !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_phase: null output");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
+    qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, phase);
+    QCK(cudaStreamSynchronize(s));
+  });
+}
+
+int qbxg_multipole_buffer(qbxg_handle* hp, double** d_multipoles, int64_t* row_doubles, int32_t* cuts) {
+  return qbxg::guarded([&] {
+    if (!hp || !d_multipoles || !row_doubles) throw qbxg::InvalidArgument("qbxg_multipole_buffer: null argument");
+    auto& H = hp->h;
+    *d_multipoles = reinterpret_cast<double*>(H.D.M);
+    *row_doubles = int64_t(2) * H.D.kp;
+    if (cuts) std::copy(H.cuts.begin(), H.cuts.end(), cuts);
+  });
+}
+
+int qbxg_exchange_local(qbxg_handle** hs, int32_t n) {
+  return qbxg::guarded([&] {
+    if (!hs || n < 1) throw qbxg::InvalidArgument("qbxg_exchange_local: bad argument");
+    for (int r = 0; r < n; ++r) {
+      auto& src = hs[r]->h;
+      if (src.nranks != n || src.rank != r) throw qbxg::InvalidArgument("qbxg_exchange_local: handles not rank-ordered");
+      const size_t row = size_t(2) * src.D.kp * sizeof(double);
+      const size_t a = size_t(src.cuts[r]), b = size_t(src.cuts[r + 1]);
+      for (int q = 0; q < n; ++q) {
+        if (q == r || b <= a) continue;
+        auto& dst = hs[q]->h;
+        QCK(cudaMemcpy(reinterpret_cast<char*>(dst.D.M) + a * row, reinterpret_cast<char*>(src.D.M) + a * row,
+                       (b - a) * row, cudaMemcpyDefault));
+      }
+    }
+  });
+}
+
+int qbxg_nccl_unique_id(uint8_t* out128) {
+  return qbxg::guarded([&] {
+    if (!out128) throw qbxg::InvalidArgument("qbxg_nccl_unique_id: null argument");
+    ncclUniqueId id;
+    qbxg::nck(qbxg::nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+  });
+}
+
+int qbxg_nccl_attach(qbxg_handle* hp, const uint8_t* id128) {
+  return qbxg::guarded([&] {
+    if (!hp || !id128) throw qbxg::InvalidArgument("qbxg_nccl_attach: null argument");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    ncclComm_t comm;
+    qbxg::nck(qbxg::nccl().CommInitRank(&comm, H.nranks, id, H.rank), "ncclCommInitRank");
+    H.nccl_comm = comm;
   });
 }
 
@@ -757,7 +990,7 @@ int qbxg_apply(qbxg_handle* hp, const double* weights, const double* dipoles, do
       QCK(cudaMemcpyAsync(H.d_mu_in, dipoles, 3 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
       h2d += 24 * H.ns;
     }
-    qbxg::run_device(H, H.d_w, dip ? H.d_mu_in : nullptr, H.d_pot, out_center_coeffs ? H.d_coeffs : nullptr, s, 0);
+    qbxg::full_apply(H, H.d_w, dip ? H.d_mu_in : nullptr, H.d_pot, out_center_coeffs ? H.d_coeffs : nullptr, s);
     QCK(cudaMemcpyAsync(out_target_pot, H.d_pot, H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (out_center_coeffs) {
       const size_t nbytes = size_t(H.nc) * 2 * H.D.kq * sizeof(double);

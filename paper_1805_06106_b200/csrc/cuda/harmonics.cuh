@@ -25,8 +25,19 @@ __host__ __device__ constexpr int hidx(int n, int m) { return n * (n + 1) / 2 + 
 __host__ __device__ constexpr int hsize(int p) { return (p + 1) * (p + 2) / 2; }
 
 // 1 / ((n-m)(n+m)) for the regular recurrence, indexed hidx(n, m) (n >= m+2).
-// (one copy per translation unit; uploaded by upload_constants() in kernels.cu)
+// Without -rdc every translation unit owns its copy: each TU that calls a
+// regular_* helper must call upload_inv_nm() (host) before launching.
 __constant__ double c_inv_nm[hsize(kMaxOrder)];
+
+static inline void upload_inv_nm() {
+  static bool done = false;  // per translation unit
+  if (done) return;
+  double h[hsize(kMaxOrder)];
+  for (int n = 0; n <= kMaxOrder; ++n)
+    for (int m = 0; m <= n; ++m) h[hidx(n, m)] = (n >= m + 2) ? 1.0 / double((n - m) * (n + m)) : 0.0;
+  cudaMemcpyToSymbol(c_inv_nm, h, sizeof(h));
+  done = true;
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));

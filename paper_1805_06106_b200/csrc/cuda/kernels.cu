@@ -16,15 +16,7 @@
 namespace qbxg {
 namespace dev {
 
-void upload_constants() {
-  static bool done = false;
-  if (done) return;
-  double h[hsize(kMaxOrder)];
-  for (int n = 0; n <= kMaxOrder; ++n)
-    for (int m = 0; m <= n; ++m) h[hidx(n, m)] = (n >= m + 2) ? 1.0 / double((n - m) * (n + m)) : 0.0;
-  cudaMemcpyToSymbol(c_inv_nm, h, sizeof(h));
-  done = true;
-}
+void upload_constants() { upload_inv_nm(); }
 
 namespace {
 
@@ -690,10 +682,12 @@ __global__ void __launch_bounds__(256) k_l2qbxl(DevData D, const int* __restrict
 
 // ---------------------------------------------------------------- Stage 9
 // QBXL2P: pot_t = (1/4pi) sum L~_c R((t - c)/r);  L2P: pot_t = (1/4pi)(phi_t + sum L~_b R((t - c_b)/h))
-__global__ void k_eval_assoc(DevData D, int nt, const double* __restrict__ tpos, const int* __restrict__ assoc,
-                             const int* __restrict__ ctr_sorted, double* __restrict__ pot) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
+__global__ void k_eval_assoc(DevData D, int n, const int* __restrict__ items, const double* __restrict__ tpos,
+                             const int* __restrict__ assoc, const int* __restrict__ ctr_sorted,
+                             double* __restrict__ pot) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = items[t];
   const int a = assoc[i];
   if (a < 0) return;
   const int cs = ctr_sorted[a];
@@ -704,10 +698,11 @@ __global__ void k_eval_assoc(DevData D, int nt, const double* __restrict__ tpos,
   pot[i] = kInv4Pi * v;
 }
 
-__global__ void k_eval_conv(DevData D, int nconv, const int* __restrict__ tgt_perm, const int* __restrict__ tgt_box,
-                            double* __restrict__ pot) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nconv) return;
+__global__ void k_eval_conv(DevData D, int n, const int* __restrict__ items, const int* __restrict__ tgt_perm,
+                            const int* __restrict__ tgt_box, double* __restrict__ pot) {
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n) return;
+  const int i = items[it];
   const int b = tgt_box[i];
   const double4 bc = D.box[b];
   const double ih = 1.0 / bc.w;
@@ -719,10 +714,11 @@ __global__ void k_eval_conv(DevData D, int nconv, const int* __restrict__ tgt_pe
 
 // Centre coefficients in the paper's normalisation (Eq. (5)):
 //   L^paper_n^m = (L~_n^m / r^n) / (4 pi N_nm (n+m)!),  N_nm = sqrt((2n+1)/(4 pi) (n-m)!/(n+m)!)
-__global__ void k_centre_out(DevData D, int nc, const int* __restrict__ ctr_perm, double* __restrict__ out) {
+__global__ void k_centre_out(DevData D, int nc, const int* __restrict__ items, const int* __restrict__ ctr_perm,
+                             double* __restrict__ out) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= int64_t(nc) * D.kq) return;
-  const int cs = int(t / D.kq), c = int(t % D.kq);
+  const int cs = items[int(t / D.kq)], c = int(t % D.kq);
   int n, m;
   idx_nm(c, n, m);
   const double r = D.ctr[cs].w;
@@ -888,24 +884,25 @@ int launch_l2qbxl(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-int launch_eval(const DevData& D, int nt, const double* tpos, const int* assoc, const int* ctr_sorted, int nconv,
-                const int* tgt_perm, const int* tgt_box, double* pot, cudaStream_t s) {
+int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
+                const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
+                double* pot, cudaStream_t s) {
   int k = 0;
-  if (nt > 0) {
-    k_eval_assoc<<<(nt + 127) / 128, 128, 0, s>>>(D, nt, tpos, assoc, ctr_sorted, pot);
+  if (n_assoc > 0) {
+    k_eval_assoc<<<(n_assoc + 127) / 128, 128, 0, s>>>(D, n_assoc, assoc_items, tpos, assoc, ctr_sorted, pot);
     ++k;
   }
-  if (nconv > 0) {
-    k_eval_conv<<<(nconv + 127) / 128, 128, 0, s>>>(D, nconv, tgt_perm, tgt_box, pot);
+  if (n_conv > 0) {
+    k_eval_conv<<<(n_conv + 127) / 128, 128, 0, s>>>(D, n_conv, conv_items, tgt_perm, tgt_box, pot);
     ++k;
   }
   return k;
 }
 
-int launch_centre_out(const DevData& D, int nc, const int* ctr_perm, double* out, cudaStream_t s) {
+int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr_perm, double* out, cudaStream_t s) {
   const int64_t n = int64_t(nc) * D.kq;
   if (n == 0) return 0;
-  k_centre_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(D, nc, ctr_perm, out);
+  k_centre_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(D, nc, items, ctr_perm, out);
   return 1;
 }
 

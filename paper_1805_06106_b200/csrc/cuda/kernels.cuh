@@ -127,9 +127,10 @@ int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_l2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_l2qbxl(const DevData& D, const int* boxes, int n, cudaStream_t s);
-int launch_eval(const DevData& D, int nt, const double* tpos, const int* assoc, const int* ctr_sorted,
-                int nconv, const int* tgt_perm, const int* tgt_box, double* pot, cudaStream_t s);
-int launch_centre_out(const DevData& D, int nc, const int* ctr_perm, double* out, cudaStream_t s);
+int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
+                const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
+                double* pot, cudaStream_t s);
+int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr_perm, double* out, cudaStream_t s);
 int launch_tables(const DevData& D, double2* m2l_tab, double2* oct_m2m, double2* oct_l2l, cudaStream_t s);
 int launch_direct_sum(int ns, const double4* src, const double4* mu, int nt, const double4* tgt, double* pot,
                       unsigned long long* bad, cudaStream_t s);

@@ -313,6 +313,7 @@ int gemm_any(int KRp, const double* ops, int n_tiles, const int4* tiles, const i
 }  // namespace
 
 int launch_shift_ops(int mode, int p, int KR, int KRp, const int4* rdof, double* ops, cudaStream_t s) {
+  upload_inv_nm();  // k_shift_ops uses regular_column (this TU's constant table)
   cudaFuncSetAttribute(k_shift_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_shift_ops<<<8, 256, hsize(p) * sizeof(double2), s>>>(mode, p, KR, KRp, rdof, ops);
   return 1;

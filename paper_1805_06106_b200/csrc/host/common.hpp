@@ -19,6 +19,7 @@ namespace qbxg {
 struct InvalidArgument : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DomainError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NcclError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 void set_last_error(const std::string& msg);
 const char* get_last_error();
@@ -44,6 +45,9 @@ int guarded(F&& f) {
   } catch (const CudaError& e) {
     set_last_error(e.what());
     return QBXG_ERR_CUDA;
+  } catch (const NcclError& e) {
+    set_last_error(e.what());
+    return QBXG_ERR_NCCL;
   } catch (const std::exception& e) {
     set_last_error(e.what());
     return QBXG_ERR_INTERNAL;

@@ -573,11 +573,77 @@ void compute_ledger(const Plan& P, qbxg_ledger& L) {
   L.n_qbxl2p_targets = P.ntgt - P.nconv;
 }
 
+// Contiguous DFS-preorder ranges balanced by a per-box cost estimate (fp64
+// flops of the work attached to the box: near field, List 2, List 3 far,
+// List 4 far, L2QBXL, upward/downward shifts; SURVEY.md §8d unit costs at
+// p=15, q=5 scaled with the configured orders).
+void compute_shard(const Plan& P, int nranks, int rank, std::vector<int32_t>& cuts, std::vector<uint8_t>& mask) {
+  const int32_t nb = P.nb;
+  const double p = P.cfg.p_fmm, q = P.cfg.p_qbx;
+  const double kp = (p + 1) * (p + 2) / 2, kq = (q + 1) * (q + 2) / 2;
+  const double c_near = 26 * kq + 40, c_dense = 2 * std::pow(p + 1, 4), c_wfar = 8 * kp * kq, c_p2 = 26 * kp + 40;
+  std::vector<double> cost(nb, 0.0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int32_t b = 0; b < nb; ++b) {
+    const double nc = P.ctr_own_count[b], nt = P.tgt_own_count[b];
+    double c = c_dense;  // one shift up and one down
+    for (int k : {int(QBXG_LIST_U), int(QBXG_LIST_W_CLOSE), int(QBXG_LIST_X_CLOSE)})
+      for (int64_t i = P.lst_starts[k][b]; i < P.lst_starts[k][b + 1]; ++i)
+        c += P.src_own_count[P.lst[k][i]] * (c_near * nc + 30 * nt);
+    c += double(P.lst_starts[QBXG_LIST_V][b + 1] - P.lst_starts[QBXG_LIST_V][b]) * c_dense;
+    c += double(P.lst_starts[QBXG_LIST_W_FAR][b + 1] - P.lst_starts[QBXG_LIST_W_FAR][b]) * (c_wfar * nc + c_p2 * nt);
+    for (int64_t i = P.lst_starts[QBXG_LIST_X_FAR][b]; i < P.lst_starts[QBXG_LIST_X_FAR][b + 1]; ++i)
+      c += P.src_own_count[P.lst[QBXG_LIST_X_FAR][i]] * c_p2;
+    c += nc * c_wfar + P.src_own_count[b] * c_p2;
+    cost[b] = c;
+  }
+  double total = 0;
+  for (double c : cost) total += c;
+  cuts.assign(nranks + 1, nb);
+  cuts[0] = 0;
+  double acc = 0;
+  int k = 1;
+  for (int32_t b = 0; b < nb && k < nranks; ++b) {
+    while (k < nranks && acc >= total * k / nranks) cuts[k++] = b;
+    acc += cost[b];
+  }
+  for (; k < nranks; ++k) cuts[k] = nb;
+  mask.assign(nb, 0);
+  const int32_t lo = cuts[rank], hi = cuts[rank + 1];
+  // straddling: subtree [b, end) not inside one rank range
+  std::vector<int32_t> owner(nb, 0);
+  for (int r = 0; r < nranks; ++r)
+    for (int32_t b = cuts[r]; b < cuts[r + 1]; ++b) owner[b] = r;
+  for (int32_t b = 0; b < nb; ++b) {
+    uint8_t m = 0;
+    const int32_t e = P.subtree_end[b];
+    if (b >= lo && b < hi) m |= QBXG_SHARD_OWN;
+    if (b >= lo && e <= hi) m |= QBXG_SHARD_SUBTREE;
+    if (e > cuts[owner[b] + 1]) m |= QBXG_SHARD_STRADDLE;
+    if (b >= lo && b < hi) m |= QBXG_SHARD_DOWN;
+    mask[b] = m;
+  }
+  if (lo < nb)
+    for (int32_t a = P.parent[lo]; a >= 0; a = P.parent[a]) mask[a] |= QBXG_SHARD_DOWN;
+}
+
 }  // namespace qbxg
 
 struct qbxg_plan {
   qbxg::Plan p;
 };
+
+extern "C" int qbxg_plan_shard(const qbxg_plan* pl, int32_t n_ranks, int32_t rank, int32_t* cuts, uint8_t* mask) {
+  return qbxg::guarded([&] {
+    if (!pl || !cuts) throw qbxg::InvalidArgument("plan_shard: null argument");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw qbxg::InvalidArgument("plan_shard: bad rank");
+    std::vector<int32_t> c;
+    std::vector<uint8_t> m;
+    qbxg::compute_shard(pl->p, n_ranks, rank, c, m);
+    std::copy(c.begin(), c.end(), cuts);
+    if (mask) std::copy(m.begin(), m.end(), mask);
+  });
+}
 
 extern "C" {
 

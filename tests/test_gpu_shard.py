@@ -1,0 +1,77 @@
+"""Sharded (multi-GPU) apply, emulated on one GPU: ranks are separate handles
+driven phase by phase in one process (no kernel ever waits on another rank),
+the multipole exchange is a device copy (qbxg_exchange_local) standing in for
+the NCCL broadcasts.  The sum of the ranks' outputs must equal the unsharded
+apply bitwise (SURVEY.md §8e parity requirement)."""
+import numpy as np
+import pytest
+
+from paper_1805_06106_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def _sharded(cfg, g, plan, nranks, w, mu, want_centres=True):
+    import torch
+    dev = torch.device("cuda", 0)
+    dw = torch.from_numpy(w).to(dev)
+    dm = torch.from_numpy(mu.reshape(-1)).to(dev) if mu is not None else None
+    engines = [api.FmmEngine(cfg, g, plan, shard=(nranks, r)) for r in range(nranks)]
+    pots = [torch.empty(g.n_targets, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    coefs = [torch.empty(g.n_centers * 2 * cfg.kq, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    for e in engines:
+        e.apply_phase(1, dw.data_ptr(), dm.data_ptr() if dm is not None else None, None)
+    api.exchange_local(engines)
+    for e, p, c in zip(engines, pots, coefs):
+        e.apply_phase(2, dw.data_ptr(), dm.data_ptr() if dm is not None else None, p.data_ptr(),
+                      c.data_ptr() if want_centres else None)
+    torch.cuda.synchronize()
+    pot = sum(p for p in pots).cpu().numpy()
+    c = sum(x for x in coefs).cpu().numpy().reshape(g.n_centers, cfg.kq, 2)
+    for e in engines:
+        e.close()
+    return pot, c[..., 0] + 1j * c[..., 1]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("case", ["torus", "urchin_vol"])
+def test_sharded_equals_single_bitwise(nranks, case):
+    if case == "torus":
+        g = api.config_geometry(1, nu=48, nv=24)
+        cfg = api.config_fmm(1)
+        mu = g.dipoles()
+    else:
+        g = api.config_geometry(2, level=2, n_volume_targets=3000)
+        cfg = api.config_fmm(2)
+        mu = None
+    plan = api.Plan(cfg, g)
+    w = g.weights()
+    ref = api.FmmEngine(cfg, g, plan)
+    pot1, c1 = ref.apply(w, mu, want_centers=True)
+    ref.close()
+    pot, c = _sharded(cfg, g, plan, nranks, w, mu)
+    assert np.array_equal(pot, pot1), np.abs(pot - pot1).max()
+    assert np.array_equal(c, c1)
+
+
+def test_shard_roles_partition():
+    g = api.config_geometry(1, nu=48, nv=24)
+    plan = api.Plan(api.config_fmm(1), g)
+    a = plan.arrays()
+    n = 4
+    owners = np.zeros(plan.view.n_boxes, dtype=np.int32)
+    for r in range(n):
+        cuts, mask = api.plan_shard(plan, n, r)
+        own = (mask & 1) > 0
+        assert np.all(np.nonzero(own)[0] == np.arange(cuts[r], cuts[r + 1]))
+        owners[own] += 1
+        # every owned box is also in the downward set; straddle bits agree across ranks
+        assert np.all((mask[own] & 8) > 0)
+        if r == 0:
+            straddle0 = (mask & 4) > 0
+        else:
+            assert np.array_equal((mask & 4) > 0, straddle0)
+    assert np.all(owners == 1)
+    assert straddle0[0]  # the root straddles every cut
+    # cost balance: every rank holds at least some target boxes
+    assert len(np.unique(cuts)) == n + 1
