@@ -21,7 +21,7 @@ namespace dev {
 
 namespace {
 
-constexpr int kCT = 64;  // threads (centres) per CTA
+constexpr int kCT = 32;  // threads (centres) per CTA: one warp per box
 
 __device__ __forceinline__ int fidx(int j, int k) { return j * j + j + k; }
 
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kCT) k_l2qbxl2(DevData D, const int* __restric
     if (ci >= nctr) continue;
     const double4 c = D.ctr[c0 + ci];
     double tx[KQ], ty[KQ];
-    contract_any<Q, false>(A, D.p, (c.x - bc.x) * ih, (c.y - bc.y) * ih, (c.z - bc.z) * ih, col, tx, ty);
+    contract<Q, false>(A, D.p, (c.x - bc.x) * ih, (c.y - bc.y) * ih, (c.z - bc.z) * ih, col, tx, ty);
     double2* out = D.Lc + size_t(c0 + ci) * KQ;
     double f = 1.0;
     const double rh = c.w * ih;

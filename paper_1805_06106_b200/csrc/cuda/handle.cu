@@ -107,7 +107,8 @@ struct Handle {
   int* d_flat_all = nullptr;     // 0..nc-1
   int* d_flat_wfar = nullptr;    // sorted centres of boxes with List 3 far entries
   int n_flat_wfar = 0;
-  int ctr_mode = 0;              // 0 flat, 1 gemm, 2 per-box
+  int ctr_mode = 0;              // W far M2QBXL: 0 pairs, 1 gemm, 2 per-box
+  int l2q_mode = 0;              // L2QBXL: 0 flat, 1 gemm, 2 warp per box
   dev::PairPlan wpairs;          // M2QBXL (centre, W_far box) pairs
   double* ops_m2m = nullptr;     // 8 octant operators (real DOF)
   double* ops_l2l = nullptr;
@@ -191,6 +192,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     }
   }
   P.n_ops = int(used.size());
+  if (const char* e = std::getenv("QBXG_M2L_BN")) P.bn = std::atoi(e) == 32 ? 32 : 64;
   const auto& mk = H.mask;
 
   // --- tree shifts: octant operators and per-level tiles
@@ -325,8 +327,8 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
         }
       std::vector<int4> tiles;
       for (int o = 0; o < P.n_ops; ++o)
-        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += 64)
-          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(64, cnt_op[o + 1] - i)), 0));
+        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += P.bn)
+          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(P.bn, cnt_op[o + 1] - i)), 0));
       C.n_tiles = int(tiles.size());
       C.tiles = dupload(O, tiles, s);
       C.col_src = dupload(O, col_src, s);
@@ -567,6 +569,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_flat_wfar = int(fw.size());
     if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
     if (const char* m = std::getenv("QBXG_SHIFT_MODE")) H.shift_mode = std::atoi(m);
+    if (const char* m = std::getenv("QBXG_L2Q_MODE")) H.l2q_mode = std::atoi(m);
     // (centre, W_far box) pairs, centre-major, chunked to bound the staging buffer
     {
       const int64_t cap_pairs = int64_t(1) << 24;
@@ -761,9 +764,9 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
       chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
   }
   QCK(cudaEventRecord(ev[8], s));
-  if (H.ctr_mode == 0)
+  if (H.l2q_mode == 0)
     chk(dev::launch_ctr_flat(D, H.d_flat_all, H.n_own_ctr, H.d_ctr_box, false, s));
-  else if (H.ctr_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
+  else if (H.l2q_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
     chk(dev::launch_ctr_gemm(D, H.d_items_ctr, H.n_items_ctr, false, s));
   else
     chk(dev::launch_l2qbxl2(D, H.d_ctr_boxes, H.n_ctr_boxes, s));

@@ -225,40 +225,75 @@ __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int*
           for (int j = sl; j < nch; j += S) {
             const double4 x = s_src[j];
             const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
-            double2 I[KI];
-            irregular_regs<Q + (DIP ? 1 : 0)>(ux, uy, uz, I);
+            // J_n^m = r^{2n+1} I_n^m: polynomial recurrences without 1/r^2 per step;
+            // the r^{-(2n+1)} factor is folded into the per-degree source weights.
+            constexpr int P1 = Q + (DIP ? 1 : 0);
+            const double r2 = ux * ux + uy * uy + uz * uz;
+            const double ir2 = 1.0 / r2;
+            double2 J[KI];
+#pragma unroll
+            for (int m = 0; m <= P1; ++m) {
+              if (m == 0) {
+                J[0] = make_double2(1.0, 0.0);
+              } else {
+                const double2 d = J[hidx(m - 1, m - 1)];
+                const double f = double(2 * m - 1);
+                J[hidx(m, m)] = make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
+              }
+              if (m + 1 <= P1) {
+                const double f = double(2 * m + 1) * uz;
+                J[hidx(m + 1, m)] = make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
+              }
+#pragma unroll
+              for (int n = m + 2; n <= P1; ++n) {
+                const double zc = double(2 * n - 1) * uz;
+                const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
+                const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
+                J[hidx(n, m)] = make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
+              }
+            }
+            double sc[P1 + 1];  // r^{-(2n+1)}
+            sc[0] = sqrt(ir2);
+#pragma unroll
+            for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
             const double w = x.w;
 #pragma unroll
-            for (int n = 0; n <= Q; ++n)
+            for (int n = 0; n <= Q; ++n) {
+              const double wn = w * sc[n];
 #pragma unroll
               for (int m = 0; m <= n; ++m) {
                 const int id = hidx(n, m);
-                ax[id] = fma(w, I[id].x, ax[id]);
-                ay[id] = fma(-w, I[id].y, ay[id]);
+                ax[id] = fma(wn, J[id].x, ax[id]);
+                ay[id] = fma(-wn, J[id].y, ay[id]);
               }
+            }
             if (DIP) {
+              // acc += conj(g), g = -mz I_{n+1}^m + (hx + i hy) I_{n+1}^{m-1} - (hx - i hy) I_{n+1}^{m+1}
               const double4 u = s_mu[j];
-              const double hx = 0.5 * u.x * ir, hy = 0.5 * u.y * ir, mz = u.z * ir;
 #pragma unroll
-              for (int n = 0; n <= Q; ++n)
+              for (int n = 0; n <= Q; ++n) {
+                const double s1 = sc[n + 1] * ir;
+                const double mz = u.z * s1, hx = 0.5 * u.x * s1, hy = 0.5 * u.y * s1;
 #pragma unroll
                 for (int m = 0; m <= n; ++m) {
                   const int id = hidx(n, m);
-                  const double2 i0 = I[hidx(n + 1, m)];
-                  const double2 ip = I[hidx(n + 1, m + 1)];
+                  const double2 i0 = J[hidx(n + 1, m)];
+                  const double2 ip = J[hidx(n + 1, m + 1)];
                   double2 im;
                   if (m >= 1) {
-                    im = I[hidx(n + 1, m - 1)];
+                    im = J[hidx(n + 1, m - 1)];
                   } else {
-                    const double2 t = I[hidx(n + 1, 1)];
-                    im = make_double2(-t.x, t.y);  // I_{n+1}^{-1} = -conj(I_{n+1}^1)
+                    const double2 t = J[hidx(n + 1, 1)];
+                    im = make_double2(-t.x, t.y);  // X_{n+1}^{-1} = -conj(X_{n+1}^1)
                   }
-                  // g = -mz i0 + (hx + i hy) im - (hx - i hy) ip ; acc += conj(g)
-                  const double gx = -mz * i0.x + (hx * im.x - hy * im.y) - (hx * ip.x + hy * ip.y);
-                  const double gy = -mz * i0.y + (hx * im.y + hy * im.x) - (hx * ip.y - hy * ip.x);
-                  ax[id] += gx;
-                  ay[id] -= gy;
+                  ax[id] = fma(-mz, i0.x, ax[id]);
+                  ax[id] = fma(hx, im.x - ip.x, ax[id]);
+                  ax[id] = fma(-hy, im.y + ip.y, ax[id]);
+                  ay[id] = fma(mz, i0.y, ay[id]);
+                  ay[id] = fma(-hx, im.y - ip.y, ay[id]);
+                  ay[id] = fma(-hy, im.x + ip.x, ay[id]);
                 }
+              }
             }
           }
         }

@@ -66,6 +66,7 @@ struct M2LChunk {
 struct M2LPlan {
   int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64
   int n_ops = 0;               // used offsets
+  int bn = 32;                 // columns per GEMM tile (64: 1 CTA/SM, 32: 2 CTAs/SM; 32 measured faster)
   double* ops = nullptr;       // n_ops x KRp x KRp
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
   double* temp = nullptr;      // staging: max chunk entries x KRp

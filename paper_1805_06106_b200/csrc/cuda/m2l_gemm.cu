@@ -29,8 +29,7 @@ namespace {
 
 constexpr int kKC = 16;          // K chunk per pipeline stage
 constexpr int kAPad = kKC + 4;   // A smem row stride (doubles): conflict-free fragment reads
-constexpr int kBN = 64;          // columns (pairs) per CTA tile
-constexpr int kBPad = kBN + 4;   // B smem row stride
+// columns (pairs) per CTA tile: BN = 64 (1 CTA/SM) or 32 (2 CTAs/SM); B smem row stride BN + 4
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -163,14 +162,15 @@ __global__ void __launch_bounds__(256) k_seg_reduce(const int* __restrict__ boxe
   }
 }
 
-// One CTA: one offset, up to kBN pairs; 8 warps x (8*MT rows); full K.
-template <int MT>
-__global__ void __launch_bounds__(256) k_m2l_gemm(const double* __restrict__ ops, const int4* __restrict__ tiles,
+// One CTA: one offset, up to BN pairs; 8 warps x (8*MT rows); full K.
+template <int MT, int BN>
+__global__ void __launch_bounds__(256, BN == 32 ? 2 : 1) k_m2l_gemm(const double* __restrict__ ops, const int4* __restrict__ tiles,
                                                   const int* __restrict__ col_src, const int* __restrict__ col_pos,
                                                   const double* __restrict__ col_scale,
                                                   const int* __restrict__ rmap, const double* __restrict__ M,
                                                   int kp2, double* __restrict__ temp) {
   constexpr int KRp = 64 * MT;
+  constexpr int kBN = BN, kBPad = BN + 4, NT = BN / 8;
   extern __shared__ double smem[];
   double* As = smem;                              // 2 x KRp x kAPad
   double* Bs = smem + 2 * KRp * kAPad;            // 2 x kKC x kBPad
@@ -203,11 +203,11 @@ __global__ void __launch_bounds__(256) k_m2l_gemm(const double* __restrict__ ops
     cp_async_commit();
   };
 
-  double acc[MT][8][2];
+  double acc[MT][NT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = KRp / kKC;
   load_stage(0, 0);
@@ -224,21 +224,21 @@ __global__ void __launch_bounds__(256) k_m2l_gemm(const double* __restrict__ ops
     const double* B = Bs + (kc & 1) * kKC * kBPad;
 #pragma unroll
     for (int kk = 0; kk < kKC; kk += 4) {
-      double a[MT], b[8];
+      double a[MT], b[NT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) a[i] = A[(row_w + i * 8 + (lane >> 2)) * kAPad + kk + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = B[(kk + (lane & 3)) * kBPad + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NT; ++j) b[j] = B[(kk + (lane & 3)) * kBPad + j * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     __syncthreads();
   }
   // epilogue: temp[pos][row] = scale * acc
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < NT; ++j) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = j * 8 + (lane & 3) * 2 + h;
@@ -284,27 +284,33 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
 
 template <int MT>
 void gemm_mt(const double* ops, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s) {
-  const size_t smem = (2 * 64 * MT * kAPad + 2 * kKC * kBPad) * sizeof(double);
+             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s,
+             int bn) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_m2l_gemm<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_m2l_gemm<MT, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_m2l_gemm<MT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_m2l_gemm<MT><<<n_tiles, 256, smem, s>>>(ops, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp);
+  const size_t smem = (2 * 64 * MT * kAPad + 2 * kKC * (bn + 4)) * sizeof(double);
+  if (bn == 32)
+    k_m2l_gemm<MT, 32><<<n_tiles, 256, smem, s>>>(ops, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp);
+  else
+    k_m2l_gemm<MT, 64><<<n_tiles, 256, smem, s>>>(ops, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp);
 }
 
 int gemm_any(int KRp, const double* ops, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s) {
+             const double* col_scale, const int* rmap, const double* X, int kp2, double* temp, cudaStream_t s,
+             int bn = 64) {
   switch (KRp / 64) {
-    case 1: gemm_mt<1>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 2: gemm_mt<2>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 3: gemm_mt<3>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 4: gemm_mt<4>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 5: gemm_mt<5>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 6: gemm_mt<6>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 7: gemm_mt<7>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
-    case 8: gemm_mt<8>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s); break;
+    case 1: gemm_mt<1>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 2: gemm_mt<2>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 3: gemm_mt<3>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 4: gemm_mt<4>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 5: gemm_mt<5>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 6: gemm_mt<6>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 7: gemm_mt<7>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
+    case 8: gemm_mt<8>(ops, n_tiles, tiles, col_src, col_pos, col_scale, rmap, X, kp2, temp, s, bn); break;
     default: return -1;
   }
   return 1;
@@ -345,7 +351,7 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
     if (gemm_any(P.KRp, P.ops, C.n_tiles, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap,
-                 reinterpret_cast<const double*>(D.M), kp2, P.temp, s) < 0)
+                 reinterpret_cast<const double*>(D.M), kp2, P.temp, s, P.bn) < 0)
       return -1;
     k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp,
                                             reinterpret_cast<double*>(D.L), kp2);
