@@ -24,6 +24,7 @@
 #include "../host/common.hpp"
 #include "harmonics.cuh"
 #include "kernels.cuh"
+#include "../host/rotation.hpp"
 
 namespace qbxg {
 
@@ -192,7 +193,10 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     }
   }
   P.n_ops = int(used.size());
-  if (const char* e = std::getenv("QBXG_M2L_BN")) P.bn = std::atoi(e) == 32 ? 32 : 64;
+  if (const char* e = std::getenv("QBXG_M2L_BN")) {
+    const int v = std::atoi(e);
+    P.bn = (v == 8 || v == 16 || v == 32) ? v : 64;
+  }
   const auto& mk = H.mask;
 
   // --- tree shifts: octant operators and per-level tiles
@@ -287,9 +291,34 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     return;
   }
   int* d_used = dupload(O, used, s);
-  P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
-  dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
-  QCK(cudaGetLastError());
+  // M2L operator form: rotation + z-translation (default, QBXG_M2L_MODE=rot) or the
+  // dense per-offset real-DOF matrix (QBXG_M2L_MODE=dense); both batched by offset.
+  {
+    const char* mode = std::getenv("QBXG_M2L_MODE");
+    // dense is the default: the rotation kernels are correct (parity-tested) but
+    // latency-bound so far (116 ms vs 84 ms at config 1); opt in with QBXG_M2L_MODE=rot
+    P.rot = (mode && std::string(mode) == "rot") && dev::m2l_rot_smem(p, 16) <= 220 * 1024;
+  }
+  if (P.rot) {
+    if (!std::getenv("QBXG_M2L_BN")) P.bn = 16;
+    P.rot_stride = rot_blocks_size(p);
+    std::vector<double> rf(size_t(P.n_ops) * P.rot_stride), rb(rf.size()), rho(P.n_ops);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int o = 0; o < P.n_ops; ++o) {
+      const int sl = used[o];
+      const double v[3] = {2.0 * (sl / 121 - 5), 2.0 * ((sl / 11) % 11 - 5), 2.0 * (sl % 11 - 5)};
+      m2l_rotation_blocks(p, v, &rf[size_t(o) * P.rot_stride], &rb[size_t(o) * P.rot_stride]);
+      rho[o] = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    }
+    P.rotF = dupload(O, rf, s);
+    P.rotB = dupload(O, rb, s);
+    P.rho_op = dupload(O, rho, s);
+    QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
+  } else {
+    P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
+    dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
+    QCK(cudaGetLastError());
+  }
 
   // chunking by staging-buffer capacity
   size_t free_b = 0, total_b = 0;
@@ -326,9 +355,12 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
           col_scale[i] = 1.0 / V.box_radius[b];
         }
       std::vector<int4> tiles;
-      for (int o = 0; o < P.n_ops; ++o)
-        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += P.bn)
-          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(P.bn, cnt_op[o + 1] - i)), 0));
+      {
+        const int64_t tw = P.rot ? dev::kRotSuper : P.bn;
+        for (int o = 0; o < P.n_ops; ++o)
+          for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
+            tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), 0));
+      }
       C.n_tiles = int(tiles.size());
       C.tiles = dupload(O, tiles, s);
       C.col_src = dupload(O, col_src, s);
@@ -708,9 +740,19 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   dev::DevData& D = H.D;
   if (D.dipole && !d_mu && (phase & 1)) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
   int L = (phase & 1) ? 0 : H.last_launches;
+  static const bool debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
+  int stage_no = 0;
   auto chk = [&](int k) {
     if (k < 0) throw InvalidArgument("qbxg_apply: unsupported order");
     L += k;
+    ++stage_no;
+    if (debug_sync) {  // localise asynchronous faults to the launch that caused them
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error after launch group ") + std::to_string(stage_no) + " (phase " +
+                        std::to_string(phase) + "): " + cudaGetErrorString(e));
+    }
   };
   auto& ev = H.ev;
   if (phase & 1) {

@@ -71,7 +71,18 @@ struct M2LPlan {
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
   double* temp = nullptr;      // staging: max chunk entries x KRp
   std::vector<M2LChunk> chunks;
+  // rotation (point-and-shoot) variant, m2l_rot.cu
+  bool rot = false;
+  double* rotF = nullptr;      // n_ops x rot_stride: multipole rotation blocks (v -> +z)
+  double* rotB = nullptr;      // n_ops x rot_stride: local back-rotation blocks
+  double* rho_op = nullptr;    // n_ops: |v| in box units
+  size_t rot_stride = 0;
 };
+int launch_m2l_rot_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
+// rotation blocks staged once per CTA; tiles of up to kRotSuper same-offset columns
+constexpr int kRotSuper = 256;
+int launch_m2l_rot2_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
+size_t m2l_rot_smem(int p, int bn);
 int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
 
 // Tree shifts (Stage 2 M2M, Stage 7 L2L) as DMMA GEMMs over 8 octant operators:

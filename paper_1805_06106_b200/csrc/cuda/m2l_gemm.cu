@@ -350,9 +350,12 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
   for (int c = 0; c < int(P.chunks.size()); ++c) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
-    if (gemm_any(P.KRp, P.ops, C.n_tiles, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap,
-                 reinterpret_cast<const double*>(D.M), kp2, P.temp, s, P.bn) < 0)
+    if (P.rot) {
+      launch_m2l_rot2_chunk(P, C, D, s);
+    } else if (gemm_any(P.KRp, P.ops, C.n_tiles, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap,
+                        reinterpret_cast<const double*>(D.M), kp2, P.temp, s, P.bn) < 0) {
       return -1;
+    }
     k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp,
                                             reinterpret_cast<double*>(D.L), kp2);
     k += 2;
