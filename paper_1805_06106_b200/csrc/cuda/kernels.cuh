@@ -82,6 +82,10 @@ int launch_m2l_rot_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, 
 // rotation blocks staged once per CTA; tiles of up to kRotSuper same-offset columns
 constexpr int kRotSuper = 256;
 int launch_m2l_rot2_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
+bool m2l_rot3_ok(int p);
+bool m2l_rot4_ok(int p);
+int launch_m2l_rot4_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
+int launch_m2l_rot3_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
 size_t m2l_rot_smem(int p, int bn);
 int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
 

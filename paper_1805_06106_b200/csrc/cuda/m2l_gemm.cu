@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "qbxg.h"
 #include "harmonics.cuh"
@@ -351,7 +352,13 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
     if (P.rot) {
-      launch_m2l_rot2_chunk(P, C, D, s);
+      static const bool v3 = std::getenv("QBXG_M2L_ROTV") && std::getenv("QBXG_M2L_ROTV")[0] == '3';
+      if (!v3 && m2l_rot4_ok(D.p))
+        launch_m2l_rot4_chunk(P, C, D, s);
+      else if (m2l_rot3_ok(D.p))
+        launch_m2l_rot3_chunk(P, C, D, s);
+      else
+        launch_m2l_rot2_chunk(P, C, D, s);
     } else if (gemm_any(P.KRp, P.ops, C.n_tiles, C.tiles, C.col_src, C.col_pos, C.col_scale, P.rmap,
                         reinterpret_cast<const double*>(D.M), kp2, P.temp, s, P.bn) < 0) {
       return -1;
