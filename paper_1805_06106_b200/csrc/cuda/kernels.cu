@@ -8,6 +8,7 @@
 // box locals L~ = L |b|^n, QBX locals L~_c = L_c r_c^n.  The formulas are the
 // same as the CPU oracle's (oracle/qbx_oracle.cpp), restated on half tables.
 #include <cstdio>
+#include <cstdlib>
 
 #include "qbxg.h"
 #include "harmonics.cuh"
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(256) k_wfar(DevData D, const int* __restrict__
 
 // ---------------------------------------------------------------- P2L (Stage 6b)
 // L~_b += (1/h)[w conj(I(u)) + conj(mu . grad I(u))/h], u = (s - c_b)/h, sources of X_far boxes
-constexpr int kP2LBatch = 16;
+constexpr int kP2LBatch = 15;  // 15 sources x 17 columns fill one 256-thread pass at p = 15 (SL+DL)
 
 __global__ void __launch_bounds__(256) k_p2l(DevData D, const int* __restrict__ boxes) {
   extern __shared__ double2 sm[];
@@ -624,6 +625,110 @@ __global__ void __launch_bounds__(256) k_p2l(DevData D, const int* __restrict__ 
     v.x += acc[slot].x * ih;
     v.y += acc[slot].y * ih;
     D.L[size_t(b) * D.kp + c] = v;
+  }
+}
+
+// P2L, warp per target box: lane m owns azimuthal column m of the source's
+// irregular harmonics I_N^m((s - c_b)/h) (N <= P+1) in registers and the
+// output coefficients L~(n, m); the dipole's neighbouring columns m +- 1 come
+// from lanes m +- 1 by shuffles.  No block barriers; sources stream through
+// the read-only cache (every lane reads the same source).
+template <int P, bool DIP>
+__global__ void __launch_bounds__(128) k_p2l_warp(DevData D, const int* __restrict__ boxes, int n) {
+  constexpr int P1 = P + 1;  // dipole needs order P+1
+  const int wid = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  const int b = boxes[wid];
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  const int m = lane;  // column
+  double ax[P + 1], ay[P + 1];
+#pragma unroll
+  for (int k = 0; k <= P; ++k) ax[k] = ay[k] = 0.0;
+  // (2m-1)!! for this lane's diagonal
+  double dfact = 1.0;
+  for (int k = 1; k <= m && k <= P1; ++k) dfact *= (2 * k - 1);
+  for (int64_t e = D.xfar_starts[b]; e < D.xfar_starts[b + 1]; ++e) {
+    const int2 sg = D.xfar_seg[e];
+    for (int si = sg.x; si < sg.x + sg.y; ++si) {
+      const double4 x = D.src[si];
+      const double ux = (x.x - bc.x) * ih, uy = (x.y - bc.y) * ih, uz = (x.z - bc.z) * ih;
+      const double r2 = ux * ux + uy * uy + uz * uz;
+      const double ir2 = 1.0 / r2;
+      // diagonal I_m^m = (2m-1)!! (x+iy)^m / r^(2m+1)
+      double px = 1.0, py = 0.0;
+      for (int k = 0; k < m && k < P1; ++k) {
+        const double t = px * ux - py * uy;
+        py = px * uy + py * ux;
+        px = t;
+      }
+      double sc = sqrt(ir2);
+      for (int k = 0; k < m && k < P1; ++k) sc *= ir2;
+      const double dgx = dfact * px * sc, dgy = dfact * py * sc;
+      // column m: col[N] valid for N >= m (garbage zeros below)
+      double cx[P1 + 1], cy[P1 + 1];
+#pragma unroll
+      for (int N = 0; N <= P1; ++N) {
+        double vx, vy;
+        if (N == 0) {
+          vx = dgx;  // only used when m == 0
+          vy = dgy;
+        } else {
+          const double ax1 = cx[N - 1], ay1 = cy[N - 1];
+          const double ax2 = N >= 2 ? cx[N - 2] : 0.0, ay2 = N >= 2 ? cy[N - 2] : 0.0;
+          const double c1 = (2 * N - 1) * uz * ir2;
+          const double c2 = double((N - 1 + m) * (N - 1 - m)) * ir2;
+          vx = c1 * ax1 - c2 * ax2;
+          vy = c1 * ay1 - c2 * ay2;
+          if (N == m + 1) {  // I_{m+1}^m = (2m+1) z / r^2 I_m^m
+            vx = (2 * m + 1) * uz * ir2 * ax1;
+            vy = (2 * m + 1) * uz * ir2 * ay1;
+          }
+        }
+        const bool diag = (N == m);
+        cx[N] = diag ? dgx : (N < m ? 0.0 : vx);
+        cy[N] = diag ? dgy : (N < m ? 0.0 : vy);
+      }
+      const double w = x.w;
+      double hx = 0, hy = 0, mz = 0;
+      if (DIP) {
+        const double4 u = D.mu[si];
+        hx = 0.5 * u.x * ih;
+        hy = 0.5 * u.y * ih;
+        mz = u.z * ih;
+      }
+#pragma unroll
+      for (int nn = 0; nn <= P; ++nn) {
+        // monopole: L(nn, m) += w conj(I_nn^m)
+        double tx = w * cx[nn], ty = -w * cy[nn];
+        if (DIP) {
+          const double ipx = __shfl_down_sync(0xffffffffu, cx[nn + 1], 1);  // I_{nn+1}^{m+1}
+          const double ipy = __shfl_down_sync(0xffffffffu, cy[nn + 1], 1);
+          double imx = __shfl_up_sync(0xffffffffu, cx[nn + 1], 1);         // I_{nn+1}^{m-1}
+          double imy = __shfl_up_sync(0xffffffffu, cy[nn + 1], 1);
+          if (m == 0) {  // I^{-1} = -conj(I^1), from lane 1
+            imx = -ipx;
+            imy = ipy;
+          }
+          const double i0x = cx[nn + 1], i0y = cy[nn + 1];
+          // acc += conj(g), g = -mz i0 + (hx + i hy) im - (hx - i hy) ip
+          tx += -mz * i0x + hx * (imx - ipx) - hy * (imy + ipy);
+          ty -= -mz * i0y + hx * (imy - ipy) + hy * (imx + ipx);
+        }
+        ax[nn] += tx;
+        ay[nn] += ty;
+      }
+    }
+  }
+  if (m > P) return;
+#pragma unroll
+  for (int nn = 0; nn <= P; ++nn) {
+    if (nn < m) continue;
+    double2* dst = D.L + size_t(b) * D.kp + hidx(nn, m);
+    double2 v = *dst;
+    v.x += ax[nn] * ih;
+    v.y += ay[nn] * ih;
+    *dst = v;
   }
 }
 
@@ -899,8 +1004,23 @@ int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
+template <int P>
+bool p2l_warp_p(const DevData& D, const int* boxes, int n, cudaStream_t s) {
+  if (D.p != P) return false;
+  if (D.dipole)
+    k_p2l_warp<P, true><<<(n + 3) / 4, 128, 0, s>>>(D, boxes, n);
+  else
+    k_p2l_warp<P, false><<<(n + 3) / 4, 128, 0, s>>>(D, boxes, n);
+  return true;
+}
+
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
+  // warp-per-box variant measured slower at config 1 (20 vs 12 ms): opt-in only
+  static const bool warp = std::getenv("QBXG_P2L_WARP") != nullptr;
+  if (warp && (p2l_warp_p<4>(D, boxes, n, s) || p2l_warp_p<8>(D, boxes, n, s) || p2l_warp_p<10>(D, boxes, n, s) ||
+                  p2l_warp_p<12>(D, boxes, n, s) || p2l_warp_p<15>(D, boxes, n, s) || p2l_warp_p<20>(D, boxes, n, s)))
+    return 1;
   const size_t smem = kP2LBatch * hsize(D.p + 1) * sizeof(double2);
   k_p2l<<<n, block_for(D.kp), smem, s>>>(D, boxes);
   return 1;
