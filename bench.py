@@ -32,7 +32,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 CONFIG_ID = 1
-CPU_SAMPLE = dict(nu=48, nv=24)  # 2,304 triangles, 36,864 sources: same family and orders, ~1/28 size
+CPU_SAMPLE = dict(nu=64, nv=32)  # 4,096 triangles, 65,536 sources: same family and orders, 1/16 size
 
 
 def parse():
@@ -296,9 +296,18 @@ def run_ours(args, rank, world, local_rank):
                      "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4), "flops": flops[k]}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     d = stages[dom]
+    traffic, traffic_note = None, None
+    tp = os.path.join(HERE, "profiles", "r01_ncu_m2l.json")
+    if dom == "m2l" and os.path.exists(tp) and not args.small:
+        with open(tp) as fh:
+            t = json.load(fh)
+        # one ncu --set full capture of the M2L GEMM launch (chunk 1 of 2); bytes per launch
+        traffic = (t["dram_read_GB"] + t["dram_write_GB"]) * 1e9
+        traffic_note = (f"bytes per launch of {t['kernel']} (profiles/r01_ncu_m2l.json); dominated by the "
+                        "2 KB/entry staging rows of the deterministic CSR reduction")
     roofline = {"bound": "fp64", "kernel": dom, "achieved": d["tflops"],
                 "peak": round(peak_dmma if dom == "m2l" else peak, 3), "unit": "TFLOP/s",
-                "frac": d["frac_fp64"], "traffic": None,
+                "frac": d["frac_fp64"], "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "in-run microbenchmarks (qbxg_measure_fp64_peak DFMA = %.1f, qbxg_measure_dmma_peak "
                                "DMMA = %.1f TFLOP/s); MEASURED_PEAKS.json has no fp64 entry" % (peak, peak_dmma),
                 "algorithmic_flops_per_launch": flops[dom], "share_of_step": round(d["ms"] / ms, 3)}
