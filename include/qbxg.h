@@ -283,6 +283,19 @@ int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* w
                     const double* dipoles_or_null, int64_t n_targets, const double* target_pos,
                     double* out_pot);
 
+/* ---- unaccelerated QBX, the GPU counterpart of the spec's direct_qbx ------ */
+/* each associated target (association[i] =
+ * centre id) gets the order-p_qbx local expansion of its centre formed from ALL
+ * sources, evaluated at the target (Eq. (9)); conventional targets
+ * (association[i] = -1) get the direct sum.  Same formulas and 1/(4 pi) as
+ * qbxg_apply, so |apply - direct_qbx| measures the FMM error alone (Theorem 1).
+ * p_qbx in [0, 8]; QBXG_ERR_INVALID_ARGUMENT on bad ids / radii / orders,
+ * QBXG_ERR_DOMAIN when a conventional target coincides with a source. */
+int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* weights,
+                    const double* dipoles_or_null, int64_t n_centers, const double* center_pos,
+                    const double* center_radius, int64_t n_targets, const double* target_pos,
+                    const int32_t* association, int32_t p_qbx, double* out_pot);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char* qbxg_last_error(void);
 int qbxg_device_count(int32_t* out);

@@ -392,6 +392,21 @@ def direct_sum(sources: SourceEnsemble, targets: TargetSet) -> np.ndarray:
     return pot
 
 
+def direct_qbx(geom: Geometry, weights, dipoles=None, p_qbx: int = 5) -> np.ndarray:
+    """Unaccelerated QBX on the GPU: every centre's local
+    expansion from all sources, same formulas as ``FmmEngine.apply``."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    mu = None if dipoles is None else np.ascontiguousarray(dipoles, dtype=np.float64).reshape(-1, 3)
+    if w.shape != (geom.n_sources,) or (mu is not None and mu.shape[0] != geom.n_sources):
+        raise ValueError("direct_qbx: density shape does not match the geometry")
+    pot = np.empty(geom.n_targets, dtype=np.float64)
+    _check(_abi.lib().qbxg_direct_qbx(geom.n_sources, _ptr(geom.source_pos), _ptr(w), _ptr(mu), geom.n_centers,
+                                      _ptr(geom.center_pos), _ptr(geom.center_radius), geom.n_targets,
+                                      _ptr(geom.target_pos), _ptr(geom.association, C.c_int32),
+                                      int(p_qbx), _ptr(pot)))
+    return pot
+
+
 def device_count() -> int:
     n = C.c_int32(0)
     _check(_abi.lib().qbxg_device_count(C.byref(n)))

@@ -1097,4 +1097,88 @@ int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* w
   });
 }
 
+int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* weights, const double* dipoles_or_null,
+                    int64_t n_centers, const double* center_pos, const double* center_radius, int64_t n_targets,
+                    const double* target_pos, const int32_t* association, int32_t p_qbx, double* out_pot) {
+  return qbxg::guarded([&] {
+    using qbxg::InvalidArgument;
+    if (n_sources < 0 || n_centers < 0 || n_targets < 0) throw InvalidArgument("direct_qbx: negative size");
+    if (n_sources >= (int64_t(1) << 31) || n_centers >= (int64_t(1) << 31) || n_targets >= (int64_t(1) << 31))
+      throw InvalidArgument("direct_qbx: too many points");
+    if (p_qbx < 0 || p_qbx > 8) throw InvalidArgument("direct_qbx: p_qbx must be in [0, 8]");
+    if ((n_sources && (!source_pos || !weights)) || (n_centers && (!center_pos || !center_radius)) ||
+        (n_targets && (!target_pos || !association || !out_pot)))
+      throw InvalidArgument("direct_qbx: null array");
+    qbxg::validate_sources(n_sources, source_pos, weights, dipoles_or_null);
+    for (int64_t c = 0; c < n_centers; ++c)
+      if (!(center_radius[c] > 0) || !std::isfinite(center_radius[c]) || !std::isfinite(center_pos[3 * c]) ||
+          !std::isfinite(center_pos[3 * c + 1]) || !std::isfinite(center_pos[3 * c + 2]))
+        throw InvalidArgument("direct_qbx: centre " + std::to_string(c) + " has a bad position or radius");
+    std::vector<int> conv;
+    for (int64_t i = 0; i < n_targets; ++i) {
+      const int32_t a = association[i];
+      if (a < -1 || a >= n_centers)
+        throw InvalidArgument("direct_qbx: target " + std::to_string(i) + " has association " + std::to_string(a) +
+                              " outside [-1, n_centers)");
+      if (a < 0) conv.push_back(int(i));
+    }
+    if (n_targets == 0) return;
+    qbxg::check_device();
+    std::vector<void*> owned;
+    struct Free {
+      std::vector<void*>& o;
+      ~Free() {
+        for (void* p : o) cudaFree(p);
+      }
+    } fr{owned};
+    std::vector<double4> src(n_sources), mu(dipoles_or_null ? n_sources : 0), ctr(n_centers), ctg(conv.size());
+    for (int64_t i = 0; i < n_sources; ++i) {
+      src[i] = make_double4(source_pos[3 * i], source_pos[3 * i + 1], source_pos[3 * i + 2], weights[i]);
+      if (dipoles_or_null)
+        mu[i] = make_double4(dipoles_or_null[3 * i], dipoles_or_null[3 * i + 1], dipoles_or_null[3 * i + 2], 0);
+    }
+    for (int64_t c = 0; c < n_centers; ++c)
+      ctr[c] = make_double4(center_pos[3 * c], center_pos[3 * c + 1], center_pos[3 * c + 2], center_radius[c]);
+    for (size_t j = 0; j < conv.size(); ++j) {
+      const int64_t i = conv[j];
+      ctg[j] = make_double4(target_pos[3 * i], target_pos[3 * i + 1], target_pos[3 * i + 2], 0);
+    }
+    cudaStream_t s = nullptr;
+    qbxg::dev::upload_constants();
+    double4* ds = qbxg::dupload(owned, src, s);
+    double4* dm = dipoles_or_null ? qbxg::dupload(owned, mu, s) : nullptr;
+    double4* dc = qbxg::dupload(owned, ctr, s);
+    std::vector<double> tp(target_pos, target_pos + 3 * n_targets);
+    std::vector<int> as(association, association + n_targets);
+    double* dtp = qbxg::dupload(owned, tp, s);
+    int* das = qbxg::dupload(owned, as, s);
+    double2* dl = qbxg::dalloc<double2>(owned, size_t(std::max<int64_t>(n_centers, 1)) * ((p_qbx + 1) * (p_qbx + 2) / 2));
+    double* dp = qbxg::dalloc<double>(owned, n_targets);
+    QCK(cudaMemsetAsync(dp, 0, n_targets * sizeof(double), s));
+    qbxg::dev::launch_direct_qbx(p_qbx, int(n_sources), ds, dm, int(n_centers), dc, dl, s);
+    QCK(cudaGetLastError());
+    qbxg::dev::launch_direct_qbx_eval(p_qbx, int(n_targets), dtp, das, dc, dl, dp, s);
+    QCK(cudaGetLastError());
+    std::vector<double> pot(n_targets);
+    QCK(cudaMemcpy(pot.data(), dp, n_targets * sizeof(double), cudaMemcpyDeviceToHost));
+    if (!conv.empty()) {
+      double4* dt = qbxg::dupload(owned, ctg, s);
+      double* dq = qbxg::dalloc<double>(owned, conv.size());
+      unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
+      QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+      qbxg::dev::launch_direct_sum(int(n_sources), ds, dm, int(conv.size()), dt, dq, bad, s);
+      QCK(cudaGetLastError());
+      unsigned long long hb = 0;
+      QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+      if (hb != ~0ull)
+        throw qbxg::DomainError("direct_qbx: target " + std::to_string(conv[hb >> 32]) +
+                                " coincides with source " + std::to_string(hb & 0xffffffffull));
+      std::vector<double> pc(conv.size());
+      QCK(cudaMemcpy(pc.data(), dq, conv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (size_t j = 0; j < conv.size(); ++j) pot[conv[j]] = pc[j];
+    }
+    std::copy(pot.begin(), pot.end(), out_pot);
+  });
+}
+
 }  // extern "C"

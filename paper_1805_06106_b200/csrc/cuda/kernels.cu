@@ -186,11 +186,87 @@ __device__ __forceinline__ int seg_source(int f, int nseg, const int* s_start, c
   return s_start[lo] + (f - s_pre[lo]);
 }
 
+// One source -> one centre P2QBXL contribution (accumulators unscaled by 1/r).
+template <int Q, bool DIP>
+__device__ __forceinline__ void near_pair(const double4 x, const double4 u, const double4 c, const double ir,
+                                          double* ax, double* ay) {
+  constexpr int KI = hsize(Q + (DIP ? 1 : 0));
+  const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
+  // J_n^m = r^{2n+1} I_n^m: polynomial recurrences without 1/r^2 per step;
+  // the r^{-(2n+1)} factor is folded into the per-degree source weights.
+  constexpr int P1 = Q + (DIP ? 1 : 0);
+  const double r2 = ux * ux + uy * uy + uz * uz;
+  const double ir2 = 1.0 / r2;
+  double2 J[KI];
+#pragma unroll
+  for (int m = 0; m <= P1; ++m) {
+    if (m == 0) {
+      J[0] = make_double2(1.0, 0.0);
+    } else {
+      const double2 d = J[hidx(m - 1, m - 1)];
+      const double f = double(2 * m - 1);
+      J[hidx(m, m)] = make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
+    }
+    if (m + 1 <= P1) {
+      const double f = double(2 * m + 1) * uz;
+      J[hidx(m + 1, m)] = make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
+    }
+#pragma unroll
+    for (int n = m + 2; n <= P1; ++n) {
+      const double zc = double(2 * n - 1) * uz;
+      const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
+      const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
+      J[hidx(n, m)] = make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
+    }
+  }
+  double sc[P1 + 1];  // r^{-(2n+1)}
+  sc[0] = sqrt(ir2);
+#pragma unroll
+  for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
+  const double w = x.w;
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) {
+    const double wn = w * sc[n];
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      const int id = hidx(n, m);
+      ax[id] = fma(wn, J[id].x, ax[id]);
+      ay[id] = fma(-wn, J[id].y, ay[id]);
+    }
+  }
+  if (DIP) {
+    // acc += conj(g), g = -mz I_{n+1}^m + (hx + i hy) I_{n+1}^{m-1} - (hx - i hy) I_{n+1}^{m+1}
+#pragma unroll
+    for (int n = 0; n <= Q; ++n) {
+      const double s1 = sc[n + 1] * ir;
+      const double mz = u.z * s1, hx = 0.5 * u.x * s1, hy = 0.5 * u.y * s1;
+#pragma unroll
+      for (int m = 0; m <= n; ++m) {
+        const int id = hidx(n, m);
+        const double2 i0 = J[hidx(n + 1, m)];
+        const double2 ip = J[hidx(n + 1, m + 1)];
+        double2 im;
+        if (m >= 1) {
+          im = J[hidx(n + 1, m - 1)];
+        } else {
+          const double2 t = J[hidx(n + 1, 1)];
+          im = make_double2(-t.x, t.y);  // X_{n+1}^{-1} = -conj(X_{n+1}^1)
+        }
+        ax[id] = fma(-mz, i0.x, ax[id]);
+        ax[id] = fma(hx, im.x - ip.x, ax[id]);
+        ax[id] = fma(-hy, im.y + ip.y, ax[id]);
+        ay[id] = fma(mz, i0.y, ay[id]);
+        ay[id] = fma(-hx, im.y - ip.y, ay[id]);
+        ay[id] = fma(-hy, im.x + ip.x, ay[id]);
+      }
+    }
+  }
+}
+
 // P2QBXL: L~_c += (1/r)[w conj(I(u)) + conj(mu . grad I(u)) / r], u = (s - c)/r   (Eq. (8))
 template <int Q, bool DIP>
 __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int* __restrict__ boxes) {
   constexpr int KQ = hsize(Q);
-  constexpr int KI = hsize(Q + (DIP ? 1 : 0));
   __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
   __shared__ double4 s_src[kNearChunk];
   __shared__ double4 s_mu[DIP ? kNearChunk : 1];
@@ -224,78 +300,7 @@ __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int*
         __syncthreads();
         if (active) {
           for (int j = sl; j < nch; j += S) {
-            const double4 x = s_src[j];
-            const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
-            // J_n^m = r^{2n+1} I_n^m: polynomial recurrences without 1/r^2 per step;
-            // the r^{-(2n+1)} factor is folded into the per-degree source weights.
-            constexpr int P1 = Q + (DIP ? 1 : 0);
-            const double r2 = ux * ux + uy * uy + uz * uz;
-            const double ir2 = 1.0 / r2;
-            double2 J[KI];
-#pragma unroll
-            for (int m = 0; m <= P1; ++m) {
-              if (m == 0) {
-                J[0] = make_double2(1.0, 0.0);
-              } else {
-                const double2 d = J[hidx(m - 1, m - 1)];
-                const double f = double(2 * m - 1);
-                J[hidx(m, m)] = make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
-              }
-              if (m + 1 <= P1) {
-                const double f = double(2 * m + 1) * uz;
-                J[hidx(m + 1, m)] = make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
-              }
-#pragma unroll
-              for (int n = m + 2; n <= P1; ++n) {
-                const double zc = double(2 * n - 1) * uz;
-                const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
-                const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
-                J[hidx(n, m)] = make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
-              }
-            }
-            double sc[P1 + 1];  // r^{-(2n+1)}
-            sc[0] = sqrt(ir2);
-#pragma unroll
-            for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
-            const double w = x.w;
-#pragma unroll
-            for (int n = 0; n <= Q; ++n) {
-              const double wn = w * sc[n];
-#pragma unroll
-              for (int m = 0; m <= n; ++m) {
-                const int id = hidx(n, m);
-                ax[id] = fma(wn, J[id].x, ax[id]);
-                ay[id] = fma(-wn, J[id].y, ay[id]);
-              }
-            }
-            if (DIP) {
-              // acc += conj(g), g = -mz I_{n+1}^m + (hx + i hy) I_{n+1}^{m-1} - (hx - i hy) I_{n+1}^{m+1}
-              const double4 u = s_mu[j];
-#pragma unroll
-              for (int n = 0; n <= Q; ++n) {
-                const double s1 = sc[n + 1] * ir;
-                const double mz = u.z * s1, hx = 0.5 * u.x * s1, hy = 0.5 * u.y * s1;
-#pragma unroll
-                for (int m = 0; m <= n; ++m) {
-                  const int id = hidx(n, m);
-                  const double2 i0 = J[hidx(n + 1, m)];
-                  const double2 ip = J[hidx(n + 1, m + 1)];
-                  double2 im;
-                  if (m >= 1) {
-                    im = J[hidx(n + 1, m - 1)];
-                  } else {
-                    const double2 t = J[hidx(n + 1, 1)];
-                    im = make_double2(-t.x, t.y);  // X_{n+1}^{-1} = -conj(X_{n+1}^1)
-                  }
-                  ax[id] = fma(-mz, i0.x, ax[id]);
-                  ax[id] = fma(hx, im.x - ip.x, ax[id]);
-                  ax[id] = fma(-hy, im.y + ip.y, ax[id]);
-                  ay[id] = fma(mz, i0.y, ay[id]);
-                  ay[id] = fma(-hx, im.y - ip.y, ay[id]);
-                  ay[id] = fma(-hy, im.x + ip.x, ay[id]);
-                }
-              }
-            }
+            near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
           }
         }
       }
@@ -852,6 +857,65 @@ __global__ void k_eval_conv(DevData D, int n, const int* __restrict__ items, con
   pot[tgt_perm[i]] = kInv4Pi * (D.phi[i] + v);
 }
 
+// ---------------------------------------------------------------- direct QBX
+// Unaccelerated QBX: every centre's local expansion from ALL sources (the same
+// P2QBXL pair kernel as the near field), 32 centres x 4 source slices per CTA,
+// sources staged once per chunk for the whole CTA.
+constexpr int kDqCentres = 32;
+template <int Q, bool DIP>
+__global__ void __launch_bounds__(128) k_direct_qbx(int ns, const double4* __restrict__ src,
+                                                    const double4* __restrict__ mu, int nc,
+                                                    const double4* __restrict__ ctr, double2* __restrict__ Lc) {
+  constexpr int KQ = hsize(Q);
+  __shared__ double4 s_src[kNearChunk];
+  __shared__ double4 s_mu[DIP ? kNearChunk : 1];
+  const int ci = threadIdx.x >> 2, sl = threadIdx.x & 3;
+  const int cid = blockIdx.x * kDqCentres + ci;
+  const bool active = cid < nc;
+  const double4 c = active ? ctr[cid] : make_double4(0, 0, 0, 1);
+  const double ir = 1.0 / c.w;
+  double ax[KQ], ay[KQ];
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
+  for (int ch = 0; ch < ns; ch += kNearChunk) {
+    const int nch = min(kNearChunk, ns - ch);
+    __syncthreads();
+    for (int f = threadIdx.x; f < nch; f += blockDim.x) {
+      s_src[f] = src[ch + f];
+      if (DIP) s_mu[f] = mu[ch + f];
+    }
+    __syncthreads();
+    if (active)
+      for (int j = sl; j < nch; j += 4)
+        near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+  }
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) {
+    ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], 1, 4);
+    ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], 1, 4);
+    ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], 2, 4);
+    ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], 2, 4);
+  }
+  if (active && sl == 0) {
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) Lc[size_t(cid) * KQ + i] = make_double2(ax[i] * ir, ay[i] * ir);
+  }
+}
+
+// QBXL2P for direct QBX: associated targets, caller's order (Eq. (9)).
+__global__ void k_direct_qbx_eval(int q, int n, const double* __restrict__ tpos, const int* __restrict__ assoc,
+                                  const double4* __restrict__ ctr, const double2* __restrict__ Lc,
+                                  double* __restrict__ pot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = assoc[i];
+  if (a < 0) return;
+  const double4 c = ctr[a];
+  const double ir = 1.0 / c.w;
+  pot[i] = kInv4Pi * eval_regular_sum(Lc + size_t(a) * hsize(q), q, (tpos[3 * i] - c.x) * ir,
+                                      (tpos[3 * i + 1] - c.y) * ir, (tpos[3 * i + 2] - c.z) * ir);
+}
+
 // Centre coefficients in the paper's normalisation (Eq. (5)):
 //   L^paper_n^m = (L~_n^m / r^n) / (4 pi N_nm (n+m)!),  N_nm = sqrt((2n+1)/(4 pi) (n-m)!/(n+m)!)
 __global__ void k_centre_out(DevData D, int nc, const int* __restrict__ items, const int* __restrict__ ctr_perm,
@@ -978,6 +1042,41 @@ int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s) {
     case 8: near_qbx_q<8>(D, boxes, n, s); break;
     default: return -1;
   }
+  return 1;
+}
+
+template <int Q>
+static void direct_qbx_q(int ns, const double4* src, const double4* mu, int nc, const double4* ctr, double2* Lc,
+                         cudaStream_t s) {
+  const int grid = (nc + kDqCentres - 1) / kDqCentres;
+  if (mu)
+    k_direct_qbx<Q, true><<<grid, 128, 0, s>>>(ns, src, mu, nc, ctr, Lc);
+  else
+    k_direct_qbx<Q, false><<<grid, 128, 0, s>>>(ns, src, mu, nc, ctr, Lc);
+}
+
+int launch_direct_qbx(int q, int ns, const double4* src, const double4* mu, int nc, const double4* ctr,
+                      double2* Lc, cudaStream_t s) {
+  if (nc == 0) return 0;
+  switch (q) {
+    case 0: direct_qbx_q<0>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 1: direct_qbx_q<1>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 2: direct_qbx_q<2>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 3: direct_qbx_q<3>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 4: direct_qbx_q<4>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 5: direct_qbx_q<5>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 6: direct_qbx_q<6>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 7: direct_qbx_q<7>(ns, src, mu, nc, ctr, Lc, s); break;
+    case 8: direct_qbx_q<8>(ns, src, mu, nc, ctr, Lc, s); break;
+    default: return -1;
+  }
+  return 1;
+}
+
+int launch_direct_qbx_eval(int q, int n, const double* tpos, const int* assoc, const double4* ctr,
+                           const double2* Lc, double* pot, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_direct_qbx_eval<<<(n + 127) / 128, 128, 0, s>>>(q, n, tpos, assoc, ctr, Lc, pot);
   return 1;
 }
 

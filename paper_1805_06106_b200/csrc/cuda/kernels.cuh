@@ -150,6 +150,10 @@ int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr
 int launch_tables(const DevData& D, double2* m2l_tab, double2* oct_m2m, double2* oct_l2l, cudaStream_t s);
 int launch_direct_sum(int ns, const double4* src, const double4* mu, int nt, const double4* tgt, double* pot,
                       unsigned long long* bad, cudaStream_t s);
+int launch_direct_qbx(int q, int ns, const double4* src, const double4* mu, int nc, const double4* ctr,
+                      double2* Lc, cudaStream_t s);
+int launch_direct_qbx_eval(int q, int n, const double* tpos, const int* assoc, const double4* ctr,
+                           const double2* Lc, double* pot, cudaStream_t s);
 void upload_constants();
 void set_smem_limits();
 
