@@ -535,6 +535,140 @@ void pair_q(const DevData& D, const int2* pairs, int n, double2* temp, cudaStrea
   k_m2qbxl_pair<Q><<<(n + kFT - 1) / kFT, kFT, smem, s>>>(D, pairs, n, temp);
 }
 
+// L2QBXL, box-table variant: a CTA takes up to kL3Threads consecutive centres
+// spanning at most kL3Boxes boxes (host-built descriptors).  Each box's local
+// is staged once as a zero-padded full table of degree p+q in shared memory, so
+// the contraction
+//   L~_c(n,m) = (r/h)^n sum_{N,K} [T(N+n, m+K) R_N^K + T(N+n, m-K) R_N^{-K}]
+// needs no range predicates, no conjugate-symmetry branches and no global loads:
+// per (N, K) every thread issues 2 x hsize(q) complex FMAs against warp-broadcast
+// shared reads, with R_N^K streamed from a register recurrence.
+template <int Q>
+__global__ void __launch_bounds__(kL3Threads) k_l2qbxl3(DevData D, const int* __restrict__ items,
+                                                        const int2* __restrict__ ctas,
+                                                        const int* __restrict__ ctr_box) {
+  constexpr int KQ = hsize(Q);
+  extern __shared__ double2 s_tab[];  // kL3Boxes x TS
+  __shared__ int s_box[kL3Boxes];
+  __shared__ int s_wcount[kL3Threads / 32];
+  const int P = D.p, NT = P + Q + 1, TS = NT * NT;
+  const int2 cta = ctas[blockIdx.x];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const bool active = t < cta.y;
+  int cs = -1, b = -1, prevb = -2;
+  if (active) {
+    cs = items[cta.x + t];
+    b = ctr_box[cs];
+    if (t > 0) prevb = ctr_box[items[cta.x + t - 1]];
+  }
+  const bool head = active && b != prevb;
+  const unsigned bal = __ballot_sync(0xffffffffu, head);
+  if (lane == 0) s_wcount[w] = __popc(bal);
+  __syncthreads();
+  int base = 0, nbox = 0;
+#pragma unroll
+  for (int i = 0; i < kL3Threads / 32; ++i) {
+    base += i < w ? s_wcount[i] : 0;
+    nbox += s_wcount[i];
+  }
+  const int slot = base + __popc(bal & ((2u << lane) - 1u)) - 1;
+  if (head) s_box[slot] = b;
+  __syncthreads();
+  for (int e = t; e < nbox * TS; e += kL3Threads) {
+    const int sb = e / TS, r = e - sb * TS;
+    int j = int(sqrt(double(r)));
+    while (j * j > r) --j;
+    while ((j + 1) * (j + 1) <= r) ++j;
+    const int k = r - j * j - j;
+    double2 v = make_double2(0.0, 0.0);
+    if (j <= P) {
+      const double2 h = D.L[size_t(s_box[sb]) * D.kp + hidx(j, k < 0 ? -k : k)];
+      v = k >= 0 ? h : ((k & 1) ? make_double2(-h.x, h.y) : make_double2(h.x, -h.y));
+    }
+    s_tab[e] = v;
+  }
+  __syncthreads();
+  if (!active) return;
+  const double2* __restrict__ tb = s_tab + slot * TS;
+  const double4 bc = D.box[b];
+  const double ih = 1.0 / bc.w;
+  const double4 c = D.ctr[cs];
+  const double x = (c.x - bc.x) * ih, y = (c.y - bc.y) * ih, z = (c.z - bc.z) * ih;
+  const double r2 = x * x + y * y + z * z;
+  double ax[KQ], ay[KQ];
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
+  double2 diag = make_double2(1.0, 0.0);
+  for (int K = 0; K <= P; ++K) {
+    if (K > 0) {
+      const double s = 1.0 / (2.0 * K);
+      diag = make_double2((diag.x * x - diag.y * y) * s, (diag.x * y + diag.y * x) * s);
+    }
+    const double sg = (K & 1) ? -1.0 : 1.0;
+    double2 ra = make_double2(0.0, 0.0), rb = diag;
+    for (int N = K; N <= P; ++N) {
+      double2 cur;
+      if (N == K) {
+        cur = diag;
+      } else if (N == K + 1) {
+        cur = make_double2(z * diag.x, z * diag.y);
+      } else {
+        const double c1 = (2 * N - 1) * z;
+        const double f = 1.0 / double((N - K) * (N + K));
+        cur = make_double2((c1 * rb.x - r2 * ra.x) * f, (c1 * rb.y - r2 * ra.y) * f);
+      }
+      if (N > K) {
+        ra = rb;
+        rb = cur;
+      }
+      const double2 cm = make_double2(sg * cur.x, -sg * cur.y);  // R_N^{-K}
+#pragma unroll
+      for (int n = 0; n <= Q; ++n) {
+        const int j = N + n;
+        const double2* __restrict__ row = tb + j * j + j;
+#pragma unroll
+        for (int m = 0; m <= n; ++m) {
+          const int id = hidx(n, m);
+          const double2 a1 = row[m + K];
+          ax[id] = fma(a1.x, cur.x, fma(-a1.y, cur.y, ax[id]));
+          ay[id] = fma(a1.x, cur.y, fma(a1.y, cur.x, ay[id]));
+          if (K > 0) {
+            const double2 a2 = row[m - K];
+            ax[id] = fma(a2.x, cm.x, fma(-a2.y, cm.y, ax[id]));
+            ay[id] = fma(a2.x, cm.y, fma(a2.y, cm.x, ay[id]));
+          }
+        }
+      }
+    }
+  }
+  double f = 1.0;
+  const double rh = c.w * ih;
+  double2* out = D.Lc + size_t(cs) * KQ;
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) {
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      double2 v = out[hidx(n, m)];
+      v.x += ax[hidx(n, m)] * f;
+      v.y += ay[hidx(n, m)] * f;
+      out[hidx(n, m)] = v;
+    }
+    f *= rh;
+  }
+}
+
+template <int Q>
+void l2qbxl3_q(const DevData& D, const int* items, const int2* ctas, int n_ctas, const int* ctr_box,
+               cudaStream_t s) {
+  const size_t smem = size_t(kL3Boxes) * (D.p + Q + 1) * (D.p + Q + 1) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_l2qbxl3<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_l2qbxl3<Q><<<n_ctas, kL3Threads, smem, s>>>(D, items, ctas, ctr_box);
+}
+
 template <int Q>
 void flat_q(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s) {
   const size_t smem = size_t(kFT) * (D.p + D.q + 1) * sizeof(double2);
@@ -642,6 +776,24 @@ int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_bo
     case 6: flat_q<6>(D, items, n, ctr_box, irreg, s); break;
     case 7: flat_q<7>(D, items, n, ctr_box, irreg, s); break;
     case 8: flat_q<8>(D, items, n, ctr_box, irreg, s); break;
+    default: return -1;
+  }
+  return 1;
+}
+
+int launch_l2qbxl3(const DevData& D, const int* items, const int2* ctas, int n_ctas, const int* ctr_box,
+                   cudaStream_t s) {
+  if (n_ctas == 0) return 0;
+  switch (D.q) {
+    case 0: l2qbxl3_q<0>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 1: l2qbxl3_q<1>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 2: l2qbxl3_q<2>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 3: l2qbxl3_q<3>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 4: l2qbxl3_q<4>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 5: l2qbxl3_q<5>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 6: l2qbxl3_q<6>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 7: l2qbxl3_q<7>(D, items, ctas, n_ctas, ctr_box, s); break;
+    case 8: l2qbxl3_q<8>(D, items, ctas, n_ctas, ctr_box, s); break;
     default: return -1;
   }
   return 1;

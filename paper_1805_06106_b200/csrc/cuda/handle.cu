@@ -109,7 +109,9 @@ struct Handle {
   int* d_flat_wfar = nullptr;    // sorted centres of boxes with List 3 far entries
   int n_flat_wfar = 0;
   int ctr_mode = 0;              // W far M2QBXL: 0 pairs, 1 gemm, 2 per-box
-  int l2q_mode = 0;              // L2QBXL: 0 flat, 1 gemm, 2 warp per box
+  int l2q_mode = 3;              // L2QBXL: 3 box tables (default), 0 flat, 1 gemm, 2 warp per box
+  int2* d_l3_ctas = nullptr;     // L2QBXL CTA descriptors (first item in d_flat_all, count)
+  int n_l3_ctas = 0;
   dev::PairPlan wpairs;          // M2QBXL (centre, W_far box) pairs
   double* ops_m2m = nullptr;     // 8 octant operators (real DOF)
   double* ops_l2l = nullptr;
@@ -597,6 +599,26 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       for (int j = 0; j < V.ctr_own_count[b]; ++j) fw.push_back(V.ctr_own_start[b] + j);
     H.d_ctr_box = dupload(O, cbox, s);
     H.d_flat_all = dupload(O, all, s);
+    {
+      std::vector<int2> l3;
+      size_t i = 0;
+      while (i < all.size()) {
+        const size_t first = i;
+        int nbx = 0, last = -1;
+        while (i < all.size() && i - first < size_t(dev::kL3Threads)) {
+          const int bx = cbox[all[i]];
+          if (bx != last) {
+            if (nbx == dev::kL3Boxes) break;
+            ++nbx;
+            last = bx;
+          }
+          ++i;
+        }
+        l3.push_back(make_int2(int(first), int(i - first)));
+      }
+      H.d_l3_ctas = dupload(O, l3, s);
+      H.n_l3_ctas = int(l3.size());
+    }
     H.d_flat_wfar = dupload(O, fw, s);
     H.n_flat_wfar = int(fw.size());
     if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
@@ -806,7 +828,9 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
       chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
   }
   QCK(cudaEventRecord(ev[8], s));
-  if (H.l2q_mode == 0)
+  if (H.l2q_mode == 3)
+    chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
+  else if (H.l2q_mode == 0)
     chk(dev::launch_ctr_flat(D, H.d_flat_all, H.n_own_ctr, H.d_ctr_box, false, s));
   else if (H.l2q_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
     chk(dev::launch_ctr_gemm(D, H.d_items_ctr, H.n_items_ctr, false, s));

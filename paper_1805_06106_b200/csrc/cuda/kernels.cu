@@ -196,7 +196,8 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
   // the r^{-(2n+1)} factor is folded into the per-degree source weights.
   constexpr int P1 = Q + (DIP ? 1 : 0);
   const double r2 = ux * ux + uy * uy + uz * uz;
-  const double ir2 = 1.0 / r2;
+  const double rs = rsqrt(r2);  // 1/r (1 ulp); 1/r^2 and r^{-(2n+1)} follow by products
+  const double ir2 = rs * rs;
   double2 J[KI];
 #pragma unroll
   for (int m = 0; m <= P1; ++m) {
@@ -220,7 +221,7 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
     }
   }
   double sc[P1 + 1];  // r^{-(2n+1)}
-  sc[0] = sqrt(ir2);
+  sc[0] = rs;
 #pragma unroll
   for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
   const double w = x.w;
@@ -633,107 +634,175 @@ __global__ void __launch_bounds__(256) k_p2l(DevData D, const int* __restrict__ 
   }
 }
 
-// P2L, warp per target box: lane m owns azimuthal column m of the source's
-// irregular harmonics I_N^m((s - c_b)/h) (N <= P+1) in registers and the
-// output coefficients L~(n, m); the dipole's neighbouring columns m +- 1 come
-// from lanes m +- 1 by shuffles.  No block barriers; sources stream through
-// the read-only cache (every lane reads the same source).
+// P2L, column-pair lanes.  One CTA per target box: kP3Slices source slices x 8
+// lanes.  Lane cl owns output columns m = cl and m = P - cl (P + 2 coefficients
+// for every lane at P = 15, so the lanes are balanced) in registers and streams
+// I_n^m, I_{n+1}^{m-1}, I_{n+1}^m, I_{n+1}^{m+1} of each source through three
+// register recurrences in n.  The diagonals I_k^k = (2k-1)!! w^k / r, with
+// w = (ux + i uy)/r^2, are computed by the 8 lanes of a slice (repeated squaring)
+// and shared through shared memory.  Slices are summed in fixed order.
+constexpr int kP3Slices = 16;
+__constant__ double c_dfact[22] = {
+    1, 1, 3, 15, 105, 945, 10395, 135135, 2027025, 34459425, 654729075, 13749310575, 316234143225,
+    7905853580625, 213458046676875, 6190283353629375, 1.9189878396251062e+17, 6.3326598707628503e+18,
+    2.2164309547669976e+20, 8.2007945326378919e+21, 3.1983098677287775e+23, 1.3113070457687988e+25};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
 template <int P, bool DIP>
-__global__ void __launch_bounds__(128) k_p2l_warp(DevData D, const int* __restrict__ boxes, int n) {
-  constexpr int P1 = P + 1;  // dipole needs order P+1
-  const int wid = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  const int b = boxes[wid];
+__global__ void __launch_bounds__(128) k_p2l3(DevData D, const int* __restrict__ boxes) {
+  static_assert(P <= 15, "two columns per lane, 8 lanes");
+  constexpr int NS = kP3Slices;
+  constexpr int KP = hsize(P);
+  constexpr int ND = P + 2;  // diagonals D_0 .. D_{P+1}
+  __shared__ double2 s_diag[NS][ND];
+  __shared__ double2 s_red[NS * KP];
+  const int t = threadIdx.x, sl = t >> 3, cl = t & 7;
+  const unsigned smask = 0xffu << (t & 24);
+  const int b = boxes[blockIdx.x];
   const double4 bc = D.box[b];
   const double ih = 1.0 / bc.w;
-  const int m = lane;  // column
-  double ax[P + 1], ay[P + 1];
+  const int mA = cl, mB = P - cl;
+  const int nA = mA <= mB ? P + 1 - mA : 0;
+  const int nB = mB > mA ? P + 1 - mB : 0;
+  double2 acc[P + 2];
 #pragma unroll
-  for (int k = 0; k <= P; ++k) ax[k] = ay[k] = 0.0;
-  // (2m-1)!! for this lane's diagonal
-  double dfact = 1.0;
-  for (int k = 1; k <= m && k <= P1; ++k) dfact *= (2 * k - 1);
-  for (int64_t e = D.xfar_starts[b]; e < D.xfar_starts[b + 1]; ++e) {
-    const int2 sg = D.xfar_seg[e];
-    for (int si = sg.x; si < sg.x + sg.y; ++si) {
-      const double4 x = D.src[si];
-      const double ux = (x.x - bc.x) * ih, uy = (x.y - bc.y) * ih, uz = (x.z - bc.z) * ih;
-      const double r2 = ux * ux + uy * uy + uz * uz;
-      const double ir2 = 1.0 / r2;
-      // diagonal I_m^m = (2m-1)!! (x+iy)^m / r^(2m+1)
-      double px = 1.0, py = 0.0;
-      for (int k = 0; k < m && k < P1; ++k) {
-        const double t = px * ux - py * uy;
-        py = px * uy + py * ux;
-        px = t;
-      }
-      double sc = sqrt(ir2);
-      for (int k = 0; k < m && k < P1; ++k) sc *= ir2;
-      const double dgx = dfact * px * sc, dgy = dfact * py * sc;
-      // column m: col[N] valid for N >= m (garbage zeros below)
-      double cx[P1 + 1], cy[P1 + 1];
+  for (int i = 0; i < P + 2; ++i) acc[i] = make_double2(0.0, 0.0);
+  // cursor over the X_far segments: slice sl takes flat sources sl, sl + NS, ...
+  const int64_t sb = D.xfar_starts[b], se = D.xfar_starts[b + 1];
+  const int2* __restrict__ seg = D.xfar_seg;
+  int64_t k = sb;
+  int off = sl, st = 0, cnt = 0;
+  if (k < se) {
+    st = seg[k].x;
+    cnt = seg[k].y;
+  }
+  while (k < se && off >= cnt) {
+    off -= cnt;
+    if (++k < se) {
+      st = seg[k].x;
+      cnt = seg[k].y;
+    }
+  }
+  while (k < se) {
+    const int s = st + off;
+    const double4 x = D.src[s];
+    double4 mu = make_double4(0, 0, 0, 0);
+    if (DIP) mu = D.mu[s];
+    const double ux = (x.x - bc.x) * ih, uy = (x.y - bc.y) * ih, uz = (x.z - bc.z) * ih;
+    const double r2 = ux * ux + uy * uy + uz * uz;
+    const double rs = rsqrt(r2);
+    const double ir2 = rs * rs;
+    {  // diagonals D_cl, D_{cl+8}, D_16
+      const double2 w = make_double2(ux * ir2, uy * ir2);
+      double2 pw = make_double2(1.0, 0.0), q = w;
 #pragma unroll
-      for (int N = 0; N <= P1; ++N) {
-        double vx, vy;
-        if (N == 0) {
-          vx = dgx;  // only used when m == 0
-          vy = dgy;
-        } else {
-          const double ax1 = cx[N - 1], ay1 = cy[N - 1];
-          const double ax2 = N >= 2 ? cx[N - 2] : 0.0, ay2 = N >= 2 ? cy[N - 2] : 0.0;
-          const double c1 = (2 * N - 1) * uz * ir2;
-          const double c2 = double((N - 1 + m) * (N - 1 - m)) * ir2;
-          vx = c1 * ax1 - c2 * ax2;
-          vy = c1 * ay1 - c2 * ay2;
-          if (N == m + 1) {  // I_{m+1}^m = (2m+1) z / r^2 I_m^m
-            vx = (2 * m + 1) * uz * ir2 * ax1;
-            vy = (2 * m + 1) * uz * ir2 * ay1;
-          }
-        }
-        const bool diag = (N == m);
-        cx[N] = diag ? dgx : (N < m ? 0.0 : vx);
-        cy[N] = diag ? dgy : (N < m ? 0.0 : vy);
+      for (int bit = 0; bit < 3; ++bit) {
+        if ((cl >> bit) & 1) pw = cmul(pw, q);
+        q = cmul(q, q);
       }
-      const double w = x.w;
-      double hx = 0, hy = 0, mz = 0;
-      if (DIP) {
-        const double4 u = D.mu[si];
-        hx = 0.5 * u.x * ih;
-        hy = 0.5 * u.y * ih;
-        mz = u.z * ih;
+      if (cl < ND) s_diag[sl][cl] = make_double2(c_dfact[cl] * rs * pw.x, c_dfact[cl] * rs * pw.y);
+      if (cl + 8 < ND) {
+        const double2 p8 = cmul(pw, q);
+        s_diag[sl][cl + 8] = make_double2(c_dfact[cl + 8] * rs * p8.x, c_dfact[cl + 8] * rs * p8.y);
       }
+      if (cl == 0 && 16 < ND) {
+        const double2 p16 = cmul(q, q);
+        s_diag[sl][16] = make_double2(c_dfact[16] * rs * p16.x, c_dfact[16] * rs * p16.y);
+      }
+    }
+    __syncwarp(smask);
+    const double w = x.w;
+    const double hx = 0.5 * mu.x * ih, hy = 0.5 * mu.y * ih, mz = mu.z * ih;
+    // column state: c0 = I_n^m, c0n = I_{n+1}^m, cp/cpp = I_{n+1}^{m+1}/I_n^{m+1},
+    // cm/cmp = I_{n+1}^{m-1}/I_n^{m-1}
+    int m = 0, n = 0;
+    double2 c0 = {}, c0n = {}, cp = {}, cpp = {}, cm = {}, cmp = {};
+    auto init = [&](int mm) {
+      m = mm;
+      n = mm;
+      const double2 dm = s_diag[sl][mm], dp = s_diag[sl][mm + 1];
+      c0 = dm;
+      const double f0 = (2 * mm + 1) * uz * ir2;
+      c0n = make_double2(f0 * dm.x, f0 * dm.y);
+      cp = dp;
+      cpp = make_double2(0.0, 0.0);
+      if (mm > 0) {
+        const double2 dd = s_diag[sl][mm - 1];
+        const double fa = (2 * mm - 1) * uz * ir2;
+        const double2 a = make_double2(fa * dd.x, fa * dd.y);  // I_mm^{mm-1}
+        const double c1 = (2 * mm + 1) * uz, c2 = double(2 * mm - 1);
+        cm = make_double2((c1 * a.x - c2 * dd.x) * ir2, (c1 * a.y - c2 * dd.y) * ir2);
+        cmp = a;
+      } else {
+        cm = cmp = make_double2(0.0, 0.0);
+      }
+    };
+    if (nA + nB > 0) init(nA > 0 ? mA : mB);
 #pragma unroll
-      for (int nn = 0; nn <= P; ++nn) {
-        // monopole: L(nn, m) += w conj(I_nn^m)
-        double tx = w * cx[nn], ty = -w * cy[nn];
+    for (int tt = 0; tt < P + 2; ++tt) {
+      if (tt < nA + nB) {
+        if (tt == nA && tt > 0) init(mB);
+        acc[tt].x = fma(w, c0.x, acc[tt].x);
+        acc[tt].y = fma(-w, c0.y, acc[tt].y);
         if (DIP) {
-          const double ipx = __shfl_down_sync(0xffffffffu, cx[nn + 1], 1);  // I_{nn+1}^{m+1}
-          const double ipy = __shfl_down_sync(0xffffffffu, cy[nn + 1], 1);
-          double imx = __shfl_up_sync(0xffffffffu, cx[nn + 1], 1);         // I_{nn+1}^{m-1}
-          double imy = __shfl_up_sync(0xffffffffu, cy[nn + 1], 1);
-          if (m == 0) {  // I^{-1} = -conj(I^1), from lane 1
-            imx = -ipx;
-            imy = ipy;
-          }
-          const double i0x = cx[nn + 1], i0y = cy[nn + 1];
-          // acc += conj(g), g = -mz i0 + (hx + i hy) im - (hx - i hy) ip
-          tx += -mz * i0x + hx * (imx - ipx) - hy * (imy + ipy);
-          ty -= -mz * i0y + hx * (imy - ipy) + hy * (imx + ipx);
+          const double2 im = m == 0 ? make_double2(-cp.x, cp.y) : cm;
+          const double gx = -mz * c0n.x + (hx * im.x - hy * im.y) - (hx * cp.x + hy * cp.y);
+          const double gy = -mz * c0n.y + (hx * im.y + hy * im.x) - (hx * cp.y - hy * cp.x);
+          acc[tt].x += gx;
+          acc[tt].y -= gy;
         }
-        ax[nn] += tx;
-        ay[nn] += ty;
+        if (tt + 1 < nA + nB) {  // advance n -> n + 1
+          const double c1 = (2 * n + 3) * uz;
+          const int n1 = (n + 1) * (n + 1);
+          const double a0 = double(n1 - m * m), ap = double(n1 - (m + 1) * (m + 1)),
+                       am = double(n1 - (m - 1) * (m - 1));
+          const double2 nc0n = make_double2((c1 * c0n.x - a0 * c0.x) * ir2, (c1 * c0n.y - a0 * c0.y) * ir2);
+          const double2 ncp = make_double2((c1 * cp.x - ap * cpp.x) * ir2, (c1 * cp.y - ap * cpp.y) * ir2);
+          const double2 ncm = make_double2((c1 * cm.x - am * cmp.x) * ir2, (c1 * cm.y - am * cmp.y) * ir2);
+          c0 = c0n;
+          c0n = nc0n;
+          cpp = cp;
+          cp = ncp;
+          cmp = cm;
+          cm = ncm;
+          ++n;
+        }
+      }
+    }
+    __syncwarp(smask);
+    off += NS;
+    while (k < se && off >= cnt) {
+      off -= cnt;
+      if (++k < se) {
+        st = seg[k].x;
+        cnt = seg[k].y;
       }
     }
   }
-  if (m > P) return;
+  // fixed-order reduction over slices
 #pragma unroll
-  for (int nn = 0; nn <= P; ++nn) {
-    if (nn < m) continue;
-    double2* dst = D.L + size_t(b) * D.kp + hidx(nn, m);
-    double2 v = *dst;
-    v.x += ax[nn] * ih;
-    v.y += ay[nn] * ih;
-    *dst = v;
+  for (int tt = 0; tt < P + 2; ++tt) {
+    if (tt < nA + nB) {
+      const int mm = tt < nA ? mA : mB;
+      const int nn = tt < nA ? mA + tt : mB + tt - nA;
+      s_red[sl * KP + hidx(nn, mm)] = acc[tt];
+    }
+  }
+  __syncthreads();
+  for (int c = t; c < KP; c += blockDim.x) {
+    double sx = 0, sy = 0;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      sx += s_red[i * KP + c].x;
+      sy += s_red[i * KP + c].y;
+    }
+    double2 v = D.L[size_t(b) * D.kp + c];
+    v.x += sx * ih;
+    v.y += sy * ih;
+    D.L[size_t(b) * D.kp + c] = v;
   }
 }
 
@@ -1103,23 +1172,25 @@ int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-template <int P>
-bool p2l_warp_p(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (D.p != P) return false;
-  if (D.dipole)
-    k_p2l_warp<P, true><<<(n + 3) / 4, 128, 0, s>>>(D, boxes, n);
-  else
-    k_p2l_warp<P, false><<<(n + 3) / 4, 128, 0, s>>>(D, boxes, n);
-  return true;
-}
-
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
-  // warp-per-box variant measured slower at config 1 (20 vs 12 ms): opt-in only
-  static const bool warp = std::getenv("QBXG_P2L_WARP") != nullptr;
-  if (warp && (p2l_warp_p<4>(D, boxes, n, s) || p2l_warp_p<8>(D, boxes, n, s) || p2l_warp_p<10>(D, boxes, n, s) ||
-                  p2l_warp_p<12>(D, boxes, n, s) || p2l_warp_p<15>(D, boxes, n, s) || p2l_warp_p<20>(D, boxes, n, s)))
-    return 1;
+  static const bool legacy = std::getenv("QBXG_P2L_LEGACY") != nullptr;
+  if (!legacy) {
+#define QBXG_P2L3(PP)                                           \
+  if (D.p == PP) {                                              \
+    if (D.dipole)                                               \
+      k_p2l3<PP, true><<<n, 128, 0, s>>>(D, boxes);             \
+    else                                                        \
+      k_p2l3<PP, false><<<n, 128, 0, s>>>(D, boxes);            \
+    return 1;                                                   \
+  }
+    QBXG_P2L3(4)
+    QBXG_P2L3(8)
+    QBXG_P2L3(10)
+    QBXG_P2L3(12)
+    QBXG_P2L3(15)
+#undef QBXG_P2L3
+  }
   const size_t smem = kP2LBatch * hsize(D.p + 1) * sizeof(double2);
   k_p2l<<<n, block_for(D.kp), smem, s>>>(D, boxes);
   return 1;

@@ -129,6 +129,12 @@ struct PairPlan {
   std::vector<PairChunk> chunks;
 };
 int launch_m2qbxl_pairs(const DevData& D, const PairPlan& P, cudaStream_t s);
+// L2QBXL over host-built CTA descriptors (first item, count): <= kL3Threads
+// consecutive centres from <= kL3Boxes boxes, box tables staged in shared memory.
+constexpr int kL3Threads = 128;
+constexpr int kL3Boxes = 8;
+int launch_l2qbxl3(const DevData& D, const int* items, const int2* ctas, int n_ctas, const int* ctr_box,
+                   cudaStream_t s);
 // flat thread-per-centre variant: items = sorted centre indices, ctr_box = owner box
 int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s);
 
