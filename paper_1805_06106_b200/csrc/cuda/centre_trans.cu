@@ -669,6 +669,150 @@ void l2qbxl3_q(const DevData& D, const int* items, const int2* ctas, int n_ctas,
   k_l2qbxl3<Q><<<n_ctas, kL3Threads, smem, s>>>(D, items, ctas, ctr_box);
 }
 
+// M2QBXL over (centre, List-3-far box) pairs in box-major order: a CTA takes up
+// to kW3Threads pairs drawn from at most kW3Boxes source boxes; each box's
+// multipole is staged once as a zero-padded table T(j, k), j in [-q, p+q],
+// |k| <= j + 2q, so that with I_N^K streamed from a register recurrence
+//   L~_c(n,m) = (r/h)^n (1/h) (-1)^{n+m} sum_{N,K} [T(N-n, K+m) I_N^K + T(N-n, m-K) I_N^{-K}]
+// runs without range predicates or global loads.  Each thread writes its pair's
+// staging row; k_pair_reduce sums a centre's rows in list order as before.
+template <int Q>
+__device__ __forceinline__ int w3_idx(int j, int k, int P) {
+  const int r = j + Q;
+  return r * r + 2 * Q * r + r + Q + k;
+}
+
+template <int Q>
+__global__ void __launch_bounds__(kW3Threads) k_m2qbxl3(DevData D, const int2* __restrict__ pairs,
+                                                        const int* __restrict__ perm,
+                                                        const int2* __restrict__ ctas,
+                                                        double2* __restrict__ temp) {
+  constexpr int KQ = hsize(Q);
+  extern __shared__ double2 s_tab[];
+  __shared__ int s_box[kW3Boxes];
+  __shared__ int s_wcount[kW3Threads / 32];
+  const int P = D.p, NR = P + 2 * Q + 1, TS = NR * (NR + 2 * Q);
+  const int2 cta = ctas[blockIdx.x];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const bool active = t < cta.y;
+  int pi = -1, d = -1, prevd = -2, cs = 0;
+  if (active) {
+    pi = perm[cta.x + t];
+    const int2 pr = pairs[pi];
+    cs = pr.x;
+    d = pr.y;
+    if (t > 0) prevd = pairs[perm[cta.x + t - 1]].y;
+  }
+  const bool head = active && d != prevd;
+  const unsigned bal = __ballot_sync(0xffffffffu, head);
+  if (lane == 0) s_wcount[w] = __popc(bal);
+  __syncthreads();
+  int base = 0, nbox = 0;
+#pragma unroll
+  for (int i = 0; i < kW3Threads / 32; ++i) {
+    base += i < w ? s_wcount[i] : 0;
+    nbox += s_wcount[i];
+  }
+  const int slot = base + __popc(bal & ((2u << lane) - 1u)) - 1;
+  if (head) s_box[slot] = d;
+  __syncthreads();
+  for (int e = t; e < nbox * TS; e += kW3Threads) {
+    const int sb = e / TS, o = e - sb * TS;
+    // o = r^2 + 2 Q r + (r + Q) + k, k in [-(r + Q), r + Q]
+    int r = int(sqrt(double(o + Q * Q))) - Q;
+    while (r > 0 && r * r + 2 * Q * r > o) --r;
+    while ((r + 1) * (r + 1) + 2 * Q * (r + 1) <= o) ++r;
+    const int j = r - Q, k = o - (r * r + 2 * Q * r) - (r + Q);
+    double2 v = make_double2(0.0, 0.0);
+    if (j >= 0 && j <= P && k >= -j && k <= j) {
+      const double2 h = D.M[size_t(s_box[sb]) * D.kp + hidx(j, k < 0 ? -k : k)];
+      v = k >= 0 ? h : ((k & 1) ? make_double2(-h.x, h.y) : make_double2(h.x, -h.y));
+    }
+    s_tab[e] = v;
+  }
+  __syncthreads();
+  if (!active) return;
+  const double2* __restrict__ tb = s_tab + slot * TS;
+  const double4 bd = D.box[d];
+  const double ih = 1.0 / bd.w;
+  const double4 c = D.ctr[cs];
+  const double x = (c.x - bd.x) * ih, y = (c.y - bd.y) * ih, z = (c.z - bd.z) * ih;
+  const double r2 = x * x + y * y + z * z;
+  const double rs = rsqrt(r2);
+  const double ir2 = rs * rs;
+  double ax[KQ], ay[KQ];
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
+  const int NN = P + Q;
+  double2 diag = make_double2(rs, 0.0);
+  for (int K = 0; K <= NN; ++K) {
+    if (K > 0) {
+      const double f = (2 * K - 1) * ir2;
+      diag = make_double2((diag.x * x - diag.y * y) * f, (diag.x * y + diag.y * x) * f);
+    }
+    const double sg = (K & 1) ? -1.0 : 1.0;
+    double2 ra = make_double2(0.0, 0.0), rb = diag;
+    for (int N = K; N <= NN; ++N) {
+      double2 cur;
+      if (N == K) {
+        cur = diag;
+      } else if (N == K + 1) {
+        const double f = (2 * K + 1) * z * ir2;
+        cur = make_double2(f * diag.x, f * diag.y);
+      } else {
+        const double c1 = (2 * N - 1) * z;
+        const double c2 = double((N - 1 + K) * (N - 1 - K));
+        cur = make_double2((c1 * rb.x - c2 * ra.x) * ir2, (c1 * rb.y - c2 * ra.y) * ir2);
+      }
+      if (N > K) {
+        ra = rb;
+        rb = cur;
+      }
+      const double2 cm = make_double2(sg * cur.x, -sg * cur.y);  // I_N^{-K}
+#pragma unroll
+      for (int n = 0; n <= Q; ++n) {
+        const double2* __restrict__ row = tb + w3_idx<Q>(N - n, 0, P);
+#pragma unroll
+        for (int m = 0; m <= n; ++m) {
+          const int id = hidx(n, m);
+          const double2 a1 = row[K + m];
+          ax[id] = fma(a1.x, cur.x, fma(-a1.y, cur.y, ax[id]));
+          ay[id] = fma(a1.x, cur.y, fma(a1.y, cur.x, ay[id]));
+          if (K > 0) {
+            const double2 a2 = row[m - K];
+            ax[id] = fma(a2.x, cm.x, fma(-a2.y, cm.y, ax[id]));
+            ay[id] = fma(a2.x, cm.y, fma(a2.y, cm.x, ay[id]));
+          }
+        }
+      }
+    }
+  }
+  double f = ih;
+  const double rh = c.w * ih;
+  double2* out = temp + size_t(pi) * KQ;
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) {
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      const double sgn = ((n + m) & 1) ? -f : f;
+      out[hidx(n, m)] = make_double2(sgn * ax[hidx(n, m)], sgn * ay[hidx(n, m)]);
+    }
+    f *= rh;
+  }
+}
+
+template <int Q>
+void w3_q(const DevData& D, const PairChunk& C, double2* temp, cudaStream_t s) {
+  const int NR = D.p + 2 * Q + 1;
+  const size_t smem = size_t(kW3Boxes) * NR * (NR + 2 * Q) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2qbxl3<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_m2qbxl3<Q><<<C.n_ctas, kW3Threads, smem, s>>>(D, C.pairs, C.perm, C.ctas, temp);
+}
+
 template <int Q>
 void flat_q(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s) {
   const size_t smem = size_t(kFT) * (D.p + D.q + 1) * sizeof(double2);
@@ -744,7 +888,20 @@ int launch_m2qbxl_pairs(const DevData& D, const PairPlan& P, cudaStream_t s) {
   int k = 0;
   for (const PairChunk& C : P.chunks) {
     if (C.n_pairs == 0) continue;
-    switch (D.q) {
+    if (P.box_major) {
+      switch (D.q) {
+        case 0: w3_q<0>(D, C, P.temp, s); break;
+        case 1: w3_q<1>(D, C, P.temp, s); break;
+        case 2: w3_q<2>(D, C, P.temp, s); break;
+        case 3: w3_q<3>(D, C, P.temp, s); break;
+        case 4: w3_q<4>(D, C, P.temp, s); break;
+        case 5: w3_q<5>(D, C, P.temp, s); break;
+        case 6: w3_q<6>(D, C, P.temp, s); break;
+        case 7: w3_q<7>(D, C, P.temp, s); break;
+        case 8: w3_q<8>(D, C, P.temp, s); break;
+        default: return -1;
+      }
+    } else switch (D.q) {
       case 0: pair_q<0>(D, C.pairs, C.n_pairs, P.temp, s); break;
       case 1: pair_q<1>(D, C.pairs, C.n_pairs, P.temp, s); break;
       case 2: pair_q<2>(D, C.pairs, C.n_pairs, P.temp, s); break;

@@ -624,6 +624,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
     if (const char* m = std::getenv("QBXG_SHIFT_MODE")) H.shift_mode = std::atoi(m);
     if (const char* m = std::getenv("QBXG_L2Q_MODE")) H.l2q_mode = std::atoi(m);
+    if (const char* m = std::getenv("QBXG_WFAR_MODE")) H.wpairs.box_major = std::atoi(m) != 0;
     // (centre, W_far box) pairs, centre-major, chunked to bound the staging buffer
     {
       const int64_t cap_pairs = int64_t(1) << 24;
@@ -638,6 +639,30 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
         C.n_centres = int(centres.size());
         starts.push_back(int(total));
         C.pairs = dupload(O, pairs, s);
+        {
+          std::vector<int> perm(pairs.size());
+          for (size_t i = 0; i < perm.size(); ++i) perm[i] = int(i);
+          std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return pairs[a].y < pairs[b].y; });
+          std::vector<int2> ctas;
+          size_t i = 0;
+          while (i < perm.size()) {
+            const size_t first = i;
+            int nbx = 0, last = -1;
+            while (i < perm.size() && i - first < size_t(dev::kW3Threads)) {
+              const int bx = pairs[perm[i]].y;
+              if (bx != last) {
+                if (nbx == dev::kW3Boxes) break;
+                ++nbx;
+                last = bx;
+              }
+              ++i;
+            }
+            ctas.push_back(make_int2(int(first), int(i - first)));
+          }
+          C.perm = dupload(O, perm, s);
+          C.ctas = dupload(O, ctas, s);
+          C.n_ctas = int(ctas.size());
+        }
         C.centres = dupload(O, centres, s);
         C.starts = dupload(O, starts, s);
         H.wpairs.chunks.push_back(C);

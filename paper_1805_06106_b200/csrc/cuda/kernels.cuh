@@ -123,8 +123,14 @@ struct PairChunk {
   int n_centres = 0;
   int* centres = nullptr;  // sorted centre ids of the chunk
   int* starts = nullptr;   // n_centres + 1 global pair offsets
+  int* perm = nullptr;     // chunk pair indices in source-box order (stable)
+  int2* ctas = nullptr;    // box-major CTA descriptors (first perm index, count)
+  int n_ctas = 0;
 };
+constexpr int kW3Threads = 128;
+constexpr int kW3Boxes = 4;
 struct PairPlan {
+  bool box_major = true;    // staged-table kernel (k_m2qbxl3); false: thread per pair from global
   double2* temp = nullptr;  // max chunk pairs x kq
   std::vector<PairChunk> chunks;
 };
