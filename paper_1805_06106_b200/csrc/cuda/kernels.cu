@@ -265,9 +265,13 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
 }
 
 // P2QBXL: L~_c += (1/r)[w conj(I(u)) + conj(mu . grad I(u)) / r], u = (s - c)/r   (Eq. (8))
-template <int Q, bool DIP>
+// GEN: S = floor(128 / n_centres) slices per centre (not only powers of two) so
+// up to ~all 128 lanes are busy; the slices are then summed through shared
+// memory in slice order (deterministic) instead of by width-S shuffles.
+template <int Q, bool DIP, int U, bool GEN>
 __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int* __restrict__ boxes) {
   constexpr int KQ = hsize(Q);
+  extern __shared__ double s_part[];  // GEN: 2 KQ x kNearThreads partial sums
   __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
   __shared__ double4 s_src[kNearChunk];
   __shared__ double4 s_mu[DIP ? kNearChunk : 1];
@@ -277,7 +281,11 @@ __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int*
   for (int cc = 0; cc < nctr; cc += kNearThreads) {
     const int ncc = min(kNearThreads, nctr - cc);
     int S = 1;
-    while (S * 2 * ncc <= kNearThreads && S < 32) S *= 2;
+    if (GEN) {
+      S = kNearThreads / ncc;
+    } else {
+      while (S * 2 * ncc <= kNearThreads && S < 32) S *= 2;
+    }
     const int ci = threadIdx.x / S, sl = threadIdx.x % S;
     const bool active = ci < ncc;
     double4 c = make_double4(0, 0, 0, 1);
@@ -300,24 +308,52 @@ __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int*
         }
         __syncthreads();
         if (active) {
-          for (int j = sl; j < nch; j += S) {
-            near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+          int j = sl;
+          if (U == 2) {  // two independent pairs in flight per iteration (ILP)
+            for (; j + S < nch; j += 2 * S) {
+              near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+              near_pair<Q, DIP>(s_src[j + S], DIP ? s_mu[j + S] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+            }
           }
+          for (; j < nch; j += S)
+            near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
         }
       }
     }
-    // reduce over the S slices of each centre (contiguous lanes, S <= 32)
-    for (int off = S >> 1; off > 0; off >>= 1) {
+    if (GEN) {
+      __syncthreads();
 #pragma unroll
       for (int i = 0; i < KQ; ++i) {
-        ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], off, S);
-        ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], off, S);
+        s_part[(2 * i) * kNearThreads + threadIdx.x] = ax[i];
+        s_part[(2 * i + 1) * kNearThreads + threadIdx.x] = ay[i];
       }
-    }
-    if (active && sl == 0) {
-      double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
+      __syncthreads();
+      if (active && sl == 0) {
+        double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
+        for (int i = 0; i < KQ; ++i) {
+          double sx = 0, sy = 0;
+          for (int k = 0; k < S; ++k) {
+            sx += s_part[(2 * i) * kNearThreads + threadIdx.x + k];
+            sy += s_part[(2 * i + 1) * kNearThreads + threadIdx.x + k];
+          }
+          out[i] = make_double2(sx * ir, sy * ir);
+        }
+      }
+      __syncthreads();
+    } else {
+      // reduce over the S slices of each centre (contiguous lanes, S <= 32)
+      for (int off = S >> 1; off > 0; off >>= 1) {
 #pragma unroll
-      for (int i = 0; i < KQ; ++i) out[i] = make_double2(ax[i] * ir, ay[i] * ir);
+        for (int i = 0; i < KQ; ++i) {
+          ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], off, S);
+          ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], off, S);
+        }
+      }
+      if (active && sl == 0) {
+        double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) out[i] = make_double2(ax[i] * ir, ay[i] * ir);
+      }
     }
   }
 }
@@ -1068,10 +1104,35 @@ __global__ void __launch_bounds__(256) k_direct_sum(int ns, const double4* __res
 
 template <int Q>
 void near_qbx_q(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (D.dipole)
-    k_near_qbx<Q, true><<<n, kNearThreads, 0, s>>>(D, boxes);
-  else
-    k_near_qbx<Q, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+  // QBXG_NEAR_MODE: 2 (default) generic slice count, 1 power-of-two slices + 2 pairs
+  // in flight, 0 power-of-two slices, one pair at a time
+  static const int mode = [] {
+    const char* e = std::getenv("QBXG_NEAR_MODE");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (mode == 2) {
+    const size_t smem = size_t(2) * hsize(Q) * kNearThreads * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_near_qbx<Q, true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_near_qbx<Q, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = true;
+    }
+    if (D.dipole)
+      k_near_qbx<Q, true, 2, true><<<n, kNearThreads, smem, s>>>(D, boxes);
+    else
+      k_near_qbx<Q, false, 2, true><<<n, kNearThreads, smem, s>>>(D, boxes);
+  } else if (mode == 1) {
+    if (D.dipole)
+      k_near_qbx<Q, true, 2, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+    else
+      k_near_qbx<Q, false, 2, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+  } else {
+    if (D.dipole)
+      k_near_qbx<Q, true, 1, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+    else
+      k_near_qbx<Q, false, 1, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+  }
 }
 
 int block_for(int k) { return k <= 128 ? 128 : 256; }
