@@ -300,6 +300,9 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     // dense is the default: the rotation kernels are correct (parity-tested) but
     // latency-bound so far (116 ms vs 84 ms at config 1); opt in with QBXG_M2L_MODE=rot
     P.rot = (mode && std::string(mode) == "rot") && dev::m2l_rot_smem(p, 16) <= 220 * 1024;
+    // split (block-diagonal after an azimuthal rotation) is the default where its
+    // padded block fits the kernel (p <= 20); QBXG_M2L_MODE=dense keeps the full matrix
+    P.split = !P.rot && !(mode && std::string(mode) == "dense") && dev::split_nh(p) <= 240;
   }
   if (P.rot) {
     if (!std::getenv("QBXG_M2L_BN")) P.bn = 16;
@@ -316,6 +319,18 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     P.rotB = dupload(O, rb, s);
     P.rho_op = dupload(O, rho, s);
     QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
+  } else if (P.split) {
+    const int NH = dev::split_nh(p);
+    P.sops = dalloc<double>(O, size_t(P.n_ops) * 2 * NH * NH);
+    P.cs = dalloc<double2>(O, size_t(P.n_ops) * (p + 1));
+    {
+      std::vector<int> eo(nent);
+      for (int64_t e = 0; e < nent; ++e) eo[e] = slot_to_op[slot[e]];
+      P.ent_op = dupload(O, eo, s);
+      QCK(cudaStreamSynchronize(s));
+    }
+    dev::launch_m2l_ops_split(P, p, d_used, s);
+    QCK(cudaGetLastError());
   } else {
     P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
     dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
@@ -325,7 +340,8 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   // chunking by staging-buffer capacity
   size_t free_b = 0, total_b = 0;
   QCK(cudaMemGetInfo(&free_b, &total_b));
-  const size_t row_bytes = size_t(P.KRp) * sizeof(double);
+  P.srow = P.split ? std::max(P.KRp, 2 * dev::split_nh(p)) : P.KRp;
+  const size_t row_bytes = size_t(P.srow) * sizeof(double);
   size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
   int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);
   if (const char* env = std::getenv("QBXG_M2L_CHUNK_ENTRIES")) cap = std::max<int64_t>(64, std::atoll(env));
@@ -358,7 +374,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
         }
       std::vector<int4> tiles;
       {
-        const int64_t tw = P.rot ? dev::kRotSuper : P.bn;
+        const int64_t tw = P.rot ? dev::kRotSuper : P.split ? dev::split_tile_cols() : P.bn;
         for (int o = 0; o < P.n_ops; ++o)
           for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
             tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), 0));
@@ -375,7 +391,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     }
     b0 = b1;
   }
-  P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.KRp);
+  P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.srow);
 }
 
 void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device,

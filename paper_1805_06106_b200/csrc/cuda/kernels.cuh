@@ -71,6 +71,12 @@ struct M2LPlan {
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
   double* temp = nullptr;      // staging: max chunk entries x KRp
   std::vector<M2LChunk> chunks;
+  // azimuthally split variant (default): two real hsize(p) blocks per offset
+  bool split = false;
+  double* sops = nullptr;      // n_ops x 2NH x NH (Re block rows, then Im block rows)
+  double2* cs = nullptr;       // n_ops x (p+1): (cos k alpha, sin k alpha)
+  int* ent_op = nullptr;       // operator index of every List-2 CSR entry
+  int srow = 0;                // staging row length (doubles): KRp, or 2 NH for split
   // rotation (point-and-shoot) variant, m2l_rot.cu
   bool rot = false;
   double* rotF = nullptr;      // n_ops x rot_stride: multipole rotation blocks (v -> +z)
@@ -105,6 +111,9 @@ int launch_shift_ops(int mode, int p, int KR, int KRp, const int4* rdof, double*
 int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops, double2* X, int kp, bool accumulate,
                        cudaStream_t s);
 int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
+int split_nh(int p);  // padded block size of the split M2L (multiple of 48)
+int split_tile_cols();  // columns per split-M2L tile
+int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s);
 
 // Box expansion -> centre locals as DMMA GEMMs (centre_gemm.cu); items are
 // (box, first centre offset) chunks of up to 16 centres.

@@ -245,25 +245,271 @@ __global__ void __launch_bounds__(256, BN == 32 ? 2 : 1) k_m2l_gemm(const double
       const int c = j * 8 + (lane & 3) * 2 + h;
       if (c >= tile.z) continue;
       const int pos = col_pos[tile.y + c];
-      const double sc = col_scale[tile.y + c];
+      // no fp64 arithmetic here: it would queue behind the co-resident CTA's DMMAs
+      // (shared pipe); the 1/|b| scale is applied once per target box in the reduce
       double* out = temp + size_t(pos) * KRp;
 #pragma unroll
-      for (int i = 0; i < MT; ++i) out[row_w + i * 8 + (lane >> 2)] = sc * acc[i][j][h];
+      for (int i = 0; i < MT; ++i) out[row_w + i * 8 + (lane >> 2)] = acc[i][j][h];
     }
   }
+}
+
+// ---- azimuthally split M2L ------------------------------------------------
+// Rotating the frame about z by alpha = atan2(dy, dx) puts the offset in the
+// xz-plane, where I_N^K(v') is real.  With M' = M e^{i k alpha} and
+// L = L' e^{-i m alpha} (both diagonal per coefficient) the M2L operator is then
+// block diagonal in (Re, Im):
+//   Re L'(n,m) = sum_{j,k>=0} s [I_{j+n}^{k-m} + (k>0)(-1)^k I_{j+n}^{-k-m}] Re M'(j,k)
+//   Im L'(n,m) = sum_{j,k>=1} s [I_{j+n}^{k-m} -       (-1)^k I_{j+n}^{-k-m}] Im M'(j,k)
+// with s = (-1)^{n+m}: two hsize(p) x hsize(p) real blocks (2 x 144^2 padded at
+// p = 15) instead of one (p+1)^2 x (p+1)^2 block (256^2) -- 0.63x the DMMA work.
+// Rows / columns in half-table order q = hidx(n, m), padded to NH (multiple of 48).
+__device__ __forceinline__ void q_nm(int q, int& n, int& m) {
+  n = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
+  while (hidx(n + 1, 0) <= q) ++n;
+  while (hidx(n, 0) > q) --n;
+  m = q - hidx(n, 0);
+}
+
+__global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, const int* __restrict__ used_slot,
+                                                       double* __restrict__ ops, double2* __restrict__ cs) {
+  extern __shared__ double2 sI[];  // hsize(2p)
+  const int o = blockIdx.x;
+  const int slot = used_slot[o];
+  const int dx = slot / 121 - 5, dy = (slot / 11) % 11 - 5, dz = slot % 11 - 5;
+  const int P2 = 2 * p, NR = hsize(p);
+  const double rho = sqrt(double(dx * dx + dy * dy));
+  const double alpha = (dx == 0 && dy == 0) ? 0.0 : atan2(double(dy), double(dx));
+  if (threadIdx.x <= P2) {
+    double2 col[kMaxOrder + 1];
+    irregular_column(2.0 * rho, 0.0, 2.0 * dz, threadIdx.x, P2, col);
+    for (int n = threadIdx.x; n <= P2; ++n) sI[hidx(n, threadIdx.x)] = col[n - threadIdx.x];
+  }
+  if (threadIdx.x <= p) {
+    double sn, cn;
+    sincos(threadIdx.x * alpha, &sn, &cn);
+    cs[size_t(o) * (p + 1) + threadIdx.x] = make_double2(cn, sn);
+  }
+  __syncthreads();
+  double* T = ops + size_t(o) * 2 * NH * NH;
+  for (int idx = threadIdx.x; idx < 2 * NH * NH; idx += blockDim.x) {
+    const int ro = idx / NH, qi = idx % NH;
+    const bool im = ro >= NH;
+    const int qo = im ? ro - NH : ro;
+    double v = 0.0;
+    if (qo < NR && qi < NR) {
+      int n, m, j, k;
+      q_nm(qo, n, m);
+      q_nm(qi, j, k);
+      const double sg = ((n + m) & 1) ? -1.0 : 1.0;
+      const double a = hget(sI, j + n, k - m).x;
+      const double b = k > 0 ? ((k & 1) ? -1.0 : 1.0) * hget(sI, j + n, -k - m).x : 0.0;
+      if (!im)
+        v = sg * (a + b);
+      else if (m > 0 && k > 0)
+        v = sg * (a - b);
+    }
+    T[idx] = v;
+  }
+}
+
+// One CTA: one offset, up to BN pairs; NW warps: the first half on the Re
+// block, the second half on the Im block, NH/(NW/2) rows each; K chunks of 16
+// double-buffered (operator rows by cp.async, rotated multipole columns
+// through registers one chunk ahead).  NW = 6, BN = 32 at p = 15 gives 110 KB of
+// shared memory and 2 CTAs per SM.
+template <int NH, int NW, int BN, int KC>
+__global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
+    const double* __restrict__ ops, const double2* __restrict__ cs_all, int p, const int4* __restrict__ tiles,
+    const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ col_scale,
+    const double* __restrict__ M, int kp2, int KRp, double* __restrict__ temp) {
+  constexpr int MT = 2 * NH / (NW * 8);
+  static_assert(MT * 8 * NW == 2 * NH, "rows must split evenly over the warps");
+  constexpr int kBPad = BN + 4, NT = BN / 8, NTH = NW * 32;
+  constexpr int kAP = KC + 4;                     // A row stride: conflict-free fragment reads
+  constexpr int kLd = (KC * BN + NTH - 1) / NTH;  // B elements per thread per chunk
+  extern __shared__ double smem[];
+  double* As = smem;                          // 2 x 2NH x kAP
+  double* Bs = smem + 2 * 2 * NH * kAP;       // 2 buffers x 2 halves x KC x kBPad
+  __shared__ int s_src[BN];
+  __shared__ double2 s_cs[kMaxOrder + 1];
+  __shared__ unsigned char s_n[NH], s_m[NH];
+  const int4 tile = tiles[blockIdx.x];  // (op index, first column, count, -)
+  const double* T = ops + size_t(tile.x) * 2 * NH * NH;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NR = hsize(p);
+  if (tid < BN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+  if (tid <= p) s_cs[tid] = cs_all[size_t(tile.x) * (p + 1) + tid];
+  for (int q = tid; q < NH; q += NTH) {
+    int n = 0, m = 0;
+    if (q < NR) q_nm(q, n, m);
+    s_n[q] = (unsigned char)n;
+    s_m[q] = (unsigned char)m;
+  }
+  __syncthreads();
+
+  auto load_a = [&](int buf, int k0) {
+    double* A = As + buf * 2 * NH * kAP;
+    for (int i = tid; i < 2 * NH * (KC / 2); i += NTH) {
+      const int r = i / (KC / 2), c = (i % (KC / 2)) * 2;
+      cp_async16(A + r * kAP + c, T + size_t(r) * NH + k0 + c);
+    }
+    cp_async_commit();
+  };
+  double bx[kLd], by[kLd];
+  auto fetch_b = [&](int k0) {
+#pragma unroll
+    for (int it = 0; it < kLd; ++it) {
+      const int e = tid + it * NTH;
+      bx[it] = by[it] = 0.0;
+      if (e < KC * BN) {
+        const int kk = e / BN, c = e % BN, q = k0 + kk, src = s_src[c];
+        if (src >= 0 && q < NR) {
+          const double2 v = *reinterpret_cast<const double2*>(M + size_t(src) * kp2 + 2 * q);
+          bx[it] = v.x;
+          by[it] = v.y;
+        }
+      }
+    }
+  };
+  auto store_b = [&](int buf, int k0) {
+    double* Br = Bs + buf * 2 * KC * kBPad;
+    double* Bi = Br + KC * kBPad;
+#pragma unroll
+    for (int it = 0; it < kLd; ++it) {
+      const int e = tid + it * NTH;
+      if (e < KC * BN) {
+        const int kk = e / BN, c = e % BN;
+        const double2 r = s_cs[s_m[k0 + kk]];
+        Br[kk * kBPad + c] = bx[it] * r.x - by[it] * r.y;  // M' = M e^{i k alpha}
+        Bi[kk * kBPad + c] = bx[it] * r.y + by[it] * r.x;
+      }
+    }
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = NH / KC;
+  const bool imw = warp >= NW / 2;
+  const int row_w = (imw ? NH + (warp - NW / 2) * 8 * MT : warp * 8 * MT);
+  load_a(0, 0);
+  fetch_b(0);
+  store_b(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    const int cur = kc & 1;
+    if (kc + 1 < nk) {
+      load_a(cur ^ 1, (kc + 1) * KC);
+      fetch_b((kc + 1) * KC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* A = As + cur * 2 * NH * kAP;
+    const double* B = Bs + cur * 2 * KC * kBPad + (imw ? KC * kBPad : 0);
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double a[MT], b[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = A[(row_w + i * 8 + (lane >> 2)) * kAP + kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = B[(kk + (lane & 3)) * kBPad + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (kc + 1 < nk) store_b(cur ^ 1, (kc + 1) * KC);
+    __syncthreads();
+  }
+  // epilogue: raw L' rows (rotated frame, unscaled) straight from registers into
+  // the staging row (Re block rows 0..NH-1, Im block rows NH..2NH-1), 8
+  // consecutive doubles per lane group.  No fp64 arithmetic here: it would queue
+  // behind the co-resident CTA's DMMAs on the shared fp64 pipe.  The back
+  // rotation and the 1/|b| scale are applied per entry in k_m2l_reduce_split.
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = j * 8 + (lane & 3) * 2 + h;
+      if (c >= tile.z) continue;
+      double* out = temp + size_t(col_pos[tile.y + c]) * (2 * NH);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) out[row_w + i * 8 + (lane >> 2)] = acc[i][j][h];
+    }
+  }
+}
+
+template <int NH, int NW, int BN, int KC>
+void split_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2l_split<NH, NW, BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  const size_t smem = size_t(2 * 2 * NH * (KC + 4) + 2 * 2 * KC * (BN + 4)) * sizeof(double);
+  k_m2l_split<NH, NW, BN, KC><<<C.n_tiles, NW * 32, smem, s>>>(P.sops, P.cs, p, C.tiles, C.col_src, C.col_pos,
+                                                               C.col_scale, X, kp2, P.KRp, P.temp);
+}
+
+
+template <int NH>
+void split_nh_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
+  split_launch<NH, 12, 32, 16>(P, C, X, kp2, p, s);  // 12 warps, 2 CTAs/SM up to NH = 144
 }
 
 // Sum each target box's staged rows in List-2 CSR order and add to L~_b.
 __global__ void __launch_bounds__(256) k_m2l_reduce(const int* __restrict__ boxes, const int64_t* __restrict__ v_starts,
                                                     int64_t chunk_base, int KR, int KRp,
                                                     const int* __restrict__ rmap, const double* __restrict__ temp,
-                                                    double* __restrict__ L, int kp2) {
+                                                    const double4* __restrict__ box, double* __restrict__ L,
+                                                    int kp2) {
   const int b = boxes[blockIdx.x];
   const int64_t a = v_starts[b] - chunk_base, e = v_starts[b + 1] - chunk_base;
+  const double ih = 1.0 / box[b].w;
   for (int r = threadIdx.x; r < KR; r += blockDim.x) {
     double s = 0.0;
     for (int64_t pos = a; pos < e; ++pos) s += temp[pos * KRp + r];
-    L[size_t(b) * kp2 + rmap[r]] += s;
+    L[size_t(b) * kp2 + rmap[r]] += s * ih;
+  }
+}
+
+// Split-M2L reduce: each staging row holds L' of one List-2 entry in its offset's
+// rotated frame (Re block rows 0..NH-1, Im block rows NH..).  Rotate back
+// (L = L' e^{-i m alpha}) and sum in CSR order; scale by 1/|b| once.
+__global__ void __launch_bounds__(160) k_m2l_reduce_split(const int* __restrict__ boxes,
+                                                          const int64_t* __restrict__ v_starts,
+                                                          const int* __restrict__ ent_op,
+                                                          const double2* __restrict__ cs, int p, int NH,
+                                                          int64_t chunk_base, const double* __restrict__ temp,
+                                                          const double4* __restrict__ box, double* __restrict__ L,
+                                                          int kp2) {
+  const int b = boxes[blockIdx.x];
+  const int64_t a = v_starts[b], e = v_starts[b + 1];
+  const int NR = hsize(p);
+  const double ih = 1.0 / box[b].w;
+  for (int q = threadIdx.x; q < NR; q += blockDim.x) {
+    int n, m;
+    q_nm(q, n, m);
+    double sx = 0.0, sy = 0.0;
+    for (int64_t pos = a; pos < e; ++pos) {
+      const double* row = temp + (pos - chunk_base) * (2 * NH);
+      const double re = row[q];
+      if (m == 0) {
+        sx += re;
+      } else {
+        const double im = row[NH + q];
+        const double2 r = cs[size_t(ent_op[pos]) * (p + 1) + m];
+        sx += re * r.x + im * r.y;
+        sy += im * r.x - re * r.y;
+      }
+    }
+    L[size_t(b) * kp2 + 2 * q] += sx * ih;
+    if (m > 0) L[size_t(b) * kp2 + 2 * q + 1] += sy * ih;
   }
 }
 
@@ -345,13 +591,33 @@ int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rd
   return 1;
 }
 
+int split_nh(int p) { return (hsize(p) + 47) / 48 * 48; }
+int split_tile_cols() { return 32; }
+
+int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s) {
+  const size_t smem = hsize(2 * p) * sizeof(double2);
+  cudaFuncSetAttribute(k_m2l_ops_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_m2l_ops_split<<<P.n_ops, 256, smem, s>>>(p, split_nh(p), used_slot, P.sops, P.cs);
+  return 1;
+}
+
 int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
   int k = 0;
   const int kp2 = 2 * D.kp;
   for (int c = 0; c < int(P.chunks.size()); ++c) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
-    if (P.rot) {
+    if (P.split) {
+      const double* X = reinterpret_cast<const double*>(D.M);
+      switch (split_nh(D.p)) {
+        case 48: split_nh_launch<48>(P, C, X, kp2, D.p, s); break;
+        case 96: split_nh_launch<96>(P, C, X, kp2, D.p, s); break;
+        case 144: split_nh_launch<144>(P, C, X, kp2, D.p, s); break;
+        case 192: split_nh_launch<192>(P, C, X, kp2, D.p, s); break;
+        case 240: split_nh_launch<240>(P, C, X, kp2, D.p, s); break;
+        default: return -1;
+      }
+    } else if (P.rot) {
       static const bool v3 = std::getenv("QBXG_M2L_ROTV") && std::getenv("QBXG_M2L_ROTV")[0] == '3';
       if (!v3 && m2l_rot4_ok(D.p))
         launch_m2l_rot4_chunk(P, C, D, s);
@@ -363,8 +629,12 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
                         reinterpret_cast<const double*>(D.M), kp2, P.temp, s, P.bn) < 0) {
       return -1;
     }
-    k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp,
-                                            reinterpret_cast<double*>(D.L), kp2);
+    if (P.split)
+      k_m2l_reduce_split<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, split_nh(D.p), C.base,
+                                                   P.temp, D.box, reinterpret_cast<double*>(D.L), kp2);
+    else
+      k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp, D.box,
+                                              reinterpret_cast<double*>(D.L), kp2);
     k += 2;
   }
   return k;
