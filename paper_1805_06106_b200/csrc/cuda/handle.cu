@@ -321,7 +321,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
   } else if (P.split) {
     const int NH = dev::split_nh(p);
-    P.sops = dalloc<double>(O, size_t(P.n_ops) * 2 * NH * NH);
+    P.sops = dalloc<double>(O, size_t(P.n_ops) * (NH + dev::split_nhi(p, NH)) * NH);
     P.cs = dalloc<double2>(O, size_t(P.n_ops) * (p + 1));
     {
       std::vector<int> eo(nent);
@@ -340,7 +340,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   // chunking by staging-buffer capacity
   size_t free_b = 0, total_b = 0;
   QCK(cudaMemGetInfo(&free_b, &total_b));
-  P.srow = P.split ? std::max(P.KRp, 2 * dev::split_nh(p)) : P.KRp;
+  P.srow = P.KRp;  // split staging rows: Re (hsize(p)) + compacted Im = (p+1)^2 <= KRp
   const size_t row_bytes = size_t(P.srow) * sizeof(double);
   size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
   int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);

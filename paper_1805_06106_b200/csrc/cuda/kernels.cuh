@@ -76,7 +76,7 @@ struct M2LPlan {
   double* sops = nullptr;      // n_ops x 2NH x NH (Re block rows, then Im block rows)
   double2* cs = nullptr;       // n_ops x (p+1): (cos k alpha, sin k alpha)
   int* ent_op = nullptr;       // operator index of every List-2 CSR entry
-  int srow = 0;                // staging row length (doubles): KRp, or 2 NH for split
+  int srow = 0;                // staging row length (doubles)
   // rotation (point-and-shoot) variant, m2l_rot.cu
   bool rot = false;
   double* rotF = nullptr;      // n_ops x rot_stride: multipole rotation blocks (v -> +z)
@@ -113,6 +113,7 @@ int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops,
 int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
 int split_nh(int p);  // padded block size of the split M2L (multiple of 48)
 int split_tile_cols();  // columns per split-M2L tile
+int split_nhi(int p, int NH);  // rows of the compacted Im block
 int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s);
 
 // Box expansion -> centre locals as DMMA GEMMs (centre_gemm.cu); items are

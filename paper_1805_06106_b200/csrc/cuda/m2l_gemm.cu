@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(256, BN == 32 ? 2 : 1) k_m2l_gemm(const double
 //   Im L'(n,m) = sum_{j,k>=1} s [I_{j+n}^{k-m} -       (-1)^k I_{j+n}^{-k-m}] Im M'(j,k)
 // with s = (-1)^{n+m}: two hsize(p) x hsize(p) real blocks (2 x 144^2 padded at
 // p = 15) instead of one (p+1)^2 x (p+1)^2 block (256^2) -- 0.63x the DMMA work.
-// Rows / columns in half-table order q = hidx(n, m), padded to NH (multiple of 48).
+// Re block: rows and columns in half-table order q = hidx(n, m), padded to NH
+// (multiple of 48).  Im block: rows in compacted order t = n(n-1)/2 + m - 1 over
+// m >= 1 only (its m = 0 rows vanish), padded to NHI; columns in q order like
+// the Re block, so one gathered multipole column feeds both blocks.
 __device__ __forceinline__ void q_nm(int q, int& n, int& m) {
   n = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
   while (hidx(n + 1, 0) <= q) ++n;
@@ -271,7 +274,14 @@ __device__ __forceinline__ void q_nm(int q, int& n, int& m) {
   m = q - hidx(n, 0);
 }
 
-__global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, const int* __restrict__ used_slot,
+__device__ __forceinline__ void t_nm(int t, int& n, int& m) {
+  n = int((1.0f + sqrtf(1.0f + 8.0f * t)) * 0.5f);
+  while (n * (n - 1) / 2 > t) --n;
+  while ((n + 1) * n / 2 <= t) ++n;
+  m = t - n * (n - 1) / 2 + 1;
+}
+
+__global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, int NHI, const int* __restrict__ used_slot,
                                                        double* __restrict__ ops, double2* __restrict__ cs) {
   extern __shared__ double2 sI[];  // hsize(2p)
   const int o = blockIdx.x;
@@ -291,15 +301,18 @@ __global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, const int*
     cs[size_t(o) * (p + 1) + threadIdx.x] = make_double2(cn, sn);
   }
   __syncthreads();
-  double* T = ops + size_t(o) * 2 * NH * NH;
-  for (int idx = threadIdx.x; idx < 2 * NH * NH; idx += blockDim.x) {
+  double* T = ops + size_t(o) * (NH + NHI) * NH;
+  for (int idx = threadIdx.x; idx < (NH + NHI) * NH; idx += blockDim.x) {
     const int ro = idx / NH, qi = idx % NH;
     const bool im = ro >= NH;
     const int qo = im ? ro - NH : ro;
     double v = 0.0;
-    if (qo < NR && qi < NR) {
+    if (qo < (im ? NR - (p + 1) : NR) && qi < NR) {
       int n, m, j, k;
-      q_nm(qo, n, m);
+      if (im)
+        t_nm(qo, n, m);
+      else
+        q_nm(qo, n, m);
       q_nm(qi, j, k);
       const double sg = ((n + m) & 1) ? -1.0 : 1.0;
       const double a = hget(sI, j + n, k - m).x;
@@ -319,25 +332,27 @@ __global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, const int*
 // through registers one chunk ahead).  NW = 6, BN = 32 at p = 15 gives 110 KB of
 // shared memory and 2 CTAs per SM.
 template <int NH, int NW, int BN, int KC>
-__global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
+__global__ void __launch_bounds__(2 * NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(int NHI,
     const double* __restrict__ ops, const double2* __restrict__ cs_all, int p, const int4* __restrict__ tiles,
     const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ col_scale,
     const double* __restrict__ M, int kp2, int KRp, double* __restrict__ temp) {
-  constexpr int MT = 2 * NH / (NW * 8);
-  static_assert(MT * 8 * NW == 2 * NH, "rows must split evenly over the warps");
-  constexpr int kBPad = BN + 4, NT = BN / 8, NTH = NW * 32;
-  constexpr int kAP = KC + 4;                     // A row stride: conflict-free fragment reads
-  constexpr int kLd = (KC * BN + NTH - 1) / NTH;  // B elements per thread per chunk
+  // NW = warps on the Re block (NH rows); NHI / (8 MT) more warps on the Im block
+  constexpr int MT = NH / (NW * 8);
+  static_assert(MT * 8 * NW == NH, "Re rows must split evenly over the warps");
+  constexpr int kBPad = BN + 4, NT = BN / 8;
+  constexpr int kAP = KC + 4;                   // A row stride: conflict-free fragment reads
+  constexpr int kLd = (KC * BN + 255) / 256;    // B elements per thread per chunk (>= 256 threads)
+  const int NTH = blockDim.x, RA = NH + NHI;    // threads, operator rows
   extern __shared__ double smem[];
-  double* As = smem;                          // 2 x 2NH x kAP
-  double* Bs = smem + 2 * 2 * NH * kAP;       // 2 buffers x 2 halves x KC x kBPad
+  double* As = smem;                          // 2 x RA x kAP
+  double* Bs = smem + 2 * RA * kAP;           // 2 buffers x 2 halves x KC x kBPad
   __shared__ int s_src[BN];
   __shared__ double2 s_cs[kMaxOrder + 1];
   __shared__ unsigned char s_n[NH], s_m[NH];
   const int4 tile = tiles[blockIdx.x];  // (op index, first column, count, -)
-  const double* T = ops + size_t(tile.x) * 2 * NH * NH;
+  const double* T = ops + size_t(tile.x) * RA * NH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NR = hsize(p);
+  const int NR = hsize(p), NI = NR - (p + 1);
   if (tid < BN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
   if (tid <= p) s_cs[tid] = cs_all[size_t(tile.x) * (p + 1) + tid];
   for (int q = tid; q < NH; q += NTH) {
@@ -349,8 +364,8 @@ __global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
   __syncthreads();
 
   auto load_a = [&](int buf, int k0) {
-    double* A = As + buf * 2 * NH * kAP;
-    for (int i = tid; i < 2 * NH * (KC / 2); i += NTH) {
+    double* A = As + buf * RA * kAP;
+    for (int i = tid; i < RA * (KC / 2); i += NTH) {
       const int r = i / (KC / 2), c = (i % (KC / 2)) * 2;
       cp_async16(A + r * kAP + c, T + size_t(r) * NH + k0 + c);
     }
@@ -394,8 +409,8 @@ __global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = NH / KC;
-  const bool imw = warp >= NW / 2;
-  const int row_w = (imw ? NH + (warp - NW / 2) * 8 * MT : warp * 8 * MT);
+  const bool imw = warp >= NW;
+  const int row_w = warp * 8 * MT;  // Re rows [0, NH), Im rows [NH, NH + NHI)
   load_a(0, 0);
   fetch_b(0);
   store_b(0, 0);
@@ -409,7 +424,7 @@ __global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* A = As + cur * 2 * NH * kAP;
+    const double* A = As + cur * RA * kAP;
     const double* B = Bs + cur * 2 * KC * kBPad + (imw ? KC * kBPad : 0);
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
@@ -427,8 +442,8 @@ __global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
     __syncthreads();
   }
   // epilogue: raw L' rows (rotated frame, unscaled) straight from registers into
-  // the staging row (Re block rows 0..NH-1, Im block rows NH..2NH-1), 8
-  // consecutive doubles per lane group.  No fp64 arithmetic here: it would queue
+  // the staging row (Re rows q at [q], Im rows t at [NR + t]: (p+1)^2 doubles),
+  // 8 consecutive doubles per lane group.  No fp64 arithmetic here: it would queue
   // behind the co-resident CTA's DMMAs on the shared fp64 pipe.  The back
   // rotation and the 1/|b| scale are applied per entry in k_m2l_reduce_split.
 #pragma unroll
@@ -437,9 +452,16 @@ __global__ void __launch_bounds__(NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(
     for (int h = 0; h < 2; ++h) {
       const int c = j * 8 + (lane & 3) * 2 + h;
       if (c >= tile.z) continue;
-      double* out = temp + size_t(col_pos[tile.y + c]) * (2 * NH);
+      double* out = temp + size_t(col_pos[tile.y + c]) * KRp;
 #pragma unroll
-      for (int i = 0; i < MT; ++i) out[row_w + i * 8 + (lane >> 2)] = acc[i][j][h];
+      for (int i = 0; i < MT; ++i) {
+        const int r = row_w + i * 8 + (lane >> 2);
+        if (!imw) {
+          if (r < NR) out[r] = acc[i][j][h];
+        } else if (r - NH < NI) {
+          out[NR + r - NH] = acc[i][j][h];
+        }
+      }
     }
   }
 }
@@ -451,15 +473,17 @@ void split_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2,
     cudaFuncSetAttribute(k_m2l_split<NH, NW, BN, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  const size_t smem = size_t(2 * 2 * NH * (KC + 4) + 2 * 2 * KC * (BN + 4)) * sizeof(double);
-  k_m2l_split<NH, NW, BN, KC><<<C.n_tiles, NW * 32, smem, s>>>(P.sops, P.cs, p, C.tiles, C.col_src, C.col_pos,
-                                                               C.col_scale, X, kp2, P.KRp, P.temp);
+  const int NHI = split_nhi(p, NH);
+  const int threads = (NH + NHI) / (NH / NW) * 32;
+  const size_t smem = size_t(2 * (NH + NHI) * (KC + 4) + 2 * 2 * KC * (BN + 4)) * sizeof(double);
+  k_m2l_split<NH, NW, BN, KC><<<C.n_tiles, threads, smem, s>>>(NHI, P.sops, P.cs, p, C.tiles, C.col_src,
+                                                               C.col_pos, C.col_scale, X, kp2, P.KRp, P.temp);
 }
 
 
 template <int NH>
 void split_nh_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
-  split_launch<NH, 12, 32, 16>(P, C, X, kp2, p, s);  // 12 warps, 2 CTAs/SM up to NH = 144
+  split_launch<NH, 6, 32, 16>(P, C, X, kp2, p, s);  // 6 Re warps + Im warps; 2 CTAs/SM up to NH = 144
 }
 
 // Sum each target box's staged rows in List-2 CSR order and add to L~_b.
@@ -484,7 +508,7 @@ __global__ void __launch_bounds__(256) k_m2l_reduce(const int* __restrict__ boxe
 __global__ void __launch_bounds__(160) k_m2l_reduce_split(const int* __restrict__ boxes,
                                                           const int64_t* __restrict__ v_starts,
                                                           const int* __restrict__ ent_op,
-                                                          const double2* __restrict__ cs, int p, int NH,
+                                                          const double2* __restrict__ cs, int p, int KRp,
                                                           int64_t chunk_base, const double* __restrict__ temp,
                                                           const double4* __restrict__ box, double* __restrict__ L,
                                                           int kp2) {
@@ -497,12 +521,12 @@ __global__ void __launch_bounds__(160) k_m2l_reduce_split(const int* __restrict_
     q_nm(q, n, m);
     double sx = 0.0, sy = 0.0;
     for (int64_t pos = a; pos < e; ++pos) {
-      const double* row = temp + (pos - chunk_base) * (2 * NH);
+      const double* row = temp + (pos - chunk_base) * KRp;
       const double re = row[q];
       if (m == 0) {
         sx += re;
       } else {
-        const double im = row[NH + q];
+        const double im = row[NR + n * (n - 1) / 2 + m - 1];
         const double2 r = cs[size_t(ent_op[pos]) * (p + 1) + m];
         sx += re * r.x + im * r.y;
         sy += im * r.x - re * r.y;
@@ -592,12 +616,16 @@ int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rd
 }
 
 int split_nh(int p) { return (hsize(p) + 47) / 48 * 48; }
+int split_nhi(int p, int NH) {  // Im block rows: whole warps of 8 * MT rows (MT = NH / 48)
+  const int rows = 8 * (NH / 48), ni = hsize(p) - (p + 1);
+  return (ni + rows - 1) / rows * rows;
+}
 int split_tile_cols() { return 32; }
 
 int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s) {
   const size_t smem = hsize(2 * p) * sizeof(double2);
   cudaFuncSetAttribute(k_m2l_ops_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_m2l_ops_split<<<P.n_ops, 256, smem, s>>>(p, split_nh(p), used_slot, P.sops, P.cs);
+  k_m2l_ops_split<<<P.n_ops, 256, smem, s>>>(p, split_nh(p), split_nhi(p, split_nh(p)), used_slot, P.sops, P.cs);
   return 1;
 }
 
@@ -630,7 +658,7 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
       return -1;
     }
     if (P.split)
-      k_m2l_reduce_split<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, split_nh(D.p), C.base,
+      k_m2l_reduce_split<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, P.KRp, C.base,
                                                    P.temp, D.box, reinterpret_cast<double*>(D.L), kp2);
     else
       k_m2l_reduce<<<C.n_boxes, 256, 0, s>>>(C.boxes, D.v_starts, C.base, P.KR, P.KRp, P.rmap, P.temp, D.box,
