@@ -466,6 +466,136 @@ __global__ void __launch_bounds__(2 * NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(in
   }
 }
 
+// Barrier-free variant: the whole rotated multipole tile (Re and Im halves,
+// NH rows x BN columns) is gathered, rotated and stored in shared memory once per
+// tile -- the only fp64 CUDA-core work, done while the co-resident CTA keeps the
+// tensor pipe busy -- and every warp then streams its own operator rows from L2
+// straight into registers (each operator element has exactly one consumer warp,
+// so shared memory buys nothing), two k-steps ahead, with no barrier in the K loop.
+template <int NH, int NW, int BN>
+__global__ void __launch_bounds__(2 * NW * 32, NH <= 144 ? 2 : 1) k_m2l_split2(int NHI,
+    const double* __restrict__ ops, const double2* __restrict__ cs_all, int p, const int4* __restrict__ tiles,
+    const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ M, int kp2,
+    int KRp, double* __restrict__ temp) {
+  constexpr int MT = NH / (NW * 8);
+  static_assert(MT * 8 * NW == NH, "Re rows must split evenly over the warps");
+  constexpr int kBPad = BN + 4, NT = BN / 8;
+  constexpr int kSt = 8;  // staging gathers per thread per round (16 measured slower: register cap)
+  const int NTH = blockDim.x, RA = NH + NHI;
+  extern __shared__ double smem[];
+  double* Br = smem;              // NH x kBPad: Re M'
+  double* Bi = smem + NH * kBPad;  // NH x kBPad: Im M'
+  __shared__ int s_src[BN];
+  __shared__ double2 s_cs[kMaxOrder + 1];
+  __shared__ unsigned char s_m[NH];
+  const int4 tile = tiles[blockIdx.x];
+  const double* T = ops + size_t(tile.x) * RA * NH;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NR = hsize(p), NI = NR - (p + 1);
+  if (tid < BN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+  if (tid <= p) s_cs[tid] = cs_all[size_t(tile.x) * (p + 1) + tid];
+  for (int q = tid; q < NH; q += NTH) {
+    int n = int((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while (hidx(n + 1, 0) <= q) ++n;
+    while (hidx(n, 0) > q) --n;
+    s_m[q] = (unsigned char)(q < NR ? q - hidx(n, 0) : 0);
+  }
+  __syncthreads();
+  const bool imw = warp >= NW;
+  const int row_w = warp * 8 * MT;
+  const double* B = imw ? Bi : Br;
+  const double* Arow = T + size_t(row_w + (lane >> 2)) * NH + (lane & 3);
+  const int nks = (NR + 3) / 4;  // k-steps over nonzero K rows
+  // first two operator k-steps in flight while the tile is staged
+  double a0[MT], a1[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    a0[i] = __ldg(Arow + size_t(i * 8) * NH);
+    a1[i] = nks > 1 ? __ldg(Arow + size_t(i * 8) * NH + 4) : 0.0;
+  }
+  // stage M' = M e^{i k alpha}: consecutive threads walk one column's contiguous
+  // half table; kSt gathers in flight per thread before any is used
+  for (int base = 0; base < NH * BN; base += kSt * NTH) {
+    double2 v[kSt];
+#pragma unroll
+    for (int u = 0; u < kSt; ++u) {
+      const int e = base + tid + u * NTH;
+      const int c = e / NH, q = e - c * NH;
+      v[u] = make_double2(0.0, 0.0);
+      if (e < NH * BN && q < NR) {
+        const int src = s_src[c];
+        if (src >= 0) v[u] = *reinterpret_cast<const double2*>(M + size_t(src) * kp2 + 2 * q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSt; ++u) {
+      const int e = base + tid + u * NTH;
+      if (e < NH * BN) {
+        const int c = e / NH, q = e - c * NH;
+        const double2 r = s_cs[s_m[q]];
+        Br[q * kBPad + c] = v[u].x * r.x - v[u].y * r.y;
+        Bi[q * kBPad + c] = v[u].x * r.y + v[u].y * r.x;
+      }
+    }
+  }
+  __syncthreads();
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int ks = 0; ks < nks; ++ks) {
+    double an[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) an[i] = ks + 2 < nks ? __ldg(Arow + size_t(i * 8) * NH + 4 * (ks + 2)) : 0.0;
+    double b[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) b[j] = B[(4 * ks + (lane & 3)) * kBPad + j * 8 + (lane >> 2)];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a0[i], b[j]);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      a0[i] = a1[i];
+      a1[i] = an[i];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = j * 8 + (lane & 3) * 2 + h;
+      if (c >= tile.z) continue;
+      double* out = temp + size_t(col_pos[tile.y + c]) * KRp;
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int r = row_w + i * 8 + (lane >> 2);
+        if (!imw) {
+          if (r < NR) out[r] = acc[i][j][h];
+        } else if (r - NH < NI) {
+          out[NR + r - NH] = acc[i][j][h];
+        }
+      }
+    }
+  }
+}
+
+template <int NH, int NW, int BN>
+void split2_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2l_split2<NH, NW, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  const int NHI = split_nhi(p, NH);
+  const int threads = (NH + NHI) / (NH / NW) * 32;
+  const size_t smem = size_t(2 * NH * (BN + 4)) * sizeof(double);
+  k_m2l_split2<NH, NW, BN><<<C.n_tiles, threads, smem, s>>>(NHI, P.sops, P.cs, p, C.tiles, C.col_src, C.col_pos,
+                                                            X, kp2, P.KRp, P.temp);
+}
+
 template <int NH, int NW, int BN, int KC>
 void split_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
   static bool attr = false;
@@ -483,7 +613,11 @@ void split_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2,
 
 template <int NH>
 void split_nh_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
-  split_launch<NH, 6, 32, 16>(P, C, X, kp2, p, s);  // 6 Re warps + Im warps; 2 CTAs/SM up to NH = 144
+  static const bool v1 = std::getenv("QBXG_SPLIT_V1") != nullptr;
+  if (v1)
+    split_launch<NH, 6, 32, 16>(P, C, X, kp2, p, s);  // 6 Re warps + Im warps; 2 CTAs/SM up to NH = 144
+  else
+    split2_launch<NH, 6, 32>(P, C, X, kp2, p, s);
 }
 
 // Sum each target box's staged rows in List-2 CSR order and add to L~_b.
