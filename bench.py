@@ -64,8 +64,13 @@ def stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
     f["near"] = led["pairs_qbx_near"] * ((26 if dl else 10) * kq + (40 if dl else 30)) + \
         led["pairs_p2p_near"] * (30 if dl else 20)
     b["near"] = n_src * src_b + n_ctr * (32 + 16 * kq) + n_conv * 32
-    # dense real operator on the (p+1)^2 real degrees of freedom, one per offset
-    f["m2l"] = led["entries"]["V"] * 2 * (p + 1) ** 4
+    # default (split) M2L: after the azimuthal rotation the operator is two real blocks,
+    # K_p x K_p (Re) and (K_p-p-1) x (K_p-p-1) (Im, m >= 1); QBXG_M2L_MODE=dense uses
+    # the full real operator on the (p+1)^2 real degrees of freedom
+    if os.environ.get("QBXG_M2L_MODE", "") == "dense":
+        f["m2l"] = led["entries"]["V"] * 2 * (p + 1) ** 4
+    else:
+        f["m2l"] = led["entries"]["V"] * 2 * (kp * kp + (kp - p - 1) ** 2)
     # compulsory: multipoles in + locals out once per box (operators ~0.6 GB amortised)
     b["m2l"] = 2 * 8 * (p + 1) ** 2 * led["n_l2l"]
     f["wfar"] = led["pairs_wfar_centre"] * (8 * kp * kq + 10 * kpq + 30) + led["pairs_wfar_target"] * (10 * kp + 30)
@@ -297,15 +302,14 @@ def run_ours(args, rank, world, local_rank):
     dom = max(stages, key=lambda k: stages[k]["ms"])
     d = stages[dom]
     traffic, traffic_note = None, None
-    tp = os.path.join(HERE, "profiles", "r01_ncu_m2l.json")
-    if dom == "m2l" and os.path.exists(tp) and not args.small:
+    tp = os.path.join(HERE, "profiles", f"r01_ncu_{dom}.json")
+    if os.path.exists(tp) and not args.small:
         with open(tp) as fh:
             t = json.load(fh)
-        # one ncu --set full capture of the M2L GEMM launch (chunk 1 of 2); bytes per launch
+        # one ncu --set full capture of the stage's main kernel; bytes per launch
         traffic = (t["dram_read_GB"] + t["dram_write_GB"]) * 1e9
-        traffic_note = (f"bytes per launch of {t['kernel']} (profiles/r01_ncu_m2l.json); dominated by the "
-                        "2 KB/entry staging rows of the deterministic CSR reduction")
-    roofline = {"bound": "fp64", "kernel": dom, "achieved": d["tflops"],
+        traffic_note = f"dram bytes of one launch of {t['kernel']} ({os.path.relpath(tp, HERE)}); {t.get('note', '')}"
+    roofline = {"bound": "tensor" if dom == "m2l" else "fp64", "kernel": dom, "achieved": d["tflops"],
                 "peak": round(peak_dmma if dom == "m2l" else peak, 3), "unit": "TFLOP/s",
                 "frac": d["frac_fp64"], "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "in-run microbenchmarks (qbxg_measure_fp64_peak DFMA = %.1f, qbxg_measure_dmma_peak "
