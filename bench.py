@@ -295,9 +295,10 @@ def run_ours(args, rank, world, local_rank):
             continue
         tf = flops[k] / t / 1e12
         gbs = bytes_[k] / t / 1e9
-        pk = peak_dmma if k == "m2l" else peak  # M2L runs on the fp64 tensor pipe
+        tensor = k in ("m2l", "m2m", "l2l")  # DMMA GEMMs on the fp64 tensor pipe
+        pk = peak_dmma if tensor else peak
         stages[k] = {"ms": round(stage_ms[k], 4), "tflops": round(tf, 3), "frac_fp64": round(tf / pk, 4),
-                     "pipe": "dmma" if k == "m2l" else "dfma",
+                     "pipe": "dmma" if tensor else "dfma",
                      "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4), "flops": flops[k]}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     d = stages[dom]
