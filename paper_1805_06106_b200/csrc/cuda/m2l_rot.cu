@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_m2l_rot(int p, int KR, int KRp, const i
   __syncthreads();
   for (int idx = tid; idx < ncol * KR; idx += 256) {
     const int c = idx / KR, r = idx % KR;
-    temp[size_t(col_pos[c0 + c]) * KRp + r] = col_scale[c0 + c] * Ys[r * SB + c];
+    temp[size_t(col_pos[c0 + c]) * KRp + r] = Ys[r * SB + c];  // 1/|b| applied by the reduce
   }
 }
 
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) k_m2l_rot2(int p, int KR, int KRp, const 
     const int nc = min(BN, ncol - first);
     for (int idx = tid; idx < nc * KR; idx += 256) {
       const int c = idx / KR, r = idx % KR;
-      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = col_scale[c0 + first + c] * Ys[r * SB + c];
+      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = Ys[r * SB + c];  // 1/|b| applied by the reduce
     }
     __syncthreads();
     buf ^= 1;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_m2l_rot3(int p, int KR, int KRp, const 
     const int nc = min(kV3Cols, ncol - first);
     for (int idx = tid; idx < nc * KR; idx += 256) {
       const int c = idx / KR, r = idx % KR;
-      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = col_scale[c0 + first + c] * Ys[r * kV3SB + c];
+      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = Ys[r * kV3SB + c];  // 1/|b| applied by the reduce
     }
     __syncthreads();
     buf ^= 1;
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(256) k_m2l_rot4(int p, int KR, int KRp, const 
     const int nc = min(kV4Cols, ncol - first);
     for (int idx = tid; idx < nc * KR; idx += 256) {
       const int c = idx / KR, r = idx % KR;
-      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = col_scale[c0 + first + c] * Ys[r * kV4SB + c];
+      temp[size_t(col_pos[c0 + first + c]) * KRp + r] = Ys[r * kV4SB + c];  // 1/|b| applied by the reduce
     }
     __syncthreads();
     buf ^= 1;
