@@ -466,6 +466,8 @@ __global__ void __launch_bounds__(2 * NW * 32, NH <= 144 ? 2 : 1) k_m2l_split(in
   }
 }
 
+constexpr int kSplitBN = 32;  // columns per split-M2L tile (40 measured slower: 72 vs 58 ms)
+
 // Barrier-free variant: the whole rotated multipole tile (Re and Im halves,
 // NH rows x BN columns) is gathered, rotated and stored in shared memory once per
 // tile -- the only fp64 CUDA-core work, done while the co-resident CTA keeps the
@@ -617,7 +619,7 @@ void split_nh_launch(const M2LPlan& P, const M2LChunk& C, const double* X, int k
   if (v1)
     split_launch<NH, 6, 32, 16>(P, C, X, kp2, p, s);  // 6 Re warps + Im warps; 2 CTAs/SM up to NH = 144
   else
-    split2_launch<NH, 6, 32>(P, C, X, kp2, p, s);
+    split2_launch<NH, 6, kSplitBN>(P, C, X, kp2, p, s);
 }
 
 // Sum each target box's staged rows in List-2 CSR order and add to L~_b.
@@ -754,7 +756,7 @@ int split_nhi(int p, int NH) {  // Im block rows: whole warps of 8 * MT rows (MT
   const int rows = 8 * (NH / 48), ni = hsize(p) - (p + 1);
   return (ni + rows - 1) / rows * rows;
 }
-int split_tile_cols() { return 32; }
+int split_tile_cols() { return std::getenv("QBXG_SPLIT_V1") ? 32 : kSplitBN; }
 
 int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s) {
   const size_t smem = hsize(2 * p) * sizeof(double2);
