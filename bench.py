@@ -277,6 +277,31 @@ def run_ours(args, rank, world, local_rank):
     # sanity: device-resident and host paths agree bitwise
     same = bool(np.array_equal(pot, d_pot.cpu().numpy()))
 
+    # batched densities (qbxg_apply_batch_device): device time per density
+    batch = None
+    if world == 1 and not args.small:
+        R = 4
+        rng = np.random.default_rng(5)
+        dens = rng.uniform(-1.0, 1.0, (R, g.n_sources))
+        bW = torch.from_numpy(np.stack([g.weights(d) for d in dens])).to(dev)
+        bMU = (torch.from_numpy(np.stack([g.dipoles(d) for d in dens]).reshape(R, -1)).to(dev)
+               if cfg.kernel == 1 else None)
+        bP = torch.empty((R, g.n_targets), dtype=torch.float64, device=dev)
+        bt = []
+        for i in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            eng.apply_batch_device(R, bW.data_ptr(), bMU.data_ptr() if bMU is not None else None, bP.data_ptr(),
+                                   None, stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:
+                bt.append(e0.elapsed_time(e1))
+        bms = float(np.mean(bt)) / R
+        batch = {"n_rhs": R, "ms_per_density": round(bms, 3), "value": units / (bms * 1e-3), "unit": "points/s",
+                 "note": "near field shares one harmonic table per (centre, source) pair between 2 densities"}
+
     # roofline of the dominant kernel, per-stage fractions
     peak = api.measure_fp64_peak(local_rank)
     peak_dmma = api.measure_dmma_peak(local_rank)
@@ -336,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
                            "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"},
                 "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
+                "batch": batch,
                 "cpu_baseline": cpu,
                 "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
                             "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3)},

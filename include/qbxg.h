@@ -274,6 +274,20 @@ int qbxg_exchange_local(qbxg_handle** handles, int32_t n_ranks);
 int qbxg_nccl_unique_id(uint8_t* out128);
 int qbxg_nccl_attach(qbxg_handle* h, const uint8_t* id128);
 
+/* ---- batched densities (repeated applies in iterative
+ * solves) ---------------------------------------------------
+ * n_rhs densities on one handle, arrays rhs-major with a leading batch dimension:
+ * weights [n_rhs][n_sources], dipoles [n_rhs][n_sources][3] (SL+DL), potentials
+ * [n_rhs][n_targets], centre coefficients [n_rhs][n_centers][K_q][2] (or null).
+ * Each density's result equals qbxg_apply on that density up to rounding; the
+ * near field shares one harmonic table per (centre, source) pair between two
+ * densities.  The timings report only QBXG_T_TOTAL and the launch count. */
+int qbxg_apply_batch(qbxg_handle* h, int32_t n_rhs, const double* weights, const double* dipoles,
+                     double* out_target_pot, double* out_center_coeffs_or_null, qbxg_timings* timings);
+int qbxg_apply_batch_device(qbxg_handle* h, int32_t n_rhs, const double* d_weights, const double* d_dipoles,
+                            double* d_out_target_pot, double* d_out_center_coeffs_or_null, void* cuda_stream,
+                            qbxg_timings* timings);
+
 /* ---- near-field P2P, the GPU counterpart of qbx::direct_sum ------------ */
 /* pot[i] = (1/4pi) sum_j [w_j/|x_i-y_j| + m_j.(x_i-y_j)/|x_i-y_j|^3].
  * Returns QBXG_ERR_DOMAIN when a target coincides with a source (message names

@@ -344,6 +344,33 @@ class FmmEngine:
             return pot, c[..., 0] + 1j * c[..., 1]
         return pot
 
+    def apply_batch(self, weights, dipoles=None, want_centers=False):
+        """Several densities at once (leading batch dimension): weights (R, N_S),
+        dipoles (R, N_S, 3); returns potentials (R, N_T) [and centre coefficients
+        (R, N_C, K_q) complex].  Same results as R calls of ``apply``."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        if w.ndim != 2 or w.shape[1] != self.geom.n_sources:
+            raise ValueError("apply_batch: weights must have shape (n_rhs, n_sources)")
+        R = w.shape[0]
+        m = None
+        if dipoles is not None:
+            m = np.ascontiguousarray(dipoles, dtype=np.float64).reshape(R, self.geom.n_sources, 3)
+        pot = np.empty((R, self.geom.n_targets), dtype=np.float64)
+        coeffs = np.empty((R, self.geom.n_centers, self.cfg.kq, 2), dtype=np.float64) if want_centers else None
+        _check(_abi.lib().qbxg_apply_batch(self.handle, R, _ptr(w), _ptr(m), _ptr(pot), _ptr(coeffs),
+                                           C.byref(self.timings)))
+        if want_centers:
+            return pot, coeffs[..., 0] + 1j * coeffs[..., 1]
+        return pot
+
+    def apply_batch_device(self, n_rhs: int, d_weights: int, d_dipoles: int | None, d_pot: int,
+                           d_coeffs: int | None = None, stream: int | None = None):
+        """Device-pointer batch apply (rhs-major arrays, see include/qbxg.h)."""
+        _check(_abi.lib().qbxg_apply_batch_device(self.handle, int(n_rhs), C.c_void_p(d_weights),
+                                                  C.c_void_p(d_dipoles or 0), C.c_void_p(d_pot),
+                                                  C.c_void_p(d_coeffs or 0), C.c_void_p(stream or 0),
+                                                  C.byref(self.timings)))
+
     def apply_device(self, d_weights: int, d_dipoles: int | None, d_pot: int, d_coeffs: int | None = None,
                      stream: int | None = None):
         """Device pointers (ints, e.g. torch tensor.data_ptr()) in original ordering."""

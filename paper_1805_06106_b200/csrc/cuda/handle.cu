@@ -136,6 +136,13 @@ struct Handle {
   double* d_coeffs = nullptr;
   dev::M2LPlan m2l;
   int last_launches = 0;
+  // batched densities (qbxg_apply_batch*): NR-wide near-field buffers, grown on demand
+  int bnr = 0;                   // densities per near-field pass (0: not allocated)
+  double* d_bw = nullptr;        // bnr x ns sorted weights
+  double4* d_bmu = nullptr;      // bnr x ns sorted dipoles
+  double2* d_bLc = nullptr;      // bnr x nc x kq centre locals (near part, then completed in place)
+  int64_t bhost_cap = 0;         // densities the host staging below can hold
+  double *d_bw_in = nullptr, *d_bmu_in = nullptr, *d_bpot = nullptr, *d_bcoeffs = nullptr;
 
   ~Handle() {
     if (stream) cudaStreamSynchronize(stream);
@@ -799,7 +806,7 @@ void exchange_nccl(Handle& H, cudaStream_t s) {
 // phase bit 1: density gather, P2M, M2M of the rank's subtrees.
 // phase bit 2: M2M of straddling boxes, then Stages 3-9 for the rank's boxes.
 void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s,
-                int phase) {
+                int phase, bool near_done = false) {
   dev::DevData& D = H.D;
   if (D.dipole && !d_mu && (phase & 1)) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
   int L = (phase & 1) ? 0 : H.last_launches;
@@ -842,7 +849,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     for (int l = H.nlev - 2; l >= 0; --l)
       chk(dev::launch_shift_level(H.m2l, H.m2m_straddle[l], H.ops_m2m, D.M, D.kp, false, s));
   QCK(cudaEventRecord(ev[3], s));
-  chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  if (!near_done) chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
   if (std::getenv("QBXG_M2L_NAIVE"))
@@ -906,6 +913,57 @@ void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
       nck(n.AllReduce(d_coeffs, d_coeffs, size_t(H.nc) * 2 * H.D.kq, ncclFloat64, ncclSum, comm, s),
           "ncclAllReduce(centre coefficients)");
   }
+}
+
+// R densities (rhs-major device arrays).  Densities go through the near field NR
+// at a time (one harmonic table per pair feeds NR densities); every other stage
+// runs per density on its own completed centre locals.  Results equal R single
+// applies up to rounding.  Sharded handles loop over full applies.
+void batch_apply(Handle& H, int R, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs,
+                 cudaStream_t s) {
+  dev::DevData& D = H.D;
+  const int NR = dev::near_batch_width(D.q);
+  if (H.nranks > 1 || NR < 2 || R < 2) {
+    for (int r = 0; r < R; ++r)
+      full_apply(H, d_w + size_t(r) * H.ns, d_mu ? d_mu + size_t(r) * 3 * H.ns : nullptr, d_pot + size_t(r) * H.nt,
+                 d_coeffs ? d_coeffs + size_t(r) * H.nc * 2 * D.kq : nullptr, s);
+    return;
+  }
+  if (H.bnr < NR) {
+    H.d_bw = dalloc<double>(H.owned, size_t(NR) * H.ns);
+    H.d_bmu = dalloc<double4>(H.owned, size_t(NR) * H.ns);
+    H.d_bLc = dalloc<double2>(H.owned, size_t(NR) * std::max<int64_t>(H.nc, 1) * D.kq);
+    H.bnr = NR;
+  }
+  double2* const lc_single = D.Lc;
+  int L = 0;
+  int r0 = 0;
+  for (; r0 + NR <= R; r0 += NR) {
+    dev::launch_gather_batch(D, int(H.ns), NR, H.d_src_perm, d_w + size_t(r0) * H.ns,
+                             d_mu ? d_mu + size_t(r0) * 3 * H.ns : nullptr, H.d_bw, H.d_bmu, s);
+    if (dev::launch_near_qbx_batch(D, H.d_ctr_boxes, H.n_ctr_boxes, NR, H.d_bw, H.d_bmu, H.ns, H.d_bLc, H.nc, s) < 0)
+      throw InvalidArgument("qbxg_apply_batch: unsupported order");
+    L += 2;
+    for (int k = 0; k < NR; ++k) {
+      const int r = r0 + k;
+      D.Lc = H.d_bLc + size_t(k) * H.nc * D.kq;
+      try {
+        run_device(H, d_w + size_t(r) * H.ns, d_mu ? d_mu + size_t(r) * 3 * H.ns : nullptr, d_pot + size_t(r) * H.nt,
+                   d_coeffs ? d_coeffs + size_t(r) * H.nc * 2 * D.kq : nullptr, s, 3, true);
+      } catch (...) {
+        D.Lc = lc_single;
+        throw;
+      }
+      D.Lc = lc_single;
+      L += H.last_launches;
+    }
+  }
+  for (; r0 < R; ++r0) {
+    full_apply(H, d_w + size_t(r0) * H.ns, d_mu ? d_mu + size_t(r0) * 3 * H.ns : nullptr, d_pot + size_t(r0) * H.nt,
+               d_coeffs ? d_coeffs + size_t(r0) * H.nc * 2 * D.kq : nullptr, s);
+    L += H.last_launches;
+  }
+  H.last_launches = L;
 }
 
 void fill_timings(Handle& H, qbxg_timings* t, bool host_copies, int64_t h2d, int64_t d2h) {
@@ -1110,6 +1168,75 @@ int qbxg_apply(qbxg_handle* hp, const double* weights, const double* dipoles, do
     QCK(cudaEventRecord(H.ev[12], s));
     qbxg::fill_timings(H, timings, true, h2d, d2h);
     QCK(cudaStreamSynchronize(s));
+  });
+}
+
+int qbxg_apply_batch_device(qbxg_handle* hp, int32_t n_rhs, const double* d_weights, const double* d_dipoles,
+                            double* d_out_target_pot, double* d_out_center_coeffs, void* cuda_stream,
+                            qbxg_timings* timings) {
+  return qbxg::guarded([&] {
+    if (!hp || !d_weights || !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_batch_device: null argument");
+    if (n_rhs < 1) throw qbxg::InvalidArgument("qbxg_apply_batch_device: n_rhs must be >= 1");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    if (H.D.dipole && !d_dipoles) throw qbxg::InvalidArgument("qbxg_apply_batch: Laplace SL+DL requires dipole moments");
+    cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
+    QCK(cudaEventRecord(H.ev[11], s));
+    qbxg::batch_apply(H, n_rhs, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s);
+    QCK(cudaEventRecord(H.ev[12], s));
+    QCK(cudaEventSynchronize(H.ev[12]));
+    if (timings) {
+      std::memset(timings, 0, sizeof(*timings));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, H.ev[11], H.ev[12]);
+      timings->ms[QBXG_T_TOTAL] = ms;
+      timings->kernel_launches = H.last_launches;
+    }
+  });
+}
+
+int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, const double* dipoles,
+                     double* out_target_pot, double* out_center_coeffs, qbxg_timings* timings) {
+  return qbxg::guarded([&] {
+    if (!hp || !weights || !out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_batch: null argument");
+    if (n_rhs < 1) throw qbxg::InvalidArgument("qbxg_apply_batch: n_rhs must be >= 1");
+    auto& H = hp->h;
+    QCK(cudaSetDevice(H.device));
+    const bool dip = H.D.dipole;
+    if (dip && !dipoles) throw qbxg::InvalidArgument("qbxg_apply_batch: Laplace SL+DL requires dipole moments");
+    cudaStream_t s = H.stream;
+    if (H.bhost_cap < n_rhs) {  // host-path staging grows to the largest batch seen
+      H.d_bw_in = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * H.ns);
+      H.d_bmu_in = dip ? qbxg::dalloc<double>(H.owned, size_t(n_rhs) * 3 * H.ns) : nullptr;
+      H.d_bpot = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * std::max<int64_t>(H.nt, 1));
+      H.d_bcoeffs = nullptr;
+      H.bhost_cap = n_rhs;
+    }
+    const size_t cbytes = size_t(H.nc) * 2 * H.D.kq * sizeof(double);
+    double* d_coeffs = nullptr;
+    if (out_center_coeffs) d_coeffs = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * std::max<int64_t>(H.nc, 1) * 2 * H.D.kq);
+    QCK(cudaEventRecord(H.ev[11], s));
+    QCK(cudaMemcpyAsync(H.d_bw_in, weights, size_t(n_rhs) * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (dip)
+      QCK(cudaMemcpyAsync(H.d_bmu_in, dipoles, size_t(n_rhs) * 3 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+    qbxg::batch_apply(H, n_rhs, H.d_bw_in, dip ? H.d_bmu_in : nullptr, H.d_bpot, d_coeffs, s);
+    QCK(cudaMemcpyAsync(out_target_pot, H.d_bpot, size_t(n_rhs) * H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (d_coeffs) QCK(cudaMemcpyAsync(out_center_coeffs, d_coeffs, size_t(n_rhs) * cbytes, cudaMemcpyDeviceToHost, s));
+    QCK(cudaEventRecord(H.ev[12], s));
+    QCK(cudaStreamSynchronize(s));
+    if (d_coeffs) {  // per-call buffer: release it now
+      cudaFree(d_coeffs);
+      H.owned.erase(std::find(H.owned.begin(), H.owned.end(), static_cast<void*>(d_coeffs)));
+    }
+    if (timings) {
+      std::memset(timings, 0, sizeof(*timings));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, H.ev[11], H.ev[12]);
+      timings->ms[QBXG_T_TOTAL] = ms;
+      timings->kernel_launches = H.last_launches;
+      timings->h2d_bytes = int64_t(n_rhs) * H.ns * (dip ? 32 : 8);
+      timings->d2h_bytes = int64_t(n_rhs) * H.nt * 8 + (d_coeffs ? int64_t(n_rhs) * int64_t(cbytes) : 0);
+    }
   });
 }
 

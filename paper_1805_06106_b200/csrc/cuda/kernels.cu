@@ -44,6 +44,19 @@ __global__ void k_gather(int ns, const int* __restrict__ perm, const double* __r
   if (smu) smu[i] = make_double4(mu[3 * o], mu[3 * o + 1], mu[3 * o + 2], 0.0);
 }
 
+// Batched densities: weights / dipoles of R right-hand sides into box-sorted order
+// (bw: R x ns, bmu: R x ns), rhs-major like the caller's arrays.
+__global__ void k_gather_batch(int ns, int R, const int* __restrict__ perm, const double* __restrict__ w,
+                               const double* __restrict__ mu, double* __restrict__ bw,
+                               double4* __restrict__ bmu) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(ns) * R) return;
+  const int r = int(t / ns), i = int(t - int64_t(r) * ns);
+  const int64_t o = int64_t(r) * ns + perm[i];
+  bw[t] = w[o];
+  if (bmu) bmu[t] = make_double4(mu[3 * o], mu[3 * o + 1], mu[3 * o + 2], 0.0);
+}
+
 // ---------------------------------------------------------------- P2M (Stage 2)
 // M~_n^m = sum_s w conj(R_n^m(u)) + conj(mu . grad R_n^m(u)) / h,  u = (s - c)/h
 constexpr int kP2MBatch = 16;
@@ -355,6 +368,168 @@ __global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int*
         for (int i = 0; i < KQ; ++i) out[i] = make_double2(ax[i] * ir, ay[i] * ir);
       }
     }
+  }
+}
+
+// Batched P2QBXL: one (centre, source) harmonic table J feeds NR densities.  The
+// per-pair table costs about a third of the pair's fp64 work, so NR = 2 saves ~1/6
+// per density; accumulation order per density is the single-density kernel's.
+template <int Q, bool DIP, int NR>
+__device__ __forceinline__ void near_pair_batch(const double4 x, const double* w, const double4* u, const double4 c,
+                                                const double ir, double (*ax)[hsize(Q)], double (*ay)[hsize(Q)]) {
+  constexpr int KI = hsize(Q + (DIP ? 1 : 0));
+  constexpr int P1 = Q + (DIP ? 1 : 0);
+  const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
+  const double r2 = ux * ux + uy * uy + uz * uz;
+  const double rs = rsqrt(r2);
+  const double ir2 = rs * rs;
+  double2 J[KI];
+#pragma unroll
+  for (int m = 0; m <= P1; ++m) {
+    if (m == 0) {
+      J[0] = make_double2(1.0, 0.0);
+    } else {
+      const double2 d = J[hidx(m - 1, m - 1)];
+      const double f = double(2 * m - 1);
+      J[hidx(m, m)] = make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
+    }
+    if (m + 1 <= P1) {
+      const double f = double(2 * m + 1) * uz;
+      J[hidx(m + 1, m)] = make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
+    }
+#pragma unroll
+    for (int n = m + 2; n <= P1; ++n) {
+      const double zc = double(2 * n - 1) * uz;
+      const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
+      const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
+      J[hidx(n, m)] = make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
+    }
+  }
+  double sc[P1 + 1];
+  sc[0] = rs;
+#pragma unroll
+  for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+#pragma unroll
+    for (int n = 0; n <= Q; ++n) {
+      const double wn = w[r] * sc[n];
+#pragma unroll
+      for (int m = 0; m <= n; ++m) {
+        const int id = hidx(n, m);
+        ax[r][id] = fma(wn, J[id].x, ax[r][id]);
+        ay[r][id] = fma(-wn, J[id].y, ay[r][id]);
+      }
+    }
+    if (DIP) {
+#pragma unroll
+      for (int n = 0; n <= Q; ++n) {
+        const double s1 = sc[n + 1] * ir;
+        const double mz = u[r].z * s1, hx = 0.5 * u[r].x * s1, hy = 0.5 * u[r].y * s1;
+#pragma unroll
+        for (int m = 0; m <= n; ++m) {
+          const int id = hidx(n, m);
+          const double2 i0 = J[hidx(n + 1, m)];
+          const double2 ip = J[hidx(n + 1, m + 1)];
+          double2 im;
+          if (m >= 1) {
+            im = J[hidx(n + 1, m - 1)];
+          } else {
+            const double2 t = J[hidx(n + 1, 1)];
+            im = make_double2(-t.x, t.y);
+          }
+          ax[r][id] = fma(-mz, i0.x, ax[r][id]);
+          ax[r][id] = fma(hx, im.x - ip.x, ax[r][id]);
+          ax[r][id] = fma(-hy, im.y + ip.y, ax[r][id]);
+          ay[r][id] = fma(mz, i0.y, ay[r][id]);
+          ay[r][id] = fma(-hx, im.y - ip.y, ay[r][id]);
+          ay[r][id] = fma(-hy, im.x + ip.x, ay[r][id]);
+        }
+      }
+    }
+  }
+}
+
+template <int Q, bool DIP, int NR>
+__global__ void __launch_bounds__(kNearThreads) k_near_qbx_batch(DevData D, const int* __restrict__ boxes,
+                                                                  const double* __restrict__ bw,
+                                                                  const double4* __restrict__ bmu, int64_t ns,
+                                                                  double2* __restrict__ bLc, int64_t nc) {
+  constexpr int KQ = hsize(Q);
+  extern __shared__ double s_part[];  // 2 KQ x kNearThreads partial sums (one density at a time)
+  __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
+  __shared__ double4 s_src[kNearChunk];
+  __shared__ double s_w[NR][kNearChunk];
+  __shared__ double4 s_mu[DIP ? NR : 1][DIP ? kNearChunk : 1];
+  const int b = boxes[blockIdx.x];
+  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
+  const int64_t sb = D.near_starts[b], se = D.near_starts[b + 1];
+  for (int cc = 0; cc < nctr; cc += kNearThreads) {
+    const int ncc = min(kNearThreads, nctr - cc);
+    const int S = kNearThreads / ncc;
+    const int ci = threadIdx.x / S, sl = threadIdx.x % S;
+    const bool active = ci < ncc;
+    double4 c = make_double4(0, 0, 0, 1);
+    if (active) c = D.ctr[c0 + cc + ci];
+    const double ir = 1.0 / c.w;
+    double ax[NR][KQ], ay[NR][KQ];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) ax[r][i] = ay[r][i] = 0.0;
+    for (int64_t s0 = sb; s0 < se; s0 += kMaxSeg) {
+      const int nseg = int(se - s0 < kMaxSeg ? se - s0 : kMaxSeg);
+      __syncthreads();
+      const int total = load_segments(D.near_seg, s0, nseg, s_start, s_pre);
+      for (int ch = 0; ch < total; ch += kNearChunk) {
+        const int nch = min(kNearChunk, total - ch);
+        __syncthreads();
+        for (int f = threadIdx.x; f < nch; f += kNearThreads) {
+          const int s = seg_source(ch + f, nseg, s_start, s_pre);
+          s_src[f] = D.src[s];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            s_w[r][f] = bw[r * ns + s];
+            if (DIP) s_mu[r][f] = bmu[r * ns + s];
+          }
+        }
+        __syncthreads();
+        if (active) {
+          for (int j = sl; j < nch; j += S) {
+            double w[NR];
+            double4 u[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+              w[r] = s_w[r][j];
+              u[r] = DIP ? s_mu[r][j] : make_double4(0, 0, 0, 0);
+            }
+            near_pair_batch<Q, DIP, NR>(s_src[j], w, u, c, ir, ax, ay);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {  // one density at a time through the reduction buffer
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) {
+        s_part[(2 * i) * kNearThreads + threadIdx.x] = ax[r][i];
+        s_part[(2 * i + 1) * kNearThreads + threadIdx.x] = ay[r][i];
+      }
+      __syncthreads();
+      if (active && sl == 0) {
+        double2* out = bLc + int64_t(r) * nc * KQ + size_t(c0 + cc + ci) * KQ;
+        for (int i = 0; i < KQ; ++i) {
+          double sx = 0, sy = 0;
+          for (int k = 0; k < S; ++k) {
+            sx += s_part[(2 * i) * kNearThreads + threadIdx.x + k];
+            sy += s_part[(2 * i + 1) * kNearThreads + threadIdx.x + k];
+          }
+          out[i] = make_double2(sx * ir, sy * ir);
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1142,6 +1317,50 @@ int block_for(int k) { return k <= 128 ? 128 : 256; }
 int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s) {
   if (ns == 0) return 0;
   k_gather<<<(ns + 255) / 256, 256, 0, s>>>(ns, perm, w, D.dipole ? mu : nullptr, D.src, D.dipole ? D.mu : nullptr);
+  return 1;
+}
+
+int launch_gather_batch(const DevData& D, int ns, int R, const int* perm, const double* w, const double* mu,
+                        double* bw, double4* bmu, cudaStream_t s) {
+  if (ns == 0 || R == 0) return 0;
+  const int64_t n = int64_t(ns) * R;
+  k_gather_batch<<<unsigned((n + 255) / 256), 256, 0, s>>>(ns, R, perm, w, D.dipole ? mu : nullptr, bw,
+                                                           D.dipole ? bmu : nullptr);
+  return 1;
+}
+
+template <int Q, int NR>
+static void near_batch_q(const DevData& D, const int* boxes, int n, const double* bw, const double4* bmu, int64_t ns,
+                         double2* bLc, int64_t nc, cudaStream_t s) {
+  const size_t smem = size_t(2) * hsize(Q) * kNearThreads * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    // dynamic limit = 227 KB minus this kernel's ~31 KB of static staging
+    cudaFuncSetAttribute(k_near_qbx_batch<Q, true, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    cudaFuncSetAttribute(k_near_qbx_batch<Q, false, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    attr = true;
+  }
+  if (D.dipole)
+    k_near_qbx_batch<Q, true, NR><<<n, kNearThreads, smem, s>>>(D, boxes, bw, bmu, ns, bLc, nc);
+  else
+    k_near_qbx_batch<Q, false, NR><<<n, kNearThreads, smem, s>>>(D, boxes, bw, bmu, ns, bLc, nc);
+}
+
+int near_batch_width(int q) { return q <= 5 ? 2 : 1; }
+
+int launch_near_qbx_batch(const DevData& D, const int* boxes, int n, int NR, const double* bw, const double4* bmu,
+                          int64_t ns, double2* bLc, int64_t nc, cudaStream_t s) {
+  if (n == 0) return 0;
+  if (NR != 2) return -1;
+  switch (D.q) {
+    case 0: near_batch_q<0, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    case 1: near_batch_q<1, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    case 2: near_batch_q<2, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    case 3: near_batch_q<3, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    case 4: near_batch_q<4, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    case 5: near_batch_q<5, 2>(D, boxes, n, bw, bmu, ns, bLc, nc, s); break;
+    default: return -1;
+  }
   return 1;
 }
 

@@ -157,6 +157,13 @@ int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_bo
 // launchers (return number of kernels launched)
 int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s);
 int launch_p2m(const DevData& D, const int* boxes, int n, cudaStream_t s);
+// batched densities (R right-hand sides): sorted weights / dipoles, and the
+// near-field P2QBXL for NR = near_batch_width(q) densities per pass
+int launch_gather_batch(const DevData& D, int ns, int R, const int* perm, const double* w, const double* mu,
+                        double* bw, double4* bmu, cudaStream_t s);
+int near_batch_width(int q);
+int launch_near_qbx_batch(const DevData& D, const int* boxes, int n, int NR, const double* bw, const double4* bmu,
+                          int64_t ns, double2* bLc, int64_t nc, cudaStream_t s);
 int launch_m2m(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s);
