@@ -252,6 +252,24 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
+    # per-stage CUDA-event times for the rooflines come from a second block of K steps
+    # with the near field on the main stream: in the overlapped headline run the
+    # near field shares the SMs with M2L/P2L/L2L and per-stage times add contention
+    eng.set_overlap(False)
+    stage_ms = {}
+    torch.cuda.synchronize(dev)
+    es0 = torch.cuda.Event(enable_timing=True)
+    es1 = torch.cuda.Event(enable_timing=True)
+    es0.record(stream)
+    for _ in range(args.steps):
+        step()
+        tm, _, _, _ = eng.last_timings()
+        for k, v in tm.items():
+            stage_ms[k] = stage_ms.get(k, 0.0) + v
+    es1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_seq = es0.elapsed_time(es1) / args.steps
+    eng.set_overlap(True)
     for k in stage_ms:
         stage_ms[k] /= args.steps
     units = g.n_sources + g.n_targets
@@ -340,7 +358,10 @@ def run_ours(args, rank, world, local_rank):
                 "frac": d["frac_fp64"], "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "in-run microbenchmarks (qbxg_measure_fp64_peak DFMA = %.1f, qbxg_measure_dmma_peak "
                                "DMMA = %.1f TFLOP/s); MEASURED_PEAKS.json has no fp64 entry" % (peak, peak_dmma),
-                "algorithmic_flops_per_launch": flops[dom], "share_of_step": round(d["ms"] / ms, 3)}
+                "algorithmic_flops_per_launch": flops[dom], "share_of_step": round(d["ms"] / ms_seq, 3),
+                "stage_timing": ("CUDA events per stage over a second block of K steps with the near field on the "
+                                 "main stream (%.2f ms/step); the headline value overlaps the near field with "
+                                 "M2L/P2L/L2L on a second stream (%.2f ms/step)" % (ms_seq, ms))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -274,6 +274,13 @@ int qbxg_exchange_local(qbxg_handle** handles, int32_t n_ranks);
 int qbxg_nccl_unique_id(uint8_t* out128);
 int qbxg_nccl_attach(qbxg_handle* h, const uint8_t* id128);
 
+/* Stream overlap (default on; QBXG_OVERLAP=0 in the environment turns the default
+ * off): the near field runs on a second stream beside the far-field chain (M2L,
+ * P2L, L2L) and is joined before the first stage that adds into the centre
+ * locals.  Results are bitwise identical either way; per-stage timings of an
+ * overlapped apply include the contention between the two streams. */
+int qbxg_set_overlap(qbxg_handle* h, int32_t enable);
+
 /* ---- batched densities (repeated applies in iterative
  * solves) ---------------------------------------------------
  * n_rhs densities on one handle, arrays rhs-major with a leading batch dimension:

@@ -344,6 +344,10 @@ class FmmEngine:
             return pot, c[..., 0] + 1j * c[..., 1]
         return pot
 
+    def set_overlap(self, enable: bool):
+        """Near field on a second stream beside M2L/P2L/L2L (default on); bitwise-identical results."""
+        _check(_abi.lib().qbxg_set_overlap(self.handle, 1 if enable else 0))
+
     def apply_batch(self, weights, dipoles=None, want_centers=False):
         """Several densities at once (leading batch dimension): weights (R, N_S),
         dipoles (R, N_S, 3); returns potentials (R, N_T) [and centre coefficients

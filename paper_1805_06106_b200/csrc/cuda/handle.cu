@@ -67,6 +67,10 @@ void check_device() {
 struct Handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;   // near field overlapped with the far-field chain (QBXG_OVERLAP)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t evx[4] = {};       // near begin/end (side stream), P2L end, L2L end
+  bool overlap = false, timed_overlap = false;
   cudaEvent_t ev[QBXG_NUM_TIMERS + 2] = {};
   qbxg_config cfg{};
   int64_t ns = 0, nc = 0, nt = 0, nconv = 0;
@@ -157,6 +161,11 @@ struct Handle {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    for (auto& e : evx)
+      if (e) cudaEventDestroy(e);
+    if (join_ev) cudaEventDestroy(join_ev);
   }
 };
 
@@ -429,6 +438,11 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   dev::set_smem_limits();
   QCK(cudaStreamCreateWithFlags(&H.stream, cudaStreamNonBlocking));
   for (auto& e : H.ev) QCK(cudaEventCreate(&e));
+  for (auto& e : H.evx) QCK(cudaEventCreate(&e));
+  H.overlap = !(std::getenv("QBXG_OVERLAP") && std::getenv("QBXG_OVERLAP")[0] == '0');
+  QCK(cudaStreamCreateWithFlags(&H.side, cudaStreamNonBlocking));
+  QCK(cudaEventCreateWithFlags(&H.fork_ev, cudaEventDisableTiming));
+  QCK(cudaEventCreateWithFlags(&H.join_ev, cudaEventDisableTiming));
   cudaStream_t s = H.stream;
   auto& O = H.owned;
   H.cfg = cfg;
@@ -825,9 +839,19 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     }
   };
   auto& ev = H.ev;
+  bool near_forked = false;
   if (phase & 1) {
   QCK(cudaEventRecord(ev[0], s));
   chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
+  if (H.overlap && !near_done && phase == 3) {  // near field needs only the gathered sources:
+    QCK(cudaEventRecord(H.fork_ev, s));        // run it beside the whole far-field chain
+    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
+    QCK(cudaEventRecord(H.evx[0], H.side));
+    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, H.side));
+    QCK(cudaEventRecord(H.evx[1], H.side));
+    QCK(cudaEventRecord(H.join_ev, H.side));
+    near_forked = true;
+  }
   QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
   QCK(cudaMemsetAsync(D.L, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
   QCK(cudaMemsetAsync(D.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double), s));
@@ -849,7 +873,21 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     for (int l = H.nlev - 2; l >= 0; --l)
       chk(dev::launch_shift_level(H.m2l, H.m2m_straddle[l], H.ops_m2m, D.M, D.kp, false, s));
   QCK(cudaEventRecord(ev[3], s));
-  if (!near_done) chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  // Order: near field | M2L | P2L | L2L | W far | L2QBXL | eval.  With QBXG_OVERLAP the
+  // near field (CUDA-core fp64, writes the centre locals) runs on a side stream beside
+  // the far-field chain (M2L, P2L, L2L touch only box expansions) and is joined before
+  // W far, the first stage that accumulates into the centre locals.
+  const bool ovl = H.overlap && !near_done;
+  if (ovl && !near_forked) {
+    QCK(cudaEventRecord(H.fork_ev, s));
+    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
+    QCK(cudaEventRecord(H.evx[0], H.side));
+    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, H.side));
+    QCK(cudaEventRecord(H.evx[1], H.side));
+    QCK(cudaEventRecord(H.join_ev, H.side));
+  } else if (!near_done && !ovl) {
+    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  }
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
   if (std::getenv("QBXG_M2L_NAIVE"))
@@ -857,6 +895,16 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   else
     chk(dev::launch_m2l_dense(H.m2l, D, s));
   QCK(cudaEventRecord(ev[5], s));
+  chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
+  QCK(cudaEventRecord(H.evx[2], s));
+  for (int l = 1; l < H.nlev; ++l) {
+    if (H.shift_mode == 0)
+      chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
+    else
+      chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
+  }
+  QCK(cudaEventRecord(H.evx[3], s));
+  if (ovl) QCK(cudaStreamWaitEvent(s, H.join_ev, 0));
   if (H.ctr_mode == 0) {
     chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
     chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
@@ -867,15 +915,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     chk(dev::launch_wfar2(D, H.d_wfar_boxes, H.n_wfar_boxes, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
   }
   QCK(cudaEventRecord(ev[6], s));
-  chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
-  QCK(cudaEventRecord(ev[7], s));
-  for (int l = 1; l < H.nlev; ++l) {
-    if (H.shift_mode == 0)
-      chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
-    else
-      chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
-  }
-  QCK(cudaEventRecord(ev[8], s));
+  H.timed_overlap = ovl;
   if (H.l2q_mode == 3)
     chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
   else if (H.l2q_mode == 0)
@@ -975,14 +1015,20 @@ void fill_timings(Handle& H, qbxg_timings* t, bool host_copies, int64_t h2d, int
     cudaEventElapsedTime(&ms, H.ev[a], H.ev[b]);
     return double(ms);
   };
+  auto elx = [&](cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return double(ms);
+  };
   t->ms[QBXG_T_P2M] = el(1, 2);
   t->ms[QBXG_T_M2M] = el(2, 3);
-  t->ms[QBXG_T_NEAR] = el(3, 4);
+  // near: the P2QBXL kernel on whichever stream ran it, plus the conventional-target P2P
+  t->ms[QBXG_T_NEAR] = el(3, 4) + (H.timed_overlap ? elx(H.evx[0], H.evx[1]) : 0.0);
   t->ms[QBXG_T_M2L] = el(4, 5);
-  t->ms[QBXG_T_WFAR] = el(5, 6);
-  t->ms[QBXG_T_P2L] = el(6, 7);
-  t->ms[QBXG_T_L2L] = el(7, 8);
-  t->ms[QBXG_T_L2QBXL] = el(8, 9);
+  t->ms[QBXG_T_P2L] = elx(H.ev[5], H.evx[2]);
+  t->ms[QBXG_T_L2L] = elx(H.evx[2], H.evx[3]);
+  t->ms[QBXG_T_WFAR] = elx(H.evx[3], H.ev[6]);  // with overlap this includes any wait for the near field
+  t->ms[QBXG_T_L2QBXL] = el(6, 9);
   t->ms[QBXG_T_EVAL] = el(9, 10);
   if (host_copies) {
     t->ms[QBXG_T_H2D] = el(11, 0) + el(0, 1);
@@ -1237,6 +1283,13 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
       timings->h2d_bytes = int64_t(n_rhs) * H.ns * (dip ? 32 : 8);
       timings->d2h_bytes = int64_t(n_rhs) * H.nt * 8 + (d_coeffs ? int64_t(n_rhs) * int64_t(cbytes) : 0);
     }
+  });
+}
+
+int qbxg_set_overlap(qbxg_handle* hp, int32_t enable) {
+  return qbxg::guarded([&] {
+    if (!hp) throw qbxg::InvalidArgument("qbxg_set_overlap: null handle");
+    hp->h.overlap = enable != 0;
   });
 }
 

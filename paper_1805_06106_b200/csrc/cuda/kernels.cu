@@ -7,6 +7,7 @@
 // Coefficient conventions: see harmonics.cuh.  Box multipoles M~ = M/|b|^n,
 // box locals L~ = L |b|^n, QBX locals L~_c = L_c r_c^n.  The formulas are the
 // same as the CPU oracle's (oracle/qbx_oracle.cpp), restated on half tables.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1286,7 +1287,10 @@ void near_qbx_q(const DevData& D, const int* boxes, int n, cudaStream_t s) {
     return e ? std::atoi(e) : 2;
   }();
   if (mode == 2) {
-    const size_t smem = size_t(2) * hsize(Q) * kNearThreads * sizeof(double);
+    // QBXG_NEAR_SMEM_KB pads the dynamic shared memory to cap near-field CTAs per SM
+    // (experiment: leave room for co-resident M2L CTAs when the two overlap)
+    static const size_t pad = std::getenv("QBXG_NEAR_SMEM_KB") ? size_t(std::atoi(std::getenv("QBXG_NEAR_SMEM_KB"))) * 1024 : 0;
+    const size_t smem = std::max(size_t(2) * hsize(Q) * kNearThreads * sizeof(double), pad);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_near_qbx<Q, true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

@@ -53,6 +53,7 @@ VARIANTS = [
     {"QBXG_CTR_MODE": "2"},
     {"QBXG_M2L_NAIVE": "1"},
     {"QBXG_M2L_CHUNK_ENTRIES": "5000"},
+    {"QBXG_OVERLAP": "0"},
 ]
 
 
