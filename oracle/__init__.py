@@ -47,6 +47,18 @@ def lib():
                                    _dp, _dp, _dp]
         L.qbxo_direct_qbx.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _i32p, C.c_int,
                                       _dp]
+        L.qbxo_helm_last_error.restype = C.c_char_p
+        L.qbxo_helm_ylm.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.qbxo_helm_bessel.argtypes = [C.c_int, C.c_double, _dp, _dp]
+        L.qbxo_helm_gaunt.argtypes = [C.c_int] * 5 + [_dp]
+        L.qbxo_helm_form.argtypes = [C.c_int, C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int, _dp]
+        L.qbxo_helm_eval.argtypes = [C.c_int, C.c_double, _dp, C.c_int, _dp, _dp, _dp]
+        L.qbxo_helm_translate.argtypes = [C.c_int, C.c_double, _dp, C.c_int, _dp, _dp, C.c_int, _dp]
+        L.qbxo_helm_direct_sum.argtypes = [C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]
+        L.qbxo_helm_direct_qbx.argtypes = [C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p,
+                                           C.c_int, _dp]
+        L.qbxo_helm_execute.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _i32p, _dp, _dp,
+                                        _dp]
         L.qbxo_lists_brute.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int64, _i64p * 6, _i32p * 6, _i64p]
         _o = L
     return _o
@@ -226,3 +238,86 @@ def execute_phase(plan, geom, weights, dipoles, mask, phase, Mbuf, want_centers=
         c = coeffs.reshape(geom.n_centers, cfg.kq, 2)
         return pot, c[..., 0] + 1j * c[..., 1]
     return pot, None
+
+
+# ---- Helmholtz single layer (helm_oracle.cpp; parity unpinned, see its header) ----
+def _hchk(st):
+    if st != 0:
+        raise RuntimeError(lib().qbxo_helm_last_error().decode())
+
+
+def _cplx(a):
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    return a.view(np.float64)
+
+
+def helm_ylm(n, m, v):
+    out = np.zeros(2)
+    _hchk(lib().qbxo_helm_ylm(n, m, _p(v), out.ctypes.data_as(_dp)))
+    return complex(out[0], out[1])
+
+
+def helm_bessel(P, x):
+    j = np.zeros(P + 1)
+    h = np.zeros(2 * (P + 1))
+    _hchk(lib().qbxo_helm_bessel(P, x, j.ctypes.data_as(_dp), h.ctypes.data_as(_dp)))
+    return j, h.view(np.complex128)
+
+
+def helm_gaunt(n, m, n2, m2, l):
+    out = np.zeros(1)
+    _hchk(lib().qbxo_helm_gaunt(n, m, n2, m2, l, out.ctypes.data_as(_dp)))
+    return float(out[0])
+
+
+def helm_form(kind, k, pos, w, center, P):
+    """kind 0: multipole (P2M), 1: local (P2L); w complex weights."""
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(2 * (P + 1) ** 2)
+    _hchk(lib().qbxo_helm_form(kind, k, pos.shape[0], _p(pos), _p(_cplx(w)), _p(center), P,
+                               out.ctypes.data_as(_dp)))
+    return out.view(np.complex128)
+
+
+def helm_eval(kind, k, coeffs, P, center, t):
+    out = np.zeros(2)
+    _hchk(lib().qbxo_helm_eval(kind, k, _p(_cplx(coeffs)), P, _p(center), _p(t), out.ctypes.data_as(_dp)))
+    return complex(out[0], out[1])
+
+
+def helm_translate(kind, k, coeffs, Pin, c, C_, Pout):
+    """kind 0: M2M, 1: M2L, 2: L2L."""
+    out = np.zeros(2 * (Pout + 1) ** 2)
+    _hchk(lib().qbxo_helm_translate(kind, k, _p(_cplx(coeffs)), Pin, _p(c), _p(C_), Pout,
+                                    out.ctypes.data_as(_dp)))
+    return out.view(np.complex128)
+
+
+def helm_direct_sum(k, pos, w, tpos):
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    tpos = np.ascontiguousarray(tpos, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(2 * tpos.shape[0])
+    _hchk(lib().qbxo_helm_direct_sum(k, pos.shape[0], _p(pos), _p(_cplx(w)), tpos.shape[0], _p(tpos),
+                                     out.ctypes.data_as(_dp)))
+    return out.view(np.complex128)
+
+
+def helm_direct_qbx(k, geom, w, q):
+    out = np.zeros(2 * geom.n_targets)
+    _hchk(lib().qbxo_helm_direct_qbx(k, geom.n_sources, _p(geom.source_pos), _p(_cplx(w)), geom.n_centers,
+                                     _p(geom.center_pos), geom.n_targets, _p(geom.target_pos),
+                                     geom.association.ctypes.data_as(_i32p), q, out.ctypes.data_as(_dp)))
+    return out.view(np.complex128)
+
+
+def helm_execute(plan, geom, k, p, q, w, want_centers=False):
+    """Stages 2-9 for the Helmholtz single layer on the host plan (same tree and lists)."""
+    pot = np.zeros(2 * geom.n_targets)
+    cc = np.zeros(2 * geom.n_centers * (q + 1) ** 2) if want_centers else None
+    _hchk(lib().qbxo_helm_execute(C.addressof(plan.view), k, p, q, _p(geom.source_pos), _p(geom.center_pos),
+                                  _p(geom.target_pos), geom.association.ctypes.data_as(_i32p), _p(_cplx(w)),
+                                  pot.ctypes.data_as(_dp), None if cc is None else cc.ctypes.data_as(_dp)))
+    pot = pot.view(np.complex128)
+    if want_centers:
+        return pot, cc.view(np.complex128).reshape(geom.n_centers, (q + 1) ** 2)
+    return pot

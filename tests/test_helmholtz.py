@@ -1,0 +1,99 @@
+"""Helmholtz single layer (BASELINE config 3): the complex128 CPU
+oracle (oracle/helm_oracle.cpp) pinned against analytic anchors, since no reference
+implementation exists (parity unpinned):
+special functions and Gaunt coefficients against scipy, the Gegenbauer expansion and
+the three translation theorems against direct sums, and the FMM converging to direct
+QBX on the same tree and lists."""
+from math import factorial
+
+import numpy as np
+import pytest
+from scipy.special import lpmv, spherical_jn, spherical_yn
+
+import oracle as O
+from paper_1805_06106_b200 import api
+
+K = 3.0  # config 3 wavenumber
+
+
+def _pbar(n, a, x):
+    return np.sqrt((2 * n + 1) / (4 * np.pi) * factorial(n - a) / factorial(n + a)) * lpmv(a, n, x) * (-1) ** a
+
+
+@pytest.mark.parametrize("x", [1e-3, 0.3, 0.999, 1.0, 2.5, 7.0, 25.0])
+def test_spherical_bessel_hankel(x):
+    j, h = O.helm_bessel(20, x)
+    n = np.arange(21)
+    jr, yr = spherical_jn(n, x), spherical_yn(n, x)
+    assert np.max(np.abs(j - jr) / np.abs(jr)) < 1e-12
+    assert np.max(np.abs(h.imag - yr) / np.abs(yr)) < 1e-12
+    assert np.array_equal(h.real, j)
+
+
+def test_harmonics_and_gaunt():
+    v = np.array([0.3, -0.5, 0.8])
+    r = np.linalg.norm(v)
+    th, ph = np.arccos(v[2] / r), np.arctan2(v[1], v[0])
+    for n, m in [(0, 0), (3, 2), (7, -5), (20, 13)]:
+        ref = _pbar(n, abs(m), np.cos(th)) * np.exp(1j * m * ph)
+        assert abs(O.helm_ylm(n, m, v) - ref) <= 1e-14 * abs(ref) + 1e-300
+    xg, wg = np.polynomial.legendre.leggauss(90)
+    for n, m, n2, m2, l in [(3, 2, 5, -1, 4), (10, 3, 12, 7, 6), (20, -5, 20, 8, 38), (4, 1, 2, 1, 3)]:
+        ref = 2 * np.pi * np.sum(wg * _pbar(n, abs(m), xg) * _pbar(n2, abs(m2), xg) * _pbar(l, abs(m - m2), xg))
+        assert abs(O.helm_gaunt(n, m, n2, m2, l) - ref) <= 1e-13
+
+
+def test_expansions_and_translations():
+    rng = np.random.default_rng(1)
+    src = rng.normal(size=(20, 3)) * 0.1
+    w = rng.normal(size=20) + 1j * rng.normal(size=20)
+    c, P = np.zeros(3), 16
+    t_far = np.array([1.3, -0.7, 0.9])
+    direct = O.helm_direct_sum(K, src, w, t_far[None])[0]
+    M = O.helm_form(0, K, src, w, c, P)
+    assert abs(O.helm_eval(0, K, M, P, c, t_far) - direct) < 1e-12 * abs(direct)
+    far = src + np.array([2.0, 0.0, 0.0])
+    tn = np.array([0.05, -0.08, 0.03])
+    L = O.helm_form(1, K, far, w, c, P)
+    assert abs(O.helm_eval(1, K, L, P, c, tn) - O.helm_direct_sum(K, far, w, tn[None])[0]) < 1e-13
+    C = np.array([0.1, 0.05, -0.1])  # M2M
+    M2 = O.helm_translate(0, K, M, P, c, C, P)
+    assert abs(O.helm_eval(0, K, M2, P, C, t_far) - direct) < 1e-9 * abs(direct)
+    C2 = np.array([1.5, 0.4, 0.2])  # M2L
+    tt = C2 + np.array([0.05, 0.02, -0.04])
+    L2 = O.helm_translate(1, K, M, P, c, C2, P)
+    ref = O.helm_direct_sum(K, src, w, tt[None])[0]
+    assert abs(O.helm_eval(1, K, L2, P, C2, tt) - ref) < 1e-11 * abs(ref)
+    C3 = C2 + np.array([0.03, -0.02, 0.01])  # L2L (exact up to the truncated tail)
+    L3 = O.helm_translate(2, K, L2, P, C2, C3, P)
+    assert abs(O.helm_eval(1, K, L3, P, C3, tt) - O.helm_eval(1, K, L2, P, C2, tt)) < 1e-12 * abs(ref)
+
+
+def _config3_small(level=1, seed=3):
+    g = api.config_geometry(3, level=level)
+    rng = np.random.default_rng(seed)
+    mu = rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources)  # Re, Im ~ U[-1,1]
+    return g, g.quad_weight * mu
+
+
+def test_direct_sum_reciprocity():
+    rng = np.random.default_rng(2)
+    a, b = rng.normal(size=(30, 3)), rng.normal(size=(40, 3)) + 3.0
+    wa, wb = rng.normal(size=30) + 1j * rng.normal(size=30), rng.normal(size=40) + 1j * rng.normal(size=40)
+    # sum_b wb phi_a(b) == sum_a wa phi_b(a): G_k is symmetric
+    lhs = np.sum(wb * O.helm_direct_sum(K, a, wa, b))
+    rhs = np.sum(wa * O.helm_direct_sum(K, b, wb, a))
+    assert abs(lhs - rhs) < 1e-12 * abs(lhs)
+
+
+def test_fmm_converges_to_direct_qbx():
+    """Theorem 1 analogue: the Helmholtz FMM error against direct QBX falls with p."""
+    g, w = _config3_small(level=1)
+    d = O.helm_direct_qbx(K, g, w, 3)
+    errs = []
+    for p in (3, 5, 8):
+        plan = api.Plan(api.FmmConfig(p_fmm=p, p_qbx=3, n_max=64, kernel=0), g)  # kernel-independent tree
+        f = O.helm_execute(plan, g, K, p, 3, w)
+        errs.append(float(np.linalg.norm(f - d) / np.linalg.norm(d)))
+    assert errs[0] > errs[1] > errs[2], errs
+    assert errs[2] < 1e-5, errs
