@@ -317,6 +317,21 @@ int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* w
                     const double* center_radius, int64_t n_targets, const double* target_pos,
                     const int32_t* association, int32_t p_qbx, double* out_pot);
 
+/* ---- Helmholtz single layer, unaccelerated (BASELINE config 3) --
+ * G_k = e^{ik|x-y|}/(4 pi |x-y|), complex weights and potentials interleaved
+ * (re, im).  qbxg_helm_direct_sum: pot[t] = sum_s w_s G_k(t, s) (QBXG_ERR_DOMAIN on a
+ * coincidence).  qbxg_helm_direct_qbx: the spec's direct_qbx for G_k -- each
+ * associated target gets its centre's order-p_qbx local from all sources,
+ *   L_n^m = ik sum_s w_s h_n(k|s-c|) conj(Y_n^m(s-c)), pot = sum L_n^m j_n(k|t-c|) Y_n^m(t-c)
+ * (orthonormal Y without the Condon-Shortley phase), conventional targets the direct
+ * sum.  No reference implementation exists; parity is against the
+ * complex128 oracle in oracle/helm_oracle.cpp.  The Helmholtz FMM is not built yet. */
+int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
+                         int64_t n_targets, const double* target_pos, double* out_pot_c);
+int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
+                         int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
+                         const int32_t* association, int32_t p_qbx, double* out_pot_c);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char* qbxg_last_error(void);
 int qbxg_device_count(int32_t* out);

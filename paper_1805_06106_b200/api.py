@@ -438,6 +438,35 @@ def direct_qbx(geom: Geometry, weights, dipoles=None, p_qbx: int = 5) -> np.ndar
     return pot
 
 
+def _as_cplx(w, n):
+    w = np.ascontiguousarray(w, dtype=np.complex128).reshape(-1)
+    if w.shape[0] != n:
+        raise ValueError("weights do not match the number of sources")
+    return w.view(np.float64)
+
+
+def helm_direct_sum(k: float, source_pos, weights, target_pos) -> np.ndarray:
+    """Helmholtz single layer G_k = e^{ik r}/(4 pi r) summed directly on the GPU (complex)."""
+    pos = np.ascontiguousarray(source_pos, dtype=np.float64).reshape(-1, 3)
+    tpos = np.ascontiguousarray(target_pos, dtype=np.float64).reshape(-1, 3)
+    wc = _as_cplx(weights, pos.shape[0])
+    out = np.empty(2 * tpos.shape[0], dtype=np.float64)
+    _check(_abi.lib().qbxg_helm_direct_sum(float(k), pos.shape[0], _ptr(pos), _ptr(wc), tpos.shape[0], _ptr(tpos),
+                                           _ptr(out)))
+    return out.view(np.complex128)
+
+
+def helm_direct_qbx(k: float, geom: Geometry, weights, p_qbx: int = 5) -> np.ndarray:
+    """Unaccelerated QBX for the Helmholtz single layer on the GPU (complex potentials)."""
+    wc = _as_cplx(weights, geom.n_sources)
+    out = np.empty(2 * geom.n_targets, dtype=np.float64)
+    _check(_abi.lib().qbxg_helm_direct_qbx(float(k), geom.n_sources, _ptr(geom.source_pos), _ptr(wc),
+                                           geom.n_centers, _ptr(geom.center_pos), geom.n_targets,
+                                           _ptr(geom.target_pos), _ptr(geom.association, C.c_int32), int(p_qbx),
+                                           _ptr(out)))
+    return out.view(np.complex128)
+
+
 def device_count() -> int:
     n = C.c_int32(0)
     _check(_abi.lib().qbxg_device_count(C.byref(n)))

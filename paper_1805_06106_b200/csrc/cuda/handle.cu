@@ -1342,6 +1342,127 @@ int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* w
   });
 }
 
+int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
+                         int64_t n_targets, const double* target_pos, double* out_pot_c) {
+  return qbxg::guarded([&] {
+    using qbxg::InvalidArgument;
+    if (n_sources < 0 || n_targets < 0) throw InvalidArgument("helm_direct_sum: negative size");
+    if (n_sources >= (int64_t(1) << 31) || n_targets >= (int64_t(1) << 31))
+      throw InvalidArgument("helm_direct_sum: too many points");
+    if ((n_sources && (!source_pos || !weights_c)) || (n_targets && (!target_pos || !out_pot_c)))
+      throw InvalidArgument("helm_direct_sum: null array");
+    if (!(k > 0) || !std::isfinite(k)) throw InvalidArgument("helm_direct_sum: wavenumber must be positive");
+    for (int64_t i = 0; i < 2 * n_sources; ++i)
+      if (!std::isfinite(weights_c[i])) throw InvalidArgument("helm_direct_sum: non-finite weight");
+    if (n_targets == 0) return;
+    qbxg::check_device();
+    std::vector<void*> owned;
+    struct Free {
+      std::vector<void*>& o;
+      ~Free() {
+        for (void* p : o) cudaFree(p);
+      }
+    } fr{owned};
+    std::vector<double4> src(n_sources), tgt(n_targets);
+    std::vector<double2> w(n_sources);
+    for (int64_t i = 0; i < n_sources; ++i) {
+      src[i] = make_double4(source_pos[3 * i], source_pos[3 * i + 1], source_pos[3 * i + 2], 0);
+      w[i] = make_double2(weights_c[2 * i], weights_c[2 * i + 1]);
+    }
+    for (int64_t i = 0; i < n_targets; ++i)
+      tgt[i] = make_double4(target_pos[3 * i], target_pos[3 * i + 1], target_pos[3 * i + 2], 0);
+    cudaStream_t s = nullptr;
+    double4* ds = qbxg::dupload(owned, src, s);
+    double2* dw = qbxg::dupload(owned, w, s);
+    double4* dt = qbxg::dupload(owned, tgt, s);
+    double2* dp = qbxg::dalloc<double2>(owned, n_targets);
+    unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
+    QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+    qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, int(n_targets), dt, dp, bad, s);
+    QCK(cudaGetLastError());
+    unsigned long long hb = 0;
+    QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+    if (hb != ~0ull)
+      throw qbxg::DomainError("helm_direct_sum: target " + std::to_string(hb >> 32) + " coincides with source " +
+                              std::to_string(hb & 0xffffffffull));
+    QCK(cudaMemcpy(out_pot_c, dp, n_targets * sizeof(double2), cudaMemcpyDeviceToHost));
+  });
+}
+
+int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
+                         int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
+                         const int32_t* association, int32_t p_qbx, double* out_pot_c) {
+  return qbxg::guarded([&] {
+    using qbxg::InvalidArgument;
+    if (n_sources < 0 || n_centers < 0 || n_targets < 0) throw InvalidArgument("helm_direct_qbx: negative size");
+    if (n_sources >= (int64_t(1) << 31) || n_centers >= (int64_t(1) << 31) || n_targets >= (int64_t(1) << 31))
+      throw InvalidArgument("helm_direct_qbx: too many points");
+    if (p_qbx < 0 || p_qbx > 8) throw InvalidArgument("helm_direct_qbx: p_qbx must be in [0, 8]");
+    if (!(k > 0) || !std::isfinite(k)) throw InvalidArgument("helm_direct_qbx: wavenumber must be positive");
+    if ((n_sources && (!source_pos || !weights_c)) || (n_centers && !center_pos) ||
+        (n_targets && (!target_pos || !association || !out_pot_c)))
+      throw InvalidArgument("helm_direct_qbx: null array");
+    std::vector<int> conv;
+    for (int64_t i = 0; i < n_targets; ++i) {
+      const int32_t a = association[i];
+      if (a < -1 || a >= n_centers)
+        throw InvalidArgument("helm_direct_qbx: target " + std::to_string(i) + " has association " +
+                              std::to_string(a) + " outside [-1, n_centers)");
+      if (a < 0) conv.push_back(int(i));
+    }
+    if (n_targets == 0) return;
+    qbxg::check_device();
+    std::vector<void*> owned;
+    struct Free {
+      std::vector<void*>& o;
+      ~Free() {
+        for (void* p : o) cudaFree(p);
+      }
+    } fr{owned};
+    std::vector<double4> src(n_sources), ctr(n_centers), ctg(conv.size());
+    std::vector<double2> w(n_sources);
+    for (int64_t i = 0; i < n_sources; ++i) {
+      src[i] = make_double4(source_pos[3 * i], source_pos[3 * i + 1], source_pos[3 * i + 2], 0);
+      w[i] = make_double2(weights_c[2 * i], weights_c[2 * i + 1]);
+    }
+    for (int64_t c = 0; c < n_centers; ++c)
+      ctr[c] = make_double4(center_pos[3 * c], center_pos[3 * c + 1], center_pos[3 * c + 2], 0);
+    for (size_t j = 0; j < conv.size(); ++j)
+      ctg[j] = make_double4(target_pos[3 * conv[j]], target_pos[3 * conv[j] + 1], target_pos[3 * conv[j] + 2], 0);
+    cudaStream_t s = nullptr;
+    double4* ds = qbxg::dupload(owned, src, s);
+    double2* dw = qbxg::dupload(owned, w, s);
+    double4* dc = qbxg::dupload(owned, ctr, s);
+    double* dtp = qbxg::dupload(owned, std::vector<double>(target_pos, target_pos + 3 * n_targets), s);
+    int* das = qbxg::dupload(owned, std::vector<int>(association, association + n_targets), s);
+    double2* dl = qbxg::dalloc<double2>(owned, size_t(std::max<int64_t>(n_centers, 1)) * (p_qbx + 1) * (p_qbx + 1));
+    double2* dp = qbxg::dalloc<double2>(owned, n_targets);
+    QCK(cudaMemsetAsync(dp, 0, n_targets * sizeof(double2), s));
+    qbxg::dev::launch_helm_direct_qbx(k, p_qbx, int(n_sources), ds, dw, int(n_centers), dc, dl, int(n_targets), dtp,
+                                      das, dp, s);
+    QCK(cudaGetLastError());
+    std::vector<double2> pot(n_targets);
+    QCK(cudaMemcpy(pot.data(), dp, n_targets * sizeof(double2), cudaMemcpyDeviceToHost));
+    if (!conv.empty()) {
+      double4* dt = qbxg::dupload(owned, ctg, s);
+      double2* dq = qbxg::dalloc<double2>(owned, conv.size());
+      unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
+      QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+      qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, int(conv.size()), dt, dq, bad, s);
+      QCK(cudaGetLastError());
+      unsigned long long hb = 0;
+      QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+      if (hb != ~0ull)
+        throw qbxg::DomainError("helm_direct_qbx: target " + std::to_string(conv[hb >> 32]) +
+                                " coincides with source " + std::to_string(hb & 0xffffffffull));
+      std::vector<double2> pc(conv.size());
+      QCK(cudaMemcpy(pc.data(), dq, conv.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+      for (size_t j = 0; j < conv.size(); ++j) pot[conv[j]] = pc[j];
+    }
+    std::memcpy(out_pot_c, pot.data(), n_targets * sizeof(double2));
+  });
+}
+
 int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* weights, const double* dipoles_or_null,
                     int64_t n_centers, const double* center_pos, const double* center_radius, int64_t n_targets,
                     const double* target_pos, const int32_t* association, int32_t p_qbx, double* out_pot) {

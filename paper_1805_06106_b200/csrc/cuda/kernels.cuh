@@ -183,6 +183,12 @@ int launch_direct_qbx(int q, int ns, const double4* src, const double4* mu, int 
                       double2* Lc, cudaStream_t s);
 int launch_direct_qbx_eval(int q, int n, const double* tpos, const int* assoc, const double4* ctr,
                            const double2* Lc, double* pot, cudaStream_t s);
+// Helmholtz single layer, unaccelerated (helm.cu): complex weights / potentials
+int launch_helm_direct_sum(double k, int ns, const double4* src, const double2* w, int nt, const double4* tgt,
+                           double2* pot, unsigned long long* bad, cudaStream_t s);
+int launch_helm_direct_qbx(double k, int q, int ns, const double4* src, const double2* w, int nc,
+                           const double4* ctr, double2* Lc, int nt, const double* tpos, const int* assoc,
+                           double2* pot, cudaStream_t s);
 void upload_constants();
 void set_smem_limits();
 

@@ -97,3 +97,32 @@ def test_fmm_converges_to_direct_qbx():
         errs.append(float(np.linalg.norm(f - d) / np.linalg.norm(d)))
     assert errs[0] > errs[1] > errs[2], errs
     assert errs[2] < 1e-5, errs
+
+
+def test_gpu_entry_points_validate_on_host():
+    """Argument checks of the GPU Helmholtz entry points run before any device work."""
+    g, w = _config3_small(level=1)
+    with pytest.raises(ValueError):
+        api.helm_direct_sum(-1.0, g.source_pos, w, g.target_pos[:5])
+    with pytest.raises(ValueError):
+        api.helm_direct_qbx(K, g, w, 9)
+    with pytest.raises(ValueError):
+        api.helm_direct_qbx(K, g, w[:-1], 3)
+
+
+@pytest.mark.gpu
+def test_gpu_helm_direct_sum_matches_oracle():
+    g, w = _config3_small(level=1)
+    t = g.target_pos[:700] + 0.01
+    pot = api.helm_direct_sum(K, g.source_pos, w, t)
+    ref = O.helm_direct_sum(K, g.source_pos, w, t)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("q", [0, 3, 5])
+def test_gpu_helm_direct_qbx_matches_oracle(q):
+    g, w = _config3_small(level=1)
+    pot = api.helm_direct_qbx(K, g, w, q)
+    ref = O.helm_direct_qbx(K, g, w, q)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
