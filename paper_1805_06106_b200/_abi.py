@@ -97,6 +97,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_measure_dmma_peak", "qbxg_plan_shard", "qbxg_create_sharded", "qbxg_apply_phase",
     "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
     "qbxg_direct_qbx", "qbxg_apply_batch", "qbxg_apply_batch_device", "qbxg_set_overlap", "qbxg_helm_direct_sum", "qbxg_helm_direct_qbx",
+    "qbxg_apply_complex",
 )
 
 SHARD_OWN, SHARD_SUBTREE, SHARD_STRADDLE, SHARD_DOWN = 1, 2, 4, 8
@@ -117,6 +118,7 @@ def _declare(lib):
         "qbxg_apply": ([C.c_void_p, _dp, _dp, _dp, _dp, P(Timings)], C.c_int),
         "qbxg_apply_device": ([C.c_void_p] * 6 + [P(Timings)], C.c_int),
         "qbxg_set_overlap": ([C.c_void_p, C.c_int32], C.c_int),
+        "qbxg_apply_complex": ([C.c_void_p, _dp, _dp, _dp, P(Timings)], C.c_int),
         "qbxg_helm_direct_sum": ([C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp], C.c_int),
         "qbxg_helm_direct_qbx": ([C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p, C.c_int32,
                                   _dp], C.c_int),

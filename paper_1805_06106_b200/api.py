@@ -106,9 +106,11 @@ class FmmConfig:
     n_max: int = 64
     kernel: int = _abi.KERNEL_LAPLACE_SL
     w_far_demote: int = 0
+    helmholtz_k: float = 0.0  # wavenumber, kernel 2 (Helmholtz single layer)
 
     def to_c(self):
-        return _abi.Config(self.p_fmm, self.p_qbx, self.t_f, self.n_max, self.kernel, 0.0, self.w_far_demote, 0)
+        return _abi.Config(self.p_fmm, self.p_qbx, self.t_f, self.n_max, self.kernel, float(self.helmholtz_k),
+                           self.w_far_demote, 0)
 
     @property
     def kq(self):
@@ -342,6 +344,22 @@ class FmmEngine:
         if want_centers:
             c = coeffs.reshape(self.geom.n_centers, self.cfg.kq, 2)
             return pot, c[..., 0] + 1j * c[..., 1]
+        return pot
+
+    def apply_complex(self, weights, want_centers=False):
+        """Helmholtz single layer (kernel 2): complex weights in, complex potentials
+        out; centre locals (N_C, (q+1)^2) in the internal basis (include/qbxg.h)."""
+        w = np.ascontiguousarray(weights, dtype=np.complex128).reshape(-1)
+        if w.shape[0] != self.geom.n_sources:
+            raise ValueError("apply_complex: weights do not match the geometry")
+        pot = np.empty(2 * self.geom.n_targets, dtype=np.float64)
+        kq = (self.cfg.p_qbx + 1) ** 2
+        cc = np.empty(2 * self.geom.n_centers * kq, dtype=np.float64) if want_centers else None
+        _check(_abi.lib().qbxg_apply_complex(self.handle, _ptr(w.view(np.float64)), _ptr(pot), _ptr(cc),
+                                             C.byref(self.timings)))
+        pot = pot.view(np.complex128)
+        if want_centers:
+            return pot, cc.view(np.complex128).reshape(self.geom.n_centers, kq)
         return pot
 
     def set_overlap(self, enable: bool):

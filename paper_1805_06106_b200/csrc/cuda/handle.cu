@@ -23,6 +23,7 @@
 
 #include "../host/common.hpp"
 #include "harmonics.cuh"
+#include "helm.cuh"
 #include "kernels.cuh"
 #include "../host/rotation.hpp"
 
@@ -140,6 +141,34 @@ struct Handle {
   double* d_coeffs = nullptr;
   dev::M2LPlan m2l;
   int last_launches = 0;
+  // Helmholtz single layer (cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL): helm_setup / run_helm
+  bool helm = false;
+  dev::HelmData HD{};
+  std::vector<double2*> h_ops_m2m, h_ops_l2l;  // per level: 8 octant operators
+  double2* h_ops_m2l = nullptr;                // per (level, offset) operators
+  struct HelmM2LChunk {
+    int n_tiles = 0;
+    int4* tiles = nullptr;
+    int* col_src = nullptr;
+    int* col_pos = nullptr;
+    int n_boxes = 0;
+    int* boxes = nullptr;
+    int64_t base = 0;
+  };
+  std::vector<HelmM2LChunk> h_m2l;
+  double2* h_temp = nullptr;                   // M2L staging rows (KP complex)
+  int h_n_wctas = 0, h_n_wcentres = 0;         // M2QBXL: box-major CTAs, centre-major reduce
+  int4* h_wctas = nullptr;
+  int *h_wctr = nullptr, *h_wrow = nullptr, *h_wcentres = nullptr, *h_wstarts = nullptr;
+  double2* h_wrows = nullptr;
+  int n_tgt_boxes_eval = 0;                    // boxes owning conventional targets (L2P)
+  int* d_tgt_boxes_eval = nullptr;
+  int h_n_lctas = 0;                           // L2QBXL CTAs over each box's centres
+  int4* h_lctas = nullptr;
+  int* h_lctr = nullptr;
+  double* d_wc = nullptr;                      // host-apply staging: complex weights, potentials
+  double* d_potc = nullptr;
+  double* d_coeffc = nullptr;
   // batched densities (qbxg_apply_batch*): NR-wide near-field buffers, grown on demand
   int bnr = 0;                   // densities per near-field pass (0: not allocated)
   double* d_bw = nullptr;        // bnr x ns sorted weights
@@ -410,6 +439,268 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.srow);
 }
 
+// ---- Helmholtz single layer: device data, operators and work lists --------
+void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& vs, const std::vector<int2>& vent,
+                cudaStream_t s) {
+  auto& O = H.owned;
+  dev::DevData& D = H.D;
+  dev::HelmData& HD = H.HD;
+  const int p = H.cfg.p_fmm, q = H.cfg.p_qbx, nb = H.nb;
+  HD.k = H.cfg.helmholtz_k;
+  HD.P = p;
+  HD.Q = q;
+  HD.KP = (p + 1) * (p + 1);
+  HD.KQ = (q + 1) * (q + 1);
+  HD.GL = p + 1;
+  HD.box = D.box;
+  HD.child_starts = D.child_starts;
+  HD.children = D.children;
+  HD.parent = D.parent;
+  HD.src_own_start = D.src_own_start;
+  HD.src_own_count = D.src_own_count;
+  HD.ctr_own_start = D.ctr_own_start;
+  HD.ctr_own_count = D.ctr_own_count;
+  HD.tgt_own_start = D.tgt_own_start;
+  HD.tgt_own_count = D.tgt_own_count;
+  HD.src = D.src;
+  HD.ctr = D.ctr;
+  HD.tgt = D.tgt;
+  HD.near_starts = D.near_starts;
+  HD.near_seg = D.near_seg;
+  HD.xfar_starts = D.xfar_starts;
+  HD.xfar_seg = D.xfar_seg;
+  HD.v_starts = D.v_starts;
+  HD.wfar_starts = D.wfar_starts;
+  HD.wfar_box = D.wfar_box;
+  HD.hw = dalloc<double2>(O, std::max<int64_t>(H.ns, 1));
+  HD.M = dalloc<double2>(O, size_t(nb) * HD.KP);
+  HD.L = dalloc<double2>(O, size_t(nb) * HD.KP);
+  HD.Lc = dalloc<double2>(O, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ);
+  HD.phi = dalloc<double2>(O, std::max<int64_t>(H.nconv, 1));
+  HD.gaunt = dupload(O, helm_gaunt_table(p), s);
+  H.d_wc = dalloc<double>(O, 2 * std::max<int64_t>(H.ns, 1));
+  H.d_potc = dalloc<double>(O, 2 * std::max<int64_t>(H.nt, 1));
+  H.d_coeffc = dalloc<double>(O, 2 * std::max<int64_t>(H.nc, 1) * HD.KQ);
+  const size_t opsz = size_t(HD.KP) * HD.KP;
+
+  // level radii and M2M / L2L octant operators (child offset d_o = (+-h, +-h, +-h))
+  std::vector<double> hl(H.nlev, 0.0);
+  for (int l = 0; l < H.nlev; ++l)
+    if (V.level_starts[l + 1] > V.level_starts[l]) hl[l] = V.box_radius[V.level_boxes[V.level_starts[l]]];
+  std::vector<double4> shifts;
+  auto octv = [](int o, double h, double sg) {
+    return make_double4(sg * ((o & 4) ? h : -h), sg * ((o & 2) ? h : -h), sg * ((o & 1) ? h : -h), 0.0);
+  };
+  for (int l = 0; l + 1 < H.nlev; ++l)  // M2M into parents at level l: t = parent - child
+    for (int o = 0; o < 8; ++o) shifts.push_back(octv(o, hl[l + 1], -1.0));
+  for (int l = 1; l < H.nlev; ++l)  // L2L into children at level l: t = child - parent
+    for (int o = 0; o < 8; ++o) shifts.push_back(octv(o, hl[l], 1.0));
+  double2* shift_ops = dalloc<double2>(O, std::max<size_t>(shifts.size(), 1) * opsz);
+  if (!shifts.empty()) dev::helm_build_ops(HD, int(shifts.size()), dupload(O, shifts, s), shift_ops, s);
+  H.h_ops_m2m.assign(H.nlev, nullptr);
+  H.h_ops_l2l.assign(H.nlev, nullptr);
+  {
+    size_t k = 0;
+    for (int l = 0; l + 1 < H.nlev; ++l, k += 8) H.h_ops_m2m[l] = shift_ops + k * opsz;
+    for (int l = 1; l < H.nlev; ++l, k += 8) H.h_ops_l2l[l] = shift_ops + k * opsz;
+  }
+
+  // M2L operators per (level, offset slot) in use: t = c_b - c_d = 2 h_l delta
+  const int64_t nent = vs[nb];
+  std::vector<int> key_op;
+  std::vector<int> op_of_entry(nent);
+  {
+    std::vector<int> key_to_op(size_t(H.nlev) * 1331, -1);
+    std::vector<double4> msh;
+    for (int b = 0; b < nb; ++b)
+      for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
+        const int l = V.box_level[b], sl = vent[e].y;
+        int& op = key_to_op[size_t(l) * 1331 + sl];
+        if (op < 0) {
+          op = int(msh.size());
+          const double dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
+          msh.push_back(make_double4(2 * hl[l] * dx, 2 * hl[l] * dy, 2 * hl[l] * dz, 1.0));
+        }
+        op_of_entry[e] = op;
+      }
+    const size_t bytes = msh.size() * opsz * sizeof(double2);
+    size_t free_b = 0, total_b = 0;
+    QCK(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > size_t(double(free_b) * 0.7))
+      throw InvalidArgument("qbxg_create: Helmholtz M2L operators (" + std::to_string(bytes >> 20) +
+                            " MiB) exceed device memory");
+    H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * opsz);
+    if (!msh.empty()) dev::helm_build_ops(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, s);
+    // tiles of same-operator entries, chunked over contiguous target boxes
+    const int cols = dev::helm_m2l_cols();
+    size_t free2 = 0;
+    QCK(cudaMemGetInfo(&free2, &total_b));
+    const int64_t cap = std::max<int64_t>(
+        int64_t(std::min<size_t>(size_t(8) << 30, size_t(double(free2) * 0.4)) / (HD.KP * sizeof(double2))), 1024);
+    int64_t max_chunk = 0;
+    int b0 = 0;
+    const int n_ops = int(msh.size());
+    while (b0 < nb) {
+      int b1 = b0;
+      while (b1 < nb && (vs[b1 + 1] - vs[b0] <= cap || b1 == b0)) ++b1;
+      const int64_t base = vs[b0], cnt = vs[b1] - vs[b0];
+      if (cnt > 0) {
+        Handle::HelmM2LChunk C;
+        C.base = base;
+        std::vector<int> boxes;
+        for (int b = b0; b < b1; ++b)
+          if (vs[b + 1] > vs[b]) boxes.push_back(b);
+        std::vector<int64_t> cnt_op(n_ops + 1, 0);
+        for (int64_t e = base; e < base + cnt; ++e) cnt_op[op_of_entry[e] + 1]++;
+        for (int o = 0; o < n_ops; ++o) cnt_op[o + 1] += cnt_op[o];
+        std::vector<int> csrc(cnt), cpos(cnt);
+        std::vector<int64_t> fill(cnt_op.begin(), cnt_op.end() - 1);
+        for (int64_t e = base; e < base + cnt; ++e) {
+          const int64_t i = fill[op_of_entry[e]]++;
+          csrc[i] = vent[e].x;
+          cpos[i] = int(e - base);
+        }
+        std::vector<int4> tiles;
+        for (int o = 0; o < n_ops; ++o)
+          for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += cols)
+            tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(cols, cnt_op[o + 1] - i)), 0));
+        C.n_tiles = int(tiles.size());
+        C.tiles = dupload(O, tiles, s);
+        C.col_src = dupload(O, csrc, s);
+        C.col_pos = dupload(O, cpos, s);
+        C.n_boxes = int(boxes.size());
+        C.boxes = dupload(O, boxes, s);
+        H.h_m2l.push_back(C);
+        max_chunk = std::max(max_chunk, cnt);
+        QCK(cudaStreamSynchronize(s));
+      }
+      b0 = b1;
+    }
+    H.h_temp = dalloc<double2>(O, size_t(std::max<int64_t>(max_chunk, 1)) * HD.KP);
+  }
+
+  // M2QBXL pairs (centre, W_far box): centre-major index for the reduce, box-major CTAs
+  {
+    std::vector<int2> pr;  // (sorted centre, box), centre-major
+    std::vector<int> centres, starts;
+    for (int b = 0; b < nb; ++b) {
+      const int64_t a = V.list_starts[QBXG_LIST_W_FAR][b], e = V.list_starts[QBXG_LIST_W_FAR][b + 1];
+      if (a == e || !(V.box_flags[b] & QBXG_BOX_TARGET)) continue;
+      for (int j = 0; j < V.ctr_own_count[b]; ++j) {
+        const int cs = V.ctr_own_start[b] + j;
+        centres.push_back(cs);
+        starts.push_back(int(pr.size()));
+        for (int64_t i = a; i < e; ++i) pr.push_back(make_int2(cs, V.list_boxes[QBXG_LIST_W_FAR][i]));
+      }
+    }
+    starts.push_back(int(pr.size()));
+    std::vector<int> perm(pr.size());
+    for (size_t i = 0; i < perm.size(); ++i) perm[i] = int(i);
+    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return pr[x].y < pr[y].y; });
+    std::vector<int> wctr(pr.size()), wrow(pr.size());
+    std::vector<int4> ctas;
+    for (size_t i = 0; i < perm.size(); ++i) {
+      wctr[i] = pr[perm[i]].x;
+      wrow[i] = perm[i];
+    }
+    size_t i = 0;
+    while (i < perm.size()) {
+      const int box = pr[perm[i]].y;
+      size_t j = i;
+      while (j < perm.size() && pr[perm[j]].y == box && j - i < size_t(dev::kHCtrMax)) ++j;
+      ctas.push_back(make_int4(box, int(i), int(j - i), 0));
+      i = j;
+    }
+    H.h_n_wctas = int(ctas.size());
+    H.h_wctas = dupload(O, ctas, s);
+    H.h_wctr = dupload(O, wctr, s);
+    H.h_wrow = dupload(O, wrow, s);
+    H.h_n_wcentres = int(centres.size());
+    H.h_wcentres = dupload(O, centres, s);
+    H.h_wstarts = dupload(O, starts, s);
+    H.h_wrows = dalloc<double2>(O, std::max<size_t>(pr.size(), 1) * HD.KQ);
+  }
+  {
+    std::vector<int> tb;
+    for (int b = 0; b < nb; ++b)
+      if (V.tgt_own_count[b] > 0) tb.push_back(b);
+    H.n_tgt_boxes_eval = int(tb.size());
+    H.d_tgt_boxes_eval = dupload(O, tb, s);
+  }
+  // L2QBXL: each box's centres in CTAs of <= kHCtrMax
+  {
+    std::vector<int4> ctas;
+    std::vector<int> lctr;
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < V.ctr_own_count[b]; j += dev::kHCtrMax) {
+        const int n = std::min(dev::kHCtrMax, V.ctr_own_count[b] - j);
+        ctas.push_back(make_int4(b, int(lctr.size()), n, 0));
+        for (int k = 0; k < n; ++k) lctr.push_back(V.ctr_own_start[b] + j + k);
+      }
+    H.h_n_lctas = int(ctas.size());
+    H.h_lctas = dupload(O, ctas, s);
+    H.h_lctr = dupload(O, lctr, s);
+  }
+  QCK(cudaStreamSynchronize(s));
+}
+
+// One Helmholtz apply: d_wc complex weights (caller order, interleaved), d_pot
+// complex potentials (caller order), d_coeffs optional centre locals (caller order).
+void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cudaStream_t s) {
+  dev::HelmData& HD = H.HD;
+  auto& ev = H.ev;
+  int L = 0;
+  static const bool debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
+  int stage_no = 0;
+  auto chk = [&](int k) {
+    if (k < 0) throw InvalidArgument("qbxg_apply: unsupported Helmholtz order");
+    L += k;
+    ++stage_no;
+    cudaError_t e = cudaPeekAtLastError();
+    if (e == cudaSuccess && debug_sync) {
+      e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    if (e != cudaSuccess)
+      throw CudaError(std::string("CUDA error after Helmholtz launch group ") + std::to_string(stage_no) + ": " +
+                      cudaGetErrorString(e));
+  };
+  QCK(cudaEventRecord(ev[0], s));
+  chk(dev::helm_gather(HD, H.ns, H.d_src_perm, d_wc, s));
+  QCK(cudaMemsetAsync(HD.M, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
+  QCK(cudaMemsetAsync(HD.L, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
+  QCK(cudaMemsetAsync(HD.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double2), s));
+  QCK(cudaEventRecord(ev[1], s));
+  chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
+  QCK(cudaEventRecord(ev[2], s));
+  for (int l = H.nlev - 2; l >= 0; --l) chk(dev::helm_shift(HD, 0, H.d_m2m_level[l], H.n_m2m_level[l], H.h_ops_m2m[l], s));
+  QCK(cudaEventRecord(ev[3], s));
+  chk(dev::helm_near(HD, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
+  QCK(cudaEventRecord(ev[4], s));
+  for (const auto& C : H.h_m2l)
+    chk(dev::helm_m2l(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_temp, C.n_boxes, C.boxes,
+                      C.base, s));
+  QCK(cudaEventRecord(ev[5], s));
+  chk(dev::helm_p2l(HD, H.d_xfar_boxes, H.n_xfar_boxes, s));
+  QCK(cudaEventRecord(H.evx[2], s));
+  for (int l = 1; l < H.nlev; ++l) chk(dev::helm_shift(HD, 1, H.d_l2l_level[l], H.n_l2l_level[l], H.h_ops_l2l[l], s));
+  QCK(cudaEventRecord(H.evx[3], s));
+  chk(dev::helm_ctr(HD, 1, HD.M, H.h_n_wctas, H.h_wctas, H.h_wctr, H.h_wrow, H.h_wrows, 0, s));
+  chk(dev::helm_pair_reduce(HD, H.h_wcentres, H.h_wstarts, H.h_n_wcentres, H.h_wrows, s));
+  chk(dev::helm_m2p(HD, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
+  QCK(cudaEventRecord(ev[6], s));
+  chk(dev::helm_ctr(HD, 0, HD.L, H.h_n_lctas, H.h_lctas, H.h_lctr, H.h_lctr, HD.Lc, 1, s));
+  QCK(cudaEventRecord(ev[9], s));
+  chk(dev::helm_eval(HD, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_tgt_boxes_eval,
+                     H.d_tgt_boxes_eval, H.d_tgt_perm, d_pot, s));
+  if (d_coeffs) chk(dev::helm_centre_out(HD, int(H.nc), H.d_ctr_perm, d_coeffs, s));
+  QCK(cudaEventRecord(ev[10], s));
+  QCK(cudaGetLastError());
+  H.timed_overlap = false;
+  H.last_launches = L;
+}
+
 void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device,
             int nranks = 1, int rank = 0) {
   check_device();
@@ -424,8 +715,15 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     if (qbxg_plan_shard(plan, nranks, rank, H.cuts.data(), H.mask.data()) != QBXG_OK)
       throw InvalidArgument(get_last_error());
   }
-  if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL)
-    throw InvalidArgument("qbxg_create: only Laplace kernels are implemented");
+  if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL &&
+      cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL)
+    throw InvalidArgument("qbxg_create: unknown kernel");
+  H.helm = cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL;
+  if (H.helm && nranks > 1) throw InvalidArgument("qbxg_create: Helmholtz runs on one GPU in this build");
+  if (H.helm && (cfg.p_fmm > 20 || cfg.p_qbx > 6))
+    throw InvalidArgument("qbxg_create: Helmholtz supports p_fmm <= 20, p_qbx <= 6");
+  if (H.helm && !(cfg.helmholtz_k > 0 && std::isfinite(cfg.helmholtz_k)))
+    throw InvalidArgument("qbxg_create: Helmholtz needs a positive wavenumber");
   if (cfg.p_fmm > 21) throw InvalidArgument("qbxg_create: p_fmm > 21 not supported on the GPU path");
   if (cfg.p_qbx > 8) throw InvalidArgument("qbxg_create: p_qbx > 8 not supported on the GPU path");
   qbxg_plan_view V;
@@ -741,6 +1039,12 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     }
   }
 
+  if (H.helm) {
+    helm_setup(H, V, vs, vent, s);
+    QCK(cudaGetLastError());
+    QCK(cudaStreamSynchronize(s));
+    return;
+  }
   // --- operator tables
   double2* m2l_tab = dalloc<double2>(O, size_t(1331) * D.ktab_m2l);
   double2* oct_m2m = dalloc<double2>(O, size_t(8) * D.kp);
@@ -1101,6 +1405,7 @@ int qbxg_apply_device(qbxg_handle* hp, const double* d_weights, const double* d_
   return qbxg::guarded([&] {
     if (!hp || !d_weights || !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_device: null argument");
     auto& H = hp->h;
+    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply_device: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
     qbxg::full_apply(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s);
@@ -1193,6 +1498,7 @@ int qbxg_apply(qbxg_handle* hp, const double* weights, const double* dipoles, do
   return qbxg::guarded([&] {
     if (!hp || !weights || !out_target_pot) throw qbxg::InvalidArgument("qbxg_apply: null argument");
     auto& H = hp->h;
+    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     cudaStream_t s = H.stream;
     const bool dip = H.D.dipole;
@@ -1283,6 +1589,28 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
       timings->h2d_bytes = int64_t(n_rhs) * H.ns * (dip ? 32 : 8);
       timings->d2h_bytes = int64_t(n_rhs) * H.nt * 8 + (d_coeffs ? int64_t(n_rhs) * int64_t(cbytes) : 0);
     }
+  });
+}
+
+int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, double* out_target_pot_c,
+                       double* out_center_coeffs_c, qbxg_timings* timings) {
+  return qbxg::guarded([&] {
+    if (!hp || !weights_c || !out_target_pot_c) throw qbxg::InvalidArgument("qbxg_apply_complex: null argument");
+    auto& H = hp->h;
+    if (!H.helm) throw qbxg::InvalidArgument("qbxg_apply_complex: handle was not created for the Helmholtz kernel");
+    QCK(cudaSetDevice(H.device));
+    cudaStream_t s = H.stream;
+    for (int64_t i = 0; i < 2 * H.ns; ++i)
+      if (!std::isfinite(weights_c[i])) throw qbxg::InvalidArgument("qbxg_apply_complex: non-finite weight");
+    QCK(cudaEventRecord(H.ev[11], s));
+    QCK(cudaMemcpyAsync(H.d_wc, weights_c, 2 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+    qbxg::run_helm(H, H.d_wc, H.d_potc, out_center_coeffs_c ? H.d_coeffc : nullptr, s);
+    QCK(cudaMemcpyAsync(out_target_pot_c, H.d_potc, 2 * H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    const size_t cbytes = size_t(H.nc) * 2 * H.HD.KQ * sizeof(double);
+    if (out_center_coeffs_c) QCK(cudaMemcpyAsync(out_center_coeffs_c, H.d_coeffc, cbytes, cudaMemcpyDeviceToHost, s));
+    QCK(cudaEventRecord(H.ev[12], s));
+    qbxg::fill_timings(H, timings, true, 16 * H.ns, 16 * H.nt + (out_center_coeffs_c ? int64_t(cbytes) : 0));
+    QCK(cudaStreamSynchronize(s));
   });
 }
 

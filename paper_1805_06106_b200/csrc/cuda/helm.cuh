@@ -1,0 +1,71 @@
+// Helmholtz single-layer FMM (helm_fmm.cu): device data and launchers.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace qbxg {
+namespace dev {
+
+struct HelmData {
+  double k;
+  int P, Q, KP, KQ, GL;  // orders, full table sizes (P+1)^2 / (Q+1)^2, Gaunt l-slots (P+1)
+  // tree and particles (shared with the Laplace uploads)
+  const double4* box;
+  const int* child_starts;
+  const int* children;
+  const int* parent;
+  const int* src_own_start;
+  const int* src_own_count;
+  const int* ctr_own_start;
+  const int* ctr_own_count;
+  const int* tgt_own_start;
+  const int* tgt_own_count;
+  const double4* src;  // positions (w unused)
+  const double4* ctr;  // (x, y, z, r)
+  const double4* tgt;
+  double2* hw;         // sorted complex weights
+  // expansions: full complex tables, index n^2 + n + m
+  double2* M;          // nb x KP
+  double2* L;          // nb x KP
+  double2* Lc;         // nc x KQ (sorted centre order)
+  double2* phi;        // conventional targets (sorted)
+  // lists
+  const int64_t* near_starts;
+  const int2* near_seg;
+  const int64_t* xfar_starts;
+  const int2* xfar_seg;
+  const int64_t* v_starts;
+  const int64_t* wfar_starts;
+  const int* wfar_box;
+  const double* gaunt;  // KP x KP x GL
+};
+
+// one centre-translation CTA: box, first entry in the item list, count (<= kHCtrMax)
+constexpr int kHCtrMax = 32;
+
+int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s);
+int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s);
+int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s);
+int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2* ops, cudaStream_t s);
+int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+             const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s);
+int helm_m2l_cols();
+int helm_near(const HelmData& H, const int* boxes, int n, cudaStream_t s);
+int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s);
+int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s);
+// centre translations: ctas (box, first, count) over item lists ctr_of (sorted centre)
+// and out_row (row of `out`, KQ complex each); accumulate = add into out rows
+int helm_ctr(const HelmData& H, int singular, const double2* X, int n_ctas, const int4* ctas, const int* ctr_of,
+             const int* out_row, double2* out, int accumulate, cudaStream_t s);
+int helm_pair_reduce(const HelmData& H, const int* centres, const int* starts, int n, const double2* rows,
+                     cudaStream_t s);
+int helm_m2p(const HelmData& H, const int* boxes, int n, cudaStream_t s);
+int helm_eval(const HelmData& H, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
+              const int* ctr_sorted, int n_tboxes, const int* tboxes, const int* tgt_perm, double* pot,
+              cudaStream_t s);
+int helm_centre_out(const HelmData& H, int nc, const int* ctr_perm, double* out, cudaStream_t s);
+
+}  // namespace dev
+}  // namespace qbxg

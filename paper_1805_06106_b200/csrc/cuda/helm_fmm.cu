@@ -1,0 +1,727 @@
+// Helmholtz single-layer FMM stages (BASELINE config 3) on the
+// tree, lists and stage order of the Laplace path; complex densities and
+// potentials, full tables (p+1)^2, formulation of oracle/helm_oracle.cpp:
+//   multipole M = ik sum w j_n conj(Y), phi = sum M h_n Y;  local L = ik sum w h_n conj(Y), phi = sum L j_n Y
+//   E_n^m(x+t) = sum_{n',m'} [4 pi sum_l i^{n'+l-n} G(n,m;n',m';l) F_l^{m-m'}(t)] E'_{n'}^{m'}(x)
+// Operators are not scale invariant: M2M / L2L use one dense complex operator per
+// (level, octant), M2L one per (level, offset), all built on the device from the
+// Gaunt table; M2L applies them as operator-batched complex GEMMs (CUDA cores)
+// into CSR-ordered staging rows reduced per target box.  The centre translations
+// (M2QBXL, L2QBXL) contract the box expansion with the Gaunt table once per box
+// and azimuthal index mu -- C_mu(n',m',l) = 4 pi sum_n i^{n'+l-n} G X_n^{m'+mu} --
+// and each centre then only needs its wave-function column F_l^mu(c - c_box):
+// (q+1)^2 (p+q+1) work per centre and mu instead of a per-centre operator.
+// Every output has one owner and a fixed summation order (deterministic).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "helm.cuh"
+#include "helm_math.cuh"
+
+namespace qbxg {
+namespace dev {
+namespace {
+
+using namespace hm;
+
+__device__ __forceinline__ void nm_of(int i, int& n, int& m) {
+  n = int(sqrt(double(i)));
+  while (n * n > i) --n;
+  while ((n + 1) * (n + 1) <= i) ++n;
+  m = i - n * n - n;
+}
+
+// cooperative wave-function table F[fi(l, mu)] = rad_l Y_l^mu(t), l <= P: threads
+// 0..P build one azimuthal column each, threads 0..P one radial value each;
+// rad = j_l (regular) or h_l = j_l + i y_l (singular).  Ends with __syncthreads.
+__device__ void wave_table_cta(double k, int P, double tx, double ty, double tz, bool singular, double2* F,
+                               double2* rad) {
+  const double r = sqrt(tx * tx + ty * ty + tz * tz);
+  const double x = k * r;
+  const double ct = r > 0 ? tz / r : 1.0, st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  const double ph = atan2(ty, tx);
+  for (int m = threadIdx.x; m <= P; m += blockDim.x) {
+    double mm = 1.0 / sqrt(4.0 * kPi);
+    for (int i = 1; i <= m; ++i) mm *= sqrt((2.0 * i + 1.0) / (2.0 * i)) * st;
+    double s, c;
+    sincos(m * ph, &s, &c);
+    double a = mm;
+    F[fi(m, m)] = make_double2(a * c, a * s);
+    F[fi(m, -m)] = make_double2(a * c, -a * s);
+    if (m + 1 <= P) {
+      double b = sqrt(2.0 * m + 3.0) * ct * a;
+      F[fi(m + 1, m)] = make_double2(b * c, b * s);
+      F[fi(m + 1, -m)] = make_double2(b * c, -b * s);
+      for (int n = m + 2; n <= P; ++n) {
+        const double an = sqrt((4.0 * n * n - 1.0) / (double(n) * n - double(m) * m));
+        const double bn = sqrt(((n - 1.0) * (n - 1.0) - double(m) * m) / (4.0 * (n - 1.0) * (n - 1.0) - 1.0));
+        const double cc = an * (ct * b - bn * a);
+        F[fi(n, m)] = make_double2(cc * c, cc * s);
+        F[fi(n, -m)] = make_double2(cc * c, -cc * s);
+        a = b;
+        b = cc;
+      }
+    }
+  }
+  for (int n = threadIdx.x; n <= P; n += blockDim.x) rad[n] = make_double2(sph_j1(n, x), 0.0);
+  __syncthreads();
+  if (singular && threadIdx.x == 0) {
+    double ym = -cos(x) / x, y0 = -cos(x) / (x * x) - sin(x) / x;
+    rad[0].y = ym;
+    if (P >= 1) rad[1].y = y0;
+    for (int n = 2; n <= P; ++n) {
+      const double yn = (2.0 * n - 1.0) / x * y0 - ym;
+      ym = y0;
+      y0 = yn;
+      rad[n].y = yn;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (P + 1) * (P + 1); i += blockDim.x) {
+    int n, m;
+    nm_of(i, n, m);
+    F[i] = cmul(F[i], rad[n]);
+  }
+  __syncthreads();
+}
+
+__global__ void k_h_gather(int64_t ns, const int* __restrict__ perm, const double* __restrict__ w,
+                           double2* __restrict__ hw) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int64_t o = perm[i];
+  hw[i] = make_double2(w[2 * o], w[2 * o + 1]);
+}
+
+// Stage 2 P2M at leaves: M_b += ik w conj(R_n^m(s - c_b))
+__global__ void __launch_bounds__(256) k_h_p2m(HelmData H, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* R = sm;
+  double2* rad = sm + H.KP;
+  const int b = boxes[blockIdx.x];
+  const double4 bc = H.box[b];
+  const int s0 = H.src_own_start[b], ns = H.src_own_count[b];
+  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+  for (int si = 0; si < ns; ++si) {
+    const double4 x = H.src[s0 + si];
+    const double2 w = H.hw[s0 + si];
+    __syncthreads();
+    wave_table_cta(H.k, H.P, x.x - bc.x, x.y - bc.y, x.z - bc.z, false, R, rad);
+    const double2 f = make_double2(-H.k * w.y, H.k * w.x);  // ik w
+    int slot = 0;
+    for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot)
+      acc[slot] = cfma(f, make_double2(R[i].x, -R[i].y), acc[slot]);
+  }
+  int slot = 0;
+  for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) H.M[size_t(b) * H.KP + i] = acc[slot];
+}
+
+// M2M (mode 0, CTA per parent, sum over children) / L2L (mode 1, CTA per child):
+// out[i] (+)= sum_k T[k][i] in[k], T k-major, 8 octant operators of the level
+__global__ void __launch_bounds__(512) k_h_shift(HelmData H, int mode, const int* __restrict__ boxes,
+                                                 const double2* __restrict__ ops) {
+  extern __shared__ double2 sm[];
+  double2* X = sm;
+  const int b = boxes[blockIdx.x];
+  const int KP = H.KP, i = threadIdx.x;
+  auto octant = [&](int child, int par) {
+    const double4 c = H.box[child], p = H.box[par];
+    return (c.x > p.x ? 4 : 0) + (c.y > p.y ? 2 : 0) + (c.z > p.z ? 1 : 0);
+  };
+  double2 acc = make_double2(0, 0);
+  if (mode == 0) {
+    for (int kk = H.child_starts[b]; kk < H.child_starts[b + 1]; ++kk) {
+      const int c = H.children[kk];
+      const double2* T = ops + size_t(octant(c, b)) * KP * KP;
+      __syncthreads();
+      for (int j = threadIdx.x; j < KP; j += blockDim.x) X[j] = H.M[size_t(c) * KP + j];
+      __syncthreads();
+      if (i < KP)
+        for (int k2 = 0; k2 < KP; ++k2) acc = cfma(T[size_t(k2) * KP + i], X[k2], acc);
+    }
+    if (i < KP) H.M[size_t(b) * KP + i] = acc;
+  } else {
+    const int a = H.parent[b];
+    const double2* T = ops + size_t(octant(b, a)) * KP * KP;
+    for (int j = threadIdx.x; j < KP; j += blockDim.x) X[j] = H.L[size_t(a) * KP + j];
+    __syncthreads();
+    if (i < KP) {
+      for (int k2 = 0; k2 < KP; ++k2) acc = cfma(T[size_t(k2) * KP + i], X[k2], acc);
+      const double2 v = H.L[size_t(b) * KP + i];
+      H.L[size_t(b) * KP + i] = make_double2(v.x + acc.x, v.y + acc.y);
+    }
+  }
+}
+
+// operator builder, one CTA per operator: T[k][i] = 4 pi sum_l i^{n'+l-n} G F_l^{m-m'}(t)
+__global__ void __launch_bounds__(256) k_h_build_ops(HelmData H, const double4* __restrict__ shifts,
+                                                     double2* __restrict__ ops) {
+  extern __shared__ double2 sm[];
+  const int P = H.P, KP = H.KP, L = 2 * P;
+  double2* F = sm;
+  double2* rad = sm + (L + 1) * (L + 1);
+  const double4 t = shifts[blockIdx.x];  // (tx, ty, tz, singular)
+  wave_table_cta(H.k, L, t.x, t.y, t.z, t.w != 0.0, F, rad);
+  double2* T = ops + size_t(blockIdx.x) * KP * KP;
+  for (int e = threadIdx.x; e < KP * KP; e += blockDim.x) {
+    const int kin = e / KP, iout = e % KP;
+    int n, m, n2, m2;
+    nm_of(kin, n, m);
+    nm_of(iout, n2, m2);
+    const double* g = H.gaunt + (size_t(kin) * KP + iout) * H.GL;
+    double2 acc = make_double2(0, 0);
+    const int l0 = abs(n - n2);
+    for (int li = 0; li < H.GL; ++li) {
+      const int l = l0 + 2 * li;
+      if (l > n + n2) break;
+      const double gv = g[li];
+      if (gv == 0.0 || abs(m - m2) > l) continue;
+      const double2 f = cmul(ipow(n2 + l - n), F[fi(l, m - m2)]);
+      acc.x += gv * f.x;
+      acc.y += gv * f.y;
+    }
+    T[e] = make_double2(4.0 * kPi * acc.x, 4.0 * kPi * acc.y);
+  }
+}
+
+// Stage 4 M2L: one CTA per (operator, up to kHCols List-2 entries); thread per output row
+constexpr int kHCols = 8;
+__global__ void __launch_bounds__(512) k_h_m2l(HelmData H, const int4* __restrict__ tiles,
+                                               const int* __restrict__ col_src, const int* __restrict__ col_pos,
+                                               const double2* __restrict__ ops, double2* __restrict__ temp) {
+  extern __shared__ double2 sm[];
+  double2* B = sm;  // kHCols x KP
+  const int4 tile = tiles[blockIdx.x];
+  const int KP = H.KP;
+  for (int e = threadIdx.x; e < kHCols * KP; e += blockDim.x) {
+    const int c = e / KP, kk = e % KP;
+    B[e] = c < tile.z ? H.M[size_t(col_src[tile.y + c]) * KP + kk] : make_double2(0, 0);
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= KP) return;
+  const double2* T = ops + size_t(tile.x) * KP * KP;
+  double2 acc[kHCols];
+#pragma unroll
+  for (int c = 0; c < kHCols; ++c) acc[c] = make_double2(0, 0);
+  for (int kk = 0; kk < KP; ++kk) {
+    const double2 a = T[size_t(kk) * KP + i];
+#pragma unroll
+    for (int c = 0; c < kHCols; ++c) acc[c] = cfma(a, B[c * KP + kk], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kHCols; ++c)
+    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KP + i] = acc[c];
+}
+
+__global__ void __launch_bounds__(512) k_h_m2l_reduce(HelmData H, const int* __restrict__ boxes, int64_t base,
+                                                      const double2* __restrict__ temp) {
+  const int b = boxes[blockIdx.x];
+  const int i = threadIdx.x;
+  if (i >= H.KP) return;
+  double2 s = make_double2(0, 0);
+  for (int64_t pos = H.v_starts[b]; pos < H.v_starts[b + 1]; ++pos) {
+    const double2 v = temp[size_t(pos - base) * H.KP + i];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  const double2 v = H.L[size_t(b) * H.KP + i];
+  H.L[size_t(b) * H.KP + i] = make_double2(v.x + s.x, v.y + s.y);
+}
+
+// Stages 3, 5a, 6a: P2QBXL (thread per (centre, source slice)) and P2P
+template <int Q>
+__global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restrict__ boxes) {
+  constexpr int KQ = (Q + 1) * (Q + 1);
+  extern __shared__ double2 red[];  // KQ x 128
+  const int b = boxes[blockIdx.x];
+  const int nctr = H.ctr_own_count[b], c0 = H.ctr_own_start[b];
+  const int64_t sb = H.near_starts[b], se = H.near_starts[b + 1];
+  for (int cc = 0; cc < nctr; cc += 128) {
+    const int ncc = min(128, nctr - cc);
+    const int S = 128 / ncc;
+    const int ci = threadIdx.x / S, sl = threadIdx.x % S;
+    const bool active = ci < ncc;
+    double4 c = make_double4(0, 0, 0, 1);
+    if (active) c = H.ctr[c0 + cc + ci];
+    double2 acc[KQ];
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) acc[i] = make_double2(0, 0);
+    if (active) {
+      int f = sl;
+      for (int64_t sg = sb; sg < se; ++sg) {
+        const int2 seg = H.near_seg[sg];
+        for (; f < seg.y; f += S) {
+          const int s = seg.x + f;
+          const double4 x = H.src[s];
+          const double2 w = H.hw[s];
+          const double vx = x.x - c.x, vy = x.y - c.y, vz = x.z - c.z;
+          const double xr = H.k * sqrt(vx * vx + vy * vy + vz * vz);
+          double2 Y[KQ];
+          ylm_all(Q, vx, vy, vz, Y);
+          double ym = -cos(xr) / xr, y0 = -cos(xr) / (xr * xr) - sin(xr) / xr;
+          const double2 f0 = make_double2(-H.k * w.y, H.k * w.x);
+#pragma unroll
+          for (int n = 0; n <= Q; ++n) {
+            double yn;
+            if (n == 0) {
+              yn = ym;
+            } else if (n == 1) {
+              yn = y0;
+            } else {
+              yn = (2.0 * n - 1.0) / xr * y0 - ym;
+              ym = y0;
+              y0 = yn;
+            }
+            const double2 fh = cmul(f0, make_double2(sph_j1(n, xr), yn));
+#pragma unroll
+            for (int m = -n; m <= n; ++m)
+              acc[fi(n, m)] = cfma(fh, make_double2(Y[fi(n, m)].x, -Y[fi(n, m)].y), acc[fi(n, m)]);
+          }
+        }
+        f -= seg.y;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) red[i * 128 + threadIdx.x] = acc[i];
+    __syncthreads();
+    if (active && sl == 0) {
+      double2* out = H.Lc + size_t(c0 + cc + ci) * KQ;
+      for (int i = 0; i < KQ; ++i) {
+        double2 s = make_double2(0, 0);
+        for (int k2 = 0; k2 < S; ++k2) {
+          s.x += red[i * 128 + threadIdx.x + k2].x;
+          s.y += red[i * 128 + threadIdx.x + k2].y;
+        }
+        out[i] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) k_h_p2p(HelmData H, const int* __restrict__ boxes) {
+  const int b = boxes[blockIdx.x];
+  const int ntg = H.tgt_own_count[b], t0 = H.tgt_own_start[b];
+  for (int ti = threadIdx.x; ti < ntg; ti += blockDim.x) {
+    const double4 t = H.tgt[t0 + ti];
+    double2 acc = make_double2(0, 0);
+    for (int64_t sg = H.near_starts[b]; sg < H.near_starts[b + 1]; ++sg) {
+      const int2 seg = H.near_seg[sg];
+      for (int j = 0; j < seg.y; ++j) {
+        const double4 x = H.src[seg.x + j];
+        const double dx = t.x - x.x, dy = t.y - x.y, dz = t.z - x.z;
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        double s, co;
+        sincos(H.k * r, &s, &co);
+        acc = cfma(H.hw[seg.x + j], make_double2(co / (4.0 * kPi * r), s / (4.0 * kPi * r)), acc);
+      }
+    }
+    H.phi[t0 + ti] = acc;
+  }
+}
+
+// Stage 6b P2L over List 4 far: L_b += ik w h_n conj(Y) = ik w (h_n Y)_n^{-m}
+__global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* T = sm;
+  double2* rad = sm + H.KP;
+  const int b = boxes[blockIdx.x];
+  const double4 bc = H.box[b];
+  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+  for (int64_t sg = H.xfar_starts[b]; sg < H.xfar_starts[b + 1]; ++sg) {
+    const int2 seg = H.xfar_seg[sg];
+    for (int j = 0; j < seg.y; ++j) {
+      const double4 x = H.src[seg.x + j];
+      const double2 w = H.hw[seg.x + j];
+      __syncthreads();
+      wave_table_cta(H.k, H.P, x.x - bc.x, x.y - bc.y, x.z - bc.z, true, T, rad);
+      const double2 f = make_double2(-H.k * w.y, H.k * w.x);
+      int slot = 0;
+      for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) {
+        int n, m;
+        nm_of(i, n, m);
+        acc[slot] = cfma(f, T[fi(n, -m)], acc[slot]);
+      }
+    }
+  }
+  int slot = 0;
+  for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) {
+    const double2 v = H.L[size_t(b) * H.KP + i];
+    H.L[size_t(b) * H.KP + i] = make_double2(v.x + acc[slot].x, v.y + acc[slot].y);
+  }
+}
+
+// Stage 5b M2QBXL / Stage 8 L2QBXL: box expansion X (order p) -> up to kHCtrMax
+// centres (order q).  For mu = -(p+q)..p+q: C_mu[i'][l] from X and the Gaunt
+// table, F_l^mu(c_j - c_box) per centre, acc[j][i'] += sum_l F C.
+constexpr int kHCtrAcc = (kHCtrMax * 81 + 255) / 256;  // per-thread outputs (q <= 8, 256 threads)
+__global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const double2* __restrict__ X,
+                                               const int4* __restrict__ ctas, const int* __restrict__ ctr_of,
+                                               const int* __restrict__ out_row, double2* __restrict__ out,
+                                               int accumulate) {
+  extern __shared__ double2 sm[];
+  const int P = H.P, Q = H.Q, KP = H.KP, KQ = H.KQ, L = P + Q, NL = L + 1;
+  const int4 cta = ctas[blockIdx.x];  // (box, first item, count, -)
+  const int nctr = cta.z;
+  double2* Xs = sm;                      // KP
+  double2* Cm = Xs + KP;                 // KQ x NL
+  double2* rad = Cm + KQ * NL;           // kHCtrMax x NL
+  double2* Fc = rad + kHCtrMax * NL;     // kHCtrMax x NL
+  double* geo = reinterpret_cast<double*>(Fc + kHCtrMax * NL);  // kHCtrMax x 4: cos t, sin t, phi, |t|
+  const double4 bc = H.box[cta.x];
+  for (int j = threadIdx.x; j < KP; j += blockDim.x) Xs[j] = X[size_t(cta.x) * KP + j];
+  for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
+    const double4 c = H.ctr[ctr_of[cta.y + j]];
+    const double tx = c.x - bc.x, ty = c.y - bc.y, tz = c.z - bc.z;
+    const double r = sqrt(tx * tx + ty * ty + tz * tz);
+    const double ct = r > 0 ? tz / r : 1.0;
+    geo[4 * j] = ct;
+    geo[4 * j + 1] = sqrt(fmax(0.0, 1.0 - ct * ct));
+    geo[4 * j + 2] = atan2(ty, tx);
+    geo[4 * j + 3] = r;
+    const double x = H.k * r;
+    double ym = -cos(x) / x, y0 = -cos(x) / (x * x) - sin(x) / x;
+    for (int l = 0; l <= L; ++l) {
+      double yl = 0.0;
+      if (singular) {
+        if (l == 0) {
+          yl = ym;
+        } else if (l == 1) {
+          yl = y0;
+        } else {
+          yl = (2.0 * l - 1.0) / x * y0 - ym;
+          ym = y0;
+          y0 = yl;
+        }
+      }
+      rad[j * NL + l] = make_double2(sph_j1(l, x), yl);
+    }
+  }
+  double2 acc[kHCtrAcc];
+#pragma unroll
+  for (int a = 0; a < kHCtrAcc; ++a) acc[a] = make_double2(0, 0);
+  __syncthreads();
+  for (int mu = -L; mu <= L; ++mu) {
+    const int amu = abs(mu);
+    // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu}
+    for (int e = threadIdx.x; e < KQ * NL; e += blockDim.x) {
+      const int iout = e / NL, l = e % NL;
+      double2 cacc = make_double2(0, 0);
+      if (l >= amu) {
+        int n2, m2;
+        nm_of(iout, n2, m2);
+        const int m = m2 + mu;
+        const int nlo = max(max(abs(m), abs(l - n2)), 0), nhi = min(P, l + n2);
+        for (int n = nlo; n <= nhi; ++n) {
+          if ((n + n2 + l) & 1) continue;
+          if (l < abs(n - n2)) continue;
+          const int li = (l - abs(n - n2)) >> 1;
+          const double gv = H.gaunt[(size_t(fi(n, m)) * KP + iout) * H.GL + li];
+          if (gv == 0.0) continue;
+          const double2 t = cmul(ipow(n2 + l - n), Xs[fi(n, m)]);
+          cacc.x += gv * t.x;
+          cacc.y += gv * t.y;
+        }
+      }
+      Cm[e] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
+    }
+    // F column mu per centre: rad_l Y_l^mu(t), l = |mu|..L
+    for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
+      const double ct = geo[4 * j], st = geo[4 * j + 1], ph = geo[4 * j + 2];
+      double mm = 1.0 / sqrt(4.0 * kPi);
+      for (int i = 1; i <= amu; ++i) mm *= sqrt((2.0 * i + 1.0) / (2.0 * i)) * st;
+      double s, c;
+      sincos(mu * ph, &s, &c);
+      double a = mm, b = 0.0;
+      for (int l = amu; l <= L; ++l) {
+        double pl;
+        if (l == amu) {
+          pl = a;
+        } else if (l == amu + 1) {
+          b = sqrt(2.0 * amu + 3.0) * ct * a;
+          pl = b;
+        } else {
+          const double an = sqrt((4.0 * l * l - 1.0) / (double(l) * l - double(amu) * amu));
+          const double bn = sqrt(((l - 1.0) * (l - 1.0) - double(amu) * amu) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
+          pl = an * (ct * b - bn * a);
+          a = b;
+          b = pl;
+        }
+        Fc[j * NL + l] = cmul(rad[j * NL + l], make_double2(pl * c, pl * s));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < kHCtrAcc; ++a) {
+      const int e = threadIdx.x + a * blockDim.x;
+      if (e < nctr * KQ) {
+        const int j = e / KQ, iout = e % KQ;
+        double2 s2 = acc[a];
+        for (int l = amu; l <= L; ++l) s2 = cfma(Fc[j * NL + l], Cm[iout * NL + l], s2);
+        acc[a] = s2;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < kHCtrAcc; ++a) {
+    const int e = threadIdx.x + a * blockDim.x;
+    if (e < nctr * KQ) {
+      const int j = e / KQ, iout = e % KQ;
+      double2* o = out + size_t(out_row[cta.y + j]) * KQ + iout;
+      if (accumulate) {
+        const double2 v = *o;
+        *o = make_double2(v.x + acc[a].x, v.y + acc[a].y);
+      } else {
+        *o = acc[a];
+      }
+    }
+  }
+}
+
+__global__ void k_h_pair_reduce(HelmData H, const int* __restrict__ centres, const int* __restrict__ starts, int n,
+                                const double2* __restrict__ rows) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(n) * H.KQ) return;
+  const int i = int(t / H.KQ), j = int(t % H.KQ);
+  double2 a = H.Lc[size_t(centres[i]) * H.KQ + j];
+  for (int p2 = starts[i]; p2 < starts[i + 1]; ++p2) {
+    const double2 v = rows[size_t(p2) * H.KQ + j];
+    a.x += v.x;
+    a.y += v.y;
+  }
+  H.Lc[size_t(centres[i]) * H.KQ + j] = a;
+}
+
+// M2P at conventional targets of boxes with List 3 far entries
+__global__ void __launch_bounds__(128) k_h_m2p(HelmData H, const int* __restrict__ boxes) {
+  extern __shared__ double2 sm[];
+  double2* S = sm;
+  double2* rad = sm + H.KP;
+  __shared__ double2 part[128];
+  const int b = boxes[blockIdx.x];
+  for (int j = 0; j < H.tgt_own_count[b]; ++j) {
+    const int ts = H.tgt_own_start[b] + j;
+    const double4 t = H.tgt[ts];
+    double2 tot = make_double2(0, 0);
+    for (int64_t e = H.wfar_starts[b]; e < H.wfar_starts[b + 1]; ++e) {
+      const int d = H.wfar_box[e];
+      const double4 dc = H.box[d];
+      __syncthreads();
+      wave_table_cta(H.k, H.P, t.x - dc.x, t.y - dc.y, t.z - dc.z, true, S, rad);
+      double2 a = make_double2(0, 0);
+      for (int i = threadIdx.x; i < H.KP; i += blockDim.x) a = cfma(H.M[size_t(d) * H.KP + i], S[i], a);
+      part[threadIdx.x] = a;
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int i = 0; i < blockDim.x; ++i) {
+          tot.x += part[i].x;
+          tot.y += part[i].y;
+        }
+    }
+    if (threadIdx.x == 0) {
+      const double2 v = H.phi[ts];
+      H.phi[ts] = make_double2(v.x + tot.x, v.y + tot.y);
+    }
+  }
+}
+
+// Stage 9
+__global__ void k_h_eval_assoc(HelmData H, int n, const int* __restrict__ items, const double* __restrict__ tpos,
+                               const int* __restrict__ assoc, const int* __restrict__ ctr_sorted,
+                               double* __restrict__ pot) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = items[t];
+  const int cs = ctr_sorted[assoc[i]];
+  const double4 c = H.ctr[cs];
+  const double vx = tpos[3 * i] - c.x, vy = tpos[3 * i + 1] - c.y, vz = tpos[3 * i + 2] - c.z;
+  const double x = H.k * sqrt(vx * vx + vy * vy + vz * vz);
+  double2 Y[(kHQmax + 1) * (kHQmax + 1)];
+  ylm_all(H.Q, vx, vy, vz, Y);
+  double2 a = make_double2(0, 0);
+  for (int nn = 0; nn <= H.Q; ++nn) {
+    const double jn = sph_j1(nn, x);
+    for (int m = -nn; m <= nn; ++m) {
+      const double2 v = cmul(H.Lc[size_t(cs) * H.KQ + fi(nn, m)], Y[fi(nn, m)]);
+      a.x += jn * v.x;
+      a.y += jn * v.y;
+    }
+  }
+  pot[2 * size_t(i)] = a.x;
+  pot[2 * size_t(i) + 1] = a.y;
+}
+
+__global__ void __launch_bounds__(128) k_h_eval_conv(HelmData H, const int* __restrict__ boxes,
+                                                     const int* __restrict__ tgt_perm, double* __restrict__ pot) {
+  extern __shared__ double2 sm[];
+  double2* R = sm;
+  double2* rad = sm + H.KP;
+  __shared__ double2 part[128];
+  const int b = boxes[blockIdx.x];
+  const double4 bc = H.box[b];
+  for (int j = 0; j < H.tgt_own_count[b]; ++j) {
+    const int ts = H.tgt_own_start[b] + j;
+    const double4 t = H.tgt[ts];
+    __syncthreads();
+    wave_table_cta(H.k, H.P, t.x - bc.x, t.y - bc.y, t.z - bc.z, false, R, rad);
+    double2 a = make_double2(0, 0);
+    for (int i = threadIdx.x; i < H.KP; i += blockDim.x) a = cfma(H.L[size_t(b) * H.KP + i], R[i], a);
+    part[threadIdx.x] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 s = H.phi[ts];
+      for (int i = 0; i < blockDim.x; ++i) {
+        s.x += part[i].x;
+        s.y += part[i].y;
+      }
+      pot[2 * size_t(tgt_perm[ts])] = s.x;
+      pot[2 * size_t(tgt_perm[ts]) + 1] = s.y;
+    }
+  }
+}
+
+__global__ void k_h_centre_out(HelmData H, int nc, const int* __restrict__ ctr_perm, double* __restrict__ out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(nc) * H.KQ) return;
+  const int cs = int(t / H.KQ), i = int(t % H.KQ);
+  const double2 v = H.Lc[t];
+  const int64_t o = (int64_t(ctr_perm[cs]) * H.KQ + i) * 2;
+  out[o] = v.x;
+  out[o + 1] = v.y;
+}
+
+template <int Q>
+void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  const size_t smem = size_t((Q + 1) * (Q + 1)) * 128 * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_h_near<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_h_near<Q><<<n, 128, smem, s>>>(H, boxes);
+}
+
+}  // namespace
+
+int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s) {
+  if (ns == 0) return 0;
+  k_h_gather<<<unsigned((ns + 255) / 256), 256, 0, s>>>(ns, perm, w, H.hw);
+  return 1;
+}
+
+int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_h_p2m<<<n, 256, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, leaves);
+  return 1;
+}
+
+int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s) {
+  if (n == 0) return 0;
+  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
+  k_h_shift<<<n, th, H.KP * sizeof(double2), s>>>(H, mode, boxes, ops);
+  return 1;
+}
+
+int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2* ops, cudaStream_t s) {
+  if (n_ops == 0) return 0;
+  const int L = 2 * H.P;
+  const size_t smem = size_t((L + 1) * (L + 1) + L + 1) * sizeof(double2);
+  cudaFuncSetAttribute(k_h_build_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_h_build_ops<<<n_ops, 256, smem, s>>>(H, shifts, ops);
+  return 1;
+}
+
+int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+             const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s) {
+  if (n_tiles == 0) return 0;
+  const size_t smem = size_t(kHCols) * H.KP * sizeof(double2);
+  cudaFuncSetAttribute(k_h_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
+  k_h_m2l<<<n_tiles, th, smem, s>>>(H, tiles, col_src, col_pos, ops, temp);
+  k_h_m2l_reduce<<<n_boxes, th, 0, s>>>(H, boxes, base, temp);
+  return 2;
+}
+
+int helm_m2l_cols() { return kHCols; }
+
+int helm_near(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  switch (H.Q) {
+    case 0: near_q<0>(H, boxes, n, s); break;
+    case 1: near_q<1>(H, boxes, n, s); break;
+    case 2: near_q<2>(H, boxes, n, s); break;
+    case 3: near_q<3>(H, boxes, n, s); break;
+    case 4: near_q<4>(H, boxes, n, s); break;
+    case 5: near_q<5>(H, boxes, n, s); break;
+    case 6: near_q<6>(H, boxes, n, s); break;
+    default: return -1;
+  }
+  return 1;
+}
+
+int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_h_p2p<<<n, 128, 0, s>>>(H, boxes);
+  return 1;
+}
+
+int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_h_p2l<<<n, 256, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, boxes);
+  return 1;
+}
+
+int helm_ctr(const HelmData& H, int singular, const double2* X, int n_ctas, const int4* ctas, const int* ctr_of,
+             const int* out_row, double2* out, int accumulate, cudaStream_t s) {
+  if (n_ctas == 0) return 0;
+  const int NL = H.P + H.Q + 1;
+  const size_t smem =
+      size_t(H.KP + H.KQ * NL + 2 * kHCtrMax * NL) * sizeof(double2) + size_t(4 * kHCtrMax) * sizeof(double);
+  cudaFuncSetAttribute(k_h_ctr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_h_ctr<<<n_ctas, 256, smem, s>>>(H, singular, X, ctas, ctr_of, out_row, out, accumulate);
+  return 1;
+}
+
+int helm_pair_reduce(const HelmData& H, const int* centres, const int* starts, int n, const double2* rows,
+                     cudaStream_t s) {
+  if (n == 0) return 0;
+  const int64_t nt = int64_t(n) * H.KQ;
+  k_h_pair_reduce<<<unsigned((nt + 255) / 256), 256, 0, s>>>(H, centres, starts, n, rows);
+  return 1;
+}
+
+int helm_m2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_h_m2p<<<n, 128, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, boxes);
+  return 1;
+}
+
+int helm_eval(const HelmData& H, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
+              const int* ctr_sorted, int n_tboxes, const int* tboxes, const int* tgt_perm, double* pot,
+              cudaStream_t s) {
+  int k = 0;
+  if (n_assoc) {
+    k_h_eval_assoc<<<(n_assoc + 127) / 128, 128, 0, s>>>(H, n_assoc, assoc_items, tpos, assoc, ctr_sorted, pot);
+    ++k;
+  }
+  if (n_tboxes) {
+    k_h_eval_conv<<<n_tboxes, 128, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, tboxes, tgt_perm, pot);
+    ++k;
+  }
+  return k;
+}
+
+int helm_centre_out(const HelmData& H, int nc, const int* ctr_perm, double* out, cudaStream_t s) {
+  if (nc == 0) return 0;
+  const int64_t nt = int64_t(nc) * H.KQ;
+  k_h_centre_out<<<unsigned((nt + 255) / 256), 256, 0, s>>>(H, nc, ctr_perm, out);
+  return 1;
+}
+
+}  // namespace dev
+}  // namespace qbxg

@@ -22,6 +22,8 @@ struct CudaError : std::runtime_error { using std::runtime_error::runtime_error;
 struct NcclError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 void set_last_error(const std::string& msg);
+// Helmholtz translation Gaunt table (helm_tables.cpp): (P+1)^4 x (P+1) doubles
+std::vector<double> helm_gaunt_table(int P);
 const char* get_last_error();
 
 // Run f, translating exceptions to status codes; never lets one escape.

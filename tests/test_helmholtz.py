@@ -126,3 +126,30 @@ def test_gpu_helm_direct_qbx_matches_oracle(q):
     pot = api.helm_direct_qbx(K, g, w, q)
     ref = O.helm_direct_qbx(K, g, w, q)
     assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfgid,kw,p,q", [(3, dict(level=1), 6, 3), (3, dict(level=1), 10, 5),
+                                          (2, dict(level=1, n_volume_targets=300), 8, 4)])
+def test_gpu_helmholtz_fmm_matches_oracle(cfgid, kw, p, q):
+    """Stages 2-9 for G_k on the GPU (qbxg_apply_complex) against the oracle on the same plan."""
+    g = api.config_geometry(cfgid, **kw)
+    rng = np.random.default_rng(3)
+    w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
+    cfg = api.FmmConfig(p_fmm=p, p_qbx=q, n_max=64, kernel=2, helmholtz_k=K)
+    plan = api.Plan(cfg, g)
+    eng = api.FmmEngine(cfg, g, plan)
+    pot, cc = eng.apply_complex(w, want_centers=True)
+    again = eng.apply_complex(w)
+    eng.close()
+    ref, cref = O.helm_execute(plan, g, K, p, q, w, want_centers=True)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
+    assert np.linalg.norm(cc - cref) / np.linalg.norm(cref) <= 1e-11
+    assert np.array_equal(pot, again), "Helmholtz apply is not bitwise deterministic"
+
+
+def test_helmholtz_handle_rejects_real_apply():
+    """A Helmholtz plan needs a wavenumber; a Laplace call on it is refused (host-side checks)."""
+    g = api.config_geometry(0)
+    with pytest.raises(ValueError, match="wavenumber"):
+        api.Plan(api.FmmConfig(p_fmm=6, p_qbx=3, kernel=2, helmholtz_k=0.0), g)
