@@ -211,7 +211,8 @@ def config_fmm(config_id: int, **overrides) -> FmmConfig:
     PAPER.md:2246-2256) uses the spec's cost-balance threshold p^3/q^2
     (SPEC.md:382); pass w_far_demote=0 to disable it."""
     p, q, k = CONFIG_ORDERS[config_id]
-    cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k, w_far_demote=(p ** 3) // max(q * q, 1))
+    cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k, w_far_demote=(p ** 3) // max(q * q, 1),
+                    helmholtz_k=3.0 if k == _abi.KERNEL_HELMHOLTZ_SL else 0.0)  # config 3: k = 3
     for key, v in overrides.items():
         setattr(cfg, key, v)
     return cfg
