@@ -478,6 +478,7 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.Lc = dalloc<double2>(O, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ);
   HD.phi = dalloc<double2>(O, std::max<int64_t>(H.nconv, 1));
   HD.gaunt = dupload(O, helm_gaunt_table(p), s);
+  dev::helm_upload_constants();
   H.d_wc = dalloc<double>(O, 2 * std::max<int64_t>(H.ns, 1));
   H.d_potc = dalloc<double>(O, 2 * std::max<int64_t>(H.nt, 1));
   H.d_coeffc = dalloc<double>(O, 2 * std::max<int64_t>(H.nc, 1) * HD.KQ);

@@ -45,6 +45,7 @@ struct HelmData {
 // one centre-translation CTA: box, first entry in the item list, count (<= kHCtrMax)
 constexpr int kHCtrMax = 32;
 
+void helm_upload_constants();  // solid-harmonic recurrence tables (this TU's __constant__)
 int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s);
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s);
 int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s);

@@ -231,14 +231,87 @@ __global__ void __launch_bounds__(512) k_h_m2l_reduce(HelmData H, const int* __r
   H.L[size_t(b) * H.KP + i] = make_double2(v.x + s.x, v.y + s.y);
 }
 
-// Stages 3, 5a, 6a: P2QBXL (thread per (centre, source slice)) and P2P
+// Recurrence coefficients of the fully normalised solid harmonics
+// S_n^m(v) = |v|^n Y_n^m(v/|v|) (m >= 0), a polynomial in (x, y, z):
+//   S_m^m = a_m (x + i y) S_{m-1}^{m-1},  S_{m+1}^m = b_m z S_m^m,
+//   S_n^m = c_nm (z S_{n-1}^m - d_nm |v|^2 S_{n-2}^m)
+// (the normalised-Legendre recurrences times |v|^n; no trigonometry, no square roots
+// per pair).  Filled by helm_upload_constants().
+constexpr int kHSolid = 10;  // degrees covered (q <= 8, + 1)
+__constant__ double c_sa[kHSolid + 1], c_sb[kHSolid + 1];
+__constant__ double c_sc[(kHSolid + 1) * (kHSolid + 1)], c_sd[(kHSolid + 1) * (kHSolid + 1)];
+
+// j_n(k r) / r^n and y_n(k r) / r^n for n <= Q without divisions in the loops:
+//   Jt_n = j_n / r^n:  series for Jt_Q, Jt_{Q+1} (x < 1), then Jt_{n-1} = (2n+1)/k Jt_n - r^2 Jt_{n+1}
+//   Yt_n = y_n / r^n:  Yt_{n+1} = ((2n+1)/k Yt_n - Yt_{n-1}) / r^2
+constexpr int kHSer = 14;
+__constant__ double c_jser[(kHSolid + 2) * kHSer];  // -1/(2 t (2n+2t+1))
+__constant__ double c_odd[2 * kHSolid + 4];          // 2n+1 and 1/(2n+1) interleaved
+
+template <int Q>
+__device__ __forceinline__ void radial_over_rn(double k, double r, double ir, double2 (&g)[Q + 1]) {
+  const double x = k * r, x2 = x * x, r2 = r * r, ik = 1.0 / k, ir2 = ir * ir;
+  double jt[Q + 2];
+  if (x < 1.0) {
+    double kn = 1.0;  // k^n / (2n+1)!!
+    for (int n = 1; n <= Q; ++n) kn *= k * c_odd[2 * n + 1];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = Q + e;
+      if (e == 1) kn *= k * c_odd[2 * n + 1];
+      double term = 1.0, sum = 1.0;
+#pragma unroll
+      for (int t = 1; t <= kHSer; ++t) {
+        term *= x2 * c_jser[n * kHSer + t - 1];
+        sum += term;
+      }
+      jt[n] = kn * sum;
+    }
+#pragma unroll
+    for (int n = Q + 1; n >= 1; --n) {
+      const double nxt = n + 1 <= Q + 1 ? jt[n + 1] : 0.0;
+      if (n <= Q) jt[n - 1] = c_odd[2 * n] * ik * jt[n] - r2 * nxt;
+      else jt[n - 1] = jt[n - 1];
+    }
+  } else {
+    double irn = 1.0;
+#pragma unroll
+    for (int n = 0; n <= Q; ++n) {
+      jt[n] = sph_j1(n, x) * irn;
+      irn *= ir;
+    }
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double ix = ik * ir;
+  double ym = -cs * ix, y0 = (-cs * ix * ix - sn * ix) * ir;
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) {
+    double yn;
+    if (n == 0) {
+      yn = ym;
+    } else if (n == 1) {
+      yn = y0;
+    } else {
+      yn = (c_odd[2 * (n - 1)] * ik * y0 - ym) * ir2;
+      ym = y0;
+      y0 = yn;
+    }
+    g[n] = make_double2(jt[n], yn);
+  }
+}
+
+// Stages 3, 5a, 6a: P2QBXL, thread per (centre, source slice):
+//   Lc_n^m += ik w h_n(k r) conj(Y_n^m) = [ik w h_n(k r) / r^n] conj(S_n^m)   (S^{-m} = conj S^m)
 template <int Q>
 __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restrict__ boxes) {
   constexpr int KQ = (Q + 1) * (Q + 1);
+  constexpr int KH = (Q + 1) * (Q + 2) / 2;
   extern __shared__ double2 red[];  // KQ x 128
   const int b = boxes[blockIdx.x];
   const int nctr = H.ctr_own_count[b], c0 = H.ctr_own_start[b];
   const int64_t sb = H.near_starts[b], se = H.near_starts[b + 1];
+  const double k = H.k;
   for (int cc = 0; cc < nctr; cc += 128) {
     const int ncc = min(128, nctr - cc);
     const int S = 128 / ncc;
@@ -258,27 +331,41 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
           const double4 x = H.src[s];
           const double2 w = H.hw[s];
           const double vx = x.x - c.x, vy = x.y - c.y, vz = x.z - c.z;
-          const double xr = H.k * sqrt(vx * vx + vy * vy + vz * vz);
-          double2 Y[KQ];
-          ylm_all(Q, vx, vy, vz, Y);
-          double ym = -cos(xr) / xr, y0 = -cos(xr) / (xr * xr) - sin(xr) / xr;
-          const double2 f0 = make_double2(-H.k * w.y, H.k * w.x);
+          const double r2 = vx * vx + vy * vy + vz * vz;
+          const double r = sqrt(r2), ir = 1.0 / r;
+          double2 Sh[KH];  // S_n^m, m >= 0, index n(n+1)/2 + m
+#pragma unroll
+          for (int m = 0; m <= Q; ++m) {
+            const int dm = m * (m + 1) / 2 + m;
+            if (m == 0) {
+              Sh[0] = make_double2(0.28209479177387814347, 0.0);  // 1/sqrt(4 pi)
+            } else {
+              const double2 d = Sh[(m - 1) * m / 2 + m - 1];
+              Sh[dm] = make_double2(c_sa[m] * (d.x * vx - d.y * vy), c_sa[m] * (d.x * vy + d.y * vx));
+            }
+            if (m + 1 <= Q) {
+              const double f1 = c_sb[m] * vz;
+              Sh[(m + 1) * (m + 2) / 2 + m] = make_double2(f1 * Sh[dm].x, f1 * Sh[dm].y);
+            }
+#pragma unroll
+            for (int n = m + 2; n <= Q; ++n) {
+              const double cn = c_sc[n * (kHSolid + 1) + m], dn = c_sd[n * (kHSolid + 1) + m] * r2;
+              const double2 a1 = Sh[(n - 1) * n / 2 + m], a2 = Sh[(n - 2) * (n - 1) / 2 + m];
+              Sh[n * (n + 1) / 2 + m] = make_double2(cn * (vz * a1.x - dn * a2.x), cn * (vz * a1.y - dn * a2.y));
+            }
+          }
+          double2 g[Q + 1];
+          radial_over_rn<Q>(k, r, ir, g);
+          const double2 f0 = make_double2(-k * w.y, k * w.x);  // ik w
 #pragma unroll
           for (int n = 0; n <= Q; ++n) {
-            double yn;
-            if (n == 0) {
-              yn = ym;
-            } else if (n == 1) {
-              yn = y0;
-            } else {
-              yn = (2.0 * n - 1.0) / xr * y0 - ym;
-              ym = y0;
-              y0 = yn;
-            }
-            const double2 fh = cmul(f0, make_double2(sph_j1(n, xr), yn));
+            const double2 fh = cmul(f0, g[n]);
 #pragma unroll
-            for (int m = -n; m <= n; ++m)
-              acc[fi(n, m)] = cfma(fh, make_double2(Y[fi(n, m)].x, -Y[fi(n, m)].y), acc[fi(n, m)]);
+            for (int m = 0; m <= n; ++m) {
+              const double2 sv = Sh[n * (n + 1) / 2 + m];
+              acc[fi(n, m)] = cfma(fh, make_double2(sv.x, -sv.y), acc[fi(n, m)]);  // conj(S_n^m)
+              if (m > 0) acc[fi(n, -m)] = cfma(fh, sv, acc[fi(n, -m)]);             // conj(S_n^-m) = S_n^m
+            }
           }
         }
         f -= seg.y;
@@ -291,12 +378,12 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
     if (active && sl == 0) {
       double2* out = H.Lc + size_t(c0 + cc + ci) * KQ;
       for (int i = 0; i < KQ; ++i) {
-        double2 s = make_double2(0, 0);
+        double2 s2 = make_double2(0, 0);
         for (int k2 = 0; k2 < S; ++k2) {
-          s.x += red[i * 128 + threadIdx.x + k2].x;
-          s.y += red[i * 128 + threadIdx.x + k2].y;
+          s2.x += red[i * 128 + threadIdx.x + k2].x;
+          s2.y += red[i * 128 + threadIdx.x + k2].y;
         }
-        out[i] = s;
+        out[i] = s2;
       }
     }
     __syncthreads();
@@ -607,6 +694,31 @@ void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 }
 
 }  // namespace
+
+void helm_upload_constants() {
+  double sa[kHSolid + 1] = {0}, sb[kHSolid + 1] = {0};
+  double sc[(kHSolid + 1) * (kHSolid + 1)] = {0}, sd[(kHSolid + 1) * (kHSolid + 1)] = {0};
+  for (int m = 1; m <= kHSolid; ++m) sa[m] = std::sqrt((2.0 * m + 1.0) / (2.0 * m));
+  for (int m = 0; m <= kHSolid; ++m) sb[m] = std::sqrt(2.0 * m + 3.0);
+  for (int n = 2; n <= kHSolid; ++n)
+    for (int m = 0; m + 2 <= n; ++m) {
+      sc[n * (kHSolid + 1) + m] = std::sqrt((4.0 * n * n - 1.0) / (double(n) * n - double(m) * m));
+      sd[n * (kHSolid + 1) + m] = std::sqrt(((n - 1.0) * (n - 1.0) - double(m) * m) / (4.0 * (n - 1.0) * (n - 1.0) - 1.0));
+    }
+  double jser[(kHSolid + 2) * kHSer], odd[2 * kHSolid + 4];
+  for (int n = 0; n < kHSolid + 2; ++n)
+    for (int t = 1; t <= kHSer; ++t) jser[n * kHSer + t - 1] = -1.0 / (2.0 * t * (2.0 * n + 2.0 * t + 1.0));
+  for (int n = 0; n < kHSolid + 2; ++n) {
+    odd[2 * n] = 2.0 * n + 1.0;
+    odd[2 * n + 1] = 1.0 / (2.0 * n + 1.0);
+  }
+  cudaMemcpyToSymbol(c_jser, jser, sizeof(jser));
+  cudaMemcpyToSymbol(c_odd, odd, sizeof(odd));
+  cudaMemcpyToSymbol(c_sa, sa, sizeof(sa));
+  cudaMemcpyToSymbol(c_sb, sb, sizeof(sb));
+  cudaMemcpyToSymbol(c_sc, sc, sizeof(sc));
+  cudaMemcpyToSymbol(c_sd, sd, sizeof(sd));
+}
 
 int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s) {
   if (ns == 0) return 0;
