@@ -33,50 +33,180 @@ __device__ __forceinline__ void nm_of(int i, int& n, int& m) {
   m = i - n * n - n;
 }
 
-// cooperative wave-function table F[fi(l, mu)] = rad_l Y_l^mu(t), l <= P: threads
-// 0..P build one azimuthal column each, threads 0..P one radial value each;
-// rad = j_l (regular) or h_l = j_l + i y_l (singular).  Ends with __syncthreads.
-__device__ void wave_table_cta(double k, int P, double tx, double ty, double tz, bool singular, double2* F,
-                               double2* rad) {
-  const double r = sqrt(tx * tx + ty * ty + tz * tz);
-  const double x = k * r;
-  const double ct = r > 0 ? tz / r : 1.0, st = sqrt(fmax(0.0, 1.0 - ct * ct));
-  const double ph = atan2(ty, tx);
-  for (int m = threadIdx.x; m <= P; m += blockDim.x) {
-    double mm = 1.0 / sqrt(4.0 * kPi);
-    for (int i = 1; i <= m; ++i) mm *= sqrt((2.0 * i + 1.0) / (2.0 * i)) * st;
-    double s, c;
-    sincos(m * ph, &s, &c);
-    double a = mm;
-    F[fi(m, m)] = make_double2(a * c, a * s);
-    F[fi(m, -m)] = make_double2(a * c, -a * s);
-    if (m + 1 <= P) {
-      double b = sqrt(2.0 * m + 3.0) * ct * a;
-      F[fi(m + 1, m)] = make_double2(b * c, b * s);
-      F[fi(m + 1, -m)] = make_double2(b * c, -b * s);
-      for (int n = m + 2; n <= P; ++n) {
-        const double an = sqrt((4.0 * n * n - 1.0) / (double(n) * n - double(m) * m));
-        const double bn = sqrt(((n - 1.0) * (n - 1.0) - double(m) * m) / (4.0 * (n - 1.0) * (n - 1.0) - 1.0));
-        const double cc = an * (ct * b - bn * a);
-        F[fi(n, m)] = make_double2(cc * c, cc * s);
-        F[fi(n, -m)] = make_double2(cc * c, -cc * s);
-        a = b;
-        b = cc;
+// Recurrence coefficients of the fully normalised solid harmonics
+// S_n^m(v) = |v|^n Y_n^m(v/|v|) (m >= 0), a polynomial in (x, y, z):
+//   S_m^m = a_m (x + i y) S_{m-1}^{m-1},  S_{m+1}^m = b_m z S_m^m,
+//   S_n^m = c_nm (z S_{n-1}^m - d_nm |v|^2 S_{n-2}^m)
+// (the normalised-Legendre recurrences times |v|^n; no trigonometry, no square roots
+// per pair).  Filled by helm_upload_constants().
+constexpr int kHSolid = 42;  // degrees covered: operator tables need 2p (p <= 20) + 1
+__constant__ double c_sa[kHSolid + 1], c_sb[kHSolid + 1];
+__constant__ double c_sc[(kHSolid + 1) * (kHSolid + 1)], c_sd[(kHSolid + 1) * (kHSolid + 1)];
+
+// j_n(k r) / r^n and y_n(k r) / r^n for n <= Q without divisions in the loops:
+//   Jt_n = j_n / r^n:  series for Jt_Q, Jt_{Q+1} (x < 1), then Jt_{n-1} = (2n+1)/k Jt_n - r^2 Jt_{n+1}
+//   Yt_n = y_n / r^n:  Yt_{n+1} = ((2n+1)/k Yt_n - Yt_{n-1}) / r^2
+constexpr int kHSer = 14;
+__constant__ double c_jser[(kHSolid + 2) * kHSer];  // -1/(2 t (2n+2t+1))
+__constant__ double c_odd[2 * kHSolid + 4];          // 2n+1 and 1/(2n+1) interleaved
+
+template <int Q>
+__device__ __forceinline__ void radial_over_rn(double k, double r, double ir, double2 (&g)[Q + 1]) {
+  const double x = k * r, x2 = x * x, r2 = r * r, ik = 1.0 / k, ir2 = ir * ir;
+  double jt[Q + 2];
+  if (x < 1.0) {
+    double kn = 1.0;  // k^n / (2n+1)!!
+    for (int n = 1; n <= Q; ++n) kn *= k * c_odd[2 * n + 1];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = Q + e;
+      if (e == 1) kn *= k * c_odd[2 * n + 1];
+      double term = 1.0, sum = 1.0;
+#pragma unroll
+      for (int t = 1; t <= kHSer; ++t) {
+        term *= x2 * c_jser[n * kHSer + t - 1];
+        sum += term;
       }
+      jt[n] = kn * sum;
+    }
+#pragma unroll
+    for (int n = Q + 1; n >= 1; --n) {
+      const double nxt = n + 1 <= Q + 1 ? jt[n + 1] : 0.0;
+      if (n <= Q) jt[n - 1] = c_odd[2 * n] * ik * jt[n] - r2 * nxt;
+      else jt[n - 1] = jt[n - 1];
+    }
+  } else {
+    double irn = 1.0;
+#pragma unroll
+    for (int n = 0; n <= Q; ++n) {
+      jt[n] = sph_j1(n, x) * irn;
+      irn *= ir;
     }
   }
-  for (int n = threadIdx.x; n <= P; n += blockDim.x) rad[n] = make_double2(sph_j1(n, x), 0.0);
-  __syncthreads();
-  if (singular && threadIdx.x == 0) {
-    double ym = -cos(x) / x, y0 = -cos(x) / (x * x) - sin(x) / x;
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double ix = ik * ir;
+  double ym = -cs * ix, y0 = (-cs * ix * ix - sn * ix) * ir;
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) {
+    double yn;
+    if (n == 0) {
+      yn = ym;
+    } else if (n == 1) {
+      yn = y0;
+    } else {
+      yn = (c_odd[2 * (n - 1)] * ik * y0 - ym) * ir2;
+      ym = y0;
+      y0 = yn;
+    }
+    g[n] = make_double2(jt[n], yn);
+  }
+}
+
+// runtime-degree radial table rad[n] = (j_n(k r) + i s y_n(k r)) / r^n, n <= P,
+// division-free recurrences as above (series for x < 1, Miller's recurrence above);
+// computed by one thread
+__device__ void radial_table(double k, double r, int P, bool singular, double2* rad) {
+  const double x = k * r, x2 = x * x, r2 = r * r, ik = 1.0 / k, ir = 1.0 / r, ir2 = ir * ir;
+  if (x < 1.0) {
+    double kn = 1.0;
+    for (int n = 1; n <= P; ++n) kn *= k * c_odd[2 * n + 1];
+    double jt[2];
+    for (int e = 0; e < 2; ++e) {
+      const int n = P + e;
+      if (e == 1) kn *= k * c_odd[2 * n + 1];
+      double term = 1.0, sum = 1.0;
+      for (int t = 1; t <= kHSer; ++t) {
+        term *= x2 * c_jser[n * kHSer + t - 1];
+        sum += term;
+      }
+      jt[e] = kn * sum;
+    }
+    double jn = jt[0], jn1 = jt[1];
+    rad[P].x = jn;
+    for (int n = P; n >= 1; --n) {
+      const double jm = c_odd[2 * n] * ik * jn - r2 * jn1;
+      jn1 = jn;
+      jn = jm;
+      rad[n - 1].x = jm;
+    }
+  } else {
+    double irn = 1.0;
+    for (int n = 0; n <= P; ++n) {
+      rad[n].x = sph_j1(n, x) * irn;
+      irn *= ir;
+    }
+  }
+  if (singular) {
+    double sn, cs;
+    sincos(x, &sn, &cs);
+    const double ix = ik * ir;
+    double ym = -cs * ix, y0 = (-cs * ix * ix - sn * ix) * ir;
     rad[0].y = ym;
     if (P >= 1) rad[1].y = y0;
     for (int n = 2; n <= P; ++n) {
-      const double yn = (2.0 * n - 1.0) / x * y0 - ym;
+      const double yn = (c_odd[2 * (n - 1)] * ik * y0 - ym) * ir2;
       ym = y0;
       y0 = yn;
       rad[n].y = yn;
     }
+  } else {
+    for (int n = 0; n <= P; ++n) rad[n].y = 0.0;
+  }
+}
+
+// column mu >= 0 of the solid harmonics S_n^mu(v), n = mu..P, into out[n] (one thread)
+__device__ __forceinline__ void solid_column(int mu, int P, double vx, double vy, double vz, double r2, double2* out) {
+  double2 d = make_double2(0.28209479177387814347, 0.0);  // S_0^0 = 1/sqrt(4 pi)
+  for (int i = 1; i <= mu; ++i)
+    d = make_double2(c_sa[i] * (d.x * vx - d.y * vy), c_sa[i] * (d.x * vy + d.y * vx));
+  out[mu] = d;
+  if (mu + 1 > P) return;
+  double2 a = d, b = make_double2(c_sb[mu] * vz * d.x, c_sb[mu] * vz * d.y);
+  out[mu + 1] = b;
+  for (int n = mu + 2; n <= P; ++n) {
+    const double cn = c_sc[n * (kHSolid + 1) + mu], dn = c_sd[n * (kHSolid + 1) + mu] * r2;
+    const double2 c2 = make_double2(cn * (vz * b.x - dn * a.x), cn * (vz * b.y - dn * a.y));
+    out[n] = c2;
+    a = b;
+    b = c2;
+  }
+}
+
+// cooperative wave-function table F[fi(l, mu)] = rad_l Y_l^mu(t) = (rad_l / r^l) S_l^mu(t),
+// l <= P: threads 0..P build one solid-harmonic column each (Cartesian recurrences),
+// thread 0 the radial table; rad = j_l (regular) or h_l = j_l + i y_l (singular).
+// `rad` must hold P + 1 entries; F (P+1)^2.  Ends with __syncthreads.
+__device__ void wave_table_cta(double k, int P, double tx, double ty, double tz, bool singular, double2* F,
+                               double2* rad) {
+  const double r2 = tx * tx + ty * ty + tz * tz;
+  const double r = sqrt(r2);
+  if (threadIdx.x == 32 || (blockDim.x <= 32 && threadIdx.x == 0)) radial_table(k, r, P, singular, rad);
+  for (int m = threadIdx.x; m <= P; m += blockDim.x) {
+    // column m into F[fi(n, m)] (n = m..P), mirrored to -m
+    double2 d = make_double2(0.28209479177387814347, 0.0);
+    for (int i = 1; i <= m; ++i)
+      d = make_double2(c_sa[i] * (d.x * tx - d.y * ty), c_sa[i] * (d.x * ty + d.y * tx));
+    F[fi(m, m)] = d;
+    if (m + 1 <= P) {
+      double2 a = d, b = make_double2(c_sb[m] * tz * d.x, c_sb[m] * tz * d.y);
+      F[fi(m + 1, m)] = b;
+      for (int n = m + 2; n <= P; ++n) {
+        const double cn = c_sc[n * (kHSolid + 1) + m], dn = c_sd[n * (kHSolid + 1) + m] * r2;
+        const double2 c2 = make_double2(cn * (tz * b.x - dn * a.x), cn * (tz * b.y - dn * a.y));
+        F[fi(n, m)] = c2;
+        a = b;
+        b = c2;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (P + 1) * (P + 1); i += blockDim.x) {
+    int n, m;
+    nm_of(i, n, m);
+    double2 v = F[fi(n, m < 0 ? -m : m)];
+    if (m < 0) v.y = -v.y;  // S_n^{-m} = conj(S_n^m)
+    F[i] = make_double2(v.x, v.y);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < (P + 1) * (P + 1); i += blockDim.x) {
@@ -229,76 +359,6 @@ __global__ void __launch_bounds__(512) k_h_m2l_reduce(HelmData H, const int* __r
   }
   const double2 v = H.L[size_t(b) * H.KP + i];
   H.L[size_t(b) * H.KP + i] = make_double2(v.x + s.x, v.y + s.y);
-}
-
-// Recurrence coefficients of the fully normalised solid harmonics
-// S_n^m(v) = |v|^n Y_n^m(v/|v|) (m >= 0), a polynomial in (x, y, z):
-//   S_m^m = a_m (x + i y) S_{m-1}^{m-1},  S_{m+1}^m = b_m z S_m^m,
-//   S_n^m = c_nm (z S_{n-1}^m - d_nm |v|^2 S_{n-2}^m)
-// (the normalised-Legendre recurrences times |v|^n; no trigonometry, no square roots
-// per pair).  Filled by helm_upload_constants().
-constexpr int kHSolid = 10;  // degrees covered (q <= 8, + 1)
-__constant__ double c_sa[kHSolid + 1], c_sb[kHSolid + 1];
-__constant__ double c_sc[(kHSolid + 1) * (kHSolid + 1)], c_sd[(kHSolid + 1) * (kHSolid + 1)];
-
-// j_n(k r) / r^n and y_n(k r) / r^n for n <= Q without divisions in the loops:
-//   Jt_n = j_n / r^n:  series for Jt_Q, Jt_{Q+1} (x < 1), then Jt_{n-1} = (2n+1)/k Jt_n - r^2 Jt_{n+1}
-//   Yt_n = y_n / r^n:  Yt_{n+1} = ((2n+1)/k Yt_n - Yt_{n-1}) / r^2
-constexpr int kHSer = 14;
-__constant__ double c_jser[(kHSolid + 2) * kHSer];  // -1/(2 t (2n+2t+1))
-__constant__ double c_odd[2 * kHSolid + 4];          // 2n+1 and 1/(2n+1) interleaved
-
-template <int Q>
-__device__ __forceinline__ void radial_over_rn(double k, double r, double ir, double2 (&g)[Q + 1]) {
-  const double x = k * r, x2 = x * x, r2 = r * r, ik = 1.0 / k, ir2 = ir * ir;
-  double jt[Q + 2];
-  if (x < 1.0) {
-    double kn = 1.0;  // k^n / (2n+1)!!
-    for (int n = 1; n <= Q; ++n) kn *= k * c_odd[2 * n + 1];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int n = Q + e;
-      if (e == 1) kn *= k * c_odd[2 * n + 1];
-      double term = 1.0, sum = 1.0;
-#pragma unroll
-      for (int t = 1; t <= kHSer; ++t) {
-        term *= x2 * c_jser[n * kHSer + t - 1];
-        sum += term;
-      }
-      jt[n] = kn * sum;
-    }
-#pragma unroll
-    for (int n = Q + 1; n >= 1; --n) {
-      const double nxt = n + 1 <= Q + 1 ? jt[n + 1] : 0.0;
-      if (n <= Q) jt[n - 1] = c_odd[2 * n] * ik * jt[n] - r2 * nxt;
-      else jt[n - 1] = jt[n - 1];
-    }
-  } else {
-    double irn = 1.0;
-#pragma unroll
-    for (int n = 0; n <= Q; ++n) {
-      jt[n] = sph_j1(n, x) * irn;
-      irn *= ir;
-    }
-  }
-  double sn, cs;
-  sincos(x, &sn, &cs);
-  const double ix = ik * ir;
-  double ym = -cs * ix, y0 = (-cs * ix * ix - sn * ix) * ir;
-#pragma unroll
-  for (int n = 0; n <= Q; ++n) {
-    double yn;
-    if (n == 0) {
-      yn = ym;
-    } else if (n == 1) {
-      yn = y0;
-    } else {
-      yn = (c_odd[2 * (n - 1)] * ik * y0 - ym) * ir2;
-      ym = y0;
-      y0 = yn;
-    }
-    g[n] = make_double2(jt[n], yn);
-  }
 }
 
 // Stages 3, 5a, 6a: P2QBXL, thread per (centre, source slice):
@@ -461,32 +521,14 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   double* geo = reinterpret_cast<double*>(Fc + kHCtrMax * NL);  // kHCtrMax x 4: cos t, sin t, phi, |t|
   const double4 bc = H.box[cta.x];
   for (int j = threadIdx.x; j < KP; j += blockDim.x) Xs[j] = X[size_t(cta.x) * KP + j];
-  for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
+  for (int j = threadIdx.x; j < nctr; j += blockDim.x) {  // per centre: t, and rad_l / r^l
     const double4 c = H.ctr[ctr_of[cta.y + j]];
     const double tx = c.x - bc.x, ty = c.y - bc.y, tz = c.z - bc.z;
-    const double r = sqrt(tx * tx + ty * ty + tz * tz);
-    const double ct = r > 0 ? tz / r : 1.0;
-    geo[4 * j] = ct;
-    geo[4 * j + 1] = sqrt(fmax(0.0, 1.0 - ct * ct));
-    geo[4 * j + 2] = atan2(ty, tx);
-    geo[4 * j + 3] = r;
-    const double x = H.k * r;
-    double ym = -cos(x) / x, y0 = -cos(x) / (x * x) - sin(x) / x;
-    for (int l = 0; l <= L; ++l) {
-      double yl = 0.0;
-      if (singular) {
-        if (l == 0) {
-          yl = ym;
-        } else if (l == 1) {
-          yl = y0;
-        } else {
-          yl = (2.0 * l - 1.0) / x * y0 - ym;
-          ym = y0;
-          y0 = yl;
-        }
-      }
-      rad[j * NL + l] = make_double2(sph_j1(l, x), yl);
-    }
+    geo[4 * j] = tx;
+    geo[4 * j + 1] = ty;
+    geo[4 * j + 2] = tz;
+    geo[4 * j + 3] = tx * tx + ty * ty + tz * tz;
+    radial_table(H.k, sqrt(geo[4 * j + 3]), L, singular != 0, rad + j * NL);
   }
   double2 acc[kHCtrAcc];
 #pragma unroll
@@ -516,29 +558,13 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
       }
       Cm[e] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
     }
-    // F column mu per centre: rad_l Y_l^mu(t), l = |mu|..L
+    // F column mu per centre: (rad_l / r^l) S_l^mu(t), l = |mu|..L  (S^{-mu} = conj S^mu)
     for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
-      const double ct = geo[4 * j], st = geo[4 * j + 1], ph = geo[4 * j + 2];
-      double mm = 1.0 / sqrt(4.0 * kPi);
-      for (int i = 1; i <= amu; ++i) mm *= sqrt((2.0 * i + 1.0) / (2.0 * i)) * st;
-      double s, c;
-      sincos(mu * ph, &s, &c);
-      double a = mm, b = 0.0;
+      double2* col = Fc + j * NL;
+      solid_column(amu, L, geo[4 * j], geo[4 * j + 1], geo[4 * j + 2], geo[4 * j + 3], col);
       for (int l = amu; l <= L; ++l) {
-        double pl;
-        if (l == amu) {
-          pl = a;
-        } else if (l == amu + 1) {
-          b = sqrt(2.0 * amu + 3.0) * ct * a;
-          pl = b;
-        } else {
-          const double an = sqrt((4.0 * l * l - 1.0) / (double(l) * l - double(amu) * amu));
-          const double bn = sqrt(((l - 1.0) * (l - 1.0) - double(amu) * amu) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
-          pl = an * (ct * b - bn * a);
-          a = b;
-          b = pl;
-        }
-        Fc[j * NL + l] = cmul(rad[j * NL + l], make_double2(pl * c, pl * s));
+        const double2 sv = mu < 0 ? make_double2(col[l].x, -col[l].y) : col[l];
+        col[l] = cmul(rad[j * NL + l], sv);
       }
     }
     __syncthreads();
