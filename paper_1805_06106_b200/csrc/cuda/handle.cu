@@ -145,7 +145,10 @@ struct Handle {
   bool helm = false;
   dev::HelmData HD{};
   std::vector<double2*> h_ops_m2m, h_ops_l2l;  // per level: 8 octant operators
-  double2* h_ops_m2l = nullptr;                // per (level, offset) operators
+  double2* h_ops_m2l = nullptr;                // per (level, offset) operators (split: even / odd blocks)
+  double2* h_cs = nullptr;                     // per operator e^{i m alpha}, m <= p (split form)
+  int* h_ent_op = nullptr;                     // operator of every List-2 CSR entry (split form)
+  bool h_split = true;                         // QBXG_HELM_M2L=full keeps the full operators
   struct HelmM2LChunk {
     int n_tiles = 0;
     int4* tiles = nullptr;
@@ -524,14 +527,23 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
         }
         op_of_entry[e] = op;
       }
-    const size_t bytes = msh.size() * opsz * sizeof(double2);
+    H.h_split = !(std::getenv("QBXG_HELM_M2L") && std::string(std::getenv("QBXG_HELM_M2L")) == "full");
+    const size_t per_op = H.h_split ? dev::helm_split_op_size(p) : opsz;
+    const size_t bytes = msh.size() * per_op * sizeof(double2);
     size_t free_b = 0, total_b = 0;
     QCK(cudaMemGetInfo(&free_b, &total_b));
     if (bytes > size_t(double(free_b) * 0.7))
       throw InvalidArgument("qbxg_create: Helmholtz M2L operators (" + std::to_string(bytes >> 20) +
                             " MiB) exceed device memory");
-    H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * opsz);
-    if (!msh.empty()) dev::helm_build_ops(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, s);
+    H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * per_op);
+    if (H.h_split) {
+      for (auto& v : msh) v.w = 0.0;  // the split builder takes the plain offset vector
+      H.h_cs = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * (p + 1));
+      if (!msh.empty()) dev::helm_build_split(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, H.h_cs, s);
+      H.h_ent_op = dupload(O, op_of_entry, s);
+    } else if (!msh.empty()) {
+      dev::helm_build_ops(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, s);
+    }
     // tiles of same-operator entries, chunked over contiguous target boxes
     const int cols = dev::helm_m2l_cols();
     size_t free2 = 0;
@@ -679,9 +691,14 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   chk(dev::helm_near(HD, H.d_ctr_boxes, H.n_ctr_boxes, s));
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
-  for (const auto& C : H.h_m2l)
-    chk(dev::helm_m2l(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_temp, C.n_boxes, C.boxes,
-                      C.base, s));
+  for (const auto& C : H.h_m2l) {
+    if (H.h_split)
+      chk(dev::helm_m2l_split(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_cs, H.h_temp,
+                              C.n_boxes, C.boxes, C.base, H.h_ent_op, s));
+    else
+      chk(dev::helm_m2l(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_temp, C.n_boxes, C.boxes,
+                        C.base, s));
+  }
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::helm_p2l(HD, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));

@@ -316,6 +316,181 @@ __global__ void __launch_bounds__(256) k_h_build_ops(HelmData H, const double4* 
   }
 }
 
+// ---- Stage 4 M2L, split form -------------------------------------------------
+// Rotating the frame about z by alpha = atan2(dy, dx) puts the offset in the
+// xz-plane (t'); there Y_l^mu(t') is real and F_l^{-mu} = F_l^mu, and with the
+// sign symmetry of the Gaunt coefficients T(-m', -m) = T(m', m).  In the even / odd
+// coordinates a_m = x_m + x_{-m}, b_m = x_m - x_{-m} (m > 0), a_0 = x_0 the operator
+// is block diagonal:
+//   A_{m'} = sum_{m>0} [T(m',m) + T(m',-m)] a_m + c T(m',0) a_0  (c = 2 for m' > 0, 1 for m' = 0,
+//            and the m > 0 terms are halved for m' = 0)
+//   B_{m'} = sum_{m>0} [T(m',m) - T(m',-m)] b_m
+// (sizes (p+1)(p+2)/2 and p(p+1)/2: half the complex MACs of the full operator).
+// Columns enter as M' = M e^{i m alpha}; the reduce rebuilds y_{+-m'} = (A +- B)/2
+// and rotates back, L = y e^{-i m alpha}.
+__device__ __forceinline__ int ev_idx(int n, int m) { return n * (n + 1) / 2 + m; }      // m >= 0
+__device__ __forceinline__ int od_idx(int n, int m) { return n * (n - 1) / 2 + m - 1; }  // m >= 1
+__device__ __forceinline__ void ev_nm(int e, int& n, int& m) {
+  n = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+  while ((n + 1) * (n + 2) / 2 <= e) ++n;
+  while (n * (n + 1) / 2 > e) --n;
+  m = e - n * (n + 1) / 2;
+}
+__device__ __forceinline__ void od_nm(int o, int& n, int& m) {
+  n = int((1.0 + sqrt(8.0 * o + 1.0)) * 0.5);
+  while (n * (n - 1) / 2 > o) --n;
+  while ((n + 1) * n / 2 <= o) ++n;
+  m = o - n * (n - 1) / 2 + 1;
+}
+
+// one operator entry T(n',m' <- n,m) of the rotated-frame operator from the F table
+__device__ __forceinline__ double2 t_entry(const HelmData& H, const double2* F, int n2, int m2, int n, int m) {
+  const double* g = H.gaunt + (size_t(fi(n, m)) * H.KP + fi(n2, m2)) * H.GL;
+  double2 acc = make_double2(0, 0);
+  const int l0 = abs(n - n2);
+  for (int li = 0; li < H.GL; ++li) {
+    const int l = l0 + 2 * li;
+    if (l > n + n2) break;
+    const double gv = g[li];
+    if (gv == 0.0 || abs(m - m2) > l) continue;
+    const double2 f = cmul(ipow(n2 + l - n), F[fi(l, m - m2)]);
+    acc.x += gv * f.x;
+    acc.y += gv * f.y;
+  }
+  return make_double2(4.0 * kPi * acc.x, 4.0 * kPi * acc.y);
+}
+
+// operator builder (split): per op, E (NE x NE) then O (NO x NO), k-major; cs = e^{i m alpha}
+__global__ void __launch_bounds__(256) k_h_build_split(HelmData H, const double4* __restrict__ shifts,
+                                                       double2* __restrict__ ops, double2* __restrict__ cs) {
+  extern __shared__ double2 sm[];
+  const int P = H.P, L = 2 * P;
+  const int NE = (P + 1) * (P + 2) / 2, NO = P * (P + 1) / 2;
+  double2* F = sm;
+  double2* rad = sm + (L + 1) * (L + 1);
+  const double4 t = shifts[blockIdx.x];  // original offset vector
+  const double rho = sqrt(t.x * t.x + t.y * t.y);
+  const double alpha = rho > 0 ? atan2(t.y, t.x) : 0.0;
+  if (threadIdx.x <= P) {
+    double sn, cn;
+    sincos(threadIdx.x * alpha, &sn, &cn);
+    cs[size_t(blockIdx.x) * (P + 1) + threadIdx.x] = make_double2(cn, sn);
+  }
+  wave_table_cta(H.k, L, rho, 0.0, t.z, true, F, rad);
+  double2* E = ops + size_t(blockIdx.x) * (size_t(NE) * NE + size_t(NO) * NO);
+  double2* Od = E + size_t(NE) * NE;
+  for (int e = threadIdx.x; e < NE * NE; e += blockDim.x) {
+    const int kin = e / NE, iout = e % NE;
+    int n, m, n2, m2;
+    ev_nm(kin, n, m);
+    ev_nm(iout, n2, m2);
+    double2 v;
+    if (m == 0) {
+      v = t_entry(H, F, n2, m2, n, 0);
+      if (m2 > 0) v = make_double2(2.0 * v.x, 2.0 * v.y);
+    } else {
+      const double2 a = t_entry(H, F, n2, m2, n, m), b = t_entry(H, F, n2, m2, n, -m);
+      v = make_double2(a.x + b.x, a.y + b.y);
+      if (m2 == 0) v = make_double2(0.5 * v.x, 0.5 * v.y);
+    }
+    E[e] = v;
+  }
+  for (int e = threadIdx.x; e < NO * NO; e += blockDim.x) {
+    const int kin = e / NO, iout = e % NO;
+    int n, m, n2, m2;
+    od_nm(kin, n, m);
+    od_nm(iout, n2, m2);
+    const double2 a = t_entry(H, F, n2, m2, n, m), b = t_entry(H, F, n2, m2, n, -m);
+    Od[e] = make_double2(a.x - b.x, a.y - b.y);
+  }
+}
+
+// one CTA: one operator, up to kHCols entries; threads 0..NE-1 the even rows,
+// NE..NE+NO-1 the odd rows; staging row = [A (NE) ; B (NO)]
+constexpr int kHColsS = 8;
+__global__ void __launch_bounds__(512) k_h_m2l_split(HelmData H, const int4* __restrict__ tiles,
+                                                     const int* __restrict__ col_src, const int* __restrict__ col_pos,
+                                                     const double2* __restrict__ ops, const double2* __restrict__ cs,
+                                                     double2* __restrict__ temp) {
+  extern __shared__ double2 sm[];
+  const int P = H.P, KP = H.KP;
+  const int NE = (P + 1) * (P + 2) / 2, NO = P * (P + 1) / 2;
+  double2* Ba = sm;                  // kHColsS x NE
+  double2* Bb = sm + kHColsS * NE;   // kHColsS x NO
+  const int4 tile = tiles[blockIdx.x];
+  const double2* rot = cs + size_t(tile.x) * (P + 1);
+  for (int e = threadIdx.x; e < kHColsS * NE; e += blockDim.x) {
+    const int c = e / NE, q = e % NE;
+    int n, m;
+    ev_nm(q, n, m);
+    double2 a = make_double2(0, 0), bb = make_double2(0, 0);
+    if (c < tile.z) {
+      const double2* X = H.M + size_t(col_src[tile.y + c]) * KP;
+      const double2 r = rot[m];
+      const double2 xp = cmul(X[fi(n, m)], r);  // M' = M e^{i m alpha}
+      if (m == 0) {
+        a = xp;
+      } else {
+        const double2 xm = cmul(X[fi(n, -m)], make_double2(r.x, -r.y));
+        a = make_double2(xp.x + xm.x, xp.y + xm.y);
+        bb = make_double2(xp.x - xm.x, xp.y - xm.y);
+      }
+    }
+    Ba[c * NE + q] = a;
+    if (m > 0) Bb[c * NO + od_idx(n, m)] = bb;
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= NE + NO) return;
+  const bool odd = i >= NE;
+  const int row = odd ? i - NE : i, K = odd ? NO : NE;
+  const double2* T = ops + size_t(tile.x) * (size_t(NE) * NE + size_t(NO) * NO) + (odd ? size_t(NE) * NE : 0);
+  const double2* B = odd ? Bb : Ba;
+  double2 acc[kHColsS];
+#pragma unroll
+  for (int c = 0; c < kHColsS; ++c) acc[c] = make_double2(0, 0);
+  for (int kk = 0; kk < K; ++kk) {
+    const double2 a = T[size_t(kk) * K + row];
+#pragma unroll
+    for (int c = 0; c < kHColsS; ++c) acc[c] = cfma(a, B[c * K + kk], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kHColsS; ++c)
+    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KP + i] = acc[c];
+}
+
+// reduce: rebuild y_{+-m} = (A +- B)/2 in the rotated frame, rotate back, sum in CSR order
+__global__ void __launch_bounds__(512) k_h_m2l_reduce_split(HelmData H, const int* __restrict__ boxes, int64_t base,
+                                                            const double2* __restrict__ temp,
+                                                            const int* __restrict__ ent_op,
+                                                            const double2* __restrict__ cs) {
+  const int b = boxes[blockIdx.x];
+  const int P = H.P, KP = H.KP, NE = (P + 1) * (P + 2) / 2;
+  const int i = threadIdx.x;
+  if (i >= KP) return;
+  int n, m;
+  nm_of(i, n, m);
+  const int am = abs(m);
+  const int ie = ev_idx(n, am), io = am > 0 ? NE + od_idx(n, am) : -1;
+  double2 s = make_double2(0, 0);
+  for (int64_t pos = H.v_starts[b]; pos < H.v_starts[b + 1]; ++pos) {
+    const double2* row = temp + size_t(pos - base) * KP;
+    double2 y = row[ie];
+    if (am > 0) {
+      const double2 bv = row[io];
+      y = m > 0 ? make_double2(0.5 * (y.x + bv.x), 0.5 * (y.y + bv.y))
+                : make_double2(0.5 * (y.x - bv.x), 0.5 * (y.y - bv.y));
+    }
+    double2 r = cs[size_t(ent_op[pos]) * (P + 1) + am];  // e^{i |m| alpha}
+    if (m >= 0) r.y = -r.y;                            // L = y e^{-i m alpha}
+    const double2 v = cmul(y, r);
+    s.x += v.x;
+    s.y += v.y;
+  }
+  const double2 v = H.L[size_t(b) * KP + i];
+  H.L[size_t(b) * KP + i] = make_double2(v.x + s.x, v.y + s.y);
+}
+
 // Stage 4 M2L: one CTA per (operator, up to kHCols List-2 entries); thread per output row
 constexpr int kHCols = 8;
 __global__ void __launch_bounds__(512) k_h_m2l(HelmData H, const int4* __restrict__ tiles,
@@ -786,6 +961,32 @@ int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_s
 }
 
 int helm_m2l_cols() { return kHCols; }
+
+size_t helm_split_op_size(int P) {
+  const size_t NE = size_t(P + 1) * (P + 2) / 2, NO = size_t(P) * (P + 1) / 2;
+  return NE * NE + NO * NO;
+}
+
+int helm_build_split(const HelmData& H, int n_ops, const double4* shifts, double2* ops, double2* cs, cudaStream_t s) {
+  if (n_ops == 0) return 0;
+  const int L = 2 * H.P;
+  const size_t smem = size_t((L + 1) * (L + 1) + L + 1) * sizeof(double2);
+  cudaFuncSetAttribute(k_h_build_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_h_build_split<<<n_ops, 256, smem, s>>>(H, shifts, ops, cs);
+  return 1;
+}
+
+int helm_m2l_split(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+                   const double2* ops, const double2* cs, double2* temp, int n_boxes, const int* boxes, int64_t base,
+                   const int* ent_op, cudaStream_t s) {
+  if (n_tiles == 0) return 0;
+  const size_t smem = size_t(kHColsS) * H.KP * sizeof(double2);
+  cudaFuncSetAttribute(k_h_m2l_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
+  k_h_m2l_split<<<n_tiles, th, smem, s>>>(H, tiles, col_src, col_pos, ops, cs, temp);
+  k_h_m2l_reduce_split<<<n_boxes, th, 0, s>>>(H, boxes, base, temp, ent_op, cs);
+  return 2;
+}
 
 int helm_near(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
