@@ -545,7 +545,7 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
       dev::helm_build_ops(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, s);
     }
     // tiles of same-operator entries, chunked over contiguous target boxes
-    const int cols = dev::helm_m2l_cols();
+    const int cols = H.h_split ? dev::helm_m2l_split_cols() : dev::helm_m2l_cols();
     size_t free2 = 0;
     QCK(cudaMemGetInfo(&free2, &total_b));
     const int64_t cap = std::max<int64_t>(

@@ -53,6 +53,7 @@ int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2*
 int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
              const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s);
 int helm_m2l_cols();
+int helm_m2l_split_cols();
 // split M2L (even / odd blocks in the rotated frame): operator size, builder, apply
 size_t helm_split_op_size(int P);
 int helm_build_split(const HelmData& H, int n_ops, const double4* shifts, double2* ops, double2* cs, cudaStream_t s);

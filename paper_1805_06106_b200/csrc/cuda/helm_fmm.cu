@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(256) k_h_build_split(HelmData H, const double4
 
 // one CTA: one operator, up to kHCols entries; threads 0..NE-1 the even rows,
 // NE..NE+NO-1 the odd rows; staging row = [A (NE) ; B (NO)]
-constexpr int kHColsS = 8;
+constexpr int kHColsS = 16;
 __global__ void __launch_bounds__(512) k_h_m2l_split(HelmData H, const int4* __restrict__ tiles,
                                                      const int* __restrict__ col_src, const int* __restrict__ col_pos,
                                                      const double2* __restrict__ ops, const double2* __restrict__ cs,
@@ -961,6 +961,7 @@ int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_s
 }
 
 int helm_m2l_cols() { return kHCols; }
+int helm_m2l_split_cols() { return kHColsS; }
 
 size_t helm_split_op_size(int P) {
   const size_t NE = size_t(P + 1) * (P + 2) / 2, NO = size_t(P) * (P + 1) / 2;

@@ -56,6 +56,32 @@ VARIANTS = [
     {"QBXG_OVERLAP": "0"},
 ]
 
+HELM_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+import oracle as O
+from paper_1805_06106_b200 import api
+g = api.config_geometry(3, level=1)
+rng = np.random.default_rng(3)
+w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
+cfg = api.FmmConfig(p_fmm=8, p_qbx=4, n_max=64, kernel=2, helmholtz_k=3.0)
+plan = api.Plan(cfg, g)
+eng = api.FmmEngine(cfg, g, plan)
+pot = eng.apply_complex(w)
+eng.close()
+ref = O.helm_execute(plan, g, 3.0, 8, 4, w)
+print(json.dumps({"helm": float(np.linalg.norm(pot - ref) / np.linalg.norm(ref))}))
+""" % ROOT
+
+
+def test_helmholtz_full_m2l_variant():
+    full = dict(os.environ)
+    full["QBXG_HELM_M2L"] = "full"
+    r = subprocess.run([sys.executable, "-c", HELM_SCRIPT], env=full, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["helm"] <= 1e-11
+
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_parity(env):
