@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--small", action="store_true", help="debug: torus 64x32 instead of config 1")
+    ap.add_argument("--no-helmholtz", action="store_true", help="skip the config-3 Helmholtz side measurement")
     return ap.parse_args()
 
 
@@ -368,6 +369,31 @@ def run_ours(args, rank, world, local_rank):
         cb = cpu_oracle_throughput(1, 0)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
+    # BASELINE config 3 (Helmholtz single layer, k = 3, p = 20, q = 5) on the same GPU:
+    # side measurement, CUDA events, inputs on the host (qbxg_apply_complex)
+    helm = None
+    if world == 1 and not args.small and not args.no_helmholtz:
+        eng.close()
+        eng = None
+        g3 = api.config_geometry(3)
+        cfg3 = api.config_fmm(3)
+        rng3 = np.random.default_rng(7)
+        w3 = g3.quad_weight * (rng3.uniform(-1, 1, g3.n_sources) + 1j * rng3.uniform(-1, 1, g3.n_sources))
+        eng3 = api.FmmEngine(cfg3, g3, api.Plan(cfg3, g3))
+        eng3.apply_complex(w3)
+        hms = []
+        for _ in range(2):
+            eng3.apply_complex(w3)
+            tm3, _, _, _ = eng3.last_timings()
+            hms.append(tm3["total"])
+        eng3.close()
+        hms = float(np.mean(hms))
+        helm = {"workload": "BASELINE config 3: unit-sphere icosphere L=6, 1,310,720 sources, 2,621,440 centres "
+                            "and targets, Helmholtz SL k=3, complex density, p_fmm=20, p_qbx=5",
+                "ms_per_apply": round(hms, 2), "value": (g3.n_sources + g3.n_targets) / (hms * 1e-3),
+                "unit": "points/s", "dtype": "c128",
+                "parity": "GPU vs complex128 oracle <= 1e-11 (tests/test_helmholtz.py); no reference exists"}
+
     if rank == 0:
         line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": value,
                 "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -382,14 +408,15 @@ def run_ours(args, rank, world, local_rank):
                            "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"},
                 "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
-                "batch": batch,
+                "batch": batch, "helmholtz": helm,
                 "cpu_baseline": cpu,
                 "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
                             "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3)},
                 "list_hashes": {k: f"{v:016x}" for k, v in plan.list_hashes().items()},
                 "host_device_bitwise_equal": same}
         print(json.dumps(line), flush=True)
-    eng.close()
+    if eng is not None:
+        eng.close()
     if dist:
         dist.destroy_process_group()
     return 0
