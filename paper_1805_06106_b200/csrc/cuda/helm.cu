@@ -4,7 +4,7 @@
 // in complex128, with the formulation of oracle/helm_oracle.cpp:
 //   L_n^m = ik sum_s w_s h_n(k|s-c|) conj(Y_n^m(s-c)),  phi(t) = sum L_n^m j_n(k|t-c|) Y_n^m(t-c),
 // orthonormal Y_n^m without the Condon-Shortley phase, full tables (q+1)^2, index
-// n^2 + n + m.  The FMM stages for Helmholtz are not built yet.
+// n^2 + n + m.  The FMM stages are in helm_fmm.cu.
 #include <cuda_runtime.h>
 
 #include <cmath>
