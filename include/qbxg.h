@@ -342,6 +342,42 @@ int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, 
                          int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
                          const int32_t* association, int32_t p_qbx, double* out_pot_c);
 
+/* ---- target association and area queries on the GPU --
+ * Algorithm 3 (spec associate_targets) and
+ * Algorithm 5 (spec area_query) over the tree
+ * of a plan built from the sources and centres (its targets, if any, are ignored).
+ * A locator holds that tree, the box-sorted sources with their danger radii and
+ * the box-sorted centres on the device.
+ *   qbxg_locator_create: source_danger_radius[n_sources] (the r_danger(s) of
+ *     Algorithm 3, >= 0); center_side[n_centers] (int8 side tag, e.g. -1/+1) or
+ *     NULL.  geom must hold the sources and centres the plan was built from.
+ *   qbxg_associate_targets: target t is endangered iff |t - s| <= r_danger(s) for
+ *     some source s; an endangered target is associated with the nearest centre c
+ *     with |t - c| <= r_c (1 + eps_ta) (ties: lowest centre id), restricted to
+ *     centres with center_side[c] == side_pref[t] when side_pref[t] != 0.
+ *     out_association[t] = centre id, -1 (not endangered: conventional) or -2
+ *     (endangered, no centre: flagged, counted in *out_n_flagged).  Distances are
+ *     compared squared, (dx^2 + dy^2) + dz^2 rounded per operation.
+ *   qbxg_area_query: the leaf boxes (plan box ids, ascending) whose closed cube
+ *     intersects the closed l-inf ball B(r_i, c_i), i.e. |c_i,d - box_d| <= r_i + |b|
+ *     for d = x, y, z.  out_starts[n_queries+1] is always written; out_leaves
+ *     (NULL = counts only) is written when leaves_capacity >= out_starts[n_queries],
+ *     else QBXG_ERR_INVALID_ARGUMENT after the counts.  side_pref without centre
+ *     sides at create is QBXG_ERR_INVALID_ARGUMENT.
+ *   The _device variants take device pointers and run on `stream` (NULL = the
+ *   locator's stream), without host synchronisation. */
+typedef struct qbxg_locator qbxg_locator;
+int qbxg_locator_create(const qbxg_plan* plan, const qbxg_geometry* geom, const double* source_danger_radius,
+                        const int8_t* center_side_or_null, qbxg_locator** out);
+int qbxg_associate_targets(qbxg_locator* loc, int64_t n_targets, const double* target_pos, double eps_ta,
+                           const int8_t* side_pref_or_null, int32_t* out_association, int64_t* out_n_flagged);
+int qbxg_associate_targets_device(qbxg_locator* loc, int64_t n_targets, const double* d_target_pos, double eps_ta,
+                                  const int8_t* d_side_pref_or_null, int32_t* d_out_association,
+                                  unsigned long long* d_out_n_flagged, void* stream);
+int qbxg_area_query(qbxg_locator* loc, int64_t n_queries, const double* centers, const double* radii,
+                    int64_t* out_starts, int32_t* out_leaves, int64_t leaves_capacity);
+void qbxg_locator_destroy(qbxg_locator* loc);
+
 /* ---- misc ---------------------------------------------------------------- */
 const char* qbxg_last_error(void);
 int qbxg_device_count(int32_t* out);

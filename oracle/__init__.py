@@ -59,6 +59,9 @@ def lib():
                                            C.c_int, _dp]
         L.qbxo_helm_execute.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _i32p, _dp, _dp,
                                         _dp]
+        L.oracle_associate.argtypes = [C.c_int64, _dp, _dp, C.c_int64, _dp, _dp, C.c_void_p, C.c_int64, _dp,
+                                       C.c_double, C.c_void_p, _i32p, _i64p]
+        L.oracle_area_query.argtypes = [C.c_int32, _dp, _dp, _i32p, C.c_int64, _dp, _dp, _i64p, _i64p, _i32p]
         L.qbxo_lists_brute.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int64, _i64p * 6, _i32p * 6, _i64p]
         _o = L
     return _o
@@ -321,3 +324,45 @@ def helm_execute(plan, geom, k, p, q, w, want_centers=False):
     if want_centers:
         return pot, cc.view(np.complex128).reshape(geom.n_centers, (q + 1) ** 2)
     return pot
+
+
+def _i8(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int8)
+
+
+def associate_targets(source_pos, danger_radius, center_pos, center_radius, target_pos, eps_ta=0.0,
+                      center_side=None, side_pref=None):
+    """Algorithm 3 by brute force (oracle/assoc_brute.cpp): association int32[n_t]
+    (centre id, -1 not endangered, -2 flagged) and the flagged count."""
+    sp = np.ascontiguousarray(source_pos, dtype=np.float64).reshape(-1, 3)
+    cp = np.ascontiguousarray(center_pos, dtype=np.float64).reshape(-1, 3)
+    tp = np.ascontiguousarray(target_pos, dtype=np.float64).reshape(-1, 3)
+    dr = np.ascontiguousarray(danger_radius, dtype=np.float64)
+    cr = np.ascontiguousarray(center_radius, dtype=np.float64)
+    cs, tsd = _i8(center_side), _i8(side_pref)
+    out = np.empty(len(tp), dtype=np.int32)
+    nf = C.c_int64(0)
+    lib().oracle_associate(len(sp), _p(sp), _p(dr), len(cp), _p(cp), _p(cr),
+                           None if cs is None else cs.ctypes.data, len(tp), _p(tp), float(eps_ta),
+                           None if tsd is None else tsd.ctypes.data, out.ctypes.data_as(_i32p), C.byref(nf))
+    return out, int(nf.value)
+
+
+def area_query(plan, centers, radii):
+    """Algorithm 5 by the brute-force leaf scan: (starts int64[n+1], leaves int32)."""
+    a = plan.arrays()
+    qc = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+    qr = np.ascontiguousarray(radii, dtype=np.float64)
+    n = len(qc)
+    bc = np.ascontiguousarray(a["box_center"])
+    br = np.ascontiguousarray(a["box_radius"])
+    cs = np.ascontiguousarray(a["child_starts"])
+    cnt = np.zeros(n, dtype=np.int64)
+    args = (int(a["n_boxes"]), _p(bc), _p(br), cs.ctypes.data_as(_i32p), n, _p(qc), _p(qr))
+    lib().oracle_area_query(*args, cnt.ctypes.data_as(_i64p), None, None)
+    starts = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(cnt, out=starts[1:])
+    leaves = np.zeros(max(1, int(starts[-1])), dtype=np.int32)
+    lib().oracle_area_query(*args, cnt.ctypes.data_as(_i64p), starts.ctypes.data_as(_i64p),
+                            leaves.ctypes.data_as(_i32p))
+    return starts, leaves[:int(starts[-1])]

@@ -97,7 +97,8 @@ EXPORTED_SYMBOLS = (
     "qbxg_measure_dmma_peak", "qbxg_plan_shard", "qbxg_create_sharded", "qbxg_apply_phase",
     "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
     "qbxg_direct_qbx", "qbxg_apply_batch", "qbxg_apply_batch_device", "qbxg_set_overlap", "qbxg_helm_direct_sum", "qbxg_helm_direct_qbx",
-    "qbxg_apply_complex",
+    "qbxg_apply_complex", "qbxg_locator_create", "qbxg_associate_targets", "qbxg_associate_targets_device",
+    "qbxg_area_query", "qbxg_locator_destroy",
 )
 
 SHARD_OWN, SHARD_SUBTREE, SHARD_STRADDLE, SHARD_DOWN = 1, 2, 4, 8
@@ -141,6 +142,12 @@ def _declare(lib):
         "qbxg_exchange_local": ([P(C.c_void_p), C.c_int32], C.c_int),
         "qbxg_nccl_unique_id": ([C.c_char_p], C.c_int),
         "qbxg_nccl_attach": ([C.c_void_p, C.c_char_p], C.c_int),
+        "qbxg_locator_create": ([C.c_void_p, P(Geometry), _dp, C.c_void_p, P(C.c_void_p)], C.c_int),
+        "qbxg_associate_targets": ([C.c_void_p, C.c_int64, _dp, C.c_double, C.c_void_p, _i32p, _i64p], C.c_int),
+        "qbxg_associate_targets_device": ([C.c_void_p, C.c_int64, C.c_void_p, C.c_double] + [C.c_void_p] * 4,
+                                          C.c_int),
+        "qbxg_area_query": ([C.c_void_p, C.c_int64, _dp, _dp, _i64p, _i32p, C.c_int64], C.c_int),
+        "qbxg_locator_destroy": ([C.c_void_p], None),
     }
     for name, (args, res) in sig.items():
         if not hasattr(lib, name):

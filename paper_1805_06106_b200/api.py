@@ -277,6 +277,75 @@ class Plan:
         return d
 
 
+class Locator:
+    """Target association (Algorithm 3; spec associate_targets,
+    SPEC.md:296-304) and area queries (Algorithm 5; spec
+    area_query) on the GPU, over the tree of ``plan`` (built from
+    the sources and centres of ``geom``).  ``danger_radius[s]`` is r_danger of
+    source s; ``center_side`` (int8 per centre, optional) enables ``side_pref``."""
+
+    def __init__(self, plan: "Plan", geom: Geometry, danger_radius, center_side=None):
+        self.plan = plan
+        self._c_geom = geom.to_c()
+        self._danger = np.ascontiguousarray(danger_radius, dtype=np.float64)
+        if self._danger.shape != (geom.n_sources,):
+            raise ValueError("danger_radius must have one entry per source")
+        cs = None if center_side is None else np.ascontiguousarray(center_side, dtype=np.int8)
+        if cs is not None and cs.shape != (geom.n_centers,):
+            raise ValueError("center_side must have one entry per centre")
+        self.handle = C.c_void_p()
+        _check(_abi.lib().qbxg_locator_create(plan.handle, C.byref(self._c_geom), _ptr(self._danger),
+                                              None if cs is None else cs.ctypes.data, C.byref(self.handle)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _abi.lib().qbxg_locator_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    def associate(self, target_pos, eps_ta: float = 0.0, side_pref=None):
+        """-> (association int32[n]: centre id / -1 conventional / -2 flagged, n_flagged)."""
+        t = np.ascontiguousarray(target_pos, dtype=np.float64).reshape(-1, 3)
+        sp = None if side_pref is None else np.ascontiguousarray(side_pref, dtype=np.int8)
+        if sp is not None and sp.shape != (len(t),):
+            raise ValueError("side_pref must have one entry per target")
+        out = np.empty(len(t), dtype=np.int32)
+        nf = C.c_int64(0)
+        _check(_abi.lib().qbxg_associate_targets(self.handle, len(t), _ptr(t), float(eps_ta),
+                                                 None if sp is None else sp.ctypes.data,
+                                                 out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nf)))
+        return out, int(nf.value)
+
+    def associate_device(self, n: int, d_target_pos: int, eps_ta: float, d_side_pref: int | None, d_out: int,
+                         d_n_flagged: int, stream: int | None = None):
+        _check(_abi.lib().qbxg_associate_targets_device(self.handle, n, d_target_pos, float(eps_ta), d_side_pref,
+                                                        d_out, d_n_flagged, stream))
+
+    def area_query(self, centers, radii):
+        """-> (starts int64[n+1], leaves int32): leaf box ids meeting each closed l-inf ball."""
+        c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
+        r = np.ascontiguousarray(radii, dtype=np.float64)
+        if r.shape != (len(c),):
+            raise ValueError("one radius per query centre")
+        starts = np.zeros(len(c) + 1, dtype=np.int64)
+        i64 = C.POINTER(C.c_int64)
+        _check(_abi.lib().qbxg_area_query(self.handle, len(c), _ptr(c), _ptr(r), starts.ctypes.data_as(i64), None,
+                                          0))
+        leaves = np.zeros(max(1, int(starts[-1])), dtype=np.int32)
+        _check(_abi.lib().qbxg_area_query(self.handle, len(c), _ptr(c), _ptr(r), starts.ctypes.data_as(i64),
+                                          leaves.ctypes.data_as(C.POINTER(C.c_int32)), len(leaves)))
+        return starts, leaves[:int(starts[-1])]
+
+
+def danger_radius_of(geom: Geometry):
+    """Per-source danger radius of the procedural configs: the expansion radius
+    r = 0.5 sqrt(area) of the source's triangle (the radius the volume-target
+    filter of BASELINE config 2 uses), read off centre 2s (csrc/host/geometry.cpp)."""
+    return np.ascontiguousarray(geom.center_radius[0::2], dtype=np.float64)
+
+
 def build_plan(cfg: FmmConfig, geom: Geometry) -> Plan:
     return Plan(cfg, geom)
 
