@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--small", action="store_true", help="debug: torus 64x32 instead of config 1")
-    ap.add_argument("--no-helmholtz", action="store_true", help="skip the config-3 Helmholtz side measurement")
+    ap.add_argument("--no-helmholtz", action="store_true", help="skip the side measurements (config-3 Helmholtz, config-2 association)")
     return ap.parse_args()
 
 
@@ -394,6 +394,41 @@ def run_ours(args, rank, world, local_rank):
                 "unit": "points/s", "dtype": "c128",
                 "parity": "GPU vs complex128 oracle <= 1e-11 (tests/test_helmholtz.py); no reference exists"}
 
+    # target association (Algorithm 3) on BASELINE config 2: 655,360
+    # on-surface nodes + the retained volume targets, device-resident, CUDA events
+    assoc = None
+    if world == 1 and not args.small and not args.no_helmholtz:
+        g2 = api.config_geometry(2)
+        sc2 = api.Geometry(source_pos=g2.source_pos, center_pos=g2.center_pos, center_radius=g2.center_radius,
+                           target_pos=np.zeros((0, 3)), association=np.zeros(0, dtype=np.int32))
+        ns2 = 2 * g2.n_sources
+        sp2 = np.r_[np.where(np.arange(ns2) % 2 == 0, 1, -1), np.zeros(g2.n_targets - ns2)].astype(np.int8)
+        loc = api.Locator(api.Plan(api.config_fmm(2), sc2), sc2, api.danger_radius_of(g2),
+                          np.where(np.arange(g2.n_centers) % 2 == 0, 1, -1).astype(np.int8))
+        dT = torch.from_numpy(g2.target_pos.copy()).to(dev)
+        dS = torch.from_numpy(sp2).to(dev)
+        dA = torch.empty(g2.n_targets, dtype=torch.int32, device=dev)
+        dC = torch.zeros(1, dtype=torch.int64, device=dev)
+        cs = torch.cuda.current_stream()
+        run = lambda: loc.associate_device(g2.n_targets, dT.data_ptr(), 0.05, dS.data_ptr(), dA.data_ptr(),  # noqa
+                                           dC.data_ptr(), cs.cuda_stream)
+        for _ in range(3):
+            run()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(cs)
+        for _ in range(10):
+            run()
+        eb.record(cs)
+        torch.cuda.synchronize()
+        ams = ea.elapsed_time(eb) / 10
+        a2 = dA.cpu().numpy()
+        assoc = {"workload": "BASELINE config 2 targets (655,360 on-surface with side preference + retained volume "
+                             "targets), eps_ta=0.05, danger radius = panel expansion radius",
+                 "n_targets": int(g2.n_targets), "ms": round(ams, 4), "value": g2.n_targets / (ams * 1e-3),
+                 "unit": "targets/s", "n_flagged": int(dC.item()), "n_conventional": int((a2 == -1).sum()),
+                 "parity": "bit-exact vs brute-force oracle (tests/test_association.py)"}
+        loc.close()
+
     if rank == 0:
         line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": value,
                 "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -408,7 +443,7 @@ def run_ours(args, rank, world, local_rank):
                            "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"},
                 "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
-                "batch": batch, "helmholtz": helm,
+                "batch": batch, "helmholtz": helm, "association": assoc,
                 "cpu_baseline": cpu,
                 "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
                             "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3)},
