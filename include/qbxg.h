@@ -222,6 +222,11 @@ int qbxg_plan_shard(const qbxg_plan* plan, int32_t n_ranks, int32_t rank, int32_
 
 int qbxg_plan_create(const qbxg_config* cfg, const qbxg_geometry* geom, qbxg_plan** out);
 int qbxg_plan_view_get(const qbxg_plan* plan, qbxg_plan_view* out);
+/* Stage 1 on the GPU: the same plan as qbxg_plan_create,
+ * bit for bit (boxes, DFS numbering, permutations, lists and their hashes), with
+ * the octree built on the device and the lists built on the device when
+ * gpu_lists != 0 (on the host otherwise).  QBXG_ERR_CUDA without a device. */
+int qbxg_plan_create_gpu(const qbxg_config* cfg, const qbxg_geometry* geom, int32_t gpu_lists, qbxg_plan** out);
 int qbxg_plan_ledger(const qbxg_plan* plan, qbxg_ledger* out);
 void qbxg_plan_destroy(qbxg_plan* plan);
 

@@ -98,7 +98,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
     "qbxg_direct_qbx", "qbxg_apply_batch", "qbxg_apply_batch_device", "qbxg_set_overlap", "qbxg_helm_direct_sum", "qbxg_helm_direct_qbx",
     "qbxg_apply_complex", "qbxg_locator_create", "qbxg_associate_targets", "qbxg_associate_targets_device",
-    "qbxg_area_query", "qbxg_locator_destroy",
+    "qbxg_area_query", "qbxg_locator_destroy", "qbxg_plan_create_gpu",
 )
 
 SHARD_OWN, SHARD_SUBTREE, SHARD_STRADDLE, SHARD_DOWN = 1, 2, 4, 8
@@ -112,6 +112,7 @@ def _declare(lib):
         "qbxg_geometry_view": ([C.c_void_p, P(GeneratedView)], C.c_int),
         "qbxg_geometry_destroy": ([C.c_void_p], None),
         "qbxg_plan_create": ([P(Config), P(Geometry), P(C.c_void_p)], C.c_int),
+        "qbxg_plan_create_gpu": ([P(Config), P(Geometry), C.c_int32, P(C.c_void_p)], C.c_int),
         "qbxg_plan_view_get": ([C.c_void_p, P(PlanView)], C.c_int),
         "qbxg_plan_ledger": ([C.c_void_p, P(Ledger)], C.c_int),
         "qbxg_plan_destroy": ([C.c_void_p], None),

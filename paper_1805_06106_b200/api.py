@@ -222,13 +222,22 @@ def config_fmm(config_id: int, **overrides) -> FmmConfig:
 class Plan:
     """Host octree + interaction lists (Stage 1), built by libqbxg's host C++."""
 
-    def __init__(self, cfg: FmmConfig, geom: Geometry):
+    def __init__(self, cfg: FmmConfig, geom: Geometry, device: str = "host", gpu_lists: bool = True):
+        """device="host": Stage 1 in host C++ (csrc/host/plan.cpp); device="gpu": the same
+        plan bit for bit, octree (and, with gpu_lists, the lists) built on the GPU
+        (csrc/cuda/plan_gpu.cu)."""
         self.cfg = cfg
         self.geom = geom
         self._c_cfg = cfg.to_c()
         self._c_geom = geom.to_c()
         self.handle = C.c_void_p()
-        _check(_abi.lib().qbxg_plan_create(C.byref(self._c_cfg), C.byref(self._c_geom), C.byref(self.handle)))
+        if device == "host":
+            _check(_abi.lib().qbxg_plan_create(C.byref(self._c_cfg), C.byref(self._c_geom), C.byref(self.handle)))
+        elif device == "gpu":
+            _check(_abi.lib().qbxg_plan_create_gpu(C.byref(self._c_cfg), C.byref(self._c_geom),
+                                                   1 if gpu_lists else 0, C.byref(self.handle)))
+        else:
+            raise ValueError("Plan: device must be 'host' or 'gpu'")
         self.view = _abi.PlanView()
         _check(_abi.lib().qbxg_plan_view_get(self.handle, C.byref(self.view)))
 

@@ -25,45 +25,9 @@
 #include <limits>
 #include <numeric>
 
-#include "common.hpp"
-#include "predicates.hpp"
+#include "plan.hpp"
 
 namespace qbxg {
-
-namespace {
-constexpr int kMaxDepth = 60;
-}
-
-struct Plan {
-  qbxg_config cfg{};
-  int32_t nb = 0, nlev = 0;
-  double root_c[3] = {0, 0, 0}, root_h = 1;
-  std::vector<double> center, h;
-  std::vector<int32_t> level, parent, child_starts, children, level_starts, level_boxes, subtree_end;
-  std::vector<int64_t> ic;  // 3*nb integer coordinates at the box's level
-  std::vector<int32_t> src_own_start, src_own_count, src_sub_start, src_sub_count;
-  std::vector<int32_t> ctr_own_start, ctr_own_count, ctr_sub_start, ctr_sub_count;
-  std::vector<int32_t> tgt_own_start, tgt_own_count, tgt_sub_start, tgt_sub_count;
-  std::vector<int32_t> src_perm, ctr_perm, tgt_perm;
-  std::vector<uint8_t> flags;
-  std::vector<std::vector<int32_t>> coll;  // 2-colleagues incl. self, sorted
-  std::vector<int64_t> lst_starts[QBXG_NUM_LISTS];
-  std::vector<int32_t> lst[QBXG_NUM_LISTS];
-  uint64_t hash[QBXG_NUM_LISTS] = {};
-  int64_t ns = 0, nc = 0, nconv = 0, ntgt = 0;
-  double t_tree = 0, t_lists = 0;
-
-  bool leaf(int32_t b) const { return child_starts[b + 1] == child_starts[b]; }
-  bool has_src(int32_t b) const { return src_sub_count[b] > 0; }
-  bool adjacent(int32_t a, int32_t b) const {
-    return boxes_adjacent(&ic[3 * a], level[a], &ic[3 * b], level[b]);
-  }
-  int64_t cheb(int32_t a, int32_t b) const {  // same-level offset (l-inf, in boxes)
-    int64_t m = 0;
-    for (int d = 0; d < 3; ++d) m = std::max<int64_t>(m, std::llabs(ic[3 * a + d] - ic[3 * b + d]));
-    return m;
-  }
-};
 
 namespace {
 
@@ -75,6 +39,8 @@ struct BuildBox {
   int64_t start, end, own;
   int32_t child[8];
 };
+
+}  // namespace
 
 void validate_inputs(const qbxg_config& cfg, const qbxg_geometry& g) {
   if (cfg.p_fmm < 0 || cfg.p_qbx < 0) throw InvalidArgument("FmmConfig: negative order");
@@ -370,6 +336,7 @@ void build_tree(Plan& P, const qbxg_geometry& g) {
   P.t_tree = now_seconds() - t0;
 }
 
+namespace {
 void flatten(const std::vector<std::vector<int32_t>>& rows, std::vector<int64_t>& starts, std::vector<int32_t>& out) {
   starts.assign(rows.size() + 1, 0);
   for (size_t b = 0; b < rows.size(); ++b) starts[b + 1] = starts[b] + int64_t(rows[b].size());
@@ -377,6 +344,14 @@ void flatten(const std::vector<std::vector<int32_t>>& rows, std::vector<int64_t>
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < int64_t(rows.size()); ++b)
     std::copy(rows[b].begin(), rows[b].end(), out.begin() + starts[b]);
+}
+}  // namespace
+
+void hash_lists(Plan& P) {
+  for (int k = 0; k < QBXG_NUM_LISTS; ++k) {
+    const uint64_t hsh = fnv1a(P.lst_starts[k].data(), P.lst_starts[k].size() * sizeof(int64_t));
+    P.hash[k] = fnv1a(P.lst[k].data(), P.lst[k].size() * sizeof(int32_t), hsh);
+  }
 }
 
 void build_lists(Plan& P) {
@@ -522,15 +497,10 @@ void build_lists(Plan& P) {
     }
   }
 
-  for (int k = 0; k < QBXG_NUM_LISTS; ++k) {
-    flatten(rows[k], P.lst_starts[k], P.lst[k]);
-    uint64_t hsh = fnv1a(P.lst_starts[k].data(), P.lst_starts[k].size() * sizeof(int64_t));
-    P.hash[k] = fnv1a(P.lst[k].data(), P.lst[k].size() * sizeof(int32_t), hsh);
-  }
+  for (int k = 0; k < QBXG_NUM_LISTS; ++k) flatten(rows[k], P.lst_starts[k], P.lst[k]);
+  hash_lists(P);
   P.t_lists = now_seconds() - t0;
 }
-
-}  // namespace
 
 void compute_ledger(const Plan& P, qbxg_ledger& L) {
   std::memset(&L, 0, sizeof(L));
@@ -632,9 +602,6 @@ void compute_shard(const Plan& P, int nranks, int rank, std::vector<int32_t>& cu
 
 }  // namespace qbxg
 
-struct qbxg_plan {
-  qbxg::Plan p;
-};
 
 extern "C" int qbxg_plan_shard(const qbxg_plan* pl, int32_t n_ranks, int32_t rank, int32_t* cuts, uint8_t* mask) {
   return qbxg::guarded([&] {
@@ -659,6 +626,26 @@ int qbxg_plan_create(const qbxg_config* cfg, const qbxg_geometry* geom, qbxg_pla
       pl->p.cfg = *cfg;
       qbxg::build_tree(pl->p, *geom);
       qbxg::build_lists(pl->p);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    *out = pl;
+  });
+}
+
+int qbxg_plan_create_gpu(const qbxg_config* cfg, const qbxg_geometry* geom, int32_t gpu_lists, qbxg_plan** out) {
+  return qbxg::guarded([&] {
+    if (!cfg || !geom || !out) throw qbxg::InvalidArgument("plan_create_gpu: null argument");
+    qbxg::validate_inputs(*cfg, *geom);
+    auto* pl = new qbxg_plan;
+    try {
+      pl->p.cfg = *cfg;
+      qbxg::build_tree_gpu(pl->p, *geom);
+      if (gpu_lists)
+        qbxg::build_lists_gpu(pl->p);
+      else
+        qbxg::build_lists(pl->p);
     } catch (...) {
       delete pl;
       throw;
