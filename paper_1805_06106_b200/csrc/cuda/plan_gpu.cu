@@ -31,6 +31,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -562,6 +563,410 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
 
 }  // namespace qbxg
 
+// ============================================================================
+// Interaction lists on the GPU (Definitions 1-8; plan.cpp
+// build_lists): the same rows, sorted by box id, hence the same CSR arrays and
+// hashes.  One thread per box; the host's explicit-stack descents become
+// stackless preorder walks (descend = b + 1, prune = b = sub_end[b]), which
+// visit the same boxes in a different order -- rows are sorted at the end
+// (segmented sort), so order is immaterial.  Two passes (count, fill) per list.
+// Colleague rows and the List-2 rows come out sorted by construction (children
+// of sorted colleagues in DFS order).  List 4 is top-down by level because a
+// box inherits its parent's List-4-close candidates.
+// ============================================================================
 namespace qbxg {
-void build_lists_gpu(Plan&) { throw InvalidArgument("plan_create_gpu: device lists not built yet"); }
+namespace {
+
+constexpr int kColl = 125;  // 2-colleagues: at most 5^3
+
+struct DTree {
+  int nb;
+  const double* center;
+  const double* h;
+  const int* level;
+  const int* parent;
+  const long long* ic;
+  const int* cstart;
+  const int* kids;
+  const int* sub_end;
+  const int* src_own;
+  const int* src_sub;
+  const unsigned char* flags;
+  const int* coll;
+  const int* ncoll;
+};
+
+__device__ __forceinline__ bool t_leaf(const DTree& T, int b) { return T.cstart[b + 1] == T.cstart[b]; }
+__device__ __forceinline__ bool t_src(const DTree& T, int b) { return T.src_sub[b] > 0; }
+__device__ __forceinline__ long long t_cheb(const DTree& T, int a, int b) {
+  long long m = 0;
+  for (int d = 0; d < 3; ++d) m = max(m, llabs(T.ic[3 * a + d] - T.ic[3 * b + d]));
+  return m;
+}
+__device__ __forceinline__ bool t_adj(const DTree& T, int a, int b) {  // predicates.hpp boxes_adjacent
+  const int la = T.level[a], lb = T.level[b], L = max(la, lb);
+  for (int d = 0; d < 3; ++d) {
+    const long long alo = T.ic[3 * a + d] << (L - la), ahi = (T.ic[3 * a + d] + 1) << (L - la);
+    const long long blo = T.ic[3 * b + d] << (L - lb), bhi = (T.ic[3 * b + d] + 1) << (L - lb);
+    if (alo > bhi || blo > ahi) return false;
+  }
+  return true;
+}
+// predicates.hpp sep_box_tcr(centre(a), |a|, centre(b), |b|): a < TCR(b)
+__device__ __forceinline__ bool t_sep_box_tcr(const DTree& T, int a, int b, double tf) {
+  const double dx = T.center[3 * a] - T.center[3 * b], dy = T.center[3 * a + 1] - T.center[3 * b + 1],
+               dz = T.center[3 * a + 2] - T.center[3 * b + 2];
+  const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  return __dsub_rn(d, __dmul_rn(__dmul_rn(kSqrt3, T.h[b]), __dadd_rn(1.0, tf))) >= __dmul_rn(3.0, T.h[a]);
+}
+// predicates.hpp sep_tcr_box(centre(a), |a|, centre(b), |b|): TCR(a) < b
+__device__ __forceinline__ bool t_sep_tcr_box(const DTree& T, int a, int b, double tf) {
+  const double dx = fabs(T.center[3 * a] - T.center[3 * b]), dy = fabs(T.center[3 * a + 1] - T.center[3 * b + 1]),
+               dz = fabs(T.center[3 * a + 2] - T.center[3 * b + 2]);
+  const double d = dx > dy ? (dx > dz ? dx : dz) : (dy > dz ? dy : dz);
+  return __dsub_rn(d, T.h[b]) >= __dmul_rn(__dmul_rn(3.0, T.h[a]), __dadd_rn(1.0, tf));
+}
+
+__global__ void k_coll(DTree T, const int* __restrict__ lboxes, int n, int* __restrict__ coll,
+                       int* __restrict__ ncoll) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = lboxes[i], p = T.parent[b];
+  int c = 0;
+  for (int j = 0; j < T.ncoll[p]; ++j) {
+    const int pc = T.coll[kColl * p + j];
+    for (int k = T.cstart[pc]; k < T.cstart[pc + 1]; ++k) {
+      const int d = T.kids[k];
+      if (t_cheb(T, d, b) <= 2) coll[kColl * size_t(b) + c++] = d;
+    }
+  }
+  ncoll[b] = c;
+}
+
+enum { LU = 0, LV = 1, LWC = 2, LWF = 3 };
+
+// Lists 1, 2, 3 close / far for every box: pass 0 counts into cnt[k][b], pass 1
+// writes at start[k][b]
+struct Rows {
+  long long* cnt[4];
+  const long long* start[4];
+  int* out[4];
+};
+
+template <bool FILL>
+__global__ void k_uvw(DTree T, double tf, int demote, Rows R) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= T.nb) return;
+  long long n[4] = {0, 0, 0, 0};
+  auto emit = [&](int k, int x) {
+    if (FILL) R.out[k][R.start[k][b] + n[k]] = x;
+    ++n[k];
+  };
+  const unsigned char f = T.flags[b];
+  const bool tgt = f & QBXG_BOX_TARGET, tgt_anc = f & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR);
+  if (tgt_anc && b != 0) {  // List 2: children of the parent's colleagues, well separated, with sources
+    const int p = T.parent[b];
+    for (int j = 0; j < T.ncoll[p]; ++j) {
+      const int pc = T.coll[kColl * p + j];
+      for (int k = T.cstart[pc]; k < T.cstart[pc + 1]; ++k) {
+        const int d = T.kids[k];
+        if (t_src(T, d) && t_cheb(T, d, b) > 2) emit(LV, d);
+      }
+    }
+  }
+  if (tgt) {
+    // List 1 (Definition 1): source leaves of the subtree ...
+    for (int d = b; d < T.sub_end[b];) {
+      if (!t_src(T, d)) {
+        d = T.sub_end[d];
+        continue;
+      }
+      if (t_leaf(T, d) && T.src_own[d] > 0) emit(LU, d);
+      ++d;
+    }
+    const int* cb = T.coll + kColl * size_t(b);
+    const int ncb = T.ncoll[b];
+    // ... source leaves adjacent to b below its adjacent colleagues ...
+    for (int j = 0; j < ncb; ++j) {
+      const int e = cb[j];
+      if (e == b || t_cheb(T, e, b) > 1) continue;
+      for (int x = e; x < T.sub_end[e];) {
+        if (!t_src(T, x) || !t_adj(T, x, b)) {
+          x = T.sub_end[x];
+        } else {
+          if (t_leaf(T, x)) emit(LU, x);
+          ++x;
+        }
+      }
+    }
+    // ... and coarser source leaves adjacent to b among the ancestors' near colleagues
+    for (int a = T.parent[b]; a >= 0; a = T.parent[a])
+      for (int j = 0; j < T.ncoll[a]; ++j) {
+        const int e = T.coll[kColl * size_t(a) + j];
+        if (e != a && t_cheb(T, e, a) <= 1 && t_leaf(T, e) && T.src_own[e] > 0 && t_adj(T, e, b)) emit(LU, e);
+      }
+    // List 3 (Definition 3), split close / far (Definitions 5, 6; Remark 1 demotion)
+    for (int j = 0; j < ncb; ++j) {
+      const int e = cb[j];
+      if (e == b || t_leaf(T, e)) continue;
+      for (int d = e + 1; d < T.sub_end[e];) {
+        if (!t_src(T, d)) {
+          d = T.sub_end[d];
+          continue;
+        }
+        if (t_adj(T, d, b)) {
+          ++d;  // adjacent: descend (a leaf's subtree is itself)
+          continue;
+        }
+        for (int y = d; y < T.sub_end[d];) {  // d is in List 3: classify its subtree
+          if (!t_src(T, y)) {
+            y = T.sub_end[y];
+          } else if (t_sep_box_tcr(T, y, b, tf)) {
+            if (demote > 0 && T.src_sub[y] < demote) {
+              for (int x = y; x < T.sub_end[y]; ++x)
+                if (t_leaf(T, x) && T.src_own[x] > 0) emit(LWC, x);
+            } else {
+              emit(LWF, y);
+            }
+            y = T.sub_end[y];
+          } else {
+            if (t_leaf(T, y)) emit(LWC, y);
+            ++y;
+          }
+        }
+        d = T.sub_end[d];
+      }
+    }
+  }
+  if (!FILL)
+    for (int k = 0; k < 4; ++k) R.cnt[k][b] = n[k];
+}
+
+// List 4 (Definition 4) close / far (Definitions 7, 8) for the boxes of one level;
+// the parent's close row is read from (xc_off, xc_len) in the pool
+template <bool FILL>
+__global__ void k_x(DTree T, double tf, const int* __restrict__ lboxes, int n, long long* __restrict__ cxc,
+                    long long* __restrict__ cxf, const long long* __restrict__ oxc, const long long* __restrict__ oxf,
+                    long long* __restrict__ xc_off, int* __restrict__ xc_len, long long* __restrict__ xf_off,
+                    int* __restrict__ xf_len, int* __restrict__ pool) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = lboxes[i];
+  long long nc = 0, nf = 0;
+  auto put = [&](int d) {
+    if (t_sep_tcr_box(T, b, d, tf)) {
+      if (FILL) pool[oxf[i] + nf] = d;
+      ++nf;
+    } else {
+      if (FILL) pool[oxc[i] + nc] = d;
+      ++nc;
+    }
+  };
+  if (T.flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) {
+    for (int j = 0; j < T.ncoll[b]; ++j) {
+      const int c = T.coll[kColl * size_t(b) + j];
+      if (c != b && t_leaf(T, c) && T.src_own[c] > 0 && !t_adj(T, c, b)) put(c);
+    }
+    const int par = T.parent[b];
+    if (par >= 0) {
+      for (int anc = par; anc >= 0; anc = T.parent[anc])
+        for (int j = 0; j < T.ncoll[anc]; ++j) {
+          const int c = T.coll[kColl * size_t(anc) + j];
+          if (t_leaf(T, c) && T.src_own[c] > 0 && t_adj(T, c, par) && !t_adj(T, c, b)) put(c);
+        }
+      for (int j = 0; j < xc_len[par]; ++j) put(pool[xc_off[par] + j]);
+    }
+  }
+  if (FILL) {
+    xc_off[b] = oxc[i];
+    xc_len[b] = int(nc);
+    xf_off[b] = oxf[i];
+    xf_len[b] = int(nf);
+  } else {
+    cxc[i] = nc;
+    cxf[i] = nf;
+  }
+}
+
+__global__ void k_gather(int nb, const long long* __restrict__ off, const int* __restrict__ len,
+                         const long long* __restrict__ start, const int* __restrict__ pool, int* __restrict__ out) {
+  const int b = blockIdx.x;
+  for (int j = threadIdx.x; j < len[b]; j += blockDim.x) out[start[b] + j] = pool[off[b] + j];
+}
+
+__global__ void k_len64(int nb, const int* __restrict__ len, long long* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b <= nb) out[b] = b < nb ? len[b] : 0;
+}
+
+void exclusive_sum64(Arena& A, const long long* in, long long* out, long long n) {
+  size_t tb = 0;
+  PCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n));
+  void* t = A.alloc<char>(tb);
+  PCK(cub::DeviceScan::ExclusiveSum(t, tb, in, out, n));
+}
+
+// sort each row of a CSR list in place (rows begin at start[b], end at start[b+1])
+void sort_rows(Arena& A, int* keys, long long total, int nb, const long long* start) {
+  if (total == 0) return;
+  int* tmp = A.alloc<int>(total);
+  size_t tb = 0;
+  PCK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys, tmp, total, nb, start, start + 1));
+  void* t = A.alloc<char>(tb);
+  PCK(cub::DeviceSegmentedSort::SortKeys(t, tb, keys, tmp, total, nb, start, start + 1));
+  PCK(cudaMemcpy(keys, tmp, sizeof(int) * size_t(total), cudaMemcpyDeviceToDevice));
+}
+
+__global__ void k_add(long long* __restrict__ v, int n, long long c) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] += c;
+}
+
+void add_offset(long long* v, int n, long long c) {
+  if (c != 0 && n > 0) k_add<<<(n + 255) / 256, 256>>>(v, n, c);
+}
+
+template <class T>
+T* up(Arena& A, const std::vector<T>& v) {
+  return upload(A, v.data(), v.size());
+}
+
+}  // namespace
+
+void build_lists_gpu(Plan& P) {
+  const double t0 = now_seconds();
+  const int nb = P.nb;
+  const double tf = P.cfg.t_f;
+  const int demote = P.cfg.w_far_demote;
+  Arena A;
+  std::vector<long long> icll(P.ic.begin(), P.ic.end());
+  DTree T{};
+  T.nb = nb;
+  T.center = up(A, P.center);
+  T.h = up(A, P.h);
+  T.level = up(A, P.level);
+  T.parent = up(A, P.parent);
+  T.ic = up(A, icll);
+  T.cstart = up(A, P.child_starts);
+  T.kids = up(A, P.children);
+  T.sub_end = up(A, P.subtree_end);
+  T.src_own = up(A, P.src_own_count);
+  T.src_sub = up(A, P.src_sub_count);
+  T.flags = up(A, P.flags);
+  int* coll = A.alloc<int>(size_t(kColl) * nb);
+  int* ncoll = A.alloc<int>(nb);
+  T.coll = coll;
+  T.ncoll = ncoll;
+  const int* lboxes = up(A, P.level_boxes);
+  const int tb = 128;
+  // 2-colleagues, level by level (root: itself)
+  {
+    const int zero = 0, one = 1;
+    PCK(cudaMemcpy(coll, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    PCK(cudaMemcpy(ncoll, &one, sizeof(int), cudaMemcpyHostToDevice));
+    for (int l = 1; l < P.nlev; ++l) {
+      const int a = P.level_starts[l], n = P.level_starts[l + 1] - a;
+      if (n) k_coll<<<(n + tb - 1) / tb, tb>>>(T, lboxes + a, n, coll, ncoll);
+    }
+  }
+  // Lists 1, 2, 3
+  Rows R{};
+  long long* st[4];
+  for (int k = 0; k < 4; ++k) {
+    R.cnt[k] = A.alloc<long long>(size_t(nb) + 1);
+    st[k] = A.alloc<long long>(size_t(nb) + 1);
+    R.start[k] = st[k];
+    PCK(cudaMemset(R.cnt[k] + nb, 0, sizeof(long long)));
+  }
+  const unsigned gb = unsigned((nb + tb - 1) / tb);
+  k_uvw<false><<<gb, tb>>>(T, tf, demote, R);
+  PCK(cudaGetLastError());
+  long long tot[4];
+  for (int k = 0; k < 4; ++k) {
+    exclusive_sum64(A, R.cnt[k], st[k], nb + 1);
+    PCK(cudaMemcpy(&tot[k], st[k] + nb, sizeof(long long), cudaMemcpyDeviceToHost));
+    R.out[k] = A.alloc<int>(size_t(tot[k]));
+  }
+  k_uvw<true><<<gb, tb>>>(T, tf, demote, R);
+  PCK(cudaGetLastError());
+  sort_rows(A, R.out[LU], tot[LU], nb, st[LU]);  // List 2 rows are sorted by construction
+  sort_rows(A, R.out[LWC], tot[LWC], nb, st[LWC]);
+  sort_rows(A, R.out[LWF], tot[LWF], nb, st[LWF]);
+
+  // List 4, top-down by level; rows live in a growing pool until the final gather
+  long long* xc_off = A.alloc<long long>(nb);
+  long long* xf_off = A.alloc<long long>(nb);
+  int* xc_len = A.alloc<int>(nb);
+  int* xf_len = A.alloc<int>(nb);
+  PCK(cudaMemset(xc_len, 0, sizeof(int) * size_t(nb)));
+  PCK(cudaMemset(xf_len, 0, sizeof(int) * size_t(nb)));
+  int maxw = 0;
+  for (int l = 0; l < P.nlev; ++l) maxw = std::max(maxw, P.level_starts[l + 1] - P.level_starts[l]);
+  long long* cxc = A.alloc<long long>(size_t(maxw) + 1);
+  long long* cxf = A.alloc<long long>(size_t(maxw) + 1);
+  long long* oxc = A.alloc<long long>(size_t(maxw) + 1);
+  long long* oxf = A.alloc<long long>(size_t(maxw) + 1);
+  size_t pool_cap = std::max<size_t>(1 << 20, size_t(nb) * 16);
+  int* pool = A.alloc<int>(pool_cap);
+  long long pool_used = 0;
+  for (int l = 0; l < P.nlev; ++l) {
+    const int a = P.level_starts[l], n = P.level_starts[l + 1] - a;
+    if (n == 0) continue;
+    const unsigned g = unsigned((n + tb - 1) / tb);
+    k_x<false><<<g, tb>>>(T, tf, lboxes + a, n, cxc, cxf, nullptr, nullptr, xc_off, xc_len, xf_off, xf_len, pool);
+    PCK(cudaMemset(cxc + n, 0, sizeof(long long)));
+    PCK(cudaMemset(cxf + n, 0, sizeof(long long)));
+    exclusive_sum64(A, cxc, oxc, n + 1);
+    exclusive_sum64(A, cxf, oxf, n + 1);
+    long long nc = 0, nf = 0;
+    PCK(cudaMemcpy(&nc, oxc + n, sizeof(long long), cudaMemcpyDeviceToHost));
+    PCK(cudaMemcpy(&nf, oxf + n, sizeof(long long), cudaMemcpyDeviceToHost));
+    if (size_t(pool_used + nc + nf) > pool_cap) {
+      const size_t ncap = std::max(2 * pool_cap, size_t(pool_used + nc + nf));
+      int* np2 = A.alloc<int>(ncap);
+      PCK(cudaMemcpy(np2, pool, sizeof(int) * size_t(pool_used), cudaMemcpyDeviceToDevice));
+      pool = np2;
+      pool_cap = ncap;
+    }
+    // close rows at [pool_used, +nc), far rows after them
+    add_offset(oxc, n, pool_used);
+    add_offset(oxf, n, pool_used + nc);
+    k_x<true><<<g, tb>>>(T, tf, lboxes + a, n, nullptr, nullptr, oxc, oxf, xc_off, xc_len, xf_off, xf_len, pool);
+    PCK(cudaGetLastError());
+    pool_used += nc + nf;
+  }
+  long long* xst[2];
+  int* xout[2];
+  long long xtot[2];
+  {
+    const long long* offs[2] = {xc_off, xf_off};
+    const int* lens[2] = {xc_len, xf_len};
+    for (int k = 0; k < 2; ++k) {
+      long long* l64 = A.alloc<long long>(size_t(nb) + 1);
+      k_len64<<<(nb + 1 + tb - 1) / tb, tb>>>(nb, lens[k], l64);
+      xst[k] = A.alloc<long long>(size_t(nb) + 1);
+      exclusive_sum64(A, l64, xst[k], nb + 1);
+      PCK(cudaMemcpy(&xtot[k], xst[k] + nb, sizeof(long long), cudaMemcpyDeviceToHost));
+      xout[k] = A.alloc<int>(size_t(xtot[k]));
+      k_gather<<<nb, 64>>>(nb, offs[k], lens[k], xst[k], pool, xout[k]);
+      sort_rows(A, xout[k], xtot[k], nb, xst[k]);
+    }
+  }
+  PCK(cudaGetLastError());
+
+  // download in the host layout and hash
+  const int map[QBXG_NUM_LISTS] = {LU, LV, LWC, LWF, -1, -2};
+  for (int k = 0; k < QBXG_NUM_LISTS; ++k) {
+    const long long* s = map[k] >= 0 ? st[map[k]] : xst[-1 - map[k]];
+    const int* o = map[k] >= 0 ? R.out[map[k]] : xout[-1 - map[k]];
+    const long long t = map[k] >= 0 ? tot[map[k]] : xtot[-1 - map[k]];
+    std::vector<long long> s64;
+    to_host(s64, s, size_t(nb) + 1);
+    P.lst_starts[k].assign(s64.begin(), s64.end());
+    to_host(P.lst[k], o, size_t(t));
+  }
+  hash_lists(P);
+  P.t_lists = now_seconds() - t0;
+}
+
 }  // namespace qbxg

@@ -37,7 +37,9 @@ CASES = [("config0", lambda: api.config_geometry(0), api.config_fmm(0)),
          ("config2_small", lambda: api.config_geometry(2, level=2, n_volume_targets=3000), api.config_fmm(2)),
          ("cloud", lambda: _cloud(0), api.FmmConfig(p_fmm=8, p_qbx=3, n_max=32)),
          ("clustered", lambda: _cloud(1, clustered=True), api.FmmConfig(p_fmm=8, p_qbx=3, n_max=16)),
-         ("one_box", lambda: _cloud(2, 20, 10, 5), api.FmmConfig(p_fmm=4, p_qbx=2, n_max=64))]
+         ("one_box", lambda: _cloud(2, 20, 10, 5), api.FmmConfig(p_fmm=4, p_qbx=2, n_max=64)),
+         ("no_demotion_tf0", lambda: api.config_geometry(0, level=3), api.config_fmm(0, w_far_demote=0, t_f=0.0)),
+         ("torus_small", lambda: api.config_geometry(1, nu=64, nv=32), api.config_fmm(1))]
 
 
 def test_gpu_plan_refuses_without_device():
@@ -55,7 +57,16 @@ def test_gpu_tree_matches_host(name, geo, cfg):
 
 
 @pytest.mark.gpu
-def test_gpu_tree_config1_full_size():
+@pytest.mark.parametrize("name,geo,cfg", CASES, ids=[c[0] for c in CASES])
+def test_gpu_plan_with_lists_matches_host(name, geo, cfg):
+    g = geo()
+    _same(api.Plan(cfg, g), api.Plan(cfg, g, device="gpu"))
+
+
+@pytest.mark.gpu
+def test_gpu_plan_config1_full_size():
     g = api.config_geometry(1)
     cfg = api.config_fmm(1)
-    _same(api.Plan(cfg, g), api.Plan(cfg, g, device="gpu", gpu_lists=False))
+    host = api.Plan(cfg, g)
+    _same(host, api.Plan(cfg, g, device="gpu", gpu_lists=False), lists=False)
+    _same(host, api.Plan(cfg, g, device="gpu"))
