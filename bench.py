@@ -212,6 +212,18 @@ def run_ours(args, rank, world, local_rank):
     else:
         eng = api.FmmEngine(cfg, g, plan, device=local_rank)
     t3 = time.perf_counter()
+    # Stage 1 on the GPU (qbxg_plan_create_gpu): same plan bit for bit
+    plan_gpu = None
+    if world == 1:
+        api.Plan(cfg, g, device="gpu")  # warm-up (CUB kernels, allocator)
+        tg = time.perf_counter()
+        pg = api.Plan(cfg, g, device="gpu")
+        tg = time.perf_counter() - tg
+        ha, ga = plan.arrays(), pg.arrays()
+        same_plan = pg.list_hashes() == plan.list_hashes() and all(np.array_equal(ha[k], ga[k]) for k in ha)
+        plan_gpu = {"total": round(tg, 4), "tree": round(pg.view.build_seconds_tree, 4),
+                    "lists": round(pg.view.build_seconds_lists, 4), "bitwise_equal_to_host": bool(same_plan)}
+        del pg
     led = plan.ledger()
     w, mu = g.weights(), g.dipoles()
     dev = torch.device("cuda", local_rank)
@@ -446,7 +458,8 @@ def run_ours(args, rank, world, local_rank):
                 "batch": batch, "helmholtz": helm, "association": assoc,
                 "cpu_baseline": cpu,
                 "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
-                            "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3)},
+                            "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3),
+                            "plan_gpu": plan_gpu},
                 "list_hashes": {k: f"{v:016x}" for k, v in plan.list_hashes().items()},
                 "host_device_bitwise_equal": same}
         print(json.dumps(line), flush=True)

@@ -35,6 +35,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -73,6 +75,19 @@ struct Arena {
   }
   ~Arena() {
     for (void* q : p) cudaFree(q);
+  }
+};
+
+// QBXG_PLAN_TIMING=1: per-phase wall times (device-synchronised) on stderr
+struct PhaseClock {
+  bool on = std::getenv("QBXG_PLAN_TIMING") != nullptr;
+  double t = now_seconds();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const double n = now_seconds();
+    std::fprintf(stderr, "[plan_gpu] %-24s %8.2f ms\n", what, (n - t) * 1e3);
+    t = n;
   }
 };
 
@@ -375,6 +390,7 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
   const long long np = P.ns + P.nc + P.nconv;
   if (np == 0) throw InvalidArgument("plan_create_device: no particles");
   Arena A;
+  PhaseClock clk;
   const double* dsp = upload(A, g.source_pos, 3 * size_t(P.ns));
   const double* dcp = upload(A, g.center_pos, 3 * size_t(P.nc));
   const double* dcr = upload(A, g.center_radius, size_t(P.nc));
@@ -406,6 +422,7 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
   if (!(hroot > 0)) hroot = 1.0;
   hroot *= 1.0 + 1.0 / 1024.0;
   P.root_h = hroot;
+  clk.mark("upload + root");
 
   // box table (creation order), grown on demand
   size_t cap = std::max<size_t>(1024, size_t(4 * np / std::max(1, cfg.n_max)) + 64);
@@ -469,6 +486,7 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
     ncur = tot;
   }
   PCK(cudaGetLastError());
+  clk.mark("levels");
 
   // DFS preorder = order of (range start, level)
   const int lev_bits = 6;
@@ -522,6 +540,7 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
   k_box_roles<<<gb, tb>>>(nb, bstart, bend, bown, fs, fc, ft, R[0], R[1], R[2], nchild, dflags);
   PCK(cudaGetLastError());
 
+  clk.mark("dfs + roles");
   // download into the host plan
   P.nb = nb;
   to_host(P.center, dcen, 3 * size_t(nb));
@@ -558,6 +577,7 @@ void build_tree_gpu(Plan& P, const qbxg_geometry& g) {
     std::vector<int32_t> fill(P.level_starts.begin(), P.level_starts.end() - 1);
     for (int32_t b = 0; b < nb; ++b) P.level_boxes[fill[P.level[b]]++] = b;
   }
+  clk.mark("download");
   P.t_tree = now_seconds() - t0;
 }
 
@@ -839,6 +859,7 @@ void build_lists_gpu(Plan& P) {
   const double tf = P.cfg.t_f;
   const int demote = P.cfg.w_far_demote;
   Arena A;
+  PhaseClock clk;
   std::vector<long long> icll(P.ic.begin(), P.ic.end());
   DTree T{};
   T.nb = nb;
@@ -869,6 +890,7 @@ void build_lists_gpu(Plan& P) {
       if (n) k_coll<<<(n + tb - 1) / tb, tb>>>(T, lboxes + a, n, coll, ncoll);
     }
   }
+  clk.mark("upload + colleagues");
   // Lists 1, 2, 3
   Rows R{};
   long long* st[4];
@@ -892,6 +914,7 @@ void build_lists_gpu(Plan& P) {
   sort_rows(A, R.out[LU], tot[LU], nb, st[LU]);  // List 2 rows are sorted by construction
   sort_rows(A, R.out[LWC], tot[LWC], nb, st[LWC]);
   sort_rows(A, R.out[LWF], tot[LWF], nb, st[LWF]);
+  clk.mark("lists 1-3");
 
   // List 4, top-down by level; rows live in a growing pool until the final gather
   long long* xc_off = A.alloc<long long>(nb);
@@ -953,6 +976,7 @@ void build_lists_gpu(Plan& P) {
     }
   }
   PCK(cudaGetLastError());
+  clk.mark("list 4");
 
   // download in the host layout and hash
   const int map[QBXG_NUM_LISTS] = {LU, LV, LWC, LWF, -1, -2};
@@ -965,7 +989,9 @@ void build_lists_gpu(Plan& P) {
     P.lst_starts[k].assign(s64.begin(), s64.end());
     to_host(P.lst[k], o, size_t(t));
   }
+  clk.mark("download");
   hash_lists(P);
+  clk.mark("hash");
   P.t_lists = now_seconds() - t0;
 }
 
