@@ -351,6 +351,8 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     // split (block-diagonal after an azimuthal rotation) is the default where its
     // padded block fits the kernel (p <= 20); QBXG_M2L_MODE=dense keeps the full matrix
     P.split = !P.rot && !(mode && std::string(mode) == "dense") && dev::split_nh(p) <= 240;
+    // point-and-shoot on the split frame's real blocks (QBXG_M2L_MODE=pas)
+    P.pas = P.split && mode && std::string(mode) == "pas" && dev::pas_supported(p);
   }
   if (P.rot) {
     if (!std::getenv("QBXG_M2L_BN")) P.bn = 16;
@@ -379,6 +381,15 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     }
     dev::launch_m2l_ops_split(P, p, d_used, s);
     QCK(cudaGetLastError());
+    if (P.pas) {
+      std::vector<double> pops;
+      std::vector<int> tab;
+      dev::pas_build_ops(p, P.n_ops, used.data(), pops, P.pas_stride, tab, P.pas_nblk, P.pas_phase, P.pas_base);
+      P.pas_ops = dupload(O, pops, s);
+      P.pas_tab = dupload(O, tab, s);
+      P.pas_tab_n = int(tab.size());
+      QCK(cudaStreamSynchronize(s));
+    }
   } else {
     P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
     dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
@@ -422,7 +433,10 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
         }
       std::vector<int4> tiles;
       {
-        const int64_t tw = P.rot ? dev::kRotSuper : P.split ? dev::split_tile_cols() : P.bn;
+        const int64_t tw = P.rot     ? dev::kRotSuper
+                           : P.pas   ? dev::pas_tile_cols()
+                           : P.split ? dev::split_tile_cols()
+                                     : P.bn;
         for (int o = 0; o < P.n_ops; ++o)
           for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
             tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), 0));

@@ -83,7 +83,20 @@ struct M2LPlan {
   double* rotB = nullptr;      // n_ops x rot_stride: local back-rotation blocks
   double* rho_op = nullptr;    // n_ops: |v| in box units
   size_t rot_stride = 0;
+  // point-and-shoot in the azimuthal frame on real half-table blocks (m2l_pas.cu):
+  // replaces the split GEMM, same staging rows and reduce
+  bool pas = false;
+  double* pas_ops = nullptr;   // n_ops x pas_stride: [W | Z | V]
+  int pas_stride = 0, pas_phase = 0, pas_nblk = 0;
+  int* pas_tab = nullptr;      // block row sets and per-unit segment schedule
+  int pas_tab_n = 0;
+  int pas_base[3] = {0, 0, 0};
 };
+bool pas_supported(int p);
+int pas_tile_cols();
+void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& ops, int& op_stride,
+                   std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]);
+int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s);
 int launch_m2l_rot_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
 // rotation blocks staged once per CTA; tiles of up to kRotSuper same-offset columns
 constexpr int kRotSuper = 256;

@@ -771,7 +771,9 @@ int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s) {
   for (int c = 0; c < int(P.chunks.size()); ++c) {
     const M2LChunk& C = P.chunks[c];
     if (C.n_tiles == 0) continue;
-    if (P.split) {
+    if (P.pas) {
+      launch_m2l_pas(P, C, reinterpret_cast<const double*>(D.M), kp2, D.p, s);
+    } else if (P.split) {
       const double* X = reinterpret_cast<const double*>(D.M);
       switch (split_nh(D.p)) {
         case 48: split_nh_launch<48>(P, C, X, kp2, D.p, s); break;

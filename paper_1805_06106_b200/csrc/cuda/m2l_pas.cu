@@ -1,0 +1,369 @@
+// Stage 4 M2L (List 2) as point-and-shoot in the azimuthal frame, on real
+// half-table blocks.
+//
+// The split M2L (m2l_gemm.cu) rotates about z by alpha = atan2(dy, dx) so the
+// offset v' = (2 rho, 0, 2 dz) lies in the xz-plane; there the operator is real
+// and block diagonal in (Re, Im) -- two dense hsize(p)^2 blocks.  Rotating on
+// about y by theta = angle(v', z) puts v' on +z, where the translation is
+// diagonal in the order m.  For real data (M_n^{-m} = (-1)^m conj M_n^m) each of
+// the three factors keeps Re and Im parts apart:
+//   W (multipole rotation):  per degree j, a (j+1)^2 Re block and a j^2 Im block
+//   Z (z-translation):       per order m, rows n / columns j in [m, p]:
+//                            (-1)^{n+m} (j+n)! / |v'|^{j+n+1}, the same for Re and Im
+//   V (local back-rotation): per degree n, like W
+// 3 x 2,736 multiply-adds per List-2 entry at p = 15 instead of 32,896 for the two
+// dense blocks: 4x less arithmetic (3x on the tensor pipe after padding blocks to
+// 8-row / 4-column DMMA tiles).
+// W and V are the real parts of the validated rotation blocks of rotation.cpp
+// evaluated at v' (phi = 0, so their Re/Im cross terms vanish; checked at setup).
+//
+// Kernel: one CTA = one offset x 32 entries (tiles as the split M2L).  The
+// gathered, alpha-rotated multipoles sit in shared memory as (p+1)^2 rows (Re in
+// hidx order, Im in compacted order) x 32 columns.  In each phase every warp owns
+// a fixed list of whole blocks (longest-processing-time balanced on the host), so
+// the phase runs in place: the warp reads a block's operator (A fragments, from
+// L2) and its rows (B fragments, from shared memory) into registers, runs the
+// m8n8k4 DMMAs, then writes its rows.  Output rows use the split M2L's
+// staging layout, so its CSR-order reduce (back-rotation by alpha, 1/|b|)
+// finishes the job unchanged.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "harmonics.cuh"
+#include "kernels.cuh"
+#include "../host/rotation.hpp"
+
+namespace qbxg {
+namespace dev {
+
+namespace {
+
+constexpr int kPasMaxS = 16;  // largest block: p + 1
+constexpr int kPasPhases = 3;
+constexpr int kWarps = 8, kBN = 32, kLD = kBN + 1;
+
+// table layout (ints), per phase: [nblk+1 row offsets][nblk op offsets]
+// [(p+1)^2 rows][kWarps+1 warp offsets][block ids]
+struct TabHead {
+  int base[kPasPhases];
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// One block of size S in place on the fp64 tensor pipe (mma.sync m8n8k4): the
+// operator (rows padded to 8, columns to 4, zeros) as A fragments from L2, the
+// block's rows x 32 columns as B fragments from shared memory -- all read before
+// any row is written, so the warp may overwrite its own block.
+template <int S>
+__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* __restrict__ Ob, int lane) {
+  constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, K4 = 4 * KS, NT = kBN / 8;
+  double a[MT][KS], b[KS][NT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = __ldg(Ob + (mt * 8 + (lane >> 2)) * K4 + ks * 4 + (lane & 3));
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + (lane & 3);
+    const int row = k < S ? rw[k] : 0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[row * kLD + nt * 8 + (lane >> 2)] : 0.0;
+  }
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[ks][nt]);
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = mt * 8 + (lane >> 2);
+    if (r < S) {
+      const int row = rw[r];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        X[row * kLD + nt * 8 + (lane & 3) * 2] = acc[mt][nt][0];
+        X[row * kLD + nt * 8 + (lane & 3) * 2 + 1] = acc[mt][nt][1];
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restrict__ tab, int tab_n, TabHead hd,
+                                                           int nblk, const double* __restrict__ ops, int op_stride,
+                                                           int phase_size, const double2* __restrict__ cs_all,
+                                                           const int4* __restrict__ tiles,
+                                                           const int* __restrict__ col_src,
+                                                           const int* __restrict__ col_pos,
+                                                           const double* __restrict__ M, int kp2, int KRp,
+                                                           double* __restrict__ temp) {
+  constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), NTH = kWarps * 32;
+  extern __shared__ double smem[];
+  double* X = smem;
+  int* s_tab = reinterpret_cast<int*>(X + NROW * kLD);
+  __shared__ int s_src[kBN];
+  __shared__ double2 s_cs[P + 1];
+  __shared__ int s_code[NR];  // Re row | Im row << 10 (0 for m = 0) | m << 20 of half-table index q
+  const int4 tile = tiles[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < tab_n; i += NTH) s_tab[i] = tab[i];
+  if (tid < kBN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+  if (tid <= P) s_cs[tid] = cs_all[size_t(tile.x) * (P + 1) + tid];
+  for (int q = tid; q < NR; q += NTH) {
+    int n = 0;
+    while (hidx(n + 1, 0) <= q) ++n;
+    const int m = q - hidx(n, 0);
+    s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0) << 10 | m << 20;
+  }
+  __syncthreads();
+  // gather M' = M e^{i k alpha}, coalesced along each multipole, kSt loads in flight per thread
+  constexpr int kSt = 6;
+  for (int base = 0; base < NR * kBN; base += kSt * NTH) {
+    double2 v[kSt];
+#pragma unroll
+    for (int u = 0; u < kSt; ++u) {
+      const int e = base + tid + u * NTH;
+      v[u] = make_double2(0.0, 0.0);
+      if (e < NR * kBN) {
+        const int c = e / NR, q = e - c * NR;
+        const int src = s_src[c];
+        if (src >= 0) v[u] = __ldg(reinterpret_cast<const double2*>(M + size_t(src) * kp2) + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSt; ++u) {
+      const int e = base + tid + u * NTH;
+      if (e < NR * kBN) {
+        const int c = e / NR, q = e - c * NR;
+        const int code = s_code[q], ri = (code >> 10) & 1023;
+        const double2 r = s_cs[code >> 20];
+        X[(code & 1023) * kLD + c] = v[u].x * r.x - v[u].y * r.y;
+        if (ri) X[ri * kLD + c] = v[u].x * r.y + v[u].y * r.x;
+      }
+    }
+  }
+  __syncthreads();
+  const double* opb = ops + size_t(tile.x) * op_stride;
+#pragma unroll 1
+  for (int ph = 0; ph < kPasPhases; ++ph) {
+    const int* T = s_tab + hd.base[ph];
+    const int* rowoff = T;
+    const int* opoff = T + nblk + 1;
+    const int* rows = opoff + nblk;
+    const int* woff = rows + NROW;
+    const int* wblk = woff + kWarps + 1;
+    const double* Op = opb + size_t(ph) * phase_size;
+#pragma unroll 1
+    for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
+      const int b = wblk[i];
+      const int* rw = rows + rowoff[b];
+      const double* Ob = Op + opoff[b];
+      switch (rowoff[b + 1] - rowoff[b]) {
+#define QBXG_PAS_CASE(S) \
+  case S:                \
+    pas_block<S>(X, rw, Ob, lane); \
+    break;
+        QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
+        QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11) QBXG_PAS_CASE(12)
+        QBXG_PAS_CASE(13) QBXG_PAS_CASE(14) QBXG_PAS_CASE(15) QBXG_PAS_CASE(16)
+#undef QBXG_PAS_CASE
+        default: break;
+      }
+    }
+    __syncthreads();
+  }
+  // staging row = Re (NR) then compacted Im, coalesced along each row
+  for (int e = tid; e < NROW * kBN; e += NTH) {
+    const int c = e / NROW, r = e - c * NROW;
+    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KRp + r] = X[r * kLD + c];
+  }
+}
+
+// ---------------------------------------------------------------- host side
+struct PasLayout {
+  int nblk = 0, phase_size = 0;
+  std::vector<int> tab;
+  TabHead hd{};
+};
+
+// blocks of one phase: row index sets (Re rows hidx(n, m); Im rows NR + n(n-1)/2 + m - 1)
+void phase_blocks(int p, int ph, std::vector<std::vector<int>>& blocks) {
+  const int NR = hsize(p);
+  auto re = [&](int n, int m) { return hidx(n, m); };
+  auto im = [&](int n, int m) { return NR + n * (n - 1) / 2 + m - 1; };
+  blocks.clear();
+  for (int part = 0; part < 2; ++part)
+    for (int a = part; a <= p; ++a) {
+      std::vector<int> b;
+      if (ph != 1)  // W, V: degree a, orders part..a
+        for (int m = part; m <= a; ++m) b.push_back(part ? im(a, m) : re(a, m));
+      else  // Z: order a, degrees a..p
+        for (int n = a; n <= p; ++n) b.push_back(part ? im(n, a) : re(n, a));
+      blocks.push_back(b);
+    }
+}
+
+PasLayout make_layout(int p) {
+  PasLayout L;
+  for (int ph = 0; ph < kPasPhases; ++ph) {
+    std::vector<std::vector<int>> blocks;
+    phase_blocks(p, ph, blocks);
+    L.nblk = int(blocks.size());
+    L.hd.base[ph] = int(L.tab.size());
+    std::vector<int> rowoff{0}, opoff, rows;
+    int oo = 0;
+    for (auto& b : blocks) {
+      const int s = int(b.size());
+      rows.insert(rows.end(), b.begin(), b.end());
+      rowoff.push_back(int(rows.size()));
+      opoff.push_back(oo);
+      oo += (s + 7) / 8 * 8 * ((s + 3) / 4 * 4);  // rows padded to 8, columns to 4
+    }
+    L.phase_size = oo;  // the same for the three phases (same block sizes)
+    // whole blocks per warp, longest processing time first
+    std::vector<int> order(blocks.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return blocks[a].size() > blocks[b].size(); });
+    std::vector<std::vector<int>> wl(kWarps);
+    std::vector<long> load(kWarps, 0);
+    for (int bi : order) {
+      const int w = int(std::min_element(load.begin(), load.end()) - load.begin());
+      load[w] += long(blocks[bi].size() * blocks[bi].size());
+      wl[w].push_back(bi);
+    }
+    std::vector<int> woff{0}, wblk;
+    for (auto& v : wl) {
+      wblk.insert(wblk.end(), v.begin(), v.end());
+      woff.push_back(int(wblk.size()));
+    }
+    for (auto* v : {&rowoff, &opoff, &rows, &woff, &wblk}) L.tab.insert(L.tab.end(), v->begin(), v->end());
+  }
+  return L;
+}
+
+template <int P>
+int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
+  constexpr int NROW = (P + 1) * (P + 1);
+  const size_t smem = size_t(NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_m2l_pas<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+      return -1;
+    attr = smem;
+  }
+  TabHead hd;
+  for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
+  k_m2l_pas<P><<<C.n_tiles, kWarps * 32, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops,
+                                                    Pl.pas_stride, Pl.pas_phase, Pl.cs, C.tiles, C.col_src,
+                                                    C.col_pos, X, kp2, Pl.KRp, Pl.temp);
+  return 1;
+}
+
+}  // namespace
+
+bool pas_supported(int p) { return p >= 4 && p <= 15; }
+int pas_tile_cols() { return kBN; }
+
+// Per-offset operators: [W | Z | V], blocks in phase_blocks order, each row-major
+// with rows padded to 8 and columns to 4 (zeros): DMMA A fragments without guards.
+void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& ops, int& op_stride,
+                   std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]) {
+  const PasLayout L = make_layout(p);
+  nblk = L.nblk;
+  phase_size = L.phase_size;
+  op_stride = kPasPhases * L.phase_size;
+  tab = L.tab;
+  for (int k = 0; k < 3; ++k) base[k] = L.hd.base[k];
+  ops.assign(size_t(n_ops) * op_stride, 0.0);
+  const size_t rs = rot_blocks_size(p);
+  double worst = 0.0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(max : worst)
+  for (int o = 0; o < n_ops; ++o) {
+    const int sl = used_slot[o];
+    const int dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
+    const double v[3] = {2.0 * std::sqrt(double(dx * dx + dy * dy)), 0.0, 2.0 * dz};
+    const double rho = std::sqrt(v[0] * v[0] + v[2] * v[2]);
+    std::vector<double> Rf(rs), Rb(rs);
+    m2l_rotation_blocks(p, v, Rf.data(), Rb.data());
+    double* W = &ops[size_t(o) * op_stride];
+    double* Z = W + L.phase_size;
+    double* V = Z + L.phase_size;
+    auto re = [](int m) { return m == 0 ? 0 : 2 * m - 1; };
+    auto im = [](int m) { return 2 * m; };
+    size_t w = 0, z = 0;
+    for (int part = 0; part < 2; ++part)
+      for (int a = part; a <= p; ++a) {
+        // W, V: degree a (rows / columns = orders part..a); rows padded to 8, columns to 4
+        const int d = 2 * a + 1, s = a + 1 - part, sr = (s + 7) / 8 * 8, sp = (s + 3) / 4 * 4;
+        const double* F = &Rf[rot_block_offset(a)];
+        const double* B = &Rb[rot_block_offset(a)];
+        for (int i = 0; i < sr; ++i)
+          for (int k = 0; k < sp; ++k) {
+            const bool pad = i >= s || k >= s;
+            const int mi = part + (pad ? 0 : i), mk = part + (pad ? 0 : k);
+            const int ri = part ? im(mi) : re(mi), rk = part ? im(mk) : re(mk);
+            W[w + size_t(i) * sp + k] = pad ? 0.0 : F[ri * d + rk];
+            V[w + size_t(i) * sp + k] = pad ? 0.0 : B[ri * d + rk];
+          }
+        w += size_t(sr) * sp;
+        for (int i = 0; i <= a; ++i)  // Re/Im cross terms vanish at phi = 0
+          for (int k = 1; k <= a; ++k) {
+            worst = std::max(worst, std::fabs(F[re(i) * d + im(k)]) + std::fabs(F[im(k) * d + re(i)]));
+            worst = std::max(worst, std::fabs(B[re(i) * d + im(k)]) + std::fabs(B[im(k) * d + re(i)]));
+          }
+        // Z: order m = a, rows n / columns j in [m, p]: (-1)^{n+m} (j+n)! / rho^{j+n+1}
+        const int m = a, sz = p - m + 1, szr = (sz + 7) / 8 * 8, szp = (sz + 3) / 4 * 4;
+        for (int i = 0; i < szr; ++i)
+          for (int k = 0; k < szp; ++k) {
+            double val = 0.0;
+            if (i < sz && k < sz) {
+              const int n = m + i, j = m + k;
+              double f = 1.0;
+              for (int t = 2; t <= j + n; ++t) f *= t;
+              val = (((n + m) & 1) ? -1.0 : 1.0) * f / std::pow(rho, j + n + 1);
+            }
+            Z[z + size_t(i) * szp + k] = val;
+          }
+        z += size_t(szr) * szp;
+      }
+  }
+  if (worst > 1e-12) throw std::runtime_error("pas_build_ops: rotation blocks mix Re and Im at phi = 0");
+}
+
+int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
+  switch (p) {
+    case 4: return pas_launch_p<4>(P, C, X, kp2, s);
+    case 5: return pas_launch_p<5>(P, C, X, kp2, s);
+    case 6: return pas_launch_p<6>(P, C, X, kp2, s);
+    case 7: return pas_launch_p<7>(P, C, X, kp2, s);
+    case 8: return pas_launch_p<8>(P, C, X, kp2, s);
+    case 9: return pas_launch_p<9>(P, C, X, kp2, s);
+    case 10: return pas_launch_p<10>(P, C, X, kp2, s);
+    case 11: return pas_launch_p<11>(P, C, X, kp2, s);
+    case 12: return pas_launch_p<12>(P, C, X, kp2, s);
+    case 13: return pas_launch_p<13>(P, C, X, kp2, s);
+    case 14: return pas_launch_p<14>(P, C, X, kp2, s);
+    case 15: return pas_launch_p<15>(P, C, X, kp2, s);
+    default: return -1;
+  }
+}
+
+}  // namespace dev
+}  // namespace qbxg
