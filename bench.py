@@ -68,8 +68,15 @@ def stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
     # default (split) M2L: after the azimuthal rotation the operator is two real blocks,
     # K_p x K_p (Re) and (K_p-p-1) x (K_p-p-1) (Im, m >= 1); QBXG_M2L_MODE=dense uses
     # the full real operator on the (p+1)^2 real degrees of freedom
-    if os.environ.get("QBXG_M2L_MODE", "") == "dense":
+    mode = os.environ.get("QBXG_M2L_MODE", "")
+    if mode == "dense":
         f["m2l"] = led["entries"]["V"] * 2 * (p + 1) ** 4
+    elif 4 <= p <= 15 and mode not in ("split", "rot"):
+        # point-and-shoot (default for 4 <= p <= 15): W (rotation about y), Z (z-shift) and
+        # V (rotation back) are each block diagonal -- Re blocks of size 1..p+1 and Im blocks
+        # of size 1..p -- so sum(s^2) multiply-adds per factor per entry
+        blk = sum(s * s for s in range(1, p + 2)) + sum(s * s for s in range(1, p + 1))
+        f["m2l"] = led["entries"]["V"] * 2 * 3 * blk
     else:
         f["m2l"] = led["entries"]["V"] * 2 * (kp * kp + (kp - p - 1) ** 2)
     # compulsory: multipoles in + locals out once per box (operators ~0.6 GB amortised)

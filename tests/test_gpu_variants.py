@@ -38,11 +38,11 @@ print(json.dumps(out))
 VARIANTS = [
     {"QBXG_M2L_MODE": "dense"},
     {"QBXG_M2L_MODE": "dense", "QBXG_M2L_BN": "64"},
-    {"QBXG_SPLIT_V1": "1"},
+    {"QBXG_M2L_MODE": "split", "QBXG_SPLIT_V1": "1"},
     {"QBXG_M2L_MODE": "rot"},
     {"QBXG_M2L_MODE": "rot", "QBXG_M2L_ROTV": "3"},
-    {"QBXG_M2L_MODE": "pas"},
-    {"QBXG_M2L_MODE": "pas", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
+    {"QBXG_M2L_MODE": "split"},
+    {"QBXG_M2L_MODE": "split", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
     {"QBXG_NEAR_MODE": "0"},
     {"QBXG_NEAR_MODE": "1"},
     {"QBXG_P2L_LEGACY": "1"},
