@@ -95,6 +95,7 @@ struct Handle {
   std::vector<int> n_l2l_level;
   int* d_ctr_boxes = nullptr;
   int n_ctr_boxes = 0;
+  int* d_near_boxes = nullptr;  // d_ctr_boxes, heaviest near field first (no tail of big boxes)
   int* d_tgt_boxes = nullptr;
   int n_tgt_boxes = 0;
   int* d_v_boxes = nullptr;
@@ -704,7 +705,7 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   QCK(cudaEventRecord(ev[2], s));
   for (int l = H.nlev - 2; l >= 0; --l) chk(dev::helm_shift(HD, 0, H.d_m2m_level[l], H.n_m2m_level[l], H.h_ops_m2m[l], s));
   QCK(cudaEventRecord(ev[3], s));
-  chk(dev::helm_near(HD, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  chk(dev::helm_near(HD, H.d_near_boxes, H.n_ctr_boxes, s));
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
   for (const auto& C : H.h_m2l) {
@@ -928,6 +929,19 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_leaves = int(leaves.size());
     H.d_ctr_boxes = dupload(O, cb, s);
     H.n_ctr_boxes = int(cb.size());
+    {
+      // near-field launch order: decreasing (centres x near sources), ties in box order;
+      // every CTA owns its centres, so the order changes no result
+      std::vector<int64_t> cost(nb, 0);
+      for (int b : cb) {
+        int64_t nsrc = 0;
+        for (int64_t i = ns_[b]; i < ns_[b + 1]; ++i) nsrc += nseg[i].y;
+        cost[b] = nsrc * int64_t(V.ctr_own_count[b]);
+      }
+      std::vector<int> nbx(cb);
+      std::stable_sort(nbx.begin(), nbx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+      H.d_near_boxes = dupload(O, nbx, s);
+    }
     H.d_tgt_boxes = dupload(O, tb, s);
     H.n_tgt_boxes = int(tb.size());
     H.d_v_boxes = dupload(O, vb, s);
@@ -1185,7 +1199,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     QCK(cudaEventRecord(H.fork_ev, s));        // run it beside the whole far-field chain
     QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
     QCK(cudaEventRecord(H.evx[0], H.side));
-    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, H.side));
+    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
     QCK(cudaEventRecord(H.evx[1], H.side));
     QCK(cudaEventRecord(H.join_ev, H.side));
     near_forked = true;
@@ -1220,11 +1234,11 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     QCK(cudaEventRecord(H.fork_ev, s));
     QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
     QCK(cudaEventRecord(H.evx[0], H.side));
-    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, H.side));
+    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
     QCK(cudaEventRecord(H.evx[1], H.side));
     QCK(cudaEventRecord(H.join_ev, H.side));
   } else if (!near_done && !ovl) {
-    chk(dev::launch_near_qbx(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, s));
   }
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
@@ -1319,7 +1333,7 @@ void batch_apply(Handle& H, int R, const double* d_w, const double* d_mu, double
   for (; r0 + NR <= R; r0 += NR) {
     dev::launch_gather_batch(D, int(H.ns), NR, H.d_src_perm, d_w + size_t(r0) * H.ns,
                              d_mu ? d_mu + size_t(r0) * 3 * H.ns : nullptr, H.d_bw, H.d_bmu, s);
-    if (dev::launch_near_qbx_batch(D, H.d_ctr_boxes, H.n_ctr_boxes, NR, H.d_bw, H.d_bmu, H.ns, H.d_bLc, H.nc, s) < 0)
+    if (dev::launch_near_qbx_batch(D, H.d_near_boxes, H.n_ctr_boxes, NR, H.d_bw, H.d_bmu, H.ns, H.d_bLc, H.nc, s) < 0)
       throw InvalidArgument("qbxg_apply_batch: unsupported order");
     L += 2;
     for (int k = 0; k < NR; ++k) {

@@ -206,60 +206,56 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
                                           double* ax, double* ay) {
   constexpr int KI = hsize(Q + (DIP ? 1 : 0));
   const double ux = (x.x - c.x) * ir, uy = (x.y - c.y) * ir, uz = (x.z - c.z) * ir;
-  // J_n^m = r^{2n+1} I_n^m: polynomial recurrences without 1/r^2 per step;
-  // the r^{-(2n+1)} factor is folded into the per-degree source weights.
   constexpr int P1 = Q + (DIP ? 1 : 0);
   const double r2 = ux * ux + uy * uy + uz * uz;
-  const double rs = rsqrt(r2);  // 1/r (1 ulp); 1/r^2 and r^{-(2n+1)} follow by products
+  const double rs = rsqrt(r2);  // 1/r (1 ulp)
   const double ir2 = rs * rs;
-  // The m = 0 column is real (J_n^0 is a polynomial in uz and r2): its imaginary
-  // parts are never formed, and L_n^0 gets no imaginary contribution (ay[hidx(n, 0)]
-  // stays 0) -- about 1/7 of the pair's fp64 instructions at q = 5 with dipoles.
+  // I_n^m(u) directly (I_0^0 = 1/r; every recurrence step carries its 1/r^2 in the
+  // coefficients vx, vy, vz, zc, rc): the source weight and the dipole's (mz, hx, hy)
+  // then multiply the table with no per-degree scale factors.
+  // The m = 0 column is real: its imaginary parts are never formed, and L_n^0 gets no
+  // imaginary contribution (ay[hidx(n, 0)] stays 0).
+  const double vx = ux * ir2, vy = uy * ir2, vz = uz * ir2;
   double2 J[KI];
 #pragma unroll
   for (int m = 0; m <= P1; ++m) {
     if (m == 0) {
-      J[0] = make_double2(1.0, 0.0);
+      J[0] = make_double2(rs, 0.0);
     } else {
       const double2 d = J[hidx(m - 1, m - 1)];
       const double f = double(2 * m - 1);
-      J[hidx(m, m)] = m == 1 ? make_double2(ux, uy)
-                             : make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
+      J[hidx(m, m)] = m == 1 ? make_double2(d.x * vx, d.x * vy)
+                             : make_double2(f * (d.x * vx - d.y * vy), f * (d.x * vy + d.y * vx));
     }
     if (m + 1 <= P1) {
-      const double f = double(2 * m + 1) * uz;
-      J[hidx(m + 1, m)] = m == 0 ? make_double2(uz, 0.0) : make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
+      const double f = double(2 * m + 1) * vz;
+      J[hidx(m + 1, m)] = m == 0 ? make_double2(vz * J[0].x, 0.0)
+                                 : make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
     }
 #pragma unroll
     for (int n = m + 2; n <= P1; ++n) {
-      const double zc = double(2 * n - 1) * uz;
-      const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
+      const double zc = double(2 * n - 1) * vz;
+      const double rc = -double((n - 1 + m) * (n - 1 - m)) * ir2;
       const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
       J[hidx(n, m)] = m == 0 ? make_double2(fma(zc, b.x, rc * a.x), 0.0)
                              : make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
     }
   }
-  double sc[P1 + 1];  // r^{-(2n+1)}
-  sc[0] = rs;
-#pragma unroll
-  for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
   const double w = x.w;
 #pragma unroll
   for (int n = 0; n <= Q; ++n) {
-    const double wn = w * sc[n];
 #pragma unroll
     for (int m = 0; m <= n; ++m) {
       const int id = hidx(n, m);
-      ax[id] = fma(wn, J[id].x, ax[id]);
-      if (m > 0) ay[id] = fma(-wn, J[id].y, ay[id]);
+      ax[id] = fma(w, J[id].x, ax[id]);
+      if (m > 0) ay[id] = fma(-w, J[id].y, ay[id]);
     }
   }
   if (DIP) {
     // acc += conj(g), g = -mz I_{n+1}^m + (hx + i hy) I_{n+1}^{m-1} - (hx - i hy) I_{n+1}^{m+1}
+    const double mz = u.z * ir, hx = 0.5 * u.x * ir, hy = 0.5 * u.y * ir;
 #pragma unroll
     for (int n = 0; n <= Q; ++n) {
-      const double s1 = sc[n + 1] * ir;
-      const double mz = u.z * s1, hx = 0.5 * u.x * s1, hy = 0.5 * u.y * s1;
 #pragma unroll
       for (int m = 0; m <= n; ++m) {
         const int id = hidx(n, m);
@@ -390,51 +386,47 @@ __device__ __forceinline__ void near_pair_batch(const double4 x, const double* w
   const double r2 = ux * ux + uy * uy + uz * uz;
   const double rs = rsqrt(r2);
   const double ir2 = rs * rs;
+  const double vx = ux * ir2, vy = uy * ir2, vz = uz * ir2;  // I_n^m(u) directly, as near_pair
   double2 J[KI];
 #pragma unroll
   for (int m = 0; m <= P1; ++m) {
     if (m == 0) {
-      J[0] = make_double2(1.0, 0.0);
+      J[0] = make_double2(rs, 0.0);
     } else {
       const double2 d = J[hidx(m - 1, m - 1)];
       const double f = double(2 * m - 1);
-      J[hidx(m, m)] = m == 1 ? make_double2(ux, uy)
-                             : make_double2(f * (d.x * ux - d.y * uy), f * (d.x * uy + d.y * ux));
+      J[hidx(m, m)] = m == 1 ? make_double2(d.x * vx, d.x * vy)
+                             : make_double2(f * (d.x * vx - d.y * vy), f * (d.x * vy + d.y * vx));
     }
     if (m + 1 <= P1) {
-      const double f = double(2 * m + 1) * uz;
-      J[hidx(m + 1, m)] = m == 0 ? make_double2(uz, 0.0) : make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
+      const double f = double(2 * m + 1) * vz;
+      J[hidx(m + 1, m)] = m == 0 ? make_double2(vz * J[0].x, 0.0)
+                                 : make_double2(f * J[hidx(m, m)].x, f * J[hidx(m, m)].y);
     }
 #pragma unroll
     for (int n = m + 2; n <= P1; ++n) {
-      const double zc = double(2 * n - 1) * uz;
-      const double rc = -double((n - 1 + m) * (n - 1 - m)) * r2;
+      const double zc = double(2 * n - 1) * vz;
+      const double rc = -double((n - 1 + m) * (n - 1 - m)) * ir2;
       const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
       J[hidx(n, m)] = m == 0 ? make_double2(fma(zc, b.x, rc * a.x), 0.0)
                              : make_double2(fma(zc, b.x, rc * a.x), fma(zc, b.y, rc * a.y));
     }
   }
-  double sc[P1 + 1];
-  sc[0] = rs;
-#pragma unroll
-  for (int n = 1; n <= P1; ++n) sc[n] = sc[n - 1] * ir2;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
 #pragma unroll
     for (int n = 0; n <= Q; ++n) {
-      const double wn = w[r] * sc[n];
 #pragma unroll
       for (int m = 0; m <= n; ++m) {
         const int id = hidx(n, m);
-        ax[r][id] = fma(wn, J[id].x, ax[r][id]);
-        if (m > 0) ay[r][id] = fma(-wn, J[id].y, ay[r][id]);
+        ax[r][id] = fma(w[r], J[id].x, ax[r][id]);
+        if (m > 0) ay[r][id] = fma(-w[r], J[id].y, ay[r][id]);
       }
     }
     if (DIP) {
+      const double mz = u[r].z * ir, hx = 0.5 * u[r].x * ir, hy = 0.5 * u[r].y * ir;
 #pragma unroll
       for (int n = 0; n <= Q; ++n) {
-        const double s1 = sc[n + 1] * ir;
-        const double mz = u[r].z * s1, hx = 0.5 * u[r].x * s1, hy = 0.5 * u[r].y * s1;
 #pragma unroll
         for (int m = 0; m <= n; ++m) {
           const int id = hidx(n, m);

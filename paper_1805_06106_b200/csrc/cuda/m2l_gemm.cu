@@ -656,13 +656,38 @@ __global__ void __launch_bounds__(160) k_m2l_reduce_split(const int* __restrict_
     int n, m;
     q_nm(q, n, m);
     double sx = 0.0, sy = 0.0;
-    for (int64_t pos = a; pos < e; ++pos) {
+    const int qi = m > 0 ? NR + n * (n - 1) / 2 + m - 1 : q;
+    // kU entries' loads in flight per thread (the kernel is HBM-bound on the staging
+    // rows); the sums still run in CSR order
+    constexpr int kU = 4;
+    int64_t pos = a;
+    for (; pos + kU <= e; pos += kU) {
+      double re[kU], im[kU];
+      double2 r[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const double* row = temp + (pos + u - chunk_base) * KRp;
+        re[u] = __ldcs(row + q);
+        im[u] = m > 0 ? __ldcs(row + qi) : 0.0;
+        r[u] = m > 0 ? cs[size_t(__ldg(ent_op + pos + u)) * (p + 1) + m] : make_double2(1.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (m == 0) {
+          sx += re[u];
+        } else {
+          sx += re[u] * r[u].x + im[u] * r[u].y;
+          sy += im[u] * r[u].x - re[u] * r[u].y;
+        }
+      }
+    }
+    for (; pos < e; ++pos) {
       const double* row = temp + (pos - chunk_base) * KRp;
-      const double re = row[q];
+      const double re = __ldcs(row + q);
       if (m == 0) {
         sx += re;
       } else {
-        const double im = row[NR + n * (n - 1) / 2 + m - 1];
+        const double im = __ldcs(row + qi);
         const double2 r = cs[size_t(ent_op[pos]) * (p + 1) + m];
         sx += re * r.x + im * r.y;
         sy += im * r.x - re * r.y;

@@ -44,7 +44,6 @@ namespace dev {
 
 namespace {
 
-constexpr int kPasMaxS = 16;  // largest block: p + 1
 constexpr int kPasPhases = 3;
 constexpr int kWarps = 8, kBN = 32, kLD = kBN + 1;
 
@@ -196,6 +195,182 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
   }
 }
 
+// ------------------------------------------------- v2: persistent, operator in smem
+// One CTA per SM walks a contiguous run of the offset-sorted tiles.  The offset's
+// operator [W | Z | V] (96 KB at p = 15) is copied into shared memory once per run
+// of same-offset tiles (~460 tiles per offset at config 1) and read as DMMA A
+// fragments in fragment order (conflict-free); the next tile's multipoles are
+// loaded into registers while the current tile runs its three phases.  16 warps:
+// warp w owns the blocks of LPT list w % 8 for columns 16 (w / 8) .. + 15.
+//
+// The tile is 32 columns per row with the columns XOR-swizzled per row by
+// f(n + m) = 4 sigma + tau, sigma = (2, 1, 3, 0)[(n + m) & 3], tau = ((n + m) >> 2) & 3:
+//  - any 4 consecutive rows of a W/V block (consecutive m) or Z block (consecutive
+//    n) have distinct sigma: the B-fragment loads (4 rows x 4 columns per half warp)
+//    are conflict-free;
+//  - adjacent block rows differ in sigma's bit 1: the C-fragment stores (double2,
+//    2 rows x 8 columns per quarter warp) are conflict-free;
+//  - f is a bijection of (n + m) mod 16: the column passes (16 consecutive rows of one
+//    column per half warp) conflict only where a degree ends inside the 16 rows.
+constexpr int kWarps2 = 16;
+__host__ __device__ constexpr int pas2_f(int n, int m) {
+  return 4 * ((0x36 >> (2 * ((n + m) & 3))) & 3) + (((n + m) >> 2) & 3);
+}
+__host__ __device__ constexpr int pas2_code(int row, int n, int m) { return row * kBN | pas2_f(n, m); }
+
+template <int S>
+__device__ __forceinline__ void pas2_block(double* X, const int* rw, const double* Ob, int lane, int colbase) {
+  constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, NT = 2;
+  double a[MT][KS], b[KS][NT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + (lane & 3);
+    const int code = k < S ? rw[k] : 0, base = code & ~(kBN - 1), msk = code & (kBN - 1);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[base + ((colbase + nt * 8 + (lane >> 2)) ^ msk)] : 0.0;
+  }
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[ks][nt]);
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = mt * 8 + (lane >> 2);
+    if (r < S) {
+      const int code = rw[r], base = code & ~(kBN - 1), msk = code & (kBN - 1);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int pos = ((colbase + nt * 8 + (lane & 3) * 2) ^ msk) & ~1;
+        *reinterpret_cast<double2*>(X + base + pos) =
+            (msk & 1) ? make_double2(acc[mt][nt][1], acc[mt][nt][0]) : make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kWarps2 * 32, 1)
+    k_m2l_pas2(const int* __restrict__ tab, int tab_n, TabHead hd, int nblk, const double* __restrict__ ops,
+               int op_stride, int phase_size, const double2* __restrict__ cs_all, const int4* __restrict__ tiles,
+               int n_tiles, const int* __restrict__ col_src, const int* __restrict__ col_pos,
+               const double* __restrict__ M, int kp2, int KRp, double* __restrict__ temp) {
+  constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), NTH = kWarps2 * 32;
+  constexpr int NV = (NR * kBN + NTH - 1) / NTH;  // multipole coefficients prefetched per thread
+  extern __shared__ double smem[];
+  double* OPS = smem;
+  double* X = OPS + op_stride;
+  int* s_tab = reinterpret_cast<int*>(X + NROW * kBN);
+  __shared__ double2 s_cs[P + 1];
+  __shared__ int s_rc[NROW];  // row codes (row * 32 | swizzle) of the storage rows
+  __shared__ int s_qi[NR];    // m | Im storage row << 8 of half-table index q
+  __shared__ int s_pos[kBN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < tab_n; i += NTH) s_tab[i] = tab[i];
+  for (int q = tid; q < NR; q += NTH) {
+    int n = 0;
+    while (hidx(n + 1, 0) <= q) ++n;
+    const int m = q - hidx(n, 0), ri = m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0;
+    s_qi[q] = m | ri << 8;
+    s_rc[q] = pas2_code(q, n, m);
+    if (m > 0) s_rc[ri] = pas2_code(ri, n, m);
+  }
+  const int t0 = int(int64_t(blockIdx.x) * n_tiles / gridDim.x);
+  const int t1 = int(int64_t(blockIdx.x + 1) * n_tiles / gridDim.x);
+  double2 v[NV];
+  auto prefetch = [&](int t) {
+    const int4 tl = tiles[t];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int e = tid + u * NTH, c = e / NR, q = e - c * NR;
+      v[u] = make_double2(0.0, 0.0);
+      if (e < NR * kBN && c < tl.z)
+        v[u] = __ldg(reinterpret_cast<const double2*>(M + size_t(__ldg(col_src + tl.y + c)) * kp2) + q);
+    }
+  };
+  if (t0 < t1) prefetch(t0);
+  int cur = -1;
+#pragma unroll 1
+  for (int t = t0; t < t1; ++t) {
+    const int4 tile = tiles[t];
+    __syncthreads();  // the previous tile's write-out has read X
+    if (tile.x != cur) {
+      cur = tile.x;
+      const double2* src = reinterpret_cast<const double2*>(ops + size_t(cur) * op_stride);
+      for (int i = tid; i < op_stride / 2; i += NTH) reinterpret_cast<double2*>(OPS)[i] = __ldg(src + i);
+      if (tid <= P) s_cs[tid] = cs_all[size_t(cur) * (P + 1) + tid];
+      __syncthreads();
+    }
+    if (tid < kBN) s_pos[tid] = tid < tile.z ? col_pos[tile.y + tid] : -1;
+    // M' = M e^{i k alpha} into the tile
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int e = tid + u * NTH, c = e / NR, q = e - c * NR;
+      if (e < NR * kBN) {
+        const int qi = s_qi[q], m = qi & 255;
+        const double2 r = s_cs[m];
+        const int code = s_rc[q];
+        X[(code & ~(kBN - 1)) + (c ^ (code & (kBN - 1)))] = v[u].x * r.x - v[u].y * r.y;
+        if (m > 0) {
+          const int ci = s_rc[qi >> 8];
+          X[(ci & ~(kBN - 1)) + (c ^ (ci & (kBN - 1)))] = v[u].x * r.y + v[u].y * r.x;
+        }
+      }
+    }
+    __syncthreads();
+    if (t + 1 < t1) prefetch(t + 1);  // in flight during the phases
+    const int colbase = (warp >> 3) * 16, wq = warp & 7;
+#pragma unroll 1
+    for (int ph = 0; ph < kPasPhases; ++ph) {
+      const int* T = s_tab + hd.base[ph];
+      const int* rowoff = T;
+      const int* opoff = T + nblk + 1;
+      const int* rows = opoff + nblk;
+      const int* woff = rows + NROW;
+      const int* wblk = woff + kWarps + 1;
+      const double* Op = OPS + size_t(ph) * phase_size;
+#pragma unroll 1
+      for (int i = woff[wq]; i < woff[wq + 1]; ++i) {
+        const int b = wblk[i];
+        const int* rw = rows + rowoff[b];
+        const double* Ob = Op + opoff[b];
+        switch (rowoff[b + 1] - rowoff[b]) {
+#define QBXG_PAS2_CASE(S) \
+  case S:                 \
+    pas2_block<S>(X, rw, Ob, lane, colbase); \
+    break;
+          QBXG_PAS2_CASE(1) QBXG_PAS2_CASE(2) QBXG_PAS2_CASE(3) QBXG_PAS2_CASE(4) QBXG_PAS2_CASE(5)
+          QBXG_PAS2_CASE(6) QBXG_PAS2_CASE(7) QBXG_PAS2_CASE(8) QBXG_PAS2_CASE(9) QBXG_PAS2_CASE(10)
+          QBXG_PAS2_CASE(11) QBXG_PAS2_CASE(12) QBXG_PAS2_CASE(13) QBXG_PAS2_CASE(14) QBXG_PAS2_CASE(15)
+          QBXG_PAS2_CASE(16)
+#undef QBXG_PAS2_CASE
+          default: break;
+        }
+      }
+      __syncthreads();
+    }
+    // staging rows (Re, then compacted Im): consecutive lanes walk one column's rows
+    for (int e = tid; e < NROW * kBN; e += NTH) {
+      const int c = e / NROW, r = e - c * NROW, pos = s_pos[c];
+      if (pos >= 0) {
+        const int code = s_rc[r];
+        temp[size_t(pos) * KRp + r] = X[(code & ~(kBN - 1)) + (c ^ (code & (kBN - 1)))];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 struct PasLayout {
   int nblk = 0, phase_size = 0;
@@ -203,11 +378,15 @@ struct PasLayout {
   TabHead hd{};
 };
 
-// blocks of one phase: row index sets (Re rows hidx(n, m); Im rows NR + n(n-1)/2 + m - 1)
-void phase_blocks(int p, int ph, std::vector<std::vector<int>>& blocks) {
+// blocks of one phase: storage rows (Re rows hidx(n, m); Im rows NR + n(n-1)/2 + m - 1),
+// as row indices (v1) or as row codes with the v2 swizzle
+void phase_blocks(int p, int ph, bool v2, std::vector<std::vector<int>>& blocks) {
   const int NR = hsize(p);
-  auto re = [&](int n, int m) { return hidx(n, m); };
-  auto im = [&](int n, int m) { return NR + n * (n - 1) / 2 + m - 1; };
+  auto re = [&](int n, int m) { return v2 ? pas2_code(hidx(n, m), n, m) : hidx(n, m); };
+  auto im = [&](int n, int m) {
+    const int r = NR + n * (n - 1) / 2 + m - 1;
+    return v2 ? pas2_code(r, n, m) : r;
+  };
   blocks.clear();
   for (int part = 0; part < 2; ++part)
     for (int a = part; a <= p; ++a) {
@@ -220,11 +399,11 @@ void phase_blocks(int p, int ph, std::vector<std::vector<int>>& blocks) {
     }
 }
 
-PasLayout make_layout(int p) {
+PasLayout make_layout(int p, bool v2) {
   PasLayout L;
   for (int ph = 0; ph < kPasPhases; ++ph) {
     std::vector<std::vector<int>> blocks;
-    phase_blocks(p, ph, blocks);
+    phase_blocks(p, ph, v2, blocks);
     L.nblk = int(blocks.size());
     L.hd.base[ph] = int(L.tab.size());
     std::vector<int> rowoff{0}, opoff, rows;
@@ -258,8 +437,43 @@ PasLayout make_layout(int p) {
   return L;
 }
 
+// v1 (one tile per CTA, 3 CTAs per SM, operators read from L2) is the default: the
+// persistent v2 (QBXG_PAS_V2=1, 1 CTA of 16 warps per SM, operator in shared memory)
+// is parity-green but slower at config 1 (64.2 vs 45.8 ms for the M2L stage): with one
+// CTA per SM nothing fills the phase barriers and the staging stores.
+bool pas_v2() {
+  static const bool v2 = std::getenv("QBXG_PAS_V2") != nullptr;
+  return v2;
+}
+
+template <int P>
+int pas2_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
+  constexpr int NROW = (P + 1) * (P + 1);
+  const size_t smem = size_t(Pl.pas_stride + NROW * kBN) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
+  static size_t attr = 0;
+  static int n_sm = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_m2l_pas2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+      return -1;
+    attr = smem;
+  }
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  TabHead hd;
+  for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
+  const int grid = std::max(1, std::min(C.n_tiles, n_sm));
+  k_m2l_pas2<P><<<grid, kWarps2 * 32, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops, Pl.pas_stride,
+                                                 Pl.pas_phase, Pl.cs, C.tiles, C.n_tiles, C.col_src, C.col_pos, X,
+                                                 kp2, Pl.KRp, Pl.temp);
+  return 1;
+}
+
 template <int P>
 int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
+  if (pas_v2()) return pas2_launch_p<P>(Pl, C, X, kp2, s);
   constexpr int NROW = (P + 1) * (P + 1);
   const size_t smem = size_t(NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
   static size_t attr = 0;
@@ -281,11 +495,14 @@ int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2,
 bool pas_supported(int p) { return p >= 4 && p <= 15; }
 int pas_tile_cols() { return kBN; }
 
-// Per-offset operators: [W | Z | V], blocks in phase_blocks order, each row-major
-// with rows padded to 8 and columns to 4 (zeros): DMMA A fragments without guards.
+// Per-offset operators: [W | Z | V], blocks in phase_blocks order, each with rows
+// padded to 8 and columns to 4 (zeros): DMMA A fragments without guards.  v1: each
+// block row-major; v2: each block in fragment order (8x4 fragment (mt, ks) as 32
+// consecutive doubles, lane l holding element (mt*8 + l/4, ks*4 + l%4)).
 void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& ops, int& op_stride,
                    std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]) {
-  const PasLayout L = make_layout(p);
+  const bool v2 = pas_v2();
+  const PasLayout L = make_layout(p, v2);
   nblk = L.nblk;
   phase_size = L.phase_size;
   op_stride = kPasPhases * L.phase_size;
@@ -345,6 +562,32 @@ void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& 
       }
   }
   if (worst > 1e-12) throw std::runtime_error("pas_build_ops: rotation blocks mix Re and Im at phi = 0");
+  if (!v2) return;
+  // row-major blocks -> fragment order, block by block (W and V share sizes, Z its own)
+  std::vector<int> wsz, zsz;
+  for (int part = 0; part < 2; ++part)
+    for (int a = part; a <= p; ++a) {
+      wsz.push_back(a + 1 - part);
+      zsz.push_back(p - a + 1);
+    }
+#pragma omp parallel for schedule(static)
+  for (int o = 0; o < n_ops; ++o) {
+    std::vector<double> tmp(size_t(L.phase_size));
+    for (int ph = 0; ph < kPasPhases; ++ph) {
+      double* A = &ops[size_t(o) * op_stride + size_t(ph) * L.phase_size];
+      const std::vector<int>& sz = ph == 1 ? zsz : wsz;
+      size_t off = 0;
+      for (int s : sz) {
+        const int MT = (s + 7) / 8, KS = (s + 3) / 4, sp = KS * 4;
+        for (int mt = 0; mt < MT; ++mt)
+          for (int ks = 0; ks < KS; ++ks)
+            for (int l = 0; l < 32; ++l)
+              tmp[off + size_t(mt * KS + ks) * 32 + l] = A[off + size_t(mt * 8 + l / 4) * sp + ks * 4 + l % 4];
+        off += size_t(MT) * 8 * sp;
+      }
+      std::copy(tmp.begin(), tmp.end(), A);
+    }
+  }
 }
 
 int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s) {
