@@ -279,8 +279,8 @@ int qbxg_exchange_local(qbxg_handle** handles, int32_t n_ranks);
 int qbxg_nccl_unique_id(uint8_t* out128);
 int qbxg_nccl_attach(qbxg_handle* h, const uint8_t* id128);
 
-/* Stream overlap (default on; QBXG_OVERLAP=0 in the environment turns the default
- * off): the near field runs on a second stream beside the far-field chain (M2L,
+/* Stream overlap (default off; QBXG_OVERLAP=1 or 2 in the environment turns the
+ * default on): the near field runs on a second stream beside the far-field chain (M2L,
  * P2L, L2L) and is joined before the first stage that adds into the centre
  * locals.  Results are bitwise identical either way; per-stage timings of an
  * overlapped apply include the contention between the two streams. */

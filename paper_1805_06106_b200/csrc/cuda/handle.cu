@@ -72,6 +72,7 @@ struct Handle {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t evx[4] = {};       // near begin/end (side stream), P2L end, L2L end
   bool overlap = false, timed_overlap = false;
+  bool overlap_late = false;  // QBXG_OVERLAP=2: fork the near field after the M2L launch
   cudaEvent_t ev[QBXG_NUM_TIMERS + 2] = {};
   qbxg_config cfg{};
   int64_t ns = 0, nc = 0, nt = 0, nconv = 0;
@@ -772,7 +773,13 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   QCK(cudaStreamCreateWithFlags(&H.stream, cudaStreamNonBlocking));
   for (auto& e : H.ev) QCK(cudaEventCreate(&e));
   for (auto& e : H.evx) QCK(cudaEventCreate(&e));
-  H.overlap = !(std::getenv("QBXG_OVERLAP") && std::getenv("QBXG_OVERLAP")[0] == '0');
+  // off by default: the near field and the M2L both live on the fp64 pipe, and since
+  // the near field launches heaviest boxes first the overlapped apply measured no
+  // faster than the sequential one (107.4 vs 106.4 ms at config 1); QBXG_OVERLAP=1
+  // forks it after the gather, QBXG_OVERLAP=2 after the M2L launch
+  H.overlap = std::getenv("QBXG_OVERLAP") && (std::getenv("QBXG_OVERLAP")[0] == '1' ||
+                                              std::getenv("QBXG_OVERLAP")[0] == '2');
+  H.overlap_late = std::getenv("QBXG_OVERLAP") && std::getenv("QBXG_OVERLAP")[0] == '2';
   QCK(cudaStreamCreateWithFlags(&H.side, cudaStreamNonBlocking));
   QCK(cudaEventCreateWithFlags(&H.fork_ev, cudaEventDisableTiming));
   QCK(cudaEventCreateWithFlags(&H.join_ev, cudaEventDisableTiming));
@@ -1195,7 +1202,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   if (phase & 1) {
   QCK(cudaEventRecord(ev[0], s));
   chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
-  if (H.overlap && !near_done && phase == 3) {  // near field needs only the gathered sources:
+  if (H.overlap && !H.overlap_late && !near_done && phase == 3) {  // near field needs only the gathered sources:
     QCK(cudaEventRecord(H.fork_ev, s));        // run it beside the whole far-field chain
     QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
     QCK(cudaEventRecord(H.evx[0], H.side));
@@ -1230,7 +1237,17 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   // the far-field chain (M2L, P2L, L2L touch only box expansions) and is joined before
   // W far, the first stage that accumulates into the centre locals.
   const bool ovl = H.overlap && !near_done;
-  if (ovl && !near_forked) {
+  auto fork_near = [&] {
+    QCK(cudaEventRecord(H.fork_ev, s));
+    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
+    QCK(cudaEventRecord(H.evx[0], H.side));
+    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
+    QCK(cudaEventRecord(H.evx[1], H.side));
+    QCK(cudaEventRecord(H.join_ev, H.side));
+  };
+  if (ovl && !near_forked && H.overlap_late) {
+    // forked right after the M2L launch below
+  } else if (ovl && !near_forked) {
     QCK(cudaEventRecord(H.fork_ev, s));
     QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
     QCK(cudaEventRecord(H.evx[0], H.side));
@@ -1246,6 +1263,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     chk(dev::launch_m2l(D, H.d_v_boxes, H.n_v_boxes, s));
   else
     chk(dev::launch_m2l_dense(H.m2l, D, s));
+  if (ovl && !near_forked && H.overlap_late) fork_near();
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));

@@ -57,7 +57,8 @@ VARIANTS = [
     {"QBXG_CTR_MODE": "2"},
     {"QBXG_M2L_NAIVE": "1"},
     {"QBXG_M2L_CHUNK_ENTRIES": "5000"},
-    {"QBXG_OVERLAP": "0"},
+    {"QBXG_OVERLAP": "1"},
+    {"QBXG_OVERLAP": "2"},
 ]
 
 HELM_SCRIPT = r"""

@@ -1,5 +1,6 @@
 """Per-stage CUDA-event times of a device-resident apply (near field on the main
-stream), for A/B runs of kernel variants selected by QBXG_* environment switches.
+stream unless QBXG_OVERLAP is set), for A/B runs of kernel variants selected by
+QBXG_* environment switches.
 
     QBXG_PAS_MAP=0 python tools/stage_times.py [config] [n_applies]
 """
@@ -21,7 +22,7 @@ def main():
     g = api.config_geometry(cfg_id)
     cfg = api.config_fmm(cfg_id)
     eng = api.FmmEngine(cfg, g)
-    eng.set_overlap(False)
+    eng.set_overlap(os.environ.get("QBXG_OVERLAP", "0") != "0")
     w = torch.from_numpy(g.weights()).cuda()
     mu = torch.from_numpy(np.ascontiguousarray(g.dipoles())).cuda() if cfg.kernel == 1 else None
     pot = torch.empty(g.n_targets, dtype=torch.float64, device="cuda")
