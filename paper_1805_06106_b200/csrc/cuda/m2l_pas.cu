@@ -46,6 +46,19 @@ namespace {
 
 constexpr int kPasPhases = 3;
 constexpr int kWarps = 8, kBN = 32, kLD = kBN + 1;
+constexpr int kWarps2 = 16;
+__host__ __device__ constexpr int pas2_f(int n, int m) {
+  return 4 * ((0x36 >> (2 * ((n + m) & 3))) & 3) + (((n + m) >> 2) & 3);
+}
+__host__ __device__ constexpr int pas2_code(int row, int n, int m) { return row * kBN | pas2_f(n, m); }
+
+// shared-memory address of (row, column): plain rows of kLD doubles (row codes are row
+// indices) or swizzled rows of 32 (row codes from pas2_code)
+template <bool SWZ>
+__device__ __forceinline__ int xa(int code, int c) {
+  return SWZ ? (code & ~(kBN - 1)) + (c ^ (code & (kBN - 1))) : code * kLD + c;
+}
+
 
 // table layout (ints), per phase: [nblk+1 row offsets][nblk op offsets]
 // [(p+1)^2 rows][kWarps+1 warp offsets][block ids]
@@ -63,7 +76,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // operator (rows padded to 8, columns to 4, zeros) as A fragments from L2, the
 // block's rows x 32 columns as B fragments from shared memory -- all read before
 // any row is written, so the warp may overwrite its own block.
-template <int S>
+template <int S, bool SWZ>
 __device__ __forceinline__ void pas_block(double* X, const int* rw, const double* __restrict__ Ob, int lane) {
   constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, K4 = 4 * KS, NT = kBN / 8;
   double a[MT][KS], b[KS][NT];
@@ -76,7 +89,7 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
     const int k = ks * 4 + (lane & 3);
     const int row = k < S ? rw[k] : 0;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[row * kLD + nt * 8 + (lane >> 2)] : 0.0;
+    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[xa<SWZ>(row, nt * 8 + (lane >> 2))] : 0.0;
   }
   double acc[MT][NT][2];
 #pragma unroll
@@ -97,14 +110,21 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
       const int row = rw[r];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        X[row * kLD + nt * 8 + (lane & 3) * 2] = acc[mt][nt][0];
-        X[row * kLD + nt * 8 + (lane & 3) * 2 + 1] = acc[mt][nt][1];
+        if (SWZ) {  // the swizzle keeps column pairs (2t, 2t+1) adjacent, possibly swapped
+          const int msk = row & (kBN - 1);
+          const int pos = (row & ~(kBN - 1)) + (((nt * 8 + (lane & 3) * 2) ^ msk) & ~1);
+          *reinterpret_cast<double2*>(X + pos) = (msk & 1) ? make_double2(acc[mt][nt][1], acc[mt][nt][0])
+                                                           : make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        } else {
+          X[row * kLD + nt * 8 + (lane & 3) * 2] = acc[mt][nt][0];
+          X[row * kLD + nt * 8 + (lane & 3) * 2 + 1] = acc[mt][nt][1];
+        }
       }
     }
   }
 }
 
-template <int P>
+template <int P, bool SWZ>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restrict__ tab, int tab_n, TabHead hd,
                                                            int nblk, const double* __restrict__ ops, int op_stride,
                                                            int phase_size, const double2* __restrict__ cs_all,
@@ -116,20 +136,27 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
   constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), NTH = kWarps * 32;
   extern __shared__ double smem[];
   double* X = smem;
-  int* s_tab = reinterpret_cast<int*>(X + NROW * kLD);
+  int* s_tab = reinterpret_cast<int*>(X + NROW * (SWZ ? kBN : kLD));
   __shared__ int s_src[kBN];
   __shared__ double2 s_cs[P + 1];
-  __shared__ int s_code[NR];  // Re row | Im row << 10 (0 for m = 0) | m << 20 of half-table index q
+  // half-table index q: Re row | Im row << 10 (0 for m = 0) | m << 20 | swizzle << 25
+  __shared__ int s_code[NR];
+  __shared__ int s_rc[NROW];  // row code of each storage row (xa)
+  __shared__ int s_pos[kBN];
   const int4 tile = tiles[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < tab_n; i += NTH) s_tab[i] = tab[i];
   if (tid < kBN) s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+  if (tid < kBN) s_pos[tid] = tid < tile.z ? col_pos[tile.y + tid] : -1;
   if (tid <= P) s_cs[tid] = cs_all[size_t(tile.x) * (P + 1) + tid];
   for (int q = tid; q < NR; q += NTH) {
     int n = 0;
     while (hidx(n + 1, 0) <= q) ++n;
     const int m = q - hidx(n, 0);
-    s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0) << 10 | m << 20;
+    const int ri = m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0;
+    s_code[q] = q | ri << 10 | m << 20 | (SWZ ? pas2_f(n, m) : 0) << 25;
+    s_rc[q] = SWZ ? pas2_code(q, n, m) : q;
+    if (m > 0) s_rc[ri] = SWZ ? pas2_code(ri, n, m) : ri;
   }
   __syncthreads();
   // gather M' = M e^{i k alpha}, coalesced along each multipole, kSt loads in flight per thread
@@ -152,9 +179,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
       if (e < NR * kBN) {
         const int c = e / NR, q = e - c * NR;
         const int code = s_code[q], ri = (code >> 10) & 1023;
-        const double2 r = s_cs[code >> 20];
-        X[(code & 1023) * kLD + c] = v[u].x * r.x - v[u].y * r.y;
-        if (ri) X[ri * kLD + c] = v[u].x * r.y + v[u].y * r.x;
+        const double2 r = s_cs[(code >> 20) & 31];
+        const int cs = SWZ ? c ^ (code >> 25) : c, ld = SWZ ? kBN : kLD;
+        X[(code & 1023) * ld + cs] = v[u].x * r.x - v[u].y * r.y;
+        if (ri) X[ri * ld + cs] = v[u].x * r.y + v[u].y * r.x;
       }
     }
   }
@@ -177,7 +205,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
       switch (rowoff[b + 1] - rowoff[b]) {
 #define QBXG_PAS_CASE(S) \
   case S:                \
-    pas_block<S>(X, rw, Ob, lane); \
+    pas_block<S, SWZ>(X, rw, Ob, lane); \
     break;
         QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
         QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11) QBXG_PAS_CASE(12)
@@ -189,9 +217,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
     __syncthreads();
   }
   // staging row = Re (NR) then compacted Im, coalesced along each row
-  for (int e = tid; e < NROW * kBN; e += NTH) {
-    const int c = e / NROW, r = e - c * NROW;
-    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KRp + r] = X[r * kLD + c];
+  // (row-outer: one row code per thread and row; consecutive lanes, consecutive rows)
+  for (int r = tid; r < NROW; r += NTH) {
+    const int code = s_rc[r];
+    for (int c = 0; c < tile.z; ++c) temp[size_t(s_pos[c]) * KRp + r] = X[xa<SWZ>(code, c)];
   }
 }
 
@@ -212,12 +241,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_m2l_pas(const int* __restric
 //    2 rows x 8 columns per quarter warp) are conflict-free;
 //  - f is a bijection of (n + m) mod 16: the column passes (16 consecutive rows of one
 //    column per half warp) conflict only where a degree ends inside the 16 rows.
-constexpr int kWarps2 = 16;
-__host__ __device__ constexpr int pas2_f(int n, int m) {
-  return 4 * ((0x36 >> (2 * ((n + m) & 3))) & 3) + (((n + m) >> 2) & 3);
-}
-__host__ __device__ constexpr int pas2_code(int row, int n, int m) { return row * kBN | pas2_f(n, m); }
-
 template <int S>
 __device__ __forceinline__ void pas2_block(double* X, const int* rw, const double* Ob, int lane, int colbase) {
   constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, NT = 2;
@@ -445,6 +468,14 @@ bool pas_v2() {
   static const bool v2 = std::getenv("QBXG_PAS_V2") != nullptr;
   return v2;
 }
+// v1 tile layout: padded rows of 33 (default) or swizzled rows of 32 (QBXG_PAS_SWZ=1).
+// The swizzle removes the B-load / C-store bank conflicts (shared wavefronts 4.7G ->
+// 3.3G per chunk-1 launch) but its per-access XOR addressing costs 36% more issued
+// instructions, and the kernel is latency/issue-limited: 32.4 vs 25.7 ms (ncu).
+bool pas_swz() {
+  static const bool on = std::getenv("QBXG_PAS_SWZ") && std::getenv("QBXG_PAS_SWZ")[0] == '1';
+  return on;
+}
 
 template <int P>
 int pas2_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
@@ -471,20 +502,28 @@ int pas2_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2
   return 1;
 }
 
+template <int P, bool SWZ>
+int pas1_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s);
+
 template <int P>
 int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
   if (pas_v2()) return pas2_launch_p<P>(Pl, C, X, kp2, s);
+  return pas_swz() ? pas1_launch_p<P, true>(Pl, C, X, kp2, s) : pas1_launch_p<P, false>(Pl, C, X, kp2, s);
+}
+
+template <int P, bool SWZ>
+int pas1_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
   constexpr int NROW = (P + 1) * (P + 1);
-  const size_t smem = size_t(NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
+  const size_t smem = size_t(NROW * (SWZ ? kBN : kLD)) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
   static size_t attr = 0;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(k_m2l_pas<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_m2l_pas<P, SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
       return -1;
     attr = smem;
   }
   TabHead hd;
   for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
-  k_m2l_pas<P><<<C.n_tiles, kWarps * 32, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops,
+  k_m2l_pas<P, SWZ><<<C.n_tiles, kWarps * 32, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops,
                                                     Pl.pas_stride, Pl.pas_phase, Pl.cs, C.tiles, C.col_src,
                                                     C.col_pos, X, kp2, Pl.KRp, Pl.temp);
   return 1;
@@ -502,7 +541,7 @@ int pas_tile_cols() { return kBN; }
 void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& ops, int& op_stride,
                    std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]) {
   const bool v2 = pas_v2();
-  const PasLayout L = make_layout(p, v2);
+  const PasLayout L = make_layout(p, v2 || pas_swz());
   nblk = L.nblk;
   phase_size = L.phase_size;
   op_stride = kPasPhases * L.phase_size;
