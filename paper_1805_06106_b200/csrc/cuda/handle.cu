@@ -375,7 +375,8 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
   } else if (P.split) {
     const int NH = dev::split_nh(p);
-    P.sops = dalloc<double>(O, size_t(P.n_ops) * (NH + dev::split_nhi(p, NH)) * NH);
+    // the two dense blocks (400 MB at config 1) only when the split kernel runs
+    if (!P.pas) P.sops = dalloc<double>(O, size_t(P.n_ops) * (NH + dev::split_nhi(p, NH)) * NH);
     P.cs = dalloc<double2>(O, size_t(P.n_ops) * (p + 1));
     {
       std::vector<int> eo(nent);

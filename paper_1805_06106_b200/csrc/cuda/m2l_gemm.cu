@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(256) k_m2l_ops_split(int p, int NH, int NHI, c
     cs[size_t(o) * (p + 1) + threadIdx.x] = make_double2(cn, sn);
   }
   __syncthreads();
+  if (ops == nullptr) return;  // point-and-shoot needs only the (cos, sin) table
   double* T = ops + size_t(o) * (NH + NHI) * NH;
   for (int idx = threadIdx.x; idx < (NH + NHI) * NH; idx += blockDim.x) {
     const int ro = idx / NH, qi = idx % NH;
