@@ -1076,6 +1076,14 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       flush();
       H.wpairs.temp = dalloc<double2>(O, size_t(std::max<int64_t>(max_chunk, 1)) * D.kq);
     }
+    {
+      // P2L launch order: decreasing X_far source count (one CTA per box, so the order
+      // changes no result; no tail of heavy boxes)
+      std::vector<int64_t> cost(nb, 0);
+      for (int b : xb)
+        for (int64_t i = xs[b]; i < xs[b + 1]; ++i) cost[b] += xseg[i].y;
+      std::stable_sort(xb.begin(), xb.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    }
     H.d_xfar_boxes = dupload(O, xb, s);
     H.n_xfar_boxes = int(xb.size());
     for (int l = 0; l < H.nlev; ++l) {

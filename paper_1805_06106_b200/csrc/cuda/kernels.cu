@@ -285,7 +285,7 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
 // up to ~all 128 lanes are busy; the slices are then summed through shared
 // memory in slice order (deterministic) instead of by width-S shuffles.
 template <int Q, bool DIP, int U, bool GEN>
-__global__ void __launch_bounds__(kNearThreads) k_near_qbx(DevData D, const int* __restrict__ boxes) {
+__global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevData D, const int* __restrict__ boxes) {
   constexpr int KQ = hsize(Q);
   extern __shared__ double s_part[];  // GEN: 2 KQ x kNearThreads partial sums
   __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
@@ -864,7 +864,7 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 template <int P, bool DIP>
-__global__ void __launch_bounds__(128) k_p2l3(DevData D, const int* __restrict__ boxes) {
+__global__ void __launch_bounds__(128, P >= 12 ? 4 : 1) k_p2l3(DevData D, const int* __restrict__ boxes) {
   static_assert(P <= 15, "two columns per lane, 8 lanes");
   constexpr int NS = kP3Slices;
   constexpr int KP = hsize(P);
