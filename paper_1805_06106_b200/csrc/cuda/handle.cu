@@ -24,6 +24,7 @@
 #include "../host/common.hpp"
 #include "harmonics.cuh"
 #include "helm.cuh"
+#include "../host/helm_rot.hpp"
 #include "kernels.cuh"
 #include "../host/rotation.hpp"
 
@@ -151,6 +152,14 @@ struct Handle {
   double2* h_cs = nullptr;                     // per operator e^{i m alpha}, m <= p (split form)
   int* h_ent_op = nullptr;                     // operator of every List-2 CSR entry (split form)
   bool h_split = true;                         // QBXG_HELM_M2L=full keeps the full operators
+  // point-and-shoot M2L (default for p <= 20; QBXG_HELM_M2L=split or full opts out)
+  bool h_pas = false;
+  double* h_zops = nullptr;   // per operator: Z blocks (fragment order)
+  double* h_wvops = nullptr;  // per polar-angle class: W and V blocks
+  int* h_op_cls = nullptr;    // operator -> polar-angle class
+  int* h_pas_tab = nullptr;
+  int h_pas_tab_n = 0, h_zstride = 0, h_wvstride = 0;
+  int h_pas_base[2][3] = {};
   struct HelmM2LChunk {
     int n_tiles = 0;
     int4* tiles = nullptr;
@@ -546,16 +555,57 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
         }
         op_of_entry[e] = op;
       }
-    H.h_split = !(std::getenv("QBXG_HELM_M2L") && std::string(std::getenv("QBXG_HELM_M2L")) == "full");
-    const size_t per_op = H.h_split ? dev::helm_split_op_size(p) : opsz;
+    const char* hm = std::getenv("QBXG_HELM_M2L");
+    H.h_split = !(hm && std::string(hm) == "full");
+    H.h_pas = H.h_split && !hm && dev::helm_pas_supported(p);
+    const size_t per_op = H.h_pas ? 0 : H.h_split ? dev::helm_split_op_size(p) : opsz;
     const size_t bytes = msh.size() * per_op * sizeof(double2);
     size_t free_b = 0, total_b = 0;
     QCK(cudaMemGetInfo(&free_b, &total_b));
     if (bytes > size_t(double(free_b) * 0.7))
       throw InvalidArgument("qbxg_create: Helmholtz M2L operators (" + std::to_string(bytes >> 20) +
                             " MiB) exceed device memory");
-    H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * per_op);
-    if (H.h_split) {
+    if (!H.h_pas) H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * per_op);
+    if (H.h_pas) {
+      // W, V per polar angle of the integer offset (level independent), Z per (level, offset)
+      const HpasLayout PL = hpas_layout(p);
+      std::vector<int> cls(msh.size()), key_cls;
+      std::vector<double> thetas;
+      {
+        std::vector<int> key_to_cls(51 * 11, -1);
+        for (int l = 0; l < H.nlev; ++l)
+          for (int sl = 0; sl < 1331; ++sl) {
+            const int op = key_to_op[size_t(l) * 1331 + sl];
+            if (op < 0) continue;
+            const int dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
+            int& c = key_to_cls[size_t(dx * dx + dy * dy) * 11 + (dz + 5)];
+            if (c < 0) {
+              c = int(thetas.size());
+              thetas.push_back(std::atan2(std::sqrt(double(dx * dx + dy * dy)), double(dz)));
+            }
+            cls[op] = c;
+          }
+      }
+      std::vector<double> wv;
+      hpas_build_wv(p, thetas, wv);
+      H.h_wvops = dupload(O, wv, s);
+      H.h_op_cls = dupload(O, cls, s);
+      H.h_wvstride = int(PL.wv_stride);
+      H.h_zstride = int(PL.z_stride);
+      H.h_zops = dalloc<double>(O, std::max<size_t>(msh.size(), 1) * PL.z_stride);
+      H.h_cs = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * (p + 1));
+      for (auto& v : msh) v.w = 0.0;
+      std::vector<int> zoff(PL.z_off.begin(), PL.z_off.end());
+      if (!msh.empty())
+        dev::helm_build_zpas(HD, int(msh.size()), dupload(O, msh, s), zoff.data(), H.h_zstride, H.h_zops, H.h_cs, s);
+      std::vector<int> tab;
+      dev::helm_pas_tables(p, PL.wv_off[0][0].data(), PL.wv_off[0][1].data(), PL.wv_off[1][0].data(),
+                           PL.wv_off[1][1].data(), PL.z_off.data(), tab, H.h_pas_base);
+      H.h_pas_tab = dupload(O, tab, s);
+      H.h_pas_tab_n = int(tab.size());
+      H.h_ent_op = dupload(O, op_of_entry, s);
+      QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
+    } else if (H.h_split) {
       for (auto& v : msh) v.w = 0.0;  // the split builder takes the plain offset vector
       H.h_cs = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * (p + 1));
       if (!msh.empty()) dev::helm_build_split(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, H.h_cs, s);
@@ -711,7 +761,11 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
   for (const auto& C : H.h_m2l) {
-    if (H.h_split)
+    if (H.h_pas)
+      chk(dev::helm_m2l_pas(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_pas_tab, H.h_pas_tab_n, H.h_pas_base,
+                            H.h_zops, H.h_zstride, H.h_wvops, H.h_wvstride, H.h_op_cls, H.h_cs, H.h_temp, C.n_boxes,
+                            C.boxes, C.base, H.h_ent_op, s));
+    else if (H.h_split)
       chk(dev::helm_m2l_split(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_cs, H.h_temp,
                               C.n_boxes, C.boxes, C.base, H.h_ent_op, s));
     else

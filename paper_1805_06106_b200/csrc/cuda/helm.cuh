@@ -1,6 +1,8 @@
 // Helmholtz single-layer FMM (helm_fmm.cu): device data and launchers.
 #pragma once
 
+#include <vector>
+
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -60,6 +62,17 @@ int helm_build_split(const HelmData& H, int n_ops, const double4* shifts, double
 int helm_m2l_split(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
                    const double2* ops, const double2* cs, double2* temp, int n_boxes, const int* boxes, int64_t base,
                    const int* ent_op, cudaStream_t s);
+// point-and-shoot M2L (even / odd split frame): Z blocks + e^{i m alpha} per operator,
+// block tables, apply (pas kernel + the split reduce)
+bool helm_pas_supported(int P);
+int helm_build_zpas(const HelmData& H, int n_ops, const double4* shifts, const int* z_off, int zstride, double* zops,
+                    double2* cs, cudaStream_t s);
+void helm_pas_tables(int P, const size_t* wv_off_w0, const size_t* wv_off_w1, const size_t* wv_off_v0,
+                     const size_t* wv_off_v1, const size_t* z_off, std::vector<int>& tab, int (&base)[2][3]);
+int helm_m2l_pas(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+                 const int* tab, int tab_n, const int (&base)[2][3], const double* zops, int zstride,
+                 const double* wvops, int wvstride, const int* op_cls, const double2* cs, double2* temp, int n_boxes,
+                 const int* boxes, int64_t vbase, const int* ent_op, cudaStream_t s);
 int helm_near(const HelmData& H, const int* boxes, int n, cudaStream_t s);
 int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s);
 int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s);

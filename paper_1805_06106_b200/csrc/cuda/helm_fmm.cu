@@ -15,7 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "helm.cuh"
 #include "helm_math.cuh"
@@ -894,6 +896,207 @@ void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   k_h_near<Q><<<n, 128, smem, s>>>(H, boxes);
 }
 
+
+// ---------------------------------------------------------------- point-and-shoot M2L
+// (default for P <= 20; QBXG_HELM_M2L=split keeps the even / odd dense blocks)
+// In the split M2L's azimuthal frame the operator of offset v' = (rho, 0, z) factors as
+// V(theta) Z(|v'|) W(theta): W rotates the multipole so v' lies on +z, Z translates along
+// z (diagonal in m, one complex (P+1-m)^2 block per m, the same for the even and odd
+// parts), V rotates the local back (csrc/host/helm_rot.cpp).  All three keep the even /
+// odd split (A = y_m + y_-m, B = y_m - y_-m), so one CTA takes one parity of a tile of
+// kHColsS entries: (2 x 231 or 2 x 210 real rows) x 16 columns in shared memory, and each
+// phase runs its blocks in place as m8n8k4 DMMAs (W, V real, applied to the Re and Im
+// rows separately; Z as the real embedding [[Re, -Im], [Im, Re]]).  Output rows are the
+// split M2L's staging rows, so k_h_m2l_reduce_split finishes the job.  Per List-2 entry at
+// p = 20: 4 x (3,311 + 2,870) real multiply-adds instead of 4 x (231^2 + 210^2).
+constexpr int kHpW = 8, kHpLD = kHColsS + 1;
+
+__device__ __forceinline__ void hp_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// one block of runtime size S <= 48 in place: operator A-fragments (ks, mt) from L2
+// (one k-step ahead), rows rw[] x 16 columns from shared memory
+__device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const double* __restrict__ Ob, int lane) {
+  const int MT = (S + 7) >> 3, KS = (S + 3) >> 2;
+  double acc[6][2][2];
+#pragma unroll
+  for (int mt = 0; mt < 6; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+  double an[6];
+#pragma unroll
+  for (int mt = 0; mt < 6; ++mt) an[mt] = mt < MT ? __ldg(Ob + mt * 32 + lane) : 0.0;
+  for (int ks = 0; ks < KS; ++ks) {
+    double a[6];
+#pragma unroll
+    for (int mt = 0; mt < 6; ++mt) a[mt] = an[mt];
+    if (ks + 1 < KS) {
+#pragma unroll
+      for (int mt = 0; mt < 6; ++mt)
+        if (mt < MT) an[mt] = __ldg(Ob + ((ks + 1) * MT + mt) * 32 + lane);
+    }
+    const int k = ks * 4 + (lane & 3);
+    const int row = k < S ? rw[k] : -1;
+    const double b0 = row >= 0 ? X[row * kHpLD + (lane >> 2)] : 0.0;
+    const double b1 = row >= 0 ? X[row * kHpLD + 8 + (lane >> 2)] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 6; ++mt)
+      if (mt < MT) {
+        hp_dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
+        hp_dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
+      }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 6; ++mt)
+    if (mt < MT) {
+      const int r = mt * 8 + (lane >> 2);
+      if (r < S) {
+        double* x = X + rw[r] * kHpLD + (lane & 3) * 2;
+        x[0] = acc[mt][0][0];
+        x[1] = acc[mt][0][1];
+        x[8] = acc[mt][1][0];
+        x[9] = acc[mt][1][1];
+      }
+    }
+}
+
+struct HpHead {
+  int base[2][3];  // table offset of (parity, phase)
+};
+
+__global__ void __launch_bounds__(kHpW * 32, 3)
+    k_h_m2l_pas(HelmData H, const int* __restrict__ tab, int tab_n, HpHead hd, const int4* __restrict__ tiles,
+                const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ zops,
+                int zstride, const double* __restrict__ wvops, int wvstride, const int* __restrict__ op_cls,
+                const double2* __restrict__ cs, double2* __restrict__ temp) {
+  extern __shared__ double smp[];
+  const int P = H.P, KP = H.KP;
+  const int NE = (P + 1) * (P + 2) / 2, NO = P * (P + 1) / 2;
+  const int par = blockIdx.x & 1, NC = par ? NO : NE;
+  double* X = smp;                                              // 2 NE rows x kHpLD
+  int* s_tab = reinterpret_cast<int*>(X + 2 * NE * kHpLD);  // this parity's three tables
+  const int t0 = hd.base[par][0], tn = (par == 0 ? hd.base[1][0] : tab_n) - t0;
+  int* s_nm = s_tab + tn;                                      // NC: n | m << 8
+  __shared__ int s_src[kHColsS], s_pos[kHColsS];
+  __shared__ double2 s_cs[kHSolid + 1];
+  const int4 tile = tiles[blockIdx.x >> 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < tn; i += blockDim.x) s_tab[i] = tab[t0 + i];
+  for (int r = tid; r < NC; r += blockDim.x) {
+    int n, m;
+    if (par)
+      od_nm(r, n, m);
+    else
+      ev_nm(r, n, m);
+    s_nm[r] = n | m << 8;
+  }
+  if (tid < kHColsS) {
+    s_src[tid] = tid < tile.z ? col_src[tile.y + tid] : -1;
+    s_pos[tid] = tid < tile.z ? col_pos[tile.y + tid] : -1;
+  }
+  if (tid <= P) s_cs[tid] = cs[size_t(tile.x) * (P + 1) + tid];
+  __syncthreads();
+  // gather: M' = M e^{i m alpha}, then A = M'_m + M'_-m (A_0 = M'_0) or B = M'_m - M'_-m
+  for (int e = tid; e < NC * kHColsS; e += blockDim.x) {
+    const int c = e / NC, r = e - c * NC;
+    double2 v = make_double2(0.0, 0.0);
+    if (s_src[c] >= 0) {
+      const int nm = s_nm[r], n = nm & 255, m = nm >> 8;
+      const double2* Mb = H.M + size_t(s_src[c]) * KP;
+      const double2 ro = s_cs[m];
+      const double2 xp = cmul(__ldg(Mb + fi(n, m)), ro);
+      if (m == 0) {
+        v = xp;
+      } else {
+        const double2 xm = cmul(__ldg(Mb + fi(n, -m)), make_double2(ro.x, -ro.y));
+        v = par ? make_double2(xp.x - xm.x, xp.y - xm.y) : make_double2(xp.x + xm.x, xp.y + xm.y);
+      }
+    }
+    X[(2 * r) * kHpLD + c] = v.x;
+    X[(2 * r + 1) * kHpLD + c] = v.y;
+  }
+  __syncthreads();
+  const double* wv = wvops + size_t(op_cls[tile.x]) * wvstride;
+  const double* z = zops + size_t(tile.x) * zstride;
+#pragma unroll 1
+  for (int ph = 0; ph < 3; ++ph) {
+    const int* T = s_tab + (hd.base[par][ph] - t0);
+    const int nblk = T[0];
+    const int* rowoff = T + 1;
+    const int* opoff = rowoff + nblk + 1;
+    const int* bsz = opoff + nblk;
+    const int* rows = bsz + nblk;
+    const int* woff = rows + rowoff[nblk];
+    const int* wblk = woff + kHpW + 1;
+    const double* Op = ph == 1 ? z : wv;
+#pragma unroll 1
+    for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
+      const int b = wblk[i];
+      hp_block(X, rows + rowoff[b], bsz[b], Op + opoff[b], lane);
+    }
+    __syncthreads();
+  }
+  // staging rows: [A (NE) ; B (NO)] complex per entry
+  for (int r = tid; r < NC; r += blockDim.x)
+    for (int c = 0; c < tile.z; ++c)
+      temp[size_t(s_pos[c]) * KP + (par ? NE : 0) + r] =
+          make_double2(X[(2 * r) * kHpLD + c], X[(2 * r + 1) * kHpLD + c]);
+}
+
+// Z blocks (fragment order, real embedding) and e^{i m alpha} per operator
+struct HpZOff {
+  int off[kHSolid + 1];
+};
+__global__ void __launch_bounds__(256) k_h_build_zpas(HelmData H, const double4* __restrict__ shifts, HpZOff zo,
+                                                      int zstride, double* __restrict__ zops,
+                                                      double2* __restrict__ cs) {
+  extern __shared__ double2 smz[];
+  const int P = H.P, L = 2 * P;
+  double2* F = smz;
+  double2* rad = F + (L + 1) * (L + 1);
+  double2* Zc = rad + L + 1;  // per m: (P+1-m)^2, row-major [out n2][in n]
+  const double4 t = shifts[blockIdx.x];
+  const double rho = sqrt(t.x * t.x + t.y * t.y);
+  const double alpha = rho > 0 ? atan2(t.y, t.x) : 0.0;
+  if (threadIdx.x <= P) {
+    double sn, cn;
+    sincos(threadIdx.x * alpha, &sn, &cn);
+    cs[size_t(blockIdx.x) * (P + 1) + threadIdx.x] = make_double2(cn, sn);
+  }
+  wave_table_cta(H.k, L, 0.0, 0.0, sqrt(rho * rho + t.z * t.z), true, F, rad);
+  int tot = 0;
+  for (int m = 0; m <= P; ++m) tot += (P + 1 - m) * (P + 1 - m);
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    int m = 0, base = 0;
+    while (e >= base + (P + 1 - m) * (P + 1 - m)) {
+      base += (P + 1 - m) * (P + 1 - m);
+      ++m;
+    }
+    const int tq = P + 1 - m, i = (e - base) / tq, j = (e - base) % tq;
+    Zc[e] = t_entry(H, F, m + i, m, m + j, m);
+  }
+  __syncthreads();
+  double* Zb = zops + size_t(blockIdx.x) * zstride;
+  int base = 0;
+  for (int m = 0; m <= P; ++m) {
+    const int tq = P + 1 - m, s = 2 * tq, MT = (s + 7) / 8, KS = (s + 3) / 4;
+    for (int e = threadIdx.x; e < MT * KS * 32; e += blockDim.x) {
+      const int fr = e >> 5, l = e & 31, ks = fr / MT, mt = fr - ks * MT;
+      const int i = mt * 8 + l / 4, j = ks * 4 + l % 4;
+      double v = 0.0;
+      if (i < s && j < s) {
+        const double2 zz = Zc[base + (i % tq) * tq + (j % tq)];
+        const int pi = i / tq, pj = j / tq;
+        v = (pi == pj) ? zz.x : (pi == 0 ? -zz.y : zz.y);
+      }
+      Zb[zo.off[m] + e] = v;
+    }
+    base += tq * tq;
+  }
+}
+
 }  // namespace
 
 void helm_upload_constants() {
@@ -986,6 +1189,111 @@ int helm_m2l_split(const HelmData& H, int n_tiles, const int4* tiles, const int*
   const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
   k_h_m2l_split<<<n_tiles, th, smem, s>>>(H, tiles, col_src, col_pos, ops, cs, temp);
   k_h_m2l_reduce_split<<<n_boxes, th, 0, s>>>(H, boxes, base, temp, ent_op, cs);
+  return 2;
+}
+
+bool helm_pas_supported(int P) { return P >= 1 && P <= 20; }
+
+int helm_build_zpas(const HelmData& H, int n_ops, const double4* shifts, const int* z_off, int zstride, double* zops,
+                    double2* cs, cudaStream_t s) {
+  if (n_ops == 0) return 0;
+  const int L = 2 * H.P;
+  int tot = 0;
+  for (int m = 0; m <= H.P; ++m) tot += (H.P + 1 - m) * (H.P + 1 - m);
+  const size_t smem = size_t((L + 1) * (L + 1) + L + 1 + tot) * sizeof(double2);
+  HpZOff zo{};
+  for (int m = 0; m <= H.P; ++m) zo.off[m] = z_off[m];
+  cudaFuncSetAttribute(k_h_build_zpas, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_h_build_zpas<<<n_ops, 256, smem, s>>>(H, shifts, zo, zstride, zops, cs);
+  return 1;
+}
+
+// block tables of the pas kernel: per (parity, phase) [nblk][rowoff (nblk+1)][opoff][size]
+// [rows][warp offsets (kHpW+1)][block ids], whole blocks per warp by longest-first
+void helm_pas_tables(int P, const size_t* wv_off_w0, const size_t* wv_off_w1, const size_t* wv_off_v0,
+                     const size_t* wv_off_v1, const size_t* z_off, std::vector<int>& tab, int (&base)[2][3]) {
+  auto ev = [](int n, int m) { return n * (n + 1) / 2 + m; };
+  auto od = [](int n, int m) { return n * (n - 1) / 2 + m - 1; };
+  tab.clear();
+  for (int par = 0; par < 2; ++par)
+    for (int ph = 0; ph < 3; ++ph) {
+      std::vector<std::vector<int>> blocks;
+      std::vector<int> opo;
+      auto cr = [&](int n, int m) { return par ? od(n, m) : ev(n, m); };
+      if (ph != 1) {
+        const size_t* off = ph == 0 ? (par ? wv_off_w1 : wv_off_w0) : (par ? wv_off_v1 : wv_off_v0);
+        for (int n = par; n <= P; ++n)
+          for (int part = 0; part < 2; ++part) {  // Re rows, then Im rows, same operator
+            std::vector<int> b;
+            for (int m = par; m <= n; ++m) b.push_back(2 * cr(n, m) + part);
+            blocks.push_back(b);
+            opo.push_back(int(off[n - par]));
+          }
+      } else {
+        for (int m = par; m <= P; ++m) {
+          std::vector<int> b;
+          for (int part = 0; part < 2; ++part)
+            for (int n = m; n <= P; ++n) b.push_back(2 * cr(n, m) + part);
+          blocks.push_back(b);
+          opo.push_back(int(z_off[m]));
+        }
+      }
+      const int nb = int(blocks.size());
+      base[par][ph] = int(tab.size());
+      tab.push_back(nb);
+      std::vector<int> rows, rowoff{0};
+      for (auto& b : blocks) {
+        rows.insert(rows.end(), b.begin(), b.end());
+        rowoff.push_back(int(rows.size()));
+      }
+      tab.insert(tab.end(), rowoff.begin(), rowoff.end());
+      tab.insert(tab.end(), opo.begin(), opo.end());
+      for (auto& b : blocks) tab.push_back(int(b.size()));
+      tab.insert(tab.end(), rows.begin(), rows.end());
+      std::vector<int> order(nb);
+      for (int i = 0; i < nb; ++i) order[i] = i;
+      auto cost = [&](int i) {
+        const int sz = int(blocks[i].size());
+        return long((sz + 7) / 8) * ((sz + 3) / 4);
+      };
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+      std::vector<std::vector<int>> wl(kHpW);
+      std::vector<long> load(kHpW, 0);
+      for (int bi : order) {
+        const int w = int(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += cost(bi);
+        wl[w].push_back(bi);
+      }
+      std::vector<int> woff{0}, wblk;
+      for (auto& v : wl) {
+        wblk.insert(wblk.end(), v.begin(), v.end());
+        woff.push_back(int(wblk.size()));
+      }
+      tab.insert(tab.end(), woff.begin(), woff.end());
+      tab.insert(tab.end(), wblk.begin(), wblk.end());
+    }
+}
+
+int helm_m2l_pas(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
+                 const int* tab, int tab_n, const int (&base)[2][3], const double* zops, int zstride,
+                 const double* wvops, int wvstride, const int* op_cls, const double2* cs, double2* temp, int n_boxes,
+                 const int* boxes, int64_t vbase, const int* ent_op, cudaStream_t s) {
+  if (n_tiles == 0) return 0;
+  const int P = H.P, NE = (P + 1) * (P + 2) / 2;
+  const size_t smem = size_t(2 * NE * kHpLD) * sizeof(double) + size_t(std::max(base[1][0], tab_n - base[1][0]) + NE) * sizeof(int);
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_h_m2l_pas, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+      return -1;
+    attr = smem;
+  }
+  HpHead hd;
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 3; ++b) hd.base[a][b] = base[a][b];
+  k_h_m2l_pas<<<2 * n_tiles, kHpW * 32, smem, s>>>(H, tab, tab_n, hd, tiles, col_src, col_pos, zops, zstride, wvops,
+                                                    wvstride, op_cls, cs, temp);
+  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
+  k_h_m2l_reduce_split<<<n_boxes, th, 0, s>>>(H, boxes, vbase, temp, ent_op, cs);
   return 2;
 }
 
