@@ -17,6 +17,8 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "helm.cuh"
@@ -679,6 +681,107 @@ __global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict
   }
 }
 
+// P2L (List 4 far), one source per warp: lane 0 forms the radial table, lanes 0..P the
+// solid-harmonic columns m >= 0 (Cartesian recurrences), then every lane adds its
+// ceil(KP/32) coefficients f h_n conj(Y_n^m) -- the negative orders read the m >= 0
+// column (Y^{-m} = conj(Y^m)).  8 sources in flight per CTA instead of one CTA-wide
+// table per source; the warps' partial sums are added in warp order (deterministic).
+constexpr int kHP2LSlots = 14;  // ceil(441 / 32): P <= 20
+__global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __restrict__ boxes) {
+  extern __shared__ double2 smw[];
+  const int P = H.P, KP = H.KP, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+  double2* T = smw + warp * (KP + P + 1);
+  double2* rad = T + KP;
+  const int b = boxes[blockIdx.x];
+  const double4 bc = H.box[b];
+  double2 acc[kHP2LSlots];
+  int code[kHP2LSlots];  // fi(n, |m|) | n << 16 | (m < 0) << 30
+#pragma unroll
+  for (int sl = 0; sl < kHP2LSlots; ++sl) {
+    acc[sl] = make_double2(0.0, 0.0);
+    const int i = lane + 32 * sl;
+    code[sl] = -1;
+    if (i < KP) {
+      int n, m;
+      nm_of(i, n, m);
+      code[sl] = fi(n, m < 0 ? -m : m) | n << 16 | (m < 0 ? 1 << 30 : 0);
+    }
+  }
+  const int64_t sb = H.xfar_starts[b], se = H.xfar_starts[b + 1];
+  int64_t k = sb;
+  int off = warp, st = 0, cnt = 0;
+  if (k < se) {
+    st = H.xfar_seg[k].x;
+    cnt = H.xfar_seg[k].y;
+  }
+  while (k < se && off >= cnt) {
+    off -= cnt;
+    if (++k < se) {
+      st = H.xfar_seg[k].x;
+      cnt = H.xfar_seg[k].y;
+    }
+  }
+  while (k < se) {
+    const int src = st + off;
+    const double4 x = H.src[src];
+    const double2 w = H.hw[src];
+    const double tx = x.x - bc.x, ty = x.y - bc.y, tz = x.z - bc.z, r2 = tx * tx + ty * ty + tz * tz;
+    if (lane == 0) radial_table(H.k, sqrt(r2), P, true, rad);
+    if (lane <= P) {  // column m = lane of S_n^m(t), n = m..P
+      const int m = lane;
+      double2 d = make_double2(0.28209479177387814347, 0.0);
+      for (int i = 1; i <= m; ++i)
+        d = make_double2(c_sa[i] * (d.x * tx - d.y * ty), c_sa[i] * (d.x * ty + d.y * tx));
+      T[fi(m, m)] = d;
+      if (m + 1 <= P) {
+        double2 a = d, bb = make_double2(c_sb[m] * tz * d.x, c_sb[m] * tz * d.y);
+        T[fi(m + 1, m)] = bb;
+        for (int n = m + 2; n <= P; ++n) {
+          const double cn = c_sc[n * (kHSolid + 1) + m], dn = c_sd[n * (kHSolid + 1) + m] * r2;
+          const double2 c2 = make_double2(cn * (tz * bb.x - dn * a.x), cn * (tz * bb.y - dn * a.y));
+          T[fi(n, m)] = c2;
+          a = bb;
+          bb = c2;
+        }
+      }
+    }
+    __syncwarp();
+    const double2 f = make_double2(-H.k * w.y, H.k * w.x);  // i k w
+#pragma unroll
+    for (int sl = 0; sl < kHP2LSlots; ++sl) {
+      if (code[sl] < 0) continue;
+      double2 v = T[code[sl] & 0xffff];
+      if (!(code[sl] >> 30)) v.y = -v.y;  // m >= 0: conj(S_n^m)
+      const double2 fr = cmul(f, rad[(code[sl] >> 16) & 0x3fff]);
+      acc[sl] = cfma(fr, v, acc[sl]);
+    }
+    __syncwarp();
+    off += NW;
+    while (k < se && off >= cnt) {
+      off -= cnt;
+      if (++k < se) {
+        st = H.xfar_seg[k].x;
+        cnt = H.xfar_seg[k].y;
+      }
+    }
+  }
+  __syncthreads();
+  double2* red = smw;  // NW x KP
+#pragma unroll
+  for (int sl = 0; sl < kHP2LSlots; ++sl)
+    if (code[sl] >= 0) red[warp * KP + lane + 32 * sl] = acc[sl];
+  __syncthreads();
+  for (int i = threadIdx.x; i < KP; i += blockDim.x) {
+    double sx = 0.0, sy = 0.0;
+    for (int ww = 0; ww < NW; ++ww) {
+      sx += red[ww * KP + i].x;
+      sy += red[ww * KP + i].y;
+    }
+    const double2 v = H.L[size_t(b) * KP + i];
+    H.L[size_t(b) * KP + i] = make_double2(v.x + sx, v.y + sy);
+  }
+}
+
 // Stage 5b M2QBXL / Stage 8 L2QBXL: box expansion X (order p) -> up to kHCtrMax
 // centres (order q).  For mu = -(p+q)..p+q: C_mu[i'][l] from X and the Gaunt
 // table, F_l^mu(c_j - c_box) per centre, acc[j][i'] += sum_l F C.
@@ -1320,6 +1423,14 @@ int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 
 int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
+  // warp per source (default for P <= 20); QBXG_HELM_P2L=cta keeps one CTA-wide table per source
+  static const bool cta = std::getenv("QBXG_HELM_P2L") && std::string(std::getenv("QBXG_HELM_P2L")) == "cta";
+  if (!cta && H.KP <= 32 * kHP2LSlots) {
+    const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
+    cudaFuncSetAttribute(k_h_p2l_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_h_p2l_w<<<n, 256, smem, s>>>(H, boxes);
+    return 1;
+  }
   k_h_p2l<<<n, 256, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, boxes);
   return 1;
 }

@@ -81,13 +81,16 @@ print(json.dumps({"helm": float(np.linalg.norm(pot - ref) / np.linalg.norm(ref))
 """ % ROOT
 
 
-@pytest.mark.parametrize("mode", ["full", "split"])
+@pytest.mark.parametrize("mode", ["full", "split", "p2l-cta"])
 def test_helmholtz_m2l_variant(mode):
     """QBXG_HELM_M2L=full (dense per-offset operators) and =split (even / odd dense
     blocks) against the oracle; the default point-and-shoot M2L is covered by
     tests/test_helmholtz.py."""
     full = dict(os.environ)
-    full["QBXG_HELM_M2L"] = mode
+    if mode == "p2l-cta":
+        full["QBXG_HELM_P2L"] = "cta"  # one CTA-wide wave table per source in P2L
+    else:
+        full["QBXG_HELM_M2L"] = mode
     r = subprocess.run([sys.executable, "-c", HELM_SCRIPT], env=full, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["helm"] <= 1e-11
