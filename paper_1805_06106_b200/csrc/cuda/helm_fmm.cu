@@ -817,26 +817,26 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   for (int mu = -L; mu <= L; ++mu) {
     const int amu = abs(mu);
     // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu}
-    for (int e = threadIdx.x; e < KQ * NL; e += blockDim.x) {
-      const int iout = e / NL, l = e % NL;
+    // only the l >= |mu| entries are used, and only n with n + n' + l even contribute:
+    // enumerate exactly those (no idle lanes, no parity branches)
+    const int NLm = NL - amu;
+    for (int e = threadIdx.x; e < KQ * NLm; e += blockDim.x) {
+      const int iout = e / NLm, l = amu + e % NLm;
       double2 cacc = make_double2(0, 0);
-      if (l >= amu) {
-        int n2, m2;
-        nm_of(iout, n2, m2);
-        const int m = m2 + mu;
-        const int nlo = max(max(abs(m), abs(l - n2)), 0), nhi = min(P, l + n2);
-        for (int n = nlo; n <= nhi; ++n) {
-          if ((n + n2 + l) & 1) continue;
-          if (l < abs(n - n2)) continue;
-          const int li = (l - abs(n - n2)) >> 1;
-          const double gv = H.gaunt[(size_t(fi(n, m)) * KP + iout) * H.GL + li];
-          if (gv == 0.0) continue;
-          const double2 t = cmul(ipow(n2 + l - n), Xs[fi(n, m)]);
-          cacc.x += gv * t.x;
-          cacc.y += gv * t.y;
-        }
+      int n2, m2;
+      nm_of(iout, n2, m2);
+      const int m = m2 + mu;
+      int nlo = max(abs(m), abs(l - n2));
+      nlo += (nlo + n2 + l) & 1;
+      const int nhi = min(P, l + n2);
+      for (int n = nlo; n <= nhi; n += 2) {
+        const int li = (l - abs(n - n2)) >> 1;
+        const double gv = __ldg(H.gaunt + (size_t(fi(n, m)) * KP + iout) * H.GL + li);
+        const double2 t = cmul(ipow(n2 + l - n), Xs[fi(n, m)]);
+        cacc.x = fma(gv, t.x, cacc.x);
+        cacc.y = fma(gv, t.y, cacc.y);
       }
-      Cm[e] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
+      Cm[iout * NL + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
     }
     // F column mu per centre: (rad_l / r^l) S_l^mu(t), l = |mu|..L  (S^{-mu} = conj S^mu)
     for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
