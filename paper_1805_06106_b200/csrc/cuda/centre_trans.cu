@@ -624,6 +624,7 @@ __global__ void __launch_bounds__(kL3Threads) k_l2qbxl3(DevData D, const int* __
       const double2 cm = make_double2(sg * cur.x, -sg * cur.y);  // R_N^{-K}
 #pragma unroll
       for (int n = 0; n <= Q; ++n) {
+        if (N + n > P) break;  // the box local has no degree above p (uniform branch: ~1/3 of the terms)
         const int j = N + n;
         const double2* __restrict__ row = tb + j * j + j;
 #pragma unroll
