@@ -1011,7 +1011,7 @@ void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 // phase runs its blocks in place as m8n8k4 DMMAs (W, V real, applied to the Re and Im
 // rows separately; Z as the real embedding [[Re, -Im], [Im, Re]]).  Output rows are the
 // split M2L's staging rows, so k_h_m2l_reduce_split finishes the job.  Per List-2 entry at
-// p = 20: 4 x (3,311 + 2,870) real multiply-adds instead of 4 x (231^2 + 210^2).
+// p = 20: 8 x (3,311 + 2,870) real multiply-adds instead of 4 x (231^2 + 210^2).
 constexpr int kHpW = 8, kHpLD = kHColsS + 1;
 
 __device__ __forceinline__ void hp_dmma(double& d0, double& d1, double a, double b) {
