@@ -394,6 +394,180 @@ __global__ void __launch_bounds__(kWarps2 * 32, 1)
   }
 }
 
+// ------------------------------------------- v3: persistent, warp-specialised pipeline
+// One CTA per SM walks tiles blockIdx.x, blockIdx.x + grid, ... through two tile buffers.
+// kMemW memory warps gather tile k+1 (and write out tile k-1's staging rows) while the
+// compute warps run tile k's three phases; the hand-off uses named barriers
+// (FULL[b]: memory -> compute, DONE[b]: compute -> memory; bar.arrive / bar.sync).
+// CW = 8 compute warps own all 32 columns of their blocks, CW = 16 split them in halves.
+constexpr int kMemW = 4;
+
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// block of size S on NT 8-column groups starting at column cb (padded rows of kLD)
+template <int S, int NT>
+__device__ __forceinline__ void pas3_block(double* X, const int* rw, const double* __restrict__ Ob, int lane, int cb) {
+  constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, K4 = 4 * KS;
+  double a[MT][KS], b[KS][NT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = __ldg(Ob + (mt * 8 + (lane >> 2)) * K4 + ks * 4 + (lane & 3));
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + (lane & 3);
+    const int row = k < S ? rw[k] : 0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[row * kLD + cb + nt * 8 + (lane >> 2)] : 0.0;
+  }
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[ks][nt]);
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = mt * 8 + (lane >> 2);
+    if (r < S) {
+      double* x = X + rw[r] * kLD + cb + (lane & 3) * 2;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        x[nt * 8] = acc[mt][nt][0];
+        x[nt * 8 + 1] = acc[mt][nt][1];
+      }
+    }
+  }
+}
+
+template <int P, int CW>
+__global__ void __launch_bounds__((CW + kMemW) * 32, 1)
+    k_m2l_pas3(const int* __restrict__ tab, int tab_n, TabHead hd, int nblk, const double* __restrict__ ops,
+               int op_stride, int phase_size, const double2* __restrict__ cs_all, const int4* __restrict__ tiles,
+               int n_tiles, const int* __restrict__ col_src, const int* __restrict__ col_pos,
+               const double* __restrict__ M, int kp2, int KRp, double* __restrict__ temp) {
+  constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), CT = CW * 32, MEMT = kMemW * 32, NTHR = CT + MEMT;
+  constexpr int NT = CW == 8 ? 4 : 2;
+  extern __shared__ double smem[];
+  double* Xb = smem;  // two tiles of NROW x kLD
+  int* s_tab = reinterpret_cast<int*>(Xb + 2 * NROW * kLD);
+  __shared__ int s_src[2][kBN], s_pos[2][kBN], s_op[2], s_cnt[2];
+  __shared__ double2 s_cs[2][P + 1];
+  __shared__ int s_code[NR];  // Re row | Im row << 10 (0 for m = 0) | m << 20 of half-table index q
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < tab_n; i += NTHR) s_tab[i] = tab[i];
+  for (int q = tid; q < NR; q += NTHR) {
+    int n = 0;
+    while (hidx(n + 1, 0) <= q) ++n;
+    const int m = q - hidx(n, 0);
+    s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0) << 10 | m << 20;
+  }
+  __syncthreads();
+  const int ntl = blockIdx.x < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  if (warp >= CW) {
+    // ---- memory warps: write out tile k-2, gather tile k, into buffer k & 1
+    const int mt = tid - CT;
+    for (int k = 0; k < ntl + 2; ++k) {
+      const int b = k & 1;
+      double* X = Xb + b * NROW * kLD;
+      if (k >= 2) {
+        nb_sync(3 + b, NTHR);  // DONE[b]: tile k-2's phases are finished
+        const int cnt = s_cnt[b];
+        for (int r = mt; r < NROW; r += MEMT)
+          for (int c = 0; c < cnt; ++c) temp[size_t(s_pos[b][c]) * KRp + r] = X[r * kLD + c];
+        nb_sync(5, MEMT);
+      }
+      if (k < ntl) {
+        const int4 tile = tiles[blockIdx.x + size_t(k) * gridDim.x];
+        if (mt < kBN) {
+          s_src[b][mt] = mt < tile.z ? col_src[tile.y + mt] : -1;
+          s_pos[b][mt] = mt < tile.z ? col_pos[tile.y + mt] : -1;
+        }
+        if (mt <= P) s_cs[b][mt] = cs_all[size_t(tile.x) * (P + 1) + mt];
+        if (mt == 0) {
+          s_op[b] = tile.x;
+          s_cnt[b] = tile.z;
+        }
+        nb_sync(5, MEMT);
+        constexpr int kSt = 8;
+        for (int base = 0; base < NR * kBN; base += kSt * MEMT) {
+          double2 v[kSt];
+#pragma unroll
+          for (int u = 0; u < kSt; ++u) {
+            const int e = base + mt + u * MEMT;
+            v[u] = make_double2(0.0, 0.0);
+            if (e < NR * kBN) {
+              const int c = e / NR, q = e - c * NR;
+              const int src = s_src[b][c];
+              if (src >= 0) v[u] = __ldg(reinterpret_cast<const double2*>(M + size_t(src) * kp2) + q);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kSt; ++u) {
+            const int e = base + mt + u * MEMT;
+            if (e < NR * kBN) {
+              const int c = e / NR, q = e - c * NR;
+              const int code = s_code[q], ri = (code >> 10) & 1023;
+              const double2 r = s_cs[b][code >> 20];
+              X[(code & 1023) * kLD + c] = v[u].x * r.x - v[u].y * r.y;
+              if (ri) X[ri * kLD + c] = v[u].x * r.y + v[u].y * r.x;
+            }
+          }
+        }
+        nb_arrive(1 + b, NTHR);  // FULL[b]
+      }
+    }
+  } else {
+    // ---- compute warps: the three phases of tile k in buffer k & 1
+    const int wq = warp % kWarps, cb = CW == 8 ? 0 : (warp / kWarps) * 16;
+    for (int k = 0; k < ntl; ++k) {
+      const int b = k & 1;
+      double* X = Xb + b * NROW * kLD;
+      nb_sync(1 + b, NTHR);  // FULL[b]
+      const double* opb = ops + size_t(s_op[b]) * op_stride;
+#pragma unroll 1
+      for (int ph = 0; ph < kPasPhases; ++ph) {
+        const int* T = s_tab + hd.base[ph];
+        const int* rowoff = T;
+        const int* opoff = T + nblk + 1;
+        const int* rows = opoff + nblk;
+        const int* woff = rows + NROW;
+        const int* wblk = woff + kWarps + 1;
+        const double* Op = opb + size_t(ph) * phase_size;
+#pragma unroll 1
+        for (int i = woff[wq]; i < woff[wq + 1]; ++i) {
+          const int bl = wblk[i];
+          const int* rw = rows + rowoff[bl];
+          const double* Ob = Op + opoff[bl];
+          switch (rowoff[bl + 1] - rowoff[bl]) {
+#define QBXG_PAS3_CASE(S) \
+  case S:                 \
+    pas3_block<S, NT>(X, rw, Ob, lane, cb); \
+    break;
+            QBXG_PAS3_CASE(1) QBXG_PAS3_CASE(2) QBXG_PAS3_CASE(3) QBXG_PAS3_CASE(4) QBXG_PAS3_CASE(5)
+            QBXG_PAS3_CASE(6) QBXG_PAS3_CASE(7) QBXG_PAS3_CASE(8) QBXG_PAS3_CASE(9) QBXG_PAS3_CASE(10)
+            QBXG_PAS3_CASE(11) QBXG_PAS3_CASE(12) QBXG_PAS3_CASE(13) QBXG_PAS3_CASE(14) QBXG_PAS3_CASE(15)
+            QBXG_PAS3_CASE(16)
+#undef QBXG_PAS3_CASE
+            default: break;
+          }
+        }
+        nb_sync(6, CT);  // compute warps only
+      }
+      nb_arrive(3 + b, NTHR);  // DONE[b]
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 struct PasLayout {
   int nblk = 0, phase_size = 0;
@@ -505,9 +679,47 @@ int pas2_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2
 template <int P, bool SWZ>
 int pas1_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s);
 
+// v3 (QBXG_PAS_V3=8 or 16 compute warps): the warp-specialised pipeline.  Parity-green but
+// slower at config 1 (M2L 57.5 / 61.0 vs 42.9 ms): with one CTA per SM the phases of a
+// single tile cannot hide the operator-fragment latency the three co-resident v1 CTAs hide.
+// (A warp-owned-columns variant without any CTA barrier measured 82 ms: with one 8-column
+// group per warp each operator fragment feeds one DMMA instead of four.)
+int pas_v3() {
+  static const int cw = std::getenv("QBXG_PAS_V3") ? std::atoi(std::getenv("QBXG_PAS_V3")) : 0;
+  return cw == 8 || cw == 16 ? cw : 0;
+}
+
+template <int P, int CW>
+int pas3_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
+  constexpr int NROW = (P + 1) * (P + 1);
+  const size_t smem = size_t(2 * NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
+  static size_t attr = 0;
+  static int n_sm = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(k_m2l_pas3<P, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+      return -1;
+    attr = smem;
+  }
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  TabHead hd;
+  for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
+  const int grid = std::max(1, std::min(C.n_tiles, n_sm));
+  k_m2l_pas3<P, CW><<<grid, (CW + kMemW) * 32, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops,
+                                                          Pl.pas_stride, Pl.pas_phase, Pl.cs, C.tiles, C.n_tiles,
+                                                          C.col_src, C.col_pos, X, kp2, Pl.KRp, Pl.temp);
+  return 1;
+}
+
 template <int P>
 int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
   if (pas_v2()) return pas2_launch_p<P>(Pl, C, X, kp2, s);
+  if (pas_v3() == 8) return pas3_launch_p<P, 8>(Pl, C, X, kp2, s);
+  if (pas_v3() == 16) return pas3_launch_p<P, 16>(Pl, C, X, kp2, s);
   return pas_swz() ? pas1_launch_p<P, true>(Pl, C, X, kp2, s) : pas1_launch_p<P, false>(Pl, C, X, kp2, s);
 }
 

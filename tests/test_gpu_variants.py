@@ -44,6 +44,8 @@ VARIANTS = [
     {"QBXG_M2L_MODE": "split"},
     {"QBXG_PAS_V2": "1"},
     {"QBXG_PAS_SWZ": "1"},
+    {"QBXG_PAS_V3": "8"},
+    {"QBXG_PAS_V3": "16", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
     {"QBXG_PAS_V2": "1", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
     {"QBXG_M2L_MODE": "split", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
     {"QBXG_NEAR_MODE": "0"},
