@@ -45,7 +45,7 @@ struct HelmData {
 };
 
 // one centre-translation CTA: box, first entry in the item list, count (<= kHCtrMax)
-constexpr int kHCtrMax = 64;
+constexpr int kHCtrMax = 32;
 
 void helm_upload_constants();  // solid-harmonic recurrence tables (this TU's __constant__)
 int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s);

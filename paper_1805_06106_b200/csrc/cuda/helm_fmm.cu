@@ -795,10 +795,10 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   const int4 cta = ctas[blockIdx.x];  // (box, first item, count, -)
   const int nctr = cta.z;
   double2* Xs = sm;                      // KP
-  double2* Cm = Xs + KP;                 // KQ x NL
-  double2* rad = Cm + KQ * NL;           // kHCtrMax x NL
-  double2* Fc = rad + kHCtrMax * NL;     // kHCtrMax x NL
-  double* geo = reinterpret_cast<double*>(Fc + kHCtrMax * NL);  // kHCtrMax x 4: cos t, sin t, phi, |t|
+  double2* Cm = Xs + KP;                 // 2 x KQ x NL: C_{+|mu|}, C_{-|mu|}
+  double2* rad = Cm + 2 * KQ * NL;       // kHCtrMax x NL
+  double2* Fc = rad + kHCtrMax * NL;     // 2 x kHCtrMax x NL: F^{+|mu|}, F^{-|mu|}
+  double* geo = reinterpret_cast<double*>(Fc + 2 * kHCtrMax * NL);  // kHCtrMax x 4: t, |t|^2
   const double4 bc = H.box[cta.x];
   for (int j = threadIdx.x; j < KP; j += blockDim.x) Xs[j] = X[size_t(cta.x) * KP + j];
   for (int j = threadIdx.x; j < nctr; j += blockDim.x) {  // per centre: t, and rad_l / r^l
@@ -814,14 +814,16 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
 #pragma unroll
   for (int a = 0; a < kHCtrAcc; ++a) acc[a] = make_double2(0, 0);
   __syncthreads();
-  for (int mu = -L; mu <= L; ++mu) {
-    const int amu = abs(mu);
-    // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu}
-    // only the l >= |mu| entries are used, and only n with n + n' + l even contribute:
-    // enumerate exactly those (no idle lanes, no parity branches)
+  // mu and -mu together: one solid-harmonic column per |mu| serves both signs
+  // (S^{-mu} = conj S^mu), and half as many barriers
+  for (int amu = 0; amu <= L; ++amu) {
+    const int ns = amu == 0 ? 1 : 2;  // sign index 0: mu = +|mu|, 1: mu = -|mu|
+    // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu} over the used
+    // terms only: l >= |mu| and n + n' + l even
     const int NLm = NL - amu;
-    for (int e = threadIdx.x; e < KQ * NLm; e += blockDim.x) {
-      const int iout = e / NLm, l = amu + e % NLm;
+    for (int e = threadIdx.x; e < ns * KQ * NLm; e += blockDim.x) {
+      const int sg = e / (KQ * NLm), er = e - sg * KQ * NLm;
+      const int iout = er / NLm, l = amu + er % NLm, mu = sg ? -amu : amu;
       double2 cacc = make_double2(0, 0);
       int n2, m2;
       nm_of(iout, n2, m2);
@@ -836,15 +838,17 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
         cacc.x = fma(gv, t.x, cacc.x);
         cacc.y = fma(gv, t.y, cacc.y);
       }
-      Cm[iout * NL + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
+      Cm[(sg * KQ + iout) * NL + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
     }
-    // F column mu per centre: (rad_l / r^l) S_l^mu(t), l = |mu|..L  (S^{-mu} = conj S^mu)
+    // F columns per centre: (rad_l / r^l) S_l^{+-|mu|}(t), l = |mu|..L
     for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
-      double2* col = Fc + j * NL;
-      solid_column(amu, L, geo[4 * j], geo[4 * j + 1], geo[4 * j + 2], geo[4 * j + 3], col);
+      double2* colp = Fc + j * NL;
+      double2* colm = Fc + (kHCtrMax + j) * NL;
+      solid_column(amu, L, geo[4 * j], geo[4 * j + 1], geo[4 * j + 2], geo[4 * j + 3], colp);
       for (int l = amu; l <= L; ++l) {
-        const double2 sv = mu < 0 ? make_double2(col[l].x, -col[l].y) : col[l];
-        col[l] = cmul(rad[j * NL + l], sv);
+        const double2 sv = colp[l], rl = rad[j * NL + l];
+        colp[l] = cmul(rl, sv);
+        colm[l] = cmul(rl, make_double2(sv.x, -sv.y));
       }
     }
     __syncthreads();
@@ -854,7 +858,11 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
       if (e < nctr * KQ) {
         const int j = e / KQ, iout = e % KQ;
         double2 s2 = acc[a];
-        for (int l = amu; l <= L; ++l) s2 = cfma(Fc[j * NL + l], Cm[iout * NL + l], s2);
+        for (int sg = 0; sg < ns; ++sg) {
+          const double2* F = Fc + (sg * kHCtrMax + j) * NL;
+          const double2* C = Cm + (sg * KQ + iout) * NL;
+          for (int l = amu; l <= L; ++l) s2 = cfma(F[l], C[l], s2);
+        }
         acc[a] = s2;
       }
     }
@@ -1440,7 +1448,7 @@ int helm_ctr(const HelmData& H, int singular, const double2* X, int n_ctas, cons
   if (n_ctas == 0) return 0;
   const int NL = H.P + H.Q + 1;
   const size_t smem =
-      size_t(H.KP + H.KQ * NL + 2 * kHCtrMax * NL) * sizeof(double2) + size_t(4 * kHCtrMax) * sizeof(double);
+      size_t(H.KP + 2 * H.KQ * NL + 3 * kHCtrMax * NL) * sizeof(double2) + size_t(4 * kHCtrMax) * sizeof(double);
   cudaFuncSetAttribute(k_h_ctr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_h_ctr<<<n_ctas, 256, smem, s>>>(H, singular, X, ctas, ctr_of, out_row, out, accumulate);
   return 1;
