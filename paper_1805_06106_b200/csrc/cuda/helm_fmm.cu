@@ -1035,18 +1035,14 @@ __device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const 
   double acc[6][2][2];
 #pragma unroll
   for (int mt = 0; mt < 6; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
-  double an[6];
+  // operator fragments two k-steps ahead (ring of two register sets)
+  double A0[6], A1[6];
+  auto load = [&](double (&A)[6], int ks) {
 #pragma unroll
-  for (int mt = 0; mt < 6; ++mt) an[mt] = mt < MT ? __ldg(Ob + mt * 32 + lane) : 0.0;
-  for (int ks = 0; ks < KS; ++ks) {
-    double a[6];
-#pragma unroll
-    for (int mt = 0; mt < 6; ++mt) a[mt] = an[mt];
-    if (ks + 1 < KS) {
-#pragma unroll
-      for (int mt = 0; mt < 6; ++mt)
-        if (mt < MT) an[mt] = __ldg(Ob + ((ks + 1) * MT + mt) * 32 + lane);
-    }
+    for (int mt = 0; mt < 6; ++mt)
+      if (mt < MT) A[mt] = __ldg(Ob + (ks * MT + mt) * 32 + lane);
+  };
+  auto step = [&](const double (&a)[6], int ks) {
     const int k = ks * 4 + (lane & 3);
     const int row = k < S ? rw[k] : -1;
     const double b0 = row >= 0 ? X[row * kHpLD + (lane >> 2)] : 0.0;
@@ -1057,6 +1053,26 @@ __device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const 
         hp_dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
         hp_dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
       }
+  };
+#pragma unroll
+  for (int mt = 0; mt < 6; ++mt) A0[mt] = A1[mt] = 0.0;
+  load(A0, 0);
+  if (KS > 1) load(A1, 1);
+  for (int ks = 0; ks < KS; ks += 2) {
+    {
+      double a[6];
+#pragma unroll
+      for (int mt = 0; mt < 6; ++mt) a[mt] = A0[mt];
+      if (ks + 2 < KS) load(A0, ks + 2);
+      step(a, ks);
+    }
+    if (ks + 1 < KS) {
+      double a[6];
+#pragma unroll
+      for (int mt = 0; mt < 6; ++mt) a[mt] = A1[mt];
+      if (ks + 3 < KS) load(A1, ks + 3);
+      step(a, ks + 1);
+    }
   }
   __syncwarp();
 #pragma unroll
@@ -1077,7 +1093,7 @@ struct HpHead {
   int base[2][3];  // table offset of (parity, phase)
 };
 
-__global__ void __launch_bounds__(kHpW * 32, 3)
+__global__ void __launch_bounds__(kHpW * 32, 2)
     k_h_m2l_pas(HelmData H, const int* __restrict__ tab, int tab_n, HpHead hd, const int4* __restrict__ tiles,
                 const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ zops,
                 int zstride, const double* __restrict__ wvops, int wvstride, const int* __restrict__ op_cls,
