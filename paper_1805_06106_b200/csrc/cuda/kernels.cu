@@ -84,9 +84,28 @@ __global__ void __launch_bounds__(256) k_p2m(DevData D, const int* __restrict__ 
     for (int t = threadIdx.x; t < nb * (D.p + 1); t += blockDim.x) {
       const int s = t / (D.p + 1), m = t % (D.p + 1);
       const double4 x = s_src[s];
-      double2 col[kMaxOrder + 1];
-      regular_column((x.x - bc.x) * ih, (x.y - bc.y) * ih, (x.z - bc.z) * ih, m, D.p, col);
-      for (int n = m; n <= D.p; ++n) tab[s * D.kp + hidx(n, m)] = col[n - m];
+      // regular_column's recurrence written straight into the shared table (no local array)
+      const double ux = (x.x - bc.x) * ih, uy = (x.y - bc.y) * ih, uz = (x.z - bc.z) * ih;
+      const double r2 = ux * ux + uy * uy + uz * uz;
+      double2 rmm = make_double2(1.0, 0.0);
+      for (int k = 1; k <= m; ++k) {
+        const double sk = 1.0 / (2.0 * k);
+        rmm = make_double2((rmm.x * ux - rmm.y * uy) * sk, (rmm.x * uy + rmm.y * ux) * sk);
+      }
+      double2* T = tab + s * D.kp;
+      T[hidx(m, m)] = rmm;
+      if (m + 1 <= D.p) {
+        double2 a = rmm, b = make_double2(uz * rmm.x, uz * rmm.y);
+        T[hidx(m + 1, m)] = b;
+        for (int n = m + 2; n <= D.p; ++n) {
+          const double f = c_inv_nm[hidx(n, m)];
+          const double c1 = (2 * n - 1) * uz;
+          const double2 c = make_double2((c1 * b.x - r2 * a.x) * f, (c1 * b.y - r2 * a.y) * f);
+          T[hidx(n, m)] = c;
+          a = b;
+          b = c;
+        }
+      }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < D.kp; c += blockDim.x) {
