@@ -596,14 +596,25 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
           double2 g[Q + 1];
           radial_over_rn<Q>(k, r, ir, g);
           const double2 f0 = make_double2(-k * w.y, k * w.x);  // ik w
+          // L_n^m += fh conj(S_n^m), L_n^-m += fh S_n^m with fh = c + i d, S = a + i b:
+          // the two share the four real products, so accumulate (sum c a, sum d b) in slot
+          // (n, m) and (sum d a, sum c b) in slot (n, -m) -- 4 FMAs instead of 8 -- and form
+          // the coefficients after the slice reduction.  S_n^0 is real: L_n^0 += fh a.
 #pragma unroll
           for (int n = 0; n <= Q; ++n) {
             const double2 fh = cmul(f0, g[n]);
 #pragma unroll
             for (int m = 0; m <= n; ++m) {
               const double2 sv = Sh[n * (n + 1) / 2 + m];
-              acc[fi(n, m)] = cfma(fh, make_double2(sv.x, -sv.y), acc[fi(n, m)]);  // conj(S_n^m)
-              if (m > 0) acc[fi(n, -m)] = cfma(fh, sv, acc[fi(n, -m)]);             // conj(S_n^-m) = S_n^m
+              if (m == 0) {
+                acc[fi(n, 0)].x = fma(fh.x, sv.x, acc[fi(n, 0)].x);
+                acc[fi(n, 0)].y = fma(fh.y, sv.x, acc[fi(n, 0)].y);
+              } else {
+                acc[fi(n, m)].x = fma(fh.x, sv.x, acc[fi(n, m)].x);    // c a
+                acc[fi(n, m)].y = fma(fh.y, sv.y, acc[fi(n, m)].y);    // d b
+                acc[fi(n, -m)].x = fma(fh.y, sv.x, acc[fi(n, -m)].x);  // d a
+                acc[fi(n, -m)].y = fma(fh.x, sv.y, acc[fi(n, -m)].y);  // c b
+              }
             }
           }
         }
@@ -616,14 +627,26 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
     __syncthreads();
     if (active && sl == 0) {
       double2* out = H.Lc + size_t(c0 + cc + ci) * KQ;
-      for (int i = 0; i < KQ; ++i) {
-        double2 s2 = make_double2(0, 0);
-        for (int k2 = 0; k2 < S; ++k2) {
-          s2.x += red[i * 128 + threadIdx.x + k2].x;
-          s2.y += red[i * 128 + threadIdx.x + k2].y;
+      for (int n = 0; n <= Q; ++n)
+        for (int m = 0; m <= n; ++m) {
+          double2 sp = make_double2(0, 0), sm2 = make_double2(0, 0);
+          for (int k2 = 0; k2 < S; ++k2) {
+            const double2 vp = red[fi(n, m) * 128 + threadIdx.x + k2];
+            sp.x += vp.x;
+            sp.y += vp.y;
+            if (m > 0) {
+              const double2 vm = red[fi(n, -m) * 128 + threadIdx.x + k2];
+              sm2.x += vm.x;
+              sm2.y += vm.y;
+            }
+          }
+          if (m == 0) {
+            out[fi(n, 0)] = sp;
+          } else {  // (ca + db, da - cb) and (ca - db, da + cb)
+            out[fi(n, m)] = make_double2(sp.x + sp.y, sm2.x - sm2.y);
+            out[fi(n, -m)] = make_double2(sp.x - sp.y, sm2.x + sm2.y);
+          }
         }
-        out[i] = s2;
-      }
     }
     __syncthreads();
   }
