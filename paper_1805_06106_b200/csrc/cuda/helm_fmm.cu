@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
           const double2 w = H.hw[s];
           const double vx = x.x - c.x, vy = x.y - c.y, vz = x.z - c.z;
           const double r2 = vx * vx + vy * vy + vz * vz;
-          const double r = sqrt(r2), ir = 1.0 / r;
+          const double ir = rsqrt(r2), r = r2 * ir;  // one rsqrt instead of sqrt + divide
           double2 Sh[KH];  // S_n^m, m >= 0, index n(n+1)/2 + m
 #pragma unroll
           for (int m = 0; m <= Q; ++m) {
