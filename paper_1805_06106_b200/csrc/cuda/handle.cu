@@ -148,6 +148,11 @@ struct Handle {
   bool helm = false;
   dev::HelmData HD{};
   std::vector<double2*> h_ops_m2m, h_ops_l2l;  // per level: 8 octant operators
+  // batched shifts: (src, dst) pairs grouped by (level, octant); QBXG_HELM_SHIFT=box keeps k_h_shift
+  bool h_shift_batched = true;
+  int2* h_m2m_pairs = nullptr;
+  int2* h_l2l_pairs = nullptr;
+  std::vector<int> h_m2m_off, h_l2l_off;  // (nlev x 8 + 1) offsets
   double2* h_ops_m2l = nullptr;                // per (level, offset) operators (split: even / odd blocks)
   double2* h_cs = nullptr;                     // per operator e^{i m alpha}, m <= p (split form)
   int* h_ent_op = nullptr;                     // operator of every List-2 CSR entry (split form)
@@ -536,6 +541,43 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
     for (int l = 0; l + 1 < H.nlev; ++l, k += 8) H.h_ops_m2m[l] = shift_ops + k * opsz;
     for (int l = 1; l < H.nlev; ++l, k += 8) H.h_ops_l2l[l] = shift_ops + k * opsz;
   }
+  H.h_shift_batched = !(std::getenv("QBXG_HELM_SHIFT") && std::string(std::getenv("QBXG_HELM_SHIFT")) == "box");
+  {
+    // (src, dst) pairs per (level, octant) with the operators' octant convention (x 4, y 2, z 1)
+    auto hoct = [&](int c, int par) {
+      return (V.box_center[3 * c] > V.box_center[3 * par] ? 4 : 0) +
+             (V.box_center[3 * c + 1] > V.box_center[3 * par + 1] ? 2 : 0) +
+             (V.box_center[3 * c + 2] > V.box_center[3 * par + 2] ? 1 : 0);
+    };
+    const auto& mk = H.mask;
+    std::vector<std::vector<int2>> m2m(size_t(H.nlev) * 8), l2l(size_t(H.nlev) * 8);
+    for (int l = 0; l < H.nlev; ++l)
+      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
+        const int b = V.level_boxes[i];
+        if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES) &&
+            (mk[b] & QBXG_SHARD_SUBTREE))
+          for (int k = V.child_starts[b]; k < V.child_starts[b + 1]; ++k) {
+            const int c = V.children[k];
+            if (V.src_sub_count[c] > 0) m2m[size_t(l) * 8 + hoct(c, b)].push_back(make_int2(c, b));
+          }
+        if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) && (mk[b] & QBXG_SHARD_DOWN)) {
+          const int a = V.box_parent[b];
+          l2l[size_t(l) * 8 + hoct(b, a)].push_back(make_int2(a, b));
+        }
+      }
+    std::vector<int2> pm, pl;
+    H.h_m2m_off.assign(size_t(H.nlev) * 8 + 1, 0);
+    H.h_l2l_off.assign(size_t(H.nlev) * 8 + 1, 0);
+    for (size_t g = 0; g < m2m.size(); ++g) {
+      pm.insert(pm.end(), m2m[g].begin(), m2m[g].end());
+      H.h_m2m_off[g + 1] = int(pm.size());
+      pl.insert(pl.end(), l2l[g].begin(), l2l[g].end());
+      H.h_l2l_off[g + 1] = int(pl.size());
+    }
+    H.h_m2m_pairs = dupload(O, pm, s);
+    H.h_l2l_pairs = dupload(O, pl, s);
+    QCK(cudaStreamSynchronize(s));
+  }
 
   // M2L operators per (level, offset slot) in use: t = c_b - c_d = 2 h_l delta
   const int64_t nent = vs[nb];
@@ -755,7 +797,16 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   QCK(cudaEventRecord(ev[1], s));
   chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
-  for (int l = H.nlev - 2; l >= 0; --l) chk(dev::helm_shift(HD, 0, H.d_m2m_level[l], H.n_m2m_level[l], H.h_ops_m2m[l], s));
+  for (int l = H.nlev - 2; l >= 0; --l) {
+    if (!H.h_shift_batched) {
+      chk(dev::helm_shift(HD, 0, H.d_m2m_level[l], H.n_m2m_level[l], H.h_ops_m2m[l], s));
+      continue;
+    }
+    for (int o = 0; o < 8; ++o) {  // octants in a fixed order: deterministic sums into the parents
+      const int a = H.h_m2m_off[size_t(l) * 8 + o], e = H.h_m2m_off[size_t(l) * 8 + o + 1];
+      chk(dev::helm_shift_pairs(HD, 0, H.h_m2m_pairs + a, e - a, H.h_ops_m2m[l] + size_t(o) * HD.KP * HD.KP, s));
+    }
+  }
   QCK(cudaEventRecord(ev[3], s));
   chk(dev::helm_near(HD, H.d_near_boxes, H.n_ctr_boxes, s));
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
@@ -775,7 +826,16 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::helm_p2l(HD, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));
-  for (int l = 1; l < H.nlev; ++l) chk(dev::helm_shift(HD, 1, H.d_l2l_level[l], H.n_l2l_level[l], H.h_ops_l2l[l], s));
+  for (int l = 1; l < H.nlev; ++l) {
+    if (!H.h_shift_batched) {
+      chk(dev::helm_shift(HD, 1, H.d_l2l_level[l], H.n_l2l_level[l], H.h_ops_l2l[l], s));
+      continue;
+    }
+    for (int o = 0; o < 8; ++o) {
+      const int a = H.h_l2l_off[size_t(l) * 8 + o], e = H.h_l2l_off[size_t(l) * 8 + o + 1];
+      chk(dev::helm_shift_pairs(HD, 1, H.h_l2l_pairs + a, e - a, H.h_ops_l2l[l] + size_t(o) * HD.KP * HD.KP, s));
+    }
+  }
   QCK(cudaEventRecord(H.evx[3], s));
   chk(dev::helm_ctr(HD, 1, HD.M, H.h_n_wctas, H.h_wctas, H.h_wctr, H.h_wrow, H.h_wrows, 0, s));
   chk(dev::helm_pair_reduce(HD, H.h_wcentres, H.h_wstarts, H.h_n_wcentres, H.h_wrows, s));

@@ -52,6 +52,9 @@ int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w,
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s);
 int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s);
 int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2* ops, cudaStream_t s);
+// M2M (mode 0: M[dst] += T M[src]) / L2L (mode 1: L[dst] += T L[src]) over (src, dst)
+// pairs that share one (level, octant) operator, 8 pairs per CTA
+int helm_shift_pairs(const HelmData& H, int mode, const int2* pairs, int n, const double2* ops, cudaStream_t s);
 int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
              const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s);
 int helm_m2l_cols();

@@ -289,6 +289,41 @@ __global__ void __launch_bounds__(512) k_h_shift(HelmData H, int mode, const int
   }
 }
 
+// M2M / L2L batched by (level, octant): one CTA applies the level's octant operator to
+// NB (source box, destination box) pairs, so each operator element read from L2 feeds NB
+// complex multiply-adds instead of one (k_h_shift streams the 3 MB operator per box).
+// dst += T src, thread per output row; each destination appears once per launch and the
+// octant launches run in a fixed order, so the sums are deterministic.
+template <int NB>
+__global__ void __launch_bounds__(512) k_h_shift_b(HelmData H, int mode, const int2* __restrict__ pairs, int n,
+                                                   const double2* __restrict__ T) {
+  extern __shared__ double2 smb[];  // NB x KP
+  const int KP = H.KP, i = threadIdx.x, p0 = blockIdx.x * NB;
+  const int np = min(NB, n - p0);
+  double2* Xs = mode == 0 ? H.M : H.L;
+  for (int e = threadIdx.x; e < NB * KP; e += blockDim.x) {
+    const int j = e / KP, q = e - j * KP;
+    smb[e] = j < np ? Xs[size_t(pairs[p0 + j].x) * KP + q] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  if (i >= KP) return;
+  double2 acc[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) acc[j] = make_double2(0.0, 0.0);
+  for (int k2 = 0; k2 < KP; ++k2) {
+    const double2 a = __ldg(T + size_t(k2) * KP + i);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = cfma(a, smb[j * KP + k2], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+    if (j < np) {
+      double2* d = Xs + size_t(pairs[p0 + j].y) * KP + i;
+      const double2 v = *d;
+      *d = make_double2(v.x + acc[j].x, v.y + acc[j].y);
+    }
+}
+
 // operator builder, one CTA per operator: T[k][i] = 4 pi sum_l i^{n'+l-n} G F_l^{m-m'}(t)
 __global__ void __launch_bounds__(256) k_h_build_ops(HelmData H, const double4* __restrict__ shifts,
                                                      double2* __restrict__ ops) {
@@ -1290,6 +1325,19 @@ int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const doubl
   if (n == 0) return 0;
   const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
   k_h_shift<<<n, th, H.KP * sizeof(double2), s>>>(H, mode, boxes, ops);
+  return 1;
+}
+
+int helm_shift_pairs(const HelmData& H, int mode, const int2* pairs, int n, const double2* ops, cudaStream_t s) {
+  if (n == 0) return 0;
+  constexpr int NB = 8;  // 16 measured slower (fewer CTAs per SM)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_h_shift_b<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
+  k_h_shift_b<NB><<<(n + NB - 1) / NB, th, size_t(NB) * H.KP * sizeof(double2), s>>>(H, mode, pairs, n, ops);
   return 1;
 }
 

@@ -83,7 +83,7 @@ print(json.dumps({"helm": float(np.linalg.norm(pot - ref) / np.linalg.norm(ref))
 """ % ROOT
 
 
-@pytest.mark.parametrize("mode", ["full", "split", "p2l-cta"])
+@pytest.mark.parametrize("mode", ["full", "split", "p2l-cta", "shift-box"])
 def test_helmholtz_m2l_variant(mode):
     """QBXG_HELM_M2L=full (dense per-offset operators) and =split (even / odd dense
     blocks) against the oracle; the default point-and-shoot M2L is covered by
@@ -91,6 +91,8 @@ def test_helmholtz_m2l_variant(mode):
     full = dict(os.environ)
     if mode == "p2l-cta":
         full["QBXG_HELM_P2L"] = "cta"  # one CTA-wide wave table per source in P2L
+    elif mode == "shift-box":
+        full["QBXG_HELM_SHIFT"] = "box"  # M2M / L2L one box per CTA
     else:
         full["QBXG_HELM_M2L"] = mode
     r = subprocess.run([sys.executable, "-c", HELM_SCRIPT], env=full, capture_output=True, text=True, timeout=600)
