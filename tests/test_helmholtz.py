@@ -153,3 +153,26 @@ def test_helmholtz_handle_rejects_real_apply():
     g = api.config_geometry(0)
     with pytest.raises(ValueError, match="wavenumber"):
         api.Plan(api.FmmConfig(p_fmm=6, p_qbx=3, kernel=2, helmholtz_k=0.0), g)
+
+
+@pytest.mark.gpu
+def test_gpu_helmholtz_p20_matches_oracle_fixture():
+    """BASELINE config 3's orders (p = 20, q = 5, k = 3: the point-and-shoot M2L at its largest
+    blocks) against the oracle, via tests/golden/oracle_helm_p20.npz (the oracle needs minutes at
+    p = 20; tests/golden/make_helm_p20.py regenerates it).  Same procedural inputs and plan,
+    checked by the list hashes."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    import make_helm_p20 as M
+    fx = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_helm_p20.npz"))
+    g, w, cfg = M.inputs()
+    assert np.array_equal(w, fx["weights"])
+    plan = api.Plan(cfg, g)
+    hashes = np.array([plan.list_hashes()[k] for k in sorted(plan.list_hashes())], dtype=np.uint64)
+    assert np.array_equal(hashes, fx["list_hashes"])
+    eng = api.FmmEngine(cfg, g, plan)
+    pot, cc = eng.apply_complex(w, want_centers=True)
+    eng.close()
+    assert np.linalg.norm(pot - fx["pot"]) / np.linalg.norm(fx["pot"]) <= 1e-11
+    assert np.linalg.norm(cc[:64] - fx["centres"]) / np.linalg.norm(fx["centres"]) <= 1e-11
