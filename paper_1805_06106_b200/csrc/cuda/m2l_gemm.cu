@@ -782,7 +782,10 @@ int split_nhi(int p, int NH) {  // Im block rows: whole warps of 8 * MT rows (MT
   const int rows = 8 * (NH / 48), ni = hsize(p) - (p + 1);
   return (ni + rows - 1) / rows * rows;
 }
-int split_tile_cols() { return std::getenv("QBXG_SPLIT_V1") != nullptr ? 32 : kSplitBN; }
+int split_tile_cols() {
+  const char* v1 = std::getenv("QBXG_SPLIT_V1");
+  return v1 != nullptr ? 32 : kSplitBN;
+}
 
 int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s) {
   const size_t smem = hsize(2 * p) * sizeof(double2);
