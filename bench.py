@@ -148,13 +148,38 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- CPU legs (oracle)
-def cpu_oracle_throughput(steps: int, warmup: int):
-    """The CPU restatement of the path (oracle/) on a bounded sample of the workload."""
+def host_info():
+    """nproc and the lscpu model name of the host the CPU legs run on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def workload_config(g, n_boxes, world, small=False):
+    return {"workload": "BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
+                        "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9" if not small else "debug: torus 64x32",
+            "n_sources": g.n_sources, "n_targets": g.n_targets, "n_centers": g.n_centers, "n_boxes": n_boxes,
+            "parallelism": f"morton-shard x{world} (NCCL multipole broadcast)" if world > 1 else "single GPU",
+            "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"}
+
+
+def cpu_oracle_throughput(steps: int, warmup: int, full: bool = False):
+    """The CPU restatement of the path (oracle/, OpenMP over all host threads) on the
+    full config-1 workload (full=True: the reference arm) or on a bounded 1/16 sample
+    of it (the cpu_baseline field of the GPU line)."""
     import oracle as O
     from paper_1805_06106_b200 import api
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    g = api.config_geometry(CONFIG_ID, **CPU_SAMPLE)
+    over = {} if full else CPU_SAMPLE
+    g = api.config_geometry(CONFIG_ID, **over)
     cfg = api.config_fmm(CONFIG_ID)
     plan = api.Plan(cfg, g)
     w, mu = g.weights(), g.dipoles()
@@ -167,26 +192,32 @@ def cpu_oracle_throughput(steps: int, warmup: int):
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
     units = g.n_sources + g.n_targets
+    what = ("full BASELINE config 1" if full else f"torus {CPU_SAMPLE['nu']}x{CPU_SAMPLE['nv']} cells, 1/16 of config 1")
     return dict(value=units / t, unit="points/s", cores=cores, kind="port",
-                sample=f"torus {CPU_SAMPLE['nu']}x{CPU_SAMPLE['nv']} cells ({g.n_sources} sources + {g.n_targets} "
-                       f"targets), p=15 q=5 SL+DL, oracle/ OpenMP restatement of Stages 2-9, mean of {steps} "
-                       f"after {warmup} warm-up", seconds_per_step=t)
+                sample=f"{what} ({g.n_sources} sources + {g.n_targets} targets), p=15 q=5 SL+DL, oracle/ OpenMP "
+                       f"restatement of Stages 2-9 on the same host plan, mean of {steps} after {warmup} warm-up",
+                seconds_per_step=t, g=g, n_boxes=plan.view.n_boxes, host=host_info())
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU path timed on the box's host cores on the SAME workload
+    as the GPU arm (full config 1; one oracle apply takes minutes, so at most 1 warm-up
+    and 2 timed steps regardless of --steps / --warmup).  Under torchrun only rank 0 runs."""
     if rank != 0:
         return 0
-    steps, warm = max(1, min(args.steps, 2)), 0
-    cb = cpu_oracle_throughput(steps, warm)
+    steps, warm = max(1, min(args.steps, 2)), min(max(args.warmup, 0), 1)
+    cb = cpu_oracle_throughput(steps, warm, full=not args.small)
+    cfgd = workload_config(cb["g"], cb["n_boxes"], world, args.small)
     line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": cb["value"],
             "unit": "points/s", "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
             "ms_per_step": cb["seconds_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (procedural torus, seeded density)",
-            "config": {"workload": "BASELINE config 1 family (torus SL+DL, p=15, q=5), bounded CPU sample",
-                       "sample": cb["sample"]},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (procedural torus, seeded Fourier density)",
+            "config": cfgd,
             "cpu_baseline": {"value": cb["value"], "unit": "points/s", "cores": cb["cores"], "kind": "port",
-                             "sample": cb["sample"]},
-            "e2e": {"value": cb["value"], "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": cb["sample"], **cb["host"]},
+            "e2e": {"value": cb["value"], "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": ("steps/warm-up capped at 2/1: one CPU apply of the full workload takes minutes; the reference "
+                     "ships no FMM code (SURVEY.md §0), so the CPU path is the oracle restatement (kind: port)")}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -385,7 +416,7 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_oracle_throughput(1, 0)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {**{k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}, **cb["host"]}
 
     # BASELINE config 3 (Helmholtz single layer, k = 3, p = 20, q = 5) on the same GPU:
     # side measurement, CUDA events, inputs on the host (qbxg_apply_complex)
@@ -453,12 +484,7 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (procedural torus, seeded Fourier density)",
-                "config": {"workload": "BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
-                                       "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9" if not args.small
-                           else "debug: torus 64x32", "n_sources": g.n_sources, "n_targets": g.n_targets,
-                           "n_centers": g.n_centers, "n_boxes": plan.view.n_boxes,
-                           "parallelism": f"morton-shard x{world} (NCCL multipole broadcast)" if world > 1 else "single GPU",
-                           "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"},
+                "config": workload_config(g, plan.view.n_boxes, world, args.small),
                 "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
                 "batch": batch, "helmholtz": helm, "association": assoc,

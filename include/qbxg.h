@@ -229,6 +229,14 @@ int qbxg_plan_view_get(const qbxg_plan* plan, qbxg_plan_view* out);
 int qbxg_plan_create_gpu(const qbxg_config* cfg, const qbxg_geometry* geom, int32_t gpu_lists, qbxg_plan** out);
 int qbxg_plan_ledger(const qbxg_plan* plan, qbxg_ledger* out);
 void qbxg_plan_destroy(qbxg_plan* plan);
+/* SPEC.md:370-378 adequately_separated(kind, a, b, t_f), the relation the list
+ * builder uses: kind 0 = box_vs_tcr (a < TCR(b): l2 distance from centre(a) to the
+ * boundary of the ball of radius sqrt(3)|b|(1+t_f) about centre(b) >= 3|a|),
+ * kind 1 = tcr_vs_box (TCR(a) < b: l-inf distance from centre(a) to the boundary
+ * of b >= 3|a|(1+t_f)).  ca/cb: box centres (3 doubles), ha/hb: half widths |a|, |b|.
+ * *out = 1 when separated.  Pure host function, no device needed. */
+int qbxg_adequately_separated(int32_t kind, const double* ca, double ha, const double* cb, double hb, double t_f,
+                              int32_t* out);
 
 /* ---- device evaluation (Stages 2-9 on one B200) ------------------------ */
 typedef struct qbxg_handle qbxg_handle;

@@ -47,6 +47,8 @@ def lib():
                                    _dp, _dp, _dp]
         L.qbxo_direct_qbx.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _i32p, C.c_int,
                                       _dp]
+        L.qbxo_adequately_separated.argtypes = [C.c_int, _dp, C.c_double, _dp, C.c_double, C.c_double]
+        L.qbxo_adequately_separated.restype = C.c_int
         L.qbxo_helm_last_error.restype = C.c_char_p
         L.qbxo_helm_ylm.argtypes = [C.c_int, C.c_int, _dp, _dp]
         L.qbxo_helm_bessel.argtypes = [C.c_int, C.c_double, _dp, _dp]
@@ -366,3 +368,10 @@ def area_query(plan, centers, radii):
     lib().oracle_area_query(*args, cnt.ctypes.data_as(_i64p), starts.ctypes.data_as(_i64p),
                             leaves.ctypes.data_as(_i32p))
     return starts, leaves[:int(starts[-1])]
+
+
+def adequately_separated(kind: int, ca, ha: float, cb, hb: float, tf: float) -> bool:
+    """Oracle restatement of SPEC.md:370-378 (kind 0 box_vs_tcr, 1 tcr_vs_box)."""
+    a = np.ascontiguousarray(ca, dtype=np.float64)
+    b = np.ascontiguousarray(cb, dtype=np.float64)
+    return bool(lib().qbxo_adequately_separated(kind, a.ctypes.data_as(_dp), ha, b.ctypes.data_as(_dp), hb, tf))

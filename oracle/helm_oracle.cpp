@@ -194,8 +194,18 @@ struct Gaunt {
     }
     pb.resize(ng);
     for (int i = 0; i < ng; ++i) pbar_table(2 * P, x[i], pb[i]);
+    // memo of every value (the same quadrature sum, evaluated once): (P+1)^4 x (2P+1)
+    const int K = nf(P);
+    tab.assign(size_t(K) * K * (2 * P + 1), 0.0);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int a = 0; a < K; ++a) {
+      const int n = int(std::sqrt(double(a))), m = a - n * n - n;
+      for (int n2 = 0; n2 <= P; ++n2)
+        for (int m2 = -n2; m2 <= n2; ++m2)
+          for (int l = 0; l <= 2 * P; ++l) tab[(size_t(a) * K + ix(n2, m2)) * (2 * P + 1) + l] = quad(n, m, n2, m2, l);
+    }
   }
-  double operator()(int n, int m, int n2, int m2, int l) const {
+  double quad(int n, int m, int n2, int m2, int l) const {
     const int mu = m - m2;
     if (std::abs(m) > n || std::abs(m2) > n2 || std::abs(mu) > l) return 0.0;
     if ((n + n2 + l) & 1) return 0.0;
@@ -204,6 +214,12 @@ struct Gaunt {
       s += w[i] * pb[i][ix(n, std::abs(m))] * pb[i][ix(n2, std::abs(m2))] * pb[i][ix(l, std::abs(mu))];
     return 2.0 * kPi * s;
   }
+  double operator()(int n, int m, int n2, int m2, int l) const {
+    if (n > P || n2 > P || l > 2 * P || l < 0) return quad(n, m, n2, m2, l);
+    if (std::abs(m) > n || std::abs(m2) > n2) return 0.0;
+    return tab[(size_t(ix(n, m)) * nf(P) + ix(n2, m2)) * (2 * P + 1) + l];
+  }
+  std::vector<double> tab;
 };
 Gaunt g_gaunt;
 

@@ -4,19 +4,36 @@
 // interaction lists (Definitions 1-8) over all box pairs,
 // O(N_B^2 * depth).  SPEC.md:386 and 398 require the production lists to equal
 // this on small trees ("lists vs brute-force definitions on depth<=4 trees").
-// It shares only the floating-point predicates (paper_1805_06106_b200/csrc/
-// host/predicates.hpp) with the production builder -- the separation relation
-// must be evaluated with the same expression for bit-exact agreement -- and
-// derives box integer coordinates independently from box centres.
+// It shares nothing with the production builder: the two separation relations
+// are restated below from SPEC.md:370-378 (and checked against its worked examples
+// and against the product's predicates in tests/test_predicates.py), and box
+// integer coordinates are derived independently from box centres.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <vector>
 
-#include "predicates.hpp"
 #include "qbxg.h"
 
 namespace {
+
+// SPEC.md:373 box_vs_tcr: the l2 distance from centre(a) to the boundary of
+// TCR(b) -- the ball of radius sqrt(3)|b|(1 + t_f) about centre(b)
+// -- is at least 3|a|.  A centre inside the ball has no such distance (false).
+bool oracle_box_vs_tcr(const double* ca, double ha, const double* cb, double hb, double tf) {
+  double d2 = 0.0;
+  for (int k = 0; k < 3; ++k) d2 += (ca[k] - cb[k]) * (ca[k] - cb[k]);
+  const double tcr_radius = std::sqrt(3.0) * hb * (1.0 + tf);
+  return std::sqrt(d2) - tcr_radius >= 3.0 * ha;
+}
+
+// SPEC.md:373 tcr_vs_box: the l-inf distance from centre(a) to the boundary of box b
+// is at least 3|a|(1 + t_f).
+bool oracle_tcr_vs_box(const double* ca, double ha, const double* cb, double hb, double tf) {
+  double dinf = 0.0;
+  for (int k = 0; k < 3; ++k) dinf = std::max(dinf, std::fabs(ca[k] - cb[k]));
+  return dinf - hb >= 3.0 * ha * (1.0 + tf);
+}
 
 struct Boxes {
   const qbxg_plan_view* V;
@@ -40,7 +57,16 @@ struct Boxes {
   bool is_anc(int a, int b) const {  // a strict ancestor of b
     return std::find(anc[b].begin(), anc[b].end(), a) != anc[b].end();
   }
-  bool adjacent(int a, int b) const { return qbxg::boxes_adjacent(&ic[3 * a], V->box_level[a], &ic[3 * b], V->box_level[b]); }
+  // closed boxes touch or overlap: compare the integer extents on the finer level's grid
+  bool adjacent(int a, int b) const {
+    const int la = V->box_level[a], lb = V->box_level[b], L = std::max(la, lb);
+    for (int k = 0; k < 3; ++k) {
+      const int64_t sa = int64_t(1) << (L - la), sb = int64_t(1) << (L - lb);
+      const int64_t a0 = ic[3 * a + k] * sa, a1 = a0 + sa, b0 = ic[3 * b + k] * sb, b1 = b0 + sb;
+      if (a1 < b0 || b1 < a0) return false;
+    }
+    return true;
+  }
   bool colleague2(int a, int b) const {  // same level, inside the 2-near neighbourhood
     if (V->box_level[a] != V->box_level[b]) return false;
     for (int d = 0; d < 3; ++d)
@@ -121,14 +147,14 @@ int qbxo_lists_brute(const qbxg_plan_view* V, double tf, int32_t demote, int64_t
     std::vector<int> far, close;
     for (int d = 0; d < nb; ++d) {
       if (!B.has_src(d) || !in_D(d)) continue;
-      const bool sep = qbxg::sep_box_tcr(ctr(d), h(d), ctr(b), h(b), tf);
+      const bool sep = oracle_box_vs_tcr(ctr(d), h(d), ctr(b), h(b), tf);
       if (!sep) {
         if (B.src_leaf(d)) close.push_back(d);
         continue;
       }
       bool ok = true;
       for (int w : B.anc[d])
-        if (in_D(w) && qbxg::sep_box_tcr(ctr(w), h(w), ctr(b), h(b), tf)) ok = false;
+        if (in_D(w) && oracle_box_vs_tcr(ctr(w), h(w), ctr(b), h(b), tf)) ok = false;
       if (ok) far.push_back(d);
     }
     // Remark 1 demotion, applied identically to the production builder's rule
@@ -149,7 +175,7 @@ int qbxo_lists_brute(const qbxg_plan_view* V, double tf, int32_t demote, int64_t
     for (int w = 0; w < nb; ++w) {
       if (!(w == b || B.is_anc(w, b))) continue;
       for (int d : L4[w])
-        if (!qbxg::sep_tcr_box(ctr(b), h(b), ctr(d), h(d), tf)) xc.push_back(d);
+        if (!oracle_tcr_vs_box(ctr(b), h(b), ctr(d), h(d), tf)) xc.push_back(d);
     }
     rows[QBXG_LIST_X_CLOSE][b] = xc;
   }
@@ -157,11 +183,11 @@ int qbxo_lists_brute(const qbxg_plan_view* V, double tf, int32_t demote, int64_t
     if (!B.target_or_anc(b)) continue;
     std::vector<int> xf;
     for (int d : L4[b])
-      if (qbxg::sep_tcr_box(ctr(b), h(b), ctr(d), h(d), tf)) xf.push_back(d);
+      if (oracle_tcr_vs_box(ctr(b), h(b), ctr(d), h(d), tf)) xf.push_back(d);
     const int pb = V->box_parent[b];
     if (pb >= 0)
       for (int d : rows[QBXG_LIST_X_CLOSE][pb])
-        if (qbxg::sep_tcr_box(ctr(b), h(b), ctr(d), h(d), tf)) xf.push_back(d);
+        if (oracle_tcr_vs_box(ctr(b), h(b), ctr(d), h(d), tf)) xf.push_back(d);
     rows[QBXG_LIST_X_FAR][b] = xf;
   }
   for (int k = 0; k < 6; ++k) {
@@ -182,3 +208,8 @@ int qbxo_lists_brute(const qbxg_plan_view* V, double tf, int32_t demote, int64_t
 }
 
 }  // extern "C"
+
+extern "C" int qbxo_adequately_separated(int kind, const double* ca, double ha, const double* cb, double hb,
+                                         double tf) {
+  return kind == 0 ? oracle_box_vs_tcr(ca, ha, cb, hb, tf) : oracle_tcr_vs_box(ca, ha, cb, hb, tf);
+}

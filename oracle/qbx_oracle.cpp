@@ -250,9 +250,20 @@ void m2l(const std::vector<cd>& M, int P, const double* c, double h, const doubl
   for (int n = 0; n <= Q; ++n) {
     const double s = std::pow(H / h, n) / h;
     for (int m = -n; m <= n; ++m) {
-      cd acc = 0;
-      for (int j = 0; j <= P; ++j)
-        for (int k = -j; k <= j; ++k) acc += M[idx(j, k)] * at(I, P + Q, j + n, k - m);
+      // |k - m| <= j + n always, so every I_{j+n}^{k-m} exists: the k-row of M and the
+      // shifted row of I are contiguous in the packed table (interleaved re, im)
+      double ar = 0.0, ai = 0.0;
+      for (int j = 0; j <= P; ++j) {
+        const double* Mj = reinterpret_cast<const double*>(&M[idx(j, 0)]);
+        const double* Ij = reinterpret_cast<const double*>(&I[idx(j + n, -m)]);
+#pragma omp simd reduction(+ : ar, ai)
+        for (int k = -j; k <= j; ++k) {
+          const double mr = Mj[2 * k], mi = Mj[2 * k + 1], ir = Ij[2 * k], ii = Ij[2 * k + 1];
+          ar += mr * ir - mi * ii;
+          ai += mr * ii + mi * ir;
+        }
+      }
+      const cd acc(ar, ai);
       L[idx(n, m)] += s * (((n + m) & 1) ? -1.0 : 1.0) * acc;
     }
   }

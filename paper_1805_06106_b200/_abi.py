@@ -98,7 +98,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
     "qbxg_direct_qbx", "qbxg_apply_batch", "qbxg_apply_batch_device", "qbxg_set_overlap", "qbxg_helm_direct_sum", "qbxg_helm_direct_qbx",
     "qbxg_apply_complex", "qbxg_locator_create", "qbxg_associate_targets", "qbxg_associate_targets_device",
-    "qbxg_area_query", "qbxg_locator_destroy", "qbxg_plan_create_gpu",
+    "qbxg_area_query", "qbxg_locator_destroy", "qbxg_plan_create_gpu", "qbxg_adequately_separated",
 )
 
 SHARD_OWN, SHARD_SUBTREE, SHARD_STRADDLE, SHARD_DOWN = 1, 2, 4, 8
@@ -149,6 +149,7 @@ def _declare(lib):
                                           C.c_int),
         "qbxg_area_query": ([C.c_void_p, C.c_int64, _dp, _dp, _i64p, _i32p, C.c_int64], C.c_int),
         "qbxg_locator_destroy": ([C.c_void_p], None),
+        "qbxg_adequately_separated": ([C.c_int32, _dp, C.c_double, _dp, C.c_double, C.c_double, _i32p], C.c_int),
     }
     for name, (args, res) in sig.items():
         if not hasattr(lib, name):

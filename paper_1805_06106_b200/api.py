@@ -417,6 +417,14 @@ class FmmEngine:
     def apply(self, weights, dipoles=None, want_centers=False):
         w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
         m = None if dipoles is None else np.ascontiguousarray(dipoles, dtype=np.float64).reshape(-1)
+        ns = self.geom.n_sources
+        # SourceEnsemble::validate (kernels.cpp:27-38): sizes are checked before any copy
+        if w.size != ns:
+            raise ValueError(f"apply: {w.size} weights for {ns} sources")
+        if m is not None and m.size != 3 * ns:
+            raise ValueError(f"apply: {m.size // 3} dipole moments for {ns} sources")
+        if m is None and self.cfg.kernel == _abi.KERNEL_LAPLACE_SL_DL:
+            raise ValueError("apply: Laplace SL+DL requires dipole moments")
         pot = np.empty(self.geom.n_targets, dtype=np.float64)
         coeffs = np.empty(self.geom.n_centers * 2 * self.cfg.kq, dtype=np.float64) if want_centers else None
         _check(_abi.lib().qbxg_apply(self.handle, _ptr(w), _ptr(m), _ptr(pot), _ptr(coeffs), C.byref(self.timings)))
@@ -509,6 +517,18 @@ def execute(geom: Geometry, weights, dipoles, cfg: FmmConfig, want_centers=False
     finally:
         eng.close()
     return out, plan.ledger()
+
+
+def adequately_separated(kind: str, a_center, a_half: float, b_center, b_half: float, t_f: float) -> bool:
+    """SPEC.md:370-378 adequately_separated: kind "box_vs_tcr" (a < TCR(b)) or
+    "tcr_vs_box" (TCR(a) < b); the predicate the host list builder uses."""
+    k = {"box_vs_tcr": 0, "tcr_vs_box": 1}[kind]
+    ca = np.ascontiguousarray(a_center, dtype=np.float64)
+    cb = np.ascontiguousarray(b_center, dtype=np.float64)
+    out = C.c_int32()
+    _check(_abi.lib().qbxg_adequately_separated(k, _ptr(ca), float(a_half), _ptr(cb), float(b_half), float(t_f),
+                                                C.byref(out)))
+    return bool(out.value)
 
 
 def direct_sum(sources: SourceEnsemble, targets: TargetSet) -> np.ndarray:

@@ -144,6 +144,7 @@ struct Handle {
   double* d_coeffs = nullptr;
   dev::M2LPlan m2l;
   int last_launches = 0;
+  unsigned int* h_bad = nullptr;  // pinned copy of D.bad, read after every apply
   // Helmholtz single layer (cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL): helm_setup / run_helm
   bool helm = false;
   dev::HelmData HD{};
@@ -194,6 +195,7 @@ struct Handle {
   double4* d_bmu = nullptr;      // bnr x ns sorted dipoles
   double2* d_bLc = nullptr;      // bnr x nc x kq centre locals (near part, then completed in place)
   int64_t bhost_cap = 0;         // densities the host staging below can hold
+  int64_t bcoeff_cap = 0;        // densities d_bcoeffs can hold
   double *d_bw_in = nullptr, *d_bmu_in = nullptr, *d_bpot = nullptr, *d_bcoeffs = nullptr;
 
   ~Handle() {
@@ -206,6 +208,7 @@ struct Handle {
       }
     }
     for (void* p : owned) cudaFree(p);
+    if (h_bad) cudaFreeHost(h_bad);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -502,6 +505,7 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.ctr = D.ctr;
   HD.tgt = D.tgt;
   HD.near_starts = D.near_starts;
+  HD.bad = D.bad;
   HD.near_seg = D.near_seg;
   HD.xfar_starts = D.xfar_starts;
   HD.xfar_seg = D.xfar_seg;
@@ -794,6 +798,7 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
   QCK(cudaMemsetAsync(HD.M, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
   QCK(cudaMemsetAsync(HD.L, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
   QCK(cudaMemsetAsync(HD.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double2), s));
+  QCK(cudaMemsetAsync(HD.bad, 0, sizeof(unsigned int), s));
   QCK(cudaEventRecord(ev[1], s));
   chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
@@ -970,6 +975,9 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   D.L = dalloc<double2>(O, size_t(nb) * D.kp);
   D.Lc = dalloc<double2>(O, size_t(H.nc) * D.kq);
   D.phi = dalloc<double>(O, H.nconv);
+  D.bad = dalloc<unsigned int>(O, 1);
+  QCK(cudaMemsetAsync(D.bad, 0, sizeof(unsigned int), s));
+  QCK(cudaMallocHost(&H.h_bad, sizeof(unsigned int)));
 
   // --- lists
   auto lrow = [&](int k, int b, int64_t& a, int64_t& e) {
@@ -1337,6 +1345,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
   QCK(cudaMemsetAsync(D.L, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
   QCK(cudaMemsetAsync(D.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double), s));
+  QCK(cudaMemsetAsync(D.bad, 0, sizeof(unsigned int), s));
   QCK(cudaEventRecord(ev[1], s));
   chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
@@ -1446,6 +1455,36 @@ void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
       nck(n.AllReduce(d_coeffs, d_coeffs, size_t(H.nc) * 2 * H.D.kq, ncclFloat64, ncclSum, comm, s),
           "ncclAllReduce(centre coefficients)");
   }
+}
+
+// Reference error semantics inside the apply (kernels.cpp:58-71): Stage 9
+// flags any non-finite potential or centre coefficient; on the error path the near
+// lists are scanned for the coincident (centre | target, source) pair, which is named
+// the way the reference's direct_sum names it.  Costs one 4-byte read per apply.
+void check_domain(Handle& H, cudaStream_t s) {
+  dev::DevData& D = H.D;
+  QCK(cudaMemcpyAsync(H.h_bad, D.bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+  QCK(cudaStreamSynchronize(s));
+  if (*H.h_bad == 0) return;
+  const unsigned kind = *H.h_bad;
+  QCK(cudaMemsetAsync(D.bad, 0, sizeof(unsigned int), s));
+  unsigned long long* d_key = dalloc<unsigned long long>(H.owned, 1);
+  QCK(cudaMemsetAsync(d_key, 0xff, sizeof(unsigned long long), s));
+  dev::launch_find_coincident(D, int(H.nc), H.d_ctr_box, H.d_ctr_perm, int(H.nconv), H.d_tgt_box, H.d_tgt_perm,
+                              H.d_src_perm, d_key, s);
+  unsigned long long key = 0;
+  QCK(cudaMemcpyAsync(&key, d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  QCK(cudaStreamSynchronize(s));
+  cudaFree(d_key);
+  H.owned.erase(std::find(H.owned.begin(), H.owned.end(), static_cast<void*>(d_key)));
+  if (key != ~0ull) {
+    const bool ctr = (key >> 62) == 0;
+    const long long id = (long long)((key >> 31) & 0x7fffffffull), src = (long long)(key & 0x7fffffffull);
+    throw DomainError(std::string("qbxg_apply: ") + (ctr ? "QBX center " : "target ") + std::to_string(id) +
+                      " coincides with source " + std::to_string(src));
+  }
+  throw DomainError(std::string("qbxg_apply: non-finite ") + ((kind & 1) ? "potential" : "center coefficient") +
+                    " (no coincident near-field pair: overflow or non-finite input)");
 }
 
 // R densities (rhs-major device arrays).  Densities go through the near field NR
@@ -1599,6 +1638,7 @@ int qbxg_apply_device(qbxg_handle* hp, const double* d_weights, const double* d_
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
     qbxg::full_apply(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s);
     qbxg::fill_timings(H, timings, false, 0, 0);
+    qbxg::check_domain(H, s);
   });
 }
 
@@ -1624,10 +1664,12 @@ int qbxg_apply_phase(qbxg_handle* hp, int32_t phase, const double* d_weights, co
     if (phase == 1 && !d_weights) throw qbxg::InvalidArgument("qbxg_apply_phase: null weights");
     if (phase == 2 && !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_phase: null output");
     auto& H = hp->h;
+    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply_phase: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
     qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, phase);
     QCK(cudaStreamSynchronize(s));
+    if (phase == 2) qbxg::check_domain(H, s);
   });
 }
 
@@ -1709,6 +1751,7 @@ int qbxg_apply(qbxg_handle* hp, const double* weights, const double* dipoles, do
     QCK(cudaEventRecord(H.ev[12], s));
     qbxg::fill_timings(H, timings, true, h2d, d2h);
     QCK(cudaStreamSynchronize(s));
+    qbxg::check_domain(H, s);
   });
 }
 
@@ -1719,6 +1762,7 @@ int qbxg_apply_batch_device(qbxg_handle* hp, int32_t n_rhs, const double* d_weig
     if (!hp || !d_weights || !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_batch_device: null argument");
     if (n_rhs < 1) throw qbxg::InvalidArgument("qbxg_apply_batch_device: n_rhs must be >= 1");
     auto& H = hp->h;
+    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply_batch_device: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     if (H.D.dipole && !d_dipoles) throw qbxg::InvalidArgument("qbxg_apply_batch: Laplace SL+DL requires dipole moments");
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
@@ -1733,6 +1777,7 @@ int qbxg_apply_batch_device(qbxg_handle* hp, int32_t n_rhs, const double* d_weig
       timings->ms[QBXG_T_TOTAL] = ms;
       timings->kernel_launches = H.last_launches;
     }
+    qbxg::check_domain(H, s);
   });
 }
 
@@ -1742,20 +1787,33 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
     if (!hp || !weights || !out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_batch: null argument");
     if (n_rhs < 1) throw qbxg::InvalidArgument("qbxg_apply_batch: n_rhs must be >= 1");
     auto& H = hp->h;
+    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply_batch: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     const bool dip = H.D.dipole;
     if (dip && !dipoles) throw qbxg::InvalidArgument("qbxg_apply_batch: Laplace SL+DL requires dipole moments");
     cudaStream_t s = H.stream;
-    if (H.bhost_cap < n_rhs) {  // host-path staging grows to the largest batch seen
-      H.d_bw_in = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * H.ns);
-      H.d_bmu_in = dip ? qbxg::dalloc<double>(H.owned, size_t(n_rhs) * 3 * H.ns) : nullptr;
-      H.d_bpot = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * std::max<int64_t>(H.nt, 1));
-      H.d_bcoeffs = nullptr;
+    // host-path staging grows to the largest batch seen; superseded buffers are freed
+    auto regrow = [&](double*& buf, size_t n) {
+      if (buf) {
+        QCK(cudaStreamSynchronize(s));
+        cudaFree(buf);
+        H.owned.erase(std::find(H.owned.begin(), H.owned.end(), static_cast<void*>(buf)));
+        buf = nullptr;
+      }
+      if (n) buf = qbxg::dalloc<double>(H.owned, n);
+    };
+    if (H.bhost_cap < n_rhs) {
+      regrow(H.d_bw_in, size_t(n_rhs) * H.ns);
+      regrow(H.d_bmu_in, dip ? size_t(n_rhs) * 3 * H.ns : 0);
+      regrow(H.d_bpot, size_t(n_rhs) * std::max<int64_t>(H.nt, 1));
       H.bhost_cap = n_rhs;
     }
     const size_t cbytes = size_t(H.nc) * 2 * H.D.kq * sizeof(double);
-    double* d_coeffs = nullptr;
-    if (out_center_coeffs) d_coeffs = qbxg::dalloc<double>(H.owned, size_t(n_rhs) * std::max<int64_t>(H.nc, 1) * 2 * H.D.kq);
+    if (out_center_coeffs && H.bcoeff_cap < n_rhs) {
+      regrow(H.d_bcoeffs, size_t(n_rhs) * std::max<int64_t>(H.nc, 1) * 2 * H.D.kq);
+      H.bcoeff_cap = n_rhs;
+    }
+    double* d_coeffs = out_center_coeffs ? H.d_bcoeffs : nullptr;
     QCK(cudaEventRecord(H.ev[11], s));
     QCK(cudaMemcpyAsync(H.d_bw_in, weights, size_t(n_rhs) * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
     if (dip)
@@ -1765,10 +1823,6 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
     if (d_coeffs) QCK(cudaMemcpyAsync(out_center_coeffs, d_coeffs, size_t(n_rhs) * cbytes, cudaMemcpyDeviceToHost, s));
     QCK(cudaEventRecord(H.ev[12], s));
     QCK(cudaStreamSynchronize(s));
-    if (d_coeffs) {  // per-call buffer: release it now
-      cudaFree(d_coeffs);
-      H.owned.erase(std::find(H.owned.begin(), H.owned.end(), static_cast<void*>(d_coeffs)));
-    }
     if (timings) {
       std::memset(timings, 0, sizeof(*timings));
       float ms = 0;
@@ -1778,6 +1832,7 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
       timings->h2d_bytes = int64_t(n_rhs) * H.ns * (dip ? 32 : 8);
       timings->d2h_bytes = int64_t(n_rhs) * H.nt * 8 + (d_coeffs ? int64_t(n_rhs) * int64_t(cbytes) : 0);
     }
+    qbxg::check_domain(H, s);
   });
 }
 
@@ -1800,6 +1855,7 @@ int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, double* out_tar
     QCK(cudaEventRecord(H.ev[12], s));
     qbxg::fill_timings(H, timings, true, 16 * H.ns, 16 * H.nt + (out_center_coeffs_c ? int64_t(cbytes) : 0));
     QCK(cudaStreamSynchronize(s));
+    qbxg::check_domain(H, s);
   });
 }
 

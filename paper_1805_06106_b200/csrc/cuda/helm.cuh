@@ -42,6 +42,7 @@ struct HelmData {
   const int64_t* wfar_starts;
   const int* wfar_box;
   const double* gaunt;  // KP x KP x GL
+  unsigned int* bad;    // Stage 9 non-finite flag (shared with the Laplace DevData)
 };
 
 // one centre-translation CTA: box, first entry in the item list, count (<= kHCtrMax)

@@ -1013,6 +1013,7 @@ __global__ void k_h_eval_assoc(HelmData H, int n, const int* __restrict__ items,
   }
   pot[2 * size_t(i)] = a.x;
   pot[2 * size_t(i) + 1] = a.y;
+  if (!isfinite(a.x) || !isfinite(a.y)) atomicOr(H.bad, 1u);
 }
 
 __global__ void __launch_bounds__(128) k_h_eval_conv(HelmData H, const int* __restrict__ boxes,
@@ -1040,6 +1041,7 @@ __global__ void __launch_bounds__(128) k_h_eval_conv(HelmData H, const int* __re
       }
       pot[2 * size_t(tgt_perm[ts])] = s.x;
       pot[2 * size_t(tgt_perm[ts]) + 1] = s.y;
+      if (!isfinite(s.x) || !isfinite(s.y)) atomicOr(H.bad, 1u);
     }
   }
 }
@@ -1052,6 +1054,7 @@ __global__ void k_h_centre_out(HelmData H, int nc, const int* __restrict__ ctr_p
   const int64_t o = (int64_t(ctr_perm[cs]) * H.KQ + i) * 2;
   out[o] = v.x;
   out[o + 1] = v.y;
+  if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(H.bad, 2u);
 }
 
 template <int Q>

@@ -1141,6 +1141,7 @@ __global__ void k_eval_assoc(DevData D, int n, const int* __restrict__ items, co
   const double v = eval_regular_sum(D.Lc + size_t(cs) * D.kq, D.q, (tpos[3 * i] - c.x) * ir,
                                     (tpos[3 * i + 1] - c.y) * ir, (tpos[3 * i + 2] - c.z) * ir);
   pot[i] = kInv4Pi * v;
+  if (!isfinite(v)) atomicOr(D.bad, 1u);
 }
 
 __global__ void k_eval_conv(DevData D, int n, const int* __restrict__ items, const int* __restrict__ tgt_perm,
@@ -1154,7 +1155,33 @@ __global__ void k_eval_conv(DevData D, int n, const int* __restrict__ items, con
   const double4 t = D.tgt[i];
   const double v = eval_regular_sum(D.L + size_t(b) * D.kp, D.p, (t.x - bc.x) * ih, (t.y - bc.y) * ih,
                                     (t.z - bc.z) * ih);
-  pot[tgt_perm[i]] = kInv4Pi * (D.phi[i] + v);
+  const double r = D.phi[i] + v;
+  pot[tgt_perm[i]] = kInv4Pi * r;
+  if (!isfinite(r)) atomicOr(D.bad, 1u);
+}
+
+// Error path: scan every centre's / conventional target's near-field sources for an
+// exactly coincident position (the r = 0 the reference rejects, kernels.cpp:58-62).
+__global__ void k_find_coincident(DevData D, int nc, const int* __restrict__ ctr_box,
+                                  const int* __restrict__ ctr_perm, int n_conv, const int* __restrict__ tgt_box,
+                                  const int* __restrict__ tgt_perm, const int* __restrict__ src_perm,
+                                  unsigned long long* out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(nc) + n_conv) return;
+  const bool is_ctr = t < nc;
+  const int i = is_ctr ? int(t) : int(t - nc);
+  const int b = is_ctr ? ctr_box[i] : tgt_box[i];
+  const double4 x = is_ctr ? D.ctr[i] : D.tgt[i];
+  for (int64_t k = D.near_starts[b]; k < D.near_starts[b + 1]; ++k) {
+    const int2 sg = D.near_seg[k];
+    for (int j = sg.x; j < sg.x + sg.y; ++j) {
+      const double4 y = D.src[j];
+      if (y.x == x.x && y.y == x.y && y.z == x.z) {
+        const unsigned long long id = is_ctr ? unsigned(ctr_perm[i]) : unsigned(tgt_perm[i]);
+        atomicMin(out, (is_ctr ? 0ull : 1ull) << 62 | id << 31 | unsigned(src_perm[j]));
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- direct QBX
@@ -1235,6 +1262,7 @@ __global__ void k_centre_out(DevData D, int nc, const int* __restrict__ items, c
   const int64_t o = (int64_t(ctr_perm[cs]) * D.kq + c) * 2;
   out[o] = v.x * f;
   out[o + 1] = v.y * f;
+  if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(D.bad, 2u);
 }
 
 // ---------------------------------------------------------------- operator tables
@@ -1531,6 +1559,16 @@ int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr
   const int64_t n = int64_t(nc) * D.kq;
   if (n == 0) return 0;
   k_centre_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(D, nc, items, ctr_perm, out);
+  return 1;
+}
+
+int launch_find_coincident(const DevData& D, int nc, const int* ctr_box, const int* ctr_perm, int n_conv,
+                           const int* tgt_box, const int* tgt_perm, const int* src_perm, unsigned long long* out,
+                           cudaStream_t s) {
+  const int64_t n = int64_t(nc) + n_conv;
+  if (n == 0) return 0;
+  k_find_coincident<<<unsigned((n + 127) / 128), 128, 0, s>>>(D, nc, ctr_box, ctr_perm, n_conv, tgt_box, tgt_perm,
+                                                              src_perm, out);
   return 1;
 }
 

@@ -49,6 +49,7 @@ struct DevData {
   const double2* m2l_tab;  // 1331 x ktab_m2l: I(2*delta) for box offsets delta in [-5,5]^3
   const double2* oct_m2m;  // 8 x kp: R((child-parent)/|child|)
   const double2* oct_l2l;  // 8 x kp: R((child-parent)/|parent|)
+  unsigned int* bad;       // set by Stage 9 when a potential / centre coefficient is non-finite
 };
 
 // Dense per-offset M2L (m2l_gemm.cu).  Work is split into chunks of target
@@ -189,6 +190,12 @@ int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const dou
                 const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
                 double* pot, cudaStream_t s);
 int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr_perm, double* out, cudaStream_t s);
+// Error path after a non-finite result: the first (kind, particle, source) triple whose
+// near-field pair is coincident, packed (kind << 62 | original id << 31 | original source id),
+// kind 0 = QBX centre, 1 = conventional target; ~0ull when there is none.
+int launch_find_coincident(const DevData& D, int nc, const int* ctr_box, const int* ctr_perm, int n_conv,
+                           const int* tgt_box, const int* tgt_perm, const int* src_perm, unsigned long long* out,
+                           cudaStream_t s);
 int launch_tables(const DevData& D, double2* m2l_tab, double2* oct_m2m, double2* oct_l2l, cudaStream_t s);
 int launch_direct_sum(int ns, const double4* src, const double4* mu, int nt, const double4* tgt, double* pot,
                       unsigned long long* bad, cudaStream_t s);

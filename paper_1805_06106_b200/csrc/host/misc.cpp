@@ -2,6 +2,7 @@
 #include <string>
 
 #include "common.hpp"
+#include "predicates.hpp"
 
 namespace qbxg {
 
@@ -18,6 +19,17 @@ extern "C" {
 
 const char* qbxg_last_error(void) { return qbxg::get_last_error(); }
 
-const char* qbxg_version(void) { return "qbxg 0.1 (sm_100a, fp64 Laplace SL/SL+DL)"; }
+const char* qbxg_version(void) {
+  return "qbxg 0.2 (sm_100a; fp64 Laplace SL / SL+DL, complex128 Helmholtz SL / SL+DL)";
+}
+
+int qbxg_adequately_separated(int32_t kind, const double* ca, double ha, const double* cb, double hb, double t_f,
+                              int32_t* out) {
+  return qbxg::guarded([&] {
+    if (!ca || !cb || !out || (kind != 0 && kind != 1))
+      throw qbxg::InvalidArgument("qbxg_adequately_separated: bad argument");
+    *out = kind == 0 ? qbxg::sep_box_tcr(ca, ha, cb, hb, t_f) : qbxg::sep_tcr_box(ca, ha, cb, hb, t_f);
+  });
+}
 
 }  // extern "C"
