@@ -58,7 +58,8 @@ enum {
 enum {
   QBXG_KERNEL_LAPLACE_SL = 0,    /* single layer: sum w G                     */
   QBXG_KERNEL_LAPLACE_SL_DL = 1, /* single + double layer: sum w G + m.grad_y G */
-  QBXG_KERNEL_HELMHOLTZ_SL = 2   /* e^{ikr}/(4 pi r), complex density: qbxg_apply_complex */
+  QBXG_KERNEL_HELMHOLTZ_SL = 2,  /* e^{ikr}/(4 pi r), complex density: qbxg_apply_complex */
+  QBXG_KERNEL_HELMHOLTZ_SL_DL = 3 /* single + double layer: sum w G_k + m.grad_y G_k (complex w, m) */
 };
 
 /* Interaction-list kinds (Definitions 1-8). */
@@ -95,7 +96,7 @@ typedef struct {
   double t_f;           /* target confinement factor, < 2 sqrt(3) - 2     */
   int32_t n_max;        /* max particles (sources+centres+targets) per box */
   int32_t kernel;       /* QBXG_KERNEL_*                                  */
-  double helmholtz_k;   /* wavenumber k of QBXG_KERNEL_HELMHOLTZ_SL        */
+  double helmholtz_k;   /* wavenumber k of the Helmholtz kernels           */
   int32_t w_far_demote; /* Remark 1: a List-3-far box whose
                            subtree holds fewer than this many sources is replaced by
                            its source leaves in List 3 close; 0 disables.  */
@@ -330,19 +331,23 @@ int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* w
                     const double* center_radius, int64_t n_targets, const double* target_pos,
                     const int32_t* association, int32_t p_qbx, double* out_pot);
 
-/* ---- Helmholtz single-layer FMM (cfg.kernel = QBXG_KERNEL_HELMHOLTZ_SL,
+/* ---- Helmholtz FMM (cfg.kernel = QBXG_KERNEL_HELMHOLTZ_SL or _SL_DL,
  * cfg.helmholtz_k > 0, p_fmm <= 20, p_qbx <= 6, one GPU) ----------------------
  * Complex weights [n_sources][2] in, complex potentials [n_targets][2] out (caller
  * order), optional centre locals [n_centers][(p_qbx+1)^2][2] in the internal basis
  * L_n^m of  phi = sum L_n^m j_n(k|x-c|) Y_n^m(x-c)  (index n^2+n+m; orthonormal Y,
  * no Condon-Shortley phase; formulas in oracle/helm_oracle.cpp).  Stages 2-9 on the
- * same tree and lists as the Laplace path. */
-int qbxg_apply_complex(qbxg_handle* h, const double* weights_c, double* out_target_pot_c,
-                       double* out_center_coeffs_c, qbxg_timings* timings);
+ * same tree and lists as the Laplace path.  SL+DL: complex dipole moments
+ * [n_sources][3][2] (m_x, m_y, m_z, each re, im) add m . grad_y G_k(x, y) -- e.g.
+ * the Brakhage-Werner combination with w = -i eta q mu and
+ * m = q mu n; dipoles_c must be NULL for the single layer. */
+int qbxg_apply_complex(qbxg_handle* h, const double* weights_c, const double* dipoles_c_or_null,
+                       double* out_target_pot_c, double* out_center_coeffs_c, qbxg_timings* timings);
 
-/* ---- Helmholtz single layer, unaccelerated (BASELINE config 3) --
+/* ---- Helmholtz single (+ double) layer, unaccelerated (BASELINE config 3) --
  * G_k = e^{ik|x-y|}/(4 pi |x-y|), complex weights and potentials interleaved
- * (re, im).  qbxg_helm_direct_sum: pot[t] = sum_s w_s G_k(t, s) (QBXG_ERR_DOMAIN on a
+ * (re, im), optional complex dipoles [n_sources][3][2].  qbxg_helm_direct_sum:
+ * pot[t] = sum_s w_s G_k(t, s) + m_s . grad_s G_k(t, s) (QBXG_ERR_DOMAIN on a
  * coincidence).  qbxg_helm_direct_qbx: the spec's direct_qbx for G_k -- each
  * associated target gets its centre's order-p_qbx local from all sources,
  *   L_n^m = ik sum_s w_s h_n(k|s-c|) conj(Y_n^m(s-c)), pot = sum L_n^m j_n(k|t-c|) Y_n^m(t-c)
@@ -350,9 +355,10 @@ int qbxg_apply_complex(qbxg_handle* h, const double* weights_c, double* out_targ
  * sum.  No reference implementation exists; parity is against the
  * complex128 oracle in oracle/helm_oracle.cpp. */
 int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
-                         int64_t n_targets, const double* target_pos, double* out_pot_c);
+                         const double* dipoles_c_or_null, int64_t n_targets, const double* target_pos,
+                         double* out_pot_c);
 int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
-                         int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
+                         const double* dipoles_c_or_null, int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
                          const int32_t* association, int32_t p_qbx, double* out_pot_c);
 
 /* ---- target association and area queries on the GPU --

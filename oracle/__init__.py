@@ -53,13 +53,13 @@ def lib():
         L.qbxo_helm_ylm.argtypes = [C.c_int, C.c_int, _dp, _dp]
         L.qbxo_helm_bessel.argtypes = [C.c_int, C.c_double, _dp, _dp]
         L.qbxo_helm_gaunt.argtypes = [C.c_int] * 5 + [_dp]
-        L.qbxo_helm_form.argtypes = [C.c_int, C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int, _dp]
+        L.qbxo_helm_form.argtypes = [C.c_int, C.c_double, C.c_int64, _dp, _dp, _dp, _dp, C.c_int, _dp]
         L.qbxo_helm_eval.argtypes = [C.c_int, C.c_double, _dp, C.c_int, _dp, _dp, _dp]
         L.qbxo_helm_translate.argtypes = [C.c_int, C.c_double, _dp, C.c_int, _dp, _dp, C.c_int, _dp]
-        L.qbxo_helm_direct_sum.argtypes = [C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]
-        L.qbxo_helm_direct_qbx.argtypes = [C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p,
+        L.qbxo_helm_direct_sum.argtypes = [C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp]
+        L.qbxo_helm_direct_qbx.argtypes = [C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p,
                                            C.c_int, _dp]
-        L.qbxo_helm_execute.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _i32p, _dp, _dp,
+        L.qbxo_helm_execute.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, _i32p, _dp, _dp, _dp,
                                         _dp]
         L.oracle_associate.argtypes = [C.c_int64, _dp, _dp, C.c_int64, _dp, _dp, C.c_void_p, C.c_int64, _dp,
                                        C.c_double, C.c_void_p, _i32p, _i64p]
@@ -275,12 +275,19 @@ def helm_gaunt(n, m, n2, m2, l):
     return float(out[0])
 
 
-def helm_form(kind, k, pos, w, center, P):
-    """kind 0: multipole (P2M), 1: local (P2L); w complex weights."""
+def _dip(mu, n):
+    """complex dipoles (n, 3) -> 6n interleaved doubles (or None)"""
+    if mu is None:
+        return None
+    return np.ascontiguousarray(np.asarray(mu, dtype=np.complex128).reshape(n, 3)).view(np.float64).reshape(-1)
+
+
+def helm_form(kind, k, pos, w, center, P, mu=None):
+    """kind 0: multipole (P2M), 1: local (P2L); w complex weights, mu complex dipoles (n, 3)."""
     pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
     out = np.zeros(2 * (P + 1) ** 2)
-    _hchk(lib().qbxo_helm_form(kind, k, pos.shape[0], _p(pos), _p(_cplx(w)), _p(center), P,
-                               out.ctypes.data_as(_dp)))
+    _hchk(lib().qbxo_helm_form(kind, k, pos.shape[0], _p(pos), _p(_cplx(w)), _p(_dip(mu, pos.shape[0])), _p(center),
+                               P, out.ctypes.data_as(_dp)))
     return out.view(np.complex128)
 
 
@@ -298,30 +305,33 @@ def helm_translate(kind, k, coeffs, Pin, c, C_, Pout):
     return out.view(np.complex128)
 
 
-def helm_direct_sum(k, pos, w, tpos):
+def helm_direct_sum(k, pos, w, tpos, mu=None):
     pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
     tpos = np.ascontiguousarray(tpos, dtype=np.float64).reshape(-1, 3)
     out = np.zeros(2 * tpos.shape[0])
-    _hchk(lib().qbxo_helm_direct_sum(k, pos.shape[0], _p(pos), _p(_cplx(w)), tpos.shape[0], _p(tpos),
+    _hchk(lib().qbxo_helm_direct_sum(k, pos.shape[0], _p(pos), _p(_cplx(w)), _p(_dip(mu, pos.shape[0])),
+                                     tpos.shape[0], _p(tpos),
                                      out.ctypes.data_as(_dp)))
     return out.view(np.complex128)
 
 
-def helm_direct_qbx(k, geom, w, q):
+def helm_direct_qbx(k, geom, w, q, mu=None):
     out = np.zeros(2 * geom.n_targets)
-    _hchk(lib().qbxo_helm_direct_qbx(k, geom.n_sources, _p(geom.source_pos), _p(_cplx(w)), geom.n_centers,
+    _hchk(lib().qbxo_helm_direct_qbx(k, geom.n_sources, _p(geom.source_pos), _p(_cplx(w)),
+                                     _p(_dip(mu, geom.n_sources)), geom.n_centers,
                                      _p(geom.center_pos), geom.n_targets, _p(geom.target_pos),
                                      geom.association.ctypes.data_as(_i32p), q, out.ctypes.data_as(_dp)))
     return out.view(np.complex128)
 
 
-def helm_execute(plan, geom, k, p, q, w, want_centers=False):
-    """Stages 2-9 for the Helmholtz single layer on the host plan (same tree and lists)."""
+def helm_execute(plan, geom, k, p, q, w, want_centers=False, mu=None):
+    """Stages 2-9 for the Helmholtz single (+ double) layer on the host plan (same tree and
+    lists); mu: complex dipole moments (N_S, 3) or None."""
     pot = np.zeros(2 * geom.n_targets)
     cc = np.zeros(2 * geom.n_centers * (q + 1) ** 2) if want_centers else None
     _hchk(lib().qbxo_helm_execute(C.addressof(plan.view), k, p, q, _p(geom.source_pos), _p(geom.center_pos),
                                   _p(geom.target_pos), geom.association.ctypes.data_as(_i32p), _p(_cplx(w)),
-                                  pot.ctypes.data_as(_dp), None if cc is None else cc.ctypes.data_as(_dp)))
+                                  _p(_dip(mu, geom.n_sources)), pot.ctypes.data_as(_dp), None if cc is None else cc.ctypes.data_as(_dp)))
     pot = pot.view(np.complex128)
     if want_centers:
         return pot, cc.view(np.complex128).reshape(geom.n_centers, (q + 1) ** 2)

@@ -264,27 +264,78 @@ void translate(double k, const std::vector<cd>& in, int Pin, const double* t, bo
 
 struct Src {
   const double* pos;
-  const double* w;  // interleaved complex
+  const double* w;   // interleaved complex
+  const double* mu;  // null, or 3 complex dipole components per source (6 doubles)
   cd weight(int64_t s) const { return cd(w[2 * s], w[2 * s + 1]); }
+  void dipole(int64_t s, cd (&m)[3]) const {
+    for (int d = 0; d < 3; ++d) m[d] = cd(mu[6 * s + 2 * d], mu[6 * s + 2 * d + 1]);
+  }
 };
 
+// mu . grad_v F_n^m(v) for a wave table F = f_n(k|v|) Y_n^m (f = j_n or h_n, orders
+// <= PF, PF >= n + 1), by the ladder identities of the spherical wave functions in this
+// normalisation (orthonormal Y without the Condon-Shortley phase; checked against
+// Richardson finite differences in tests/test_helmholtz.py):
+//   d_z F_n^m       = k [a_n^m F_{n-1}^m - a_{n+1}^m F_{n+1}^m],  a_n^m = sqrt((n^2 - m^2) / ((2n-1)(2n+1)))
+//   (d_x + i d_y) F = s+ k [c F_{n-1}^{m+1} + e F_{n+1}^{m+1}],   s+ = -1 (m >= 0), +1 (m < 0)
+//   (d_x - i d_y) F = s- k [f F_{n-1}^{m-1} + g F_{n+1}^{m-1}],   s- = +1 (m > 0), -1 (m <= 0)
+// c = sqrt((n-m-1)(n-m) / ((2n-1)(2n+1))), e = sqrt((n+m+1)(n+m+2) / ((2n+1)(2n+3))),
+// f = sqrt((n+m-1)(n+m) / ((2n-1)(2n+1))), g = sqrt((n-m+1)(n-m+2) / ((2n+1)(2n+3)));
+// mu . grad = mu_z d_z + (mu_x - i mu_y)/2 (d_x + i d_y) + (mu_x + i mu_y)/2 (d_x - i d_y).
+cd grad_dot(double k, const std::vector<cd>& F, int PF, int n, int m, const cd (&mu)[3]) {
+  auto at = [&](int nn, int mm) -> cd {
+    if (nn < 0 || nn > PF || std::abs(mm) > nn) return cd(0);
+    return F[ix(nn, mm)];
+  };
+  auto sq = [](double x) { return x > 0 ? std::sqrt(x) : 0.0; };
+  const double dn = n, dm = m;
+  const double a0 = sq((dn * dn - dm * dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double a1 = sq(((dn + 1) * (dn + 1) - dm * dm) / ((2 * dn + 1) * (2 * dn + 3)));
+  const double c = sq((dn - dm - 1) * (dn - dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double e = sq((dn + dm + 1) * (dn + dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+  const double f = sq((dn + dm - 1) * (dn + dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double g = sq((dn - dm + 1) * (dn - dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+  const cd dz = k * (a0 * at(n - 1, m) - a1 * at(n + 1, m));
+  const cd dp = (m >= 0 ? -1.0 : 1.0) * k * (c * at(n - 1, m + 1) + e * at(n + 1, m + 1));
+  const cd dmi = (m > 0 ? 1.0 : -1.0) * k * (f * at(n - 1, m - 1) + g * at(n + 1, m - 1));
+  return mu[2] * dz + 0.5 * (mu[0] - I1 * mu[1]) * dp + 0.5 * (mu[0] + I1 * mu[1]) * dmi;
+}
+
+// P2M: M_n^m += ik [w conj(R_n^m(v)) + mu . grad_s conj(R_n^m(s - c))], conj(R_n^m) = R_n^{-m}
 void p2m(double k, const Src& S, int64_t s, const double* c, int P, std::vector<cd>& M) {
   const double v[3] = {S.pos[3 * s] - c[0], S.pos[3 * s + 1] - c[1], S.pos[3 * s + 2] - c[2]};
   std::vector<cd> R;
-  wave_R(k, P, v, R);
+  const int PF = S.mu ? P + 1 : P;
+  wave_R(k, PF, v, R);
   const cd f = I1 * k * S.weight(s);
-  for (int i = 0; i < nf(P); ++i) M[i] += f * std::conj(R[i]);
+  for (int n = 0; n <= P; ++n)
+    for (int m = -n; m <= n; ++m) M[ix(n, m)] += f * std::conj(R[ix(n, m)]);
+  if (!S.mu) return;
+  cd mu[3];
+  S.dipole(s, mu);
+  for (int n = 0; n <= P; ++n)
+    for (int m = -n; m <= n; ++m) M[ix(n, m)] += I1 * k * grad_dot(k, R, PF, n, -m, mu);
 }
 
+// P2L: L_n^m += ik [w h_n conj(Y_n^m)(v) + mu . grad_s (h_n conj(Y_n^m))(s - c)], h_n conj(Y_n^m) = S_n^{-m}
 void p2l(double k, const Src& S, int64_t s, const double* c, int P, std::vector<cd>& L) {
   const double v[3] = {S.pos[3 * s] - c[0], S.pos[3 * s + 1] - c[1], S.pos[3 * s + 2] - c[2]};
   std::vector<cd> Y;
-  ylm(P, v, Y);
+  const int PF = S.mu ? P + 1 : P;
+  ylm(PF, v, Y);
   std::vector<cd> H;
-  sph_h(P, k * std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]), H);
+  sph_h(PF, k * std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]), H);
   const cd f = I1 * k * S.weight(s);
   for (int n = 0; n <= P; ++n)
     for (int m = -n; m <= n; ++m) L[ix(n, m)] += f * H[n] * std::conj(Y[ix(n, m)]);
+  if (!S.mu) return;
+  std::vector<cd> F(Y.size());
+  for (int n = 0; n <= PF; ++n)
+    for (int m = -n; m <= n; ++m) F[ix(n, m)] = H[n] * Y[ix(n, m)];
+  cd mu[3];
+  S.dipole(s, mu);
+  for (int n = 0; n <= P; ++n)
+    for (int m = -n; m <= n; ++m) L[ix(n, m)] += I1 * k * grad_dot(k, F, PF, n, -m, mu);
 }
 
 cd eval_local(double k, const std::vector<cd>& L, int P, const double* c, const double* t) {
@@ -305,11 +356,18 @@ cd eval_multipole(double k, const std::vector<cd>& M, int P, const double* c, co
   return a;
 }
 
+// w G_k(t, s) + mu . grad_s G_k(t, s) = [w + mu . (t - s) (1 - i k r) / r^2] e^{ikr} / (4 pi r)
 cd p2p(double k, const Src& S, int64_t s, const double* t) {
   const double dx = t[0] - S.pos[3 * s], dy = t[1] - S.pos[3 * s + 1], dz = t[2] - S.pos[3 * s + 2];
   const double r = std::sqrt(dx * dx + dy * dy + dz * dz);
   if (r == 0.0) throw std::invalid_argument("helmholtz p2p: target coincides with a source");
-  return S.weight(s) * std::polar(1.0, k * r) / (4.0 * kPi * r);
+  cd a = S.weight(s);
+  if (S.mu) {
+    cd mu[3];
+    S.dipole(s, mu);
+    a += (mu[0] * dx + mu[1] * dy + mu[2] * dz) * cd(1.0, -k * r) / (r * r);
+  }
+  return a * std::polar(1.0, k * r) / (4.0 * kPi * r);
 }
 
 }  // namespace
@@ -353,10 +411,10 @@ int qbxo_helm_gaunt(int n, int m, int n2, int m2, int l, double* out) {
 }
 
 // kind 0: P2M (multipole about c), 1: P2L (local about c); weights interleaved complex.
-int qbxo_helm_form(int kind, double k, int64_t ns, const double* pos, const double* w, const double* c, int P,
-                   double* out) {
+int qbxo_helm_form(int kind, double k, int64_t ns, const double* pos, const double* w, const double* mu,
+                   const double* c, int P, double* out) {
   return guard([&] {
-    Src S{pos, w};
+    Src S{pos, w, mu};
     std::vector<cd> E(size_t(nf(P)), cd(0));
     for (int64_t s = 0; s < ns; ++s) {
       if (kind == 0)
@@ -398,10 +456,10 @@ int qbxo_helm_translate(int kind, double k, const double* in, int Pin, const dou
 }
 
 // potentials (complex, interleaved) at targets from all sources
-int qbxo_helm_direct_sum(double k, int64_t ns, const double* pos, const double* w, int64_t nt, const double* tpos,
-                         double* out) {
+int qbxo_helm_direct_sum(double k, int64_t ns, const double* pos, const double* w, const double* mu, int64_t nt,
+                         const double* tpos, double* out) {
   return guard([&] {
-    Src S{pos, w};
+    Src S{pos, w, mu};
 #pragma omp parallel for schedule(static)
     for (int64_t t = 0; t < nt; ++t) {
       cd a(0);
@@ -414,11 +472,11 @@ int qbxo_helm_direct_sum(double k, int64_t ns, const double* pos, const double* 
 
 // unaccelerated QBX: each associated target gets its centre's order-q local from ALL
 // sources; conventional targets (association -1) the direct sum.
-int qbxo_helm_direct_qbx(double k, int64_t ns, const double* pos, const double* w, int64_t nc,
+int qbxo_helm_direct_qbx(double k, int64_t ns, const double* pos, const double* w, const double* mu, int64_t nc,
                          const double* cpos, int64_t nt, const double* tpos, const int32_t* assoc, int q,
                          double* out) {
   return guard([&] {
-    Src S{pos, w};
+    Src S{pos, w, mu};
     std::vector<std::vector<cd>> Lc{size_t(nc)};
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t c = 0; c < nc; ++c) {
@@ -444,11 +502,11 @@ int qbxo_helm_direct_qbx(double k, int64_t ns, const double* pos, const double* 
 // optionally, the centres' order-q locals (nc x (q+1)^2 complex, index n^2+n+m).
 int qbxo_helm_execute(const qbxg_plan_view* V, double k, int p, int q, const double* src_pos,
                       const double* center_pos, const double* target_pos, const int32_t* association,
-                      const double* weights, double* out_pot, double* out_center_coeffs) {
+                      const double* weights, const double* dipoles, double* out_pot, double* out_center_coeffs) {
   return guard([&] {
     const int nb = V->n_boxes;
     const int KP = nf(p), KQ = nf(q);
-    Src S{src_pos, weights};
+    Src S{src_pos, weights, dipoles};
     g_gaunt.build(p);
     auto src_of = [&](int64_t sorted) { return int64_t(V->src_perm[sorted]); };
     // Stage 2: P2M at leaves, M2M in postorder

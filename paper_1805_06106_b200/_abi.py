@@ -24,6 +24,7 @@ ERR_NO_DEVICE = 6
 KERNEL_LAPLACE_SL = 0
 KERNEL_LAPLACE_SL_DL = 1
 KERNEL_HELMHOLTZ_SL = 2
+KERNEL_HELMHOLTZ_SL_DL = 3
 
 BOX_TARGET, BOX_TARGET_ANCESTOR, BOX_HAS_SOURCES, BOX_LEAF = 1, 2, 4, 8
 
@@ -120,9 +121,9 @@ def _declare(lib):
         "qbxg_apply": ([C.c_void_p, _dp, _dp, _dp, _dp, P(Timings)], C.c_int),
         "qbxg_apply_device": ([C.c_void_p] * 6 + [P(Timings)], C.c_int),
         "qbxg_set_overlap": ([C.c_void_p, C.c_int32], C.c_int),
-        "qbxg_apply_complex": ([C.c_void_p, _dp, _dp, _dp, P(Timings)], C.c_int),
-        "qbxg_helm_direct_sum": ([C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp], C.c_int),
-        "qbxg_helm_direct_qbx": ([C.c_double, C.c_int64, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p, C.c_int32,
+        "qbxg_apply_complex": ([C.c_void_p, _dp, _dp, _dp, _dp, P(Timings)], C.c_int),
+        "qbxg_helm_direct_sum": ([C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, _dp], C.c_int),
+        "qbxg_helm_direct_qbx": ([C.c_double, C.c_int64, _dp, _dp, _dp, C.c_int64, _dp, C.c_int64, _dp, _i32p, C.c_int32,
                                   _dp], C.c_int),
         "qbxg_apply_batch": ([C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp, P(Timings)], C.c_int),
         "qbxg_apply_batch_device": ([C.c_void_p, C.c_int32] + [C.c_void_p] * 5 + [P(Timings)], C.c_int),

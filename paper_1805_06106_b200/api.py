@@ -212,7 +212,7 @@ def config_fmm(config_id: int, **overrides) -> FmmConfig:
     (SPEC.md:382); pass w_far_demote=0 to disable it."""
     p, q, k = CONFIG_ORDERS[config_id]
     cfg = FmmConfig(p_fmm=p, p_qbx=q, t_f=0.9, n_max=64, kernel=k, w_far_demote=(p ** 3) // max(q * q, 1),
-                    helmholtz_k=3.0 if k == _abi.KERNEL_HELMHOLTZ_SL else 0.0)  # config 3: k = 3
+                    helmholtz_k=3.0 if k in (_abi.KERNEL_HELMHOLTZ_SL, _abi.KERNEL_HELMHOLTZ_SL_DL) else 0.0)  # k = 3
     for key, v in overrides.items():
         setattr(cfg, key, v)
     return cfg
@@ -433,16 +433,23 @@ class FmmEngine:
             return pot, c[..., 0] + 1j * c[..., 1]
         return pot
 
-    def apply_complex(self, weights, want_centers=False):
-        """Helmholtz single layer (kernel 2): complex weights in, complex potentials
-        out; centre locals (N_C, (q+1)^2) in the internal basis (include/qbxg.h)."""
+    def apply_complex(self, weights, dipoles=None, want_centers=False):
+        """Helmholtz single layer (kernel 2) or single + double layer (kernel 3): complex
+        weights (N_S,) and, for kernel 3, complex dipole moments (N_S, 3) in; complex
+        potentials out; centre locals (N_C, (q+1)^2) in the internal basis (include/qbxg.h)."""
         w = np.ascontiguousarray(weights, dtype=np.complex128).reshape(-1)
         if w.shape[0] != self.geom.n_sources:
             raise ValueError("apply_complex: weights do not match the geometry")
+        m = None
+        if dipoles is not None:
+            m = np.ascontiguousarray(dipoles, dtype=np.complex128).reshape(-1)
+            if m.shape[0] != 3 * self.geom.n_sources:
+                raise ValueError("apply_complex: dipoles must have shape (n_sources, 3)")
         pot = np.empty(2 * self.geom.n_targets, dtype=np.float64)
         kq = (self.cfg.p_qbx + 1) ** 2
         cc = np.empty(2 * self.geom.n_centers * kq, dtype=np.float64) if want_centers else None
-        _check(_abi.lib().qbxg_apply_complex(self.handle, _ptr(w.view(np.float64)), _ptr(pot), _ptr(cc),
+        _check(_abi.lib().qbxg_apply_complex(self.handle, _ptr(w.view(np.float64)),
+                                             _ptr(None if m is None else m.view(np.float64)), _ptr(pot), _ptr(cc),
                                              C.byref(self.timings)))
         pot = pot.view(np.complex128)
         if want_centers:
@@ -562,22 +569,34 @@ def _as_cplx(w, n):
     return w.view(np.float64)
 
 
-def helm_direct_sum(k: float, source_pos, weights, target_pos) -> np.ndarray:
-    """Helmholtz single layer G_k = e^{ik r}/(4 pi r) summed directly on the GPU (complex)."""
+def _as_cplx_dip(dipoles, n):
+    if dipoles is None:
+        return None
+    m = np.ascontiguousarray(dipoles, dtype=np.complex128).reshape(-1)
+    if m.shape[0] != 3 * n:
+        raise ValueError("dipoles must have shape (n_sources, 3)")
+    return m.view(np.float64)
+
+
+def helm_direct_sum(k: float, source_pos, weights, target_pos, dipoles=None) -> np.ndarray:
+    """Helmholtz G_k = e^{ik r}/(4 pi r) summed directly on the GPU (complex):
+    sum_s w_s G_k(t, s) [+ m_s . grad_s G_k(t, s) with complex dipoles (N_S, 3)]."""
     pos = np.ascontiguousarray(source_pos, dtype=np.float64).reshape(-1, 3)
     tpos = np.ascontiguousarray(target_pos, dtype=np.float64).reshape(-1, 3)
     wc = _as_cplx(weights, pos.shape[0])
+    mc = _as_cplx_dip(dipoles, pos.shape[0])
     out = np.empty(2 * tpos.shape[0], dtype=np.float64)
-    _check(_abi.lib().qbxg_helm_direct_sum(float(k), pos.shape[0], _ptr(pos), _ptr(wc), tpos.shape[0], _ptr(tpos),
-                                           _ptr(out)))
+    _check(_abi.lib().qbxg_helm_direct_sum(float(k), pos.shape[0], _ptr(pos), _ptr(wc), _ptr(mc), tpos.shape[0],
+                                           _ptr(tpos), _ptr(out)))
     return out.view(np.complex128)
 
 
-def helm_direct_qbx(k: float, geom: Geometry, weights, p_qbx: int = 5) -> np.ndarray:
-    """Unaccelerated QBX for the Helmholtz single layer on the GPU (complex potentials)."""
+def helm_direct_qbx(k: float, geom: Geometry, weights, p_qbx: int = 5, dipoles=None) -> np.ndarray:
+    """Unaccelerated QBX for the Helmholtz single (+ double) layer on the GPU (complex potentials)."""
     wc = _as_cplx(weights, geom.n_sources)
+    mc = _as_cplx_dip(dipoles, geom.n_sources)
     out = np.empty(2 * geom.n_targets, dtype=np.float64)
-    _check(_abi.lib().qbxg_helm_direct_qbx(float(k), geom.n_sources, _ptr(geom.source_pos), _ptr(wc),
+    _check(_abi.lib().qbxg_helm_direct_qbx(float(k), geom.n_sources, _ptr(geom.source_pos), _ptr(wc), _ptr(mc),
                                            geom.n_centers, _ptr(geom.center_pos), geom.n_targets,
                                            _ptr(geom.target_pos), _ptr(geom.association, C.c_int32), int(p_qbx),
                                            _ptr(out)))

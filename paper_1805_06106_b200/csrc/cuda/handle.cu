@@ -108,16 +108,10 @@ struct Handle {
   int n_wfar_tboxes = 0;
   int* d_xfar_boxes = nullptr;
   int n_xfar_boxes = 0;
-  int2* d_items_wfar = nullptr;  // (box, centre offset) chunks for M2QBXL
-  int n_items_wfar = 0;
-  int2* d_items_ctr = nullptr;   // (box, centre offset) chunks for L2QBXL
-  int n_items_ctr = 0;
   int* d_ctr_box = nullptr;      // owning box of each sorted centre
   int* d_flat_all = nullptr;     // 0..nc-1
   int* d_flat_wfar = nullptr;    // sorted centres of boxes with List 3 far entries
   int n_flat_wfar = 0;
-  int ctr_mode = 0;              // W far M2QBXL: 0 pairs, 1 gemm, 2 per-box
-  int l2q_mode = 3;              // L2QBXL: 3 box tables (default), 0 flat, 1 gemm, 2 warp per box
   int2* d_l3_ctas = nullptr;     // L2QBXL CTA descriptors (first item in d_flat_all, count)
   int n_l3_ctas = 0;
   dev::PairPlan wpairs;          // M2QBXL (centre, W_far box) pairs
@@ -136,7 +130,6 @@ struct Handle {
   int* d_own_ctr = nullptr;      // owned centres (sorted index)
   int n_own_ctr = 0;
   void* nccl_comm = nullptr;     // ncclComm_t when attached
-  int shift_mode = 0;            // 0 DMMA GEMM, 1 per-box kernels
   // staging for host applies
   double* d_w = nullptr;
   double* d_mu_in = nullptr;
@@ -187,6 +180,7 @@ struct Handle {
   int4* h_lctas = nullptr;
   int* h_lctr = nullptr;
   double* d_wc = nullptr;                      // host-apply staging: complex weights, potentials
+  double* d_muc = nullptr;                     // host-apply staging: complex dipoles (SL+DL)
   double* d_potc = nullptr;
   double* d_coeffc = nullptr;
   // batched densities (qbxg_apply_batch*): NR-wide near-field buffers, grown on demand
@@ -260,11 +254,6 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       slot_to_op[sl] = int(used.size());
       used.push_back(sl);
     }
-  }
-  P.n_ops = int(used.size());
-  if (const char* e = std::getenv("QBXG_M2L_BN")) {
-    const int v = std::atoi(e);
-    P.bn = (v == 8 || v == 16 || v == 32) ? v : 64;
   }
   const auto& mk = H.mask;
 
@@ -355,81 +344,65 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       H.l2l_levels[l] = make_level(cols, outb, seg);
     }
   }
-  if (P.n_ops == 0) {
+  if (nent == 0) {
     P.temp = dalloc<double>(O, size_t(max_level_rows) * P.KRp);
     return;
   }
-  int* d_used = dupload(O, used, s);
-  // M2L operator form: rotation + z-translation (default, QBXG_M2L_MODE=rot) or the
-  // dense per-offset real-DOF matrix (QBXG_M2L_MODE=dense); both batched by offset.
+  if (!dev::pas_supported(p)) throw InvalidArgument("qbxg_create: the M2L supports 1 <= p_fmm <= 21");
+  // --- Stage 4 operators: one [W | Z | V] set per class (rho_xy^2, dz); per offset only
+  // the azimuth alpha = atan2(dy, dx) remains, as the (cos k alpha, sin k alpha) table
+  P.n_offsets = int(used.size());
+  std::vector<int> cls_of_op(P.n_offsets), cls_rxy2, cls_dz;
+  std::vector<double2> cs(size_t(P.n_offsets) * (p + 1));
   {
-    const char* mode = std::getenv("QBXG_M2L_MODE");
-    // dense is the default: the rotation kernels are correct (parity-tested) but
-    // latency-bound so far (116 ms vs 84 ms at config 1); opt in with QBXG_M2L_MODE=rot
-    P.rot = (mode && std::string(mode) == "rot") && dev::m2l_rot_smem(p, 16) <= 220 * 1024;
-    // split (block-diagonal after an azimuthal rotation) is the default where its
-    // padded block fits the kernel (p <= 20); QBXG_M2L_MODE=dense keeps the full matrix
-    P.split = !P.rot && !(mode && std::string(mode) == "dense") && dev::split_nh(p) <= 240;
-    // point-and-shoot on the split frame's real blocks is the default where it is
-    // built (4 <= p <= 15: 45.8 vs 58.6 ms at config 1); QBXG_M2L_MODE=split keeps
-    // the two dense blocks per offset
-    P.pas = P.split && !(mode && std::string(mode) == "split") && dev::pas_supported(p);
+    std::vector<int> key_to_cls(51 * 11, -1);
+    for (int o = 0; o < P.n_offsets; ++o) {
+      const int sl = used[o], dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
+      const int key = (dx * dx + dy * dy) * 11 + dz + 5;
+      if (key_to_cls[key] < 0) {
+        key_to_cls[key] = int(cls_rxy2.size());
+        cls_rxy2.push_back(dx * dx + dy * dy);
+        cls_dz.push_back(dz);
+      }
+      cls_of_op[o] = key_to_cls[key];
+      const double alpha = (dx == 0 && dy == 0) ? 0.0 : std::atan2(double(dy), double(dx));
+      for (int k = 0; k <= p; ++k) cs[size_t(o) * (p + 1) + k] = make_double2(std::cos(k * alpha), std::sin(k * alpha));
+    }
   }
-  if (P.rot) {
-    if (!std::getenv("QBXG_M2L_BN")) P.bn = 16;
-    P.rot_stride = rot_blocks_size(p);
-    std::vector<double> rf(size_t(P.n_ops) * P.rot_stride), rb(rf.size()), rho(P.n_ops);
-#pragma omp parallel for schedule(dynamic, 4)
-    for (int o = 0; o < P.n_ops; ++o) {
-      const int sl = used[o];
-      const double v[3] = {2.0 * (sl / 121 - 5), 2.0 * ((sl / 11) % 11 - 5), 2.0 * (sl % 11 - 5)};
-      m2l_rotation_blocks(p, v, &rf[size_t(o) * P.rot_stride], &rb[size_t(o) * P.rot_stride]);
-      rho[o] = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-    }
-    P.rotF = dupload(O, rf, s);
-    P.rotB = dupload(O, rb, s);
-    P.rho_op = dupload(O, rho, s);
+  P.n_classes = int(cls_rxy2.size());
+  P.cs = dupload(O, cs, s);
+  {
+    std::vector<double> pops;
+    std::vector<int> tab;
+    dev::pas_build_ops(p, P.n_classes, cls_rxy2.data(), cls_dz.data(), pops, P.pas_stride, tab, P.pas_nblk,
+                       P.pas_phase, P.pas_base);
+    P.pas_ops = dupload(O, pops, s);
+    P.pas_tab = dupload(O, tab, s);
+    P.pas_tab_n = int(tab.size());
     QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
-  } else if (P.split) {
-    const int NH = dev::split_nh(p);
-    // the two dense blocks (400 MB at config 1) only when the split kernel runs
-    if (!P.pas) P.sops = dalloc<double>(O, size_t(P.n_ops) * (NH + dev::split_nhi(p, NH)) * NH);
-    P.cs = dalloc<double2>(O, size_t(P.n_ops) * (p + 1));
-    {
-      std::vector<int> eo(nent);
-      for (int64_t e = 0; e < nent; ++e) eo[e] = slot_to_op[slot[e]];
-      P.ent_op = dupload(O, eo, s);
-      QCK(cudaStreamSynchronize(s));
-    }
-    dev::launch_m2l_ops_split(P, p, d_used, s);
-    QCK(cudaGetLastError());
-    if (P.pas) {
-      std::vector<double> pops;
-      std::vector<int> tab;
-      dev::pas_build_ops(p, P.n_ops, used.data(), pops, P.pas_stride, tab, P.pas_nblk, P.pas_phase, P.pas_base);
-      P.pas_ops = dupload(O, pops, s);
-      P.pas_tab = dupload(O, tab, s);
-      P.pas_tab_n = int(tab.size());
-      QCK(cudaStreamSynchronize(s));
-    }
-  } else {
-    P.ops = dalloc<double>(O, size_t(P.n_ops) * P.KRp * P.KRp);
-    dev::launch_m2l_ops(P, p, d_used, d_rdof, s);
-    QCK(cudaGetLastError());
+  }
+  {
+    std::vector<int> eo(nent);
+    for (int64_t e = 0; e < nent; ++e) eo[e] = slot_to_op[slot[e]];
+    P.ent_op = dupload(O, eo, s);
+    QCK(cudaStreamSynchronize(s));
   }
 
-  // chunking by staging-buffer capacity
+  // --- work order: chunks of whole target boxes bounded by the staging capacity; in a
+  // chunk, entries counting-sorted by offset (CSR order inside an offset); tiles of
+  // <= 32 same-offset columns
   size_t free_b = 0, total_b = 0;
   QCK(cudaMemGetInfo(&free_b, &total_b));
-  P.srow = P.KRp;  // split staging rows: Re (hsize(p)) + compacted Im = (p+1)^2 <= KRp
+  P.srow = ((p + 1) * (p + 1) + 15) / 16 * 16;
   const size_t row_bytes = size_t(P.srow) * sizeof(double);
-  size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
+  const size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
   int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);
+  // test hook (tests/test_gpu_variants.py): force many chunks at small sizes
   if (const char* env = std::getenv("QBXG_M2L_CHUNK_ENTRIES")) cap = std::max<int64_t>(64, std::atoll(env));
+  const int tw = dev::pas_tile_cols();
   int64_t max_chunk = 0;
   int b0 = 0;
   while (b0 < nb) {
-    // extend the chunk over whole target boxes
     int b1 = b0;
     while (b1 < nb && (vs[b1 + 1] - vs[b0] <= cap || b1 == b0)) ++b1;
     const int64_t base = vs[b0], cnt = vs[b1] - vs[b0];
@@ -439,43 +412,34 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       std::vector<int> boxes;
       for (int b = b0; b < b1; ++b)
         if (vs[b + 1] > vs[b]) boxes.push_back(b);
-      // counting sort of entries by operator, keeping CSR order inside an operator
-      std::vector<int64_t> cnt_op(P.n_ops + 1, 0);
+      std::vector<int64_t> cnt_op(P.n_offsets + 1, 0);
       for (int64_t e = base; e < base + cnt; ++e) cnt_op[slot_to_op[slot[e]] + 1]++;
-      for (int o = 0; o < P.n_ops; ++o) cnt_op[o + 1] += cnt_op[o];
+      for (int o = 0; o < P.n_offsets; ++o) cnt_op[o + 1] += cnt_op[o];
       std::vector<int> col_src(cnt), col_pos(cnt);
-      std::vector<double> col_scale(cnt);
       std::vector<int64_t> fill(cnt_op.begin(), cnt_op.end() - 1);
       for (int b = b0; b < b1; ++b)
         for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
           const int64_t i = fill[slot_to_op[slot[e]]]++;
           col_src[i] = vb[e];
           col_pos[i] = int(e - base);
-          col_scale[i] = 1.0 / V.box_radius[b];
         }
       std::vector<int4> tiles;
-      {
-        const int64_t tw = P.rot     ? dev::kRotSuper
-                           : P.pas   ? dev::pas_tile_cols()
-                           : P.split ? dev::split_tile_cols()
-                                     : P.bn;
-        for (int o = 0; o < P.n_ops; ++o)
-          for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
-            tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), 0));
-      }
+      for (int o = 0; o < P.n_offsets; ++o)
+        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
+          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), cls_of_op[o]));
       C.n_tiles = int(tiles.size());
       C.tiles = dupload(O, tiles, s);
       C.col_src = dupload(O, col_src, s);
       C.col_pos = dupload(O, col_pos, s);
-      C.col_scale = dupload(O, col_scale, s);
       C.n_boxes = int(boxes.size());
       C.boxes = dupload(O, boxes, s);
+      QCK(cudaStreamSynchronize(s));
       P.chunks.push_back(C);
       max_chunk = std::max(max_chunk, cnt);
     }
     b0 = b1;
   }
-  P.temp = dalloc<double>(O, size_t(std::max(max_chunk, max_level_rows)) * P.srow);
+  P.temp = dalloc<double>(O, std::max(size_t(max_chunk) * P.srow, size_t(max_level_rows) * P.KRp));
 }
 
 // ---- Helmholtz single layer: device data, operators and work lists --------
@@ -513,6 +477,8 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.wfar_starts = D.wfar_starts;
   HD.wfar_box = D.wfar_box;
   HD.hw = dalloc<double2>(O, std::max<int64_t>(H.ns, 1));
+  HD.hmu = H.cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL_DL ? dalloc<double2>(O, 3 * std::max<int64_t>(H.ns, 1)) : nullptr;
+  H.d_muc = HD.hmu ? dalloc<double>(O, 6 * std::max<int64_t>(H.ns, 1)) : nullptr;
   HD.M = dalloc<double2>(O, size_t(nb) * HD.KP);
   HD.L = dalloc<double2>(O, size_t(nb) * HD.KP);
   HD.Lc = dalloc<double2>(O, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ);
@@ -774,7 +740,7 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
 
 // One Helmholtz apply: d_wc complex weights (caller order, interleaved), d_pot
 // complex potentials (caller order), d_coeffs optional centre locals (caller order).
-void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cudaStream_t s) {
+void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot, double* d_coeffs, cudaStream_t s) {
   dev::HelmData& HD = H.HD;
   auto& ev = H.ev;
   int L = 0;
@@ -794,7 +760,9 @@ void run_helm(Handle& H, const double* d_wc, double* d_pot, double* d_coeffs, cu
                       cudaGetErrorString(e));
   };
   QCK(cudaEventRecord(ev[0], s));
-  chk(dev::helm_gather(HD, H.ns, H.d_src_perm, d_wc, s));
+  if (HD.hmu && !d_muc) throw InvalidArgument("qbxg_apply_complex: Helmholtz SL+DL requires dipole moments");
+  if (!HD.hmu && d_muc) throw InvalidArgument("qbxg_apply_complex: dipoles given to a single-layer handle");
+  chk(dev::helm_gather(HD, H.ns, H.d_src_perm, d_wc, d_muc, s));
   QCK(cudaMemsetAsync(HD.M, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
   QCK(cudaMemsetAsync(HD.L, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
   QCK(cudaMemsetAsync(HD.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double2), s));
@@ -872,9 +840,9 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       throw InvalidArgument(get_last_error());
   }
   if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL &&
-      cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL)
+      cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL && cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL_DL)
     throw InvalidArgument("qbxg_create: unknown kernel");
-  H.helm = cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL;
+  H.helm = cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL || cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL_DL;
   if (H.helm && nranks > 1) throw InvalidArgument("qbxg_create: Helmholtz runs on one GPU in this build");
   if (H.helm && (cfg.p_fmm > 20 || cfg.p_qbx > 6))
     throw InvalidArgument("qbxg_create: Helmholtz supports p_fmm <= 20, p_qbx <= 6");
@@ -1030,6 +998,27 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     }
     D.near_starts = dupload(O, ns_, s);
     D.near_seg = dupload(O, nseg, s);
+    {
+      // flattened near-source list of each box with centres (the P2QBXL kernel's input)
+      std::vector<int> nn(nb, 0);
+      std::vector<int64_t> off(nb + 1, 0);
+      for (int b = 0; b < nb; ++b) {
+        for (int64_t i = ns_[b]; i < ns_[b + 1]; ++i) nn[b] += nseg[i].y;
+        off[b + 1] = off[b] + (V.ctr_own_count[b] > 0 ? nn[b] : 0);
+      }
+      std::vector<int> flat(std::max<int64_t>(off[nb], 1));
+#pragma omp parallel for schedule(dynamic, 64)
+      for (int b = 0; b < nb; ++b) {
+        if (V.ctr_own_count[b] == 0) continue;
+        int64_t o = off[b];
+        for (int64_t i = ns_[b]; i < ns_[b + 1]; ++i)
+          for (int j = 0; j < nseg[i].y; ++j) flat[o++] = nseg[i].x + j;
+      }
+      D.near_nsrc = dupload(O, nn, s);
+      D.near_off = dupload(O, off, s);
+      D.near_src = dupload(O, flat, s);
+      QCK(cudaStreamSynchronize(s));
+    }
     D.xfar_starts = dupload(O, xs, s);
     D.xfar_seg = dupload(O, xseg, s);
     D.v_starts = dupload(O, vs, s);
@@ -1080,15 +1069,6 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     H.n_wfar_boxes = int(wb.size());
     H.d_wfar_tboxes = dupload(O, wtb, s);
     H.n_wfar_tboxes = int(wtb.size());
-    std::vector<int2> iw, ic;
-    for (int b : wb)
-      for (int o = 0; o < V.ctr_own_count[b]; o += 16) iw.push_back(make_int2(b, o));
-    for (int b : cb)
-      for (int o = 0; o < V.ctr_own_count[b]; o += 16) ic.push_back(make_int2(b, o));
-    H.d_items_wfar = dupload(O, iw, s);
-    H.n_items_wfar = int(iw.size());
-    H.d_items_ctr = dupload(O, ic, s);
-    H.n_items_ctr = int(ic.size());
     std::vector<int> cbox(H.nc), all, fw, eval_assoc, eval_conv;
     for (int b = 0; b < nb; ++b)
       for (int j = 0; j < V.ctr_own_count[b]; ++j) cbox[V.ctr_own_start[b] + j] = b;
@@ -1134,10 +1114,6 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     }
     H.d_flat_wfar = dupload(O, fw, s);
     H.n_flat_wfar = int(fw.size());
-    if (const char* m = std::getenv("QBXG_CTR_MODE")) H.ctr_mode = std::atoi(m);
-    if (const char* m = std::getenv("QBXG_SHIFT_MODE")) H.shift_mode = std::atoi(m);
-    if (const char* m = std::getenv("QBXG_L2Q_MODE")) H.l2q_mode = std::atoi(m);
-    if (const char* m = std::getenv("QBXG_WFAR_MODE")) H.wpairs.box_major = std::atoi(m) != 0;
     // (centre, W_far box) pairs, centre-major, chunked to bound the staging buffer
     {
       const int64_t cap_pairs = int64_t(1) << 24;
@@ -1349,12 +1325,8 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   QCK(cudaEventRecord(ev[1], s));
   chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
-  for (int l = H.nlev - 2; l >= 0; --l) {
-    if (H.shift_mode == 0 || H.nranks > 1)
-      chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
-    else
-      chk(dev::launch_m2m(D, H.d_m2m_level[l], H.n_m2m_level[l], s));
-  }
+  for (int l = H.nlev - 2; l >= 0; --l)
+    chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
   H.last_launches = L;
   }
   if (!(phase & 2)) return;
@@ -1391,41 +1363,19 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   }
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
-  if (std::getenv("QBXG_M2L_NAIVE"))
-    chk(dev::launch_m2l(D, H.d_v_boxes, H.n_v_boxes, s));
-  else
-    chk(dev::launch_m2l_dense(H.m2l, D, s));
+  chk(dev::launch_m2l(H.m2l, D, s));
   if (ovl && !near_forked && H.overlap_late) fork_near();
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));
-  for (int l = 1; l < H.nlev; ++l) {
-    if (H.shift_mode == 0)
-      chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
-    else
-      chk(dev::launch_l2l(D, H.d_l2l_level[l], H.n_l2l_level[l], s));
-  }
+  for (int l = 1; l < H.nlev; ++l) chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
   QCK(cudaEventRecord(H.evx[3], s));
   if (ovl) QCK(cudaStreamWaitEvent(s, H.join_ev, 0));
-  if (H.ctr_mode == 0) {
-    chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
-    chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
-  } else if (H.ctr_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, true)) {
-    chk(dev::launch_ctr_gemm(D, H.d_items_wfar, H.n_items_wfar, true, s));
-    chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
-  } else {
-    chk(dev::launch_wfar2(D, H.d_wfar_boxes, H.n_wfar_boxes, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
-  }
+  chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
+  chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
   QCK(cudaEventRecord(ev[6], s));
   H.timed_overlap = ovl;
-  if (H.l2q_mode == 3)
-    chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
-  else if (H.l2q_mode == 0)
-    chk(dev::launch_ctr_flat(D, H.d_flat_all, H.n_own_ctr, H.d_ctr_box, false, s));
-  else if (H.l2q_mode == 1 && dev::ctr_gemm_fits(D.p, D.q, false))
-    chk(dev::launch_ctr_gemm(D, H.d_items_ctr, H.n_items_ctr, false, s));
-  else
-    chk(dev::launch_l2qbxl2(D, H.d_ctr_boxes, H.n_ctr_boxes, s));
+  chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
   QCK(cudaEventRecord(ev[9], s));
   if (H.nranks > 1) {  // targets / centres of other ranks stay zero (summed across ranks)
     QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * sizeof(double), s));
@@ -1836,8 +1786,8 @@ int qbxg_apply_batch(qbxg_handle* hp, int32_t n_rhs, const double* weights, cons
   });
 }
 
-int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, double* out_target_pot_c,
-                       double* out_center_coeffs_c, qbxg_timings* timings) {
+int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, const double* dipoles_c,
+                       double* out_target_pot_c, double* out_center_coeffs_c, qbxg_timings* timings) {
   return qbxg::guarded([&] {
     if (!hp || !weights_c || !out_target_pot_c) throw qbxg::InvalidArgument("qbxg_apply_complex: null argument");
     auto& H = hp->h;
@@ -1846,14 +1796,22 @@ int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, double* out_tar
     cudaStream_t s = H.stream;
     for (int64_t i = 0; i < 2 * H.ns; ++i)
       if (!std::isfinite(weights_c[i])) throw qbxg::InvalidArgument("qbxg_apply_complex: non-finite weight");
+    if (dipoles_c && !H.HD.hmu)
+      throw qbxg::InvalidArgument("qbxg_apply_complex: dipoles given to a single-layer handle");
+    if (!dipoles_c && H.HD.hmu) throw qbxg::InvalidArgument("qbxg_apply_complex: Helmholtz SL+DL requires dipole moments");
+    if (dipoles_c)
+      for (int64_t i = 0; i < 6 * H.ns; ++i)
+        if (!std::isfinite(dipoles_c[i])) throw qbxg::InvalidArgument("qbxg_apply_complex: non-finite dipole");
     QCK(cudaEventRecord(H.ev[11], s));
     QCK(cudaMemcpyAsync(H.d_wc, weights_c, 2 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
-    qbxg::run_helm(H, H.d_wc, H.d_potc, out_center_coeffs_c ? H.d_coeffc : nullptr, s);
+    if (dipoles_c) QCK(cudaMemcpyAsync(H.d_muc, dipoles_c, 6 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
+    qbxg::run_helm(H, H.d_wc, dipoles_c ? H.d_muc : nullptr, H.d_potc, out_center_coeffs_c ? H.d_coeffc : nullptr, s);
     QCK(cudaMemcpyAsync(out_target_pot_c, H.d_potc, 2 * H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
     const size_t cbytes = size_t(H.nc) * 2 * H.HD.KQ * sizeof(double);
     if (out_center_coeffs_c) QCK(cudaMemcpyAsync(out_center_coeffs_c, H.d_coeffc, cbytes, cudaMemcpyDeviceToHost, s));
     QCK(cudaEventRecord(H.ev[12], s));
-    qbxg::fill_timings(H, timings, true, 16 * H.ns, 16 * H.nt + (out_center_coeffs_c ? int64_t(cbytes) : 0));
+    qbxg::fill_timings(H, timings, true, (dipoles_c ? 64 : 16) * H.ns,
+                       16 * H.nt + (out_center_coeffs_c ? int64_t(cbytes) : 0));
     QCK(cudaStreamSynchronize(s));
     qbxg::check_domain(H, s);
   });
@@ -1916,7 +1874,7 @@ int qbxg_direct_sum(int64_t n_sources, const double* source_pos, const double* w
 }
 
 int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
-                         int64_t n_targets, const double* target_pos, double* out_pot_c) {
+                         const double* dipoles_c, int64_t n_targets, const double* target_pos, double* out_pot_c) {
   return qbxg::guarded([&] {
     using qbxg::InvalidArgument;
     if (n_sources < 0 || n_targets < 0) throw InvalidArgument("helm_direct_sum: negative size");
@@ -1927,6 +1885,9 @@ int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, 
     if (!(k > 0) || !std::isfinite(k)) throw InvalidArgument("helm_direct_sum: wavenumber must be positive");
     for (int64_t i = 0; i < 2 * n_sources; ++i)
       if (!std::isfinite(weights_c[i])) throw InvalidArgument("helm_direct_sum: non-finite weight");
+    if (dipoles_c)
+      for (int64_t i = 0; i < 6 * n_sources; ++i)
+        if (!std::isfinite(dipoles_c[i])) throw InvalidArgument("helm_direct_sum: non-finite dipole");
     if (n_targets == 0) return;
     qbxg::check_device();
     std::vector<void*> owned;
@@ -1947,11 +1908,16 @@ int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, 
     cudaStream_t s = nullptr;
     double4* ds = qbxg::dupload(owned, src, s);
     double2* dw = qbxg::dupload(owned, w, s);
+    double2* dm = dipoles_c ? qbxg::dupload(owned, std::vector<double2>(reinterpret_cast<const double2*>(dipoles_c),
+                                                                         reinterpret_cast<const double2*>(dipoles_c) +
+                                                                             3 * n_sources),
+                                            s)
+                            : nullptr;
     double4* dt = qbxg::dupload(owned, tgt, s);
     double2* dp = qbxg::dalloc<double2>(owned, n_targets);
     unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
     QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
-    qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, int(n_targets), dt, dp, bad, s);
+    qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, dm, int(n_targets), dt, dp, bad, s);
     QCK(cudaGetLastError());
     unsigned long long hb = 0;
     QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
@@ -1963,7 +1929,7 @@ int qbxg_helm_direct_sum(double k, int64_t n_sources, const double* source_pos, 
 }
 
 int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, const double* weights_c,
-                         int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
+                         const double* dipoles_c, int64_t n_centers, const double* center_pos, int64_t n_targets, const double* target_pos,
                          const int32_t* association, int32_t p_qbx, double* out_pot_c) {
   return qbxg::guarded([&] {
     using qbxg::InvalidArgument;
@@ -2005,14 +1971,22 @@ int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, 
     cudaStream_t s = nullptr;
     double4* ds = qbxg::dupload(owned, src, s);
     double2* dw = qbxg::dupload(owned, w, s);
+    if (dipoles_c)
+      for (int64_t i = 0; i < 6 * n_sources; ++i)
+        if (!std::isfinite(dipoles_c[i])) throw InvalidArgument("helm_direct_qbx: non-finite dipole");
+    double2* dm = dipoles_c ? qbxg::dupload(owned, std::vector<double2>(reinterpret_cast<const double2*>(dipoles_c),
+                                                                         reinterpret_cast<const double2*>(dipoles_c) +
+                                                                             3 * n_sources),
+                                            s)
+                            : nullptr;
     double4* dc = qbxg::dupload(owned, ctr, s);
     double* dtp = qbxg::dupload(owned, std::vector<double>(target_pos, target_pos + 3 * n_targets), s);
     int* das = qbxg::dupload(owned, std::vector<int>(association, association + n_targets), s);
     double2* dl = qbxg::dalloc<double2>(owned, size_t(std::max<int64_t>(n_centers, 1)) * (p_qbx + 1) * (p_qbx + 1));
     double2* dp = qbxg::dalloc<double2>(owned, n_targets);
     QCK(cudaMemsetAsync(dp, 0, n_targets * sizeof(double2), s));
-    qbxg::dev::launch_helm_direct_qbx(k, p_qbx, int(n_sources), ds, dw, int(n_centers), dc, dl, int(n_targets), dtp,
-                                      das, dp, s);
+    qbxg::dev::launch_helm_direct_qbx(k, p_qbx, int(n_sources), ds, dw, dm, int(n_centers), dc, dl, int(n_targets),
+                                      dtp, das, dp, s);
     QCK(cudaGetLastError());
     std::vector<double2> pot(n_targets);
     QCK(cudaMemcpy(pot.data(), dp, n_targets * sizeof(double2), cudaMemcpyDeviceToHost));
@@ -2021,7 +1995,7 @@ int qbxg_helm_direct_qbx(double k, int64_t n_sources, const double* source_pos, 
       double2* dq = qbxg::dalloc<double2>(owned, conv.size());
       unsigned long long* bad = qbxg::dalloc<unsigned long long>(owned, 1);
       QCK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
-      qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, int(conv.size()), dt, dq, bad, s);
+      qbxg::dev::launch_helm_direct_sum(k, int(n_sources), ds, dw, dm, int(conv.size()), dt, dq, bad, s);
       QCK(cudaGetLastError());
       unsigned long long hb = 0;
       QCK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));

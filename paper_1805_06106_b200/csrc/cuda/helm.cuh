@@ -1,4 +1,4 @@
-// Helmholtz single-layer FMM (helm_fmm.cu): device data and launchers.
+// Helmholtz single- and double-layer FMM (helm_fmm.cu): device data and launchers.
 #pragma once
 
 #include <vector>
@@ -28,6 +28,7 @@ struct HelmData {
   const double4* ctr;  // (x, y, z, r)
   const double4* tgt;
   double2* hw;         // sorted complex weights
+  double2* hmu;        // sorted complex dipole moments (3 per source), null for the single layer
   // expansions: full complex tables, index n^2 + n + m
   double2* M;          // nb x KP
   double2* L;          // nb x KP
@@ -49,7 +50,7 @@ struct HelmData {
 constexpr int kHCtrMax = 32;
 
 void helm_upload_constants();  // solid-harmonic recurrence tables (this TU's __constant__)
-int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s);
+int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, const double* mu, cudaStream_t s);
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s);
 int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s);
 int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2* ops, cudaStream_t s);

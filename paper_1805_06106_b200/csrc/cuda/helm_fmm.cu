@@ -222,11 +222,40 @@ __device__ void wave_table_cta(double k, int P, double tx, double ty, double tz,
 }
 
 __global__ void k_h_gather(int64_t ns, const int* __restrict__ perm, const double* __restrict__ w,
-                           double2* __restrict__ hw) {
+                           const double* __restrict__ mu, double2* __restrict__ hw, double2* __restrict__ hmu) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const int64_t o = perm[i];
   hw[i] = make_double2(w[2 * o], w[2 * o + 1]);
+  if (mu)
+    for (int d = 0; d < 3; ++d) hmu[3 * i + d] = make_double2(mu[6 * o + 2 * d], mu[6 * o + 2 * d + 1]);
+}
+
+// Double layer on a CTA-shared wave table F (order PF >= n + 1, index n^2 + n + m):
+// mu . grad_v F_n^m by the ladder identities (dipole_terms in helm_math.cuh)
+__device__ double2 grad_dot_tab(double k, const double2* F, int PF, int n, int m, const double2 (&mu)[3]) {
+  auto at = [&](int nn, int mm) -> double2 {
+    if (nn < 0 || nn > PF || mm > nn || -mm > nn) return make_double2(0.0, 0.0);
+    return F[fi(nn, mm)];
+  };
+  const double dn = n, dm = m;
+  const double a0 = lad_sq((dn * dn - dm * dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double a1 = lad_sq(((dn + 1) * (dn + 1) - dm * dm) / ((2 * dn + 1) * (2 * dn + 3)));
+  const double c = lad_sq((dn - dm - 1) * (dn - dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double e = lad_sq((dn + dm + 1) * (dn + dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+  const double f = lad_sq((dn + dm - 1) * (dn + dm) / ((2 * dn - 1) * (2 * dn + 1)));
+  const double g = lad_sq((dn - dm + 1) * (dn - dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+  const double2 Fa = at(n - 1, m), Fb = at(n + 1, m);
+  const double2 dz = make_double2(k * (a0 * Fa.x - a1 * Fb.x), k * (a0 * Fa.y - a1 * Fb.y));
+  const double sp = m >= 0 ? -k : k, sm = m > 0 ? k : -k;
+  const double2 Fc = at(n - 1, m + 1), Fe = at(n + 1, m + 1), Ff = at(n - 1, m - 1), Fg = at(n + 1, m - 1);
+  const double2 dp = make_double2(sp * (c * Fc.x + e * Fe.x), sp * (c * Fc.y + e * Fe.y));
+  const double2 dmi = make_double2(sm * (f * Ff.x + g * Fg.x), sm * (f * Ff.y + g * Fg.y));
+  const double2 hp = make_double2(0.5 * (mu[0].x + mu[1].y), 0.5 * (mu[0].y - mu[1].x));
+  const double2 hm = make_double2(0.5 * (mu[0].x - mu[1].y), 0.5 * (mu[0].y + mu[1].x));
+  double2 t = cmul(mu[2], dz);
+  t = cfma(hp, dp, t);
+  return cfma(hm, dmi, t);
 }
 
 // Stage 2 P2M at leaves: M_b += ik w conj(R_n^m(s - c_b))
@@ -237,16 +266,27 @@ __global__ void __launch_bounds__(256) k_h_p2m(HelmData H, const int* __restrict
   const int b = boxes[blockIdx.x];
   const double4 bc = H.box[b];
   const int s0 = H.src_own_start[b], ns = H.src_own_count[b];
+  const int PF = H.hmu ? H.P + 1 : H.P;  // the double layer needs one more degree
+  rad = sm + (PF + 1) * (PF + 1);
   double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
   for (int si = 0; si < ns; ++si) {
     const double4 x = H.src[s0 + si];
     const double2 w = H.hw[s0 + si];
     __syncthreads();
-    wave_table_cta(H.k, H.P, x.x - bc.x, x.y - bc.y, x.z - bc.z, false, R, rad);
+    wave_table_cta(H.k, PF, x.x - bc.x, x.y - bc.y, x.z - bc.z, false, R, rad);
     const double2 f = make_double2(-H.k * w.y, H.k * w.x);  // ik w
     int slot = 0;
     for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot)
       acc[slot] = cfma(f, make_double2(R[i].x, -R[i].y), acc[slot]);
+    if (H.hmu) {  // + ik mu . grad_s conj(R_n^m)(s - c) = ik mu . grad R_n^{-m}
+      const double2 mu[3] = {H.hmu[3 * size_t(s0 + si)], H.hmu[3 * size_t(s0 + si) + 1], H.hmu[3 * size_t(s0 + si) + 2]};
+      slot = 0;
+      for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) {
+        int n, m;
+        nm_of(i, n, m);
+        acc[slot] = cfma(make_double2(0.0, H.k), grad_dot_tab(H.k, R, PF, n, -m, mu), acc[slot]);
+      }
+    }
   }
   int slot = 0;
   for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) H.M[size_t(b) * H.KP + i] = acc[slot];
@@ -687,6 +727,57 @@ __global__ void __launch_bounds__(128) k_h_near(HelmData H, const int* __restric
   }
 }
 
+// Double-layer part of P2QBXL (a second pass after k_h_near, same slices and fixed
+// slice-order reduction): Lc_n^m += ik mu . grad_s [h_n conj(Y_n^m)](s - c).
+template <int Q>
+__global__ void __launch_bounds__(128) k_h_near_dip(HelmData H, const int* __restrict__ boxes) {
+  constexpr int KQ = (Q + 1) * (Q + 1);
+  extern __shared__ double2 red[];  // KQ x 128
+  const int b = boxes[blockIdx.x];
+  const int nctr = H.ctr_own_count[b], c0 = H.ctr_own_start[b];
+  const int64_t sb = H.near_starts[b], se = H.near_starts[b + 1];
+  for (int cc = 0; cc < nctr; cc += 128) {
+    const int ncc = min(128, nctr - cc);
+    const int S = 128 / ncc;
+    const int ci = threadIdx.x / S, sl = threadIdx.x % S;
+    const bool active = ci < ncc;
+    double4 c = make_double4(0, 0, 0, 1);
+    if (active) c = H.ctr[c0 + cc + ci];
+    double2 acc[KQ];
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) acc[i] = make_double2(0, 0);
+    if (active) {
+      int f = sl;
+      for (int64_t sg = sb; sg < se; ++sg) {
+        const int2 seg = H.near_seg[sg];
+        for (; f < seg.y; f += S) {
+          const int s = seg.x + f;
+          const double4 x = H.src[s];
+          const double2 mu[3] = {H.hmu[3 * size_t(s)], H.hmu[3 * size_t(s) + 1], H.hmu[3 * size_t(s) + 2]};
+          dipole_terms<Q, true>(H.k, x.x - c.x, x.y - c.y, x.z - c.z, mu, make_double2(0.0, H.k), acc);
+        }
+        f -= seg.y;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) red[i * 128 + threadIdx.x] = acc[i];
+    __syncthreads();
+    if (active && sl == 0) {
+      double2* out = H.Lc + size_t(c0 + cc + ci) * KQ;
+      for (int i = 0; i < KQ; ++i) {
+        double2 sp = out[i];
+        for (int k2 = 0; k2 < S; ++k2) {
+          sp.x += red[i * 128 + threadIdx.x + k2].x;
+          sp.y += red[i * 128 + threadIdx.x + k2].y;
+        }
+        out[i] = sp;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(128) k_h_p2p(HelmData H, const int* __restrict__ boxes) {
   const int b = boxes[blockIdx.x];
   const int ntg = H.tgt_own_count[b], t0 = H.tgt_own_start[b];
@@ -702,6 +793,13 @@ __global__ void __launch_bounds__(128) k_h_p2p(HelmData H, const int* __restrict
         double s, co;
         sincos(H.k * r, &s, &co);
         acc = cfma(H.hw[seg.x + j], make_double2(co / (4.0 * kPi * r), s / (4.0 * kPi * r)), acc);
+        if (H.hmu) {
+          const double2 mu[3] = {H.hmu[3 * size_t(seg.x + j)], H.hmu[3 * size_t(seg.x + j) + 1],
+                                 H.hmu[3 * size_t(seg.x + j) + 2]};
+          const double2 v = dipole_kernel(H.k, dx, dy, dz, r, mu);
+          acc.x += v.x;
+          acc.y += v.y;
+        }
       }
     }
     H.phi[t0 + ti] = acc;
@@ -715,6 +813,8 @@ __global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict
   double2* rad = sm + H.KP;
   const int b = boxes[blockIdx.x];
   const double4 bc = H.box[b];
+  const int PF = H.hmu ? H.P + 1 : H.P;  // the double layer needs one more degree
+  rad = sm + (PF + 1) * (PF + 1);
   double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
   for (int64_t sg = H.xfar_starts[b]; sg < H.xfar_starts[b + 1]; ++sg) {
     const int2 seg = H.xfar_seg[sg];
@@ -722,13 +822,18 @@ __global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict
       const double4 x = H.src[seg.x + j];
       const double2 w = H.hw[seg.x + j];
       __syncthreads();
-      wave_table_cta(H.k, H.P, x.x - bc.x, x.y - bc.y, x.z - bc.z, true, T, rad);
+      wave_table_cta(H.k, PF, x.x - bc.x, x.y - bc.y, x.z - bc.z, true, T, rad);
       const double2 f = make_double2(-H.k * w.y, H.k * w.x);
       int slot = 0;
       for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) {
         int n, m;
         nm_of(i, n, m);
         acc[slot] = cfma(f, T[fi(n, -m)], acc[slot]);
+        if (H.hmu) {
+          const double2 mu[3] = {H.hmu[3 * size_t(seg.x + j)], H.hmu[3 * size_t(seg.x + j) + 1],
+                                 H.hmu[3 * size_t(seg.x + j) + 2]};
+          acc[slot] = cfma(make_double2(0.0, H.k), grad_dot_tab(H.k, T, PF, n, -m, mu), acc[slot]);
+        }
       }
     }
   }
@@ -1312,15 +1417,16 @@ void helm_upload_constants() {
   cudaMemcpyToSymbol(c_sd, sd, sizeof(sd));
 }
 
-int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, cudaStream_t s) {
+int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, const double* mu, cudaStream_t s) {
   if (ns == 0) return 0;
-  k_h_gather<<<unsigned((ns + 255) / 256), 256, 0, s>>>(ns, perm, w, H.hw);
+  k_h_gather<<<unsigned((ns + 255) / 256), 256, 0, s>>>(ns, perm, w, H.hmu ? mu : nullptr, H.hw, H.hmu);
   return 1;
 }
 
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s) {
   if (n == 0) return 0;
-  k_h_p2m<<<n, 256, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, leaves);
+  const int PF = H.hmu ? H.P + 1 : H.P;
+  k_h_p2m<<<n, 256, ((PF + 1) * (PF + 1) + PF + 1) * sizeof(double2), s>>>(H, leaves);
   return 1;
 }
 
@@ -1498,19 +1604,30 @@ int helm_m2l_pas(const HelmData& H, int n_tiles, const int4* tiles, const int* c
   return 2;
 }
 
+template <int Q>
+void near_dip_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
+  const size_t smem = size_t((Q + 1) * (Q + 1)) * 128 * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_h_near_dip<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_h_near_dip<Q><<<n, 128, smem, s>>>(H, boxes);
+}
+
 int helm_near(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
   switch (H.Q) {
-    case 0: near_q<0>(H, boxes, n, s); break;
-    case 1: near_q<1>(H, boxes, n, s); break;
-    case 2: near_q<2>(H, boxes, n, s); break;
-    case 3: near_q<3>(H, boxes, n, s); break;
-    case 4: near_q<4>(H, boxes, n, s); break;
-    case 5: near_q<5>(H, boxes, n, s); break;
-    case 6: near_q<6>(H, boxes, n, s); break;
+#define QBXG_HNEAR(Q)                             \
+  case Q:                                         \
+    near_q<Q>(H, boxes, n, s);                    \
+    if (H.hmu) near_dip_q<Q>(H, boxes, n, s);     \
+    break;
+    QBXG_HNEAR(0) QBXG_HNEAR(1) QBXG_HNEAR(2) QBXG_HNEAR(3) QBXG_HNEAR(4) QBXG_HNEAR(5) QBXG_HNEAR(6)
+#undef QBXG_HNEAR
     default: return -1;
   }
-  return 1;
+  return H.hmu ? 2 : 1;
 }
 
 int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
@@ -1522,14 +1639,16 @@ int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
   // warp per source (default for P <= 20); QBXG_HELM_P2L=cta keeps one CTA-wide table per source
+  // the double layer takes the CTA-wide table (one more degree for the ladder identities)
   static const bool cta = std::getenv("QBXG_HELM_P2L") && std::string(std::getenv("QBXG_HELM_P2L")) == "cta";
-  if (!cta && H.KP <= 32 * kHP2LSlots) {
+  if (!cta && !H.hmu && H.KP <= 32 * kHP2LSlots) {
     const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
     cudaFuncSetAttribute(k_h_p2l_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k_h_p2l_w<<<n, 256, smem, s>>>(H, boxes);
     return 1;
   }
-  k_h_p2l<<<n, 256, (H.KP + H.P + 1) * sizeof(double2), s>>>(H, boxes);
+  const int PF = H.hmu ? H.P + 1 : H.P;
+  k_h_p2l<<<n, 256, ((PF + 1) * (PF + 1) + PF + 1) * sizeof(double2), s>>>(H, boxes);
   return 1;
 }
 

@@ -84,6 +84,124 @@ __device__ inline void ylm_all(int P, double vx, double vy, double vz, double2* 
 }
 
 
+// j_n(x), n = 0..N in one pass (series below 1, one Miller recurrence above)
+template <int N>
+__device__ inline void sph_j_all(double x, double (&J)[N + 1]) {
+  if (x < 1.0) {
+#pragma unroll
+    for (int n = 0; n <= N; ++n) J[n] = sph_j1(n, x);
+    return;
+  }
+  const int M = N + 30 + int(x);
+  double t2 = 0.0, t1 = 1e-280, t0 = 0.0;
+#pragma unroll
+  for (int n = 0; n <= N; ++n) J[n] = 0.0;
+  double tone = 0.0;
+  for (int i = M; i >= 1; --i) {  // t_{i-1} = (2i+1)/x t_i - t_{i+1}
+    const double tm = (2.0 * i + 1.0) / x * t1 - t2;
+    t2 = t1;
+    t1 = tm;
+#pragma unroll
+    for (int n = 0; n <= N; ++n)
+      if (i - 1 == n) J[n] = tm;
+    if (i - 1 == 1) tone = tm;
+    if (fabs(t1) > 1e250) {
+      t1 *= 1e-250;
+      t2 *= 1e-250;
+      tone *= 1e-250;
+#pragma unroll
+      for (int n = 0; n <= N; ++n) J[n] *= 1e-250;
+    }
+  }
+  t0 = t1;
+  const double j0 = sin(x) / x, j1 = sin(x) / (x * x) - cos(x) / x;
+  const double f = fabs(j0) > fabs(j1) ? j0 / t0 : j1 / tone;
+#pragma unroll
+  for (int n = 0; n <= N; ++n) J[n] *= f;
+}
+
+// Double layer: acc[fi(n, m)] += fk * (mu . grad_v F_n^{-m}(v)), n <= N, for the wave
+// functions F_n^m = f_n(k|v|) Y_n^m(v) (f = h_n when SING, else j_n), by the ladder
+// identities of oracle/helm_oracle.cpp grad_dot (mu complex: m_x, m_y, m_z):
+//   mu . grad = mu_z d_z + (mu_x - i mu_y)/2 (d_x + i d_y) + (mu_x + i mu_y)/2 (d_x - i d_y).
+// The P2M / P2L / P2QBXL dipole coefficient of a source s about c is ik times this at
+// v = s - c (conj(F_n^m) of the monopole formula is F_n^{-m} up to the radial conjugate,
+// which the identities never touch).  Per-thread, generic; used by the double-layer
+// passes and the unaccelerated paths, not by the single-layer hot kernels.
+__device__ __forceinline__ double lad_sq(double x) { return x > 0.0 ? sqrt(x) : 0.0; }
+
+template <int N, bool SING>
+__device__ inline void dipole_terms(double k, double vx, double vy, double vz, const double2 (&mu)[3], double2 fk,
+                                   double2* acc) {
+  constexpr int N1 = N + 1;
+  double2 Y[(N1 + 1) * (N1 + 1)];
+  ylm_all(N1, vx, vy, vz, Y);
+  const double x = k * sqrt(vx * vx + vy * vy + vz * vz);
+  double J[N1 + 1];
+  sph_j_all<N1>(x, J);
+  double yv[N1 + 1];
+  if (SING) {
+    double ym = -cos(x) / x, y0 = -cos(x) / (x * x) - sin(x) / x;
+#pragma unroll
+    for (int n = 0; n <= N1; ++n) {
+      if (n == 0) {
+        yv[n] = ym;
+      } else if (n == 1) {
+        yv[n] = y0;
+      } else {
+        const double yn = (2.0 * n - 1.0) / x * y0 - ym;
+        ym = y0;
+        y0 = yn;
+        yv[n] = yn;
+      }
+    }
+  }
+  auto F = [&](int n, int m) -> double2 {
+    if (n < 0 || n > N1 || m > n || -m > n) return make_double2(0.0, 0.0);
+    const double2 y = Y[fi(n, m)];
+    if (!SING) return make_double2(J[n] * y.x, J[n] * y.y);
+    return cmul(make_double2(J[n], yv[n]), y);
+  };
+  // (mu_x - i mu_y) / 2 and (mu_x + i mu_y) / 2
+  const double2 hp = make_double2(0.5 * (mu[0].x + mu[1].y), 0.5 * (mu[0].y - mu[1].x));
+  const double2 hm = make_double2(0.5 * (mu[0].x - mu[1].y), 0.5 * (mu[0].y + mu[1].x));
+#pragma unroll
+  for (int n = 0; n <= N; ++n)
+#pragma unroll
+    for (int mo = -n; mo <= n; ++mo) {
+      const int m = -mo;  // gradient of F_n^{-mo}
+      const double dn = n, dm = m;
+      const double a0 = lad_sq((dn * dn - dm * dm) / ((2 * dn - 1) * (2 * dn + 1)));
+      const double a1 = lad_sq(((dn + 1) * (dn + 1) - dm * dm) / ((2 * dn + 1) * (2 * dn + 3)));
+      const double c = lad_sq((dn - dm - 1) * (dn - dm) / ((2 * dn - 1) * (2 * dn + 1)));
+      const double e = lad_sq((dn + dm + 1) * (dn + dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+      const double f = lad_sq((dn + dm - 1) * (dn + dm) / ((2 * dn - 1) * (2 * dn + 1)));
+      const double g = lad_sq((dn - dm + 1) * (dn - dm + 2) / ((2 * dn + 1) * (2 * dn + 3)));
+      const double2 Fa = F(n - 1, m), Fb = F(n + 1, m);
+      const double2 dz = make_double2(k * (a0 * Fa.x - a1 * Fb.x), k * (a0 * Fa.y - a1 * Fb.y));
+      const double sp = m >= 0 ? -k : k, sm = m > 0 ? k : -k;
+      const double2 Fc = F(n - 1, m + 1), Fe = F(n + 1, m + 1), Ff = F(n - 1, m - 1), Fg = F(n + 1, m - 1);
+      const double2 dp = make_double2(sp * (c * Fc.x + e * Fe.x), sp * (c * Fc.y + e * Fe.y));
+      const double2 dmi = make_double2(sm * (f * Ff.x + g * Fg.x), sm * (f * Ff.y + g * Fg.y));
+      double2 t = cmul(mu[2], dz);
+      t = cfma(hp, dp, t);
+      t = cfma(hm, dmi, t);
+      acc[fi(n, mo)] = cfma(fk, t, acc[fi(n, mo)]);
+    }
+}
+
+// the closed-form double-layer kernel: m . grad_y G_k(x, y) = m.(x - y) (1 - i k r) e^{ikr} / (4 pi r^3)
+__device__ __forceinline__ double2 dipole_kernel(double k, double dx, double dy, double dz, double r,
+                                                 const double2 (&mu)[3]) {
+  const double2 md = make_double2(mu[0].x * dx + mu[1].x * dy + mu[2].x * dz, mu[0].y * dx + mu[1].y * dy + mu[2].y * dz);
+  double s, c;
+  sincos(k * r, &s, &c);
+  const double f = 1.0 / (4.0 * kPi * r * r * r);
+  // (1 - i k r)(c + i s) = (c + k r s) + i (s - k r c)
+  const double2 e = make_double2((c + k * r * s) * f, (s - k * r * c) * f);
+  return cmul(md, e);
+}
+
 __device__ __forceinline__ double2 ipow(int e) {
   switch (e & 3) {
     case 0: return make_double2(1, 0);

@@ -300,95 +300,158 @@ __device__ __forceinline__ void near_pair(const double4 x, const double4 u, cons
 }
 
 // P2QBXL: L~_c += (1/r)[w conj(I(u)) + conj(mu . grad I(u)) / r], u = (s - c)/r   (Eq. (8))
-// GEN: S = floor(128 / n_centres) slices per centre (not only powers of two) so
-// up to ~all 128 lanes are busy; the slices are then summed through shared
-// memory in slice order (deterministic) instead of by width-S shuffles.
-template <int Q, bool DIP, int U, bool GEN>
+//
+// Work split.  A box's near sources (its flattened U u W_close u X_close list) are
+// processed in K = ceil(n / 256) chunks of one even length L <= 256 (the last padded
+// with zero-weight sources at a remote point, which contribute exactly 0).  Per chunk
+// the (centre, source) pairs, centre-major, are cut into kNearThreads equal even-length
+// ranges, the same cut every chunk: every lane does the same work whatever the centre
+// count (S = floor(128 / n_centres) slices per centre left up to half the lanes idle).
+// A range holds the thread's home centre and possibly the head of the next centre;
+// that head is accumulated after saving the home sums, and parked (added, in chunk
+// order) in that centre's output row -- only one thread straddles each centre
+// boundary, so the row has one writer.  At the end each centre sums its parked part
+// and its home threads' partial sums in thread order: a fixed order, bitwise
+// reproducible.  Sources are staged in shared memory by cp.async, one chunk ahead.
+constexpr int kNearBuf = 2;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <bool DIP>
+__device__ __forceinline__ void near_stage(const DevData& D, const int* __restrict__ list, int nsrc, int k, int L,
+                                           double4* s_src, double4* s_mu) {
+  for (int f = threadIdx.x; f < L; f += kNearThreads) {
+    const int g = k * L + f;
+    if (g < nsrc) {
+      const int si = __ldg(list + g);
+      cp_async16(&s_src[f], &D.src[si]);
+      cp_async16(reinterpret_cast<char*>(&s_src[f]) + 16, reinterpret_cast<const char*>(&D.src[si]) + 16);
+      if (DIP) {
+        cp_async16(&s_mu[f], &D.mu[si]);
+        cp_async16(reinterpret_cast<char*>(&s_mu[f]) + 16, reinterpret_cast<const char*>(&D.mu[si]) + 16);
+      }
+    } else {  // padding: zero weight and moment far away (every term is an exact 0)
+      s_src[f] = make_double4(1e30, 1e30, 1e30, 0.0);
+      if (DIP) s_mu[f] = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int Q, bool DIP>
 __global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevData D, const int* __restrict__ boxes) {
-  constexpr int KQ = hsize(Q);
-  extern __shared__ double s_part[];  // GEN: 2 KQ x kNearThreads partial sums
-  __shared__ int s_start[kMaxSeg], s_pre[kMaxSeg + 1];
-  __shared__ double4 s_src[kNearChunk];
-  __shared__ double4 s_mu[DIP ? kNearChunk : 1];
+  constexpr int KQ = hsize(Q), KY = KQ - (Q + 1);  // Re parts, Im parts of m >= 1
+  extern __shared__ double s_part[];                // (KQ + KY) x kNearThreads: saved / partial sums
+  __shared__ double4 s_src[kNearBuf][kNearChunk];
+  __shared__ double4 s_mu[kNearBuf][DIP ? kNearChunk : 1];
   const int b = boxes[blockIdx.x];
   const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
-  const int64_t sb = D.near_starts[b], se = D.near_starts[b + 1];
+  const int nsrc = D.near_nsrc[b];
+  const int* __restrict__ list = D.near_src + D.near_off[b];
+  const int tid = threadIdx.x;
+  const int K = (nsrc + kNearChunk - 1) / kNearChunk;
+  const int L = K ? 2 * ((nsrc + 2 * K - 1) / (2 * K)) : 0;  // even, <= kNearChunk
+  auto save = [&](const double* ax, const double* ay) {
+    int k = 0;
+#pragma unroll
+    for (int n = 0; n <= Q; ++n)
+#pragma unroll
+      for (int m = 0; m <= n; ++m) {
+        s_part[k++ * kNearThreads + tid] = ax[hidx(n, m)];
+        if (m > 0) s_part[k++ * kNearThreads + tid] = ay[hidx(n, m)];
+      }
+  };
+  auto restore = [&](double* ax, double* ay) {
+    int k = 0;
+#pragma unroll
+    for (int n = 0; n <= Q; ++n)
+#pragma unroll
+      for (int m = 0; m <= n; ++m) {
+        ax[hidx(n, m)] = s_part[k++ * kNearThreads + tid];
+        if (m > 0) ay[hidx(n, m)] = s_part[k++ * kNearThreads + tid];
+      }
+  };
   for (int cc = 0; cc < nctr; cc += kNearThreads) {
     const int ncc = min(kNearThreads, nctr - cc);
-    int S = 1;
-    if (GEN) {
-      S = kNearThreads / ncc;
-    } else {
-      while (S * 2 * ncc <= kNearThreads && S < 32) S *= 2;
-    }
-    const int ci = threadIdx.x / S, sl = threadIdx.x % S;
-    const bool active = ci < ncc;
+    double2* const out = D.Lc + size_t(c0 + cc) * KQ;
+    const int total = ncc * L;                                       // pairs per chunk
+    const int W = 2 * ((total + 2 * kNearThreads - 1) / (2 * kNearThreads));  // even, <= L
+    const int t0 = min(total, tid * W), nw = min(W, total - t0);     // this thread's pairs
+    const int home = L ? t0 / L : 0;
+    const int sw = L ? (home + 1) * L - t0 : 0;                      // pairs before the next centre
+    const bool straddle = nw > sw;
+    for (int c = tid; c < ncc; c += kNearThreads)
+      for (int i = 0; i < KQ; ++i) out[size_t(c) * KQ + i] = make_double2(0.0, 0.0);
     double4 c = make_double4(0, 0, 0, 1);
-    if (active) c = D.ctr[c0 + cc + ci];
-    const double ir = 1.0 / c.w;
+    if (nw > 0) c = D.ctr[c0 + cc + home];
+    double ir = 1.0 / c.w;
     double ax[KQ], ay[KQ];
 #pragma unroll
     for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
-    for (int64_t s0 = sb; s0 < se; s0 += kMaxSeg) {
-      const int nseg = int(se - s0 < kMaxSeg ? se - s0 : kMaxSeg);
-      __syncthreads();
-      const int total = load_segments(D.near_seg, s0, nseg, s_start, s_pre);
-      for (int ch = 0; ch < total; ch += kNearChunk) {
-        const int nch = min(kNearChunk, total - ch);
-        __syncthreads();
-        for (int f = threadIdx.x; f < nch; f += kNearThreads) {
-          const int s = seg_source(ch + f, nseg, s_start, s_pre);
-          s_src[f] = D.src[s];
-          if (DIP) s_mu[f] = D.mu[s];
+    __syncthreads();  // previous group's s_part reads and buffers done; rows zeroed
+    if (K > 0) near_stage<DIP>(D, list, nsrc, 0, L, s_src[0], s_mu[0]);
+    for (int k = 0; k < K; ++k) {
+      const int buf = k & 1;
+      cp_async_wait_all();
+      __syncthreads();  // chunk k staged; everyone is past chunk k - 1
+      if (k + 1 < K) near_stage<DIP>(D, list, nsrc, k + 1, L, s_src[buf ^ 1], s_mu[buf ^ 1]);
+      const double4* S = s_src[buf];
+      const double4* U = s_mu[buf];
+      int j = t0 - home * L;  // chunk slot of the thread's first pair
+      for (int i = 0; i < nw; i += 2, j += 2) {
+        if (i == sw) {  // the next centre's head: save the home sums, start from zero
+          save(ax, ay);
+#pragma unroll
+          for (int q = 0; q < KQ; ++q) ax[q] = ay[q] = 0.0;
+          c = D.ctr[c0 + cc + home + 1];
+          ir = 1.0 / c.w;
+          j = 0;
         }
-        __syncthreads();
-        if (active) {
-          int j = sl;
-          if (U == 2) {  // two independent pairs in flight per iteration (ILP)
-            for (; j + S < nch; j += 2 * S) {
-              near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
-              near_pair<Q, DIP>(s_src[j + S], DIP ? s_mu[j + S] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
-            }
-          }
-          for (; j < nch; j += S)
-            near_pair<Q, DIP>(s_src[j], DIP ? s_mu[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+        near_pair<Q, DIP>(S[j], DIP ? U[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+        near_pair<Q, DIP>(S[j + 1], DIP ? U[j + 1] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+      }
+      if (straddle) {  // park the head in its centre's row (one writer per row), back to home
+        double2* o = out + size_t(home + 1) * KQ;
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+          const double2 v = o[q];
+          o[q] = make_double2(v.x + ax[q], v.y + ay[q]);
         }
+        restore(ax, ay);
+        c = D.ctr[c0 + cc + home];
+        ir = 1.0 / c.w;
       }
     }
-    if (GEN) {
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < KQ; ++i) {
-        s_part[(2 * i) * kNearThreads + threadIdx.x] = ax[i];
-        s_part[(2 * i + 1) * kNearThreads + threadIdx.x] = ay[i];
+    __syncthreads();
+    save(ax, ay);  // home partial sums (zero for idle threads)
+    __syncthreads();
+    for (int ci = tid; ci < ncc; ci += kNearThreads) {
+      double2* o = out + size_t(ci) * KQ;
+      const double irc = 1.0 / D.ctr[c0 + cc + ci].w;
+      int t_lo = 0, t_hi = 0;
+      if (W > 0) {
+        t_lo = (ci * L + W - 1) / W;
+        t_hi = min(kNearThreads, ((ci + 1) * L + W - 1) / W);
       }
-      __syncthreads();
-      if (active && sl == 0) {
-        double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
-        for (int i = 0; i < KQ; ++i) {
-          double sx = 0, sy = 0;
-          for (int k = 0; k < S; ++k) {
-            sx += s_part[(2 * i) * kNearThreads + threadIdx.x + k];
-            sy += s_part[(2 * i + 1) * kNearThreads + threadIdx.x + k];
+      int k = 0;
+      for (int n = 0; n <= Q; ++n)
+        for (int m = 0; m <= n; ++m) {
+          const int q = hidx(n, m);
+          const double2 pk = o[q];
+          double sx = pk.x, sy = pk.y;
+          for (int t = t_lo; t < t_hi; ++t) sx += s_part[k * kNearThreads + t];
+          ++k;
+          if (m > 0) {
+            for (int t = t_lo; t < t_hi; ++t) sy += s_part[k * kNearThreads + t];
+            ++k;
           }
-          out[i] = make_double2(sx * ir, sy * ir);
+          o[q] = make_double2(sx * irc, sy * irc);
         }
-      }
-      __syncthreads();
-    } else {
-      // reduce over the S slices of each centre (contiguous lanes, S <= 32)
-      for (int off = S >> 1; off > 0; off >>= 1) {
-#pragma unroll
-        for (int i = 0; i < KQ; ++i) {
-          ax[i] += __shfl_xor_sync(0xffffffffu, ax[i], off, S);
-          ay[i] += __shfl_xor_sync(0xffffffffu, ay[i], off, S);
-        }
-      }
-      if (active && sl == 0) {
-        double2* out = D.Lc + size_t(c0 + cc + ci) * KQ;
-#pragma unroll
-        for (int i = 0; i < KQ; ++i) out[i] = make_double2(ax[i] * ir, ay[i] * ir);
-      }
     }
   }
 }
@@ -604,46 +667,6 @@ __global__ void __launch_bounds__(kNearThreads) k_near_p2p(DevData D, const int*
   }
 }
 
-// ---------------------------------------------------------------- M2L (Stage 4)
-// L~_b(n,m) += (1/h)(-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}(2 delta)
-__global__ void __launch_bounds__(256) k_m2l(DevData D, const int* __restrict__ boxes) {
-  extern __shared__ double2 sm[];
-  double2* Md = sm;               // kp
-  double2* T = sm + D.kp;         // ktab_m2l
-  const int b = boxes[blockIdx.x];
-  const double ih = 1.0 / D.box[b].w;
-  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-  for (int64_t e = D.v_starts[b]; e < D.v_starts[b + 1]; ++e) {
-    const int2 ent = D.v_ent[e];
-    __syncthreads();
-    for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(ent.x) * D.kp + i];
-    for (int i = threadIdx.x; i < D.ktab_m2l; i += blockDim.x) T[i] = D.m2l_tab[size_t(ent.y) * D.ktab_m2l + i];
-    __syncthreads();
-    int slot = 0;
-    for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
-      int n, m;
-      idx_nm(c, n, m);
-      double sx = 0, sy = 0;
-      for (int j = 0; j <= D.p; ++j)
-        for (int k = -j; k <= j; ++k) {
-          const double2 a = hget(Md, j, k);
-          const double2 t = hget(T, j + n, k - m);
-          sx += a.x * t.x - a.y * t.y;
-          sy += a.x * t.y + a.y * t.x;
-        }
-      const double sg = ((n + m) & 1) ? -1.0 : 1.0;
-      acc[slot].x += sg * sx;
-      acc[slot].y += sg * sy;
-    }
-  }
-  int slot = 0;
-  for (int c = threadIdx.x; c < D.kp; c += blockDim.x, ++slot) {
-    double2 v = D.L[size_t(b) * D.kp + c];
-    v.x += acc[slot].x * ih;
-    v.y += acc[slot].y * ih;
-    D.L[size_t(b) * D.kp + c] = v;
-  }
-}
 
 // ---------------------------------------------------------------- W far (Stage 5b)
 // M2QBXL: L~_c(n,m) += (r/h)^n (1/h)(-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}((c - c_d)/h)
@@ -1327,38 +1350,17 @@ __global__ void __launch_bounds__(256) k_direct_sum(int ns, const double4* __res
 
 template <int Q>
 void near_qbx_q(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  // QBXG_NEAR_MODE: 2 (default) generic slice count, 1 power-of-two slices + 2 pairs
-  // in flight, 0 power-of-two slices, one pair at a time
-  static const int mode = [] {
-    const char* e = std::getenv("QBXG_NEAR_MODE");
-    return e ? std::atoi(e) : 2;
-  }();
-  if (mode == 2) {
-    // QBXG_NEAR_SMEM_KB pads the dynamic shared memory to cap near-field CTAs per SM
-    // (experiment: leave room for co-resident M2L CTAs when the two overlap)
-    static const size_t pad = std::getenv("QBXG_NEAR_SMEM_KB") ? size_t(std::atoi(std::getenv("QBXG_NEAR_SMEM_KB"))) * 1024 : 0;
-    const size_t smem = std::max(size_t(2) * hsize(Q) * kNearThreads * sizeof(double), pad);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_near_qbx<Q, true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_near_qbx<Q, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      attr = true;
-    }
-    if (D.dipole)
-      k_near_qbx<Q, true, 2, true><<<n, kNearThreads, smem, s>>>(D, boxes);
-    else
-      k_near_qbx<Q, false, 2, true><<<n, kNearThreads, smem, s>>>(D, boxes);
-  } else if (mode == 1) {
-    if (D.dipole)
-      k_near_qbx<Q, true, 2, false><<<n, kNearThreads, 0, s>>>(D, boxes);
-    else
-      k_near_qbx<Q, false, 2, false><<<n, kNearThreads, 0, s>>>(D, boxes);
-  } else {
-    if (D.dipole)
-      k_near_qbx<Q, true, 1, false><<<n, kNearThreads, 0, s>>>(D, boxes);
-    else
-      k_near_qbx<Q, false, 1, false><<<n, kNearThreads, 0, s>>>(D, boxes);
+  const size_t smem = size_t(2 * hsize(Q) - (Q + 1)) * kNearThreads * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_near_qbx<Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_near_qbx<Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
   }
+  if (D.dipole)
+    k_near_qbx<Q, true><<<n, kNearThreads, smem, s>>>(D, boxes);
+  else
+    k_near_qbx<Q, false><<<n, kNearThreads, smem, s>>>(D, boxes);
 }
 
 int block_for(int k) { return k <= 128 ? 128 : 256; }
@@ -1489,13 +1491,6 @@ int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-int launch_m2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (n == 0) return 0;
-  const size_t smem = (D.kp + D.ktab_m2l) * sizeof(double2);
-  k_m2l<<<n, block_for(D.kp), smem, s>>>(D, boxes);
-  return 1;
-}
-
 int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
   const size_t smem = (D.kp + kWfarGroup * hsize(D.p + D.q)) * sizeof(double2);
@@ -1590,7 +1585,6 @@ void set_smem_limits() {
   const int lim = 200 * 1024;
   cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_wfar, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);

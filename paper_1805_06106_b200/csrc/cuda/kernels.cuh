@@ -39,6 +39,9 @@ struct DevData {
   // lists (device CSR)
   const int64_t* near_starts;  // per box -> segments (src_start, src_count) of U u W_close u X_close
   const int2* near_seg;
+  const int* near_nsrc;        // per box: sources over its near segments
+  const int64_t* near_off;     // per box: offset of its flattened near-source list in near_src
+  const int* near_src;         // flattened near-source lists (box-sorted source indices)
   const int64_t* xfar_starts;  // per box -> segments of X_far
   const int2* xfar_seg;
   const int64_t* v_starts;     // per box -> (source box, offset index)
@@ -52,62 +55,41 @@ struct DevData {
   unsigned int* bad;       // set by Stage 9 when a potential / centre coefficient is non-finite
 };
 
-// Dense per-offset M2L (m2l_gemm.cu).  Work is split into chunks of target
+// Stage 4 M2L (m2l_pas.cu): point-and-shoot on real half-table blocks, tiles of
+// same-offset List-2 entries, one operator set per offset class (rho_xy^2, dz), staged
+// rows summed per box by k_m2l_reduce.  Work is split into chunks of whole target
 // boxes (contiguous in List-2 CSR order) so the staging buffer stays bounded.
 struct M2LChunk {
   int n_tiles = 0;
-  int4* tiles = nullptr;       // (operator index, first column, column count, 0)
+  int4* tiles = nullptr;       // (offset, first column, column count, class)
   int* col_src = nullptr;      // source box of each column (offset-sorted)
   int* col_pos = nullptr;      // List-2 CSR position (relative to base) of each column
-  double* col_scale = nullptr; // 1/|b| of the target box
   int n_boxes = 0;
   int* boxes = nullptr;        // target boxes of the chunk
   int64_t base = 0;            // first CSR position of the chunk
 };
+constexpr int kMaxPasOrder = 21;
 struct M2LPlan {
-  int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64
-  int n_ops = 0;               // used offsets
-  int bn = 32;                 // columns per GEMM tile (64: 1 CTA/SM, 32: 2 CTAs/SM; 32 measured faster)
-  double* ops = nullptr;       // n_ops x KRp x KRp
+  int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64 (tree-shift GEMMs)
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
-  double* temp = nullptr;      // staging: max chunk entries x KRp
+  double* temp = nullptr;      // staging: tree-shift rows (KRp), and the M2L's rows (srow doubles each)
+  int srow = 0;                // M2L staging row length: (p+1)^2 rounded up to 16 doubles
   std::vector<M2LChunk> chunks;
-  // azimuthally split variant (default): two real hsize(p) blocks per offset
-  bool split = false;
-  double* sops = nullptr;      // n_ops x 2NH x NH (Re block rows, then Im block rows)
-  double2* cs = nullptr;       // n_ops x (p+1): (cos k alpha, sin k alpha)
-  int* ent_op = nullptr;       // operator index of every List-2 CSR entry
-  int srow = 0;                // staging row length (doubles)
-  // rotation (point-and-shoot) variant, m2l_rot.cu
-  bool rot = false;
-  double* rotF = nullptr;      // n_ops x rot_stride: multipole rotation blocks (v -> +z)
-  double* rotB = nullptr;      // n_ops x rot_stride: local back-rotation blocks
-  double* rho_op = nullptr;    // n_ops: |v| in box units
-  size_t rot_stride = 0;
-  // point-and-shoot in the azimuthal frame on real half-table blocks (m2l_pas.cu):
-  // replaces the split GEMM, same staging rows and reduce
-  bool pas = false;
-  double* pas_ops = nullptr;   // n_ops x pas_stride: [W | Z | V]
+  int n_offsets = 0, n_classes = 0;
+  double2* cs = nullptr;       // n_offsets x (p+1): (cos k alpha, sin k alpha)
+  int* ent_op = nullptr;       // offset id of every List-2 CSR entry
+  double* pas_ops = nullptr;   // n_classes x pas_stride: [W | Z | V]
   int pas_stride = 0, pas_phase = 0, pas_nblk = 0;
-  int* pas_tab = nullptr;      // block row sets and per-unit segment schedule
+  int* pas_tab = nullptr;      // block row sets and per-warp block lists of the three phases
   int pas_tab_n = 0;
   int pas_base[3] = {0, 0, 0};
 };
 bool pas_supported(int p);
 int pas_tile_cols();
-void pas_build_ops(int p, int n_ops, const int* used_slot, std::vector<double>& ops, int& op_stride,
-                   std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]);
-int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const double* X, int kp2, int p, cudaStream_t s);
-int launch_m2l_rot_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
-// rotation blocks staged once per CTA; tiles of up to kRotSuper same-offset columns
-constexpr int kRotSuper = 256;
-int launch_m2l_rot2_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
-bool m2l_rot3_ok(int p);
-bool m2l_rot4_ok(int p);
-int launch_m2l_rot4_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
-int launch_m2l_rot3_chunk(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
-size_t m2l_rot_smem(int p, int bn);
-int launch_m2l_ops(const M2LPlan& P, int p, const int* used_slot, const int4* rdof, cudaStream_t s);
+void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std::vector<double>& ops,
+                   int& op_stride, std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]);
+int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
+int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s);
 
 // Tree shifts (Stage 2 M2M, Stage 7 L2L) as DMMA GEMMs over 8 octant operators:
 // one level = tiles of same-octant columns, staged rows, segmented reduce.
@@ -124,16 +106,6 @@ struct ShiftLevel {
 int launch_shift_ops(int mode, int p, int KR, int KRp, const int4* rdof, double* ops, cudaStream_t s);
 int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops, double2* X, int kp, bool accumulate,
                        cudaStream_t s);
-int launch_m2l_dense(const M2LPlan& P, const DevData& D, cudaStream_t s);
-int split_nh(int p);  // padded block size of the split M2L (multiple of 48)
-int split_tile_cols();  // columns per split-M2L tile
-int split_nhi(int p, int NH);  // rows of the compacted Im block
-int launch_m2l_ops_split(const M2LPlan& P, int p, const int* used_slot, cudaStream_t s);
-
-// Box expansion -> centre locals as DMMA GEMMs (centre_gemm.cu); items are
-// (box, first centre offset) chunks of up to 16 centres.
-bool ctr_gemm_fits(int p, int q, bool irreg);
-int launch_ctr_gemm(const DevData& D, const int2* items, int n_items, bool irreg, cudaStream_t s);
 
 // Thread-per-centre translations (centre_trans.cu)
 int launch_wfar2(const DevData& D, const int* ctr_boxes, int n_ctr, const int* tgt_boxes, int n_tgt,
@@ -181,7 +153,6 @@ int launch_near_qbx_batch(const DevData& D, const int* boxes, int n, int NR, con
 int launch_m2m(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s);
-int launch_m2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_l2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
@@ -203,10 +174,10 @@ int launch_direct_qbx(int q, int ns, const double4* src, const double4* mu, int 
                       double2* Lc, cudaStream_t s);
 int launch_direct_qbx_eval(int q, int n, const double* tpos, const int* assoc, const double4* ctr,
                            const double2* Lc, double* pot, cudaStream_t s);
-// Helmholtz single layer, unaccelerated (helm.cu): complex weights / potentials
-int launch_helm_direct_sum(double k, int ns, const double4* src, const double2* w, int nt, const double4* tgt,
-                           double2* pot, unsigned long long* bad, cudaStream_t s);
-int launch_helm_direct_qbx(double k, int q, int ns, const double4* src, const double2* w, int nc,
+// Helmholtz single (+ double) layer, unaccelerated (helm.cu): complex weights / dipoles / potentials
+int launch_helm_direct_sum(double k, int ns, const double4* src, const double2* w, const double2* mu, int nt,
+                           const double4* tgt, double2* pot, unsigned long long* bad, cudaStream_t s);
+int launch_helm_direct_qbx(double k, int q, int ns, const double4* src, const double2* w, const double2* mu, int nc,
                            const double4* ctr, double2* Lc, int nt, const double* tpos, const int* assoc,
                            double2* pot, cudaStream_t s);
 void upload_constants();

@@ -50,9 +50,9 @@ void validate_inputs(const qbxg_config& cfg, const qbxg_geometry& g) {
     throw InvalidArgument("FmmConfig: t_f must satisfy 0 <= t_f < 2 sqrt(3) - 2 (SPEC.md:416)");
   if (cfg.n_max < 1) throw InvalidArgument("FmmConfig: n_max must be positive");
   if (cfg.kernel != QBXG_KERNEL_LAPLACE_SL && cfg.kernel != QBXG_KERNEL_LAPLACE_SL_DL &&
-      cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL)
+      cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL && cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL_DL)
     throw InvalidArgument("FmmConfig: unknown kernel");
-  if (cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL && !(cfg.helmholtz_k > 0 && std::isfinite(cfg.helmholtz_k)))
+  if ((cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL || cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL_DL) && !(cfg.helmholtz_k > 0 && std::isfinite(cfg.helmholtz_k)))
     throw InvalidArgument("FmmConfig: Helmholtz needs a positive wavenumber helmholtz_k");
   if (cfg.reserved != 0) throw InvalidArgument("FmmConfig: level restriction not implemented");
   if (g.n_sources < 0 || g.n_centers < 0 || g.n_targets < 0) throw InvalidArgument("geometry: negative size");

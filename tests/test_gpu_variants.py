@@ -1,6 +1,6 @@
-"""Every selectable kernel variant (the QBXG_* switches listed in profiles/r01_summary.md)
-stays parity-green against the oracle.  Each variant runs in its own process because
-several switches are read once per process."""
+"""Test hooks that change how work is split (not what is computed) stay parity-green
+against the oracle.  Each runs in its own process because the switches are read at
+engine creation."""
 import json
 import os
 import subprocess
@@ -36,32 +36,8 @@ print(json.dumps(out))
 """ % ROOT
 
 VARIANTS = [
-    {"QBXG_M2L_MODE": "dense"},
-    {"QBXG_M2L_MODE": "dense", "QBXG_M2L_BN": "64"},
-    {"QBXG_M2L_MODE": "split", "QBXG_SPLIT_V1": "1"},
-    {"QBXG_M2L_MODE": "rot"},
-    {"QBXG_M2L_MODE": "rot", "QBXG_M2L_ROTV": "3"},
-    {"QBXG_M2L_MODE": "split"},
-    {"QBXG_PAS_V2": "1"},
-    {"QBXG_PAS_SWZ": "1"},
-    {"QBXG_PAS_V3": "8"},
-    {"QBXG_PAS_V3": "16", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
-    {"QBXG_PAS_V2": "1", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
-    {"QBXG_M2L_MODE": "split", "QBXG_M2L_CHUNK_ENTRIES": "5000"},
-    {"QBXG_NEAR_MODE": "0"},
-    {"QBXG_NEAR_MODE": "1"},
-    {"QBXG_P2L_LEGACY": "1"},
-    {"QBXG_L2Q_MODE": "0"},
-    {"QBXG_L2Q_MODE": "1"},
-    {"QBXG_L2Q_MODE": "2"},
-    {"QBXG_WFAR_MODE": "0"},
-    {"QBXG_SHIFT_MODE": "1"},
-    {"QBXG_CTR_MODE": "1"},
-    {"QBXG_CTR_MODE": "2"},
-    {"QBXG_M2L_NAIVE": "1"},
-    {"QBXG_M2L_CHUNK_ENTRIES": "5000"},
-    {"QBXG_OVERLAP": "1"},
-    {"QBXG_OVERLAP": "2"},
+    {"QBXG_M2L_CHUNK_ENTRIES": "5000"},  # many M2L chunks: staging rows reused, counters reset per chunk
+    {"QBXG_M2L_CHUNK_ENTRIES": "300"},
 ]
 
 HELM_SCRIPT = r"""

@@ -1,4 +1,6 @@
-"""Helmholtz single layer (BASELINE config 3): the complex128 CPU
+"""Helmholtz single and double layer (BASELINE config 3; north_star
+"Helmholtz single- and double-layer"; the Brakhage-Werner representation of
+PAPER.md:3074-3075 is S(-i eta mu) + D(mu)): the complex128 CPU
 oracle (oracle/helm_oracle.cpp) pinned against analytic anchors, since no reference
 implementation exists (parity unpinned):
 special functions and Gaunt coefficients against scipy, the Gegenbauer expansion and
@@ -99,6 +101,76 @@ def test_fmm_converges_to_direct_qbx():
     assert errs[2] < 1e-5, errs
 
 
+def _dl_inputs(n, seed, scale=0.1):
+    rng = np.random.default_rng(seed)
+    src = rng.normal(size=(n, 3)) * scale
+    w = rng.normal(size=n) + 1j * rng.normal(size=n)
+    mu = rng.normal(size=(n, 3)) + 1j * rng.normal(size=(n, 3))
+    return src, w, mu
+
+
+def test_dipole_ladder_identities_vs_finite_differences():
+    """The oracle's dipole expansion terms (mu . grad_s of the source's multipole / local
+    coefficients, via the ladder identities of helm_oracle.cpp grad_dot) against
+    4th-order central differences of the monopole coefficients."""
+    rng = np.random.default_rng(7)
+    for kind, c in ((0, np.array([0.02, -0.01, 0.03])), (1, np.array([1.1, 0.6, -0.4]))):
+        for _ in range(3):
+            s = rng.normal(size=(1, 3)) * 0.2
+            mu = rng.normal(size=(1, 3)) + 1j * rng.normal(size=(1, 3))
+            P = 12
+            dl = O.helm_form(kind, K, s, np.zeros(1), c, P, mu=mu)
+            h = 1e-3
+            fd = np.zeros_like(dl)
+            for d in range(3):
+                e = np.zeros((1, 3))
+                e[0, d] = h
+                f = [O.helm_form(kind, K, s + j * e, np.ones(1), c, P) for j in (-2, -1, 1, 2)]
+                fd = fd + mu[0, d] * (f[0] - 8 * f[1] + 8 * f[2] - f[3]) / (12 * h)
+            assert np.linalg.norm(dl - fd) <= 1e-9 * np.linalg.norm(fd), (kind, np.linalg.norm(dl - fd))
+
+
+def test_double_layer_expansions_vs_direct_sum():
+    """Multipole (P2M) and local (P2L) expansions of monopoles + dipoles reproduce the
+    closed-form kernel w G_k + mu . grad_y G_k = [w + mu.(x-y)(1 - ikr)/r^2] e^{ikr}/(4 pi r)."""
+    src, w, mu = _dl_inputs(25, 5)
+    c, P = np.zeros(3), 18
+    t_far = np.array([1.4, -0.6, 1.0])
+    direct = O.helm_direct_sum(K, src, w, t_far[None], mu=mu)[0]
+    M = O.helm_form(0, K, src, w, c, P, mu=mu)
+    assert abs(O.helm_eval(0, K, M, P, c, t_far) - direct) < 1e-11 * abs(direct)
+    far = src + np.array([2.0, 0.0, 0.0])
+    tn = np.array([0.05, -0.08, 0.03])
+    L = O.helm_form(1, K, far, w, c, P, mu=mu)
+    ref = O.helm_direct_sum(K, far, w, tn[None], mu=mu)[0]
+    assert abs(O.helm_eval(1, K, L, P, c, tn) - ref) < 1e-12 * abs(ref)
+    # the dipole kernel is the source gradient of the monopole kernel (finite differences)
+    h = 1e-4
+    dd = 0
+    for d in range(3):
+        e = np.zeros(3)
+        e[d] = h
+        dd += mu[0, d] * (O.helm_direct_sum(K, src[:1] + e, [1.0], tn[None])[0] -
+                          O.helm_direct_sum(K, src[:1] - e, [1.0], tn[None])[0]) / (2 * h)
+    one = O.helm_direct_sum(K, src[:1], [0.0], tn[None], mu=mu[:1])[0]
+    assert abs(one - dd) < 1e-6 * abs(dd)
+
+
+def test_double_layer_fmm_converges_to_direct_qbx():
+    """Brakhage-Werner-type combination S(w) + D(mu) through the oracle FMM, converging to
+    direct QBX with p on the same tree and lists."""
+    g, w = _config3_small(level=1)
+    mu = g.source_normal * (g.quad_weight * np.conj(w))[:, None]
+    d = O.helm_direct_qbx(K, g, w, 3, mu=mu)
+    errs = []
+    for p in (3, 5, 8):
+        plan = api.Plan(api.FmmConfig(p_fmm=p, p_qbx=3, n_max=64, kernel=0), g)
+        f = O.helm_execute(plan, g, K, p, 3, w, mu=mu)
+        errs.append(float(np.linalg.norm(f - d) / np.linalg.norm(d)))
+    assert errs[0] > errs[1] > errs[2], errs
+    assert errs[2] < 1e-5, errs
+
+
 def test_gpu_entry_points_validate_on_host():
     """Argument checks of the GPU Helmholtz entry points run before any device work."""
     g, w = _config3_small(level=1)
@@ -176,3 +248,54 @@ def test_gpu_helmholtz_p20_matches_oracle_fixture():
     eng.close()
     assert np.linalg.norm(pot - fx["pot"]) / np.linalg.norm(fx["pot"]) <= 1e-11
     assert np.linalg.norm(cc[:64] - fx["centres"]) / np.linalg.norm(fx["centres"]) <= 1e-11
+
+
+# ---------------------------------------------------------------- double layer on the GPU
+def _bw_dipoles(g, w):
+    """Brakhage-Werner-style dipole moments m = q mu n for the density of w = q mu."""
+    return g.source_normal * w[:, None]
+
+
+@pytest.mark.gpu
+def test_gpu_helm_direct_sum_double_layer_matches_oracle():
+    g, w = _config3_small(level=1)
+    mu = _bw_dipoles(g, w)
+    t = g.target_pos[:700] * 1.01
+    pot = api.helm_direct_sum(K, g.source_pos, -1j * 3.0 * w, t, dipoles=mu)
+    ref = O.helm_direct_sum(K, g.source_pos, -1j * 3.0 * w, t, mu=mu)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("q", [0, 3, 5])
+def test_gpu_helm_direct_qbx_double_layer_matches_oracle(q):
+    g, w = _config3_small(level=1)
+    mu = _bw_dipoles(g, w)
+    pot = api.helm_direct_qbx(K, g, w, q, dipoles=mu)
+    ref = O.helm_direct_qbx(K, g, w, q, mu=mu)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfgid,kw,p,q", [(3, dict(level=1), 6, 3), (3, dict(level=1), 12, 5),
+                                          (2, dict(level=1, n_volume_targets=300), 8, 4)])
+def test_gpu_helmholtz_double_layer_fmm_matches_oracle(cfgid, kw, p, q):
+    """Helmholtz SL+DL (kernel 3) through qbxg_apply_complex against the oracle on the same
+    plan: the Brakhage-Werner combination S(-i eta q mu) + D(q mu n), eta = k."""
+    g = api.config_geometry(cfgid, **kw)
+    rng = np.random.default_rng(4)
+    w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
+    mu = _bw_dipoles(g, w)
+    ws = -1j * K * w
+    cfg = api.FmmConfig(p_fmm=p, p_qbx=q, n_max=64, kernel=3, helmholtz_k=K)
+    plan = api.Plan(cfg, g)
+    eng = api.FmmEngine(cfg, g, plan)
+    pot, cc = eng.apply_complex(ws, mu, want_centers=True)
+    again = eng.apply_complex(ws, mu)
+    with pytest.raises(ValueError, match="requires dipole"):
+        eng.apply_complex(ws)
+    eng.close()
+    ref, cref = O.helm_execute(plan, g, K, p, q, ws, want_centers=True, mu=mu)
+    assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
+    assert np.linalg.norm(cc - cref) / np.linalg.norm(cref) <= 1e-11
+    assert np.array_equal(pot, again), "Helmholtz SL+DL apply is not bitwise deterministic"
