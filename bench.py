@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--small", action="store_true", help="debug: torus 64x32 instead of config 1")
+    ap.add_argument("--workload", default="auto", choices=["auto", "config1", "config4"],
+                    help="auto: config 1 on one GPU, config 4 (64 urchins) under torchrun")
+    ap.add_argument("--weak", action="store_true", help="config 4 weak scaling: 8 urchins per GPU")
+    ap.add_argument("--no-config4", action="store_true", help="skip the one-GPU config-4 scaling base")
     ap.add_argument("--no-helmholtz", action="store_true", help="skip the side measurements (config-3 Helmholtz, config-2 association)")
     return ap.parse_args()
 
@@ -65,20 +69,11 @@ def stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
     f["near"] = led["pairs_qbx_near"] * ((26 if dl else 10) * kq + (40 if dl else 30)) + \
         led["pairs_p2p_near"] * (30 if dl else 20)
     b["near"] = n_src * src_b + n_ctr * (32 + 16 * kq) + n_conv * 32
-    # default (split) M2L: after the azimuthal rotation the operator is two real blocks,
-    # K_p x K_p (Re) and (K_p-p-1) x (K_p-p-1) (Im, m >= 1); QBXG_M2L_MODE=dense uses
-    # the full real operator on the (p+1)^2 real degrees of freedom
-    mode = os.environ.get("QBXG_M2L_MODE", "")
-    if mode == "dense":
-        f["m2l"] = led["entries"]["V"] * 2 * (p + 1) ** 4
-    elif 4 <= p <= 15 and mode not in ("split", "rot"):
-        # point-and-shoot (default for 4 <= p <= 15): W (rotation about y), Z (z-shift) and
-        # V (rotation back) are each block diagonal -- Re blocks of size 1..p+1 and Im blocks
-        # of size 1..p -- so sum(s^2) multiply-adds per factor per entry
-        blk = sum(s * s for s in range(1, p + 2)) + sum(s * s for s in range(1, p + 1))
-        f["m2l"] = led["entries"]["V"] * 2 * 3 * blk
-    else:
-        f["m2l"] = led["entries"]["V"] * 2 * (kp * kp + (kp - p - 1) ** 2)
+    # point-and-shoot M2L: W (rotation about y), Z (z-shift) and V (rotation back) are each
+    # block diagonal -- Re blocks of size 1..p+1 and Im blocks of size 1..p -- so sum(s^2)
+    # multiply-adds per factor per entry (the dense 8 K_p^2 convention would be 9x larger)
+    blk = sum(s * s for s in range(1, p + 2)) + sum(s * s for s in range(1, p + 1))
+    f["m2l"] = led["entries"]["V"] * 2 * 3 * blk
     # compulsory: multipoles in + locals out once per box (operators ~0.6 GB amortised)
     b["m2l"] = 2 * 8 * (p + 1) ** 2 * led["n_l2l"]
     f["wfar"] = led["pairs_wfar_centre"] * (8 * kp * kq + 10 * kpq + 30) + led["pairs_wfar_target"] * (10 * kp + 30)
@@ -162,25 +157,45 @@ def host_info():
     return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
-def workload_config(g, n_boxes, world, small=False):
-    return {"workload": "BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
-                        "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9" if not small else "debug: torus 64x32",
+def pick_workload(args, world):
+    """(config id, geometry overrides, label) of the bench workload: BASELINE config 1 on one
+    GPU; config 4 (4x4x4 urchins, strong scaling; --weak: 8 urchins per GPU) under torchrun."""
+    wl = args.workload if args.workload != "auto" else ("config1" if world == 1 else "config4")
+    if wl == "config1":
+        if args.small:
+            return 1, dict(nu=64, nv=32), "debug: torus 64x32"
+        return 1, {}, ("BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
+                       "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9")
+    n = 8 * world if args.weak else 64
+    return 4, dict(variant=n), (f"BASELINE config 4: {n} urchins (level 5, spacing 3.0, random rotations), "
+                                f"{n * 327680} sources, Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9; "
+                                + ("weak scaling, 8 urchins per GPU" if args.weak else "strong scaling"))
+
+
+def workload_config(g, n_boxes, world, small=False, label=None):
+    return {"workload": label or ("BASELINE config 1: torus R=2 r=1, 256x128 cells, 65,536 tris x 16 nodes, "
+                                  "Laplace SL+DL, p_fmm=15, p_qbx=5, n_max=64, t_f=0.9" if not small
+                                  else "debug: torus 64x32"),
             "n_sources": g.n_sources, "n_targets": g.n_targets, "n_centers": g.n_centers, "n_boxes": n_boxes,
             "parallelism": f"morton-shard x{world} (NCCL multipole broadcast)" if world > 1 else "single GPU",
             "l2": "working set (M, L 2x392 MB, QBX locals 672 MB) >> 126 MB L2; no flush"}
 
 
-def cpu_oracle_throughput(steps: int, warmup: int, full: bool = False):
+def cpu_oracle_throughput(steps: int, warmup: int, full: bool = False, cid: int = CONFIG_ID):
     """The CPU restatement of the path (oracle/, OpenMP over all host threads) on the
     full config-1 workload (full=True: the reference arm) or on a bounded 1/16 sample
-    of it (the cpu_baseline field of the GPU line)."""
+    of it (the cpu_baseline field of the GPU line); config 4: a bounded sample of two of
+    its urchins (the whole 64-urchin apply is ~30 CPU-minutes)."""
     import oracle as O
     from paper_1805_06106_b200 import api
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    over = {} if full else CPU_SAMPLE
-    g = api.config_geometry(CONFIG_ID, **over)
-    cfg = api.config_fmm(CONFIG_ID)
+    if cid == 4:
+        over = dict(variant=8, nx=2, ny=1, nz=1)
+    else:
+        over = {} if full else CPU_SAMPLE
+    g = api.config_geometry(cid, **over)
+    cfg = api.config_fmm(cid)
     plan = api.Plan(cfg, g)
     w, mu = g.weights(), g.dipoles()
     for _ in range(warmup):
@@ -192,7 +207,8 @@ def cpu_oracle_throughput(steps: int, warmup: int, full: bool = False):
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
     units = g.n_sources + g.n_targets
-    what = ("full BASELINE config 1" if full else f"torus {CPU_SAMPLE['nu']}x{CPU_SAMPLE['nv']} cells, 1/16 of config 1")
+    what = ("2 of the 64 urchins of BASELINE config 4 (bounded sample)" if cid == 4 else
+            "full BASELINE config 1" if full else f"torus {CPU_SAMPLE['nu']}x{CPU_SAMPLE['nv']} cells, 1/16 of config 1")
     return dict(value=units / t, unit="points/s", cores=cores, kind="port",
                 sample=f"{what} ({g.n_sources} sources + {g.n_targets} targets), p=15 q=5 SL+DL, oracle/ OpenMP "
                        f"restatement of Stages 2-9 on the same host plan, mean of {steps} after {warmup} warm-up",
@@ -206,11 +222,15 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     steps, warm = max(1, min(args.steps, 2)), min(max(args.warmup, 0), 1)
-    cb = cpu_oracle_throughput(steps, warm, full=not args.small)
-    cfgd = workload_config(cb["g"], cb["n_boxes"], world, args.small)
+    cid, _, label = pick_workload(args, world)
+    cb = cpu_oracle_throughput(steps, warm, full=not args.small, cid=cid)
+    cfgd = workload_config(cb["g"], cb["n_boxes"], world, args.small, label)
+    if cid == 4:
+        cfgd["sample"] = cb["sample"]
     line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": cb["value"],
             "unit": "points/s", "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-            "ms_per_step": cb["seconds_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": cb["seconds_per_step"] * 1e3, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (procedural torus, seeded Fourier density)",
             "config": cfgd,
             "cpu_baseline": {"value": cb["value"], "unit": "points/s", "cores": cb["cores"], "kind": "port",
@@ -223,6 +243,41 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------- GPU leg
+def measure_config4(api, torch, local_rank, steps):
+    """BASELINE config 4 (64 urchins, 20,971,520 sources) on one GPU, device-resident,
+    CUDA events: the N = 1 point of the strong-scaling curve."""
+    t0 = time.perf_counter()
+    g = api.config_geometry(4)
+    cfg = api.config_fmm(4)
+    plan = api.Plan(cfg, g, device="gpu")
+    t1 = time.perf_counter()
+    eng = api.FmmEngine(cfg, g, plan, device=local_rank)
+    t2 = time.perf_counter()
+    dev = torch.device("cuda", local_rank)
+    d_w = torch.from_numpy(g.weights()).to(dev)
+    d_mu = torch.from_numpy(g.dipoles().reshape(-1)).to(dev)
+    d_pot = torch.empty(g.n_targets, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    eng.apply_device(d_w.data_ptr(), d_mu.data_ptr(), d_pot.data_ptr(), None, stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        eng.apply_device(d_w.data_ptr(), d_mu.data_ptr(), d_pot.data_ptr(), None, stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    tm, _, _, _ = eng.last_timings()
+    eng.close()
+    units = g.n_sources + g.n_targets
+    return {"workload": "BASELINE config 4: 64 urchins, strong-scaling base (same workload as bench.py --gpus N)",
+            "n_sources": g.n_sources, "n_targets": g.n_targets, "n_boxes": plan.view.n_boxes,
+            "ms_per_apply": round(ms, 2), "value": units / (ms * 1e-3), "unit": "points/s", "steps": steps,
+            "stages_ms": {k: round(v, 2) for k, v in tm.items()},
+            "setup_s": {"geometry_and_gpu_plan": round(t1 - t0, 2), "create": round(t2 - t1, 2)}}
+
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_1805_06106_b200 import api
@@ -234,9 +289,10 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     t0 = time.perf_counter()
-    over = dict(nu=64, nv=32) if args.small else {}
-    g = api.config_geometry(CONFIG_ID, **over)
-    cfg = api.config_fmm(CONFIG_ID)
+    cid, over, label = pick_workload(args, world)
+    g = api.config_geometry(cid, **over)
+    cfg = api.config_fmm(cid)
+    side = world == 1 and cid == 1  # single-GPU side measurements ride on the config-1 run
     t1 = time.perf_counter()
     plan = api.Plan(cfg, g)
     t2 = time.perf_counter()
@@ -252,7 +308,7 @@ def run_ours(args, rank, world, local_rank):
     t3 = time.perf_counter()
     # Stage 1 on the GPU (qbxg_plan_create_gpu): same plan bit for bit
     plan_gpu = None
-    if world == 1:
+    if side:
         api.Plan(cfg, g, device="gpu")  # warm-up (CUB kernels, allocator)
         tg = time.perf_counter()
         pg = api.Plan(cfg, g, device="gpu")
@@ -303,24 +359,9 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
-    # per-stage CUDA-event times for the rooflines come from a second block of K steps
-    # with the near field on the main stream (the engine default; with QBXG_OVERLAP
-    # the headline run shares the SMs between the near field and M2L/P2L/L2L)
-    eng.set_overlap(False)
-    stage_ms = {}
-    torch.cuda.synchronize(dev)
-    es0 = torch.cuda.Event(enable_timing=True)
-    es1 = torch.cuda.Event(enable_timing=True)
-    es0.record(stream)
-    for _ in range(args.steps):
-        step()
-        tm, _, _, _ = eng.last_timings()
-        for k, v in tm.items():
-            stage_ms[k] = stage_ms.get(k, 0.0) + v
-    es1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms_seq = es0.elapsed_time(es1) / args.steps
-    eng.set_overlap(os.environ.get("QBXG_OVERLAP", "0") in ("1", "2"))
+    # per-stage CUDA-event times (the engine's own events, over the same timed steps; for a
+    # sharded apply the near field runs on a side stream beside the exchange and M2L)
+    ms_seq = ms
     for k in stage_ms:
         stage_ms[k] /= args.steps
     units = g.n_sources + g.n_targets
@@ -348,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
 
     # batched densities (qbxg_apply_batch_device): device time per density
     batch = None
-    if world == 1 and not args.small:
+    if side and not args.small:
         R = 4
         rng = np.random.default_rng(5)
         dens = rng.uniform(-1.0, 1.0, (R, g.n_sources))
@@ -397,8 +438,9 @@ def run_ours(args, rank, world, local_rank):
     dom = max(stages, key=lambda k: stages[k]["ms"])
     d = stages[dom]
     traffic, traffic_note = None, None
-    tp = os.path.join(HERE, "profiles", f"r01_ncu_{dom}.json")
-    if os.path.exists(tp) and not args.small:
+    tp = next((os.path.join(HERE, "profiles", f"r0{r}_ncu_{dom}.json") for r in (2, 1)
+               if os.path.exists(os.path.join(HERE, "profiles", f"r0{r}_ncu_{dom}.json"))), "")
+    if tp and cid == 1 and not args.small:
         with open(tp) as fh:
             t = json.load(fh)
         # one ncu --set full capture of the stage's main kernel; bytes per launch
@@ -410,20 +452,28 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "in-run microbenchmarks (qbxg_measure_fp64_peak DFMA = %.1f, qbxg_measure_dmma_peak "
                                "DMMA = %.1f TFLOP/s); MEASURED_PEAKS.json has no fp64 entry" % (peak, peak_dmma),
                 "algorithmic_flops_per_launch": flops[dom], "share_of_step": round(d["ms"] / ms_seq, 3),
-                "stage_timing": ("CUDA events per stage over a second block of K steps (%.2f ms/step; headline "
-                                 "block %.2f ms/step), near field on the main stream" % (ms_seq, ms))}
+                "stage_timing": "the engine's CUDA events per stage over the K timed steps (%.2f ms/step)" % ms}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and side and not args.no_cpu_baseline:
         cb = cpu_oracle_throughput(1, 0)
         cpu = {**{k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}, **cb["host"]}
+
+    # BASELINE config 4 (64 urchins) on this one GPU: the base of the strong-scaling curve
+    # that bench.py --gpus N (torchrun) measures at N = 2, 4, 8 on the same workload
+    c4 = None
+    if side and not args.small and not args.no_config4:
+        eng.close()
+        eng = None
+        c4 = measure_config4(api, torch, local_rank, max(2, min(args.steps, 3)))
 
     # BASELINE config 3 (Helmholtz single layer, k = 3, p = 20, q = 5) on the same GPU:
     # side measurement, CUDA events, inputs on the host (qbxg_apply_complex)
     helm = None
-    if world == 1 and not args.small and not args.no_helmholtz:
-        eng.close()
-        eng = None
+    if side and not args.small and not args.no_helmholtz:
+        if eng is not None:
+            eng.close()
+            eng = None
         g3 = api.config_geometry(3)
         cfg3 = api.config_fmm(3)
         rng3 = np.random.default_rng(7)
@@ -446,7 +496,7 @@ def run_ours(args, rank, world, local_rank):
     # target association (Algorithm 3) on BASELINE config 2: 655,360
     # on-surface nodes + the retained volume targets, device-resident, CUDA events
     assoc = None
-    if world == 1 and not args.small and not args.no_helmholtz:
+    if side and not args.small and not args.no_helmholtz:
         g2 = api.config_geometry(2)
         sc2 = api.Geometry(source_pos=g2.source_pos, center_pos=g2.center_pos, center_radius=g2.center_radius,
                            target_pos=np.zeros((0, 3)), association=np.zeros(0, dtype=np.int32))
@@ -481,13 +531,13 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {"metric": "QBX-FMM layer-potential apply: (sources+targets)/sec", "value": value,
                 "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
                 "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (procedural torus, seeded Fourier density)",
-                "config": workload_config(g, plan.view.n_boxes, world, args.small),
+                "config": workload_config(g, plan.view.n_boxes, world, args.small, label),
                 "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": launches, "roofline": roofline, "stages": stages, "clocks": clocks,
-                "batch": batch, "helmholtz": helm, "association": assoc,
+                "batch": batch, "config4_one_gpu": c4, "helmholtz": helm, "association": assoc,
                 "cpu_baseline": cpu,
                 "setup_s": {"geometry": round(t1 - t0, 3), "tree": round(plan.view.build_seconds_tree, 3),
                             "lists": round(plan.view.build_seconds_lists, 3), "upload": round(t3 - t2, 3),

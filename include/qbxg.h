@@ -100,7 +100,10 @@ typedef struct {
   int32_t w_far_demote; /* Remark 1: a List-3-far box whose
                            subtree holds fewer than this many sources is replaced by
                            its source leaves in List 3 close; 0 disables.  */
-  int32_t reserved;     /* must be 0 (level restriction not implemented)   */
+  int32_t level_restrict; /* 1: level-restricted tree (Remark C.1,
+                           PAPER.md:3661-3687): leaves are subdivided until
+                           adjacent leaves differ by at most one level; 0: off
+                           (default).  Host plan only (qbxg_plan_create).  */
 } qbxg_config;
 
 typedef struct {
@@ -285,6 +288,13 @@ int qbxg_multipole_buffer(qbxg_handle* h, double** d_multipoles, int64_t* row_do
 /* Exchange between handles of one process (device copies), e.g. ranks emulated on one GPU. */
 int qbxg_exchange_local(qbxg_handle** handles, int32_t n_ranks);
 /* NCCL (libnccl.so.2 loaded at run time): rank 0 creates the id, all ranks attach. */
+/* Result all-gather of a sharded apply emulated with device copies (ranks driven by
+ * qbxg_apply_phase in one process; tests): after phase 2, every rank's packed
+ * potentials (and centre coefficients when d_coeffs is given) are copied to all
+ * ranks and scattered, so d_pots[r] (n_targets doubles per rank) holds the whole
+ * result.  qbxg_apply_device on an NCCL-attached sharded handle does the same with
+ * one grouped broadcast per rank (qbxg_nccl_attach). */
+int qbxg_result_exchange_local(qbxg_handle** hs, int32_t n, double* const* d_pots, double* const* d_coeffs);
 int qbxg_nccl_unique_id(uint8_t* out128);
 int qbxg_nccl_attach(qbxg_handle* h, const uint8_t* id128);
 

@@ -37,7 +37,7 @@ _u8p = C.POINTER(C.c_uint8)
 class Config(C.Structure):
     _fields_ = [("p_fmm", C.c_int32), ("p_qbx", C.c_int32), ("t_f", C.c_double), ("n_max", C.c_int32),
                 ("kernel", C.c_int32), ("helmholtz_k", C.c_double), ("w_far_demote", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("level_restrict", C.c_int32)]
 
 
 class Geometry(C.Structure):
@@ -96,7 +96,7 @@ EXPORTED_SYMBOLS = (
     "qbxg_create", "qbxg_apply", "qbxg_apply_device", "qbxg_destroy", "qbxg_direct_sum",
     "qbxg_last_error", "qbxg_device_count", "qbxg_version", "qbxg_measure_fp64_peak",
     "qbxg_measure_dmma_peak", "qbxg_plan_shard", "qbxg_create_sharded", "qbxg_apply_phase",
-    "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
+    "qbxg_multipole_buffer", "qbxg_exchange_local", "qbxg_result_exchange_local", "qbxg_nccl_unique_id", "qbxg_nccl_attach",
     "qbxg_direct_qbx", "qbxg_apply_batch", "qbxg_apply_batch_device", "qbxg_set_overlap", "qbxg_helm_direct_sum", "qbxg_helm_direct_qbx",
     "qbxg_apply_complex", "qbxg_locator_create", "qbxg_associate_targets", "qbxg_associate_targets_device",
     "qbxg_area_query", "qbxg_locator_destroy", "qbxg_plan_create_gpu", "qbxg_adequately_separated",
@@ -142,6 +142,7 @@ def _declare(lib):
         "qbxg_apply_phase": ([C.c_void_p, C.c_int32] + [C.c_void_p] * 5, C.c_int),
         "qbxg_multipole_buffer": ([C.c_void_p, P(C.c_void_p), _i64p, _i32p], C.c_int),
         "qbxg_exchange_local": ([P(C.c_void_p), C.c_int32], C.c_int),
+        "qbxg_result_exchange_local": ([P(C.c_void_p), C.c_int32, P(C.c_void_p), P(C.c_void_p)], C.c_int),
         "qbxg_nccl_unique_id": ([C.c_char_p], C.c_int),
         "qbxg_nccl_attach": ([C.c_void_p, C.c_char_p], C.c_int),
         "qbxg_locator_create": ([C.c_void_p, P(Geometry), _dp, C.c_void_p, P(C.c_void_p)], C.c_int),

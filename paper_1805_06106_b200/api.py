@@ -106,11 +106,12 @@ class FmmConfig:
     n_max: int = 64
     kernel: int = _abi.KERNEL_LAPLACE_SL
     w_far_demote: int = 0
-    helmholtz_k: float = 0.0  # wavenumber, kernel 2 (Helmholtz single layer)
+    helmholtz_k: float = 0.0  # wavenumber, kernels 2 / 3 (Helmholtz single / single + double layer)
+    level_restrict: int = 0   # 1 = subdivide until adjacent leaves differ by <= 1 level
 
     def to_c(self):
         return _abi.Config(self.p_fmm, self.p_qbx, self.t_f, self.n_max, self.kernel, float(self.helmholtz_k),
-                           self.w_far_demote, 0)
+                           self.w_far_demote, int(self.level_restrict))
 
     @property
     def kq(self):
@@ -505,6 +506,16 @@ def exchange_local(engines):
     """Multipole exchange between sharded engines living in one process (device copies)."""
     arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
     _check(_abi.lib().qbxg_exchange_local(arr, len(engines)))
+
+
+def exchange_results_local(engines, d_pots, d_coeffs=None):
+    """Result all-gather between sharded engines in one process (device copies): after
+    phase 2, every d_pots[r] (device pointer, n_targets doubles) holds all potentials."""
+    n = len(engines)
+    arr = (C.c_void_p * n)(*[e.handle for e in engines])
+    pp = (C.c_void_p * n)(*d_pots)
+    cp = (C.c_void_p * n)(*d_coeffs) if d_coeffs is not None else None
+    _check(_abi.lib().qbxg_result_exchange_local(arr, n, pp, cp))
 
 
 def plan_shard(plan: "Plan", n_ranks: int, rank: int):

@@ -69,11 +69,17 @@ void check_device() {
 struct Handle {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;   // near field overlapped with the far-field chain (QBXG_OVERLAP)
+  cudaStream_t side = nullptr;   // near field forked beside the far-field chain (NEAR_SIDE)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t evx[4] = {};       // near begin/end (side stream), P2L end, L2L end
   bool overlap = false, timed_overlap = false;
-  bool overlap_late = false;  // QBXG_OVERLAP=2: fork the near field after the M2L launch
+  bool debug_sync = false;    // QBXG_DEBUG_SYNC (read once at create): sync after every launch group
+  // sharded result all-gather: packed segments per rank (targets; centre rows of 2 kq)
+  std::vector<int64_t> res_off, cres_off;
+  int* d_res_idx = nullptr;   // original target id of each packed slot
+  double* d_res_buf = nullptr;
+  int* d_cres_idx = nullptr;  // original centre id of each packed row
+  double* d_cres_buf = nullptr;
   cudaEvent_t ev[QBXG_NUM_TIMERS + 2] = {};
   qbxg_config cfg{};
   int64_t ns = 0, nc = 0, nt = 0, nconv = 0;
@@ -412,21 +418,30 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       std::vector<int> boxes;
       for (int b = b0; b < b1; ++b)
         if (vs[b + 1] > vs[b]) boxes.push_back(b);
-      std::vector<int64_t> cnt_op(P.n_offsets + 1, 0);
-      for (int64_t e = base; e < base + cnt; ++e) cnt_op[slot_to_op[slot[e]] + 1]++;
-      for (int o = 0; o < P.n_offsets; ++o) cnt_op[o + 1] += cnt_op[o];
+      // entries counting-sorted by (source block, offset): a source block is a run of
+      // consecutive source boxes whose multipoles (~24 MB) stay in L2 while its tiles
+      // run, so the gather reads each multipole from HBM about once (offsets alone
+      // would cycle the whole 392 MB multipole array through L2 per offset)
+      const int64_t sbox = std::max<int64_t>(1, (int64_t(24) << 20) / (int64_t(16) * dev::hsize(p)));
+      const int64_t nkey = ((nb + sbox - 1) / sbox) * P.n_offsets;
+      auto key = [&](int64_t e) { return (vb[e] / sbox) * P.n_offsets + slot_to_op[slot[e]]; };
+      std::vector<int64_t> cnt_k(nkey + 1, 0);
+      for (int64_t e = base; e < base + cnt; ++e) cnt_k[key(e) + 1]++;
+      for (int64_t k = 0; k < nkey; ++k) cnt_k[k + 1] += cnt_k[k];
       std::vector<int> col_src(cnt), col_pos(cnt);
-      std::vector<int64_t> fill(cnt_op.begin(), cnt_op.end() - 1);
+      std::vector<int64_t> fill(cnt_k.begin(), cnt_k.end() - 1);
       for (int b = b0; b < b1; ++b)
         for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
-          const int64_t i = fill[slot_to_op[slot[e]]]++;
+          const int64_t i = fill[key(e)]++;
           col_src[i] = vb[e];
           col_pos[i] = int(e - base);
         }
       std::vector<int4> tiles;
-      for (int o = 0; o < P.n_offsets; ++o)
-        for (int64_t i = cnt_op[o]; i < cnt_op[o + 1]; i += tw)
-          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_op[o + 1] - i)), cls_of_op[o]));
+      for (int64_t k = 0; k < nkey; ++k) {
+        const int o = int(k % P.n_offsets);
+        for (int64_t i = cnt_k[k]; i < cnt_k[k + 1]; i += tw)
+          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_k[k + 1] - i)), cls_of_op[o]));
+      }
       C.n_tiles = int(tiles.size());
       C.tiles = dupload(O, tiles, s);
       C.col_src = dupload(O, col_src, s);
@@ -744,7 +759,7 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
   dev::HelmData& HD = H.HD;
   auto& ev = H.ev;
   int L = 0;
-  static const bool debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
+  const bool debug_sync = H.debug_sync;
   int stage_no = 0;
   auto chk = [&](int k) {
     if (k < 0) throw InvalidArgument("qbxg_apply: unsupported Helmholtz order");
@@ -861,13 +876,11 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   QCK(cudaStreamCreateWithFlags(&H.stream, cudaStreamNonBlocking));
   for (auto& e : H.ev) QCK(cudaEventCreate(&e));
   for (auto& e : H.evx) QCK(cudaEventCreate(&e));
-  // off by default: the near field and the M2L both live on the fp64 pipe, and since
-  // the near field launches heaviest boxes first the overlapped apply measured no
-  // faster than the sequential one (107.4 vs 106.4 ms at config 1); QBXG_OVERLAP=1
-  // forks it after the gather, QBXG_OVERLAP=2 after the M2L launch
-  H.overlap = std::getenv("QBXG_OVERLAP") && (std::getenv("QBXG_OVERLAP")[0] == '1' ||
-                                              std::getenv("QBXG_OVERLAP")[0] == '2');
-  H.overlap_late = std::getenv("QBXG_OVERLAP") && std::getenv("QBXG_OVERLAP")[0] == '2';
+  // near field beside the far-field chain: off by default on one GPU (both live on the
+  // fp64 pipe; the sequential apply measured as fast), always on for sharded applies
+  // (it hides the multipole exchange); qbxg_set_overlap opts in
+  H.overlap = false;
+  H.debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
   QCK(cudaStreamCreateWithFlags(&H.side, cudaStreamNonBlocking));
   QCK(cudaEventCreateWithFlags(&H.fork_ev, cudaEventDisableTiming));
   QCK(cudaEventCreateWithFlags(&H.join_ev, cudaEventDisableTiming));
@@ -1092,6 +1105,39 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       for (int j = 0; j < V.ctr_own_count[b]; ++j) fw.push_back(V.ctr_own_start[b] + j);
     H.d_ctr_box = dupload(O, cbox, s);
     H.d_flat_all = dupload(O, all, s);
+    if (nranks > 1) {
+      // result all-gather layout: rank-major segments of every rank's owned targets
+      // (associated in target order, then conventional in box order) and centres
+      auto owner = [&](int b) {
+        return int(std::upper_bound(H.cuts.begin(), H.cuts.end(), int32_t(b)) - H.cuts.begin()) - 1;
+      };
+      std::vector<int> cs_of(H.nc);
+      for (int64_t i = 0; i < H.nc; ++i) cs_of[V.ctr_perm[i]] = int(i);
+      std::vector<std::vector<int>> rt(nranks), rc(nranks);
+      for (int64_t t = 0; t < H.nt; ++t)
+        if (g.association[t] >= 0) rt[owner(cbox[cs_of[g.association[t]]])].push_back(int(t));
+      for (int b = 0; b < nb; ++b) {
+        const int r = owner(b);
+        for (int j = 0; j < V.tgt_own_count[b]; ++j) rt[r].push_back(V.tgt_perm[V.tgt_own_start[b] + j]);
+        for (int j = 0; j < V.ctr_own_count[b]; ++j) rc[r].push_back(V.ctr_perm[V.ctr_own_start[b] + j]);
+      }
+      std::vector<int> ti, ci;
+      H.res_off.assign(1, 0);
+      H.cres_off.assign(1, 0);
+      for (int r = 0; r < nranks; ++r) {
+        ti.insert(ti.end(), rt[r].begin(), rt[r].end());
+        ci.insert(ci.end(), rc[r].begin(), rc[r].end());
+        H.res_off.push_back(int64_t(ti.size()));
+        H.cres_off.push_back(int64_t(ci.size()));
+      }
+      if (int64_t(ti.size()) != H.nt || int64_t(ci.size()) != H.nc)
+        throw InvalidArgument("qbxg_create_sharded: targets / centres not partitioned by the shard cuts");
+      H.d_res_idx = dupload(O, ti, s);
+      H.d_cres_idx = dupload(O, ci, s);
+      H.d_res_buf = dalloc<double>(O, std::max<int64_t>(H.nt, 1));
+      H.d_cres_buf = dalloc<double>(O, std::max<int64_t>(H.nc, 1) * 2 * D.kq);
+      QCK(cudaStreamSynchronize(s));
+    }
     {
       std::vector<int2> l3;
       size_t i = 0;
@@ -1234,8 +1280,6 @@ struct Nccl {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -1252,13 +1296,12 @@ Nccl& nccl() {
       n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(n.lib, "ncclCommInitRank"));
       n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(n.lib, "ncclCommDestroy"));
       n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(dlsym(n.lib, "ncclBroadcast"));
-      n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(n.lib, "ncclAllReduce"));
       n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(n.lib, "ncclGroupStart"));
       n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(n.lib, "ncclGroupEnd"));
       n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(n.lib, "ncclGetErrorString"));
     }
   }
-  if (!n.lib || !n.GetUniqueId || !n.CommInitRank || !n.Broadcast || !n.AllReduce || !n.GroupStart || !n.GroupEnd)
+  if (!n.lib || !n.GetUniqueId || !n.CommInitRank || !n.Broadcast || !n.GroupStart || !n.GroupEnd)
     throw NcclError("libnccl.so.2 not loadable");
   return n;
 }
@@ -1285,18 +1328,24 @@ void exchange_nccl(Handle& H, cudaStream_t s) {
 
 // phase bit 1: density gather, P2M, M2M of the rank's subtrees.
 // phase bit 2: M2M of straddling boxes, then Stages 3-9 for the rank's boxes.
+// near: NEAR_INLINE runs P2QBXL on s before M2L; NEAR_DONE skips it (the batched path
+// ran it); NEAR_SIDE forks it onto the side stream right after the gather (phase 1) --
+// it needs only the gathered sources -- and joins it before W far, the first stage
+// that adds into the centre locals, so it overlaps the upward pass, the multipole
+// exchange of a sharded apply and M2L / P2L / L2L.
+enum NearMode { NEAR_INLINE = 0, NEAR_DONE = 1, NEAR_SIDE = 2 };
+
 void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s,
-                int phase, bool near_done = false) {
+                int phase, NearMode near = NEAR_INLINE) {
   dev::DevData& D = H.D;
   if (D.dipole && !d_mu && (phase & 1)) throw InvalidArgument("qbxg_apply: Laplace SL+DL requires dipole moments");
   int L = (phase & 1) ? 0 : H.last_launches;
-  static const bool debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
   int stage_no = 0;
   auto chk = [&](int k) {
     if (k < 0) throw InvalidArgument("qbxg_apply: unsupported order");
     L += k;
     ++stage_no;
-    if (debug_sync) {  // localise asynchronous faults to the launch that caused them
+    if (H.debug_sync) {  // localise asynchronous faults to the launch that caused them
       cudaError_t e = cudaStreamSynchronize(s);
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess)
@@ -1305,29 +1354,27 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     }
   };
   auto& ev = H.ev;
-  bool near_forked = false;
   if (phase & 1) {
-  QCK(cudaEventRecord(ev[0], s));
-  chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
-  if (H.overlap && !H.overlap_late && !near_done && phase == 3) {  // near field needs only the gathered sources:
-    QCK(cudaEventRecord(H.fork_ev, s));        // run it beside the whole far-field chain
-    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
-    QCK(cudaEventRecord(H.evx[0], H.side));
-    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
-    QCK(cudaEventRecord(H.evx[1], H.side));
-    QCK(cudaEventRecord(H.join_ev, H.side));
-    near_forked = true;
-  }
-  QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
-  QCK(cudaMemsetAsync(D.L, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
-  QCK(cudaMemsetAsync(D.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double), s));
-  QCK(cudaMemsetAsync(D.bad, 0, sizeof(unsigned int), s));
-  QCK(cudaEventRecord(ev[1], s));
-  chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
-  QCK(cudaEventRecord(ev[2], s));
-  for (int l = H.nlev - 2; l >= 0; --l)
-    chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
-  H.last_launches = L;
+    QCK(cudaEventRecord(ev[0], s));
+    chk(dev::launch_gather(D, int(H.ns), H.d_src_perm, d_w, d_mu, s));
+    if (near == NEAR_SIDE) {
+      QCK(cudaEventRecord(H.fork_ev, s));
+      QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
+      QCK(cudaEventRecord(H.evx[0], H.side));
+      chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
+      QCK(cudaEventRecord(H.evx[1], H.side));
+      QCK(cudaEventRecord(H.join_ev, H.side));
+    }
+    QCK(cudaMemsetAsync(D.M, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
+    QCK(cudaMemsetAsync(D.L, 0, size_t(H.nb) * D.kp * sizeof(double2), s));
+    QCK(cudaMemsetAsync(D.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double), s));
+    QCK(cudaMemsetAsync(D.bad, 0, sizeof(unsigned int), s));
+    QCK(cudaEventRecord(ev[1], s));
+    chk(dev::launch_p2m(D, H.d_leaves, H.n_leaves, s));
+    QCK(cudaEventRecord(ev[2], s));
+    for (int l = H.nlev - 2; l >= 0; --l)
+      chk(dev::launch_shift_level(H.m2l, H.m2m_levels[l], H.ops_m2m, D.M, D.kp, false, s));
+    H.last_launches = L;
   }
   if (!(phase & 2)) return;
   // boxes whose subtree spans ranks: recomputed identically by every rank once
@@ -1336,75 +1383,81 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
     for (int l = H.nlev - 2; l >= 0; --l)
       chk(dev::launch_shift_level(H.m2l, H.m2m_straddle[l], H.ops_m2m, D.M, D.kp, false, s));
   QCK(cudaEventRecord(ev[3], s));
-  // Order: near field | M2L | P2L | L2L | W far | L2QBXL | eval.  With QBXG_OVERLAP the
-  // near field (CUDA-core fp64, writes the centre locals) runs on a side stream beside
-  // the far-field chain (M2L, P2L, L2L touch only box expansions) and is joined before
-  // W far, the first stage that accumulates into the centre locals.
-  const bool ovl = H.overlap && !near_done;
-  auto fork_near = [&] {
-    QCK(cudaEventRecord(H.fork_ev, s));
-    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
-    QCK(cudaEventRecord(H.evx[0], H.side));
-    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
-    QCK(cudaEventRecord(H.evx[1], H.side));
-    QCK(cudaEventRecord(H.join_ev, H.side));
-  };
-  if (ovl && !near_forked && H.overlap_late) {
-    // forked right after the M2L launch below
-  } else if (ovl && !near_forked) {
-    QCK(cudaEventRecord(H.fork_ev, s));
-    QCK(cudaStreamWaitEvent(H.side, H.fork_ev, 0));
-    QCK(cudaEventRecord(H.evx[0], H.side));
-    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, H.side));
-    QCK(cudaEventRecord(H.evx[1], H.side));
-    QCK(cudaEventRecord(H.join_ev, H.side));
-  } else if (!near_done && !ovl) {
-    chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, s));
-  }
+  // Order: near field | M2L | P2L | L2L | W far | L2QBXL | eval
+  if (near == NEAR_INLINE) chk(dev::launch_near_qbx(D, H.d_near_boxes, H.n_ctr_boxes, s));
   chk(dev::launch_near_p2p(D, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
   chk(dev::launch_m2l(H.m2l, D, s));
-  if (ovl && !near_forked && H.overlap_late) fork_near();
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::launch_p2l(D, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));
   for (int l = 1; l < H.nlev; ++l) chk(dev::launch_shift_level(H.m2l, H.l2l_levels[l], H.ops_l2l, D.L, D.kp, true, s));
   QCK(cudaEventRecord(H.evx[3], s));
-  if (ovl) QCK(cudaStreamWaitEvent(s, H.join_ev, 0));
+  if (near == NEAR_SIDE) QCK(cudaStreamWaitEvent(s, H.join_ev, 0));
   chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
   chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
   QCK(cudaEventRecord(ev[6], s));
-  H.timed_overlap = ovl;
+  H.timed_overlap = near == NEAR_SIDE;
   chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
   QCK(cudaEventRecord(ev[9], s));
-  if (H.nranks > 1) {  // targets / centres of other ranks stay zero (summed across ranks)
+  if (H.nranks > 1) {  // targets / centres of other ranks stay zero until the result exchange
     QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * sizeof(double), s));
     if (d_coeffs) QCK(cudaMemsetAsync(d_coeffs, 0, size_t(std::max<int64_t>(H.nc, 1)) * 2 * D.kq * sizeof(double), s));
   }
   chk(dev::launch_eval(D, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_eval_conv,
                        H.d_eval_conv, H.d_tgt_perm, H.d_tgt_box, d_pot, s));
   if (d_coeffs) chk(dev::launch_centre_out(D, H.n_own_ctr, H.d_flat_all, H.d_ctr_perm, d_coeffs, s));
+  if (H.nranks > 1) {  // the rank's results into its segment of the gather buffers
+    const int64_t a = H.res_off[H.rank], e = H.res_off[H.rank + 1];
+    chk(dev::launch_pack(int(e - a), H.d_res_idx + a, 1, d_pot, H.d_res_buf + a, false, s));
+    if (d_coeffs) {
+      const int64_t ca = H.cres_off[H.rank], ce = H.cres_off[H.rank + 1];
+      chk(dev::launch_pack(int(ce - ca), H.d_cres_idx + ca, 2 * D.kq, d_coeffs, H.d_cres_buf + ca * 2 * D.kq, false,
+                           s));
+    }
+  }
   QCK(cudaEventRecord(ev[10], s));
   QCK(cudaGetLastError());
   H.last_launches = L;
 }
 
-// One whole apply: owned upward pass, multipole exchange (NCCL) when sharded,
-// straddling M2M, downward + QBX stages, and the sum of the ranks' outputs.
+// Results of a sharded apply: every rank broadcasts its packed segment of potentials
+// (and centre coefficients) to all ranks in one NCCL group -- an all-gather of owned
+// values, N_T doubles in total, instead of an all-reduce of N_T-long zero-padded
+// vectors -- and scatters the gathered values into caller order.
+void exchange_results_nccl(Handle& H, double* d_pot, double* d_coeffs, cudaStream_t s) {
+  Nccl& n = nccl();
+  auto comm = static_cast<ncclComm_t>(H.nccl_comm);
+  const int w = 2 * H.D.kq;
+  nck(n.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < H.nranks; ++r) {
+    const int64_t a = H.res_off[r], e = H.res_off[r + 1];
+    if (e > a) nck(n.Broadcast(H.d_res_buf + a, H.d_res_buf + a, size_t(e - a), ncclFloat64, r, comm, s), "ncclBroadcast");
+    if (d_coeffs) {
+      const int64_t ca = H.cres_off[r], ce = H.cres_off[r + 1];
+      if (ce > ca)
+        nck(n.Broadcast(H.d_cres_buf + ca * w, H.d_cres_buf + ca * w, size_t(ce - ca) * w, ncclFloat64, r, comm, s),
+            "ncclBroadcast");
+    }
+  }
+  nck(n.GroupEnd(), "ncclGroupEnd");
+  dev::launch_pack(int(H.nt), H.d_res_idx, 1, d_pot, H.d_res_buf, true, s);
+  if (d_coeffs) dev::launch_pack(int(H.nc), H.d_cres_idx, w, d_coeffs, H.d_cres_buf, true, s);
+}
+
+// One whole apply.  Sharded: owned upward pass (near field forked beside it), multipole
+// exchange (NCCL), straddling M2M, downward + QBX stages, result all-gather.
 void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s) {
   if (H.nranks > 1 && !H.nccl_comm)
     throw InvalidArgument("sharded handle: attach NCCL (qbxg_nccl_attach) or drive qbxg_apply_phase");
-  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 1);
-  if (H.nranks > 1) exchange_nccl(H, s);
-  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 2);
-  if (H.nranks > 1) {
-    auto comm = static_cast<ncclComm_t>(H.nccl_comm);
-    Nccl& n = nccl();
-    nck(n.AllReduce(d_pot, d_pot, size_t(H.nt), ncclFloat64, ncclSum, comm, s), "ncclAllReduce(potentials)");
-    if (d_coeffs)
-      nck(n.AllReduce(d_coeffs, d_coeffs, size_t(H.nc) * 2 * H.D.kq, ncclFloat64, ncclSum, comm, s),
-          "ncclAllReduce(centre coefficients)");
+  if (H.nranks == 1) {
+    run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 3, H.overlap ? NEAR_SIDE : NEAR_INLINE);
+    return;
   }
+  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 1, NEAR_SIDE);
+  exchange_nccl(H, s);
+  run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 2, NEAR_SIDE);
+  exchange_results_nccl(H, d_pot, d_coeffs, s);
 }
 
 // Reference error semantics inside the apply (kernels.cpp:58-71): Stage 9
@@ -1471,7 +1524,7 @@ void batch_apply(Handle& H, int R, const double* d_w, const double* d_mu, double
       D.Lc = H.d_bLc + size_t(k) * H.nc * D.kq;
       try {
         run_device(H, d_w + size_t(r) * H.ns, d_mu ? d_mu + size_t(r) * 3 * H.ns : nullptr, d_pot + size_t(r) * H.nt,
-                   d_coeffs ? d_coeffs + size_t(r) * H.nc * 2 * D.kq : nullptr, s, 3, true);
+                   d_coeffs ? d_coeffs + size_t(r) * H.nc * 2 * D.kq : nullptr, s, 3, NEAR_DONE);
       } catch (...) {
         D.Lc = lc_single;
         throw;
@@ -1647,6 +1700,37 @@ int qbxg_exchange_local(qbxg_handle** hs, int32_t n) {
         QCK(cudaMemcpy(reinterpret_cast<char*>(dst.D.M) + a * row, reinterpret_cast<char*>(src.D.M) + a * row,
                        (b - a) * row, cudaMemcpyDefault));
       }
+    }
+  });
+}
+
+int qbxg_result_exchange_local(qbxg_handle** hs, int32_t n, double* const* d_pots, double* const* d_coeffs) {
+  return qbxg::guarded([&] {
+    if (!hs || n < 1 || !d_pots) throw qbxg::InvalidArgument("qbxg_result_exchange_local: bad argument");
+    for (int r = 0; r < n; ++r)
+      if (hs[r]->h.nranks != n || hs[r]->h.rank != r || hs[r]->h.helm)
+        throw qbxg::InvalidArgument("qbxg_result_exchange_local: handles not rank-ordered");
+    for (int r = 0; r < n; ++r) QCK(cudaStreamSynchronize(hs[r]->h.stream));
+    for (int r = 0; r < n; ++r) {  // each rank's packed segment into every other rank's buffers
+      auto& src = hs[r]->h;
+      const int w = 2 * src.D.kq;
+      for (int q = 0; q < n; ++q) {
+        if (q == r) continue;
+        auto& dst = hs[q]->h;
+        const int64_t a = src.res_off[r], e = src.res_off[r + 1];
+        if (e > a) QCK(cudaMemcpy(dst.d_res_buf + a, src.d_res_buf + a, size_t(e - a) * sizeof(double), cudaMemcpyDefault));
+        const int64_t ca = src.cres_off[r], ce = src.cres_off[r + 1];
+        if (d_coeffs && ce > ca)
+          QCK(cudaMemcpy(dst.d_cres_buf + ca * w, src.d_cres_buf + ca * w, size_t(ce - ca) * w * sizeof(double),
+                         cudaMemcpyDefault));
+      }
+    }
+    for (int r = 0; r < n; ++r) {
+      auto& H = hs[r]->h;
+      qbxg::dev::launch_pack(int(H.nt), H.d_res_idx, 1, d_pots[r], H.d_res_buf, true, H.stream);
+      if (d_coeffs && d_coeffs[r])
+        qbxg::dev::launch_pack(int(H.nc), H.d_cres_idx, 2 * H.D.kq, d_coeffs[r], H.d_cres_buf, true, H.stream);
+      QCK(cudaStreamSynchronize(H.stream));
     }
   });
 }

@@ -345,8 +345,8 @@ __device__ __forceinline__ void near_stage(const DevData& D, const int* __restri
 
 template <int Q, bool DIP>
 __global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevData D, const int* __restrict__ boxes) {
-  constexpr int KQ = hsize(Q), KY = KQ - (Q + 1);  // Re parts, Im parts of m >= 1
-  extern __shared__ double s_part[];                // (KQ + KY) x kNearThreads: saved / partial sums
+  constexpr int KQ = hsize(Q);
+  extern __shared__ double s_part[];  // (2 KQ - Q - 1) x kNearThreads: saved / partial sums (Re, Im of m >= 1)
   __shared__ double4 s_src[kNearBuf][kNearChunk];
   __shared__ double4 s_mu[kNearBuf][DIP ? kNearChunk : 1];
   const int b = boxes[blockIdx.x];
@@ -1554,6 +1554,25 @@ int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr
   const int64_t n = int64_t(nc) * D.kq;
   if (n == 0) return 0;
   k_centre_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(D, nc, items, ctr_perm, out);
+  return 1;
+}
+
+__global__ void k_pack(int n, const int* __restrict__ idx, int width, double* __restrict__ full,
+                       double* __restrict__ buf, int unpack) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(n) * width) return;
+  const int64_t k = t / width, c = t - k * width;
+  const int64_t f = int64_t(idx[k]) * width + c;
+  if (unpack)
+    full[f] = buf[t];
+  else
+    buf[t] = full[f];
+}
+
+int launch_pack(int n, const int* idx, int width, double* full, double* buf, bool unpack, cudaStream_t s) {
+  const int64_t tot = int64_t(n) * width;
+  if (tot == 0) return 0;
+  k_pack<<<unsigned((tot + 255) / 256), 256, 0, s>>>(n, idx, width, full, buf, unpack ? 1 : 0);
   return 1;
 }
 

@@ -161,6 +161,8 @@ int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const dou
                 const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
                 double* pot, cudaStream_t s);
 int launch_centre_out(const DevData& D, int nc, const int* items, const int* ctr_perm, double* out, cudaStream_t s);
+// gather rows (pack: buf[k] = full[idx[k]]) or scatter them back (unpack), `width` doubles each
+int launch_pack(int n, const int* idx, int width, double* full, double* buf, bool unpack, cudaStream_t s);
 // Error path after a non-finite result: the first (kind, particle, source) triple whose
 // near-field pair is coincident, packed (kind << 62 | original id << 31 | original source id),
 // kind 0 = QBX centre, 1 = conventional target; ~0ull when there is none.

@@ -27,7 +27,9 @@
 // Measured and not kept (profiles/r02_summary.md): fusing the reduction into this kernel
 // (target-superblock tile order, per-entry alpha, last-arriving CTA reduces from L2):
 // 50-55 ms vs 43 at config 1 -- the kernel is latency-bound, and the per-entry rotations
-// and the 1.17x tiles cost more than the 37 GB staging round trip they save.
+// and the 1.17x tiles cost more than the 37 GB staging round trip they save; a fully
+// unrolled compile-time block schedule per warp: 30% fewer instructions but 49 ms, half
+// the warp stalls on instruction fetch (the per-warp code no longer fits the I-cache).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -205,9 +207,10 @@ __global__ void __launch_bounds__(kNTh, P <= 15 ? 3 : (P <= 18 ? 2 : 1))
     __syncthreads();
   }
   // staging row = Re (NR) then compacted Im, coalesced along each row (row-outer: one
-  // row per thread and column; consecutive lanes, consecutive rows)
+  // row per thread and column; consecutive lanes, consecutive rows); streaming stores,
+  // so the rows do not evict the multipoles and operators from L2
   for (int r = tid; r < NROW; r += kNTh)
-    for (int c = 0; c < ncol; ++c) temp[size_t(s_pos[c]) * row_stride + r] = X[r * kLD + c];
+    for (int c = 0; c < ncol; ++c) __stcs(temp + size_t(s_pos[c]) * row_stride + r, X[r * kLD + c]);
 }
 
 // Each staging row holds L' of one List-2 entry in its offset's rotated frame (Re rows

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <unordered_map>
 
 #include "plan.hpp"
 
@@ -54,7 +55,8 @@ void validate_inputs(const qbxg_config& cfg, const qbxg_geometry& g) {
     throw InvalidArgument("FmmConfig: unknown kernel");
   if ((cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL || cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL_DL) && !(cfg.helmholtz_k > 0 && std::isfinite(cfg.helmholtz_k)))
     throw InvalidArgument("FmmConfig: Helmholtz needs a positive wavenumber helmholtz_k");
-  if (cfg.reserved != 0) throw InvalidArgument("FmmConfig: level restriction not implemented");
+  if (cfg.level_restrict != 0 && cfg.level_restrict != 1)
+    throw InvalidArgument("FmmConfig: level_restrict must be 0 or 1");
   if (g.n_sources < 0 || g.n_centers < 0 || g.n_targets < 0) throw InvalidArgument("geometry: negative size");
   if (g.n_sources + g.n_centers + g.n_targets >= std::numeric_limits<int32_t>::max())
     throw InvalidArgument("geometry: too many particles for int32 indexing");
@@ -223,6 +225,125 @@ void build_tree(Plan& P, const qbxg_geometry& g) {
       bx[bid] = b;
     }
     cur.swap(next);
+  }
+
+  // Level restriction (Remark C.1 PAPER.md:3661-3687; off unless
+  // cfg.level_restrict): subdivide larger leaves until adjacent leaves (closed boxes
+  // that touch) differ by at most one level.  A leaf A of level a violates when some
+  // leaf of level >= a + 2 touches it; such a leaf lies inside a level-(a+1) box that
+  // touches A, so the level-(a+1) boxes around A are looked up by integer coordinates
+  // and searched downwards through the children that still touch A.  Leaves split
+  // like any box (centres move only when their ball fits the child's TCR; a leaf
+  // whose particles cannot move stays); repeat until no leaf changes.
+  if (cfg.level_restrict) {
+    auto key = [](int level, int64_t x, int64_t y, int64_t z) {
+      return (uint64_t(level) << 58) ^ (uint64_t(x) << 38) ^ (uint64_t(y) << 19) ^ uint64_t(z);
+    };
+    auto touches = [&](const BuildBox& a, const BuildBox& b) {
+      const int L = std::max(a.level, b.level);
+      for (int d = 0; d < 3; ++d) {
+        const int64_t sa = int64_t(1) << (L - a.level), sb = int64_t(1) << (L - b.level);
+        const int64_t a0 = a.ic[d] * sa, a1 = a0 + sa, b0 = b.ic[d] * sb, b1 = b0 + sb;
+        if (a1 < b0 || b1 < a0) return false;
+      }
+      return true;
+    };
+    for (int round = 0;; ++round) {
+      std::unordered_map<uint64_t, int32_t> at;
+      at.reserve(bx.size() * 2);
+      for (int32_t i = 0; i < int32_t(bx.size()); ++i) at[key(bx[i].level, bx[i].ic[0], bx[i].ic[1], bx[i].ic[2])] = i;
+      auto is_leaf = [&](int32_t i) {
+        for (int o = 0; o < 8; ++o)
+          if (bx[i].child[o] >= 0) return false;
+        return true;
+      };
+      std::vector<int32_t> viol;
+      for (int32_t i = 0; i < int32_t(bx.size()); ++i) {
+        if (!is_leaf(i)) continue;
+        const BuildBox& A = bx[i];
+        bool bad = false;
+        for (int64_t dx = -1; dx <= 2 && !bad; ++dx)
+          for (int64_t dy = -1; dy <= 2 && !bad; ++dy)
+            for (int64_t dz = -1; dz <= 2 && !bad; ++dz) {
+              const int64_t x = 2 * A.ic[0] + dx, y = 2 * A.ic[1] + dy, z = 2 * A.ic[2] + dz;
+              if (x < 0 || y < 0 || z < 0) continue;
+              auto it = at.find(key(A.level + 1, x, y, z));
+              if (it == at.end()) continue;
+              // a leaf of level >= a + 2 touching A below this level-(a+1) box?
+              std::vector<int32_t> st;
+              for (int o = 0; o < 8; ++o)
+                if (bx[it->second].child[o] >= 0) st.push_back(bx[it->second].child[o]);
+              while (!st.empty() && !bad) {
+                const int32_t c = st.back();
+                st.pop_back();
+                if (!touches(A, bx[c])) continue;
+                if (is_leaf(c)) {
+                  bad = true;
+                  break;
+                }
+                for (int o = 0; o < 8; ++o)
+                  if (bx[c].child[o] >= 0) st.push_back(bx[c].child[o]);
+              }
+            }
+        if (bad) viol.push_back(i);
+      }
+      int split_any = 0;
+      for (int32_t bid : viol) {
+        BuildBox b = bx[bid];
+        const int64_t n = b.end - b.start;
+        if (n == 0 || b.level + 1 > kMaxDepth) continue;
+        const double hc = 0.5 * b.h;
+        std::vector<uint8_t> dest(n);
+        std::array<int64_t, 9> cnt{};
+        int64_t moving = 0;
+        for (int64_t i = 0; i < n; ++i) {
+          const int32_t k = perm[b.start + i];
+          const double* x = &pos[3 * int64_t(k)];
+          int o = (x[0] >= b.c[0] ? 1 : 0) | (x[1] >= b.c[1] ? 2 : 0) | (x[2] >= b.c[2] ? 4 : 0);
+          if (role[k] == 1) {
+            double cc[3] = {b.c[0] + ((o & 1) ? hc : -hc), b.c[1] + ((o & 2) ? hc : -hc),
+                            b.c[2] + ((o & 4) ? hc : -hc)};
+            if (!ball_fits_tcr(x, rad[k], cc, hc, cfg.t_f)) o = 8;
+          }
+          dest[i] = uint8_t(o);
+          cnt[o]++;
+          if (o != 8) moving++;
+        }
+        if (moving == 0) continue;
+        std::array<int64_t, 9> off{};
+        int64_t acc = cnt[8];
+        for (int o = 0; o < 8; ++o) {
+          off[o] = acc;
+          acc += cnt[o];
+        }
+        std::vector<int32_t> tmp(n);
+        for (int64_t i = 0; i < n; ++i) tmp[off[dest[i]]++] = perm[b.start + i];
+        std::copy(tmp.begin(), tmp.end(), perm.begin() + b.start);
+        b.own = cnt[8];
+        int64_t s = b.start + cnt[8];
+        for (int o = 0; o < 8; ++o) {
+          if (cnt[o] == 0) continue;
+          BuildBox c{};
+          c.c[0] = b.c[0] + ((o & 1) ? hc : -hc);
+          c.c[1] = b.c[1] + ((o & 2) ? hc : -hc);
+          c.c[2] = b.c[2] + ((o & 4) ? hc : -hc);
+          c.h = hc;
+          c.level = b.level + 1;
+          c.parent = bid;
+          for (int d = 0; d < 3; ++d) c.ic[d] = 2 * b.ic[d] + ((o >> d) & 1);
+          c.start = s;
+          c.end = s + cnt[o];
+          c.own = cnt[o];
+          std::fill(c.child, c.child + 8, -1);
+          s += cnt[o];
+          b.child[o] = int32_t(bx.size());
+          bx.push_back(c);
+        }
+        bx[bid] = b;
+        ++split_any;
+      }
+      if (!split_any) break;
+    }
   }
 
   // DFS preorder renumbering (children in octant order)
@@ -640,6 +761,8 @@ int qbxg_plan_create_gpu(const qbxg_config* cfg, const qbxg_geometry* geom, int3
   return qbxg::guarded([&] {
     if (!cfg || !geom || !out) throw qbxg::InvalidArgument("plan_create_gpu: null argument");
     qbxg::validate_inputs(*cfg, *geom);
+    if (cfg->level_restrict)
+      throw qbxg::InvalidArgument("plan_create_gpu: level restriction is built by the host plan (qbxg_plan_create)");
     auto* pl = new qbxg_plan;
     try {
       pl->p.cfg = *cfg;

@@ -157,3 +157,17 @@ def test_batched_densities(n_rhs):
     again = eng.apply_batch(W, MU)
     assert np.array_equal(again, pots), "batched apply is not bitwise deterministic"
     eng.close()
+
+
+def test_level_restricted_tree_vs_oracle():
+    """FmmConfig(level_restrict=1): the GPU apply on the level-restricted tree
+    matches the oracle on the same tree, and both stay within FMM accuracy of the
+    unrestricted tree's result."""
+    g = api.config_geometry(2, level=2, n_volume_targets=2000)
+    cfg = api.FmmConfig(p_fmm=10, p_qbx=4, n_max=16, level_restrict=1, w_far_demote=10 ** 3 // 16)
+    pot, _ = _check(g, cfg, False)
+    cfg0 = api.FmmConfig(p_fmm=10, p_qbx=4, n_max=16, w_far_demote=10 ** 3 // 16)
+    eng = api.FmmEngine(cfg0, g)
+    pot0 = eng.apply(g.weights())
+    eng.close()
+    assert rel(pot, pot0) < 1e-6

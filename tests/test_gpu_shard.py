@@ -75,3 +75,36 @@ def test_shard_roles_partition():
     assert straddle0[0]  # the root straddles every cut
     # cost balance: every rank holds at least some target boxes
     assert len(np.unique(cuts)) == n + 1
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_result_allgather_equals_single_bitwise(nranks):
+    """The result all-gather of a sharded apply (packed owned segments broadcast to every
+    rank and scattered; qbxg_result_exchange_local standing in for the grouped NCCL
+    broadcasts) leaves the whole single-GPU result on every rank, bitwise."""
+    import torch
+    g = api.config_geometry(2, level=2, n_volume_targets=3000)
+    cfg = api.config_fmm(2)
+    plan = api.Plan(cfg, g)
+    w = g.weights()
+    ref = api.FmmEngine(cfg, g, plan)
+    pot1, c1 = ref.apply(w, None, want_centers=True)
+    ref.close()
+    dev = torch.device("cuda", 0)
+    dw = torch.from_numpy(w).to(dev)
+    engines = [api.FmmEngine(cfg, g, plan, shard=(nranks, r)) for r in range(nranks)]
+    pots = [torch.empty(g.n_targets, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    coefs = [torch.empty(g.n_centers * 2 * cfg.kq, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    for e in engines:
+        e.apply_phase(1, dw.data_ptr(), None, None)
+    api.exchange_local(engines)
+    for e, p, c in zip(engines, pots, coefs):
+        e.apply_phase(2, dw.data_ptr(), None, p.data_ptr(), c.data_ptr())
+    api.exchange_results_local(engines, [p.data_ptr() for p in pots], [c.data_ptr() for c in coefs])
+    torch.cuda.synchronize()
+    for p, c in zip(pots, coefs):
+        assert np.array_equal(p.cpu().numpy(), pot1)
+        cc = c.cpu().numpy().reshape(g.n_centers, cfg.kq, 2)
+        assert np.array_equal(cc[..., 0] + 1j * cc[..., 1], c1)
+    for e in engines:
+        e.close()

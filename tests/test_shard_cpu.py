@@ -1,7 +1,11 @@
-"""Multi-rank protocol on CPU (gloo, world_size 2): the product's shard
-partition (qbxg_plan_shard) + multipole exchange + straddle recompute + result
-sum, executed by the oracle in two processes, must reproduce the single-process
-oracle bitwise ("G-GPU output must be bitwise identical")."""
+"""Multi-rank protocol on CPU (gloo, world_size 2): the product's shard partition
+(qbxg_plan_shard), the multipole exchange as one broadcast per rank of its box range,
+the straddle recompute, and the result all-gather as one broadcast per rank of its
+packed owned targets / centres (the layout csrc/cuda/handle.cu builds for the NCCL
+path: rank-major; associated targets in target order, then conventional targets in
+box order; centres in box order), executed by the oracle in two processes, must
+reproduce the single-process oracle bitwise ("G-GPU output must be
+bitwise identical")."""
 import os
 import socket
 
@@ -35,14 +39,42 @@ def _worker(rank, world, port, out_dir):
     Mbuf = np.zeros(plan.view.n_boxes * kp * 2)
     w, mu = g.weights(), g.dipoles()
     O.execute_phase(plan, g, w, mu, mask, 1, Mbuf)
-    t = torch.from_numpy(Mbuf)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)  # each owned row has exactly one non-zero contributor
-    Mbuf = t.numpy()
-    pot, coef = O.execute_phase(plan, g, w, mu, mask, 2, Mbuf, want_centers=True)
-    tp = torch.from_numpy(pot)
-    tc = torch.from_numpy(np.ascontiguousarray(np.stack([coef.real, coef.imag], -1)).reshape(-1))
-    dist.all_reduce(tp, op=dist.ReduceOp.SUM)
-    dist.all_reduce(tc, op=dist.ReduceOp.SUM)
+    rows = Mbuf.reshape(plan.view.n_boxes, -1)
+    for r in range(world):  # multipole exchange: rank r's box range from rank r
+        seg = torch.from_numpy(np.ascontiguousarray(rows[cuts[r]:cuts[r + 1]]))
+        dist.broadcast(seg, src=r)
+        rows[cuts[r]:cuts[r + 1]] = seg.numpy()
+    pot, coef = O.execute_phase(plan, g, w, mu, mask, 2, rows.reshape(-1), want_centers=True)
+    # result all-gather: packed owned segments, one broadcast per rank, then scatter
+    A = plan.arrays()
+    owner = lambda b: int(np.searchsorted(cuts, b, side="right") - 1)  # noqa: E731
+    ctr_box = np.empty(g.n_centers, dtype=np.int64)
+    for b in range(A["n_boxes"]):
+        s0, n = A["ctr_own_start"][b], A["ctr_own_count"][b]
+        ctr_box[A["ctr_perm"][s0:s0 + n]] = b
+    tseg = [[] for _ in range(world)]
+    cseg = [[] for _ in range(world)]
+    for t in np.nonzero(g.association >= 0)[0]:
+        tseg[owner(ctr_box[g.association[t]])].append(t)
+    for b in range(A["n_boxes"]):
+        s0, n = A["tgt_own_start"][b], A["tgt_own_count"][b]
+        tseg[owner(b)].extend(A["tgt_perm"][s0:s0 + n])
+        s0, n = A["ctr_own_start"][b], A["ctr_own_count"][b]
+        cseg[owner(b)].extend(A["ctr_perm"][s0:s0 + n])
+    full_pot = np.zeros(g.n_targets)
+    full_coef = np.zeros(coef.shape, dtype=complex)
+    for r in range(world):
+        ti, ci = np.array(tseg[r], dtype=np.int64), np.array(cseg[r], dtype=np.int64)
+        tp = torch.from_numpy(np.ascontiguousarray(pot[ti]) if r == rank else np.zeros(ti.size))
+        tc = torch.from_numpy(np.ascontiguousarray(np.stack([coef[ci].real, coef[ci].imag], -1)) if r == rank
+                              else np.zeros((ci.size,) + coef.shape[1:] + (2,)))
+        dist.broadcast(tp, src=r)
+        dist.broadcast(tc, src=r)
+        full_pot[ti] = tp.numpy()
+        full_coef[ci] = tc.numpy()[..., 0] + 1j * tc.numpy()[..., 1]
+    assert sum(len(x) for x in tseg) == g.n_targets and sum(len(x) for x in cseg) == g.n_centers
+    tp = torch.from_numpy(full_pot)
+    tc = torch.from_numpy(np.ascontiguousarray(np.stack([full_coef.real, full_coef.imag], -1)).reshape(-1))
     if rank == 0:
         np.save(os.path.join(out_dir, "pot.npy"), tp.numpy())
         np.save(os.path.join(out_dir, "coef.npy"), tc.numpy())

@@ -24,6 +24,8 @@ def _cases():
          api.FmmConfig(p_fmm=6, p_qbx=3, n_max=24, kernel=1, w_far_demote=20)),
         ("urchin-array-small", api.config_geometry(4, variant=8, level=0),
          api.FmmConfig(p_fmm=6, p_qbx=3, n_max=12)),
+        ("urchin-vol-level-restricted", api.config_geometry(2, level=1, n_volume_targets=300),
+         api.FmmConfig(p_fmm=6, p_qbx=3, n_max=16, level_restrict=1)),
     ]
 
 
@@ -156,3 +158,37 @@ def test_plan_input_errors():
     with pytest.raises(ValueError):
         api.Plan(api.FmmConfig(p_fmm=5, p_qbx=3),
                  api.Geometry(nanpos, g.center_pos, g.center_radius, g.target_pos, g.association))
+
+
+def _leaf_level_violations(a):
+    """Pairs of adjacent leaves (closed boxes that touch) more than one level apart."""
+    leaf = np.nonzero((a["box_flags"] & 8) > 0)[0]
+    c, h, lev = a["box_center"][leaf], a["box_radius"][leaf], a["box_level"][leaf]
+    d = np.abs(c[:, None, :] - c[None, :, :]).max(-1)
+    adj = d <= (h[:, None] + h[None, :]) * (1 + 1e-12)
+    return int((adj & (np.abs(lev[:, None] - lev[None, :]) > 1)).sum() // 2)
+
+
+@pytest.mark.parametrize("case", ["urchin-vol", "torus"])
+def test_level_restriction(case):
+    """SPEC.md:397 / Remark C.1: with level_restrict, adjacent leaves
+    differ by at most one level; particles and the list invariants are untouched."""
+    if case == "urchin-vol":
+        g = api.config_geometry(2, level=2, n_volume_targets=2000)
+        base = dict(p_fmm=8, p_qbx=4, n_max=16)
+    else:
+        g = api.config_geometry(1, nu=24, nv=12)
+        base = dict(p_fmm=8, p_qbx=4, n_max=24, kernel=1)
+    a0 = api.Plan(api.FmmConfig(**base), g).arrays()
+    plan = api.Plan(api.FmmConfig(**base, level_restrict=1), g)
+    a1 = plan.arrays()
+    assert _leaf_level_violations(a0) > 0           # the unrestricted tree does violate it
+    assert _leaf_level_violations(a1) == 0
+    assert a1["n_boxes"] > a0["n_boxes"]
+    for k in ("src_perm", "ctr_perm", "tgt_perm"):
+        assert np.array_equal(np.sort(a1[k]), np.sort(a0[k]))
+    for k, bound in ((1, 875), (4, 250), (5, 375)):
+        s, _ = plan.list_csr(k)
+        assert np.diff(s).max() <= bound
+    with pytest.raises(ValueError, match="host plan"):
+        api.Plan(api.FmmConfig(**base, level_restrict=1), g, device="gpu")
