@@ -1,16 +1,14 @@
-// Box expansion -> QBX-centre local translations, one thread per centre:
+// Box expansion -> QBX-centre local translations and M2P:
 //   Stage 5b M2QBXL (List 3 far):
 //     L~_c(n,m) += (r/h)^n (1/h) (-1)^{n+m} sum_{j<=p,k} M~_d(j,k) I_{j+n}^{k-m}((c - c_d)/h)
 //   Stage 8 L2QBXL:
 //     L~_c(n,m) += (r/h)^n sum_{j>=n,k} L~_b(j,k) R_{j-n}^{k-m}((c - c_b)/h)
 //   Stage 5b M2P at conventional targets:
 //     phi_t += (1/h) sum_{n,m} M~_d(n,m) I_n^m((t - c_d)/h)
-// The source expansion (shared by every centre of the CTA's box) sits in
-// shared memory as a full (p+1)^2 table and is read as warp-wide broadcasts;
-// each thread streams its own harmonics one azimuthal column K at a time
-// (Cartesian recurrences in n), keeps the column in its private shared-memory
-// slot and accumulates the q-th order local in registers.  Nothing is ever
-// materialised per (centre, source box) pair beyond one column.
+// M2QBXL runs box-major over (centre, List-3-far box) pairs (k_m2qbxl3 + the centre-major
+// pair reduce), L2QBXL over CTAs of <= 128 centres from <= 8 boxes (k_l2qbxl3); both
+// stage the box expansions in shared memory and stream each centre's harmonics one
+// azimuthal column at a time in registers.
 #include <cuda_runtime.h>
 
 #include "harmonics.cuh"
@@ -20,270 +18,6 @@ namespace qbxg {
 namespace dev {
 
 namespace {
-
-constexpr int kCT = 32;  // threads (centres) per CTA: one warp per box
-
-__device__ __forceinline__ int fidx(int j, int k) { return j * j + j + k; }
-
-// Expand a half table (order P) into a full table with X_j^{-k} = (-1)^k conj(X_j^k).
-__device__ __forceinline__ void load_full(const double2* __restrict__ half, int P, double2* full) {
-  for (int i = threadIdx.x; i < (P + 1) * (P + 1); i += blockDim.x) {
-    int j = int(sqrt(double(i)));
-    while (j * j > i) --j;
-    while ((j + 1) * (j + 1) <= i) ++j;
-    const int k = i - j * j - j;
-    double2 v = half[hidx(j, k < 0 ? -k : k)];
-    if (k < 0) v = (k & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
-    full[i] = v;
-  }
-}
-
-// t(n,m) = sum over the full input table A (order P) and one harmonic column
-// family X (irregular: X_{j+n}; regular: X_{j-n}) of A(j,k) X_N^{k-m}.
-template <int Q, bool IRREG>
-__device__ __forceinline__ void contract(const double2* __restrict__ A, int P, double x, double y, double z,
-                                         double2* __restrict__ col /* thread-strided */, double (&tx)[hsize(Q)],
-                                         double (&ty)[hsize(Q)]) {
-  const int NN = IRREG ? P + Q : P;
-  const double r2 = x * x + y * y + z * z;
-  const double ir2 = 1.0 / r2;
-  double2 diag = IRREG ? make_double2(sqrt(ir2), 0.0) : make_double2(1.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < hsize(Q); ++i) tx[i] = ty[i] = 0.0;
-  for (int K = 0; K <= NN; ++K) {
-    // --- column K: X_N^K for N = K..NN
-    if (K > 0) {
-      const double s = IRREG ? (2 * K - 1) * ir2 : 1.0 / (2.0 * K);
-      diag = make_double2((diag.x * x - diag.y * y) * s, (diag.x * y + diag.y * x) * s);
-    }
-    col[K * kCT] = diag;
-    if (K + 1 <= NN) {
-      double2 a = diag;
-      const double s1 = IRREG ? (2 * K + 1) * z * ir2 : z;
-      double2 b = make_double2(s1 * diag.x, s1 * diag.y);
-      col[(K + 1) * kCT] = b;
-      for (int N = K + 2; N <= NN; ++N) {
-        const double c1 = (2 * N - 1) * z;
-        double2 c;
-        if (IRREG) {
-          const double c2 = double((N - 1 + K) * (N - 1 - K));
-          c = make_double2((c1 * b.x - c2 * a.x) * ir2, (c1 * b.y - c2 * a.y) * ir2);
-        } else {
-          // (c_inv_nm is per translation unit and only uploaded in kernels.cu)
-          const double f = 1.0 / double((N - K) * (N + K));
-          c = make_double2((c1 * b.x - r2 * a.x) * f, (c1 * b.y - r2 * a.y) * f);
-        }
-        col[N * kCT] = c;
-        a = b;
-        b = c;
-      }
-    }
-    const double sgnK = (K & 1) ? -1.0 : 1.0;
-    // --- contraction with this column
-    for (int N = K; N <= NN; ++N) {
-      const double2 cp = col[N * kCT];
-      const double2 cm = make_double2(sgnK * cp.x, -sgnK * cp.y);  // X_N^{-K}
-#pragma unroll
-      for (int n = 0; n <= Q; ++n) {
-        const int j = IRREG ? N - n : N + n;
-        if (j < 0 || j > P) continue;
-#pragma unroll
-        for (int m = 0; m <= n; ++m) {
-          const int id = hidx(n, m);
-          const int kp = m + K;
-          if (kp <= j) {
-            const double2 a = A[fidx(j, kp)];
-            tx[id] += a.x * cp.x - a.y * cp.y;
-            ty[id] += a.x * cp.y + a.y * cp.x;
-          }
-          if (K > 0) {
-            const int km = m - K;
-            if (km >= -j && km <= j) {
-              const double2 a = A[fidx(j, km)];
-              tx[id] += a.x * cm.x - a.y * cm.y;
-              ty[id] += a.x * cm.y + a.y * cm.x;
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-// Same contraction with compile-time orders: every loop unrolls, out-of-range
-// terms vanish at compile time and the current column lives in registers.
-template <int P, int Q, bool IRREG>
-__device__ __forceinline__ void contract_fixed(const double2* __restrict__ A, double x, double y, double z,
-                                               double (&tx)[hsize(Q)], double (&ty)[hsize(Q)]) {
-  constexpr int NN = IRREG ? P + Q : P;
-  const double r2 = x * x + y * y + z * z;
-  const double ir2 = 1.0 / r2;
-  double2 diag = IRREG ? make_double2(sqrt(ir2), 0.0) : make_double2(1.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < hsize(Q); ++i) tx[i] = ty[i] = 0.0;
-#pragma unroll
-  for (int K = 0; K <= NN; ++K) {
-    if (K > 0) {
-      const double s = IRREG ? (2 * K - 1) * ir2 : 1.0 / (2.0 * K);
-      diag = make_double2((diag.x * x - diag.y * y) * s, (diag.x * y + diag.y * x) * s);
-    }
-    double2 col[NN + 1];
-    col[K] = diag;
-    if (K + 1 <= NN) {
-      const double s1 = IRREG ? (2 * K + 1) * z * ir2 : z;
-      col[K + 1] = make_double2(s1 * diag.x, s1 * diag.y);
-    }
-#pragma unroll
-    for (int N = K + 2; N <= NN; ++N) {
-      const double c1 = (2 * N - 1) * z;
-      const double2 a = col[N - 2], b = col[N - 1];
-      if (IRREG) {
-        const double c2 = double((N - 1 + K) * (N - 1 - K));
-        col[N] = make_double2((c1 * b.x - c2 * a.x) * ir2, (c1 * b.y - c2 * a.y) * ir2);
-      } else {
-        const double f = 1.0 / double((N - K) * (N + K));
-        col[N] = make_double2((c1 * b.x - r2 * a.x) * f, (c1 * b.y - r2 * a.y) * f);
-      }
-    }
-    constexpr double dummy = 0;  // keeps nvcc from complaining about unused constexpr in some paths
-    (void)dummy;
-#pragma unroll
-    for (int N = K; N <= NN; ++N) {
-      const double2 cp = col[N];
-      const double sg = (K & 1) ? -1.0 : 1.0;
-      const double2 cm = make_double2(sg * cp.x, -sg * cp.y);
-#pragma unroll
-      for (int n = 0; n <= Q; ++n) {
-        const int j = IRREG ? N - n : N + n;
-        if (j < 0 || j > P) continue;
-#pragma unroll
-        for (int m = 0; m <= n; ++m) {
-          const int id = hidx(n, m);
-          const int kp = m + K;
-          if (kp <= j) {
-            const double2 a = A[fidx(j, kp)];
-            tx[id] += a.x * cp.x - a.y * cp.y;
-            ty[id] += a.x * cp.y + a.y * cp.x;
-          }
-          const int km = m - K;
-          if (K > 0 && km >= -j && km <= j) {
-            const double2 a = A[fidx(j, km)];
-            tx[id] += a.x * cm.x - a.y * cm.y;
-            ty[id] += a.x * cm.y + a.y * cm.x;
-          }
-        }
-      }
-    }
-  }
-}
-
-// Dispatch: compile-time orders for the BASELINE (p, q) pairs, runtime otherwise.
-template <int Q, bool IRREG>
-__device__ __forceinline__ void contract_any(const double2* A, int P, double x, double y, double z, double2* col,
-                                             double (&tx)[hsize(Q)], double (&ty)[hsize(Q)]) {
-  if constexpr (Q == 5) {
-    if (P == 15) {
-      contract_fixed<15, 5, IRREG>(A, x, y, z, tx, ty);
-      return;
-    }
-  }
-  if constexpr (Q == 3) {
-    if (P == 10) {
-      contract_fixed<10, 3, IRREG>(A, x, y, z, tx, ty);
-      return;
-    }
-  }
-  contract<Q, IRREG>(A, P, x, y, z, col, tx, ty);
-}
-
-template <int Q>
-__global__ void __launch_bounds__(kCT) k_m2qbxl(DevData D, const int* __restrict__ boxes) {
-  constexpr int KQ = hsize(Q);
-  extern __shared__ double2 sm[];
-  double2* A = sm;                                   // (p+1)^2
-  double2* col = sm + (D.p + 1) * (D.p + 1) + threadIdx.x;  // thread-strided column
-  const int b = boxes[blockIdx.x];
-  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
-  const int64_t eb = D.wfar_starts[b], ee = D.wfar_starts[b + 1];
-  for (int cc = 0; cc < nctr; cc += kCT) {
-    const int ci = cc + threadIdx.x;
-    const bool active = ci < nctr;
-    double4 c = make_double4(0, 0, 0, 1);
-    if (active) c = D.ctr[c0 + ci];
-    double ax[KQ], ay[KQ];
-#pragma unroll
-    for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
-    for (int64_t e = eb; e < ee; ++e) {
-      const int d = D.wfar_box[e];
-      const double4 bd = D.box[d];
-      const double ih = 1.0 / bd.w;
-      __syncthreads();
-      load_full(D.M + size_t(d) * D.kp, D.p, A);
-      __syncthreads();
-      if (active) {
-        double tx[KQ], ty[KQ];
-        contract_any<Q, true>(A, D.p, (c.x - bd.x) * ih, (c.y - bd.y) * ih, (c.z - bd.z) * ih, col, tx, ty);
-        double f = ih;  // (r/h)^n / h
-        const double rh = c.w * ih;
-#pragma unroll
-        for (int n = 0; n <= Q; ++n) {
-#pragma unroll
-          for (int m = 0; m <= n; ++m) {
-            const double s = ((n + m) & 1) ? -f : f;
-            ax[hidx(n, m)] += s * tx[hidx(n, m)];
-            ay[hidx(n, m)] += s * ty[hidx(n, m)];
-          }
-          f *= rh;
-        }
-      }
-    }
-    if (active) {
-      double2* out = D.Lc + size_t(c0 + ci) * KQ;
-#pragma unroll
-      for (int i = 0; i < KQ; ++i) {
-        double2 v = out[i];
-        v.x += ax[i];
-        v.y += ay[i];
-        out[i] = v;
-      }
-    }
-  }
-}
-
-template <int Q>
-__global__ void __launch_bounds__(kCT) k_l2qbxl2(DevData D, const int* __restrict__ boxes) {
-  constexpr int KQ = hsize(Q);
-  extern __shared__ double2 sm[];
-  double2* A = sm;
-  double2* col = sm + (D.p + 1) * (D.p + 1) + threadIdx.x;
-  const int b = boxes[blockIdx.x];
-  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
-  const double4 bc = D.box[b];
-  const double ih = 1.0 / bc.w;
-  load_full(D.L + size_t(b) * D.kp, D.p, A);
-  __syncthreads();
-  for (int cc = 0; cc < nctr; cc += kCT) {
-    const int ci = cc + threadIdx.x;
-    if (ci >= nctr) continue;
-    const double4 c = D.ctr[c0 + ci];
-    double tx[KQ], ty[KQ];
-    contract<Q, false>(A, D.p, (c.x - bc.x) * ih, (c.y - bc.y) * ih, (c.z - bc.z) * ih, col, tx, ty);
-    double2* out = D.Lc + size_t(c0 + ci) * KQ;
-    double f = 1.0;
-    const double rh = c.w * ih;
-#pragma unroll
-    for (int n = 0; n <= Q; ++n) {
-#pragma unroll
-      for (int m = 0; m <= n; ++m) {
-        double2 v = out[hidx(n, m)];
-        v.x += f * tx[hidx(n, m)];
-        v.y += f * ty[hidx(n, m)];
-        out[hidx(n, m)] = v;
-      }
-      f *= rh;
-    }
-  }
-}
 
 // M2P: conventional targets of boxes with List 3 far entries; thread per target.
 __global__ void __launch_bounds__(128) k_m2p(DevData D, const int* __restrict__ boxes) {
@@ -338,178 +72,6 @@ __global__ void __launch_bounds__(128) k_m2p(DevData D, const int* __restrict__ 
   }
 }
 
-// ---- flat variants: one thread per centre over all centres, expansion read
-// through the read-only cache from the global half table (consecutive centres
-// share a box, so a warp touches one or two expansions).
-constexpr int kFT = 128;
-
-__device__ __forceinline__ double2 ldcoef(const double2* __restrict__ T, int j, int k) {
-  if (k >= 0) return __ldg(T + hidx(j, k));
-  const double2 v = __ldg(T + hidx(j, -k));
-  return (k & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
-}
-
-template <int Q, bool IRREG>
-__device__ __forceinline__ void contract_g(const double2* __restrict__ T, int P, double x, double y, double z,
-                                           double2* __restrict__ col, double (&tx)[hsize(Q)],
-                                           double (&ty)[hsize(Q)]) {
-  const int NN = IRREG ? P + Q : P;
-  const double r2 = x * x + y * y + z * z;
-  const double ir2 = 1.0 / r2;
-  double2 diag = IRREG ? make_double2(sqrt(ir2), 0.0) : make_double2(1.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < hsize(Q); ++i) tx[i] = ty[i] = 0.0;
-  for (int K = 0; K <= NN; ++K) {
-    if (K > 0) {
-      const double s = IRREG ? (2 * K - 1) * ir2 : 1.0 / (2.0 * K);
-      diag = make_double2((diag.x * x - diag.y * y) * s, (diag.x * y + diag.y * x) * s);
-    }
-    col[K * kFT] = diag;
-    if (K + 1 <= NN) {
-      double2 a = diag;
-      const double s1 = IRREG ? (2 * K + 1) * z * ir2 : z;
-      double2 b = make_double2(s1 * diag.x, s1 * diag.y);
-      col[(K + 1) * kFT] = b;
-      for (int N = K + 2; N <= NN; ++N) {
-        const double c1 = (2 * N - 1) * z;
-        double2 c;
-        if (IRREG) {
-          const double c2 = double((N - 1 + K) * (N - 1 - K));
-          c = make_double2((c1 * b.x - c2 * a.x) * ir2, (c1 * b.y - c2 * a.y) * ir2);
-        } else {
-          const double f = 1.0 / double((N - K) * (N + K));
-          c = make_double2((c1 * b.x - r2 * a.x) * f, (c1 * b.y - r2 * a.y) * f);
-        }
-        col[N * kFT] = c;
-        a = b;
-        b = c;
-      }
-    }
-    const double sgnK = (K & 1) ? -1.0 : 1.0;
-    for (int N = K; N <= NN; ++N) {
-      const double2 cp = col[N * kFT];
-      const double2 cm = make_double2(sgnK * cp.x, -sgnK * cp.y);
-#pragma unroll
-      for (int n = 0; n <= Q; ++n) {
-        const int j = IRREG ? N - n : N + n;
-        if (j < 0 || j > P) continue;
-#pragma unroll
-        for (int m = 0; m <= n; ++m) {
-          const int id = hidx(n, m);
-          const int kp = m + K;
-          if (kp <= j) {
-            const double2 a = __ldg(T + hidx(j, kp));
-            tx[id] += a.x * cp.x - a.y * cp.y;
-            ty[id] += a.x * cp.y + a.y * cp.x;
-          }
-          const int km = m - K;
-          if (K > 0 && km >= -j && km <= j) {
-            const double2 a = ldcoef(T, j, km);
-            tx[id] += a.x * cm.x - a.y * cm.y;
-            ty[id] += a.x * cm.y + a.y * cm.x;
-          }
-        }
-      }
-    }
-  }
-}
-
-// items: sorted centre indices (all centres for L2QBXL; centres of boxes with
-// List 3 far entries for M2QBXL); ctr_box: owning box of each sorted centre.
-template <int Q, bool IRREG>
-__global__ void __launch_bounds__(kFT) k_ctr_flat(DevData D, const int* __restrict__ items, int n,
-                                                  const int* __restrict__ ctr_box) {
-  constexpr int KQ = hsize(Q);
-  extern __shared__ double2 sm[];
-  double2* col = sm + threadIdx.x;
-  const int i = blockIdx.x * kFT + threadIdx.x;
-  if (i >= n) return;
-  const int cs = items[i];
-  const int b = ctr_box[cs];
-  const double4 c = D.ctr[cs];
-  double ax[KQ], ay[KQ];
-#pragma unroll
-  for (int t = 0; t < KQ; ++t) ax[t] = ay[t] = 0.0;
-  if (IRREG) {
-    for (int64_t e = D.wfar_starts[b]; e < D.wfar_starts[b + 1]; ++e) {
-      const int d = D.wfar_box[e];
-      const double4 bd = D.box[d];
-      const double ih = 1.0 / bd.w;
-      double tx[KQ], ty[KQ];
-      contract_g<Q, true>(D.M + size_t(d) * D.kp, D.p, (c.x - bd.x) * ih, (c.y - bd.y) * ih, (c.z - bd.z) * ih,
-                          col, tx, ty);
-      double f = ih;
-      const double rh = c.w * ih;
-#pragma unroll
-      for (int nn = 0; nn <= Q; ++nn) {
-#pragma unroll
-        for (int m = 0; m <= nn; ++m) {
-          const double s = ((nn + m) & 1) ? -f : f;
-          ax[hidx(nn, m)] += s * tx[hidx(nn, m)];
-          ay[hidx(nn, m)] += s * ty[hidx(nn, m)];
-        }
-        f *= rh;
-      }
-    }
-  } else {
-    const double4 bc = D.box[b];
-    const double ih = 1.0 / bc.w;
-    contract_g<Q, false>(D.L + size_t(b) * D.kp, D.p, (c.x - bc.x) * ih, (c.y - bc.y) * ih, (c.z - bc.z) * ih, col,
-                         ax, ay);
-    double f = 1.0;
-    const double rh = c.w * ih;
-#pragma unroll
-    for (int nn = 0; nn <= Q; ++nn) {
-#pragma unroll
-      for (int m = 0; m <= nn; ++m) {
-        ax[hidx(nn, m)] *= f;
-        ay[hidx(nn, m)] *= f;
-      }
-      f *= rh;
-    }
-  }
-  double2* out = D.Lc + size_t(cs) * KQ;
-#pragma unroll
-  for (int t = 0; t < KQ; ++t) {
-    double2 v = out[t];
-    v.x += ax[t];
-    v.y += ay[t];
-    out[t] = v;
-  }
-}
-
-// M2QBXL over (centre, List-3-far box) pairs: one thread per pair writes its
-// scaled contribution to a staging row; k_pair_reduce sums each centre's rows
-// in list order (deterministic, no atomics).
-template <int Q>
-__global__ void __launch_bounds__(kFT) k_m2qbxl_pair(DevData D, const int2* __restrict__ pairs, int n,
-                                                     double2* __restrict__ temp) {
-  constexpr int KQ = hsize(Q);
-  extern __shared__ double2 sm[];
-  double2* col = sm + threadIdx.x;
-  const int i = blockIdx.x * kFT + threadIdx.x;
-  if (i >= n) return;
-  const int2 pr = pairs[i];  // (sorted centre, source box)
-  const double4 c = D.ctr[pr.x];
-  const double4 bd = D.box[pr.y];
-  const double ih = 1.0 / bd.w;
-  double tx[KQ], ty[KQ];
-  contract_g<Q, true>(D.M + size_t(pr.y) * D.kp, D.p, (c.x - bd.x) * ih, (c.y - bd.y) * ih, (c.z - bd.z) * ih, col,
-                      tx, ty);
-  double f = ih;
-  const double rh = c.w * ih;
-  double2* out = temp + size_t(i) * KQ;
-#pragma unroll
-  for (int nn = 0; nn <= Q; ++nn) {
-#pragma unroll
-    for (int m = 0; m <= nn; ++m) {
-      const double s = ((nn + m) & 1) ? -f : f;
-      out[hidx(nn, m)] = make_double2(s * tx[hidx(nn, m)], s * ty[hidx(nn, m)]);
-    }
-    f *= rh;
-  }
-}
-
 __global__ void k_pair_reduce(const int* __restrict__ centres, const int* __restrict__ starts, int n, int kq,
                               int pair_base, const double2* __restrict__ temp, double2* __restrict__ Lc) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -524,16 +86,6 @@ __global__ void k_pair_reduce(const int* __restrict__ centres, const int* __rest
   Lc[size_t(centres[i]) * kq + c] = acc;
 }
 
-template <int Q>
-void pair_q(const DevData& D, const int2* pairs, int n, double2* temp, cudaStream_t s) {
-  const size_t smem = size_t(kFT) * (D.p + D.q + 1) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_m2qbxl_pair<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  k_m2qbxl_pair<Q><<<(n + kFT - 1) / kFT, kFT, smem, s>>>(D, pairs, n, temp);
-}
 
 // L2QBXL, box-table variant: a CTA takes up to kL3Threads consecutive centres
 // spanning at most kL3Boxes boxes (host-built descriptors).  Each box's local
@@ -814,104 +366,28 @@ void w3_q(const DevData& D, const PairChunk& C, double2* temp, cudaStream_t s) {
   k_m2qbxl3<Q><<<C.n_ctas, kW3Threads, smem, s>>>(D, C.pairs, C.perm, C.ctas, temp);
 }
 
-template <int Q>
-void flat_q(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s) {
-  const size_t smem = size_t(kFT) * (D.p + D.q + 1) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ctr_flat<Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_ctr_flat<Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  const int grid = (n + kFT - 1) / kFT;
-  if (irreg)
-    k_ctr_flat<Q, true><<<grid, kFT, smem, s>>>(D, items, n, ctr_box);
-  else
-    k_ctr_flat<Q, false><<<grid, kFT, smem, s>>>(D, items, n, ctr_box);
-}
-
-template <int Q>
-void launch_q(const DevData& D, const int* wboxes, int nw, const int* cboxes, int nc, cudaStream_t s, int& k,
-              bool l2qbxl) {
-  const size_t smem = ((D.p + 1) * (D.p + 1) + size_t(kCT) * (D.p + D.q + 1)) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_m2qbxl<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_l2qbxl2<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  if (l2qbxl) {
-    if (nc > 0) {
-      k_l2qbxl2<Q><<<nc, kCT, smem, s>>>(D, cboxes);
-      ++k;
-    }
-  } else if (nw > 0) {
-    k_m2qbxl<Q><<<nw, kCT, smem, s>>>(D, wboxes);
-    ++k;
-  }
-}
-
-int dispatch(const DevData& D, const int* wboxes, int nw, const int* cboxes, int nc, cudaStream_t s, bool l2qbxl) {
-  int k = 0;
-  switch (D.q) {
-    case 0: launch_q<0>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 1: launch_q<1>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 2: launch_q<2>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 3: launch_q<3>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 4: launch_q<4>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 5: launch_q<5>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 6: launch_q<6>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 7: launch_q<7>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    case 8: launch_q<8>(D, wboxes, nw, cboxes, nc, s, k, l2qbxl); break;
-    default: return -1;
-  }
-  return k;
-}
-
 }  // namespace
 
-int launch_wfar2(const DevData& D, const int* ctr_boxes, int n_ctr, const int* tgt_boxes, int n_tgt,
-                 cudaStream_t s) {
-  int k = dispatch(D, ctr_boxes, n_ctr, nullptr, 0, s, false);
-  if (k < 0) return k;
-  if (n_tgt > 0) {
-    k_m2p<<<n_tgt, 128, D.kp * sizeof(double2), s>>>(D, tgt_boxes);
-    ++k;
-  }
-  return k;
-}
-
-int launch_l2qbxl2(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  return dispatch(D, nullptr, 0, boxes, n, s, true);
+int launch_m2p(const DevData& D, const int* tgt_boxes, int n_tgt, cudaStream_t s) {
+  if (n_tgt == 0) return 0;
+  k_m2p<<<n_tgt, 128, D.kp * sizeof(double2), s>>>(D, tgt_boxes);
+  return 1;
 }
 
 int launch_m2qbxl_pairs(const DevData& D, const PairPlan& P, cudaStream_t s) {
   int k = 0;
   for (const PairChunk& C : P.chunks) {
     if (C.n_pairs == 0) continue;
-    if (P.box_major) {
-      switch (D.q) {
-        case 0: w3_q<0>(D, C, P.temp, s); break;
-        case 1: w3_q<1>(D, C, P.temp, s); break;
-        case 2: w3_q<2>(D, C, P.temp, s); break;
-        case 3: w3_q<3>(D, C, P.temp, s); break;
-        case 4: w3_q<4>(D, C, P.temp, s); break;
-        case 5: w3_q<5>(D, C, P.temp, s); break;
-        case 6: w3_q<6>(D, C, P.temp, s); break;
-        case 7: w3_q<7>(D, C, P.temp, s); break;
-        case 8: w3_q<8>(D, C, P.temp, s); break;
-        default: return -1;
-      }
-    } else switch (D.q) {
-      case 0: pair_q<0>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 1: pair_q<1>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 2: pair_q<2>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 3: pair_q<3>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 4: pair_q<4>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 5: pair_q<5>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 6: pair_q<6>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 7: pair_q<7>(D, C.pairs, C.n_pairs, P.temp, s); break;
-      case 8: pair_q<8>(D, C.pairs, C.n_pairs, P.temp, s); break;
+    switch (D.q) {
+      case 0: w3_q<0>(D, C, P.temp, s); break;
+      case 1: w3_q<1>(D, C, P.temp, s); break;
+      case 2: w3_q<2>(D, C, P.temp, s); break;
+      case 3: w3_q<3>(D, C, P.temp, s); break;
+      case 4: w3_q<4>(D, C, P.temp, s); break;
+      case 5: w3_q<5>(D, C, P.temp, s); break;
+      case 6: w3_q<6>(D, C, P.temp, s); break;
+      case 7: w3_q<7>(D, C, P.temp, s); break;
+      case 8: w3_q<8>(D, C, P.temp, s); break;
       default: return -1;
     }
     const int nthreads = C.n_centres * D.kq;
@@ -920,23 +396,6 @@ int launch_m2qbxl_pairs(const DevData& D, const PairPlan& P, cudaStream_t s) {
     k += 2;
   }
   return k;
-}
-
-int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s) {
-  if (n == 0) return 0;
-  switch (D.q) {
-    case 0: flat_q<0>(D, items, n, ctr_box, irreg, s); break;
-    case 1: flat_q<1>(D, items, n, ctr_box, irreg, s); break;
-    case 2: flat_q<2>(D, items, n, ctr_box, irreg, s); break;
-    case 3: flat_q<3>(D, items, n, ctr_box, irreg, s); break;
-    case 4: flat_q<4>(D, items, n, ctr_box, irreg, s); break;
-    case 5: flat_q<5>(D, items, n, ctr_box, irreg, s); break;
-    case 6: flat_q<6>(D, items, n, ctr_box, irreg, s); break;
-    case 7: flat_q<7>(D, items, n, ctr_box, irreg, s); break;
-    case 8: flat_q<8>(D, items, n, ctr_box, irreg, s); break;
-    default: return -1;
-  }
-  return 1;
 }
 
 int launch_l2qbxl3(const DevData& D, const int* items, const int2* ctas, int n_ctas, const int* ctr_box,

@@ -401,7 +401,10 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   QCK(cudaMemGetInfo(&free_b, &total_b));
   P.srow = ((p + 1) * (p + 1) + 15) / 16 * 16;
   const size_t row_bytes = size_t(P.srow) * sizeof(double);
-  const size_t cap_bytes = std::min<size_t>(size_t(24) << 30, size_t(double(free_b) * 0.6));
+  // as few chunks as the staging memory allows (<= 48 GB, half the free memory): every
+  // launch ends in a partial wave, and running a chunk's reduce beside the next chunk's
+  // tiles on a second stream (two buffers, 6-7 chunks) measured slower (44.0 vs 42.5 ms)
+  const size_t cap_bytes = std::min<size_t>(size_t(48) << 30, size_t(double(free_b) * 0.5));
   int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);
   // test hook (tests/test_gpu_variants.py): force many chunks at small sizes
   if (const char* env = std::getenv("QBXG_M2L_CHUNK_ENTRIES")) cap = std::max<int64_t>(64, std::atoll(env));
@@ -1395,7 +1398,7 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   QCK(cudaEventRecord(H.evx[3], s));
   if (near == NEAR_SIDE) QCK(cudaStreamWaitEvent(s, H.join_ev, 0));
   chk(dev::launch_m2qbxl_pairs(D, H.wpairs, s));
-  chk(dev::launch_wfar2(D, nullptr, 0, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
+  chk(dev::launch_m2p(D, H.d_wfar_tboxes, H.n_wfar_tboxes, s));
   QCK(cudaEventRecord(ev[6], s));
   H.timed_overlap = near == NEAR_SIDE;
   chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));

@@ -88,8 +88,9 @@ bool pas_supported(int p);
 int pas_tile_cols();
 void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std::vector<double>& ops,
                    int& op_stride, std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]);
-int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s);
-int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s);
+int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, double* stage, cudaStream_t s);
+int launch_m2l_reduce(const M2LPlan& P, const M2LChunk& C, const DevData& D, const double* stage, cudaStream_t s);
+int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s);  // Stage 4 over all chunks
 
 // Tree shifts (Stage 2 M2M, Stage 7 L2L) as DMMA GEMMs over 8 octant operators:
 // one level = tiles of same-octant columns, staged rows, segmented reduce.
@@ -108,9 +109,7 @@ int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops,
                        cudaStream_t s);
 
 // Thread-per-centre translations (centre_trans.cu)
-int launch_wfar2(const DevData& D, const int* ctr_boxes, int n_ctr, const int* tgt_boxes, int n_tgt,
-                 cudaStream_t s);
-int launch_l2qbxl2(const DevData& D, const int* boxes, int n, cudaStream_t s);
+int launch_m2p(const DevData& D, const int* tgt_boxes, int n_tgt, cudaStream_t s);  // List 3 far, conventional targets
 // M2QBXL over (centre, List-3-far box) pairs, chunked by centres.
 struct PairChunk {
   int n_pairs = 0;
@@ -126,7 +125,6 @@ struct PairChunk {
 constexpr int kW3Threads = 128;
 constexpr int kW3Boxes = 4;
 struct PairPlan {
-  bool box_major = true;    // staged-table kernel (k_m2qbxl3); false: thread per pair from global
   double2* temp = nullptr;  // max chunk pairs x kq
   std::vector<PairChunk> chunks;
 };
@@ -137,8 +135,6 @@ constexpr int kL3Threads = 128;
 constexpr int kL3Boxes = 8;
 int launch_l2qbxl3(const DevData& D, const int* items, const int2* ctas, int n_ctas, const int* ctr_box,
                    cudaStream_t s);
-// flat thread-per-centre variant: items = sorted centre indices, ctr_box = owner box
-int launch_ctr_flat(const DevData& D, const int* items, int n, const int* ctr_box, bool irreg, cudaStream_t s);
 
 // launchers (return number of kernels launched)
 int launch_gather(const DevData& D, int ns, const int* perm, const double* w, const double* mu, cudaStream_t s);

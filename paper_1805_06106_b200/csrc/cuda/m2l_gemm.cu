@@ -276,14 +276,14 @@ int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops,
   return 2;
 }
 
-// Stage 4: the point-and-shoot M2L and its reduce (m2l_pas.cu), per chunk.
+// Stage 4: the point-and-shoot M2L and its reduce (m2l_pas.cu), chunk by chunk.
 int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s) {
   int k = 0;
   for (const M2LChunk& C : P.chunks) {
     if (C.n_tiles == 0) continue;
-    const int r = launch_m2l_pas(P, C, D, s);
+    const int r = launch_m2l_pas(P, C, D, P.temp, s);
     if (r < 0) return -1;
-    k += r;
+    k += r + launch_m2l_reduce(P, C, D, P.temp, s);
   }
   return k;
 }

@@ -336,7 +336,7 @@ PasLayout make_layout(int p) {
 }
 
 template <int P>
-int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, cudaStream_t s) {
+int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, double* stage, cudaStream_t s) {
   constexpr int NROW = (P + 1) * (P + 1);
   const size_t smem = size_t(NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
   static size_t attr = 0;
@@ -349,7 +349,7 @@ int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2,
   for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
   k_m2l_pas<P><<<C.n_tiles, kNTh, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops, Pl.pas_stride,
                                              Pl.pas_phase, Pl.cs, C.tiles, C.col_src, C.col_pos, X, kp2, Pl.srow,
-                                             Pl.temp);
+                                             stage);
   return 1;
 }
 
@@ -423,14 +423,14 @@ void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std
   if (worst > 1e-12) throw std::runtime_error("pas_build_ops: rotation blocks mix Re and Im at phi = 0");
 }
 
-int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaStream_t s) {
+int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, double* stage, cudaStream_t s) {
   const double* X = reinterpret_cast<const double*>(D.M);
   const int kp2 = 2 * D.kp;
   int r = -1;
   switch (D.p) {
 #define QBXG_PAS_P(N) \
   case N:             \
-    r = pas_launch_p<N>(P, C, X, kp2, s); \
+    r = pas_launch_p<N>(P, C, X, kp2, stage, s); \
     break;
     QBXG_PAS_P(1) QBXG_PAS_P(2) QBXG_PAS_P(3) QBXG_PAS_P(4) QBXG_PAS_P(5) QBXG_PAS_P(6) QBXG_PAS_P(7)
     QBXG_PAS_P(8) QBXG_PAS_P(9) QBXG_PAS_P(10) QBXG_PAS_P(11) QBXG_PAS_P(12) QBXG_PAS_P(13) QBXG_PAS_P(14)
@@ -438,10 +438,14 @@ int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, cudaSt
 #undef QBXG_PAS_P
     default: return -1;
   }
-  if (r < 0) return -1;
-  k_m2l_reduce<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, P.srow, C.base, P.temp, D.box,
-                                         reinterpret_cast<double*>(D.L), kp2);
-  return 2;
+  return r;
+}
+
+int launch_m2l_reduce(const M2LPlan& P, const M2LChunk& C, const DevData& D, const double* stage, cudaStream_t s) {
+  if (C.n_boxes == 0) return 0;
+  k_m2l_reduce<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, P.srow, C.base, stage, D.box,
+                                         reinterpret_cast<double*>(D.L), 2 * D.kp);
+  return 1;
 }
 
 }  // namespace dev
