@@ -9,12 +9,14 @@ t_f=0.9.  Metric: (N_S + N_T) / t_apply.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Default (no torchrun): N=1.  Under torchrun each rank drives one GPU and owns a
-contiguous Morton (DFS-preorder) range of boxes; multipoles are exchanged by
-NCCL broadcasts inside the apply and the potentials are summed across ranks, so
-N>1 is strong scaling of config 1.  --impl reference times the CPU
-restatement of the path (oracle/, the reference ships no FMM code to run) on a
-bounded sample of the same workload with all host threads.
+Default (no torchrun): N=1, config 1, plus side measurements (config 4 on one GPU as the
+scaling base, config 3 Helmholtz with per-stage fractions, config 2 association).  Under
+torchrun each rank drives one GPU and owns a contiguous Morton (DFS-preorder) range of
+boxes of BASELINE config 4 (64 urchins, strong scaling; --weak: 8 urchins per GPU);
+multipoles are exchanged by NCCL broadcasts inside the apply, the near field overlaps
+the exchange, and the owned results are gathered.  --impl reference
+times the CPU restatement of the path (oracle/; the reference ships no FMM code to run)
+on the same workload with all host threads.
 """
 from __future__ import annotations
 
@@ -87,6 +89,29 @@ def stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
     f["eval"] = n_assoc * (10 * kq + 30) + n_conv * (10 * kp + 30)
     b["eval"] = n_assoc * (16 * kq + 24 + 4 + 8) + n_conv * (32 + 8)
     return f, b
+
+
+def helm_stage_work(led, cfg, n_src, n_ctr, n_assoc, n_conv):
+    """Algorithmic fp64 flops per stage of the Helmholtz (complex128) apply, real flops
+    with a complex multiply-add = 8: full tables K_x = (x+1)^2; a (source, box or centre)
+    pair forms K wave-function values (6 flops each from the solid-harmonic and radial
+    recurrences) and K complex multiply-adds; a translation is the dense complex K x K'
+    matrix-vector product the centre and tree shifts define; M2L is the point-and-shoot
+    factorisation (8 x 6,181 real multiply-adds per List-2 entry at p = 20)."""
+    p, q = cfg.p_fmm, cfg.p_qbx
+    kp, kq = (p + 1) ** 2, (q + 1) ** 2
+    pas = 2 * 8 * 6181 * ((p + 1) / 21.0) ** 3  # per List-2 entry; exact at p = 20 (config 3)
+    f = {}
+    f["p2m"] = led["n_p2m_sources"] * (14 * kp)
+    f["m2m"] = led["n_m2m"] * 8 * kp * kp
+    f["near"] = led["pairs_qbx_near"] * (14 * kq) + led["pairs_p2p_near"] * 40
+    f["m2l"] = int(led["entries"]["V"] * pas)
+    f["p2l"] = led["pairs_xfar_source"] * (14 * kp)
+    f["l2l"] = led["n_l2l"] * 8 * kp * kp
+    f["wfar"] = led["pairs_wfar_centre"] * 8 * kp * kq + led["pairs_wfar_target"] * 14 * kp
+    f["l2qbxl"] = n_ctr * 8 * kp * kq
+    f["eval"] = n_assoc * 14 * kq + n_conv * 14 * kp
+    return f
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -478,19 +503,35 @@ def run_ours(args, rank, world, local_rank):
         cfg3 = api.config_fmm(3)
         rng3 = np.random.default_rng(7)
         w3 = g3.quad_weight * (rng3.uniform(-1, 1, g3.n_sources) + 1j * rng3.uniform(-1, 1, g3.n_sources))
-        eng3 = api.FmmEngine(cfg3, g3, api.Plan(cfg3, g3))
+        plan3 = api.Plan(cfg3, g3)
+        eng3 = api.FmmEngine(cfg3, g3, plan3)
         eng3.apply_complex(w3)
-        hms = []
+        hms, hst = [], {}
         for _ in range(2):
             eng3.apply_complex(w3)
             tm3, _, _, _ = eng3.last_timings()
             hms.append(tm3["total"])
+            for k, v in tm3.items():
+                hst[k] = hst.get(k, 0.0) + v / 2
         eng3.close()
         hms = float(np.mean(hms))
+        n3a = int((g3.association >= 0).sum())
+        hf = helm_stage_work(plan3.ledger(), cfg3, g3.n_sources, g3.n_centers, n3a, g3.n_targets - n3a)
+        hstages = {}
+        for k, fl in hf.items():
+            t = hst.get(k, 0.0) * 1e-3
+            if t <= 0:
+                continue
+            tensor = k == "m2l"  # point-and-shoot blocks on DMMA; the rest on the FP64 pipe
+            pk = peak_dmma if tensor else peak
+            hstages[k] = {"ms": round(hst[k], 3), "tflops": round(fl / t / 1e12, 3),
+                          "frac_fp64": round(fl / t / 1e12 / pk, 4), "pipe": "dmma" if tensor else "dfma",
+                          "flops": fl}
         helm = {"workload": "BASELINE config 3: unit-sphere icosphere L=6, 1,310,720 sources, 2,621,440 centres "
                             "and targets, Helmholtz SL k=3, complex density, p_fmm=20, p_qbx=5",
                 "ms_per_apply": round(hms, 2), "value": (g3.n_sources + g3.n_targets) / (hms * 1e-3),
-                "unit": "points/s", "dtype": "c128",
+                "unit": "points/s", "dtype": "c128", "stages": hstages,
+                "work_model": "bench.helm_stage_work: real flops, complex multiply-add = 8",
                 "parity": "GPU vs complex128 oracle <= 1e-11 (tests/test_helmholtz.py); no reference exists"}
 
     # target association (Algorithm 3) on BASELINE config 2: 655,360

@@ -222,9 +222,9 @@ struct Handle {
 
 namespace {
 
-// Group List-2 entries by relative offset for the dense per-offset M2L GEMM
-// (m2l_gemm.cu): operator tables, chunks bounded by the staging buffer, tiles
-// of <= 64 same-offset columns.
+// Tree-shift levels (M2M / L2L DMMA GEMMs, m2l_gemm.cu) and the Stage 4 M2L work:
+// point-and-shoot operators per offset class and target groups with their tiles
+// (m2l_pas.cu).
 void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& vstarts,
                const std::vector<int2>& vent, cudaStream_t s) {
   auto& O = H.owned;
@@ -355,22 +355,30 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     return;
   }
   if (!dev::pas_supported(p)) throw InvalidArgument("qbxg_create: the M2L supports 1 <= p_fmm <= 21");
-  // --- Stage 4 operators: one [W | Z | V] set per class (rho_xy^2, dz); per offset only
+  // --- Stage 4 operators: one [W | Z | V] set per class (rho_xy^2, dz), classes
+  // numbered in key order (independent of which offsets a rank uses); per offset only
   // the azimuth alpha = atan2(dy, dx) remains, as the (cos k alpha, sin k alpha) table
   P.n_offsets = int(used.size());
   std::vector<int> cls_of_op(P.n_offsets), cls_rxy2, cls_dz;
   std::vector<double2> cs(size_t(P.n_offsets) * (p + 1));
   {
+    auto key_of = [&](int sl) {
+      const int dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
+      return (dx * dx + dy * dy) * 11 + dz + 5;
+    };
     std::vector<int> key_to_cls(51 * 11, -1);
-    for (int o = 0; o < P.n_offsets; ++o) {
-      const int sl = used[o], dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
-      const int key = (dx * dx + dy * dy) * 11 + dz + 5;
-      if (key_to_cls[key] < 0) {
-        key_to_cls[key] = int(cls_rxy2.size());
-        cls_rxy2.push_back(dx * dx + dy * dy);
-        cls_dz.push_back(dz);
+    for (int o = 0; o < P.n_offsets; ++o) key_to_cls[key_of(used[o])] = 0;
+    for (int k = 0; k < 51 * 11; ++k)
+      if (key_to_cls[k] == 0) {
+        key_to_cls[k] = int(cls_rxy2.size());
+        cls_rxy2.push_back(k / 11);
+        cls_dz.push_back(k % 11 - 5);
+      } else {
+        key_to_cls[k] = -1;
       }
-      cls_of_op[o] = key_to_cls[key];
+    for (int o = 0; o < P.n_offsets; ++o) {
+      const int sl = used[o], dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5;
+      cls_of_op[o] = key_to_cls[key_of(sl)];
       const double alpha = (dx == 0 && dy == 0) ? 0.0 : std::atan2(double(dy), double(dx));
       for (int k = 0; k <= p; ++k) cs[size_t(o) * (p + 1) + k] = make_double2(std::cos(k * alpha), std::sin(k * alpha));
     }
@@ -387,77 +395,68 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     P.pas_tab_n = int(tab.size());
     QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
   }
-  {
-    std::vector<int> eo(nent);
-    for (int64_t e = 0; e < nent; ++e) eo[e] = slot_to_op[slot[e]];
-    P.ent_op = dupload(O, eo, s);
-    QCK(cudaStreamSynchronize(s));
-  }
 
-  // --- work order: chunks of whole target boxes bounded by the staging capacity; in a
-  // chunk, entries counting-sorted by offset (CSR order inside an offset); tiles of
-  // <= 32 same-offset columns
-  size_t free_b = 0, total_b = 0;
-  QCK(cudaMemGetInfo(&free_b, &total_b));
-  P.srow = ((p + 1) * (p + 1) + 15) / 16 * 16;
-  const size_t row_bytes = size_t(P.srow) * sizeof(double);
-  // as few chunks as the staging memory allows (<= 48 GB, half the free memory): every
-  // launch ends in a partial wave, and running a chunk's reduce beside the next chunk's
-  // tiles on a second stream (two buffers, 6-7 chunks) measured slower (44.0 vs 42.5 ms)
-  const size_t cap_bytes = std::min<size_t>(size_t(48) << 30, size_t(double(free_b) * 0.5));
-  int64_t cap = std::max<int64_t>(int64_t(cap_bytes / row_bytes), 4096);
-  // test hook (tests/test_gpu_variants.py): force many chunks at small sizes
-  if (const char* env = std::getenv("QBXG_M2L_CHUNK_ENTRIES")) cap = std::max<int64_t>(64, std::atoll(env));
-  const int tw = dev::pas_tile_cols();
-  int64_t max_chunk = 0;
-  int b0 = 0;
-  while (b0 < nb) {
-    int b1 = b0;
-    while (b1 < nb && (vs[b1 + 1] - vs[b0] <= cap || b1 == b0)) ++b1;
-    const int64_t base = vs[b0], cnt = vs[b1] - vs[b0];
-    if (cnt > 0) {
-      dev::M2LChunk C;
-      C.base = base;
-      std::vector<int> boxes;
-      for (int b = b0; b < b1; ++b)
-        if (vs[b + 1] > vs[b]) boxes.push_back(b);
-      // entries counting-sorted by (source block, offset): a source block is a run of
-      // consecutive source boxes whose multipoles (~24 MB) stay in L2 while its tiles
-      // run, so the gather reads each multipole from HBM about once (offsets alone
-      // would cycle the whole 392 MB multipole array through L2 per offset)
-      const int64_t sbox = std::max<int64_t>(1, (int64_t(24) << 20) / (int64_t(16) * dev::hsize(p)));
-      const int64_t nkey = ((nb + sbox - 1) / sbox) * P.n_offsets;
-      auto key = [&](int64_t e) { return (vb[e] / sbox) * P.n_offsets + slot_to_op[slot[e]]; };
-      std::vector<int64_t> cnt_k(nkey + 1, 0);
-      for (int64_t e = base; e < base + cnt; ++e) cnt_k[key(e) + 1]++;
-      for (int64_t k = 0; k < nkey; ++k) cnt_k[k + 1] += cnt_k[k];
-      std::vector<int> col_src(cnt), col_pos(cnt);
-      std::vector<int64_t> fill(cnt_k.begin(), cnt_k.end() - 1);
-      for (int b = b0; b < b1; ++b)
-        for (int64_t e = vs[b]; e < vs[b + 1]; ++e) {
-          const int64_t i = fill[key(e)]++;
-          col_src[i] = vb[e];
-          col_pos[i] = int(e - base);
-        }
-      std::vector<int4> tiles;
-      for (int64_t k = 0; k < nkey; ++k) {
-        const int o = int(k % P.n_offsets);
-        for (int64_t i = cnt_k[k]; i < cnt_k[k + 1]; i += tw)
-          tiles.push_back(make_int4(o, int(i), int(std::min<int64_t>(tw, cnt_k[k + 1] - i)), cls_of_op[o]));
-      }
-      C.n_tiles = int(tiles.size());
-      C.tiles = dupload(O, tiles, s);
-      C.col_src = dupload(O, col_src, s);
-      C.col_pos = dupload(O, col_pos, s);
-      C.n_boxes = int(boxes.size());
-      C.boxes = dupload(O, boxes, s);
-      QCK(cudaStreamSynchronize(s));
-      P.chunks.push_back(C);
-      max_chunk = std::max(max_chunk, cnt);
+  // --- work order: groups of G consecutive target boxes (DFS order); a group's entries
+  // sorted by (class, target slot, offset) and cut into tiles of <= BN same-class
+  // columns.  Groups launch heaviest first.
+  const int G = dev::pas_group_size(p), BN = dev::pas_tile_cols(p);
+  std::vector<int> tb;
+  for (int b = 0; b < nb; ++b)
+    if (vs[b + 1] > vs[b]) tb.push_back(b);
+  const int ng = int((tb.size() + G - 1) / G);
+  std::vector<int> col_src(nent), col_meta(nent), grp_box(size_t(ng) * G, -1);
+  std::vector<std::vector<int4>> gtiles(ng);
+  std::vector<int64_t> gwork(ng, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int g = 0; g < ng; ++g) {
+    const int i0 = g * G, i1 = std::min<int>(int(tb.size()), i0 + G);
+    const int64_t e0 = vs[tb[i0]], e1 = vs[tb[i1 - 1] + 1];
+    std::vector<uint64_t> key;
+    key.reserve(size_t(e1 - e0));
+    for (int i = i0; i < i1; ++i) {
+      grp_box[size_t(g) * G + (i - i0)] = tb[i];
+      for (int64_t e = vs[tb[i]]; e < vs[tb[i] + 1]; ++e)
+        key.push_back(uint64_t(cls_of_op[slot_to_op[slot[e]]]) << 44 | uint64_t(i - i0) << 36 |
+                      uint64_t(slot[e]) << 24 | uint64_t(e - e0));
     }
-    b0 = b1;
+    std::sort(key.begin(), key.end());
+    auto& T = gtiles[g];
+    int64_t work = 0;
+    for (size_t k = 0; k < key.size();) {
+      const int cls = int(key[k] >> 44);
+      size_t k1 = k;
+      while (k1 < key.size() && int(key[k1] >> 44) == cls && k1 - k < size_t(BN)) ++k1;
+      T.push_back(make_int4(cls, int(k), int(k1 - k), 0));
+      work += 64 + int64_t((k1 - k + 7) / 8) * 256;
+      k = k1;
+    }
+    for (size_t k = 0; k < key.size(); ++k) {
+      const int64_t e = e0 + int64_t(key[k] & 0xFFFFFF);
+      col_src[e0 + int64_t(k)] = vb[e];
+      col_meta[e0 + int64_t(k)] = int((key[k] >> 36) & 255) | slot_to_op[slot[e]] << 8;
+    }
+    gwork[g] = work;
   }
-  P.temp = dalloc<double>(O, std::max(size_t(max_chunk) * P.srow, size_t(max_level_rows) * P.KRp));
+  std::vector<int4> tiles;
+  std::vector<int> grp_tiles{0};
+  for (int g = 0; g < ng; ++g) {
+    const int64_t e0 = vs[tb[size_t(g) * G]];
+    for (int4 t : gtiles[g]) tiles.push_back(make_int4(t.x, int(e0 + t.y), t.z, 0));
+    grp_tiles.push_back(int(tiles.size()));
+  }
+  std::vector<int> order(ng);
+  for (int g = 0; g < ng; ++g) order[g] = g;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gwork[a] > gwork[b]; });
+  P.n_groups = ng;
+  P.group = G;
+  P.grp_order = dupload(O, order, s);
+  P.grp_tiles = dupload(O, grp_tiles, s);
+  P.grp_box = dupload(O, grp_box, s);
+  P.tiles = dupload(O, tiles, s);
+  P.col_src = dupload(O, col_src, s);
+  P.col_meta = dupload(O, col_meta, s);
+  QCK(cudaStreamSynchronize(s));
+  P.temp = dalloc<double>(O, size_t(max_level_rows) * P.KRp);
 }
 
 // ---- Helmholtz single layer: device data, operators and work lists --------

@@ -55,42 +55,38 @@ struct DevData {
   unsigned int* bad;       // set by Stage 9 when a potential / centre coefficient is non-finite
 };
 
-// Stage 4 M2L (m2l_pas.cu): point-and-shoot on real half-table blocks, tiles of
-// same-offset List-2 entries, one operator set per offset class (rho_xy^2, dz), staged
-// rows summed per box by k_m2l_reduce.  Work is split into chunks of whole target
-// boxes (contiguous in List-2 CSR order) so the staging buffer stays bounded.
-struct M2LChunk {
-  int n_tiles = 0;
-  int4* tiles = nullptr;       // (offset, first column, column count, class)
-  int* col_src = nullptr;      // source box of each column (offset-sorted)
-  int* col_pos = nullptr;      // List-2 CSR position (relative to base) of each column
-  int n_boxes = 0;
-  int* boxes = nullptr;        // target boxes of the chunk
-  int64_t base = 0;            // first CSR position of the chunk
-};
+// Stage 4 M2L (m2l_pas.cu): point-and-shoot on real half-table blocks, one operator
+// set per offset class (rho_xy^2, dz).  Target-grouped: one CTA owns a group of G
+// target boxes and accumulates their List-2 contributions on chip; its work is a
+// list of tiles, each <= pas_tile_cols() entries of one class (columns sorted by
+// (target slot, offset)), so every box local is written once, in a fixed order.
 constexpr int kMaxPasOrder = 21;
 struct M2LPlan {
   int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64 (tree-shift GEMMs)
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
-  double* temp = nullptr;      // staging: tree-shift rows (KRp), and the M2L's rows (srow doubles each)
-  int srow = 0;                // M2L staging row length: (p+1)^2 rounded up to 16 doubles
-  std::vector<M2LChunk> chunks;
+  double* temp = nullptr;      // staging rows of the tree shifts (KRp doubles each)
   int n_offsets = 0, n_classes = 0;
   double2* cs = nullptr;       // n_offsets x (p+1): (cos k alpha, sin k alpha)
-  int* ent_op = nullptr;       // offset id of every List-2 CSR entry
-  double* pas_ops = nullptr;   // n_classes x pas_stride: [W | Z | V]
+  double* pas_ops = nullptr;   // n_classes x pas_stride: [W | Z | V], blocks in DMMA fragment order
   int pas_stride = 0, pas_phase = 0, pas_nblk = 0;
   int* pas_tab = nullptr;      // block row sets and per-warp block lists of the three phases
   int pas_tab_n = 0;
   int pas_base[3] = {0, 0, 0};
+  // target groups
+  int n_groups = 0, group = 0; // groups, target boxes per group (G)
+  int* grp_order = nullptr;    // launch order (heaviest first)
+  int* grp_tiles = nullptr;    // n_groups + 1 tile offsets
+  int* grp_box = nullptr;      // n_groups x G target boxes (-1: none)
+  int4* tiles = nullptr;       // (class, first column, columns, 0)
+  int* col_src = nullptr;      // source box of each column
+  int* col_meta = nullptr;     // target slot | offset id << 8
 };
 bool pas_supported(int p);
-int pas_tile_cols();
+int pas_tile_cols(int p);
+int pas_group_size(int p);
 void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std::vector<double>& ops,
                    int& op_stride, std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]);
-int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, double* stage, cudaStream_t s);
-int launch_m2l_reduce(const M2LPlan& P, const M2LChunk& C, const DevData& D, const double* stage, cudaStream_t s);
-int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s);  // Stage 4 over all chunks
+int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s);  // Stage 4
 
 // Tree shifts (Stage 2 M2M, Stage 7 L2L) as DMMA GEMMs over 8 octant operators:
 // one level = tiles of same-octant columns, staged rows, segmented reduce.

@@ -1,6 +1,6 @@
 // Tree shifts (Stage 2 M2M, Stage 7 L2L) as dense
-// contractions on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64), and the Stage 4
-// launcher (the fused point-and-shoot M2L lives in m2l_pas.cu).
+// contractions on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64).  (The Stage 4
+// M2L lives in m2l_pas.cu.)
 //
 // For real densities M_j^{-k} = (-1)^k conj(M_j^k) and M_j^0, L_n^0 are real, so a
 // shift acts on (p+1)^2 real degrees of freedom ("real DOF": per degree n, Re X_n^0,
@@ -274,18 +274,6 @@ int launch_shift_level(const M2LPlan& P, const ShiftLevel& S, const double* ops,
   k_seg_reduce<<<S.n_out, 256, 0, s>>>(S.out_boxes, S.out_seg, P.KR, P.KRp, P.rmap, P.temp, Xd, 2 * kp,
                                         accumulate ? 1 : 0);
   return 2;
-}
-
-// Stage 4: the point-and-shoot M2L and its reduce (m2l_pas.cu), chunk by chunk.
-int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s) {
-  int k = 0;
-  for (const M2LChunk& C : P.chunks) {
-    if (C.n_tiles == 0) continue;
-    const int r = launch_m2l_pas(P, C, D, P.temp, s);
-    if (r < 0) return -1;
-    k += r + launch_m2l_reduce(P, C, D, P.temp, s);
-  }
-  return k;
 }
 
 }  // namespace dev

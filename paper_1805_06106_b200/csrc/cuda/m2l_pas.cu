@@ -1,5 +1,6 @@
 // Stage 4 M2L (List 2) as point-and-shoot translations on real
-// half-table blocks.
+// half-table blocks, accumulated per target box
+// on chip.
 //
 // Operator.  With box-scaled coefficients the translation depends only on the offset
 // delta = (c_b - c_d) / (2|b|) in [-5,5]^3.  Rotating the frame about z by
@@ -12,24 +13,26 @@
 //   V (local rotation back):                    per degree n, like W
 // 3 x 2,736 multiply-adds per List-2 entry at p = 15 instead of 32,896 for the two dense
 // azimuthal blocks.  W, Z and V depend on (rho_xy^2, dz) only: the 1,206 offsets of
-// [-5,5]^3 fall into 190 classes, so one operator set per class (~19 MB at p = 15).
+// [-5,5]^3 fall into 190 classes, one operator set per class (~19 MB at p = 15).
 //
-// Kernel: one CTA = one offset x <= 32 List-2 entries (3 CTAs per SM).  The gathered,
-// alpha-rotated multipoles sit in shared memory as (p+1)^2 rows (Re in half-table order,
-// Im in compacted order) x 32 columns.  In each phase every warp owns a fixed list of
-// whole blocks (longest processing time balanced on the host), so the phase runs in
-// place: the warp reads a block's operator (A fragments, from L2) and its rows (B
-// fragments, from shared memory) into registers, runs the m8n8k4 DMMAs, then writes its
-// rows.  Each entry's output row (still in the offset's frame) goes to a staging row at
-// its List-2 CSR position; k_m2l_reduce then rotates each row back by alpha and sums a
-// box's rows in CSR order (fixed order: bitwise reproducible), x 1/|b|.
-//
-// Measured and not kept (profiles/r02_summary.md): fusing the reduction into this kernel
-// (target-superblock tile order, per-entry alpha, last-arriving CTA reduces from L2):
-// 50-55 ms vs 43 at config 1 -- the kernel is latency-bound, and the per-entry rotations
-// and the 1.17x tiles cost more than the 37 GB staging round trip they save; a fully
-// unrolled compile-time block schedule per warp: 30% fewer instructions but 49 ms, half
-// the warp stalls on instruction fetch (the per-warp code no longer fits the I-cache).
+// Work split (target-grouped).  One CTA owns a group of G target boxes (32 at p <= 15,
+// consecutive in DFS order) and walks a host-built list of tiles: a tile is <= BN
+// List-2 entries of the group that share an operator class, columns sorted by
+// (target slot, offset).  Per tile:
+//   1. the BN source multipoles arrive in shared memory by TMA bulk copies
+//      (cp.async.bulk, one per multipole, issued one tile ahead on an mbarrier);
+//   2. all threads rotate them by e^{i k alpha} into the (p+1)^2 x BN real tile X;
+//   3. the three phases W, Z, V run in place on X as m8n8k4 DMMAs, each warp owning
+//      a fixed, longest-processing-time balanced list of whole blocks; the phase's
+//      operator blocks (stored in DMMA fragment order) are TMA-loaded into one of two
+//      shared slots one phase ahead, so A fragments are conflict-free shared loads;
+//   4. each column is rotated back by e^{-i m alpha} and added to its target's
+//      accumulators, which live in registers (LPT = 256 / G threads per target,
+//      thread j owning coefficients q = j, j + LPT, ...).
+// At the end every target's local gets L += acc / |b|, once.  A target's entries are
+// summed in (class, offset) order whatever the group composition: the result is
+// bitwise reproducible run to run and identical between sharded and
+// single-GPU applies, and no staging rows leave the SM.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -47,13 +50,95 @@ namespace dev {
 namespace {
 
 constexpr int kPasPhases = 3;
-constexpr int kWarps = 8, kBN = 32, kLD = kBN + 1, kNTh = kWarps * 32;
+constexpr int kWarps = 16, kNTh = kWarps * 32;
+constexpr size_t kSmemMax = 232448 - 2048;  // 227 KB per CTA (sm_100) less static shared memory
 
-// table layout (ints), per phase: [nblk+1 row offsets][nblk op offsets]
-// [(p+1)^2 rows][kWarps+1 warp offsets][block ids]
+// per-phase operator size bound (doubles): blocks of sizes 1..p+1 (Re) and 1..p (Im),
+// rows padded to 8 and columns to 4 -- the same multiset for W, Z and V (merging
+// blocks, below, never makes a phase larger)
+__host__ __device__ constexpr int pad_blk(int s) { return (s + 7) / 8 * 8 * ((s + 3) / 4 * 4); }
+__host__ __device__ constexpr int phase_doubles(int p) {
+  int t = 0;
+  for (int s = 1; s <= p + 1; ++s) t += pad_blk(s);
+  for (int s = 1; s <= p; ++s) t += pad_blk(s);
+  return t;
+}
+// block table ints per phase (bound): [nblk][nblk+1 row offsets][nblk op offsets]
+// [(p+1)^2 rows][kWarps+1 warp offsets][nblk block ids]
+__host__ __device__ constexpr int tab_ints(int p) {
+  return kPasPhases * (1 + 3 * (2 * p + 1) + 1 + (p + 1) * (p + 1) + kWarps + 1);
+}
+constexpr int kMaxBlock = 22;  // largest (merged) block the kernel instantiates
+
+template <int P>
+struct Tg {
+  static constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), KP2 = 2 * NR;
+  static constexpr int PH = phase_doubles(P);     // operator slot size (doubles)
+  static constexpr int KA = (NR + 31) / 32;       // coefficients per lane in the accumulate
+  static constexpr int TPW = 32 / KA < 4 ? 32 / KA : 4;  // target boxes per warp
+  static constexpr int G = kWarps * TPW;          // target boxes per CTA
+  static constexpr int TW = 4 * KA;               // TMEM words (columns) per target per lane
+  // TMEM: warps w, w+4, w+8, w+12 share lane quadrant w % 4, each its own column range
+  static constexpr int TCOLS = (kWarps / 4) * TPW * TW;
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static_assert(TCOLS <= 512, "TMEM accumulators exceed 512 columns");
+  static constexpr size_t bytes(int bn, bool sops) {
+    return size_t(bn) * KP2 * 8                   // RAW: gathered multipoles (TMA)
+           + (sops ? size_t(2) * PH * 8 : 0)      // OPS: two phase slots (TMA)
+           + size_t(NROW + 1) * bn * 8            // X (+ a zero row), swizzled
+           + size_t(2) * bn * (P + 1) * 16        // (cos, sin) per column, two tiles
+           + size_t(6) * bn * 4                   // column meta, three tiles
+           + size_t(tab_ints(P)) * 4;             // block table
+  }
+  static constexpr int BN = bytes(32, false) <= kSmemMax ? 32 : 16;  // tile columns
+  static constexpr bool SOPS = bytes(BN, true) <= kSmemMax;          // operators staged by TMA
+  static constexpr size_t SMEM = bytes(BN, SOPS);
+};
+
+// X element (row r, column c) lives at r * BN + (c ^ swz(r)): the B-fragment loads
+// (4 consecutive rows x 8 columns), the accumulate's reads (32 consecutive rows, one
+// column) and the fragment stores all spread over the banks.
+__device__ __forceinline__ int swz(int r) { return ((r & 1) << 3) | ((r >> 1) & 7); }
+
 struct TabHead {
   int base[kPasPhases];
 };
+
+// ---- PTX helpers: mbarrier + TMA bulk copy (cp.async.bulk), DMMA, TMEM
+__device__ __forceinline__ unsigned sm_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = sm_addr(bar);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   sm_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sm_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sm_addr(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sm_addr(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -61,268 +146,412 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// One block of size S in place on the fp64 tensor pipe: the operator (rows padded to
-// 8, columns to 4, zeros) as A fragments from L2, the block's rows x the tile's first
-// 8*NT columns as B fragments from shared memory -- all read before any row is
-// written, so the warp may overwrite its own block.
-template <int S, int NT>
-__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* __restrict__ Ob, int lane) {
-  constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4, K4 = 4 * KS;
-  double a[MT][KS], b[KS][NT];
+// TMEM: 4K consecutive 32-bit columns of this lane <-> K (re, im) double pairs, one wait
+template <int K>
+__device__ __forceinline__ void tm_ld(unsigned ta, double* re, double* im) {
+  unsigned r[4 * K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[4 * k]), "=r"(r[4 * k + 1]), "=r"(r[4 * k + 2]), "=r"(r[4 * k + 3])
+                 : "r"(ta + 4 * k)
+                 : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    re[k] = __hiloint2double(int(r[4 * k + 1]), int(r[4 * k]));
+    im[k] = __hiloint2double(int(r[4 * k + 3]), int(r[4 * k + 2]));
+  }
+}
+// TMEM: 4 consecutive 32-bit columns of this lane <-> two doubles
+__device__ __forceinline__ void tm_ld4(unsigned ta, double& x, double& y) {
+  unsigned r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(ta)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  x = __hiloint2double(int(r1), int(r0));
+  y = __hiloint2double(int(r3), int(r2));
+}
+__device__ __forceinline__ void tm_st4(unsigned ta, double x, double y) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(ta),
+               "r"(__double2loint(x)), "r"(__double2hiint(x)), "r"(__double2loint(y)), "r"(__double2hiint(y))
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// One block of size S in place on the fp64 tensor pipe: the operator as A fragments
+// (fragment order: 32 consecutive doubles per (mt, ks), zero padded) held in registers,
+// then per 8-column tile j < nt the block's rows as B fragments from X (padding rows
+// k >= S read the zero row), the DMMAs, and the rows written back.  Tile j's reads
+// feed its DMMAs, which precede its writes; other tiles touch other columns.
+template <int S, int BN, int ZR>
+__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, int lane, int nt) {
+  constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4;
+  double a[MT][KS];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = __ldg(Ob + (mt * 8 + (lane >> 2)) * K4 + ks * 4 + (lane & 3));
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
+  int rb[KS], ro[MT];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
     const int k = ks * 4 + (lane & 3);
-    const int row = k < S ? rw[k] : 0;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[ks][nt] = k < S ? X[row * kLD + nt * 8 + (lane >> 2)] : 0.0;
+    const int r = k < S ? rw[k] : ZR;
+    rb[ks] = r * BN + ((lane >> 2) ^ swz(r));
   }
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-#pragma unroll
-  for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt][ks], b[ks][nt]);
-  __syncwarp();
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
-    const int r = mt * 8 + (lane >> 2);
-    if (r < S) {
-      const int row = rw[r];
+    const int i = mt * 8 + (lane >> 2);
+    const int r = i < S ? rw[i] : -1;
+    ro[mt] = r < 0 ? -1 : r * BN + (((lane & 3) * 2) ^ swz(r));
+  }
+#pragma unroll 1
+  for (int j = 0; j < nt; ++j) {
+    double b[KS];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        X[row * kLD + nt * 8 + (lane & 3) * 2] = acc[mt][nt][0];
-        X[row * kLD + nt * 8 + (lane & 3) * 2 + 1] = acc[mt][nt][1];
+    for (int ks = 0; ks < KS; ++ks) b[ks] = X[rb[ks] ^ (j * 8)];
+    double acc[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], a[mt][ks], b[ks]);
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+      if (ro[mt] >= 0) {
+        X[ro[mt] ^ (j * 8)] = acc[mt][0];
+        X[(ro[mt] ^ (j * 8)) ^ 1] = acc[mt][1];
       }
-    }
   }
 }
 
 template <int P>
-__global__ void __launch_bounds__(kNTh, P <= 15 ? 3 : (P <= 18 ? 2 : 1))
-    k_m2l_pas(const int* __restrict__ tab, int tab_n, TabHead hd, int nblk, const double* __restrict__ ops,
-              int op_stride, int phase_size, const double2* __restrict__ cs_all, const int4* __restrict__ tiles,
-              const int* __restrict__ col_src, const int* __restrict__ col_pos, const double* __restrict__ M, int kp2,
-              int row_stride, double* __restrict__ temp) {
-  constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1);
-  extern __shared__ double smem[];
-  double* X = smem;
-  int* s_tab = reinterpret_cast<int*>(X + NROW * kLD);
-  __shared__ int s_src[kBN];
-  __shared__ int s_pos[kBN];
-  __shared__ double2 s_cs[P + 1];
-  // half-table index q: Re row | Im row << 10 (0 for m = 0) | m << 20
-  __shared__ int s_code[NR];
-  const int4 tile = tiles[blockIdx.x];  // (offset, first column, columns, class)
-  const int ncol = tile.z;
-  const bool half = ncol <= kBN / 2;  // tiles of <= 16 columns run 2 of the 4 DMMA n-tiles
+__global__ void __launch_bounds__(kNTh, 1)
+    k_m2l_tg(const int* __restrict__ tab, int tab_n, TabHead hd, const double* __restrict__ ops, int op_stride,
+             int phase_size, const double2* __restrict__ cs_all, const int* __restrict__ grp_order,
+             const int* __restrict__ grp_tiles, const int* __restrict__ grp_box, const int4* __restrict__ tiles,
+             const int* __restrict__ col_src, const int* __restrict__ col_meta, const double2* __restrict__ M,
+             const double4* __restrict__ box, double* __restrict__ L) {
+  using C = Tg<P>;
+  constexpr int NR = C::NR, NROW = C::NROW, KP2 = C::KP2, BN = C::BN, PH = C::PH;
+  constexpr int KA = C::KA, TPW = C::TPW, TW = C::TW;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double2* RAW = reinterpret_cast<double2*>(smem);
+  double* OPS = reinterpret_cast<double*>(RAW + BN * NR);
+  double* X = OPS + (C::SOPS ? 2 * PH : 0);
+  double2* s_cs = reinterpret_cast<double2*>(X + (NROW + 1) * BN);  // [2][BN][P+1]
+  int* s_meta = reinterpret_cast<int*>(s_cs + 2 * BN * (P + 1));   // [3][BN]: target slot | offset << 8
+  int* s_msrc = s_meta + 3 * BN;                                    // [3][BN]: source box
+  int* s_tab = s_msrc + 3 * BN;
+  __shared__ int s_code[NR];  // half-table q: Re row | Im row << 10 (zero row if m = 0) | m << 20
+  __shared__ uint64_t bar[3];  // RAW, OPS slot 0, OPS slot 1
+  __shared__ unsigned s_tmem;
+
+  const int g = grp_order[blockIdx.x];
+  const int t_begin = grp_tiles[g], t_end = grp_tiles[g + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {  // accumulators of the group's target boxes live in tensor memory
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sm_addr(&s_tmem)),
+                 "n"(C::TALLOC)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
   for (int i = tid; i < tab_n; i += kNTh) s_tab[i] = tab[i];
-  if (tid < kBN) s_src[tid] = tid < ncol ? col_src[tile.y + tid] : -1;
-  if (tid < kBN) s_pos[tid] = tid < ncol ? col_pos[tile.y + tid] : -1;
-  if (tid <= P) s_cs[tid] = cs_all[size_t(tile.x) * (P + 1) + tid];
   for (int q = tid; q < NR; q += kNTh) {
     int n = 0;
     while (hidx(n + 1, 0) <= q) ++n;
     const int m = q - hidx(n, 0);
-    s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : 0) << 10 | m << 20;
+    s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : NROW) << 10 | m << 20;
   }
-  __syncthreads();
-  // gather M' = M e^{i k alpha}, coalesced along each multipole, kSt loads in flight per
-  // thread; columns past the tile are zero
-  constexpr int kSt = 6;
-  const int nel = NR * (half ? kBN / 2 : kBN);
-  for (int e0 = 0; e0 < nel; e0 += kSt * kNTh) {
-    double2 v[kSt];
-#pragma unroll
-    for (int u = 0; u < kSt; ++u) {
-      const int e = e0 + tid + u * kNTh;
-      v[u] = make_double2(0.0, 0.0);
-      if (e < nel) {
-        const int c = e / NR, q = e - c * NR;
-        const int src = s_src[c];
-        if (src >= 0) v[u] = __ldg(reinterpret_cast<const double2*>(M + size_t(src) * kp2) + q);
-      }
+  for (int c = tid; c < BN; c += kNTh) X[NROW * BN + c] = 0.0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // Tile metadata runs ahead by cp.async: column (slot | offset, source) two tiles
+  // ahead (buffer it % 3), the columns' (cos, sin) rows one tile ahead (buffer it & 1),
+  // so no thread waits on a global load between barriers.
+  auto load_cols = [&](const int4 tl, int buf) {
+    for (int i = tid; i < tl.z; i += kNTh) {
+      cp_async4(s_meta + buf * BN + i, col_meta + tl.y + i);
+      cp_async4(s_msrc + buf * BN + i, col_src + tl.y + i);
     }
-#pragma unroll
-    for (int u = 0; u < kSt; ++u) {
-      const int e = e0 + tid + u * kNTh;
-      if (e < nel) {
-        const int c = e / NR, q = e - c * NR;
-        const int code = s_code[q], ri = (code >> 10) & 1023;
-        const double2 r = s_cs[(code >> 20) & 63];
-        X[(code & 1023) * kLD + c] = v[u].x * r.x - v[u].y * r.y;
-        if (ri) X[ri * kLD + c] = v[u].x * r.y + v[u].y * r.x;
-      }
+  };
+  auto load_cs = [&](int ncols, int mbuf, int cbuf) {
+    double2* sc = s_cs + cbuf * BN * (P + 1);
+    for (int i = tid; i < ncols * (P + 1); i += kNTh) {
+      const int c = i / (P + 1), m = i - c * (P + 1);
+      cp_async16(sc + i, cs_all + size_t(s_meta[mbuf * BN + c] >> 8) * (P + 1) + m);
+    }
+  };
+  // warp 0: a tile's multipoles into RAW, one bulk copy per column
+  auto issue_raw = [&](int ncols, int mbuf) {
+    if (lane == 0) mbar_expect_tx(&bar[0], unsigned(ncols) * KP2 * 8);
+    __syncwarp();
+    if (lane < ncols) tma_load(RAW + lane * NR, M + size_t(s_msrc[mbuf * BN + lane]) * NR, KP2 * 8, &bar[0]);
+  };
+  auto issue_ops = [&](int cls, int ph, int slot) {
+    mbar_expect_tx(&bar[1 + slot], phase_size * 8);
+    tma_load(OPS + slot * PH, ops + size_t(cls) * op_stride + size_t(ph) * phase_size, phase_size * 8,
+             &bar[1 + slot]);
+  };
+  int4 tl = make_int4(0, 0, 0, 0), tn = tl;
+  if (t_begin < t_end) {
+    tl = tiles[t_begin];
+    load_cols(tl, 0);
+    if (t_begin + 1 < t_end) {
+      tn = tiles[t_begin + 1];
+      load_cols(tn, 1);
     }
   }
+  cp_async_wait_all();
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  const double* opb = ops + size_t(tile.w) * op_stride;
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (t_begin < t_end) {
+    if (warp == 0) issue_raw(tl.z, 0);
+    if (C::SOPS && tid == 0) issue_ops(tl.x, 0, 0);
+    load_cs(tl.z, 0, 0);
+  }
+  // this warp's accumulators: lane quadrant warp % 4, columns of its TPW targets
+  const unsigned tm = s_tmem + (unsigned(32 * (warp & 3)) << 16) + unsigned((warp >> 2) * TPW * TW);
 #pragma unroll 1
-  for (int ph = 0; ph < kPasPhases; ++ph) {
-    const int* T = s_tab + hd.base[ph];
-    const int* rowoff = T;
-    const int* opoff = T + nblk + 1;
-    const int* rows = opoff + nblk;
-    const int* woff = rows + NROW;
-    const int* wblk = woff + kWarps + 1;
-    const double* Op = opb + size_t(ph) * phase_size;
-#define QBXG_PAS_CASES(NT)                                                                                     \
-  QBXG_PAS_CASE(1, NT) QBXG_PAS_CASE(2, NT) QBXG_PAS_CASE(3, NT) QBXG_PAS_CASE(4, NT) QBXG_PAS_CASE(5, NT)         \
-  QBXG_PAS_CASE(6, NT) QBXG_PAS_CASE(7, NT) QBXG_PAS_CASE(8, NT) QBXG_PAS_CASE(9, NT) QBXG_PAS_CASE(10, NT)        \
-  QBXG_PAS_CASE(11, NT) QBXG_PAS_CASE(12, NT) QBXG_PAS_CASE(13, NT) QBXG_PAS_CASE(14, NT) QBXG_PAS_CASE(15, NT)    \
-  QBXG_PAS_CASE(16, NT) QBXG_PAS_CASE(17, NT) QBXG_PAS_CASE(18, NT) QBXG_PAS_CASE(19, NT) QBXG_PAS_CASE(20, NT)    \
-  QBXG_PAS_CASE(21, NT) QBXG_PAS_CASE(22, NT)
-#define QBXG_PAS_CASE(S, NT) \
-  case S:                    \
-    if (S <= P + 1) pas_block<S, NT>(X, rw, Ob, lane); \
+  for (int w = 0; w < TPW * KA; ++w) tm_st4(tm + 4 * w, 0.0, 0.0);
+  tm_wait_st();
+  cp_async_wait_all();
+  __syncthreads();
+
+  int kph = 0;  // phases run so far (operator slot kph & 1)
+#pragma unroll 1
+  for (int t = t_begin, it = 0; t < t_end; ++t, ++it) {
+    const bool more = t + 1 < t_end;
+    const int4 tn2 = t + 2 < t_end ? tiles[t + 2] : make_int4(0, 0, 0, 0);
+    const int ncols = tl.z, nt = (ncols + 7) >> 3;
+    const int mb = it % 3, mb1 = (it + 1) % 3, mb2 = (it + 2) % 3, cb = it & 1;
+    const int* sm = s_meta + mb * BN;
+    const double2* sc = s_cs + cb * BN * (P + 1);
+    // 1-2. multipoles of tile t (TMA) rotated by e^{i k alpha} into X
+    mbar_wait(&bar[0], it & 1);
+    for (int e = tid; e < ncols * NR; e += kNTh) {
+      const int c = e / NR, q = e - c * NR;
+      const int code = s_code[q], m = code >> 20;
+      const double2 v = RAW[c * NR + q];
+      const double2 r = sc[c * (P + 1) + m];
+      const int re = code & 1023, im = (code >> 10) & 1023;
+      X[re * BN + (c ^ swz(re))] = v.x * r.x - v.y * r.y;
+      if (m) X[im * BN + (c ^ swz(im))] = v.x * r.y + v.y * r.x;
+    }
+    __syncthreads();
+    if (more) {  // RAW is free: the next tile's multipoles and metadata in flight
+      if (warp == 0) issue_raw(tn.z, mb1);
+      load_cs(tn.z, mb1, cb ^ 1);
+      if (t + 2 < t_end) load_cols(tn2, mb2);
+    }
+    // 3. W, Z, V in place
+#pragma unroll 1
+    for (int ph = 0; ph < kPasPhases; ++ph, ++kph) {
+      const double* Op;
+      if (C::SOPS) {
+        if (tid == 0) {  // the slot of phase kph - 1 is free: load phase kph + 1 into it
+          const bool last = ph == kPasPhases - 1;
+          if (!last || more) issue_ops(last ? tn.x : tl.x, last ? 0 : ph + 1, (kph + 1) & 1);
+        }
+        mbar_wait(&bar[1 + (kph & 1)], (kph >> 1) & 1);
+        Op = OPS + (kph & 1) * PH;
+      } else {
+        Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
+      }
+      const int* T = s_tab + hd.base[ph];
+      const int nblk = T[0];
+      const int* rowoff = T + 1;
+      const int* opoff = rowoff + nblk + 1;
+      const int* rows = opoff + nblk;
+      const int* woff = rows + NROW;
+      const int* wblk = woff + kWarps + 1;
+#define QBXG_PAS_CASE(S) \
+  case S:                \
+    if (S <= 2 * P + 2 && S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
     break;
 #pragma unroll 1
-    for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
-      const int b = wblk[i];
-      const int* rw = rows + rowoff[b];
-      const double* Ob = Op + opoff[b];
-      if (half) {
+      for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
+        const int b = wblk[i];
+        const int* rw = rows + rowoff[b];
+        const double* Ob = Op + opoff[b];
         switch (rowoff[b + 1] - rowoff[b]) {
-          QBXG_PAS_CASES(2)
-          default: break;
-        }
-      } else {
-        switch (rowoff[b + 1] - rowoff[b]) {
-          QBXG_PAS_CASES(4)
+          QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
+          QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11)
+          QBXG_PAS_CASE(12) QBXG_PAS_CASE(13) QBXG_PAS_CASE(14) QBXG_PAS_CASE(15) QBXG_PAS_CASE(16)
+          QBXG_PAS_CASE(17) QBXG_PAS_CASE(18) QBXG_PAS_CASE(19) QBXG_PAS_CASE(20) QBXG_PAS_CASE(21)
+          QBXG_PAS_CASE(22)
           default: break;
         }
       }
-    }
 #undef QBXG_PAS_CASE
-#undef QBXG_PAS_CASES
-    __syncthreads();
-  }
-  // staging row = Re (NR) then compacted Im, coalesced along each row (row-outer: one
-  // row per thread and column; consecutive lanes, consecutive rows); streaming stores,
-  // so the rows do not evict the multipoles and operators from L2
-  for (int r = tid; r < NROW; r += kNTh)
-    for (int c = 0; c < ncol; ++c) __stcs(temp + size_t(s_pos[c]) * row_stride + r, X[r * kLD + c]);
-}
-
-// Each staging row holds L' of one List-2 entry in its offset's rotated frame (Re rows
-// in half-table order, then compacted Im rows).  Rotate back (L = L' e^{-i m alpha}) and
-// sum a box's rows in CSR order; scale by 1/|b| once.
-__global__ void __launch_bounds__(160) k_m2l_reduce(const int* __restrict__ boxes, const int64_t* __restrict__ v_starts,
-                                                    const int* __restrict__ ent_op, const double2* __restrict__ cs,
-                                                    int p, int row_stride, int64_t chunk_base,
-                                                    const double* __restrict__ temp, const double4* __restrict__ box,
-                                                    double* __restrict__ L, int kp2) {
-  const int b = boxes[blockIdx.x];
-  const int64_t a = v_starts[b], e = v_starts[b + 1];
-  const int NR = hsize(p);
-  const double ih = 1.0 / box[b].w;
-  for (int q = threadIdx.x; q < NR; q += blockDim.x) {
-    int n = int((sqrt(8.0 * q + 1.0) - 1.0) * 0.5);
-    while (hidx(n + 1, 0) <= q) ++n;
-    while (hidx(n, 0) > q) --n;
-    const int m = q - hidx(n, 0);
-    double sx = 0.0, sy = 0.0;
-    const int qi = m > 0 ? NR + n * (n - 1) / 2 + m - 1 : q;
-    // kU entries' loads in flight per thread (the kernel is HBM-bound on the staging
-    // rows); the sums still run in CSR order
-    constexpr int kU = 4;
-    int64_t pos = a;
-    for (; pos + kU <= e; pos += kU) {
-      double re[kU], im[kU];
-      double2 r[kU];
+      __syncthreads();
+    }
+    // 4. rotate back by e^{-i m alpha} and add to the owning warp's accumulators (TMEM),
+    // in column order; a target's columns are consecutive, so its accumulators are read
+    // and written once per tile
+    {
+      const int mine = lane < ncols && ((sm[lane] & 255) % kWarps) == warp;
+      unsigned mask = __ballot_sync(0xffffffffu, mine);
+      while (mask) {
+        const int slot = sm[__ffs(mask) - 1] & 255, u = slot / kWarps;
+        double are[KA], aim[KA];
+        tm_ld<KA>(tm + u * TW, are, aim);
+        while (mask && (sm[__ffs(mask) - 1] & 255) == slot) {
+          const int c = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const double2* r = sc + c * (P + 1);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const double* row = temp + (pos + u - chunk_base) * row_stride;
-        re[u] = __ldcs(row + q);
-        im[u] = m > 0 ? __ldcs(row + qi) : 0.0;
-        r[u] = m > 0 ? cs[size_t(__ldg(ent_op + pos + u)) * (p + 1) + m] : make_double2(1.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (m == 0) {
-          sx += re[u];
-        } else {
-          sx += re[u] * r[u].x + im[u] * r[u].y;
-          sy += im[u] * r[u].x - re[u] * r[u].y;
+          for (int k = 0; k < KA; ++k) {
+            const int q = lane + 32 * k;
+            const int code = q < NR ? s_code[q] : (NROW | NROW << 10);
+            const int re = code & 1023, im = (code >> 10) & 1023;
+            const double xr = X[re * BN + (c ^ swz(re))], xi = X[im * BN + (c ^ swz(im))];
+            const double2 rr = r[code >> 20];
+            are[k] += xr * rr.x + xi * rr.y;
+            aim[k] += xi * rr.x - xr * rr.y;
+          }
         }
+#pragma unroll
+        for (int k = 0; k < KA; ++k) tm_st4(tm + (u * KA + k) * 4, are[k], aim[k]);
+        tm_wait_st();
       }
     }
-    for (; pos < e; ++pos) {
-      const double* row = temp + (pos - chunk_base) * row_stride;
-      const double re = __ldcs(row + q);
-      if (m == 0) {
-        sx += re;
-      } else {
-        const double im = __ldcs(row + qi);
-        const double2 r = cs[size_t(ent_op[pos]) * (p + 1) + m];
-        sx += re * r.x + im * r.y;
-        sy += im * r.x - re * r.y;
-      }
-    }
-    L[size_t(b) * kp2 + 2 * q] += sx * ih;
-    if (m > 0) L[size_t(b) * kp2 + 2 * q + 1] += sy * ih;
+    cp_async_wait_all();  // next tiles' metadata landed
+    __syncthreads();      // X and this tile's buffers free
+    tl = tn;
+    tn = tn2;
   }
+#pragma unroll 1
+  for (int u = 0; u < TPW; ++u) {
+    const int b = grp_box[size_t(g) * C::G + u * kWarps + warp];
+    if (b < 0) continue;
+    const double ih = 1.0 / box[b].w;
+    double* Lb = L + size_t(b) * KP2;
+    double xr[KA], xi[KA];
+    tm_ld<KA>(tm + u * TW, xr, xi);
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+      const int q = lane + 32 * k;
+      if (q < NR) {
+        Lb[2 * q] += xr[k] * ih;
+        if (s_code[q] >> 20) Lb[2 * q + 1] += xi[k] * ih;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem), "n"(C::TALLOC) : "memory");
 }
 
 // ---------------------------------------------------------------- host side
-struct PasLayout {
-  int nblk = 0, phase_size = 0;
-  std::vector<int> tab;
-  TabHead hd{};
+// sub-blocks of one phase as storage rows (Re rows hidx(n, m); Im rows
+// NR + n(n-1)/2 + m - 1): W, V per degree a (orders part..a), Z per order a
+// (degrees a..p), part 0 = Re, 1 = Im
+struct SubBlock {
+  int part, a;
+  std::vector<int> rows;
 };
-
-// blocks of one phase as storage rows (Re rows hidx(n, m); Im rows NR + n(n-1)/2 + m - 1)
-void phase_blocks(int p, int ph, std::vector<std::vector<int>>& blocks) {
+std::vector<SubBlock> phase_subblocks(int p, int ph) {
   const int NR = hsize(p);
   auto re = [&](int n, int m) { return hidx(n, m); };
   auto im = [&](int n, int m) { return NR + n * (n - 1) / 2 + m - 1; };
-  blocks.clear();
+  std::vector<SubBlock> out;
   for (int part = 0; part < 2; ++part)
     for (int a = part; a <= p; ++a) {
-      std::vector<int> b;
-      if (ph != 1)  // W, V: degree a, orders part..a
-        for (int m = part; m <= a; ++m) b.push_back(part ? im(a, m) : re(a, m));
-      else  // Z: order a, degrees a..p
-        for (int n = a; n <= p; ++n) b.push_back(part ? im(n, a) : re(n, a));
-      blocks.push_back(b);
+      SubBlock b{part, a, {}};
+      if (ph != 1)
+        for (int m = part; m <= a; ++m) b.rows.push_back(part ? im(a, m) : re(a, m));
+      else
+        for (int n = a; n <= p; ++n) b.rows.push_back(part ? im(n, a) : re(n, a));
+      out.push_back(b);
     }
+  return out;
 }
+
+// Merged blocks: sub-blocks placed block-diagonally in one operator when that costs no
+// more DMMA fragments than running them apart (the padding of a large block absorbs a
+// small one), so a phase is ~17 near-square blocks instead of 2p + 1 at p = 15.
+std::vector<std::vector<int>> merge_subblocks(const std::vector<SubBlock>& sb) {
+  std::vector<int> order(sb.size());
+  for (size_t i = 0; i < sb.size(); ++i) order[i] = int(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sb[a].rows.size() > sb[b].rows.size(); });
+  std::vector<char> used(sb.size(), 0);
+  std::vector<std::vector<int>> groups;
+  for (int i : order) {
+    if (used[i]) continue;
+    used[i] = 1;
+    std::vector<int> gr{i};
+    int s = int(sb[i].rows.size()), cost = pad_blk(s);
+    for (bool grew = true; grew;) {
+      grew = false;
+      for (int j : order) {  // largest sub-block that fits for free
+        if (used[j]) continue;
+        const int u = int(sb[j].rows.size());
+        if (s + u > kMaxBlock || pad_blk(s + u) > cost + pad_blk(u)) continue;
+        used[j] = 1;
+        gr.push_back(j);
+        s += u;
+        cost = pad_blk(s);
+        grew = true;
+        break;
+      }
+    }
+    groups.push_back(gr);
+  }
+  return groups;
+}
+
+struct PasLayout {
+  int phase_size = 0;
+  std::vector<int> tab;
+  TabHead hd{};
+  std::vector<std::vector<SubBlock>> sub;             // per phase
+  std::vector<std::vector<std::vector<int>>> groups;  // per phase: merged blocks
+  std::vector<std::vector<int>> opoff;                // per phase
+};
 
 PasLayout make_layout(int p) {
   PasLayout L;
+  L.sub.resize(kPasPhases);
+  L.groups.resize(kPasPhases);
+  L.opoff.resize(kPasPhases);
   for (int ph = 0; ph < kPasPhases; ++ph) {
-    std::vector<std::vector<int>> blocks;
-    phase_blocks(p, ph, blocks);
-    L.nblk = int(blocks.size());
+    L.sub[ph] = phase_subblocks(p, ph);
+    L.groups[ph] = merge_subblocks(L.sub[ph]);
+    const auto& G = L.groups[ph];
+    const int nblk = int(G.size());
     L.hd.base[ph] = int(L.tab.size());
-    std::vector<int> rowoff{0}, opoff, rows;
+    std::vector<int> rowoff{0}, rows, sizes;
     int oo = 0;
-    for (auto& b : blocks) {
-      const int s = int(b.size());
-      rows.insert(rows.end(), b.begin(), b.end());
+    for (const auto& gr : G) {
+      for (int i : gr) rows.insert(rows.end(), L.sub[ph][i].rows.begin(), L.sub[ph][i].rows.end());
       rowoff.push_back(int(rows.size()));
-      opoff.push_back(oo);
-      oo += (s + 7) / 8 * 8 * ((s + 3) / 4 * 4);  // rows padded to 8, columns to 4
+      sizes.push_back(rowoff.back() - rowoff[rowoff.size() - 2]);
+      L.opoff[ph].push_back(oo);
+      oo += pad_blk(sizes.back());
     }
-    L.phase_size = oo;  // the same for the three phases (same block sizes)
-    // whole blocks per warp, longest processing time first
-    std::vector<int> order(blocks.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return blocks[a].size() > blocks[b].size(); });
+    L.phase_size = std::max(L.phase_size, oo);
+    // whole blocks per warp, longest processing time first; a block costs its DMMA
+    // fragments plus a fixed latency share
+    std::vector<int> order(nblk);
+    for (int i = 0; i < nblk; ++i) order[i] = i;
+    auto cost = [&](int b) { return long(pad_blk(sizes[b])) + 96; };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
     std::vector<std::vector<int>> wl(kWarps);
     std::vector<long> load(kWarps, 0);
     for (int bi : order) {
       const int w = int(std::min_element(load.begin(), load.end()) - load.begin());
-      load[w] += long(blocks[bi].size() * blocks[bi].size());
+      load[w] += cost(bi);
       wl[w].push_back(bi);
     }
     std::vector<int> woff{0}, wblk;
@@ -330,47 +559,85 @@ PasLayout make_layout(int p) {
       wblk.insert(wblk.end(), v.begin(), v.end());
       woff.push_back(int(wblk.size()));
     }
-    for (auto* v : {&rowoff, &opoff, &rows, &woff, &wblk}) L.tab.insert(L.tab.end(), v->begin(), v->end());
+    L.tab.push_back(nblk);
+    for (auto* v : {&rowoff, &L.opoff[ph], &rows, &woff, &wblk}) L.tab.insert(L.tab.end(), v->begin(), v->end());
   }
+  if (int(L.tab.size()) > tab_ints(p) || L.phase_size > phase_doubles(p))
+    throw std::logic_error("m2l_pas: block table exceeds its bound");
   return L;
 }
 
 template <int P>
-int pas_launch_p(const M2LPlan& Pl, const M2LChunk& C, const double* X, int kp2, double* stage, cudaStream_t s) {
-  constexpr int NROW = (P + 1) * (P + 1);
-  const size_t smem = size_t(NROW * kLD) * sizeof(double) + size_t(Pl.pas_tab_n) * sizeof(int);
-  static size_t attr = 0;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(k_m2l_pas<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+int tg_launch(const M2LPlan& Pl, const DevData& D, cudaStream_t s) {
+  using C = Tg<P>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_m2l_tg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)) != cudaSuccess)
       return -1;
-    attr = smem;
+    attr = true;
   }
   TabHead hd;
   for (int k = 0; k < 3; ++k) hd.base[k] = Pl.pas_base[k];
-  k_m2l_pas<P><<<C.n_tiles, kNTh, smem, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_nblk, Pl.pas_ops, Pl.pas_stride,
-                                             Pl.pas_phase, Pl.cs, C.tiles, C.col_src, C.col_pos, X, kp2, Pl.srow,
-                                             stage);
+  k_m2l_tg<P><<<Pl.n_groups, kNTh, C::SMEM, s>>>(Pl.pas_tab, Pl.pas_tab_n, hd, Pl.pas_ops, Pl.pas_stride,
+                                                   Pl.pas_phase, Pl.cs, Pl.grp_order, Pl.grp_tiles, Pl.grp_box,
+                                                   Pl.tiles, Pl.col_src, Pl.col_meta,
+                                                   D.M, D.box,
+                                                   reinterpret_cast<double*>(D.L));
   return 1;
 }
+
+#define QBXG_PAS_ORDERS(X)                                                                                   \
+  X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18) X(19) \
+      X(20) X(21)
 
 }  // namespace
 
 bool pas_supported(int p) { return p >= 1 && p <= kMaxPasOrder; }
-int pas_tile_cols() { return kBN; }
 
-// Per-class operators [W | Z | V], blocks in phase_blocks order, each row-major with
-// rows padded to 8 and columns to 4 (zeros): DMMA A fragments without guards.  A
-// class is (rho_xy^2, dz); v' = (2 rho_xy, 0, 2 dz) is the same for all its offsets.
+int pas_tile_cols(int p) {
+  switch (p) {
+#define QBXG_TG_BN(N) \
+  case N:             \
+    return Tg<N>::BN;
+    QBXG_PAS_ORDERS(QBXG_TG_BN)
+#undef QBXG_TG_BN
+    default: return 0;
+  }
+}
+
+int pas_group_size(int p) {
+  switch (p) {
+#define QBXG_TG_G(N) \
+  case N:            \
+    return Tg<N>::G;
+    QBXG_PAS_ORDERS(QBXG_TG_G)
+#undef QBXG_TG_G
+    default: return 0;
+  }
+}
+
+// Per-class operators [W | Z | V], blocks in phase_blocks order, each stored in DMMA
+// A-fragment order: for every (row tile mt, k step ks) the 32 lanes' elements
+// A[8 mt + lane/4][4 ks + lane%4] are consecutive (rows padded to 8 and columns to 4
+// with zeros).  A class is (rho_xy^2, dz); v' = (2 rho_xy, 0, 2 dz) is the same for all
+// its offsets.
 void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std::vector<double>& ops,
                    int& op_stride, std::vector<int>& tab, int& nblk, int& phase_size, int (&base)[3]) {
   const PasLayout L = make_layout(p);
-  nblk = L.nblk;
+  nblk = int(L.groups[0].size());
   phase_size = L.phase_size;
   op_stride = kPasPhases * L.phase_size;
   tab = L.tab;
   for (int k = 0; k < 3; ++k) base[k] = L.hd.base[k];
   ops.assign(size_t(n_cls) * op_stride, 0.0);
   const size_t rs = rot_blocks_size(p);
+  // element (i, k) of a block with padded column count sp, in fragment order
+  auto frag = [](int i, int k, int sp) {
+    const int ks_n = sp / 4, mt = i / 8, ks = k / 4, lane = (i % 8) * 4 + k % 4;
+    return size_t(mt * ks_n + ks) * 32 + lane;
+  };
+  auto re = [](int m) { return m == 0 ? 0 : 2 * m - 1; };
+  auto im = [](int m) { return 2 * m; };
   double worst = 0.0;
 #pragma omp parallel for schedule(dynamic, 4) reduction(max : worst)
   for (int o = 0; o < n_cls; ++o) {
@@ -378,74 +645,61 @@ void pas_build_ops(int p, int n_cls, const int* cls_rxy2, const int* cls_dz, std
     const double rho = std::sqrt(v[0] * v[0] + v[2] * v[2]);
     std::vector<double> Rf(rs), Rb(rs);
     m2l_rotation_blocks(p, v, Rf.data(), Rb.data());
-    double* W = &ops[size_t(o) * op_stride];
-    double* Z = W + L.phase_size;
-    double* V = Z + L.phase_size;
-    auto re = [](int m) { return m == 0 ? 0 : 2 * m - 1; };
-    auto im = [](int m) { return 2 * m; };
-    size_t w = 0, z = 0;
-    for (int part = 0; part < 2; ++part)
-      for (int a = part; a <= p; ++a) {
-        // W, V: degree a (rows / columns = orders part..a); rows padded to 8, columns to 4
-        const int d = 2 * a + 1, s = a + 1 - part, sr = (s + 7) / 8 * 8, sp = (s + 3) / 4 * 4;
-        const double* F = &Rf[rot_block_offset(a)];
-        const double* B = &Rb[rot_block_offset(a)];
-        for (int i = 0; i < sr; ++i)
-          for (int k = 0; k < sp; ++k) {
-            const bool pad = i >= s || k >= s;
-            const int mi = part + (pad ? 0 : i), mk = part + (pad ? 0 : k);
-            const int ri = part ? im(mi) : re(mi), rk = part ? im(mk) : re(mk);
-            W[w + size_t(i) * sp + k] = pad ? 0.0 : F[ri * d + rk];
-            V[w + size_t(i) * sp + k] = pad ? 0.0 : B[ri * d + rk];
-          }
-        w += size_t(sr) * sp;
-        for (int i = 0; i <= a; ++i)  // Re/Im cross terms vanish at phi = 0
-          for (int k = 1; k <= a; ++k) {
-            worst = std::max(worst, std::fabs(F[re(i) * d + im(k)]) + std::fabs(F[im(k) * d + re(i)]));
-            worst = std::max(worst, std::fabs(B[re(i) * d + im(k)]) + std::fabs(B[im(k) * d + re(i)]));
-          }
-        // Z: order m = a, rows n / columns j in [m, p]: (-1)^{n+m} (j+n)! / rho^{j+n+1}
-        const int m = a, sz = p - m + 1, szr = (sz + 7) / 8 * 8, szp = (sz + 3) / 4 * 4;
-        for (int i = 0; i < szr; ++i)
-          for (int k = 0; k < szp; ++k) {
-            double val = 0.0;
-            if (i < sz && k < sz) {
-              const int n = m + i, j = m + k;
-              double f = 1.0;
-              for (int t = 2; t <= j + n; ++t) f *= t;
-              val = (((n + m) & 1) ? -1.0 : 1.0) * f / std::pow(rho, j + n + 1);
+    for (int a = 0; a <= p; ++a) {  // Re/Im cross terms vanish at phi = 0
+      const int d = 2 * a + 1;
+      const double* F = &Rf[rot_block_offset(a)];
+      const double* B = &Rb[rot_block_offset(a)];
+      for (int i = 0; i <= a; ++i)
+        for (int k = 1; k <= a; ++k) {
+          worst = std::max(worst, std::fabs(F[re(i) * d + im(k)]) + std::fabs(F[im(k) * d + re(i)]));
+          worst = std::max(worst, std::fabs(B[re(i) * d + im(k)]) + std::fabs(B[im(k) * d + re(i)]));
+        }
+    }
+    for (int ph = 0; ph < kPasPhases; ++ph) {
+      double* Op = &ops[size_t(o) * op_stride + size_t(ph) * L.phase_size];
+      const auto& sub = L.sub[ph];
+      for (size_t b = 0; b < L.groups[ph].size(); ++b) {
+        const auto& gr = L.groups[ph][b];
+        int S = 0;
+        for (int i : gr) S += int(sub[i].rows.size());
+        const int sp = (S + 3) / 4 * 4;
+        double* Ob = Op + L.opoff[ph][b];
+        int off = 0;  // sub-blocks block-diagonally
+        for (int si : gr) {
+          const int part = sub[si].part, a = sub[si].a, sz = int(sub[si].rows.size());
+          for (int i = 0; i < sz; ++i)
+            for (int k = 0; k < sz; ++k) {
+              double val;
+              if (ph != 1) {  // W (rotation of the multipole), V (back-rotation of the local)
+                const int d = 2 * a + 1, mi = part + i, mk = part + k;
+                const int ri = part ? im(mi) : re(mi), rk = part ? im(mk) : re(mk);
+                val = (ph == 0 ? Rf : Rb)[rot_block_offset(a) + size_t(ri) * d + rk];
+              } else {  // Z: order m = a, rows n / columns j in [m, p]: (-1)^{n+m} (j+n)! / rho^{j+n+1}
+                const int m = a, n = m + i, j = m + k;
+                double f = 1.0;
+                for (int t = 2; t <= j + n; ++t) f *= t;
+                val = (((n + m) & 1) ? -1.0 : 1.0) * f / std::pow(rho, j + n + 1);
+              }
+              Ob[frag(off + i, off + k, sp)] = val;
             }
-            Z[z + size_t(i) * szp + k] = val;
-          }
-        z += size_t(szr) * szp;
+          off += sz;
+        }
       }
+    }
   }
   if (worst > 1e-12) throw std::runtime_error("pas_build_ops: rotation blocks mix Re and Im at phi = 0");
 }
 
-int launch_m2l_pas(const M2LPlan& P, const M2LChunk& C, const DevData& D, double* stage, cudaStream_t s) {
-  const double* X = reinterpret_cast<const double*>(D.M);
-  const int kp2 = 2 * D.kp;
-  int r = -1;
+int launch_m2l(const M2LPlan& P, const DevData& D, cudaStream_t s) {
+  if (P.n_groups == 0) return 0;
   switch (D.p) {
-#define QBXG_PAS_P(N) \
-  case N:             \
-    r = pas_launch_p<N>(P, C, X, kp2, stage, s); \
-    break;
-    QBXG_PAS_P(1) QBXG_PAS_P(2) QBXG_PAS_P(3) QBXG_PAS_P(4) QBXG_PAS_P(5) QBXG_PAS_P(6) QBXG_PAS_P(7)
-    QBXG_PAS_P(8) QBXG_PAS_P(9) QBXG_PAS_P(10) QBXG_PAS_P(11) QBXG_PAS_P(12) QBXG_PAS_P(13) QBXG_PAS_P(14)
-    QBXG_PAS_P(15) QBXG_PAS_P(16) QBXG_PAS_P(17) QBXG_PAS_P(18) QBXG_PAS_P(19) QBXG_PAS_P(20) QBXG_PAS_P(21)
-#undef QBXG_PAS_P
+#define QBXG_TG_P(N) \
+  case N:            \
+    return tg_launch<N>(P, D, s);
+    QBXG_PAS_ORDERS(QBXG_TG_P)
+#undef QBXG_TG_P
     default: return -1;
   }
-  return r;
-}
-
-int launch_m2l_reduce(const M2LPlan& P, const M2LChunk& C, const DevData& D, const double* stage, cudaStream_t s) {
-  if (C.n_boxes == 0) return 0;
-  k_m2l_reduce<<<C.n_boxes, 160, 0, s>>>(C.boxes, D.v_starts, P.ent_op, P.cs, D.p, P.srow, C.base, stage, D.box,
-                                         reinterpret_cast<double*>(D.L), 2 * D.kp);
-  return 1;
 }
 
 }  // namespace dev
