@@ -15,28 +15,34 @@
 // azimuthal blocks.  W, Z and V depend on (rho_xy^2, dz) only: the 1,206 offsets of
 // [-5,5]^3 fall into 190 classes, one operator set per class (~19 MB at p = 15).
 //
-// Work split (target-grouped).  One CTA owns a group of G target boxes (32 at p <= 15,
+// Work split (target-grouped).  One CTA owns a group of G target boxes (32 at p <= 16,
 // consecutive in DFS order) and walks a host-built list of tiles: a tile is <= BN
 // List-2 entries of the group that share an operator class, columns sorted by
-// (target slot, offset).  Per tile:
-//   1. the BN source multipoles arrive in shared memory by TMA bulk copies
-//      (cp.async.bulk, one per multipole, issued one tile ahead on an mbarrier);
-//   2. all threads rotate them by e^{i k alpha} into the (p+1)^2 x BN real tile X;
-//   3. the three phases W, Z, V run in place on X as m8n8k4 DMMAs, each warp owning
-//      a fixed, longest-processing-time balanced list of whole blocks; the phase's
-//      operator blocks (stored in DMMA fragment order) are TMA-loaded into one of two
-//      shared slots one phase ahead, so A fragments are conflict-free shared loads;
-//   4. each column is rotated back by e^{-i m alpha} and added to its target's
-//      accumulators, which live in registers (LPT = 256 / G threads per target,
-//      thread j owning coefficients q = j, j + LPT, ...).
+// (target slot, offset).  Two CTAs of 8 warps share an SM (one CTA's gather, barriers
+// and accumulate overlap the other's DMMA phases).  Per tile:
+//   1. the columns' multipoles are read from L2 and rotated by e^{i k alpha} into the
+//      (p+1)^2 x BN real tile X in shared memory (XOR-swizzled);
+//   2. W, Z and V run in place on X as m8n8k4 DMMAs; each phase's blocks (sub-blocks
+//      merged block-diagonally where that costs no extra fragments: 17 per phase at
+//      p = 15) are balanced over the warps; operator blocks are stored in DMMA
+//      fragment order and read from L2 as coalesced 256-byte fragments;
+//   3. each column is rotated back by e^{-i m alpha} and added to its target's
+//      accumulators, which live in tensor memory (tcgen05.ld / tcgen05.st; warp w owns
+//      target slots w, w + 8, ..., lane l the coefficients q = l + 32 k).
 // At the end every target's local gets L += acc / |b|, once.  A target's entries are
 // summed in (class, offset) order whatever the group composition: the result is
 // bitwise reproducible run to run and identical between sharded and
-// single-GPU applies, and no staging rows leave the SM.
+// single-GPU applies, and no staging rows leave the SM (the round-1 offset-grouped
+// kernel wrote and re-read 2 KB per List-2 entry: 95 GB per apply at config 1).
+// Measured and not kept (profiles/r02_ncu_m2l.json): one CTA of 16 warps per SM with
+// the multipoles and operators staged in shared memory by TMA bulk copies on
+// mbarriers (44.8 vs 43.1 ms), register accumulators, double-buffered tiles with the
+// gather overlapped in the phases, L1 prefetch of operator fragments.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <vector>
 
@@ -50,8 +56,8 @@ namespace dev {
 namespace {
 
 constexpr int kPasPhases = 3;
-constexpr int kWarps = 16, kNTh = kWarps * 32;
-constexpr size_t kSmemMax = 232448 - 2048;  // 227 KB per CTA (sm_100) less static shared memory
+constexpr int kWarps = 8, kNTh = kWarps * 32;  // two CTAs per SM
+constexpr size_t kSmemMax = 232448 / 2 - 2048;  // two CTAs per SM (sm_100: 228 KB), less static
 
 // per-phase operator size bound (doubles): blocks of sizes 1..p+1 (Re) and 1..p (Im),
 // rows padded to 8 and columns to 4 -- the same multiset for W, Z and V (merging
@@ -73,26 +79,22 @@ constexpr int kMaxBlock = 22;  // largest (merged) block the kernel instantiates
 template <int P>
 struct Tg {
   static constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), KP2 = 2 * NR;
-  static constexpr int PH = phase_doubles(P);     // operator slot size (doubles)
-  static constexpr int KA = (NR + 31) / 32;       // coefficients per lane in the accumulate
-  static constexpr int TPW = 32 / KA < 4 ? 32 / KA : 4;  // target boxes per warp
-  static constexpr int G = kWarps * TPW;          // target boxes per CTA
-  static constexpr int TW = 4 * KA;               // TMEM words (columns) per target per lane
-  // TMEM: warps w, w+4, w+8, w+12 share lane quadrant w % 4, each its own column range
+  static constexpr int KA = (NR + 31) / 32;                // coefficients per lane in the accumulate
+  static constexpr int TPW = 32 / KA < 4 ? 32 / KA : 4;    // target boxes per warp
+  static constexpr int G = kWarps * TPW;                   // target boxes per CTA
+  static constexpr int TW = 4 * KA;                        // TMEM words (columns) per target per lane
+  // TMEM: warps w, w + 4 share lane quadrant w % 4, each its own column range
   static constexpr int TCOLS = (kWarps / 4) * TPW * TW;
   static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
-  static_assert(TCOLS <= 512, "TMEM accumulators exceed 512 columns");
-  static constexpr size_t bytes(int bn, bool sops) {
-    return size_t(bn) * KP2 * 8                   // RAW: gathered multipoles (TMA)
-           + (sops ? size_t(2) * PH * 8 : 0)      // OPS: two phase slots (TMA)
-           + size_t(NROW + 1) * bn * 8            // X (+ a zero row), swizzled
+  static_assert(TCOLS <= 256, "TMEM accumulators exceed half of tensor memory");
+  static constexpr size_t bytes(int bn) {
+    return size_t(NROW + 1) * bn * 8              // X (+ a zero row), swizzled
            + size_t(2) * bn * (P + 1) * 16        // (cos, sin) per column, two tiles
            + size_t(6) * bn * 4                   // column meta, three tiles
            + size_t(tab_ints(P)) * 4;             // block table
   }
-  static constexpr int BN = bytes(32, false) <= kSmemMax ? 32 : 16;  // tile columns
-  static constexpr bool SOPS = bytes(BN, true) <= kSmemMax;          // operators staged by TMA
-  static constexpr size_t SMEM = bytes(BN, SOPS);
+  static constexpr int BN = bytes(32) <= kSmemMax ? 32 : 16;  // tile columns
+  static constexpr size_t SMEM = bytes(BN);
 };
 
 // X element (row r, column c) lives at r * BN + (c ^ swz(r)): the B-fragment loads
@@ -104,33 +106,9 @@ struct TabHead {
   int base[kPasPhases];
 };
 
-// ---- PTX helpers: mbarrier + TMA bulk copy (cp.async.bulk), DMMA, TMEM
+// ---- PTX helpers: cp.async, DMMA, tensor memory
 __device__ __forceinline__ unsigned sm_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = sm_addr(bar);
-  unsigned ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   sm_addr(dst)),
-               "l"(src), "r"(bytes), "r"(sm_addr(bar))
-               : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sm_addr(smem)), "l"(gmem));
@@ -146,7 +124,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// TMEM: 4K consecutive 32-bit columns of this lane <-> K (re, im) double pairs, one wait
+// TMEM: 4K consecutive 32-bit columns of this lane -> K (re, im) double pairs, one wait
 template <int K>
 __device__ __forceinline__ void tm_ld(unsigned ta, double* re, double* im) {
   unsigned r[4 * K];
@@ -163,17 +141,7 @@ __device__ __forceinline__ void tm_ld(unsigned ta, double* re, double* im) {
     im[k] = __hiloint2double(int(r[4 * k + 3]), int(r[4 * k + 2]));
   }
 }
-// TMEM: 4 consecutive 32-bit columns of this lane <-> two doubles
-__device__ __forceinline__ void tm_ld4(unsigned ta, double& x, double& y) {
-  unsigned r0, r1, r2, r3;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(ta)
-               : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-  x = __hiloint2double(int(r1), int(r0));
-  y = __hiloint2double(int(r3), int(r2));
-}
+// TMEM: 4 consecutive 32-bit columns of this lane <- two doubles
 __device__ __forceinline__ void tm_st4(unsigned ta, double x, double y) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(ta),
                "r"(__double2loint(x)), "r"(__double2hiint(x)), "r"(__double2loint(y)), "r"(__double2hiint(y))
@@ -230,25 +198,22 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
 }
 
 template <int P>
-__global__ void __launch_bounds__(kNTh, 1)
+__global__ void __launch_bounds__(kNTh, 2)
     k_m2l_tg(const int* __restrict__ tab, int tab_n, TabHead hd, const double* __restrict__ ops, int op_stride,
              int phase_size, const double2* __restrict__ cs_all, const int* __restrict__ grp_order,
              const int* __restrict__ grp_tiles, const int* __restrict__ grp_box, const int4* __restrict__ tiles,
              const int* __restrict__ col_src, const int* __restrict__ col_meta, const double2* __restrict__ M,
              const double4* __restrict__ box, double* __restrict__ L) {
   using C = Tg<P>;
-  constexpr int NR = C::NR, NROW = C::NROW, KP2 = C::KP2, BN = C::BN, PH = C::PH;
+  constexpr int NR = C::NR, NROW = C::NROW, KP2 = C::KP2, BN = C::BN;
   constexpr int KA = C::KA, TPW = C::TPW, TW = C::TW;
   extern __shared__ __align__(16) unsigned char smem[];
-  double2* RAW = reinterpret_cast<double2*>(smem);
-  double* OPS = reinterpret_cast<double*>(RAW + BN * NR);
-  double* X = OPS + (C::SOPS ? 2 * PH : 0);
+  double* X = reinterpret_cast<double*>(smem);
   double2* s_cs = reinterpret_cast<double2*>(X + (NROW + 1) * BN);  // [2][BN][P+1]
   int* s_meta = reinterpret_cast<int*>(s_cs + 2 * BN * (P + 1));   // [3][BN]: target slot | offset << 8
   int* s_msrc = s_meta + 3 * BN;                                    // [3][BN]: source box
   int* s_tab = s_msrc + 3 * BN;
   __shared__ int s_code[NR];  // half-table q: Re row | Im row << 10 (zero row if m = 0) | m << 20
-  __shared__ uint64_t bar[3];  // RAW, OPS slot 0, OPS slot 1
   __shared__ unsigned s_tmem;
 
   const int g = grp_order[blockIdx.x];
@@ -268,12 +233,6 @@ __global__ void __launch_bounds__(kNTh, 1)
     s_code[q] = q | (m > 0 ? NR + n * (n - 1) / 2 + m - 1 : NROW) << 10 | m << 20;
   }
   for (int c = tid; c < BN; c += kNTh) X[NROW * BN + c] = 0.0;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
   // Tile metadata runs ahead by cp.async: column (slot | offset, source) two tiles
   // ahead (buffer it % 3), the columns' (cos, sin) rows one tile ahead (buffer it & 1),
   // so no thread waits on a global load between barriers.
@@ -290,17 +249,6 @@ __global__ void __launch_bounds__(kNTh, 1)
       cp_async16(sc + i, cs_all + size_t(s_meta[mbuf * BN + c] >> 8) * (P + 1) + m);
     }
   };
-  // warp 0: a tile's multipoles into RAW, one bulk copy per column
-  auto issue_raw = [&](int ncols, int mbuf) {
-    if (lane == 0) mbar_expect_tx(&bar[0], unsigned(ncols) * KP2 * 8);
-    __syncwarp();
-    if (lane < ncols) tma_load(RAW + lane * NR, M + size_t(s_msrc[mbuf * BN + lane]) * NR, KP2 * 8, &bar[0]);
-  };
-  auto issue_ops = [&](int cls, int ph, int slot) {
-    mbar_expect_tx(&bar[1 + slot], phase_size * 8);
-    tma_load(OPS + slot * PH, ops + size_t(cls) * op_stride + size_t(ph) * phase_size, phase_size * 8,
-             &bar[1 + slot]);
-  };
   int4 tl = make_int4(0, 0, 0, 0), tn = tl;
   if (t_begin < t_end) {
     tl = tiles[t_begin];
@@ -314,11 +262,7 @@ __global__ void __launch_bounds__(kNTh, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (t_begin < t_end) {
-    if (warp == 0) issue_raw(tl.z, 0);
-    if (C::SOPS && tid == 0) issue_ops(tl.x, 0, 0);
-    load_cs(tl.z, 0, 0);
-  }
+  if (t_begin < t_end) load_cs(tl.z, 0, 0);
   // this warp's accumulators: lane quadrant warp % 4, columns of its TPW targets
   const unsigned tm = s_tmem + (unsigned(32 * (warp & 3)) << 16) + unsigned((warp >> 2) * TPW * TW);
 #pragma unroll 1
@@ -327,7 +271,6 @@ __global__ void __launch_bounds__(kNTh, 1)
   cp_async_wait_all();
   __syncthreads();
 
-  int kph = 0;  // phases run so far (operator slot kph & 1)
 #pragma unroll 1
   for (int t = t_begin, it = 0; t < t_end; ++t, ++it) {
     const bool more = t + 1 < t_end;
@@ -336,37 +279,44 @@ __global__ void __launch_bounds__(kNTh, 1)
     const int mb = it % 3, mb1 = (it + 1) % 3, mb2 = (it + 2) % 3, cb = it & 1;
     const int* sm = s_meta + mb * BN;
     const double2* sc = s_cs + cb * BN * (P + 1);
-    // 1-2. multipoles of tile t (TMA) rotated by e^{i k alpha} into X
-    mbar_wait(&bar[0], it & 1);
-    for (int e = tid; e < ncols * NR; e += kNTh) {
-      const int c = e / NR, q = e - c * NR;
-      const int code = s_code[q], m = code >> 20;
-      const double2 v = RAW[c * NR + q];
-      const double2 r = sc[c * (P + 1) + m];
-      const int re = code & 1023, im = (code >> 10) & 1023;
-      X[re * BN + (c ^ swz(re))] = v.x * r.x - v.y * r.y;
-      if (m) X[im * BN + (c ^ swz(im))] = v.x * r.y + v.y * r.x;
+    {  // 1. multipoles straight from L2, rotated by e^{i k alpha} into X; four loads in
+       // flight per thread
+      const int ne = ncols * NR;
+      const int* src = s_msrc + mb * BN;
+#pragma unroll 1
+      for (int e0 = tid; e0 < ne; e0 += 4 * kNTh) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kNTh;
+          if (e < ne) {
+            const int c = e / NR;
+            v[u] = __ldg(M + size_t(src[c]) * NR + (e - c * NR));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kNTh;
+          if (e < ne) {
+            const int c = e / NR, q = e - c * NR;
+            const int code = s_code[q], m = code >> 20;
+            const double2 r = sc[c * (P + 1) + m];
+            const int re = code & 1023, im = (code >> 10) & 1023;
+            X[re * BN + (c ^ swz(re))] = v[u].x * r.x - v[u].y * r.y;
+            if (m) X[im * BN + (c ^ swz(im))] = v[u].x * r.y + v[u].y * r.x;
+          }
+        }
+      }
     }
     __syncthreads();
-    if (more) {  // RAW is free: the next tile's multipoles and metadata in flight
-      if (warp == 0) issue_raw(tn.z, mb1);
+    if (more) {  // the next tiles' metadata in flight
       load_cs(tn.z, mb1, cb ^ 1);
       if (t + 2 < t_end) load_cols(tn2, mb2);
     }
-    // 3. W, Z, V in place
+    // 2. W, Z, V in place
 #pragma unroll 1
-    for (int ph = 0; ph < kPasPhases; ++ph, ++kph) {
-      const double* Op;
-      if (C::SOPS) {
-        if (tid == 0) {  // the slot of phase kph - 1 is free: load phase kph + 1 into it
-          const bool last = ph == kPasPhases - 1;
-          if (!last || more) issue_ops(last ? tn.x : tl.x, last ? 0 : ph + 1, (kph + 1) & 1);
-        }
-        mbar_wait(&bar[1 + (kph & 1)], (kph >> 1) & 1);
-        Op = OPS + (kph & 1) * PH;
-      } else {
-        Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
-      }
+    for (int ph = 0; ph < kPasPhases; ++ph) {
+      const double* Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
       const int* T = s_tab + hd.base[ph];
       const int nblk = T[0];
       const int* rowoff = T + 1;
@@ -395,7 +345,7 @@ __global__ void __launch_bounds__(kNTh, 1)
 #undef QBXG_PAS_CASE
       __syncthreads();
     }
-    // 4. rotate back by e^{-i m alpha} and add to the owning warp's accumulators (TMEM),
+    // 3. rotate back by e^{-i m alpha} and add to the owning warp's accumulators (TMEM),
     // in column order; a target's columns are consecutive, so its accumulators are read
     // and written once per tile
     {
