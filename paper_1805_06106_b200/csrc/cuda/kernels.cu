@@ -322,22 +322,29 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// Chunk slot f lives at near_pos(f, sh) = f ^ ((f >> sh) & 7), 2^sh ~ W (sh >= 3): the
+// lanes of a warp read slots W apart, and the XOR spreads them over the eight 16-byte
+// bank units a 32-byte slot pair can start on (unswizzled, an even W put every lane of
+// a warp on one or two).  The map permutes aligned groups of eight slots and keeps
+// (f, f + 1) adjacent for even f.
+__device__ __forceinline__ int near_pos(int f, int sh) { return f ^ ((f >> sh) & 7); }
+
 template <bool DIP>
 __device__ __forceinline__ void near_stage(const DevData& D, const int* __restrict__ list, int nsrc, int k, int L,
-                                           double4* s_src, double4* s_mu) {
+                                           int sh, double4* s_src, double4* s_mu) {
   for (int f = threadIdx.x; f < L; f += kNearThreads) {
-    const int g = k * L + f;
+    const int g = k * L + f, pf = near_pos(f, sh);
     if (g < nsrc) {
       const int si = __ldg(list + g);
-      cp_async16(&s_src[f], &D.src[si]);
-      cp_async16(reinterpret_cast<char*>(&s_src[f]) + 16, reinterpret_cast<const char*>(&D.src[si]) + 16);
+      cp_async16(&s_src[pf], &D.src[si]);
+      cp_async16(reinterpret_cast<char*>(&s_src[pf]) + 16, reinterpret_cast<const char*>(&D.src[si]) + 16);
       if (DIP) {
-        cp_async16(&s_mu[f], &D.mu[si]);
-        cp_async16(reinterpret_cast<char*>(&s_mu[f]) + 16, reinterpret_cast<const char*>(&D.mu[si]) + 16);
+        cp_async16(&s_mu[pf], &D.mu[si]);
+        cp_async16(reinterpret_cast<char*>(&s_mu[pf]) + 16, reinterpret_cast<const char*>(&D.mu[si]) + 16);
       }
     } else {  // padding: zero weight and moment far away (every term is an exact 0)
-      s_src[f] = make_double4(1e30, 1e30, 1e30, 0.0);
-      if (DIP) s_mu[f] = make_double4(0.0, 0.0, 0.0, 0.0);
+      s_src[pf] = make_double4(1e30, 1e30, 1e30, 0.0);
+      if (DIP) s_mu[pf] = make_double4(0.0, 0.0, 0.0, 0.0);
     }
   }
   cp_async_commit();
@@ -383,6 +390,7 @@ __global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevDa
     const int W = 2 * ((total + 2 * kNearThreads - 1) / (2 * kNearThreads));  // even, <= L
     const int t0 = min(total, tid * W), nw = min(W, total - t0);     // this thread's pairs
     const int home = L ? t0 / L : 0;
+    const int sh = W > 8 ? 31 - __clz(W) : 3;                        // slot swizzle (near_pos)
     const int sw = L ? (home + 1) * L - t0 : 0;                      // pairs before the next centre
     const bool straddle = nw > sw;
     for (int c = tid; c < ncc; c += kNearThreads)
@@ -394,12 +402,12 @@ __global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevDa
 #pragma unroll
     for (int i = 0; i < KQ; ++i) ax[i] = ay[i] = 0.0;
     __syncthreads();  // previous group's s_part reads and buffers done; rows zeroed
-    if (K > 0) near_stage<DIP>(D, list, nsrc, 0, L, s_src[0], s_mu[0]);
+    if (K > 0) near_stage<DIP>(D, list, nsrc, 0, L, sh, s_src[0], s_mu[0]);
     for (int k = 0; k < K; ++k) {
       const int buf = k & 1;
       cp_async_wait_all();
       __syncthreads();  // chunk k staged; everyone is past chunk k - 1
-      if (k + 1 < K) near_stage<DIP>(D, list, nsrc, k + 1, L, s_src[buf ^ 1], s_mu[buf ^ 1]);
+      if (k + 1 < K) near_stage<DIP>(D, list, nsrc, k + 1, L, sh, s_src[buf ^ 1], s_mu[buf ^ 1]);
       const double4* S = s_src[buf];
       const double4* U = s_mu[buf];
       int j = t0 - home * L;  // chunk slot of the thread's first pair
@@ -412,8 +420,9 @@ __global__ void __launch_bounds__(kNearThreads, Q <= 5 ? 3 : 1) k_near_qbx(DevDa
           ir = 1.0 / c.w;
           j = 0;
         }
-        near_pair<Q, DIP>(S[j], DIP ? U[j] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
-        near_pair<Q, DIP>(S[j + 1], DIP ? U[j + 1] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+        const int pj = near_pos(j, sh);  // j even: slot j + 1 sits at pj ^ 1
+        near_pair<Q, DIP>(S[pj], DIP ? U[pj] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
+        near_pair<Q, DIP>(S[pj ^ 1], DIP ? U[pj ^ 1] : make_double4(0, 0, 0, 0), c, ir, ax, ay);
       }
       if (straddle) {  // park the head in its centre's row (one writer per row), back to home
         double2* o = out + size_t(home + 1) * KQ;
