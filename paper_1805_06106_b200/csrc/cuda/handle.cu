@@ -97,10 +97,6 @@ struct Handle {
   // work lists
   int* d_leaves = nullptr;
   int n_leaves = 0;
-  std::vector<int*> d_m2m_level;
-  std::vector<int> n_m2m_level;
-  std::vector<int*> d_l2l_level;
-  std::vector<int> n_l2l_level;
   int* d_ctr_boxes = nullptr;
   int n_ctr_boxes = 0;
   int* d_near_boxes = nullptr;  // d_ctr_boxes, heaviest near field first (no tail of big boxes)
@@ -148,17 +144,12 @@ struct Handle {
   bool helm = false;
   dev::HelmData HD{};
   std::vector<double2*> h_ops_m2m, h_ops_l2l;  // per level: 8 octant operators
-  // batched shifts: (src, dst) pairs grouped by (level, octant); QBXG_HELM_SHIFT=box keeps k_h_shift
-  bool h_shift_batched = true;
+  // batched shifts: (src, dst) pairs grouped by (level, octant)
   int2* h_m2m_pairs = nullptr;
   int2* h_l2l_pairs = nullptr;
   std::vector<int> h_m2m_off, h_l2l_off;  // (nlev x 8 + 1) offsets
-  double2* h_ops_m2l = nullptr;                // per (level, offset) operators (split: even / odd blocks)
   double2* h_cs = nullptr;                     // per operator e^{i m alpha}, m <= p (split form)
   int* h_ent_op = nullptr;                     // operator of every List-2 CSR entry (split form)
-  bool h_split = true;                         // QBXG_HELM_M2L=full keeps the full operators
-  // point-and-shoot M2L (default for p <= 20; QBXG_HELM_M2L=split or full opts out)
-  bool h_pas = false;
   double* h_zops = nullptr;   // per operator: Z blocks (fragment order)
   double* h_wvops = nullptr;  // per polar-angle class: W and V blocks
   int* h_op_cls = nullptr;    // operator -> polar-angle class
@@ -528,7 +519,6 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
     for (int l = 0; l + 1 < H.nlev; ++l, k += 8) H.h_ops_m2m[l] = shift_ops + k * opsz;
     for (int l = 1; l < H.nlev; ++l, k += 8) H.h_ops_l2l[l] = shift_ops + k * opsz;
   }
-  H.h_shift_batched = !(std::getenv("QBXG_HELM_SHIFT") && std::string(std::getenv("QBXG_HELM_SHIFT")) == "box");
   {
     // (src, dst) pairs per (level, octant) with the operators' octant convention (x 4, y 2, z 1)
     auto hoct = [&](int c, int par) {
@@ -584,19 +574,8 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
         }
         op_of_entry[e] = op;
       }
-    const char* hm = std::getenv("QBXG_HELM_M2L");
-    H.h_split = !(hm && std::string(hm) == "full");
-    H.h_pas = H.h_split && !hm && dev::helm_pas_supported(p);
-    const size_t per_op = H.h_pas ? 0 : H.h_split ? dev::helm_split_op_size(p) : opsz;
-    const size_t bytes = msh.size() * per_op * sizeof(double2);
-    size_t free_b = 0, total_b = 0;
-    QCK(cudaMemGetInfo(&free_b, &total_b));
-    if (bytes > size_t(double(free_b) * 0.7))
-      throw InvalidArgument("qbxg_create: Helmholtz M2L operators (" + std::to_string(bytes >> 20) +
-                            " MiB) exceed device memory");
-    if (!H.h_pas) H.h_ops_m2l = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * per_op);
-    if (H.h_pas) {
-      // W, V per polar angle of the integer offset (level independent), Z per (level, offset)
+    if (!dev::helm_pas_supported(p)) throw InvalidArgument("qbxg_create: the Helmholtz M2L supports p_fmm <= 20");
+    {  // point-and-shoot: W, V per polar angle of the integer offset (level independent), Z per (level, offset)
       const HpasLayout PL = hpas_layout(p);
       std::vector<int> cls(msh.size()), key_cls;
       std::vector<double> thetas;
@@ -634,17 +613,10 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
       H.h_pas_tab_n = int(tab.size());
       H.h_ent_op = dupload(O, op_of_entry, s);
       QCK(cudaStreamSynchronize(s));  // host vectors go out of scope
-    } else if (H.h_split) {
-      for (auto& v : msh) v.w = 0.0;  // the split builder takes the plain offset vector
-      H.h_cs = dalloc<double2>(O, std::max<size_t>(msh.size(), 1) * (p + 1));
-      if (!msh.empty()) dev::helm_build_split(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, H.h_cs, s);
-      H.h_ent_op = dupload(O, op_of_entry, s);
-    } else if (!msh.empty()) {
-      dev::helm_build_ops(HD, int(msh.size()), dupload(O, msh, s), H.h_ops_m2l, s);
     }
     // tiles of same-operator entries, chunked over contiguous target boxes
-    const int cols = H.h_split ? dev::helm_m2l_split_cols() : dev::helm_m2l_cols();
-    size_t free2 = 0;
+    const int cols = dev::helm_m2l_split_cols();
+    size_t free2 = 0, total_b = 0;
     QCK(cudaMemGetInfo(&free2, &total_b));
     const int64_t cap = std::max<int64_t>(
         int64_t(std::min<size_t>(size_t(8) << 30, size_t(double(free2) * 0.4)) / (HD.KP * sizeof(double2))), 1024);
@@ -788,10 +760,6 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
   chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
   QCK(cudaEventRecord(ev[2], s));
   for (int l = H.nlev - 2; l >= 0; --l) {
-    if (!H.h_shift_batched) {
-      chk(dev::helm_shift(HD, 0, H.d_m2m_level[l], H.n_m2m_level[l], H.h_ops_m2m[l], s));
-      continue;
-    }
     for (int o = 0; o < 8; ++o) {  // octants in a fixed order: deterministic sums into the parents
       const int a = H.h_m2m_off[size_t(l) * 8 + o], e = H.h_m2m_off[size_t(l) * 8 + o + 1];
       chk(dev::helm_shift_pairs(HD, 0, H.h_m2m_pairs + a, e - a, H.h_ops_m2m[l] + size_t(o) * HD.KP * HD.KP, s));
@@ -801,26 +769,14 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
   chk(dev::helm_near(HD, H.d_near_boxes, H.n_ctr_boxes, s));
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
   QCK(cudaEventRecord(ev[4], s));
-  for (const auto& C : H.h_m2l) {
-    if (H.h_pas)
-      chk(dev::helm_m2l_pas(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_pas_tab, H.h_pas_tab_n, H.h_pas_base,
-                            H.h_zops, H.h_zstride, H.h_wvops, H.h_wvstride, H.h_op_cls, H.h_cs, H.h_temp, C.n_boxes,
-                            C.boxes, C.base, H.h_ent_op, s));
-    else if (H.h_split)
-      chk(dev::helm_m2l_split(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_cs, H.h_temp,
-                              C.n_boxes, C.boxes, C.base, H.h_ent_op, s));
-    else
-      chk(dev::helm_m2l(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_ops_m2l, H.h_temp, C.n_boxes, C.boxes,
-                        C.base, s));
-  }
+  for (const auto& C : H.h_m2l)
+    chk(dev::helm_m2l_pas(HD, C.n_tiles, C.tiles, C.col_src, C.col_pos, H.h_pas_tab, H.h_pas_tab_n, H.h_pas_base,
+                          H.h_zops, H.h_zstride, H.h_wvops, H.h_wvstride, H.h_op_cls, H.h_cs, H.h_temp, C.n_boxes,
+                          C.boxes, C.base, H.h_ent_op, s));
   QCK(cudaEventRecord(ev[5], s));
   chk(dev::helm_p2l(HD, H.d_xfar_boxes, H.n_xfar_boxes, s));
   QCK(cudaEventRecord(H.evx[2], s));
   for (int l = 1; l < H.nlev; ++l) {
-    if (!H.h_shift_batched) {
-      chk(dev::helm_shift(HD, 1, H.d_l2l_level[l], H.n_l2l_level[l], H.h_ops_l2l[l], s));
-      continue;
-    }
     for (int o = 0; o < 8; ++o) {
       const int a = H.h_l2l_off[size_t(l) * 8 + o], e = H.h_l2l_off[size_t(l) * 8 + o + 1];
       chk(dev::helm_shift_pairs(HD, 1, H.h_l2l_pairs + a, e - a, H.h_ops_l2l[l] + size_t(o) * HD.KP * HD.KP, s));
@@ -1043,10 +999,6 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
 
     // work lists
     std::vector<int> leaves, cb, tb, vb, wb, wtb, xb;
-    H.d_m2m_level.assign(H.nlev, nullptr);
-    H.n_m2m_level.assign(H.nlev, 0);
-    H.d_l2l_level.assign(H.nlev, nullptr);
-    H.n_l2l_level.assign(H.nlev, 0);
     for (int b = 0; b < nb; ++b) {
       const bool leaf = V.box_flags[b] & QBXG_BOX_LEAF;
       const bool own = mk[b] & QBXG_SHARD_OWN;
@@ -1232,21 +1184,6 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
     }
     H.d_xfar_boxes = dupload(O, xb, s);
     H.n_xfar_boxes = int(xb.size());
-    for (int l = 0; l < H.nlev; ++l) {
-      std::vector<int> m2m, l2l;
-      for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
-        const int b = V.level_boxes[i];
-        if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES) &&
-            (mk[b] & QBXG_SHARD_SUBTREE))
-          m2m.push_back(b);
-        if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) && (mk[b] & QBXG_SHARD_DOWN))
-          l2l.push_back(b);
-      }
-      H.d_m2m_level[l] = dupload(O, m2m, s);
-      H.n_m2m_level[l] = int(m2m.size());
-      H.d_l2l_level[l] = dupload(O, l2l, s);
-      H.n_l2l_level[l] = int(l2l.size());
-    }
   }
 
   if (H.helm) {

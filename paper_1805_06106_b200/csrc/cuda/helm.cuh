@@ -52,21 +52,11 @@ constexpr int kHCtrMax = 32;
 void helm_upload_constants();  // solid-harmonic recurrence tables (this TU's __constant__)
 int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, const double* mu, cudaStream_t s);
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s);
-int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s);
 int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2* ops, cudaStream_t s);
 // M2M (mode 0: M[dst] += T M[src]) / L2L (mode 1: L[dst] += T L[src]) over (src, dst)
 // pairs that share one (level, octant) operator, 8 pairs per CTA
 int helm_shift_pairs(const HelmData& H, int mode, const int2* pairs, int n, const double2* ops, cudaStream_t s);
-int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-             const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s);
-int helm_m2l_cols();
 int helm_m2l_split_cols();
-// split M2L (even / odd blocks in the rotated frame): operator size, builder, apply
-size_t helm_split_op_size(int P);
-int helm_build_split(const HelmData& H, int n_ops, const double4* shifts, double2* ops, double2* cs, cudaStream_t s);
-int helm_m2l_split(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-                   const double2* ops, const double2* cs, double2* temp, int n_boxes, const int* boxes, int64_t base,
-                   const int* ent_op, cudaStream_t s);
 // point-and-shoot M2L (even / odd split frame): Z blocks + e^{i m alpha} per operator,
 // block tables, apply (pas kernel + the split reduce)
 bool helm_pas_supported(int P);

@@ -292,48 +292,6 @@ __global__ void __launch_bounds__(256) k_h_p2m(HelmData H, const int* __restrict
   for (int i = threadIdx.x; i < H.KP; i += blockDim.x, ++slot) H.M[size_t(b) * H.KP + i] = acc[slot];
 }
 
-// M2M (mode 0, CTA per parent, sum over children) / L2L (mode 1, CTA per child):
-// out[i] (+)= sum_k T[k][i] in[k], T k-major, 8 octant operators of the level
-__global__ void __launch_bounds__(512) k_h_shift(HelmData H, int mode, const int* __restrict__ boxes,
-                                                 const double2* __restrict__ ops) {
-  extern __shared__ double2 sm[];
-  double2* X = sm;
-  const int b = boxes[blockIdx.x];
-  const int KP = H.KP, i = threadIdx.x;
-  auto octant = [&](int child, int par) {
-    const double4 c = H.box[child], p = H.box[par];
-    return (c.x > p.x ? 4 : 0) + (c.y > p.y ? 2 : 0) + (c.z > p.z ? 1 : 0);
-  };
-  double2 acc = make_double2(0, 0);
-  if (mode == 0) {
-    for (int kk = H.child_starts[b]; kk < H.child_starts[b + 1]; ++kk) {
-      const int c = H.children[kk];
-      const double2* T = ops + size_t(octant(c, b)) * KP * KP;
-      __syncthreads();
-      for (int j = threadIdx.x; j < KP; j += blockDim.x) X[j] = H.M[size_t(c) * KP + j];
-      __syncthreads();
-      if (i < KP)
-        for (int k2 = 0; k2 < KP; ++k2) acc = cfma(T[size_t(k2) * KP + i], X[k2], acc);
-    }
-    if (i < KP) H.M[size_t(b) * KP + i] = acc;
-  } else {
-    const int a = H.parent[b];
-    const double2* T = ops + size_t(octant(b, a)) * KP * KP;
-    for (int j = threadIdx.x; j < KP; j += blockDim.x) X[j] = H.L[size_t(a) * KP + j];
-    __syncthreads();
-    if (i < KP) {
-      for (int k2 = 0; k2 < KP; ++k2) acc = cfma(T[size_t(k2) * KP + i], X[k2], acc);
-      const double2 v = H.L[size_t(b) * KP + i];
-      H.L[size_t(b) * KP + i] = make_double2(v.x + acc.x, v.y + acc.y);
-    }
-  }
-}
-
-// M2M / L2L batched by (level, octant): one CTA applies the level's octant operator to
-// NB (source box, destination box) pairs, so each operator element read from L2 feeds NB
-// complex multiply-adds instead of one (k_h_shift streams the 3 MB operator per box).
-// dst += T src, thread per output row; each destination appears once per launch and the
-// octant launches run in a fixed order, so the sums are deterministic.
 template <int NB>
 __global__ void __launch_bounds__(512) k_h_shift_b(HelmData H, int mode, const int2* __restrict__ pairs, int n,
                                                    const double2* __restrict__ T) {
@@ -439,106 +397,8 @@ __device__ __forceinline__ double2 t_entry(const HelmData& H, const double2* F, 
   return make_double2(4.0 * kPi * acc.x, 4.0 * kPi * acc.y);
 }
 
-// operator builder (split): per op, E (NE x NE) then O (NO x NO), k-major; cs = e^{i m alpha}
-__global__ void __launch_bounds__(256) k_h_build_split(HelmData H, const double4* __restrict__ shifts,
-                                                       double2* __restrict__ ops, double2* __restrict__ cs) {
-  extern __shared__ double2 sm[];
-  const int P = H.P, L = 2 * P;
-  const int NE = (P + 1) * (P + 2) / 2, NO = P * (P + 1) / 2;
-  double2* F = sm;
-  double2* rad = sm + (L + 1) * (L + 1);
-  const double4 t = shifts[blockIdx.x];  // original offset vector
-  const double rho = sqrt(t.x * t.x + t.y * t.y);
-  const double alpha = rho > 0 ? atan2(t.y, t.x) : 0.0;
-  if (threadIdx.x <= P) {
-    double sn, cn;
-    sincos(threadIdx.x * alpha, &sn, &cn);
-    cs[size_t(blockIdx.x) * (P + 1) + threadIdx.x] = make_double2(cn, sn);
-  }
-  wave_table_cta(H.k, L, rho, 0.0, t.z, true, F, rad);
-  double2* E = ops + size_t(blockIdx.x) * (size_t(NE) * NE + size_t(NO) * NO);
-  double2* Od = E + size_t(NE) * NE;
-  for (int e = threadIdx.x; e < NE * NE; e += blockDim.x) {
-    const int kin = e / NE, iout = e % NE;
-    int n, m, n2, m2;
-    ev_nm(kin, n, m);
-    ev_nm(iout, n2, m2);
-    double2 v;
-    if (m == 0) {
-      v = t_entry(H, F, n2, m2, n, 0);
-      if (m2 > 0) v = make_double2(2.0 * v.x, 2.0 * v.y);
-    } else {
-      const double2 a = t_entry(H, F, n2, m2, n, m), b = t_entry(H, F, n2, m2, n, -m);
-      v = make_double2(a.x + b.x, a.y + b.y);
-      if (m2 == 0) v = make_double2(0.5 * v.x, 0.5 * v.y);
-    }
-    E[e] = v;
-  }
-  for (int e = threadIdx.x; e < NO * NO; e += blockDim.x) {
-    const int kin = e / NO, iout = e % NO;
-    int n, m, n2, m2;
-    od_nm(kin, n, m);
-    od_nm(iout, n2, m2);
-    const double2 a = t_entry(H, F, n2, m2, n, m), b = t_entry(H, F, n2, m2, n, -m);
-    Od[e] = make_double2(a.x - b.x, a.y - b.y);
-  }
-}
-
-// one CTA: one operator, up to kHCols entries; threads 0..NE-1 the even rows,
-// NE..NE+NO-1 the odd rows; staging row = [A (NE) ; B (NO)]
+// point-and-shoot tiles: up to kHColsS same-operator List-2 entries (k_h_m2l_pas)
 constexpr int kHColsS = 16;
-__global__ void __launch_bounds__(512) k_h_m2l_split(HelmData H, const int4* __restrict__ tiles,
-                                                     const int* __restrict__ col_src, const int* __restrict__ col_pos,
-                                                     const double2* __restrict__ ops, const double2* __restrict__ cs,
-                                                     double2* __restrict__ temp) {
-  extern __shared__ double2 sm[];
-  const int P = H.P, KP = H.KP;
-  const int NE = (P + 1) * (P + 2) / 2, NO = P * (P + 1) / 2;
-  double2* Ba = sm;                  // kHColsS x NE
-  double2* Bb = sm + kHColsS * NE;   // kHColsS x NO
-  const int4 tile = tiles[blockIdx.x];
-  const double2* rot = cs + size_t(tile.x) * (P + 1);
-  for (int e = threadIdx.x; e < kHColsS * NE; e += blockDim.x) {
-    const int c = e / NE, q = e % NE;
-    int n, m;
-    ev_nm(q, n, m);
-    double2 a = make_double2(0, 0), bb = make_double2(0, 0);
-    if (c < tile.z) {
-      const double2* X = H.M + size_t(col_src[tile.y + c]) * KP;
-      const double2 r = rot[m];
-      const double2 xp = cmul(X[fi(n, m)], r);  // M' = M e^{i m alpha}
-      if (m == 0) {
-        a = xp;
-      } else {
-        const double2 xm = cmul(X[fi(n, -m)], make_double2(r.x, -r.y));
-        a = make_double2(xp.x + xm.x, xp.y + xm.y);
-        bb = make_double2(xp.x - xm.x, xp.y - xm.y);
-      }
-    }
-    Ba[c * NE + q] = a;
-    if (m > 0) Bb[c * NO + od_idx(n, m)] = bb;
-  }
-  __syncthreads();
-  const int i = threadIdx.x;
-  if (i >= NE + NO) return;
-  const bool odd = i >= NE;
-  const int row = odd ? i - NE : i, K = odd ? NO : NE;
-  const double2* T = ops + size_t(tile.x) * (size_t(NE) * NE + size_t(NO) * NO) + (odd ? size_t(NE) * NE : 0);
-  const double2* B = odd ? Bb : Ba;
-  double2 acc[kHColsS];
-#pragma unroll
-  for (int c = 0; c < kHColsS; ++c) acc[c] = make_double2(0, 0);
-  for (int kk = 0; kk < K; ++kk) {
-    const double2 a = T[size_t(kk) * K + row];
-#pragma unroll
-    for (int c = 0; c < kHColsS; ++c) acc[c] = cfma(a, B[c * K + kk], acc[c]);
-  }
-#pragma unroll
-  for (int c = 0; c < kHColsS; ++c)
-    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KP + i] = acc[c];
-}
-
-// reduce: rebuild y_{+-m} = (A +- B)/2 in the rotated frame, rotate back, sum in CSR order
 __global__ void __launch_bounds__(512) k_h_m2l_reduce_split(HelmData H, const int* __restrict__ boxes, int64_t base,
                                                             const double2* __restrict__ temp,
                                                             const int* __restrict__ ent_op,
@@ -568,51 +428,6 @@ __global__ void __launch_bounds__(512) k_h_m2l_reduce_split(HelmData H, const in
   }
   const double2 v = H.L[size_t(b) * KP + i];
   H.L[size_t(b) * KP + i] = make_double2(v.x + s.x, v.y + s.y);
-}
-
-// Stage 4 M2L: one CTA per (operator, up to kHCols List-2 entries); thread per output row
-constexpr int kHCols = 8;
-__global__ void __launch_bounds__(512) k_h_m2l(HelmData H, const int4* __restrict__ tiles,
-                                               const int* __restrict__ col_src, const int* __restrict__ col_pos,
-                                               const double2* __restrict__ ops, double2* __restrict__ temp) {
-  extern __shared__ double2 sm[];
-  double2* B = sm;  // kHCols x KP
-  const int4 tile = tiles[blockIdx.x];
-  const int KP = H.KP;
-  for (int e = threadIdx.x; e < kHCols * KP; e += blockDim.x) {
-    const int c = e / KP, kk = e % KP;
-    B[e] = c < tile.z ? H.M[size_t(col_src[tile.y + c]) * KP + kk] : make_double2(0, 0);
-  }
-  __syncthreads();
-  const int i = threadIdx.x;
-  if (i >= KP) return;
-  const double2* T = ops + size_t(tile.x) * KP * KP;
-  double2 acc[kHCols];
-#pragma unroll
-  for (int c = 0; c < kHCols; ++c) acc[c] = make_double2(0, 0);
-  for (int kk = 0; kk < KP; ++kk) {
-    const double2 a = T[size_t(kk) * KP + i];
-#pragma unroll
-    for (int c = 0; c < kHCols; ++c) acc[c] = cfma(a, B[c * KP + kk], acc[c]);
-  }
-#pragma unroll
-  for (int c = 0; c < kHCols; ++c)
-    if (c < tile.z) temp[size_t(col_pos[tile.y + c]) * KP + i] = acc[c];
-}
-
-__global__ void __launch_bounds__(512) k_h_m2l_reduce(HelmData H, const int* __restrict__ boxes, int64_t base,
-                                                      const double2* __restrict__ temp) {
-  const int b = boxes[blockIdx.x];
-  const int i = threadIdx.x;
-  if (i >= H.KP) return;
-  double2 s = make_double2(0, 0);
-  for (int64_t pos = H.v_starts[b]; pos < H.v_starts[b + 1]; ++pos) {
-    const double2 v = temp[size_t(pos - base) * H.KP + i];
-    s.x += v.x;
-    s.y += v.y;
-  }
-  const double2 v = H.L[size_t(b) * H.KP + i];
-  H.L[size_t(b) * H.KP + i] = make_double2(v.x + s.x, v.y + s.y);
 }
 
 // Stages 3, 5a, 6a: P2QBXL, thread per (centre, source slice):
@@ -1175,7 +990,7 @@ void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 
 
 // ---------------------------------------------------------------- point-and-shoot M2L
-// (default for P <= 20; QBXG_HELM_M2L=split keeps the even / odd dense blocks)
+// (the Helmholtz M2L for P <= 20)
 // In the split M2L's azimuthal frame the operator of offset v' = (rho, 0, z) factors as
 // V(theta) Z(|v'|) W(theta): W rotates the multipole so v' lies on +z, Z translates along
 // z (diagonal in m, one complex (P+1-m)^2 block per m, the same for the even and odd
@@ -1430,13 +1245,6 @@ int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s) {
   return 1;
 }
 
-int helm_shift(const HelmData& H, int mode, const int* boxes, int n, const double2* ops, cudaStream_t s) {
-  if (n == 0) return 0;
-  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
-  k_h_shift<<<n, th, H.KP * sizeof(double2), s>>>(H, mode, boxes, ops);
-  return 1;
-}
-
 int helm_shift_pairs(const HelmData& H, int mode, const int2* pairs, int n, const double2* ops, cudaStream_t s) {
   if (n == 0) return 0;
   constexpr int NB = 8;  // 16 measured slower (fewer CTAs per SM)
@@ -1459,45 +1267,8 @@ int helm_build_ops(const HelmData& H, int n_ops, const double4* shifts, double2*
   return 1;
 }
 
-int helm_m2l(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-             const double2* ops, double2* temp, int n_boxes, const int* boxes, int64_t base, cudaStream_t s) {
-  if (n_tiles == 0) return 0;
-  const size_t smem = size_t(kHCols) * H.KP * sizeof(double2);
-  cudaFuncSetAttribute(k_h_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
-  k_h_m2l<<<n_tiles, th, smem, s>>>(H, tiles, col_src, col_pos, ops, temp);
-  k_h_m2l_reduce<<<n_boxes, th, 0, s>>>(H, boxes, base, temp);
-  return 2;
-}
-
-int helm_m2l_cols() { return kHCols; }
 int helm_m2l_split_cols() { return kHColsS; }
 
-size_t helm_split_op_size(int P) {
-  const size_t NE = size_t(P + 1) * (P + 2) / 2, NO = size_t(P) * (P + 1) / 2;
-  return NE * NE + NO * NO;
-}
-
-int helm_build_split(const HelmData& H, int n_ops, const double4* shifts, double2* ops, double2* cs, cudaStream_t s) {
-  if (n_ops == 0) return 0;
-  const int L = 2 * H.P;
-  const size_t smem = size_t((L + 1) * (L + 1) + L + 1) * sizeof(double2);
-  cudaFuncSetAttribute(k_h_build_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_h_build_split<<<n_ops, 256, smem, s>>>(H, shifts, ops, cs);
-  return 1;
-}
-
-int helm_m2l_split(const HelmData& H, int n_tiles, const int4* tiles, const int* col_src, const int* col_pos,
-                   const double2* ops, const double2* cs, double2* temp, int n_boxes, const int* boxes, int64_t base,
-                   const int* ent_op, cudaStream_t s) {
-  if (n_tiles == 0) return 0;
-  const size_t smem = size_t(kHColsS) * H.KP * sizeof(double2);
-  cudaFuncSetAttribute(k_h_m2l_split, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const int th = H.KP <= 128 ? 128 : H.KP <= 256 ? 256 : 512;
-  k_h_m2l_split<<<n_tiles, th, smem, s>>>(H, tiles, col_src, col_pos, ops, cs, temp);
-  k_h_m2l_reduce_split<<<n_boxes, th, 0, s>>>(H, boxes, base, temp, ent_op, cs);
-  return 2;
-}
 
 bool helm_pas_supported(int P) { return P >= 1 && P <= 20; }
 
@@ -1638,10 +1409,9 @@ int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 
 int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
-  // warp per source (default for P <= 20); QBXG_HELM_P2L=cta keeps one CTA-wide table per source
-  // the double layer takes the CTA-wide table (one more degree for the ladder identities)
-  static const bool cta = std::getenv("QBXG_HELM_P2L") && std::string(std::getenv("QBXG_HELM_P2L")) == "cta";
-  if (!cta && !H.hmu && H.KP <= 32 * kHP2LSlots) {
+  // warp per source (single layer, P <= 20); the double layer takes the CTA-wide table
+  // (one more degree for the ladder identities)
+  if (!H.hmu && H.KP <= 32 * kHP2LSlots) {
     const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
     cudaFuncSetAttribute(k_h_p2l_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k_h_p2l_w<<<n, 256, smem, s>>>(H, boxes);

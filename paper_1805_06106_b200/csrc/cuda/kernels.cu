@@ -137,57 +137,9 @@ __global__ void __launch_bounds__(256) k_p2m(DevData D, const int* __restrict__ 
   for (int c = threadIdx.x; c < D.kp; c += blockDim.x) D.M[size_t(b) * D.kp + c] = acc[c];
 }
 
-// ---------------------------------------------------------------- M2M (Stage 2 postorder)
-// M~_parent(n,m) = 2^-n sum_children sum_{j<=n,k} M~_c(j,k) conj(R_{n-j}^{m-k}(u_oct))
-__device__ __forceinline__ int octant_of(const double4& child, const double4& par) {
-  return (child.x > par.x ? 1 : 0) | (child.y > par.y ? 2 : 0) | (child.z > par.z ? 4 : 0);
-}
+// M2M / L2L (Stages 2, 7) are DMMA GEMMs over octant operators (m2l_gemm.cu); L2QBXL is
+// k_l2qbxl3 (centre_trans.cu).
 
-__global__ void __launch_bounds__(256) k_m2m(DevData D, const int* __restrict__ boxes) {
-  extern __shared__ double2 sm[];
-  double2* Mc = sm;           // kp
-  double2* R = sm + D.kp;     // kp
-  const int b = boxes[blockIdx.x];
-  const double4 pb = D.box[b];
-  double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-  for (int k = D.child_starts[b]; k < D.child_starts[b + 1]; ++k) {
-    const int c = D.children[k];
-    const int o = octant_of(D.box[c], pb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < D.kp; i += blockDim.x) {
-      Mc[i] = D.M[size_t(c) * D.kp + i];
-      R[i] = D.oct_m2m[o * D.kp + i];
-    }
-    __syncthreads();
-    int slot = 0;
-    for (int cidx = threadIdx.x; cidx < D.kp; cidx += blockDim.x, ++slot) {
-      int n, m;
-      idx_nm(cidx, n, m);
-      double sx = 0, sy = 0;
-      for (int j = 0; j <= n; ++j) {
-        const int nj = n - j;
-        for (int kk = -j; kk <= j; ++kk) {
-          const int mk = m - kk;
-          if (mk > nj || mk < -nj) continue;
-          const double2 a = hget(Mc, j, kk);
-          const double2 r = hget(R, nj, mk);
-          // a * conj(r)
-          sx += a.x * r.x + a.y * r.y;
-          sy += a.y * r.x - a.x * r.y;
-        }
-      }
-      acc[slot].x += sx;
-      acc[slot].y += sy;
-    }
-  }
-  int slot = 0;
-  for (int cidx = threadIdx.x; cidx < D.kp; cidx += blockDim.x, ++slot) {
-    int n, m;
-    idx_nm(cidx, n, m);
-    const double s = ldexp(1.0, -n);
-    D.M[size_t(b) * D.kp + cidx] = make_double2(acc[slot].x * s, acc[slot].y * s);
-  }
-}
 
 // ---------------------------------------------------------------- near field (Stages 3, 5a, 6a)
 constexpr int kNearThreads = 128;
@@ -677,44 +629,9 @@ __global__ void __launch_bounds__(kNearThreads) k_near_p2p(DevData D, const int*
 }
 
 
-// ---------------------------------------------------------------- W far (Stage 5b)
-// M2QBXL: L~_c(n,m) += (r/h)^n (1/h)(-1)^{n+m} sum_{j,k} M~_d(j,k) I_{j+n}^{k-m}((c - c_d)/h)
-// M2P:    phi_t += (1/h) sum M~_d(n,m) I_n^m((t - c_d)/h)
-constexpr int kWfarGroup = 8;
+// W far (Stage 5b: M2QBXL, M2P) lives in centre_trans.cu.
 
-__device__ inline double eval_irregular_sum(const double2* M, int P, double x, double y, double z) {
-  // Re sum_{n,|m|<=n} M_n^m I_n^m = sum_n [M_n^0 I_n^0 + 2 sum_{m>0} Re(M_n^m I_n^m)]
-  const double r2 = x * x + y * y + z * z;
-  const double ir2 = 1.0 / r2;
-  double2 imm = make_double2(sqrt(ir2), 0.0);
-  double acc = 0;
-  for (int m = 0; m <= P; ++m) {
-    const double f = m ? 2.0 : 1.0;
-    if (m > 0) {
-      const double s = (2 * m - 1) * ir2;
-      imm = make_double2((imm.x * x - imm.y * y) * s, (imm.x * y + imm.y * x) * s);
-    }
-    double2 a = imm;
-    double2 mm = M[hidx(m, m)];
-    acc += f * (mm.x * a.x - mm.y * a.y);
-    if (m + 1 > P) break;
-    const double s1 = (2 * m + 1) * z * ir2;
-    double2 bb = make_double2(s1 * imm.x, s1 * imm.y);
-    mm = M[hidx(m + 1, m)];
-    acc += f * (mm.x * bb.x - mm.y * bb.y);
-    for (int n = m + 2; n <= P; ++n) {
-      const double c1 = (2 * n - 1) * z;
-      const double c2 = double((n - 1 + m) * (n - 1 - m));
-      const double2 cc = make_double2((c1 * bb.x - c2 * a.x) * ir2, (c1 * bb.y - c2 * a.y) * ir2);
-      mm = M[hidx(n, m)];
-      acc += f * (mm.x * cc.x - mm.y * cc.y);
-      a = bb;
-      bb = cc;
-    }
-  }
-  return acc;
-}
-
+// ---------------------------------------------------------------- evaluation helpers
 __device__ inline double eval_regular_sum(const double2* L, int P, double x, double y, double z) {
   const double r2 = x * x + y * y + z * z;
   double2 rmm = make_double2(1.0, 0.0);
@@ -745,84 +662,6 @@ __device__ inline double eval_regular_sum(const double2* L, int P, double x, dou
   return acc;
 }
 
-__global__ void __launch_bounds__(256) k_wfar(DevData D, const int* __restrict__ boxes) {
-  extern __shared__ double2 sm[];
-  const int ktab = hsize(D.p + D.q);
-  double2* Md = sm;                 // kp
-  double2* T = sm + D.kp;           // kWfarGroup x ktab
-  const int b = boxes[blockIdx.x];
-  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
-  const int ntg = D.tgt_own_count[b], t0 = D.tgt_own_start[b];
-  const int64_t eb = D.wfar_starts[b], ee = D.wfar_starts[b + 1];
-  // centres, in groups of kWfarGroup; thread task (g, output)
-  const int G = min(kWfarGroup, int(blockDim.x) / D.kq);
-  for (int cg = 0; cg < nctr; cg += G) {
-    const int ng = min(G, nctr - cg);
-    const int g = threadIdx.x / D.kq, oc = threadIdx.x % D.kq;
-    const bool active = g < ng;
-    int n = 0, m = 0;
-    idx_nm(oc, n, m);
-    double4 c = make_double4(0, 0, 0, 1);
-    if (g < kWfarGroup && g < ng) c = D.ctr[c0 + cg + g];
-    double ax = 0, ay = 0;
-    for (int64_t e = eb; e < ee; ++e) {
-      const int d = D.wfar_box[e];
-      const double4 bd = D.box[d];
-      const double ih = 1.0 / bd.w;
-      __syncthreads();
-      for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(d) * D.kp + i];
-      // column-parallel irregular tables of (c - c_d)/h for each centre of the group
-      const int ncol = D.p + D.q + 1;
-      for (int t = threadIdx.x; t < ng * ncol; t += blockDim.x) {
-        const int gg = t / ncol, mm = t % ncol;
-        const double4 cx = D.ctr[c0 + cg + gg];
-        double2 col[kMaxOrder + 1];
-        irregular_column((cx.x - bd.x) * ih, (cx.y - bd.y) * ih, (cx.z - bd.z) * ih, mm, D.p + D.q, col);
-        double2* Tg = T + gg * ktab;
-        for (int nn = mm; nn <= D.p + D.q; ++nn) Tg[hidx(nn, mm)] = col[nn - mm];
-      }
-      __syncthreads();
-      if (active) {
-        const double2* Tg = T + g * ktab;
-        double sx = 0, sy = 0;
-        for (int j = 0; j <= D.p; ++j)
-          for (int k = -j; k <= j; ++k) {
-            const double2 a = hget(Md, j, k);
-            const double2 t = hget(Tg, j + n, k - m);
-            sx += a.x * t.x - a.y * t.y;
-            sy += a.x * t.y + a.y * t.x;
-          }
-        const double s = (((n + m) & 1) ? -1.0 : 1.0) * ipow(c.w * ih, n) * ih;
-        ax += s * sx;
-        ay += s * sy;
-      }
-    }
-    if (active) {
-      double2* out = D.Lc + size_t(c0 + cg + g) * D.kq + oc;
-      double2 v = *out;
-      v.x += ax;
-      v.y += ay;
-      *out = v;
-    }
-  }
-  // conventional targets: thread per target
-  for (int tc = 0; tc < ntg; tc += blockDim.x) {
-    const int ti = tc + threadIdx.x;
-    double acc = 0;
-    double4 t = make_double4(0, 0, 0, 0);
-    if (ti < ntg) t = D.tgt[t0 + ti];
-    for (int64_t e = eb; e < ee; ++e) {
-      const int d = D.wfar_box[e];
-      const double4 bd = D.box[d];
-      const double ih = 1.0 / bd.w;
-      __syncthreads();
-      for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Md[i] = D.M[size_t(d) * D.kp + i];
-      __syncthreads();
-      if (ti < ntg) acc += ih * eval_irregular_sum(Md, D.p, (t.x - bd.x) * ih, (t.y - bd.y) * ih, (t.z - bd.z) * ih);
-    }
-    if (ti < ntg) D.phi[t0 + ti] += acc;
-  }
-}
 
 // ---------------------------------------------------------------- P2L (Stage 6b)
 // L~_b += (1/h)[w conj(I(u)) + conj(mu . grad I(u))/h], u = (s - c_b)/h, sources of X_far boxes
@@ -1066,94 +905,6 @@ __global__ void __launch_bounds__(128, P >= 12 ? 4 : 1) k_p2l3(DevData D, const 
     v.x += sx * ih;
     v.y += sy * ih;
     D.L[size_t(b) * D.kp + c] = v;
-  }
-}
-
-// ---------------------------------------------------------------- L2L (Stage 7)
-// L~_child(n,m) += 2^-n sum_{j>=n,k} L~_parent(j,k) R_{j-n}^{k-m}(u_oct/2)
-__global__ void __launch_bounds__(256) k_l2l(DevData D, const int* __restrict__ boxes) {
-  extern __shared__ double2 sm[];
-  double2* Lp = sm;
-  double2* R = sm + D.kp;
-  const int b = boxes[blockIdx.x];
-  const int a = D.parent[b];
-  const int o = octant_of(D.box[b], D.box[a]);
-  for (int i = threadIdx.x; i < D.kp; i += blockDim.x) {
-    Lp[i] = D.L[size_t(a) * D.kp + i];
-    R[i] = D.oct_l2l[o * D.kp + i];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < D.kp; c += blockDim.x) {
-    int n, m;
-    idx_nm(c, n, m);
-    double sx = 0, sy = 0;
-    for (int j = n; j <= D.p; ++j) {
-      const int jn = j - n;
-      for (int k = -j; k <= j; ++k) {
-        const int km = k - m;
-        if (km > jn || km < -jn) continue;
-        const double2 l = hget(Lp, j, k);
-        const double2 r = hget(R, jn, km);
-        sx += l.x * r.x - l.y * r.y;
-        sy += l.x * r.y + l.y * r.x;
-      }
-    }
-    const double s = ldexp(1.0, -n);
-    double2 v = D.L[size_t(b) * D.kp + c];
-    v.x += s * sx;
-    v.y += s * sy;
-    D.L[size_t(b) * D.kp + c] = v;
-  }
-}
-
-// ---------------------------------------------------------------- L2QBXL (Stage 8)
-// L~_c(n,m) += (r/h)^n sum_{j>=n,k} L~_b(j,k) R_{j-n}^{k-m}((c - c_b)/h)
-__global__ void __launch_bounds__(256) k_l2qbxl(DevData D, const int* __restrict__ boxes) {
-  extern __shared__ double2 sm[];
-  double2* Lb = sm;          // kp
-  double2* T = sm + D.kp;    // kWfarGroup x kp
-  const int b = boxes[blockIdx.x];
-  const double4 bc = D.box[b];
-  const double ih = 1.0 / bc.w;
-  const int nctr = D.ctr_own_count[b], c0 = D.ctr_own_start[b];
-  for (int i = threadIdx.x; i < D.kp; i += blockDim.x) Lb[i] = D.L[size_t(b) * D.kp + i];
-  const int G = min(kWfarGroup, int(blockDim.x) / D.kq);
-  for (int cg = 0; cg < nctr; cg += G) {
-    const int ng = min(G, nctr - cg);
-    __syncthreads();
-    for (int t = threadIdx.x; t < ng * (D.p + 1); t += blockDim.x) {
-      const int gg = t / (D.p + 1), mm = t % (D.p + 1);
-      const double4 cx = D.ctr[c0 + cg + gg];
-      double2 col[kMaxOrder + 1];
-      regular_column((cx.x - bc.x) * ih, (cx.y - bc.y) * ih, (cx.z - bc.z) * ih, mm, D.p, col);
-      for (int nn = mm; nn <= D.p; ++nn) T[gg * D.kp + hidx(nn, mm)] = col[nn - mm];
-    }
-    __syncthreads();
-    const int g = threadIdx.x / D.kq, oc = threadIdx.x % D.kq;
-    if (g < ng) {
-      int n, m;
-      idx_nm(oc, n, m);
-      const double4 c = D.ctr[c0 + cg + g];
-      const double2* Tg = T + g * D.kp;
-      double sx = 0, sy = 0;
-      for (int j = n; j <= D.p; ++j) {
-        const int jn = j - n;
-        for (int k = -j; k <= j; ++k) {
-          const int km = k - m;
-          if (km > jn || km < -jn) continue;
-          const double2 l = hget(Lb, j, k);
-          const double2 r = hget(Tg, jn, km);
-          sx += l.x * r.x - l.y * r.y;
-          sy += l.x * r.y + l.y * r.x;
-        }
-      }
-      const double s = ipow(c.w * ih, n);
-      double2* out = D.Lc + size_t(c0 + cg + g) * D.kq + oc;
-      double2 v = *out;
-      v.x += s * sx;
-      v.y += s * sy;
-      *out = v;
-    }
   }
 }
 
@@ -1433,11 +1184,6 @@ int launch_p2m(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-int launch_m2m(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (n == 0) return 0;
-  k_m2m<<<n, block_for(D.kp), 2 * D.kp * sizeof(double2), s>>>(D, boxes);
-  return 1;
-}
 
 int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
@@ -1500,17 +1246,10 @@ int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (n == 0) return 0;
-  const size_t smem = (D.kp + kWfarGroup * hsize(D.p + D.q)) * sizeof(double2);
-  k_wfar<<<n, 256, smem, s>>>(D, boxes);
-  return 1;
-}
 
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   if (n == 0) return 0;
-  static const bool legacy = std::getenv("QBXG_P2L_LEGACY") != nullptr;
-  if (!legacy) {
+  {  // column-pair lanes for the orders it is instantiated for; the generic kernel otherwise
 #define QBXG_P2L3(PP)                                           \
   if (D.p == PP) {                                              \
     if (D.dipole)                                               \
@@ -1531,18 +1270,7 @@ int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
   return 1;
 }
 
-int launch_l2l(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (n == 0) return 0;
-  k_l2l<<<n, block_for(D.kp), 2 * D.kp * sizeof(double2), s>>>(D, boxes);
-  return 1;
-}
 
-int launch_l2qbxl(const DevData& D, const int* boxes, int n, cudaStream_t s) {
-  if (n == 0) return 0;
-  const size_t smem = (D.kp + kWfarGroup * D.kp) * sizeof(double2);
-  k_l2qbxl<<<n, 256, smem, s>>>(D, boxes);
-  return 1;
-}
 
 int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
                 const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
@@ -1612,11 +1340,7 @@ void set_smem_limits() {
   if (done) return;
   const int lim = 200 * 1024;
   cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaFuncSetAttribute(k_wfar, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  cudaFuncSetAttribute(k_l2qbxl, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   done = true;
 }
 

@@ -142,13 +142,9 @@ int launch_gather_batch(const DevData& D, int ns, int R, const int* perm, const 
 int near_batch_width(int q);
 int launch_near_qbx_batch(const DevData& D, const int* boxes, int n, int NR, const double* bw, const double4* bmu,
                           int64_t ns, double2* bLc, int64_t nc, cudaStream_t s);
-int launch_m2m(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_qbx(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_near_p2p(const DevData& D, const int* boxes, int n, cudaStream_t s);
-int launch_wfar(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_p2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
-int launch_l2l(const DevData& D, const int* boxes, int n, cudaStream_t s);
-int launch_l2qbxl(const DevData& D, const int* boxes, int n, cudaStream_t s);
 int launch_eval(const DevData& D, int n_assoc, const int* assoc_items, const double* tpos, const int* assoc,
                 const int* ctr_sorted, int n_conv, const int* conv_items, const int* tgt_perm, const int* tgt_box,
                 double* pot, cudaStream_t s);

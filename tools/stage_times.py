@@ -1,8 +1,7 @@
 """Per-stage CUDA-event times of a device-resident apply (near field on the main
-stream unless QBXG_OVERLAP is set), for A/B runs of kernel variants selected by
-QBXG_* environment switches.
+stream unless QBXG_OVERLAP is set).
 
-    QBXG_PAS_MAP=0 python tools/stage_times.py [config] [n_applies]
+    python tools/stage_times.py [config] [n_applies]
 """
 import json
 import os
