@@ -15,7 +15,7 @@
 // azimuthal blocks.  W, Z and V depend on (rho_xy^2, dz) only: the 1,206 offsets of
 // [-5,5]^3 fall into 190 classes, one operator set per class (~19 MB at p = 15).
 //
-// Work split (target-grouped).  One CTA owns a group of G target boxes (32 at p <= 16,
+// Work split (target-grouped).  One CTA owns a group of G target boxes (48 at p <= 16,
 // consecutive in DFS order) and walks a host-built list of tiles: a tile is <= BN
 // List-2 entries of the group that share an operator class, columns sorted by
 // (target slot, offset).  Two CTAs of 8 warps share an SM (one CTA's gather, barriers
@@ -80,7 +80,7 @@ template <int P>
 struct Tg {
   static constexpr int NR = hsize(P), NROW = (P + 1) * (P + 1), KP2 = 2 * NR;
   static constexpr int KA = (NR + 31) / 32;                // coefficients per lane in the accumulate
-  static constexpr int TPW = 32 / KA < 4 ? 32 / KA : 4;    // target boxes per warp
+  static constexpr int TPW = 32 / KA < 6 ? 32 / KA : 6;    // target boxes per warp
   static constexpr int G = kWarps * TPW;                   // target boxes per CTA
   static constexpr int TW = 4 * KA;                        // TMEM words (columns) per target per lane
   // TMEM: warps w, w + 4 share lane quadrant w % 4, each its own column range
