@@ -57,6 +57,7 @@ namespace {
 
 constexpr int kPasPhases = 3;
 constexpr int kWarps = 8, kNTh = kWarps * 32;  // two CTAs per SM
+constexpr int kGat = 4;                        // multipole loads in flight per thread (gather)
 constexpr size_t kSmemMax = 232448 / 2 - 2048;  // two CTAs per SM (sm_100: 228 KB), less static
 
 // per-phase operator size bound (doubles): blocks of sizes 1..p+1 (Re) and 1..p (Im),
@@ -279,15 +280,15 @@ __global__ void __launch_bounds__(kNTh, 2)
     const int mb = it % 3, mb1 = (it + 1) % 3, mb2 = (it + 2) % 3, cb = it & 1;
     const int* sm = s_meta + mb * BN;
     const double2* sc = s_cs + cb * BN * (P + 1);
-    {  // 1. multipoles straight from L2, rotated by e^{i k alpha} into X; four loads in
+    {  // 1. multipoles straight from L2, rotated by e^{i k alpha} into X; kGat loads in
        // flight per thread
       const int ne = ncols * NR;
       const int* src = s_msrc + mb * BN;
 #pragma unroll 1
-      for (int e0 = tid; e0 < ne; e0 += 4 * kNTh) {
-        double2 v[4];
+      for (int e0 = tid; e0 < ne; e0 += kGat * kNTh) {
+        double2 v[kGat];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kGat; ++u) {
           const int e = e0 + u * kNTh;
           if (e < ne) {
             const int c = e / NR;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kNTh, 2)
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kGat; ++u) {
           const int e = e0 + u * kNTh;
           if (e < ne) {
             const int c = e / NR, q = e - c * NR;
