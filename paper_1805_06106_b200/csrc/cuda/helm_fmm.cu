@@ -659,13 +659,15 @@ __global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict
   }
 }
 
-// P2L (List 4 far), one source per warp: lane 0 forms the radial table, lanes 0..P the
+// P2M (own sources of a leaf, regular j_n) and P2L (List 4 far, singular h_n), one
+// source per warp: lane 0 forms the radial table, lanes 0..P the
 // solid-harmonic columns m >= 0 (Cartesian recurrences), then every lane adds its
 // ceil(KP/32) coefficients f h_n conj(Y_n^m) -- the negative orders read the m >= 0
 // column (Y^{-m} = conj(Y^m)).  8 sources in flight per CTA instead of one CTA-wide
 // table per source; the warps' partial sums are added in warp order (deterministic).
 constexpr int kHP2LSlots = 14;  // ceil(441 / 32): P <= 20
-__global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __restrict__ boxes) {
+template <bool P2M>
+__global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restrict__ boxes) {
   extern __shared__ double2 smw[];
   const int P = H.P, KP = H.KP, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
   double2* T = smw + warp * (KP + P + 1);
@@ -685,18 +687,30 @@ __global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __res
       code[sl] = fi(n, m < 0 ? -m : m) | n << 16 | (m < 0 ? 1 << 30 : 0);
     }
   }
-  const int64_t sb = H.xfar_starts[b], se = H.xfar_starts[b + 1];
+  // sources: P2M the leaf's own (one segment), P2L its List-4-far segments; warp w takes
+  // flat sources w, w + NW, ...
+  int64_t sb, se;
+  if (P2M) {
+    sb = 0;
+    se = H.src_own_count[b] > 0 ? 1 : 0;
+  } else {
+    sb = H.xfar_starts[b];
+    se = H.xfar_starts[b + 1];
+  }
+  auto seg_at = [&](int64_t kk) {
+    return P2M ? make_int2(H.src_own_start[b], H.src_own_count[b]) : H.xfar_seg[kk];
+  };
   int64_t k = sb;
   int off = warp, st = 0, cnt = 0;
   if (k < se) {
-    st = H.xfar_seg[k].x;
-    cnt = H.xfar_seg[k].y;
+    st = seg_at(k).x;
+    cnt = seg_at(k).y;
   }
   while (k < se && off >= cnt) {
     off -= cnt;
     if (++k < se) {
-      st = H.xfar_seg[k].x;
-      cnt = H.xfar_seg[k].y;
+      st = seg_at(k).x;
+      cnt = seg_at(k).y;
     }
   }
   while (k < se) {
@@ -704,7 +718,7 @@ __global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __res
     const double4 x = H.src[src];
     const double2 w = H.hw[src];
     const double tx = x.x - bc.x, ty = x.y - bc.y, tz = x.z - bc.z, r2 = tx * tx + ty * ty + tz * tz;
-    if (lane == 0) radial_table(H.k, sqrt(r2), P, true, rad);
+    if (lane == 0) radial_table(H.k, sqrt(r2), P, !P2M, rad);  // h_n / r^n (P2L), j_n / r^n (P2M)
     if (lane <= P) {  // column m = lane of S_n^m(t), n = m..P
       const int m = lane;
       double2 d = make_double2(0.28209479177387814347, 0.0);
@@ -738,8 +752,8 @@ __global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __res
     while (k < se && off >= cnt) {
       off -= cnt;
       if (++k < se) {
-        st = H.xfar_seg[k].x;
-        cnt = H.xfar_seg[k].y;
+        st = seg_at(k).x;
+        cnt = seg_at(k).y;
       }
     }
   }
@@ -755,8 +769,9 @@ __global__ void __launch_bounds__(256, 2) k_h_p2l_w(HelmData H, const int* __res
       sx += red[ww * KP + i].x;
       sy += red[ww * KP + i].y;
     }
-    const double2 v = H.L[size_t(b) * KP + i];
-    H.L[size_t(b) * KP + i] = make_double2(v.x + sx, v.y + sy);
+    double2* out = (P2M ? H.M : H.L) + size_t(b) * KP + i;
+    const double2 v = *out;
+    *out = make_double2(v.x + sx, v.y + sy);
   }
 }
 
@@ -1240,6 +1255,12 @@ int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w,
 
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s) {
   if (n == 0) return 0;
+  if (!H.hmu && H.KP <= 32 * kHP2LSlots) {  // single layer: one source per warp
+    const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
+    cudaFuncSetAttribute(k_h_p2w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_h_p2w<true><<<n, 256, smem, s>>>(H, leaves);
+    return 1;
+  }
   const int PF = H.hmu ? H.P + 1 : H.P;
   k_h_p2m<<<n, 256, ((PF + 1) * (PF + 1) + PF + 1) * sizeof(double2), s>>>(H, leaves);
   return 1;
@@ -1413,8 +1434,8 @@ int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   // (one more degree for the ladder identities)
   if (!H.hmu && H.KP <= 32 * kHP2LSlots) {
     const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
-    cudaFuncSetAttribute(k_h_p2l_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k_h_p2l_w<<<n, 256, smem, s>>>(H, boxes);
+    cudaFuncSetAttribute(k_h_p2w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_h_p2w<false><<<n, 256, smem, s>>>(H, boxes);
     return 1;
   }
   const int PF = H.hmu ? H.P + 1 : H.P;

@@ -299,3 +299,26 @@ def test_gpu_helmholtz_double_layer_fmm_matches_oracle(cfgid, kw, p, q):
     assert np.linalg.norm(pot - ref) / np.linalg.norm(ref) <= 1e-11
     assert np.linalg.norm(cc - cref) / np.linalg.norm(cref) <= 1e-11
     assert np.array_equal(pot, again), "Helmholtz SL+DL apply is not bitwise deterministic"
+
+
+@pytest.mark.gpu
+def test_gpu_helmholtz_double_layer_p20_matches_oracle_fixture():
+    """Helmholtz SL+DL (kernel 3, Brakhage-Werner) at BASELINE config 3's orders (p = 20,
+    q = 5, k = 3) against the oracle via tests/golden/oracle_helm_p20_dl.npz
+    (tests/golden/make_helm_p20_dl.py regenerates it); same procedural inputs and plan,
+    checked by the list hashes."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    import make_helm_p20_dl as M
+    fx = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_helm_p20_dl.npz"))
+    g, ws, mu, cfg = M.inputs()
+    assert np.array_equal(ws, fx["weights"]) and np.array_equal(mu, fx["dipoles"])
+    plan = api.Plan(cfg, g)
+    hashes = np.array([plan.list_hashes()[k] for k in sorted(plan.list_hashes())], dtype=np.uint64)
+    assert np.array_equal(hashes, fx["list_hashes"])
+    eng = api.FmmEngine(cfg, g, plan)
+    pot, cc = eng.apply_complex(ws, mu, want_centers=True)
+    eng.close()
+    assert np.linalg.norm(pot - fx["pot"]) / np.linalg.norm(fx["pot"]) <= 1e-11
+    assert np.linalg.norm(cc[:64] - fx["centres"]) / np.linalg.norm(fx["centres"]) <= 1e-11
