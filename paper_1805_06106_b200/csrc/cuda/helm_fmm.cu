@@ -814,7 +814,10 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
     // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu} over the used
     // terms only: l >= |mu| and n + n' + l even
     const int NLm = NL - amu;
-    for (int e = threadIdx.x; e < ns * KQ * NLm; e += blockDim.x) {
+    // the last warp forms the centres' F columns (a recurrence in l per centre) while the
+    // other warps contract C_mu, so the column recurrence is off the critical path
+    const int nth_c = blockDim.x - 32;
+    for (int e = threadIdx.x; threadIdx.x < nth_c && e < ns * KQ * NLm; e += nth_c) {
       const int sg = e / (KQ * NLm), er = e - sg * KQ * NLm;
       const int iout = er / NLm, l = amu + er % NLm, mu = sg ? -amu : amu;
       double2 cacc = make_double2(0, 0);
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
       Cm[(sg * KQ + iout) * NL + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
     }
     // F columns per centre: (rad_l / r^l) S_l^{+-|mu|}(t), l = |mu|..L
-    for (int j = threadIdx.x; j < nctr; j += blockDim.x) {
+    for (int j = int(threadIdx.x) - nth_c; j >= 0 && j < nctr; j += 32) {
       double2* colp = Fc + j * NL;
       double2* colm = Fc + (kHCtrMax + j) * NL;
       solid_column(amu, L, geo[4 * j], geo[4 * j + 1], geo[4 * j + 2], geo[4 * j + 3], colp);
