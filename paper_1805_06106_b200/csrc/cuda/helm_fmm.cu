@@ -46,6 +46,10 @@ __device__ __forceinline__ void nm_of(int i, int& n, int& m) {
 constexpr int kHSolid = 42;  // degrees covered: operator tables need 2p (p <= 20) + 1
 __constant__ double c_sa[kHSolid + 1], c_sb[kHSolid + 1];
 __constant__ double c_sc[(kHSolid + 1) * (kHSolid + 1)], c_sd[(kHSolid + 1) * (kHSolid + 1)];
+// the same tables in global memory, for loops whose lanes index different orders m (the
+// constant cache serialises divergent addresses; these go through L1 coalesced)
+__device__ double g_sa[kHSolid + 1], g_sb[kHSolid + 1];
+__device__ double g_sc[(kHSolid + 1) * (kHSolid + 1)], g_sd[(kHSolid + 1) * (kHSolid + 1)];
 
 // j_n(k r) / r^n and y_n(k r) / r^n for n <= Q without divisions in the loops:
 //   Jt_n = j_n / r^n:  series for Jt_Q, Jt_{Q+1} (x < 1), then Jt_{n-1} = (2n+1)/k Jt_n - r^2 Jt_{n+1}
@@ -190,13 +194,13 @@ __device__ void wave_table_cta(double k, int P, double tx, double ty, double tz,
     // column m into F[fi(n, m)] (n = m..P), mirrored to -m
     double2 d = make_double2(0.28209479177387814347, 0.0);
     for (int i = 1; i <= m; ++i)
-      d = make_double2(c_sa[i] * (d.x * tx - d.y * ty), c_sa[i] * (d.x * ty + d.y * tx));
+      d = make_double2(g_sa[i] * (d.x * tx - d.y * ty), g_sa[i] * (d.x * ty + d.y * tx));
     F[fi(m, m)] = d;
     if (m + 1 <= P) {
-      double2 a = d, b = make_double2(c_sb[m] * tz * d.x, c_sb[m] * tz * d.y);
+      double2 a = d, b = make_double2(g_sb[m] * tz * d.x, g_sb[m] * tz * d.y);
       F[fi(m + 1, m)] = b;
       for (int n = m + 2; n <= P; ++n) {
-        const double cn = c_sc[n * (kHSolid + 1) + m], dn = c_sd[n * (kHSolid + 1) + m] * r2;
+        const double cn = g_sc[n * (kHSolid + 1) + m], dn = g_sd[n * (kHSolid + 1) + m] * r2;
         const double2 c2 = make_double2(cn * (tz * b.x - dn * a.x), cn * (tz * b.y - dn * a.y));
         F[fi(n, m)] = c2;
         a = b;
@@ -723,13 +727,13 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
       const int m = lane;
       double2 d = make_double2(0.28209479177387814347, 0.0);
       for (int i = 1; i <= m; ++i)
-        d = make_double2(c_sa[i] * (d.x * tx - d.y * ty), c_sa[i] * (d.x * ty + d.y * tx));
+        d = make_double2(g_sa[i] * (d.x * tx - d.y * ty), g_sa[i] * (d.x * ty + d.y * tx));
       T[fi(m, m)] = d;
       if (m + 1 <= P) {
-        double2 a = d, bb = make_double2(c_sb[m] * tz * d.x, c_sb[m] * tz * d.y);
+        double2 a = d, bb = make_double2(g_sb[m] * tz * d.x, g_sb[m] * tz * d.y);
         T[fi(m + 1, m)] = bb;
         for (int n = m + 2; n <= P; ++n) {
-          const double cn = c_sc[n * (kHSolid + 1) + m], dn = c_sd[n * (kHSolid + 1) + m] * r2;
+          const double cn = g_sc[n * (kHSolid + 1) + m], dn = g_sd[n * (kHSolid + 1) + m] * r2;
           const double2 c2 = make_double2(cn * (tz * bb.x - dn * a.x), cn * (tz * bb.y - dn * a.y));
           T[fi(n, m)] = c2;
           a = bb;
@@ -1248,6 +1252,10 @@ void helm_upload_constants() {
   cudaMemcpyToSymbol(c_sb, sb, sizeof(sb));
   cudaMemcpyToSymbol(c_sc, sc, sizeof(sc));
   cudaMemcpyToSymbol(c_sd, sd, sizeof(sd));
+  cudaMemcpyToSymbol(g_sa, sa, sizeof(sa));
+  cudaMemcpyToSymbol(g_sb, sb, sizeof(sb));
+  cudaMemcpyToSymbol(g_sc, sc, sizeof(sc));
+  cudaMemcpyToSymbol(g_sd, sd, sizeof(sd));
 }
 
 int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w, const double* mu, cudaStream_t s) {
