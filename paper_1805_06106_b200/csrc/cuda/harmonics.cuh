@@ -28,6 +28,9 @@ __host__ __device__ constexpr int hsize(int p) { return (p + 1) * (p + 2) / 2; }
 // Without -rdc every translation unit owns its copy: each TU that calls a
 // regular_* helper must call upload_inv_nm() (host) before launching.
 __constant__ double c_inv_nm[hsize(kMaxOrder)];
+// the same table in global memory, for loops whose lanes index different orders m (the
+// constant cache serialises divergent addresses)
+__device__ double g_inv_nm[hsize(kMaxOrder)];
 
 static inline void upload_inv_nm() {
   static bool done = false;  // per translation unit
@@ -36,6 +39,7 @@ static inline void upload_inv_nm() {
   for (int n = 0; n <= kMaxOrder; ++n)
     for (int m = 0; m <= n; ++m) h[hidx(n, m)] = (n >= m + 2) ? 1.0 / double((n - m) * (n + m)) : 0.0;
   cudaMemcpyToSymbol(c_inv_nm, h, sizeof(h));
+  cudaMemcpyToSymbol(g_inv_nm, h, sizeof(h));
   done = true;
 }
 

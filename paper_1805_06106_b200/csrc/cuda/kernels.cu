@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_p2m(DevData D, const int* __restrict__ 
         double2 a = rmm, b = make_double2(uz * rmm.x, uz * rmm.y);
         T[hidx(m + 1, m)] = b;
         for (int n = m + 2; n <= D.p; ++n) {
-          const double f = c_inv_nm[hidx(n, m)];
+          const double f = g_inv_nm[hidx(n, m)];  // lanes differ in m
           const double c1 = (2 * n - 1) * uz;
           const double2 c = make_double2((c1 * b.x - r2 * a.x) * f, (c1 * b.y - r2 * a.y) * f);
           T[hidx(n, m)] = c;
@@ -650,7 +650,7 @@ __device__ inline double eval_regular_sum(const double2* L, int P, double x, dou
     ll = L[hidx(m + 1, m)];
     acc += f * (ll.x * bb.x - ll.y * bb.y);
     for (int n = m + 2; n <= P; ++n) {
-      const double fi = c_inv_nm[hidx(n, m)];
+      const double fi = g_inv_nm[hidx(n, m)];
       const double c1 = (2 * n - 1) * z;
       const double2 cc = make_double2((c1 * bb.x - r2 * a.x) * fi, (c1 * bb.y - r2 * a.y) * fi);
       ll = L[hidx(n, m)];
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(256) k_p2l(DevData D, const int* __restrict__ 
 // w = (ux + i uy)/r^2, are computed by the 8 lanes of a slice (repeated squaring)
 // and shared through shared memory.  Slices are summed in fixed order.
 constexpr int kP3Slices = 16;
-__constant__ double c_dfact[22] = {
+__device__ double c_dfact[22] = {  // global, not __constant__: lanes index different entries
     1, 1, 3, 15, 105, 945, 10395, 135135, 2027025, 34459425, 654729075, 13749310575, 316234143225,
     7905853580625, 213458046676875, 6190283353629375, 1.9189878396251062e+17, 6.3326598707628503e+18,
     2.2164309547669976e+20, 8.2007945326378919e+21, 3.1983098677287775e+23, 1.3113070457687988e+25};
