@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(kNTh, 2)
         }
 #pragma unroll
         for (int k = 0; k < KA; ++k) tm_st4(tm + (u * KA + k) * 4, are[k], aim[k]);
-        tm_wait_st();
       }
+      tm_wait_st();  // each run wrote a different target's columns; one wait for all
     }
     cp_async_wait_all();  // next tiles' metadata landed
     __syncthreads();      // X and this tile's buffers free
