@@ -54,8 +54,8 @@ def test_urchin_array_sl_dl():
     _check(api.config_geometry(4, variant=8, level=1), api.config_fmm(4), True)
 
 
-@pytest.mark.parametrize("p,q,nmax,tf", [(4, 2, 16, 0.9), (8, 4, 32, 0.5), (20, 5, 64, 0.9), (12, 8, 48, 0.7), (17, 4, 64, 0.9),
-                                          (21, 3, 64, 0.9)])
+@pytest.mark.parametrize("p,q,nmax,tf", [(2, 2, 16, 0.9), (3, 1, 24, 0.9), (4, 2, 16, 0.9), (8, 4, 32, 0.5), (20, 5, 64, 0.9),
+                                          (12, 8, 48, 0.7), (17, 4, 64, 0.9), (21, 3, 64, 0.9)])
 def test_orders_and_tree_params(p, q, nmax, tf):
     """Covers every M2L tile shape: p <= 15 (32 columns, operators staged by TMA, 32
     targets per CTA), p = 17 (operators from L2, 16 targets per CTA), p >= 20 (16
