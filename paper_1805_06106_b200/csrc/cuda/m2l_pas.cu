@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kNTh, 2)
       const int* wblk = woff + kWarps + 1;
 #define QBXG_PAS_CASE(S) \
   case S:                \
-    if (S <= 2 * P + 2 && S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
+    if (S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
     break;
 #pragma unroll 1
       for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
@@ -438,6 +438,8 @@ std::vector<std::vector<int>> merge_subblocks(const std::vector<SubBlock>& sb) {
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sb[a].rows.size() > sb[b].rows.size(); });
   std::vector<char> used(sb.size(), 0);
   std::vector<std::vector<int>> groups;
+  // (merged sizes may exceed 2p + 2 when several small blocks chain: every size up to
+  // kMaxBlock is instantiated)
   for (int i : order) {
     if (used[i]) continue;
     used[i] = 1;

@@ -54,12 +54,12 @@ def test_urchin_array_sl_dl():
     _check(api.config_geometry(4, variant=8, level=1), api.config_fmm(4), True)
 
 
-@pytest.mark.parametrize("p,q,nmax,tf", [(2, 2, 16, 0.9), (3, 1, 24, 0.9), (4, 2, 16, 0.9), (8, 4, 32, 0.5), (20, 5, 64, 0.9),
+@pytest.mark.parametrize("p,q,nmax,tf", [(1, 1, 16, 0.9), (2, 2, 16, 0.9), (3, 1, 24, 0.9), (4, 2, 16, 0.9), (8, 4, 32, 0.5), (20, 5, 64, 0.9),
                                           (12, 8, 48, 0.7), (17, 4, 64, 0.9), (21, 3, 64, 0.9)])
 def test_orders_and_tree_params(p, q, nmax, tf):
-    """Covers every M2L tile shape: p <= 15 (32 columns, operators staged by TMA, 32
-    targets per CTA), p = 17 (operators from L2, 16 targets per CTA), p >= 20 (16
-    columns)."""
+    """Covers every M2L tile shape: p <= 16 (32 columns, 48 targets per CTA), p >= 17
+    (fewer targets per CTA as the TMEM accumulators grow), p >= 18 (16 columns), and the
+    smallest orders, where merged blocks are longer than 2p + 2."""
     g = api.config_geometry(2, level=1, n_volume_targets=500)
     _check(g, api.FmmConfig(p_fmm=p, p_qbx=q, n_max=nmax, t_f=tf, kernel=1), True)
 

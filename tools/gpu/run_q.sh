@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 180 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_q.log 2>&1
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_q.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/smoke_q.log
 grep -q "smoke rc=0" gpurun_out/smoke_q.log || exit 1
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_shard.py tests/test_gpu_errors.py -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_q.log 2>&1
