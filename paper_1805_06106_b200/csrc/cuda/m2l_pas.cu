@@ -55,9 +55,15 @@ namespace dev {
 
 namespace {
 
+#ifndef QBXG_M2L_PREFETCH
+#define QBXG_M2L_PREFETCH 0  // measured: 44.8 ms with, 40.8 ms without (config 1)
+#endif
 constexpr int kPasPhases = 3;
 constexpr int kWarps = 8, kNTh = kWarps * 32;  // two CTAs per SM
-constexpr int kGat = 4;                        // multipole loads in flight per thread (gather)
+#ifndef QBXG_M2L_GATCOLS
+#define QBXG_M2L_GATCOLS 1  // measured at config 1: 1 -> 36.1 ms, 2 -> 41.8 (spills), 3 -> 49.0; flat 4-deep gather 40.8
+#endif
+constexpr int kGatCols = QBXG_M2L_GATCOLS;       // columns a warp gathers at a time (KA loads each in flight per lane)
 constexpr size_t kSmemMax = 232448 / 2 - 2048;  // two CTAs per SM (sm_100: 228 KB), less static
 
 // per-phase operator size bound (doubles): blocks of sizes 1..p+1 (Re) and 1..p (Im),
@@ -95,6 +101,9 @@ struct Tg {
            + size_t(tab_ints(P)) * 4;             // block table
   }
   static constexpr int BN = bytes(32) <= kSmemMax ? 32 : 16;  // tile columns
+  // operator fragments of a block held in registers one block ahead: merged blocks are
+  // <= 16 rows for P <= 15 (8 fragments; make_layout checks); larger orders load in place
+  static constexpr int NF = (QBXG_M2L_PREFETCH && P <= 15) ? 8 : 1;
   static constexpr size_t SMEM = bytes(BN);
 };
 
@@ -155,14 +164,18 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 // then per 8-column tile j < nt the block's rows as B fragments from X (padding rows
 // k >= S read the zero row), the DMMAs, and the rows written back.  Tile j's reads
 // feed its DMMAs, which precede its writes; other tiles touch other columns.
-template <int S, int BN, int ZR>
-__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, int lane, int nt) {
+template <int S, int BN, int ZR, int NF>
+__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, const double (&af)[NF],
+                                          int lane, int nt) {
   constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4;
   double a[MT][KS];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
+    for (int ks = 0; ks < KS; ++ks) {
+      if constexpr (NF >= MT * KS) a[mt][ks] = af[mt * KS + ks];  // fetched while the previous block ran
+      else a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
+    }
   int rb[KS], ro[MT];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
@@ -264,6 +277,45 @@ __global__ void __launch_bounds__(kNTh, 2)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (t_begin < t_end) load_cs(tl.z, 0, 0);
+  // lane l owns the half-table coefficients q = l + 32 k in the gather and the accumulate:
+  // X row offset | swizzle << 16 (| m << 20) of their Re and Im rows (Im of m = 0: zero row)
+  int q_re[KA], q_im[KA];
+#pragma unroll
+  for (int k = 0; k < KA; ++k) {
+    const int q = lane + 32 * k;
+    const int code = q < NR ? s_code[q] : (NROW | NROW << 10);
+    const int re = code & 1023, im = (code >> 10) & 1023;
+    q_re[k] = re * BN | swz(re) << 16 | (code >> 20) << 20;
+    q_im[k] = im * BN | swz(im) << 16;
+  }
+  // this warp's blocks per phase, and the fragment fetch of one of them
+  constexpr int NF = C::NF;
+  int w_lo[kPasPhases], w_hi[kPasPhases], first_ph = kPasPhases;
+#pragma unroll
+  for (int ph = kPasPhases - 1; ph >= 0; --ph) {
+    const int* T = s_tab + hd.base[ph];
+    const int* woff = T + 1 + 2 * T[0] + 1 + NROW;
+    w_lo[ph] = woff[warp];
+    w_hi[ph] = woff[warp + 1];
+    if (w_lo[ph] < w_hi[ph]) first_ph = ph;
+  }
+  auto lo_of = [&](int ph) { return ph == 0 ? w_lo[0] : ph == 1 ? w_lo[1] : w_lo[2]; };
+  auto has_blk = [&](int ph) { return ph == 0 ? w_lo[0] < w_hi[0] : ph == 1 ? w_lo[1] < w_hi[1] : w_lo[2] < w_hi[2]; };
+  auto fetch = [&](int ph, int i, int cls, double (&a)[NF]) {
+    const int* T = s_tab + hd.base[ph];
+    const int nblk = T[0];
+    const int* rowoff = T + 1;
+    const int* opoff = rowoff + nblk + 1;
+    const int b = (opoff + nblk + NROW + kWarps + 1)[i];
+    const int S = rowoff[b + 1] - rowoff[b], nf = ((S + 7) >> 3) * ((S + 3) >> 2);
+    const double* Ob = ops + size_t(cls) * op_stride + size_t(ph) * phase_size + opoff[b] + lane;
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+      if (f < nf) asm volatile("ld.global.nc.f64 %0, [%1];\n" : "=d"(a[f]) : "l"(Ob + f * 32));
+  };
+  double acur[NF];
+  if constexpr (NF > 1)
+    if (t_begin < t_end && first_ph < kPasPhases) fetch(first_ph, lo_of(first_ph), tl.x, acur);
   // this warp's accumulators: lane quadrant warp % 4, columns of its TPW targets
   const unsigned tm = s_tmem + (unsigned(32 * (warp & 3)) << 16) + unsigned((warp >> 2) * TPW * TW);
 #pragma unroll 1
@@ -280,33 +332,35 @@ __global__ void __launch_bounds__(kNTh, 2)
     const int mb = it % 3, mb1 = (it + 1) % 3, mb2 = (it + 2) % 3, cb = it & 1;
     const int* sm = s_meta + mb * BN;
     const double2* sc = s_cs + cb * BN * (P + 1);
-    {  // 1. multipoles straight from L2, rotated by e^{i k alpha} into X; kGat loads in
-       // flight per thread
-      const int ne = ncols * NR;
+    {  // 1. multipoles straight from L2, rotated by e^{i k alpha} into X: a warp takes
+       // kGatCols columns at a time, lane l the coefficients q = l + 32 k (coalesced
+       // 512-byte reads, all of them in flight before the first use)
       const int* src = s_msrc + mb * BN;
 #pragma unroll 1
-      for (int e0 = tid; e0 < ne; e0 += kGat * kNTh) {
-        double2 v[kGat];
+      for (int c0 = warp * kGatCols; c0 < ncols; c0 += kWarps * kGatCols) {
+        double2 v[kGatCols][KA];
 #pragma unroll
-        for (int u = 0; u < kGat; ++u) {
-          const int e = e0 + u * kNTh;
-          if (e < ne) {
-            const int c = e / NR;
-            v[u] = __ldg(M + size_t(src[c]) * NR + (e - c * NR));
-          }
-        }
+        for (int u = 0; u < kGatCols; ++u)
+          if (c0 + u < ncols) {
+            const double2* Mb = M + size_t(src[c0 + u]) * NR + lane;
 #pragma unroll
-        for (int u = 0; u < kGat; ++u) {
-          const int e = e0 + u * kNTh;
-          if (e < ne) {
-            const int c = e / NR, q = e - c * NR;
-            const int code = s_code[q], m = code >> 20;
-            const double2 r = sc[c * (P + 1) + m];
-            const int re = code & 1023, im = (code >> 10) & 1023;
-            X[re * BN + (c ^ swz(re))] = v[u].x * r.x - v[u].y * r.y;
-            if (m) X[im * BN + (c ^ swz(im))] = v[u].x * r.y + v[u].y * r.x;
+            for (int k = 0; k < KA; ++k)
+              if (lane + 32 * k < NR) v[u][k] = __ldg(Mb + 32 * k);
           }
-        }
+#pragma unroll
+        for (int u = 0; u < kGatCols; ++u)
+          if (c0 + u < ncols) {
+            const int c = c0 + u;
+            const double2* rc = sc + c * (P + 1);
+#pragma unroll
+            for (int k = 0; k < KA; ++k)
+              if (lane + 32 * k < NR) {
+                const int m = q_re[k] >> 20;
+                const double2 r = rc[m];
+                X[(q_re[k] & 0xffff) + (c ^ ((q_re[k] >> 16) & 15))] = v[u][k].x * r.x - v[u][k].y * r.y;
+                if (m) X[(q_im[k] & 0xffff) + (c ^ (q_im[k] >> 16))] = v[u][k].x * r.y + v[u][k].y * r.x;
+              }
+          }
       }
     }
     __syncthreads();
@@ -314,7 +368,9 @@ __global__ void __launch_bounds__(kNTh, 2)
       load_cs(tn.z, mb1, cb ^ 1);
       if (t + 2 < t_end) load_cols(tn2, mb2);
     }
-    // 2. W, Z, V in place
+    // 2. W, Z, V in place.  The operator fragments of this warp's next block (of this
+    // phase, the next phase or the next tile's W) are fetched from L2 into registers
+    // before the current block runs, so no L2 latency sits between two blocks.
 #pragma unroll 1
     for (int ph = 0; ph < kPasPhases; ++ph) {
       const double* Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
@@ -327,13 +383,25 @@ __global__ void __launch_bounds__(kNTh, 2)
       const int* wblk = woff + kWarps + 1;
 #define QBXG_PAS_CASE(S) \
   case S:                \
-    if (S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
+    if (S <= kMaxBlock) pas_block<S, BN, NROW, NF>(X, rw, Ob, acur, lane, nt); \
     break;
+      const int i_end = woff[warp + 1];
 #pragma unroll 1
-      for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
+      for (int i = woff[warp]; i < i_end; ++i) {
         const int b = wblk[i];
         const int* rw = rows + rowoff[b];
         const double* Ob = Op + opoff[b];
+        double anext[NF];
+        if constexpr (NF > 1) {
+          int nph = ph, ni = i + 1, ncls = tl.x;
+          if (ni >= i_end) {
+            nph = ph + 1;
+            while (nph < kPasPhases && !has_blk(nph)) ++nph;
+            if (nph == kPasPhases && more) nph = first_ph, ncls = tn.x;
+            if (nph < kPasPhases) ni = lo_of(nph);
+          }
+          if (nph < kPasPhases) fetch(nph, ni, ncls, anext);
+        }
         switch (rowoff[b + 1] - rowoff[b]) {
           QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
           QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11)
@@ -341,6 +409,10 @@ __global__ void __launch_bounds__(kNTh, 2)
           QBXG_PAS_CASE(17) QBXG_PAS_CASE(18) QBXG_PAS_CASE(19) QBXG_PAS_CASE(20) QBXG_PAS_CASE(21)
           QBXG_PAS_CASE(22)
           default: break;
+        }
+        if constexpr (NF > 1) {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) acur[f] = anext[f];
         }
       }
 #undef QBXG_PAS_CASE
@@ -362,11 +434,9 @@ __global__ void __launch_bounds__(kNTh, 2)
           const double2* r = sc + c * (P + 1);
 #pragma unroll
           for (int k = 0; k < KA; ++k) {
-            const int q = lane + 32 * k;
-            const int code = q < NR ? s_code[q] : (NROW | NROW << 10);
-            const int re = code & 1023, im = (code >> 10) & 1023;
-            const double xr = X[re * BN + (c ^ swz(re))], xi = X[im * BN + (c ^ swz(im))];
-            const double2 rr = r[code >> 20];
+            const double xr = X[(q_re[k] & 0xffff) + (c ^ ((q_re[k] >> 16) & 15))];
+            const double xi = X[(q_im[k] & 0xffff) + (c ^ (q_im[k] >> 16))];
+            const double2 rr = r[q_re[k] >> 20];
             are[k] += xr * rr.x + xi * rr.y;
             aim[k] += xi * rr.x - xr * rr.y;
           }
@@ -490,6 +560,7 @@ PasLayout make_layout(int p) {
       for (int i : gr) rows.insert(rows.end(), L.sub[ph][i].rows.begin(), L.sub[ph][i].rows.end());
       rowoff.push_back(int(rows.size()));
       sizes.push_back(rowoff.back() - rowoff[rowoff.size() - 2]);
+      if (p <= 15 && sizes.back() > 16) throw std::logic_error("m2l_pas: merged block exceeds 8 register fragments");
       L.opoff[ph].push_back(oo);
       oo += pad_blk(sizes.back());
     }
