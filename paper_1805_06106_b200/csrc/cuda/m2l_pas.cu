@@ -173,21 +173,21 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      if constexpr (NF >= MT * KS) a[mt][ks] = af[mt * KS + ks];  // fetched while the previous block ran
+      if constexpr (NF > 1 && NF >= MT * KS) a[mt][ks] = af[mt * KS + ks];  // fetched while the previous block ran
       else a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
     }
   int rb[KS], ro[MT];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
     const int k = ks * 4 + (lane & 3);
-    const int r = k < S ? rw[k] : ZR;
-    rb[ks] = r * BN + ((lane >> 2) ^ swz(r));
+    const int t = k < S ? rw[k] : ZR * BN;  // row offset | swizzle << 16
+    rb[ks] = (t & 0xffff) + ((lane >> 2) ^ (t >> 16));
   }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int i = mt * 8 + (lane >> 2);
-    const int r = i < S ? rw[i] : -1;
-    ro[mt] = r < 0 ? -1 : r * BN + (((lane & 3) * 2) ^ swz(r));
+    const int t = i < S ? rw[i] : -1;
+    ro[mt] = t < 0 ? -1 : (t & 0xffff) + (((lane & 3) * 2) ^ (t >> 16));
   }
 #pragma unroll 1
   for (int j = 0; j < nt; ++j) {
@@ -230,6 +230,8 @@ __global__ void __launch_bounds__(kNTh, 2)
   __shared__ int s_code[NR];  // half-table q: Re row | Im row << 10 (zero row if m = 0) | m << 20
   __shared__ unsigned s_tmem;
 
+  // (a parameter array indexed by a runtime phase would be copied to local memory)
+  auto tab_base = [&](int ph) { return ph == 0 ? hd.base[0] : ph == 1 ? hd.base[1] : hd.base[2]; };
   const int g = grp_order[blockIdx.x];
   const int t_begin = grp_tiles[g], t_end = grp_tiles[g + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -239,7 +241,18 @@ __global__ void __launch_bounds__(kNTh, 2)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
-  for (int i = tid; i < tab_n; i += kNTh) s_tab[i] = tab[i];
+  {  // block table; the blocks' row lists become X row offset | swizzle << 16
+    int rs[kPasPhases];
+#pragma unroll
+    for (int ph = 0; ph < kPasPhases; ++ph) rs[ph] = hd.base[ph] + 2 + 2 * tab[hd.base[ph]];
+    for (int i = tid; i < tab_n; i += kNTh) {
+      int v = tab[i];
+#pragma unroll
+      for (int ph = 0; ph < kPasPhases; ++ph)
+        if (i >= rs[ph] && i < rs[ph] + NROW) v = v * BN | swz(v) << 16;
+      s_tab[i] = v;
+    }
+  }
   for (int q = tid; q < NR; q += kNTh) {
     int n = 0;
     while (hidx(n + 1, 0) <= q) ++n;
@@ -293,7 +306,7 @@ __global__ void __launch_bounds__(kNTh, 2)
   int w_lo[kPasPhases], w_hi[kPasPhases], first_ph = kPasPhases;
 #pragma unroll
   for (int ph = kPasPhases - 1; ph >= 0; --ph) {
-    const int* T = s_tab + hd.base[ph];
+    const int* T = s_tab + tab_base(ph);
     const int* woff = T + 1 + 2 * T[0] + 1 + NROW;
     w_lo[ph] = woff[warp];
     w_hi[ph] = woff[warp + 1];
@@ -302,7 +315,7 @@ __global__ void __launch_bounds__(kNTh, 2)
   auto lo_of = [&](int ph) { return ph == 0 ? w_lo[0] : ph == 1 ? w_lo[1] : w_lo[2]; };
   auto has_blk = [&](int ph) { return ph == 0 ? w_lo[0] < w_hi[0] : ph == 1 ? w_lo[1] < w_hi[1] : w_lo[2] < w_hi[2]; };
   auto fetch = [&](int ph, int i, int cls, double (&a)[NF]) {
-    const int* T = s_tab + hd.base[ph];
+    const int* T = s_tab + tab_base(ph);
     const int nblk = T[0];
     const int* rowoff = T + 1;
     const int* opoff = rowoff + nblk + 1;
@@ -374,7 +387,7 @@ __global__ void __launch_bounds__(kNTh, 2)
 #pragma unroll 1
     for (int ph = 0; ph < kPasPhases; ++ph) {
       const double* Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
-      const int* T = s_tab + hd.base[ph];
+      const int* T = s_tab + tab_base(ph);
       const int nblk = T[0];
       const int* rowoff = T + 1;
       const int* opoff = rowoff + nblk + 1;
