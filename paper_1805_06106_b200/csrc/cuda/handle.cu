@@ -346,7 +346,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     return;
   }
   if (!dev::pas_supported(p)) throw InvalidArgument("qbxg_create: the M2L supports 1 <= p_fmm <= 21");
-  // --- Stage 4 operators: one [W | Z | V] set per class (rho_xy^2, dz), classes
+  // --- Stage 4 operators: one [W | Z | V] set per class (rho_xy^2, |dz|), classes
   // numbered in key order (independent of which offsets a rank uses); per offset only
   // the azimuth alpha = atan2(dy, dx) remains, as the (cos k alpha, sin k alpha) table
   P.n_offsets = int(used.size());
@@ -355,7 +355,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   {
     auto key_of = [&](int sl) {
       const int dx = sl / 121 - 5, dy = (sl / 11) % 11 - 5, dz = sl % 11 - 5;
-      return (dx * dx + dy * dy) * 11 + dz + 5;
+      return (dx * dx + dy * dy) * 11 + std::abs(dz);  // dz < 0: the mirrored operator (m2l_pas.cu)
     };
     std::vector<int> key_to_cls(51 * 11, -1);
     for (int o = 0; o < P.n_offsets; ++o) key_to_cls[key_of(used[o])] = 0;
@@ -363,7 +363,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       if (key_to_cls[k] == 0) {
         key_to_cls[k] = int(cls_rxy2.size());
         cls_rxy2.push_back(k / 11);
-        cls_dz.push_back(k % 11 - 5);
+        cls_dz.push_back(k % 11);
       } else {
         key_to_cls[k] = -1;
       }
@@ -424,7 +424,8 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
     for (size_t k = 0; k < key.size(); ++k) {
       const int64_t e = e0 + int64_t(key[k] & 0xFFFFFF);
       col_src[e0 + int64_t(k)] = vb[e];
-      col_meta[e0 + int64_t(k)] = int((key[k] >> 36) & 255) | slot_to_op[slot[e]] << 8;
+      col_meta[e0 + int64_t(k)] =
+          int((key[k] >> 36) & 255) | slot_to_op[slot[e]] << 8 | (slot[e] % 11 < 5 ? dev::kPasMirror : 0);
     }
     gwork[g] = work;
   }

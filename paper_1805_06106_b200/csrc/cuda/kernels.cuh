@@ -61,6 +61,7 @@ struct DevData {
 // list of tiles, each <= pas_tile_cols() entries of one class (columns sorted by
 // (target slot, offset)), so every box local is written once, in a fixed order.
 constexpr int kMaxPasOrder = 21;
+constexpr int kPasMirror = 1 << 30;  // column flag: offset below the xy-plane, operator of (rho_xy^2, |dz|) mirrored
 struct M2LPlan {
   int KR = 0, KRp = 0;         // (p+1)^2 real DOF, padded to a multiple of 64 (tree-shift GEMMs)
   int* rmap = nullptr;         // real DOF -> double offset in a complex half table (-1 = pad)
@@ -79,7 +80,7 @@ struct M2LPlan {
   int* grp_box = nullptr;      // n_groups x G target boxes (-1: none)
   int4* tiles = nullptr;       // (class, first column, columns, 0)
   int* col_src = nullptr;      // source box of each column
-  int* col_meta = nullptr;     // target slot | offset id << 8
+  int* col_meta = nullptr;     // target slot | offset id << 8 | kPasMirror if dz < 0
 };
 bool pas_supported(int p);
 int pas_tile_cols(int p);

@@ -55,6 +55,9 @@ namespace dev {
 
 namespace {
 
+#ifndef QBXG_M2L_BN40
+#define QBXG_M2L_BN40 1
+#endif
 #ifndef QBXG_M2L_PREFETCH
 #define QBXG_M2L_PREFETCH 0  // measured: 44.8 ms with, 40.8 ms without (config 1)
 #endif
@@ -100,17 +103,28 @@ struct Tg {
            + size_t(6) * bn * 4                   // column meta, three tiles
            + size_t(tab_ints(P)) * 4;             // block table
   }
-  static constexpr int BN = bytes(32) <= kSmemMax ? 32 : 16;  // tile columns
+  static constexpr int BN = (QBXG_M2L_BN40 && bytes(40) <= kSmemMax) ? 40 : bytes(32) <= kSmemMax ? 32 : 16;  // tile columns
   // operator fragments of a block held in registers one block ahead: merged blocks are
   // <= 16 rows for P <= 15 (8 fragments; make_layout checks); larger orders load in place
   static constexpr int NF = (QBXG_M2L_PREFETCH && P <= 15) ? 8 : 1;
   static constexpr size_t SMEM = bytes(BN);
 };
 
-// X element (row r, column c) lives at r * BN + (c ^ swz(r)): the B-fragment loads
+// X element (row r, column c) lives at r * BN + (c ^ swz<BN>(r)): the B-fragment loads
 // (4 consecutive rows x 8 columns), the accumulate's reads (32 consecutive rows, one
-// column) and the fragment stores all spread over the banks.
-__device__ __forceinline__ int swz(int r) { return ((r & 1) << 3) | ((r >> 1) & 7); }
+// column) and the fragment stores all spread over the banks.  A row stride of 40 doubles
+// already puts consecutive rows 8 banks apart, so only the low three column bits are
+// permuted there (and column groups of 8 are reached by addition, not XOR).
+template <int BN>
+__device__ __forceinline__ int swz(int r) {
+  if constexpr ((BN & (BN - 1)) == 0) return ((r & 1) << 3) | ((r >> 1) & 7);
+  else return (r >> 1) & 7;
+}
+template <int BN>
+__device__ __forceinline__ int col_group(int x, int j) {  // element x of column group 0 -> group j
+  if constexpr ((BN & (BN - 1)) == 0) return x ^ (j * 8);
+  else return x + j * 8;
+}
 
 struct TabHead {
   int base[kPasPhases];
@@ -132,6 +146,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// (x, y) or -(x, y): sign bits flipped by integer XOR
+__device__ __forceinline__ double2 flip(double2 v, int neg) {
+  const int sb = neg << 31;
+  return make_double2(__hiloint2double(__double2hiint(v.x) ^ sb, __double2loint(v.x)),
+                      __hiloint2double(__double2hiint(v.y) ^ sb, __double2loint(v.y)));
 }
 
 // TMEM: 4K consecutive 32-bit columns of this lane -> K (re, im) double pairs, one wait
@@ -193,7 +214,7 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
   for (int j = 0; j < nt; ++j) {
     double b[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) b[ks] = X[rb[ks] ^ (j * 8)];
+    for (int ks = 0; ks < KS; ++ks) b[ks] = X[col_group<BN>(rb[ks], j)];
     double acc[MT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -205,8 +226,8 @@ __device__ __forceinline__ void pas_block(double* X, const int* rw, const double
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
       if (ro[mt] >= 0) {
-        X[ro[mt] ^ (j * 8)] = acc[mt][0];
-        X[(ro[mt] ^ (j * 8)) ^ 1] = acc[mt][1];
+        X[col_group<BN>(ro[mt], j)] = acc[mt][0];
+        X[col_group<BN>(ro[mt], j) ^ 1] = acc[mt][1];
       }
   }
 }
@@ -249,7 +270,7 @@ __global__ void __launch_bounds__(kNTh, 2)
       int v = tab[i];
 #pragma unroll
       for (int ph = 0; ph < kPasPhases; ++ph)
-        if (i >= rs[ph] && i < rs[ph] + NROW) v = v * BN | swz(v) << 16;
+        if (i >= rs[ph] && i < rs[ph] + NROW) v = v * BN | swz<BN>(v) << 16;
       s_tab[i] = v;
     }
   }
@@ -273,7 +294,7 @@ __global__ void __launch_bounds__(kNTh, 2)
     double2* sc = s_cs + cbuf * BN * (P + 1);
     for (int i = tid; i < ncols * (P + 1); i += kNTh) {
       const int c = i / (P + 1), m = i - c * (P + 1);
-      cp_async16(sc + i, cs_all + size_t(s_meta[mbuf * BN + c] >> 8) * (P + 1) + m);
+      cp_async16(sc + i, cs_all + size_t((s_meta[mbuf * BN + c] & (kPasMirror - 1)) >> 8) * (P + 1) + m);
     }
   };
   int4 tl = make_int4(0, 0, 0, 0), tn = tl;
@@ -297,9 +318,11 @@ __global__ void __launch_bounds__(kNTh, 2)
   for (int k = 0; k < KA; ++k) {
     const int q = lane + 32 * k;
     const int code = q < NR ? s_code[q] : (NROW | NROW << 10);
-    const int re = code & 1023, im = (code >> 10) & 1023;
-    q_re[k] = re * BN | swz(re) << 16 | (code >> 20) << 20;
-    q_im[k] = im * BN | swz(im) << 16;
+    const int re = code & 1023, im = (code >> 10) & 1023, m = code >> 20;
+    int n = 0;
+    while (q < NR && hidx(n + 1, 0) <= q) ++n;
+    q_re[k] = re * BN | swz<BN>(re) << 16 | m << 20 | ((n + m) & 1) << 25;  // bit 25: sign under z -> -z
+    q_im[k] = im * BN | swz<BN>(im) << 16;
   }
   // this warp's blocks per phase, and the fragment fetch of one of them
   constexpr int NF = C::NF;
@@ -365,11 +388,12 @@ __global__ void __launch_bounds__(kNTh, 2)
           if (c0 + u < ncols) {
             const int c = c0 + u;
             const double2* rc = sc + c * (P + 1);
+            const int mir = (sm[c] >> 30) & 1;  // offset below the xy-plane: M_n^m -> (-1)^{n+m} M_n^m
 #pragma unroll
             for (int k = 0; k < KA; ++k)
               if (lane + 32 * k < NR) {
-                const int m = q_re[k] >> 20;
-                const double2 r = rc[m];
+                const int m = (q_re[k] >> 20) & 31;
+                const double2 r = flip(rc[m], (q_re[k] >> 25) & mir);
                 X[(q_re[k] & 0xffff) + (c ^ ((q_re[k] >> 16) & 15))] = v[u][k].x * r.x - v[u][k].y * r.y;
                 if (m) X[(q_im[k] & 0xffff) + (c ^ (q_im[k] >> 16))] = v[u][k].x * r.y + v[u][k].y * r.x;
               }
@@ -435,27 +459,32 @@ __global__ void __launch_bounds__(kNTh, 2)
     // in column order; a target's columns are consecutive, so its accumulators are read
     // and written once per tile
     {
-      const int mine = lane < ncols && ((sm[lane] & 255) % kWarps) == warp;
-      unsigned mask = __ballot_sync(0xffffffffu, mine);
-      while (mask) {
-        const int slot = sm[__ffs(mask) - 1] & 255, u = slot / kWarps;
-        double are[KA], aim[KA];
-        tm_ld<KA>(tm + u * TW, are, aim);
-        while (mask && (sm[__ffs(mask) - 1] & 255) == slot) {
-          const int c = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const double2* r = sc + c * (P + 1);
+#pragma unroll 1
+      for (int cb = 0; cb < ncols; cb += 32) {  // (BN may exceed the 32 lanes of the ballot)
+        const int mine = cb + lane < ncols && ((sm[cb + lane] & 255) % kWarps) == warp;
+        unsigned mask = __ballot_sync(0xffffffffu, mine);
+        if (cb && mask) tm_wait_st();  // a target's run may continue from the previous 32 columns
+        while (mask) {
+          const int slot = sm[cb + __ffs(mask) - 1] & 255, u = slot / kWarps;
+          double are[KA], aim[KA];
+          tm_ld<KA>(tm + u * TW, are, aim);
+          while (mask && (sm[cb + __ffs(mask) - 1] & 255) == slot) {
+            const int c = cb + __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double2* r = sc + c * (P + 1);
+            const int mir = (sm[c] >> 30) & 1;  // L_n^m <- (-1)^{n+m} L_n^m of the mirrored translation
 #pragma unroll
-          for (int k = 0; k < KA; ++k) {
-            const double xr = X[(q_re[k] & 0xffff) + (c ^ ((q_re[k] >> 16) & 15))];
-            const double xi = X[(q_im[k] & 0xffff) + (c ^ (q_im[k] >> 16))];
-            const double2 rr = r[q_re[k] >> 20];
-            are[k] += xr * rr.x + xi * rr.y;
-            aim[k] += xi * rr.x - xr * rr.y;
+            for (int k = 0; k < KA; ++k) {
+              const double xr = X[(q_re[k] & 0xffff) + (c ^ ((q_re[k] >> 16) & 15))];
+              const double xi = X[(q_im[k] & 0xffff) + (c ^ (q_im[k] >> 16))];
+              const double2 rr = flip(r[(q_re[k] >> 20) & 31], (q_re[k] >> 25) & mir);
+              are[k] += xr * rr.x + xi * rr.y;
+              aim[k] += xi * rr.x - xr * rr.y;
+            }
           }
-        }
 #pragma unroll
-        for (int k = 0; k < KA; ++k) tm_st4(tm + (u * KA + k) * 4, are[k], aim[k]);
+          for (int k = 0; k < KA; ++k) tm_st4(tm + (u * KA + k) * 4, are[k], aim[k]);
+        }
       }
       tm_wait_st();  // each run wrote a different target's columns; one wait for all
     }
