@@ -58,9 +58,6 @@ namespace {
 #ifndef QBXG_M2L_BN40
 #define QBXG_M2L_BN40 1
 #endif
-#ifndef QBXG_M2L_PREFETCH
-#define QBXG_M2L_PREFETCH 0  // measured: 44.8 ms with, 40.8 ms without (config 1)
-#endif
 constexpr int kPasPhases = 3;
 constexpr int kWarps = 8, kNTh = kWarps * 32;  // two CTAs per SM
 #ifndef QBXG_M2L_GATCOLS
@@ -104,9 +101,6 @@ struct Tg {
            + size_t(tab_ints(P)) * 4;             // block table
   }
   static constexpr int BN = (QBXG_M2L_BN40 && bytes(40) <= kSmemMax) ? 40 : bytes(32) <= kSmemMax ? 32 : 16;  // tile columns
-  // operator fragments of a block held in registers one block ahead: merged blocks are
-  // <= 16 rows for P <= 15 (8 fragments; make_layout checks); larger orders load in place
-  static constexpr int NF = (QBXG_M2L_PREFETCH && P <= 15) ? 8 : 1;
   static constexpr size_t SMEM = bytes(BN);
 };
 
@@ -185,18 +179,14 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 // then per 8-column tile j < nt the block's rows as B fragments from X (padding rows
 // k >= S read the zero row), the DMMAs, and the rows written back.  Tile j's reads
 // feed its DMMAs, which precede its writes; other tiles touch other columns.
-template <int S, int BN, int ZR, int NF>
-__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, const double (&af)[NF],
-                                          int lane, int nt) {
+template <int S, int BN, int ZR>
+__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, int lane, int nt) {
   constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4;
   double a[MT][KS];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      if constexpr (NF > 1 && NF >= MT * KS) a[mt][ks] = af[mt * KS + ks];  // fetched while the previous block ran
-      else a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
-    }
+    for (int ks = 0; ks < KS; ++ks) a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
   int rb[KS], ro[MT];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
@@ -324,34 +314,6 @@ __global__ void __launch_bounds__(kNTh, 2)
     q_re[k] = re * BN | swz<BN>(re) << 16 | m << 20 | ((n + m) & 1) << 25;  // bit 25: sign under z -> -z
     q_im[k] = im * BN | swz<BN>(im) << 16;
   }
-  // this warp's blocks per phase, and the fragment fetch of one of them
-  constexpr int NF = C::NF;
-  int w_lo[kPasPhases], w_hi[kPasPhases], first_ph = kPasPhases;
-#pragma unroll
-  for (int ph = kPasPhases - 1; ph >= 0; --ph) {
-    const int* T = s_tab + tab_base(ph);
-    const int* woff = T + 1 + 2 * T[0] + 1 + NROW;
-    w_lo[ph] = woff[warp];
-    w_hi[ph] = woff[warp + 1];
-    if (w_lo[ph] < w_hi[ph]) first_ph = ph;
-  }
-  auto lo_of = [&](int ph) { return ph == 0 ? w_lo[0] : ph == 1 ? w_lo[1] : w_lo[2]; };
-  auto has_blk = [&](int ph) { return ph == 0 ? w_lo[0] < w_hi[0] : ph == 1 ? w_lo[1] < w_hi[1] : w_lo[2] < w_hi[2]; };
-  auto fetch = [&](int ph, int i, int cls, double (&a)[NF]) {
-    const int* T = s_tab + tab_base(ph);
-    const int nblk = T[0];
-    const int* rowoff = T + 1;
-    const int* opoff = rowoff + nblk + 1;
-    const int b = (opoff + nblk + NROW + kWarps + 1)[i];
-    const int S = rowoff[b + 1] - rowoff[b], nf = ((S + 7) >> 3) * ((S + 3) >> 2);
-    const double* Ob = ops + size_t(cls) * op_stride + size_t(ph) * phase_size + opoff[b] + lane;
-#pragma unroll
-    for (int f = 0; f < NF; ++f)
-      if (f < nf) asm volatile("ld.global.nc.f64 %0, [%1];\n" : "=d"(a[f]) : "l"(Ob + f * 32));
-  };
-  double acur[NF];
-  if constexpr (NF > 1)
-    if (t_begin < t_end && first_ph < kPasPhases) fetch(first_ph, lo_of(first_ph), tl.x, acur);
   // this warp's accumulators: lane quadrant warp % 4, columns of its TPW targets
   const unsigned tm = s_tmem + (unsigned(32 * (warp & 3)) << 16) + unsigned((warp >> 2) * TPW * TW);
 #pragma unroll 1
@@ -405,9 +367,7 @@ __global__ void __launch_bounds__(kNTh, 2)
       load_cs(tn.z, mb1, cb ^ 1);
       if (t + 2 < t_end) load_cols(tn2, mb2);
     }
-    // 2. W, Z, V in place.  The operator fragments of this warp's next block (of this
-    // phase, the next phase or the next tile's W) are fetched from L2 into registers
-    // before the current block runs, so no L2 latency sits between two blocks.
+    // 2. W, Z, V in place
 #pragma unroll 1
     for (int ph = 0; ph < kPasPhases; ++ph) {
       const double* Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
@@ -420,7 +380,7 @@ __global__ void __launch_bounds__(kNTh, 2)
       const int* wblk = woff + kWarps + 1;
 #define QBXG_PAS_CASE(S) \
   case S:                \
-    if (S <= kMaxBlock) pas_block<S, BN, NROW, NF>(X, rw, Ob, acur, lane, nt); \
+    if (S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
     break;
       const int i_end = woff[warp + 1];
 #pragma unroll 1
@@ -428,17 +388,6 @@ __global__ void __launch_bounds__(kNTh, 2)
         const int b = wblk[i];
         const int* rw = rows + rowoff[b];
         const double* Ob = Op + opoff[b];
-        double anext[NF];
-        if constexpr (NF > 1) {
-          int nph = ph, ni = i + 1, ncls = tl.x;
-          if (ni >= i_end) {
-            nph = ph + 1;
-            while (nph < kPasPhases && !has_blk(nph)) ++nph;
-            if (nph == kPasPhases && more) nph = first_ph, ncls = tn.x;
-            if (nph < kPasPhases) ni = lo_of(nph);
-          }
-          if (nph < kPasPhases) fetch(nph, ni, ncls, anext);
-        }
         switch (rowoff[b + 1] - rowoff[b]) {
           QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
           QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11)
@@ -446,10 +395,6 @@ __global__ void __launch_bounds__(kNTh, 2)
           QBXG_PAS_CASE(17) QBXG_PAS_CASE(18) QBXG_PAS_CASE(19) QBXG_PAS_CASE(20) QBXG_PAS_CASE(21)
           QBXG_PAS_CASE(22)
           default: break;
-        }
-        if constexpr (NF > 1) {
-#pragma unroll
-          for (int f = 0; f < NF; ++f) acur[f] = anext[f];
         }
       }
 #undef QBXG_PAS_CASE
@@ -602,7 +547,6 @@ PasLayout make_layout(int p) {
       for (int i : gr) rows.insert(rows.end(), L.sub[ph][i].rows.begin(), L.sub[ph][i].rows.end());
       rowoff.push_back(int(rows.size()));
       sizes.push_back(rowoff.back() - rowoff[rowoff.size() - 2]);
-      if (p <= 15 && sizes.back() > 16) throw std::logic_error("m2l_pas: merged block exceeds 8 register fragments");
       L.opoff[ph].push_back(oo);
       oo += pad_blk(sizes.back());
     }
