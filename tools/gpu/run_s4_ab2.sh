@@ -6,5 +6,6 @@ echo "$v $(timeout 300 python tools/stage_times.py 1 5 | tail -n 1)" >> gpurun_o
 done
 done
 # parity of the last variant
+rm -f gpurun_out/pytest_ab.log
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_shard.py -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_ab.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_ab.log
