@@ -1024,6 +1024,7 @@ void near_q(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
 // split M2L's staging rows, so k_h_m2l_reduce_split finishes the job.  Per List-2 entry at
 // p = 20: 8 x (3,311 + 2,870) real multiply-adds instead of 4 x (231^2 + 210^2).
 constexpr int kHpW = 8, kHpLD = kHColsS + 1;
+constexpr int kHpGat = 8;  // gather elements per thread with their loads in flight together
 
 __device__ __forceinline__ void hp_dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -1128,24 +1129,43 @@ __global__ void __launch_bounds__(kHpW * 32, 2)
   }
   if (tid <= P) s_cs[tid] = cs[size_t(tile.x) * (P + 1) + tid];
   __syncthreads();
-  // gather: M' = M e^{i m alpha}, then A = M'_m + M'_-m (A_0 = M'_0) or B = M'_m - M'_-m
-  for (int e = tid; e < NC * kHColsS; e += blockDim.x) {
-    const int c = e / NC, r = e - c * NC;
-    double2 v = make_double2(0.0, 0.0);
-    if (s_src[c] >= 0) {
-      const int nm = s_nm[r], n = nm & 255, m = nm >> 8;
-      const double2* Mb = H.M + size_t(s_src[c]) * KP;
-      const double2 ro = s_cs[m];
-      const double2 xp = cmul(__ldg(Mb + fi(n, m)), ro);
-      if (m == 0) {
-        v = xp;
-      } else {
-        const double2 xm = cmul(__ldg(Mb + fi(n, -m)), make_double2(ro.x, -ro.y));
-        v = par ? make_double2(xp.x - xm.x, xp.y - xm.y) : make_double2(xp.x + xm.x, xp.y + xm.y);
+  // gather: M' = M e^{i m alpha}, then A = M'_m + M'_-m (A_0 = M'_0) or B = M'_m - M'_-m;
+  // kHpGat elements per thread at a time, all their multipole loads in flight before the
+  // first use (the kernel spent a third of its time waiting on one load pair per element)
+  for (int e0 = tid; e0 < NC * kHColsS; e0 += kHpGat * blockDim.x) {
+    double2 vp[kHpGat], vm[kHpGat];
+    int cr[kHpGat];
+#pragma unroll
+    for (int u = 0; u < kHpGat; ++u) {
+      const int e = e0 + u * blockDim.x;
+      cr[u] = -1;
+      vp[u] = vm[u] = make_double2(0.0, 0.0);
+      if (e < NC * kHColsS) {
+        const int c = e / NC, r = e - c * NC;
+        cr[u] = c | r << 8;
+        if (s_src[c] >= 0) {
+          const int nm = s_nm[r], n = nm & 255, m = nm >> 8;
+          const double2* Mb = H.M + size_t(s_src[c]) * KP;
+          vp[u] = __ldg(Mb + fi(n, m));
+          if (m) vm[u] = __ldg(Mb + fi(n, -m));
+        }
       }
     }
-    X[(2 * r) * kHpLD + c] = v.x;
-    X[(2 * r + 1) * kHpLD + c] = v.y;
+#pragma unroll
+    for (int u = 0; u < kHpGat; ++u) {
+      if (cr[u] < 0) continue;
+      const int c = cr[u] & 255, r = cr[u] >> 8;
+      const int m = s_nm[r] >> 8;
+      const double2 ro = s_cs[m];
+      const double2 xp = cmul(vp[u], ro);
+      double2 v = xp;
+      if (m) {
+        const double2 xm = cmul(vm[u], make_double2(ro.x, -ro.y));
+        v = par ? make_double2(xp.x - xm.x, xp.y - xm.y) : make_double2(xp.x + xm.x, xp.y + xm.y);
+      }
+      X[(2 * r) * kHpLD + c] = v.x;
+      X[(2 * r + 1) * kHpLD + c] = v.y;
+    }
   }
   __syncthreads();
   const double* wv = wvops + size_t(op_cls[tile.x]) * wvstride;
