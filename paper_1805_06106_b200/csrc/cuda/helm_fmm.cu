@@ -782,18 +782,44 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
 // Stage 5b M2QBXL / Stage 8 L2QBXL: box expansion X (order p) -> up to kHCtrMax
 // centres (order q).  For mu = -(p+q)..p+q: C_mu[i'][l] from X and the Gaunt
 // table, F_l^mu(c_j - c_box) per centre, acc[j][i'] += sum_l F C.
-constexpr int kHCtrAcc = (kHCtrMax * 81 + 255) / 256;  // per-thread outputs (q <= 8, 256 threads)
+constexpr int kHCtrAcc = 12;  // per-thread outputs: 2 rows i' x up to 6 centres (q <= 8, 256 threads)
+// acc[2a + h] += sum_{sign} sum_l F[a][l] C[h][l] for CPG centres and two C rows: 2 + CPG
+// shared loads per 2 CPG complex multiply-adds.  Centres beyond nj repeat the last
+// valid one (their sums are never stored), so the loop has no predicates.
+template <int CPG>
+__device__ __forceinline__ void ctr_dot(double2 (&acc)[12], const double2* __restrict__ F0,
+                                        const double2* __restrict__ C0, int c1_off, int c_sign_stride, int NL, int nj,
+                                        int ns, int amu, int L) {
+  int fo[CPG];
+#pragma unroll
+  for (int a = 0; a < CPG; ++a) fo[a] = min(a, nj - 1) * NL;
+  for (int sg = 0; sg < ns; ++sg) {
+    const double2* F = F0 + sg * kHCtrMax * NL;
+    const double2* C = C0 + sg * c_sign_stride;
+    for (int l = amu; l <= L; ++l) {
+      const double2 c0 = C[l], c1 = C[c1_off + l];
+#pragma unroll
+      for (int a = 0; a < CPG; ++a) {
+        const double2 f = F[fo[a] + l];
+        acc[2 * a] = cfma(f, c0, acc[2 * a]);
+        acc[2 * a + 1] = cfma(f, c1, acc[2 * a + 1]);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const double2* __restrict__ X,
                                                const int4* __restrict__ ctas, const int* __restrict__ ctr_of,
                                                const int* __restrict__ out_row, double2* __restrict__ out,
                                                int accumulate) {
   extern __shared__ double2 sm[];
   const int P = H.P, Q = H.Q, KP = H.KP, KQ = H.KQ, L = P + Q, NL = L + 1;
+  const int NLp = NL | 1;  // odd row stride of C: lanes reading consecutive rows hit different banks
   const int4 cta = ctas[blockIdx.x];  // (box, first item, count, -)
   const int nctr = cta.z;
   double2* Xs = sm;                      // KP
-  double2* Cm = Xs + KP;                 // 2 x KQ x NL: C_{+|mu|}, C_{-|mu|}
-  double2* rad = Cm + 2 * KQ * NL;       // kHCtrMax x NL
+  double2* Cm = Xs + KP;                 // 2 x KQ x NLp: C_{+|mu|}, C_{-|mu|}
+  double2* rad = Cm + 2 * KQ * NLp;      // kHCtrMax x NL
   double2* Fc = rad + kHCtrMax * NL;     // 2 x kHCtrMax x NL: F^{+|mu|}, F^{-|mu|}
   double* geo = reinterpret_cast<double*>(Fc + 2 * kHCtrMax * NL);  // kHCtrMax x 4: t, |t|^2
   const double4 bc = H.box[cta.x];
@@ -810,6 +836,12 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   double2 acc[kHCtrAcc];
 #pragma unroll
   for (int a = 0; a < kHCtrAcc; ++a) acc[a] = make_double2(0, 0);
+  // output tiling: KQ2 row pairs (i0, i0 + KQ2) x ngrp centre groups of cpg centres
+  const int KQ2 = (KQ + 1) / 2, ngrp = min(int(blockDim.x) / KQ2, kHCtrMax);
+  const int cpg = (kHCtrMax + ngrp - 1) / ngrp;  // <= kHCtrAcc / 2 for q <= 8
+  const int grp = threadIdx.x / KQ2, i0 = threadIdx.x - grp * KQ2, j0 = grp * cpg;
+  const bool has1 = i0 + KQ2 < KQ;
+  const int nj = max(0, min(cpg, nctr - j0));
   __syncthreads();
   // mu and -mu together: one solid-harmonic column per |mu| serves both signs
   // (S^{-mu} = conj S^mu), and half as many barriers
@@ -838,7 +870,7 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
         cacc.x = fma(gv, t.x, cacc.x);
         cacc.y = fma(gv, t.y, cacc.y);
       }
-      Cm[(sg * KQ + iout) * NL + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
+      Cm[(sg * KQ + iout) * NLp + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
     }
     // F columns per centre: (rad_l / r^l) S_l^{+-|mu|}(t), l = |mu|..L
     for (int j = int(threadIdx.x) - nth_c; j >= 0 && j < nctr; j += 32) {
@@ -852,35 +884,37 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int a = 0; a < kHCtrAcc; ++a) {
-      const int e = threadIdx.x + a * blockDim.x;
-      if (e < nctr * KQ) {
-        const int j = e / KQ, iout = e % KQ;
-        double2 s2 = acc[a];
-        for (int sg = 0; sg < ns; ++sg) {
-          const double2* F = Fc + (sg * kHCtrMax + j) * NL;
-          const double2* C = Cm + (sg * KQ + iout) * NL;
-          for (int l = amu; l <= L; ++l) s2 = cfma(F[l], C[l], s2);
-        }
-        acc[a] = s2;
+    // acc[j][i'] += sum_l F[j][l] C[i'][l], register-tiled: a thread owns rows i0 and
+    // i0 + KQ2 of C and cpg centres, so one l step costs 2 + cpg shared loads for 2 cpg
+    // complex multiply-adds (a centre's sum runs in the same order as before)
+    if (nj > 0) {
+      switch (cpg) {
+        case 1: ctr_dot<1>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
+        case 2: ctr_dot<2>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
+        case 3: ctr_dot<3>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
+        case 4: ctr_dot<4>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
+        case 5: ctr_dot<5>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
+        default: ctr_dot<6>(acc, Fc + j0 * NL, Cm + i0 * NLp, has1 ? KQ2 * NLp : 0, KQ * NLp, NL, nj, ns, amu, L); break;
       }
     }
     __syncthreads();
   }
+  if (nj > 0) {
 #pragma unroll
-  for (int a = 0; a < kHCtrAcc; ++a) {
-    const int e = threadIdx.x + a * blockDim.x;
-    if (e < nctr * KQ) {
-      const int j = e / KQ, iout = e % KQ;
-      double2* o = out + size_t(out_row[cta.y + j]) * KQ + iout;
-      if (accumulate) {
-        const double2 v = *o;
-        *o = make_double2(v.x + acc[a].x, v.y + acc[a].y);
-      } else {
-        *o = acc[a];
+    for (int a = 0; a < kHCtrAcc / 2; ++a)
+      if (a < nj) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !has1) continue;
+          double2* o = out + size_t(out_row[cta.y + j0 + a]) * KQ + i0 + h * KQ2;
+          if (accumulate) {
+            const double2 v = *o;
+            *o = make_double2(v.x + acc[2 * a + h].x, v.y + acc[2 * a + h].y);
+          } else {
+            *o = acc[2 * a + h];
+          }
+        }
       }
-    }
   }
 }
 
@@ -1479,7 +1513,7 @@ int helm_ctr(const HelmData& H, int singular, const double2* X, int n_ctas, cons
   if (n_ctas == 0) return 0;
   const int NL = H.P + H.Q + 1;
   const size_t smem =
-      size_t(H.KP + 2 * H.KQ * NL + 3 * kHCtrMax * NL) * sizeof(double2) + size_t(4 * kHCtrMax) * sizeof(double);
+      size_t(H.KP + 2 * H.KQ * (NL | 1) + 3 * kHCtrMax * NL) * sizeof(double2) + size_t(4 * kHCtrMax) * sizeof(double);
   cudaFuncSetAttribute(k_h_ctr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_h_ctr<<<n_ctas, 256, smem, s>>>(H, singular, X, ctas, ctr_of, out_row, out, accumulate);
   return 1;
