@@ -841,6 +841,11 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   const int cpg = (kHCtrMax + ngrp - 1) / ngrp;  // <= kHCtrAcc / 2 for q <= 8
   const int grp = threadIdx.x / KQ2, i0 = threadIdx.x - grp * KQ2, j0 = grp * cpg;
   const bool has1 = i0 + KQ2 < KQ;
+  // C_mu contraction: thread = (row i', residue class of l) among the first 7 warps
+  const int c_ng = max(1, (int(blockDim.x) - 32) / KQ), c_iout = threadIdx.x % KQ, c_lg = threadIdx.x / KQ;
+  const bool c_act = int(threadIdx.x) < c_ng * KQ && int(threadIdx.x) < int(blockDim.x) - 32;
+  int c_n2, c_m2;
+  nm_of(c_iout, c_n2, c_m2);
   const int nj = max(0, min(cpg, nctr - j0));
   __syncthreads();
   // mu and -mu together: one solid-harmonic column per |mu| serves both signs
@@ -852,26 +857,42 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
     const int NLm = NL - amu;
     // the last warp forms the centres' F columns (a recurrence in l per centre) while the
     // other warps contract C_mu, so the column recurrence is off the critical path
-    const int nth_c = blockDim.x - 32;
-    for (int e = threadIdx.x; threadIdx.x < nth_c && e < ns * KQ * NLm; e += nth_c) {
-      const int sg = e / (KQ * NLm), er = e - sg * KQ * NLm;
-      const int iout = er / NLm, l = amu + er % NLm, mu = sg ? -amu : amu;
-      double2 cacc = make_double2(0, 0);
-      int n2, m2;
-      nm_of(iout, n2, m2);
-      const int m = m2 + mu;
-      int nlo = max(abs(m), abs(l - n2));
-      nlo += (nlo + n2 + l) & 1;
-      const int nhi = min(P, l + n2);
-      for (int n = nlo; n <= nhi; n += 2) {
-        const int li = (l - abs(n - n2)) >> 1;
-        const double gv = __ldg(H.gaunt + (size_t(fi(n, m)) * KP + iout) * H.GL + li);
-        const double2 t = cmul(ipow(n2 + l - n), Xs[fi(n, m)]);
-        cacc.x = fma(gv, t.x, cacc.x);
-        cacc.y = fma(gv, t.y, cacc.y);
+    // (thread = row i' x one of c_ng residue classes of l: no index divisions in the loop;
+    // the terms of one sum differ by a factor -1 from one n to the next, n stepping by 2, so
+    // the power of i is applied once to the signed sum -- exact, same rounding as term by term)
+    if (c_act)
+      for (int sg = 0; sg < ns; ++sg) {
+        const int mu = sg ? -amu : amu, m = c_m2 + mu;
+        for (int l = amu + c_lg; l <= L; l += c_ng) {
+          int nlo = max(abs(m), abs(l - c_n2));
+          nlo += (nlo + c_n2 + l) & 1;
+          const int nhi = min(P, l + c_n2);
+          double sx = 0.0, sy = 0.0;
+          for (int n = nlo; n <= nhi; n += 8) {
+            double g[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int nn = n + 2 * u;
+              g[u] = 0.0;
+              if (nn <= nhi)
+                g[u] = __ldg(H.gaunt + (size_t(fi(nn, m)) * KP + c_iout) * H.GL + ((l - abs(nn - c_n2)) >> 1));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int nn = n + 2 * u;
+              if (nn <= nhi) {
+                const double2 x = Xs[fi(nn, m)];
+                const double gu = (u & 1) ? -g[u] : g[u];
+                sx = fma(gu, x.x, sx);
+                sy = fma(gu, x.y, sy);
+              }
+            }
+          }
+          const double2 t = nlo <= nhi ? cmul(ipow(c_n2 + l - nlo), make_double2(sx, sy)) : make_double2(0.0, 0.0);
+          Cm[(sg * KQ + c_iout) * NLp + l] = make_double2(4.0 * kPi * t.x, 4.0 * kPi * t.y);
+        }
       }
-      Cm[(sg * KQ + iout) * NLp + l] = make_double2(4.0 * kPi * cacc.x, 4.0 * kPi * cacc.y);
-    }
+    const int nth_c = blockDim.x - 32;
     // F columns per centre: (rad_l / r^l) S_l^{+-|mu|}(t), l = |mu|..L
     for (int j = int(threadIdx.x) - nth_c; j >= 0 && j < nctr; j += 32) {
       double2* colp = Fc + j * NL;
