@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
   for (int a = 0; a < kHCtrAcc; ++a) acc[a] = make_double2(0, 0);
   // output tiling: KQ2 row pairs (i0, i0 + KQ2) x ngrp centre groups of cpg centres
   const int KQ2 = (KQ + 1) / 2, ngrp = min(int(blockDim.x) / KQ2, kHCtrMax);
-  const int cpg = (kHCtrMax + ngrp - 1) / ngrp;  // <= kHCtrAcc / 2 for q <= 8
+  const int cpg = (nctr + ngrp - 1) / ngrp;  // centres per group of this CTA; <= kHCtrAcc / 2 for q <= 8
   const int grp = threadIdx.x / KQ2, i0 = threadIdx.x - grp * KQ2, j0 = grp * cpg;
   const bool has1 = i0 + KQ2 < KQ;
   // C_mu contraction: thread = (row i', residue class of l) among the first 7 warps
