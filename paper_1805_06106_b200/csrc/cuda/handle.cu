@@ -494,6 +494,11 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.phi = dalloc<double2>(O, std::max<int64_t>(H.nconv, 1));
   HD.gaunt = dupload(O, helm_gaunt_table(p), s);
   dev::helm_upload_constants();
+  {
+    double* gc = dalloc<double>(O, dev::helm_gaunt_ctr_size(p, q));
+    HD.gaunt_ctr = gc;
+    dev::helm_build_gaunt_ctr(HD, gc, s);
+  }
   H.d_wc = dalloc<double>(O, 2 * std::max<int64_t>(H.ns, 1));
   H.d_potc = dalloc<double>(O, 2 * std::max<int64_t>(H.nt, 1));
   H.d_coeffc = dalloc<double>(O, 2 * std::max<int64_t>(H.nc, 1) * HD.KQ);

@@ -43,6 +43,9 @@ struct HelmData {
   const int64_t* wfar_starts;
   const int* wfar_box;
   const double* gaunt;  // KP x KP x GL
+  // the same coefficients in the order the centre translations read them:
+  // [|mu|][sign][l][term k][row i'] (n = n_lo + 2k), consecutive rows i' contiguous
+  const double* gaunt_ctr;
   unsigned int* bad;    // Stage 9 non-finite flag (shared with the Laplace DevData)
 };
 
@@ -73,6 +76,8 @@ int helm_p2p(const HelmData& H, const int* boxes, int n, cudaStream_t s);
 int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s);
 // centre translations: ctas (box, first, count) over item lists ctr_of (sorted centre)
 // and out_row (row of `out`, KQ complex each); accumulate = add into out rows
+size_t helm_gaunt_ctr_size(int P, int Q);
+int helm_build_gaunt_ctr(const HelmData& H, double* out, cudaStream_t s);
 int helm_ctr(const HelmData& H, int singular, const double2* X, int n_ctas, const int4* ctas, const int* ctr_of,
              const int* out_row, double2* out, int accumulate, cudaStream_t s);
 int helm_pair_reduce(const HelmData& H, const int* centres, const int* starts, int n, const double2* rows,

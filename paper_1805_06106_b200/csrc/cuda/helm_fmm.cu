@@ -783,6 +783,33 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
 // centres (order q).  For mu = -(p+q)..p+q: C_mu[i'][l] from X and the Gaunt
 // table, F_l^mu(c_j - c_box) per centre, acc[j][i'] += sum_l F C.
 constexpr int kHCtrAcc = 12;  // per-thread outputs: 2 rows i' x up to 6 centres (q <= 8, 256 threads)
+// Gaunt coefficients of the centre translations, term-major (HelmData::gaunt_ctr):
+// entry (|mu|, sign, l, k, i') = G(n, m' + mu; n', m'; l) with n = n_lo + 2k, the k-th
+// term of C_mu[i'][l] (zero beyond the last term)
+__global__ void k_h_gaunt_ctr(HelmData H, double* __restrict__ out, size_t total) {
+  const size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int P = H.P, Q = H.Q, KQ = H.KQ, NL = P + Q + 1, KT = Q + 1;
+  const int iout = int(idx % KQ);
+  size_t r = idx / KQ;
+  const int k = int(r % KT);
+  r /= KT;
+  const int l = int(r % NL);
+  r /= NL;
+  const int sg = int(r & 1), amu = int(r >> 1);
+  double v = 0.0;
+  if (l >= amu && !(amu == 0 && sg)) {
+    int n2, m2;
+    nm_of(iout, n2, m2);
+    const int m = m2 + (sg ? -amu : amu);
+    int nlo = max(abs(m), abs(l - n2));
+    nlo += (nlo + n2 + l) & 1;
+    const int nhi = min(P, l + n2), n = nlo + 2 * k;
+    if (n <= nhi) v = H.gaunt[(size_t(fi(n, m)) * H.KP + iout) * H.GL + ((l - abs(n - n2)) >> 1)];
+  }
+  out[idx] = v;
+}
+
 // acc[2a + h] += sum_{sign} sum_l F[a][l] C[h][l] for CPG centres and two C rows: 2 + CPG
 // shared loads per 2 CPG complex multiply-adds.  Centres beyond nj repeat the last
 // valid one (their sums are never stored), so the loop has no predicates.
@@ -868,14 +895,14 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
           nlo += (nlo + c_n2 + l) & 1;
           const int nhi = min(P, l + c_n2);
           double sx = 0.0, sy = 0.0;
+          const double* gt = H.gaunt_ctr + (size_t((amu * 2 + sg) * NL + l) * (Q + 1)) * KQ + c_iout;
           for (int n = nlo; n <= nhi; n += 8) {
             double g[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 4; ++u) {  // term-major table: the warp's rows i' read one 8-byte run
               const int nn = n + 2 * u;
               g[u] = 0.0;
-              if (nn <= nhi)
-                g[u] = __ldg(H.gaunt + (size_t(fi(nn, m)) * KP + c_iout) * H.GL + ((l - abs(nn - c_n2)) >> 1));
+              if (nn <= nhi) g[u] = __ldg(gt + (((nn - nlo) >> 1)) * KQ);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1526,6 +1553,17 @@ int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   }
   const int PF = H.hmu ? H.P + 1 : H.P;
   k_h_p2l<<<n, 256, ((PF + 1) * (PF + 1) + PF + 1) * sizeof(double2), s>>>(H, boxes);
+  return 1;
+}
+
+size_t helm_gaunt_ctr_size(int P, int Q) {
+  const size_t NL = P + Q + 1;
+  return NL * 2 * NL * (Q + 1) * size_t((Q + 1) * (Q + 1));
+}
+
+int helm_build_gaunt_ctr(const HelmData& H, double* out, cudaStream_t s) {
+  const size_t n = helm_gaunt_ctr_size(H.P, H.Q);
+  k_h_gaunt_ctr<<<unsigned((n + 255) / 256), 256, 0, s>>>(H, out, n);
   return 1;
 }
 
