@@ -890,19 +890,29 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
     if (c_act)
       for (int sg = 0; sg < ns; ++sg) {
         const int mu = sg ? -amu : amu, m = c_m2 + mu;
-        for (int l = amu + c_lg; l <= L; l += c_ng) {
-          int nlo = max(abs(m), abs(l - c_n2));
+        // term range and table row of one l
+        auto range = [&](int l, int& nlo, int& nhi, const double*& gt) {
+          nlo = max(abs(m), abs(l - c_n2));
           nlo += (nlo + c_n2 + l) & 1;
-          const int nhi = min(P, l + c_n2);
+          nhi = l <= L ? min(P, l + c_n2) : -1;
+          gt = H.gaunt_ctr + (size_t((amu * 2 + sg) * NL + min(l, L)) * (Q + 1)) * KQ + c_iout;
+        };
+        auto first4 = [&](int nlo, int nhi, const double* gt, double (&g)[4]) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // term-major table: the warp's rows i' read one 8-byte run
+            g[u] = 0.0;
+            if (nlo + 2 * u <= nhi) g[u] = __ldg(gt + u * KQ);
+          }
+        };
+        auto finish = [&](int l, int nlo, int nhi, const double* gt, const double (&g0)[4]) {
           double sx = 0.0, sy = 0.0;
-          const double* gt = H.gaunt_ctr + (size_t((amu * 2 + sg) * NL + l) * (Q + 1)) * KQ + c_iout;
           for (int n = nlo; n <= nhi; n += 8) {
             double g[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {  // term-major table: the warp's rows i' read one 8-byte run
+            for (int u = 0; u < 4; ++u) {
               const int nn = n + 2 * u;
-              g[u] = 0.0;
-              if (nn <= nhi) g[u] = __ldg(gt + (((nn - nlo) >> 1)) * KQ);
+              g[u] = g0[u];
+              if (n > nlo) g[u] = nn <= nhi ? __ldg(gt + ((nn - nlo) >> 1) * KQ) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -917,6 +927,18 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
           }
           const double2 t = nlo <= nhi ? cmul(ipow(c_n2 + l - nlo), make_double2(sx, sy)) : make_double2(0.0, 0.0);
           Cm[(sg * KQ + c_iout) * NLp + l] = make_double2(4.0 * kPi * t.x, 4.0 * kPi * t.y);
+        };
+        // two l at a time: the Gaunt loads of both are in flight before either sum starts
+        for (int l = amu + c_lg; l <= L; l += 2 * c_ng) {
+          int nloA, nhiA, nloB, nhiB;
+          const double *gtA, *gtB;
+          range(l, nloA, nhiA, gtA);
+          range(l + c_ng, nloB, nhiB, gtB);
+          double gA[4], gB[4];
+          first4(nloA, nhiA, gtA, gA);
+          first4(nloB, nhiB, gtB, gB);
+          finish(l, nloA, nhiA, gtA, gA);
+          if (l + c_ng <= L) finish(l + c_ng, nloB, nhiB, gtB, gB);
         }
       }
     const int nth_c = blockDim.x - 32;
