@@ -1136,65 +1136,75 @@ __device__ __forceinline__ void hp_dmma(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-// one block of runtime size S <= 48 in place: operator A-fragments (ks, mt) from L2
-// (one k-step ahead), rows rw[] x 16 columns from shared memory
-__device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const double* __restrict__ Ob, int lane) {
-  const int MT = (S + 7) >> 3, KS = (S + 3) >> 2;
-  double acc[6][2][2];
+// one block of runtime size S <= 8 MT in place: operator A-fragments (ks, mt) from L2
+// (two k-steps ahead), rows rw[] x 16 columns from shared memory.  MT (row tiles of 8)
+// is a template parameter so no predicated-off loads or DMMAs are issued for small blocks.
+template <int MT>
+__device__ __forceinline__ void hp_block_t(double* X, const int* rw, int S, const double* __restrict__ Ob, int lane) {
+  const int KS = (S + 3) >> 2;
+  double acc[MT][2][2];
 #pragma unroll
-  for (int mt = 0; mt < 6; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+  for (int mt = 0; mt < MT; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
   // operator fragments two k-steps ahead (ring of two register sets)
-  double A0[6], A1[6];
-  auto load = [&](double (&A)[6], int ks) {
+  double A0[MT], A1[MT];
+  auto load = [&](double (&A)[MT], int ks) {
 #pragma unroll
-    for (int mt = 0; mt < 6; ++mt)
-      if (mt < MT) A[mt] = __ldg(Ob + (ks * MT + mt) * 32 + lane);
+    for (int mt = 0; mt < MT; ++mt) A[mt] = __ldg(Ob + (ks * MT + mt) * 32 + lane);
   };
-  auto step = [&](const double (&a)[6], int ks) {
+  auto step = [&](const double (&a)[MT], int ks) {
     const int k = ks * 4 + (lane & 3);
     const int row = k < S ? rw[k] : -1;
     const double b0 = row >= 0 ? X[row * kHpLD + (lane >> 2)] : 0.0;
     const double b1 = row >= 0 ? X[row * kHpLD + 8 + (lane >> 2)] : 0.0;
 #pragma unroll
-    for (int mt = 0; mt < 6; ++mt)
-      if (mt < MT) {
-        hp_dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
-        hp_dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
-      }
+    for (int mt = 0; mt < MT; ++mt) {
+      hp_dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
+      hp_dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
+    }
   };
 #pragma unroll
-  for (int mt = 0; mt < 6; ++mt) A0[mt] = A1[mt] = 0.0;
+  for (int mt = 0; mt < MT; ++mt) A0[mt] = A1[mt] = 0.0;
   load(A0, 0);
   if (KS > 1) load(A1, 1);
   for (int ks = 0; ks < KS; ks += 2) {
     {
-      double a[6];
+      double a[MT];
 #pragma unroll
-      for (int mt = 0; mt < 6; ++mt) a[mt] = A0[mt];
+      for (int mt = 0; mt < MT; ++mt) a[mt] = A0[mt];
       if (ks + 2 < KS) load(A0, ks + 2);
       step(a, ks);
     }
     if (ks + 1 < KS) {
-      double a[6];
+      double a[MT];
 #pragma unroll
-      for (int mt = 0; mt < 6; ++mt) a[mt] = A1[mt];
+      for (int mt = 0; mt < MT; ++mt) a[mt] = A1[mt];
       if (ks + 3 < KS) load(A1, ks + 3);
       step(a, ks + 1);
     }
   }
   __syncwarp();
 #pragma unroll
-  for (int mt = 0; mt < 6; ++mt)
-    if (mt < MT) {
-      const int r = mt * 8 + (lane >> 2);
-      if (r < S) {
-        double* x = X + rw[r] * kHpLD + (lane & 3) * 2;
-        x[0] = acc[mt][0][0];
-        x[1] = acc[mt][0][1];
-        x[8] = acc[mt][1][0];
-        x[9] = acc[mt][1][1];
-      }
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = mt * 8 + (lane >> 2);
+    if (r < S) {
+      double* x = X + rw[r] * kHpLD + (lane & 3) * 2;
+      x[0] = acc[mt][0][0];
+      x[1] = acc[mt][0][1];
+      x[8] = acc[mt][1][0];
+      x[9] = acc[mt][1][1];
     }
+  }
+}
+
+__device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const double* __restrict__ Ob, int lane) {
+  switch ((S + 7) >> 3) {
+    case 1: hp_block_t<1>(X, rw, S, Ob, lane); break;
+    case 2: hp_block_t<2>(X, rw, S, Ob, lane); break;
+    case 3: hp_block_t<3>(X, rw, S, Ob, lane); break;
+    case 4: hp_block_t<4>(X, rw, S, Ob, lane); break;
+    case 5: hp_block_t<5>(X, rw, S, Ob, lane); break;
+    default: hp_block_t<6>(X, rw, S, Ob, lane); break;
+  }
 }
 
 struct HpHead {
