@@ -1228,7 +1228,11 @@ __global__ void __launch_bounds__(kHpW * 32, 2)
   __shared__ double2 s_cs[kHSolid + 1];
   const int4 tile = tiles[blockIdx.x >> 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < tn; i += blockDim.x) s_tab[i] = tab[t0 + i];
+  // block tables by cp.async: in flight behind the gather, awaited before the first phase
+  for (int i = tid; i < tn; i += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(s_tab + i))),
+                 "l"(tab + t0 + i));
   for (int r = tid; r < NC; r += blockDim.x) {
     int n, m;
     if (par)
@@ -1243,44 +1247,40 @@ __global__ void __launch_bounds__(kHpW * 32, 2)
   }
   if (tid <= P) s_cs[tid] = cs[size_t(tile.x) * (P + 1) + tid];
   __syncthreads();
-  // gather: M' = M e^{i m alpha}, then A = M'_m + M'_-m (A_0 = M'_0) or B = M'_m - M'_-m;
-  // kHpGat elements per thread at a time, all their multipole loads in flight before the
-  // first use (the kernel spent a third of its time waiting on one load pair per element)
-  for (int e0 = tid; e0 < NC * kHColsS; e0 += kHpGat * blockDim.x) {
-    double2 vp[kHpGat], vm[kHpGat];
-    int cr[kHpGat];
+  // gather: M' = M e^{i m alpha}, then A = M'_m + M'_-m (A_0 = M'_0) or B = M'_m - M'_-m.
+  // A thread owns a row (n, m) -- its rotation factor is read once -- and walks the
+  // columns kHpGat at a time with their multipole loads in flight together.
+  for (int r = tid; r < NC; r += blockDim.x) {
+    const int nm = s_nm[r], n = nm & 255, m = nm >> 8;
+    const double2 ro = s_cs[m], rc = make_double2(ro.x, -ro.y);
+    const int ip = fi(n, m), im = fi(n, -m);
 #pragma unroll
-    for (int u = 0; u < kHpGat; ++u) {
-      const int e = e0 + u * blockDim.x;
-      cr[u] = -1;
-      vp[u] = vm[u] = make_double2(0.0, 0.0);
-      if (e < NC * kHColsS) {
-        const int c = e / NC, r = e - c * NC;
-        cr[u] = c | r << 8;
-        if (s_src[c] >= 0) {
-          const int nm = s_nm[r], n = nm & 255, m = nm >> 8;
-          const double2* Mb = H.M + size_t(s_src[c]) * KP;
-          vp[u] = __ldg(Mb + fi(n, m));
-          if (m) vm[u] = __ldg(Mb + fi(n, -m));
+    for (int c0 = 0; c0 < kHColsS; c0 += kHpGat) {
+      double2 vp[kHpGat], vm[kHpGat];
+#pragma unroll
+      for (int u = 0; u < kHpGat; ++u) {
+        const int src = s_src[c0 + u];
+        vp[u] = vm[u] = make_double2(0.0, 0.0);
+        if (src >= 0) {
+          const double2* Mb = H.M + size_t(src) * KP;
+          vp[u] = __ldg(Mb + ip);
+          if (m) vm[u] = __ldg(Mb + im);
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < kHpGat; ++u) {
-      if (cr[u] < 0) continue;
-      const int c = cr[u] & 255, r = cr[u] >> 8;
-      const int m = s_nm[r] >> 8;
-      const double2 ro = s_cs[m];
-      const double2 xp = cmul(vp[u], ro);
-      double2 v = xp;
-      if (m) {
-        const double2 xm = cmul(vm[u], make_double2(ro.x, -ro.y));
-        v = par ? make_double2(xp.x - xm.x, xp.y - xm.y) : make_double2(xp.x + xm.x, xp.y + xm.y);
+      for (int u = 0; u < kHpGat; ++u) {
+        const double2 xp = cmul(vp[u], ro);
+        double2 v = xp;
+        if (m) {
+          const double2 xm = cmul(vm[u], rc);
+          v = par ? make_double2(xp.x - xm.x, xp.y - xm.y) : make_double2(xp.x + xm.x, xp.y + xm.y);
+        }
+        X[(2 * r) * kHpLD + c0 + u] = v.x;
+        X[(2 * r + 1) * kHpLD + c0 + u] = v.y;
       }
-      X[(2 * r) * kHpLD + c] = v.x;
-      X[(2 * r + 1) * kHpLD + c] = v.y;
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const double* wv = wvops + size_t(op_cls[tile.x]) * wvstride;
   const double* z = zops + size_t(tile.x) * zstride;
