@@ -670,12 +670,13 @@ __global__ void __launch_bounds__(256) k_h_p2l(HelmData H, const int* __restrict
 // column (Y^{-m} = conj(Y^m)).  8 sources in flight per CTA instead of one CTA-wide
 // table per source; the warps' partial sums are added in warp order (deterministic).
 constexpr int kHP2LSlots = 14;  // ceil(441 / 32): P <= 20
+constexpr int kHP2LBatch = 16;  // sources per warp whose radial tables are formed together, one per lane
 template <bool P2M>
 __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restrict__ boxes) {
   extern __shared__ double2 smw[];
   const int P = H.P, KP = H.KP, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
-  double2* T = smw + warp * (KP + P + 1);
-  double2* rad = T + KP;
+  double2* T = smw + warp * (KP + kHP2LBatch * (P + 1));
+  double2* rad = T + KP;  // kHP2LBatch radial tables
   const int b = boxes[blockIdx.x];
   const double4 bc = H.box[b];
   double2 acc[kHP2LSlots];
@@ -717,42 +718,72 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
       cnt = seg_at(k).y;
     }
   }
+  const double2 d00 = make_double2(0.28209479177387814347, 0.0);
   while (k < se) {
-    const int src = st + off;
-    const double4 x = H.src[src];
-    const double2 w = H.hw[src];
-    const double tx = x.x - bc.x, ty = x.y - bc.y, tz = x.z - bc.z, r2 = tx * tx + ty * ty + tz * tz;
-    if (lane == 0) radial_table(H.k, sqrt(r2), P, !P2M, rad);  // h_n / r^n (P2L), j_n / r^n (P2M)
-    if (lane <= P) {  // column m = lane of S_n^m(t), n = m..P
-      const int m = lane;
-      double2 d = make_double2(0.28209479177387814347, 0.0);
-      for (int i = 1; i <= m; ++i)
-        d = make_double2(g_sa[i] * (d.x * tx - d.y * ty), g_sa[i] * (d.x * ty + d.y * tx));
-      T[fi(m, m)] = d;
-      if (m + 1 <= P) {
-        double2 a = d, bb = make_double2(g_sb[m] * tz * d.x, g_sb[m] * tz * d.y);
-        T[fi(m + 1, m)] = bb;
-        for (int n = m + 2; n <= P; ++n) {
-          const double cn = g_sc[n * (kHSolid + 1) + m], dn = g_sd[n * (kHSolid + 1) + m] * r2;
-          const double2 c2 = make_double2(cn * (tz * bb.x - dn * a.x), cn * (tz * bb.y - dn * a.y));
-          T[fi(n, m)] = c2;
-          a = bb;
-          bb = c2;
+    // The radial tables of the warp's next kHP2LBatch sources, one source per lane (the
+    // recurrences are serial in n: one lane per table used to idle the other 31).  Lane
+    // j < kHP2LBatch walks the segment cursor j sources ahead.
+    int64_t kj = k;
+    int offj = off + lane * NW, stj = st, cntj = cnt;
+    if (lane < kHP2LBatch) {
+      while (kj < se && offj >= cntj) {
+        offj -= cntj;
+        if (++kj < se) {
+          stj = seg_at(kj).x;
+          cntj = seg_at(kj).y;
         }
       }
     }
-    __syncwarp();
-    const double2 f = make_double2(-H.k * w.y, H.k * w.x);  // i k w
-#pragma unroll
-    for (int sl = 0; sl < kHP2LSlots; ++sl) {
-      if (code[sl] < 0) continue;
-      double2 v = T[code[sl] & 0xffff];
-      if (!(code[sl] >> 30)) v.y = -v.y;  // m >= 0: conj(S_n^m)
-      const double2 fr = cmul(f, rad[(code[sl] >> 16) & 0x3fff]);
-      acc[sl] = cfma(fr, v, acc[sl]);
+    const bool valid = lane < kHP2LBatch && kj < se;
+    const int srcj = valid ? stj + offj : -1;
+    if (valid) {
+      const double4 xj = H.src[srcj];
+      const double ax = xj.x - bc.x, ay = xj.y - bc.y, az = xj.z - bc.z;
+      radial_table(H.k, sqrt(ax * ax + ay * ay + az * az), P, !P2M, rad + lane * (P + 1));
     }
+    const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));  // lanes 0 .. nvalid - 1
     __syncwarp();
-    off += NW;
+    for (int j = 0; j < nvalid; ++j) {
+      const int src = __shfl_sync(0xffffffffu, srcj, j);
+      const double4 x = H.src[src];
+      const double2 w = H.hw[src];
+      const double tx = x.x - bc.x, ty = x.y - bc.y, tz = x.z - bc.z, r2 = tx * tx + ty * ty + tz * tz;
+      const double2* rj = rad + j * (P + 1);
+      if (lane <= P) {  // column m = lane of S_n^m(t), n = m..P
+        const int m = lane;
+        double2 d = d00;
+        for (int i = 1; i <= m; ++i)
+          d = make_double2(g_sa[i] * (d.x * tx - d.y * ty), g_sa[i] * (d.x * ty + d.y * tx));
+        T[fi(m, m)] = d;
+        if (m + 1 <= P) {
+          double2 a = d, bb = make_double2(g_sb[m] * tz * d.x, g_sb[m] * tz * d.y);
+          T[fi(m + 1, m)] = bb;
+          for (int n = m + 2; n <= P; ++n) {
+            const double cn = g_sc[n * (kHSolid + 1) + m], dn = g_sd[n * (kHSolid + 1) + m] * r2;
+            const double2 c2 = make_double2(cn * (tz * bb.x - dn * a.x), cn * (tz * bb.y - dn * a.y));
+            T[fi(n, m)] = c2;
+            a = bb;
+            bb = c2;
+          }
+        }
+      }
+      __syncwarp();
+      const double2 f = make_double2(-H.k * w.y, H.k * w.x);  // i k w
+#pragma unroll
+      for (int sl = 0; sl < kHP2LSlots; ++sl) {
+        if (code[sl] < 0) continue;
+        double2 v = T[code[sl] & 0xffff];
+        if (!(code[sl] >> 30)) v.y = -v.y;  // m >= 0: conj(S_n^m)
+        const double2 fr = cmul(f, rj[(code[sl] >> 16) & 0x3fff]);
+        acc[sl] = cfma(fr, v, acc[sl]);
+      }
+      __syncwarp();
+    }
+    // the warp's cursor moves past the batch: the last valid lane's position, one step on
+    k = __shfl_sync(0xffffffffu, kj, nvalid - 1);
+    off = __shfl_sync(0xffffffffu, offj, nvalid - 1) + NW;
+    st = __shfl_sync(0xffffffffu, stj, nvalid - 1);
+    cnt = __shfl_sync(0xffffffffu, cntj, nvalid - 1);
     while (k < se && off >= cnt) {
       off -= cnt;
       if (++k < se) {
@@ -1401,7 +1432,7 @@ int helm_gather(const HelmData& H, int64_t ns, const int* perm, const double* w,
 int helm_p2m(const HelmData& H, const int* leaves, int n, cudaStream_t s) {
   if (n == 0) return 0;
   if (!H.hmu && H.KP <= 32 * kHP2LSlots) {  // single layer: one source per warp
-    const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
+    const size_t smem = size_t(8) * (H.KP + kHP2LBatch * (H.P + 1)) * sizeof(double2);
     cudaFuncSetAttribute(k_h_p2w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k_h_p2w<true><<<n, 256, smem, s>>>(H, leaves);
     return 1;
@@ -1578,7 +1609,7 @@ int helm_p2l(const HelmData& H, const int* boxes, int n, cudaStream_t s) {
   // warp per source (single layer, P <= 20); the double layer takes the CTA-wide table
   // (one more degree for the ladder identities)
   if (!H.hmu && H.KP <= 32 * kHP2LSlots) {
-    const size_t smem = size_t(8) * (H.KP + H.P + 1) * sizeof(double2);
+    const size_t smem = size_t(8) * (H.KP + kHP2LBatch * (H.P + 1)) * sizeof(double2);
     cudaFuncSetAttribute(k_h_p2w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     k_h_p2w<false><<<n, 256, smem, s>>>(H, boxes);
     return 1;
