@@ -49,6 +49,7 @@ __constant__ double c_sc[(kHSolid + 1) * (kHSolid + 1)], c_sd[(kHSolid + 1) * (k
 // the same tables in global memory, for loops whose lanes index different orders m (the
 // constant cache serialises divergent addresses; these go through L1 coalesced)
 __device__ double g_sa[kHSolid + 1], g_sb[kHSolid + 1];
+__device__ double g_sap[kHSolid + 1];  // Y_0^0 prod_{i <= m} sa_i: the diagonal S_m^m = g_sap[m] (x + i y)^m
 __device__ double g_sc[(kHSolid + 1) * (kHSolid + 1)], g_sd[(kHSolid + 1) * (kHSolid + 1)];
 
 // j_n(k r) / r^n and y_n(k r) / r^n for n <= Q without divisions in the loops:
@@ -718,7 +719,6 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
       cnt = seg_at(k).y;
     }
   }
-  const double2 d00 = make_double2(0.28209479177387814347, 0.0);
   while (k < se) {
     // The radial tables of the warp's next kHP2LBatch sources, one source per lane (the
     // recurrences are serial in n: one lane per table used to idle the other 31).  Lane
@@ -751,9 +751,15 @@ __global__ void __launch_bounds__(256, 2) k_h_p2w(HelmData H, const int* __restr
       const double2* rj = rad + j * (P + 1);
       if (lane <= P) {  // column m = lane of S_n^m(t), n = m..P
         const int m = lane;
-        double2 d = d00;
-        for (int i = 1; i <= m; ++i)
-          d = make_double2(g_sa[i] * (d.x * tx - d.y * ty), g_sa[i] * (d.x * ty + d.y * tx));
+        // diagonal S_m^m = g_sap[m] (tx + i ty)^m by repeated squaring (5 lock-step
+        // rounds instead of up to P dependent products)
+        double2 pw = make_double2(1.0, 0.0), qz = make_double2(tx, ty);
+#pragma unroll
+        for (int bit = 0; bit < 5; ++bit) {
+          if ((m >> bit) & 1) pw = cmul(pw, qz);
+          qz = cmul(qz, qz);
+        }
+        const double2 d = make_double2(g_sap[m] * pw.x, g_sap[m] * pw.y);
         T[fi(m, m)] = d;
         if (m + 1 <= P) {
           double2 a = d, bb = make_double2(g_sb[m] * tz * d.x, g_sb[m] * tz * d.y);
@@ -1417,6 +1423,10 @@ void helm_upload_constants() {
   cudaMemcpyToSymbol(c_sb, sb, sizeof(sb));
   cudaMemcpyToSymbol(c_sc, sc, sizeof(sc));
   cudaMemcpyToSymbol(c_sd, sd, sizeof(sd));
+  double sap[kHSolid + 1];
+  sap[0] = 0.28209479177387814347;
+  for (int m = 1; m <= kHSolid; ++m) sap[m] = sap[m - 1] * sa[m];
+  cudaMemcpyToSymbol(g_sap, sap, sizeof(sap));
   cudaMemcpyToSymbol(g_sa, sa, sizeof(sa));
   cudaMemcpyToSymbol(g_sb, sb, sizeof(sb));
   cudaMemcpyToSymbol(g_sc, sc, sizeof(sc));
