@@ -85,10 +85,12 @@ __device__ __forceinline__ void radial_over_rn(double k, double r, double ir, do
       else jt[n - 1] = jt[n - 1];
     }
   } else {
+    double jq[Q + 1];
+    sph_j_upto<Q>(x, jq);
     double irn = 1.0;
 #pragma unroll
     for (int n = 0; n <= Q; ++n) {
-      jt[n] = sph_j1(n, x) * irn;
+      jt[n] = jq[n] * irn;
       irn *= ir;
     }
   }
@@ -140,11 +142,7 @@ __device__ void radial_table(double k, double r, int P, bool singular, double2* 
       rad[n - 1].x = jm;
     }
   } else {
-    double irn = 1.0;
-    for (int n = 0; n <= P; ++n) {
-      rad[n].x = sph_j1(n, x) * irn;
-      irn *= ir;
-    }
+    sph_j_upto_rt(P, x, ir, rad);
   }
   if (singular) {
     double sn, cs;

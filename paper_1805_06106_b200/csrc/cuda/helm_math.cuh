@@ -54,6 +54,64 @@ __device__ inline double sph_j1(int n, double x) {
   return fabs(j0) > fabs(j1) ? tn * (j0 / t0) : tn * (j1 / tone);
 }
 
+// j_0 .. j_Q at x >= 1 from ONE downward Miller recurrence (sph_j1 per degree ran Q + 1
+// of them, each with a division per step): t_{i-1} = (2i+1)/x t_i - t_{i+1} from
+// i = Q + 30 + int(x), normalised by j_0 or j_1, whichever is larger.
+template <int Q>
+__device__ __forceinline__ void sph_j_upto(double x, double (&j)[Q + 1]) {
+  const int N = Q + 30 + int(x);
+  const double ix = 1.0 / x;
+  double t2 = 0.0, t1 = 1e-280, t[Q + 1];
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) t[n] = 0.0;
+  for (int i = N; i >= 1; --i) {
+    const double tm = (2.0 * i + 1.0) * ix * t1 - t2;
+    t2 = t1;
+    t1 = tm;
+#pragma unroll
+    for (int n = 0; n <= Q; ++n)
+      if (i - 1 == n) t[n] = tm;
+    if (fabs(t1) > 1e250) {
+      t1 *= 1e-250;
+      t2 *= 1e-250;
+#pragma unroll
+      for (int n = 0; n <= Q; ++n) t[n] *= 1e-250;
+    }
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double j0 = sn * ix, j1 = (sn * ix - cs) * ix;
+  const double sc = (Q == 0 || fabs(j0) > fabs(j1)) ? j0 / t[0] : j1 / t[Q == 0 ? 0 : 1];
+#pragma unroll
+  for (int n = 0; n <= Q; ++n) j[n] = t[n] * sc;
+}
+// the same for a runtime degree, into the real parts of out[0 .. P] times r^-n
+__device__ inline void sph_j_upto_rt(int P, double x, double ir, double2* out) {
+  const int N = P + 30 + int(x);
+  const double ix = 1.0 / x;
+  double t2 = 0.0, t1 = 1e-280;
+  for (int n = 0; n <= P; ++n) out[n].x = 0.0;
+  for (int i = N; i >= 1; --i) {
+    const double tm = (2.0 * i + 1.0) * ix * t1 - t2;
+    t2 = t1;
+    t1 = tm;
+    if (i - 1 <= P) out[i - 1].x = tm;
+    if (fabs(t1) > 1e250) {
+      t1 *= 1e-250;
+      t2 *= 1e-250;
+      for (int n = i - 1; n <= P; ++n) out[n].x *= 1e-250;
+    }
+  }
+  double sn, cs;
+  sincos(x, &sn, &cs);
+  const double j0 = sn * ix, j1 = (sn * ix - cs) * ix;
+  double sc = (P == 0 || fabs(j0) > fabs(j1)) ? j0 / out[0].x : j1 / out[P == 0 ? 0 : 1].x;
+  for (int n = 0; n <= P; ++n) {
+    out[n].x *= sc;
+    sc *= ir;
+  }
+}
+
 // normalised Y_n^m(v), n <= P, |m| <= n
 __device__ inline void ylm_all(int P, double vx, double vy, double vz, double2* Y) {
   const double r = sqrt(vx * vx + vy * vy + vz * vz);
