@@ -126,18 +126,39 @@ __global__ void __launch_bounds__(kL3Threads) k_l2qbxl3(DevData D, const int* __
   const int slot = base + __popc(bal & ((2u << lane) - 1u)) - 1;
   if (head) s_box[slot] = b;
   __syncthreads();
-  for (int e = t; e < nbox * TS; e += kL3Threads) {
-    const int sb = e / TS, r = e - sb * TS;
-    int j = int(sqrt(double(r)));
-    while (j * j > r) --j;
-    while ((j + 1) * (j + 1) <= r) ++j;
-    const int k = r - j * j - j;
-    double2 v = make_double2(0.0, 0.0);
-    if (j <= P) {
-      const double2 h = D.L[size_t(s_box[sb]) * D.kp + hidx(j, k < 0 ? -k : k)];
-      v = k >= 0 ? h : ((k & 1) ? make_double2(-h.x, h.y) : make_double2(h.x, -h.y));
+  {  // zero-padded full tables of the CTA's boxes.  A thread's table positions r = t + 128 u
+     // are the same for every box: their (degree, order) codes are formed once, and a box's
+     // loads are all in flight together.
+    constexpr int NU = 8;  // covers (P + Q + 1)^2 <= 1024
+    int code[NU];          // -2: beyond the table, -1: degree > p (zero), else hidx | conj << 16 | odd << 17
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int r = t + u * kL3Threads;
+      code[u] = -2;
+      if (r < TS) {
+        int j = int(sqrt(double(r)));
+        while (j * j > r) --j;
+        while ((j + 1) * (j + 1) <= r) ++j;
+        const int k = r - j * j - j;
+        code[u] = j <= P ? (hidx(j, k < 0 ? -k : k) | (k < 0 ? 1 << 16 : 0) | ((k & 1) << 17)) : -1;
+      }
     }
-    s_tab[e] = v;
+    for (int sb = 0; sb < nbox; ++sb) {
+      const double2* __restrict__ Lb = D.L + size_t(s_box[sb]) * D.kp;
+      double2 h[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        h[u] = make_double2(0.0, 0.0);
+        if (code[u] >= 0) h[u] = Lb[code[u] & 0xffff];
+      }
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (code[u] >= -1) {
+          double2 v = h[u];
+          if (code[u] >= 0 && (code[u] >> 16 & 1)) v = (code[u] >> 17 & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
+          s_tab[sb * TS + t + u * kL3Threads] = v;
+        }
+    }
   }
   __syncthreads();
   if (!active) return;
