@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kL3Threads) k_l2qbxl3(DevData D, const int* __
         cur = make_double2(z * diag.x, z * diag.y);
       } else {
         const double c1 = (2 * N - 1) * z;
-        const double f = 1.0 / double((N - K) * (N + K));
+        const double f = c_inv_nm[hidx(N, K)];  // 1 / ((N - K)(N + K)), uniform across the CTA
         cur = make_double2((c1 * rb.x - r2 * ra.x) * f, (c1 * rb.y - r2 * ra.y) * f);
       }
       if (N > K) {
@@ -240,6 +240,7 @@ void l2qbxl3_q(const DevData& D, const int* items, const int2* ctas, int n_ctas,
     cudaFuncSetAttribute(k_l2qbxl3<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+  upload_inv_nm();  // this translation unit's copy of the reciprocal table
   k_l2qbxl3<Q><<<n_ctas, kL3Threads, smem, s>>>(D, items, ctas, ctr_box);
 }
 
