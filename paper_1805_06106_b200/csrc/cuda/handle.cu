@@ -837,7 +837,12 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   QCK(cudaSetDevice(device));
   dev::upload_constants();
   dev::set_smem_limits();
-  QCK(cudaStreamCreateWithFlags(&H.stream, cudaStreamNonBlocking));
+  // the main stream outranks the side stream: with the near field forked beside the
+  // far-field chain, the chain's CTAs are placed first as SMs free up and the near field's
+  // many short CTAs fill what the chain leaves idle (small tree-shift levels, kernel tails)
+  int prio_lo = 0, prio_hi = 0;
+  QCK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  QCK(cudaStreamCreateWithPriority(&H.stream, cudaStreamNonBlocking, prio_hi));
   for (auto& e : H.ev) QCK(cudaEventCreate(&e));
   for (auto& e : H.evx) QCK(cudaEventCreate(&e));
   // near field beside the far-field chain: off by default on one GPU (both live on the
@@ -845,7 +850,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
   // (it hides the multipole exchange); qbxg_set_overlap opts in
   H.overlap = false;
   H.debug_sync = std::getenv("QBXG_DEBUG_SYNC") != nullptr;
-  QCK(cudaStreamCreateWithFlags(&H.side, cudaStreamNonBlocking));
+  QCK(cudaStreamCreateWithPriority(&H.side, cudaStreamNonBlocking, prio_lo));
   QCK(cudaEventCreateWithFlags(&H.fork_ev, cudaEventDisableTiming));
   QCK(cudaEventCreateWithFlags(&H.join_ev, cudaEventDisableTiming));
   cudaStream_t s = H.stream;

@@ -274,17 +274,18 @@ struct NearCtr {
 };
 __device__ __forceinline__ NearCtr near_ctr(const double4 c) { return NearCtr{c, 1.0 / c.w}; }
 
-// SL+DL in one pass: the table J' and its derivative along the dipole, dJ' = (mu . grad_u) J'
-// (forward-mode: every recurrence step carries its derivative), to degree q only --
-// L~_c = (1/r_c^2) (2n-1)!! [w r_c J'_n + dJ'_n]; 25 fewer fp64 operations per pair at q = 5
-// than forming J' to degree q + 1 and contracting g (near_acc).
-__device__ __forceinline__ void near_put(double2& J, double2& dJ, double& ax, double& ay, const double w,
-                                         const bool re_only, const double jx, const double jy, const double djx,
-                                         const double djy) {
+// SL+DL in one pass: the table J' and, carried by the same recurrences, the combination
+// V = w r_c J' + dJ' that is accumulated, dJ' = (mu . grad_u) J' being the derivative along
+// the dipole (forward mode, to degree q only) -- L~_c = (1/r_c^2) (2n-1)!! V_n.  Every
+// recurrence is linear in J', so V obeys it too with the source terms of dJ':
+//   V_n = vz V_{n-1} + rc V_{n-2} + dvz J_{n-1} + rc (-2t) J_{n-2},
+// one add per coefficient component instead of a multiply-add and an add.
+__device__ __forceinline__ void near_put(double2& J, double2& V, double& ax, double& ay, const bool re_only,
+                                         const double jx, const double jy, const double vx, const double vy) {
   J = make_double2(jx, jy);
-  dJ = make_double2(djx, djy);
-  ax = fma(w, jx, ax) + djx;
-  if (!re_only) ay = fma(-w, jy, ay) - djy;
+  V = make_double2(vx, vy);
+  ax += vx;
+  if (!re_only) ay -= vy;
 }
 
 template <int Q>
@@ -298,14 +299,14 @@ __device__ __forceinline__ void near_pair_dip(const double4 x, const double4 mu,
   const double vx = ux * ir2, vy = uy * ir2, vz = uz * ir2;                     // v = u / |u|^2
   const double dvx = fma(m2t, vx, mu.x * ir2), dvy = fma(m2t, vy, mu.y * ir2), dvz = fma(m2t, vz, mu.z * ir2);
   const double w = x.w * c.c.w;
-  double2 J[hsize(Q)], dJ[hsize(Q)];
-#define put(id, re_only, jx, jy, djx, djy) near_put(J[id], dJ[id], ax[id], ay[id], w, re_only, jx, jy, djx, djy)
+  double2 J[hsize(Q)], V[hsize(Q)];
+#define put(id, re_only, jx, jy, wx, wy) near_put(J[id], V[id], ax[id], ay[id], re_only, jx, jy, wx, wy)
 #pragma unroll
   for (int m = 0; m <= Q; ++m) {
     if (m == 0) {
-      put(0, true, rs, 0.0, -rs * t, 0.0);  // |u|^-1' = -|u|^-3 u.mu
+      put(0, true, rs, 0.0, rs * (w - t), 0.0);  // |u|^-1' = -|u|^-3 u.mu
     } else {
-      const double2 d = J[hidx(m - 1, m - 1)], e = dJ[hidx(m - 1, m - 1)];
+      const double2 d = J[hidx(m - 1, m - 1)], e = V[hidx(m - 1, m - 1)];
       if (m == 1)
         put(hidx(1, 1), false, d.x * vx, d.x * vy, fma(e.x, vx, d.x * dvx), fma(e.x, vy, d.x * dvy));
       else
@@ -313,7 +314,7 @@ __device__ __forceinline__ void near_pair_dip(const double4 x, const double4 mu,
             fma(e.x, vx, fma(d.x, dvx, fma(-e.y, vy, -d.y * dvy))), fma(e.x, vy, fma(d.x, dvy, fma(e.y, vx, d.y * dvx))));
     }
     if (m + 1 <= Q) {
-      const double2 d = J[hidx(m, m)], e = dJ[hidx(m, m)];
+      const double2 d = J[hidx(m, m)], e = V[hidx(m, m)];
       if (m == 0)
         put(hidx(1, 0), true, vz * d.x, 0.0, fma(vz, e.x, dvz * d.x), 0.0);
       else
@@ -322,15 +323,15 @@ __device__ __forceinline__ void near_pair_dip(const double4 x, const double4 mu,
 #pragma unroll
     for (int n = 2; n <= Q; ++n) {  // constant trip count: the nest unrolls fully
       if (n < m + 2) continue;
-      const double rc = -near_cnm(n, m) * ir2;  // (rc a)' = rc (a' - 2 t a)
+      const double rc = -near_cnm(n, m) * ir2, rcm = rc * m2t;  // (rc a)' = rc (a' - 2 t a)
       const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
-      const double2 da = dJ[hidx(n - 2, m)], db = dJ[hidx(n - 1, m)];
+      const double2 va = V[hidx(n - 2, m)], vb = V[hidx(n - 1, m)];
       if (m == 0)
-        put(hidx(n, 0), true, fma(vz, b.x, rc * a.x), 0.0, fma(vz, db.x, fma(dvz, b.x, rc * fma(m2t, a.x, da.x))), 0.0);
+        put(hidx(n, 0), true, fma(vz, b.x, rc * a.x), 0.0, fma(vz, vb.x, fma(rc, va.x, fma(dvz, b.x, rcm * a.x))), 0.0);
       else
         put(hidx(n, m), false, fma(vz, b.x, rc * a.x), fma(vz, b.y, rc * a.y),
-            fma(vz, db.x, fma(dvz, b.x, rc * fma(m2t, a.x, da.x))),
-            fma(vz, db.y, fma(dvz, b.y, rc * fma(m2t, a.y, da.y))));
+            fma(vz, vb.x, fma(rc, va.x, fma(dvz, b.x, rcm * a.x))),
+            fma(vz, vb.y, fma(rc, va.y, fma(dvz, b.y, rcm * a.y))));
     }
   }
 #undef put
