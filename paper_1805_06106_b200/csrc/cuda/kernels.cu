@@ -846,29 +846,35 @@ __global__ void __launch_bounds__(128, P >= 12 ? 4 : 1) k_p2l3(DevData D, const 
     }
     __syncwarp(smask);
     const double w = x.w;
-    const double hx = 0.5 * mu.x * ih, hy = 0.5 * mu.y * ih, mz = mu.z * ih;
-    // column state: c0 = I_n^m, c0n = I_{n+1}^m, cp/cpp = I_{n+1}^{m+1}/I_n^{m+1},
-    // cm/cmp = I_{n+1}^{m-1}/I_n^{m-1}
+    // SL + DL in one recurrence per column: V_n^m = w I_n^m + (mu' . grad_u) I_n^m with
+    // mu' = mu / |b| obeys the column recurrence of I_n^m plus source terms (forward-mode
+    // derivative; d(1/r^2) = -2t/r^2, t = u.mu'/r^2):
+    //   V_{n+2} = ((2n+3) uz V_{n+1} - a V_n)/r^2 + (2n+3) mu'_z I_{n+1}/r^2 - 2t I_{n+2},
+    //   V_m^m   = w D_m - (2m+1) t D_m + m (2m-1) (mu'_x + i mu'_y) D_{m-1} / r^2,
+    // so the neighbouring order columns I^{m+-1} are no longer formed in every lane.
+    const double mx = mu.x * ih, my = mu.y * ih, mz = mu.z * ih;
+    const double t = ir2 * (ux * mx + uy * my + uz * mz), m2t = -2.0 * t;
+    // column state: ia = I_n^m, ib = I_{n+1}^m, va / vb the same for V
     int m = 0, n = 0;
-    double2 c0 = {}, c0n = {}, cp = {}, cpp = {}, cm = {}, cmp = {};
+    double2 ia = {}, ib = {}, va = {}, vb = {};
     auto init = [&](int mm) {
       m = mm;
       n = mm;
-      const double2 dm = s_diag[sl][mm], dp = s_diag[sl][mm + 1];
-      c0 = dm;
+      const double2 dm = s_diag[sl][mm];
+      ia = dm;
       const double f0 = (2 * mm + 1) * uz * ir2;
-      c0n = make_double2(f0 * dm.x, f0 * dm.y);
-      cp = dp;
-      cpp = make_double2(0.0, 0.0);
-      if (mm > 0) {
-        const double2 dd = s_diag[sl][mm - 1];
-        const double fa = (2 * mm - 1) * uz * ir2;
-        const double2 a = make_double2(fa * dd.x, fa * dd.y);  // I_mm^{mm-1}
-        const double c1 = (2 * mm + 1) * uz, c2 = double(2 * mm - 1);
-        cm = make_double2((c1 * a.x - c2 * dd.x) * ir2, (c1 * a.y - c2 * dd.y) * ir2);
-        cmp = a;
-      } else {
-        cm = cmp = make_double2(0.0, 0.0);
+      ib = make_double2(f0 * dm.x, f0 * dm.y);
+      if (DIP) {
+        const double k0 = w - (2 * mm + 1) * t;
+        va = make_double2(k0 * dm.x, k0 * dm.y);
+        if (mm > 0) {
+          const double2 dd = s_diag[sl][mm - 1];
+          const double kd = double(mm * (2 * mm - 1)) * ir2;
+          va.x = fma(kd, mx * dd.x - my * dd.y, va.x);
+          va.y = fma(kd, mx * dd.y + my * dd.x, va.y);
+        }
+        const double df0 = (2 * mm + 1) * ir2 * fma(uz, m2t, mz);
+        vb = make_double2(fma(f0, va.x, df0 * dm.x), fma(f0, va.y, df0 * dm.y));
       }
     };
     if (nA + nB > 0) init(nA > 0 ? mA : mB);
@@ -876,29 +882,26 @@ __global__ void __launch_bounds__(128, P >= 12 ? 4 : 1) k_p2l3(DevData D, const 
     for (int tt = 0; tt < P + 2; ++tt) {
       if (tt < nA + nB) {
         if (tt == nA && tt > 0) init(mB);
-        acc[tt].x = fma(w, c0.x, acc[tt].x);
-        acc[tt].y = fma(-w, c0.y, acc[tt].y);
         if (DIP) {
-          const double2 im = m == 0 ? make_double2(-cp.x, cp.y) : cm;
-          const double gx = -mz * c0n.x + (hx * im.x - hy * im.y) - (hx * cp.x + hy * cp.y);
-          const double gy = -mz * c0n.y + (hx * im.y + hy * im.x) - (hx * cp.y - hy * cp.x);
-          acc[tt].x += gx;
-          acc[tt].y -= gy;
+          acc[tt].x += va.x;
+          acc[tt].y -= va.y;
+        } else {
+          acc[tt].x = fma(w, ia.x, acc[tt].x);
+          acc[tt].y = fma(-w, ia.y, acc[tt].y);
         }
         if (tt + 1 < nA + nB) {  // advance n -> n + 1
           const double c1 = (2 * n + 3) * uz;
-          const int n1 = (n + 1) * (n + 1);
-          const double a0 = double(n1 - m * m), ap = double(n1 - (m + 1) * (m + 1)),
-                       am = double(n1 - (m - 1) * (m - 1));
-          const double2 nc0n = make_double2((c1 * c0n.x - a0 * c0.x) * ir2, (c1 * c0n.y - a0 * c0.y) * ir2);
-          const double2 ncp = make_double2((c1 * cp.x - ap * cpp.x) * ir2, (c1 * cp.y - ap * cpp.y) * ir2);
-          const double2 ncm = make_double2((c1 * cm.x - am * cmp.x) * ir2, (c1 * cm.y - am * cmp.y) * ir2);
-          c0 = c0n;
-          c0n = nc0n;
-          cpp = cp;
-          cp = ncp;
-          cmp = cm;
-          cm = ncm;
+          const double a0 = double((n + 1) * (n + 1) - m * m);
+          const double2 nib = make_double2((c1 * ib.x - a0 * ia.x) * ir2, (c1 * ib.y - a0 * ia.y) * ir2);
+          if (DIP) {
+            const double k1 = (2 * n + 3) * mz * ir2;
+            const double2 nvb = make_double2(fma(m2t, nib.x, fma(k1, ib.x, (c1 * vb.x - a0 * va.x) * ir2)),
+                                             fma(m2t, nib.y, fma(k1, ib.y, (c1 * vb.y - a0 * va.y) * ir2)));
+            va = vb;
+            vb = nvb;
+          }
+          ia = ib;
+          ib = nib;
           ++n;
         }
       }
