@@ -278,7 +278,7 @@ __device__ __forceinline__ NearCtr near_ctr(const double4 c) { return NearCtr{c,
 // V = w r_c J' + dJ' that is accumulated, dJ' = (mu . grad_u) J' being the derivative along
 // the dipole (forward mode, to degree q only) -- L~_c = (1/r_c^2) (2n-1)!! V_n.  Every
 // recurrence is linear in J', so V obeys it too with the source terms of dJ':
-//   V_n = vz V_{n-1} + rc V_{n-2} + dvz J_{n-1} + rc (-2t) J_{n-2},
+//   V_n = vz V_{n-1} + rc (V_{n-2} - 2t J_{n-2}) + dvz J_{n-1},
 // one add per coefficient component instead of a multiply-add and an add.
 __device__ __forceinline__ void near_put(double2& J, double2& V, double& ax, double& ay, const bool re_only,
                                          const double jx, const double jy, const double vx, const double vy) {
@@ -323,15 +323,15 @@ __device__ __forceinline__ void near_pair_dip(const double4 x, const double4 mu,
 #pragma unroll
     for (int n = 2; n <= Q; ++n) {  // constant trip count: the nest unrolls fully
       if (n < m + 2) continue;
-      const double rc = -near_cnm(n, m) * ir2, rcm = rc * m2t;  // (rc a)' = rc (a' - 2 t a)
+      const double rc = -near_cnm(n, m) * ir2;  // (rc a)' = rc (a' - 2 t a)
       const double2 a = J[hidx(n - 2, m)], b = J[hidx(n - 1, m)];
       const double2 va = V[hidx(n - 2, m)], vb = V[hidx(n - 1, m)];
       if (m == 0)
-        put(hidx(n, 0), true, fma(vz, b.x, rc * a.x), 0.0, fma(vz, vb.x, fma(rc, va.x, fma(dvz, b.x, rcm * a.x))), 0.0);
+        put(hidx(n, 0), true, fma(vz, b.x, rc * a.x), 0.0, fma(vz, vb.x, fma(rc, fma(m2t, a.x, va.x), dvz * b.x)), 0.0);
       else
         put(hidx(n, m), false, fma(vz, b.x, rc * a.x), fma(vz, b.y, rc * a.y),
-            fma(vz, vb.x, fma(rc, va.x, fma(dvz, b.x, rcm * a.x))),
-            fma(vz, vb.y, fma(rc, va.y, fma(dvz, b.y, rcm * a.y))));
+            fma(vz, vb.x, fma(rc, fma(m2t, a.x, va.x), dvz * b.x)),
+            fma(vz, vb.y, fma(rc, fma(m2t, a.y, va.y), dvz * b.y)));
     }
   }
 #undef put
