@@ -435,7 +435,10 @@ def run_ours(args, rank, world, local_rank):
                 bt.append(e0.elapsed_time(e1))
         bms = float(np.mean(bt)) / R
         batch = {"n_rhs": R, "ms_per_density": round(bms, 3), "value": units / (bms * 1e-3), "unit": "points/s",
-                 "note": "near field shares one harmonic table per (centre, source) pair between 2 densities"}
+                 "note": ("SL+DL: densities run one by one on the resident plan (the single-density near field is cheaper "
+                          "per density than a shared harmonic table plus a contraction per density)"
+                          if cfg.kernel == 1 else
+                          "near field shares one harmonic table per (centre, source) pair between 2 densities")}
 
     # roofline of the dominant kernel, per-stage fractions
     peak = api.measure_fp64_peak(local_rank)

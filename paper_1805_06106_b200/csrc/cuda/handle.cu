@@ -1447,7 +1447,10 @@ void check_domain(Handle& H, cudaStream_t s) {
 void batch_apply(Handle& H, int R, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs,
                  cudaStream_t s) {
   dev::DevData& D = H.D;
-  const int NR = dev::near_batch_width(D.q);
+  // SL+DL: the single-density near field (V-form, kernels.cu near_pair_dip) costs less per
+  // density than the shared harmonic table plus one contraction per density (76.9 vs 81.6 ms
+  // per density at config 1), so only the single layer is batched through the near field
+  const int NR = D.dipole ? 1 : dev::near_batch_width(D.q);
   if (H.nranks > 1 || NR < 2 || R < 2) {
     for (int r = 0; r < R; ++r)
       full_apply(H, d_w + size_t(r) * H.ns, d_mu ? d_mu + size_t(r) * 3 * H.ns : nullptr, d_pot + size_t(r) * H.nt,
