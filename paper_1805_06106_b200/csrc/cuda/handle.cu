@@ -417,7 +417,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
       const int cls = int(key[k] >> 44);
       size_t k1 = k;
       while (k1 < key.size() && int(key[k1] >> 44) == cls && k1 - k < size_t(BN)) ++k1;
-      T.push_back(make_int4(cls, int(k), int(k1 - k), 0));
+      T.push_back(make_int4(cls, int(k), int(k1 - k), cls_rxy2[cls] == 0 ? 1 : 0));  // .w: offset on the z axis
       work += 64 + int64_t((k1 - k + 7) / 8) * 256;
       k = k1;
     }
@@ -433,7 +433,7 @@ void build_m2l(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& v
   std::vector<int> grp_tiles{0};
   for (int g = 0; g < ng; ++g) {
     const int64_t e0 = vs[tb[size_t(g) * G]];
-    for (int4 t : gtiles[g]) tiles.push_back(make_int4(t.x, int(e0 + t.y), t.z, 0));
+    for (int4 t : gtiles[g]) tiles.push_back(make_int4(t.x, int(e0 + t.y), t.z, t.w));
     grp_tiles.push_back(int(tiles.size()));
   }
   std::vector<int> order(ng);

@@ -78,7 +78,7 @@ struct M2LPlan {
   int* grp_order = nullptr;    // launch order (heaviest first)
   int* grp_tiles = nullptr;    // n_groups + 1 tile offsets
   int* grp_box = nullptr;      // n_groups x G target boxes (-1: none)
-  int4* tiles = nullptr;       // (class, first column, columns, 0)
+  int4* tiles = nullptr;       // (class, first column, columns, 1 if the class lies on the z axis: W = V = identity)
   int* col_src = nullptr;      // source box of each column
   int* col_meta = nullptr;     // target slot | offset id << 8 | kPasMirror if dz < 0
 };

@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kNTh, 2)
     // 2. W, Z, V in place
 #pragma unroll 1
     for (int ph = 0; ph < kPasPhases; ++ph) {
+      if (tl.w && ph != 1) continue;  // offset along +z (after mirroring): the rotations are the identity
       const double* Op = ops + size_t(tl.x) * op_stride + size_t(ph) * phase_size;
       const int* T = s_tab + tab_base(ph);
       const int nblk = T[0];
