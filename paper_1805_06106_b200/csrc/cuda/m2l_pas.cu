@@ -12,16 +12,21 @@
 //                                                (-1)^{n+m} (j+n)! / |v'|^{j+n+1}, the same for Re and Im
 //   V (local rotation back):                    per degree n, like W
 // 3 x 2,736 multiply-adds per List-2 entry at p = 15 instead of 32,896 for the two dense
-// azimuthal blocks.  W, Z and V depend on (rho_xy^2, dz) only: the 1,206 offsets of
-// [-5,5]^3 fall into 190 classes, one operator set per class (~19 MB at p = 15).
+// azimuthal blocks.  W, Z and V depend on (rho_xy^2, dz) only, and an offset below the
+// xy-plane is the mirror image of one above it: T(rho, -dz) = S T(rho, dz) S with the
+// diagonal sign S = (-1)^{n+m} on both expansions.  So the 1,206 offsets of [-5,5]^3 fall
+// into 102 classes (rho_xy^2, |dz|), one operator set per class (~10 MB at p = 15); the
+// signs are applied in the gather and the accumulate (kPasMirror column flag).  Classes on
+// the z axis (rho_xy = 0) have W = V = identity: their tiles run the Z phase only.
 //
 // Work split (target-grouped).  One CTA owns a group of G target boxes (48 at p <= 16,
-// consecutive in DFS order) and walks a host-built list of tiles: a tile is <= BN
-// List-2 entries of the group that share an operator class, columns sorted by
+// consecutive in DFS order) and walks a host-built list of tiles: a tile is <= BN (40 at
+// p <= 15) List-2 entries of the group that share an operator class, columns sorted by
 // (target slot, offset).  Two CTAs of 8 warps share an SM (one CTA's gather, barriers
 // and accumulate overlap the other's DMMA phases).  Per tile:
 //   1. the columns' multipoles are read from L2 and rotated by e^{i k alpha} into the
-//      (p+1)^2 x BN real tile X in shared memory (XOR-swizzled);
+//      (p+1)^2 x BN real tile X in shared memory (XOR-swizzled): a warp takes a column at
+//      a time, lane l the coefficients l + 32 k (row codes packed in registers);
 //   2. W, Z and V run in place on X as m8n8k4 DMMAs; each phase's blocks (sub-blocks
 //      merged block-diagonally where that costs no extra fragments: 17 per phase at
 //      p = 15) are balanced over the warps; operator blocks are stored in DMMA
