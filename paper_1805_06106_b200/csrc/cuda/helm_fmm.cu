@@ -916,7 +916,6 @@ __global__ void __launch_bounds__(256) k_h_ctr(HelmData H, int singular, const d
     const int ns = amu == 0 ? 1 : 2;  // sign index 0: mu = +|mu|, 1: mu = -|mu|
     // C_mu[i'][l] = 4 pi sum_n i^{n'+l-n} G(n, m'+mu; n', m'; l) X_n^{m'+mu} over the used
     // terms only: l >= |mu| and n + n' + l even
-    const int NLm = NL - amu;
     // the last warp forms the centres' F columns (a recurrence in l per centre) while the
     // other warps contract C_mu, so the column recurrence is off the critical path
     // (thread = row i' x one of c_ng residue classes of l: no index divisions in the loop;
