@@ -1241,6 +1241,86 @@ __device__ __forceinline__ void hp_block(double* X, const int* rw, int S, const 
   }
 }
 
+// W / V: the Re rows and the Im rows of a degree take the same real operator, so one call
+// serves both (rw[0..S) Re rows, rw[S..2S) Im rows): the operator fragments are read from L2
+// once and feed four DMMAs (two column groups x Re / Im) instead of two.
+template <int MT>
+__device__ __forceinline__ void hp_block_dual_t(double* X, const int* rw, int S, const double* __restrict__ Ob,
+                                                int lane) {
+  const int KS = (S + 3) >> 2;
+  double acc[MT][4][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[mt][g][0] = acc[mt][g][1] = 0.0;
+  double A0[MT], A1[MT];
+  auto load = [&](double (&A)[MT], int ks) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) A[mt] = __ldg(Ob + (ks * MT + mt) * 32 + lane);
+  };
+  auto step = [&](const double (&a)[MT], int ks) {
+    const int k = ks * 4 + (lane & 3);
+    const int rr = k < S ? rw[k] : -1, ri = k < S ? rw[S + k] : -1;
+    const double b0 = rr >= 0 ? X[rr * kHpLD + (lane >> 2)] : 0.0;
+    const double b1 = rr >= 0 ? X[rr * kHpLD + 8 + (lane >> 2)] : 0.0;
+    const double b2 = ri >= 0 ? X[ri * kHpLD + (lane >> 2)] : 0.0;
+    const double b3 = ri >= 0 ? X[ri * kHpLD + 8 + (lane >> 2)] : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      hp_dmma(acc[mt][0][0], acc[mt][0][1], a[mt], b0);
+      hp_dmma(acc[mt][1][0], acc[mt][1][1], a[mt], b1);
+      hp_dmma(acc[mt][2][0], acc[mt][2][1], a[mt], b2);
+      hp_dmma(acc[mt][3][0], acc[mt][3][1], a[mt], b3);
+    }
+  };
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) A0[mt] = A1[mt] = 0.0;
+  load(A0, 0);
+  if (KS > 1) load(A1, 1);
+  for (int ks = 0; ks < KS; ks += 2) {
+    {
+      double a[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = A0[mt];
+      if (ks + 2 < KS) load(A0, ks + 2);
+      step(a, ks);
+    }
+    if (ks + 1 < KS) {
+      double a[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = A1[mt];
+      if (ks + 3 < KS) load(A1, ks + 3);
+      step(a, ks + 1);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int r = mt * 8 + (lane >> 2);
+    if (r < S) {
+      double* x = X + rw[r] * kHpLD + (lane & 3) * 2;
+      x[0] = acc[mt][0][0];
+      x[1] = acc[mt][0][1];
+      x[8] = acc[mt][1][0];
+      x[9] = acc[mt][1][1];
+      double* y = X + rw[S + r] * kHpLD + (lane & 3) * 2;
+      y[0] = acc[mt][2][0];
+      y[1] = acc[mt][2][1];
+      y[8] = acc[mt][3][0];
+      y[9] = acc[mt][3][1];
+    }
+  }
+}
+
+__device__ __forceinline__ void hp_block_dual(double* X, const int* rw, int S, const double* __restrict__ Ob,
+                                              int lane) {
+  switch ((S + 7) >> 3) {
+    case 1: hp_block_dual_t<1>(X, rw, S, Ob, lane); break;
+    case 2: hp_block_dual_t<2>(X, rw, S, Ob, lane); break;
+    default: hp_block_dual_t<3>(X, rw, S, Ob, lane); break;  // S <= P + 1 = 21
+  }
+}
+
 struct HpHead {
   int base[2][3];  // table offset of (parity, phase)
 };
@@ -1332,7 +1412,10 @@ __global__ void __launch_bounds__(kHpW * 32, 2)
 #pragma unroll 1
     for (int i = woff[warp]; i < woff[warp + 1]; ++i) {
       const int b = wblk[i];
-      hp_block(X, rows + rowoff[b], bsz[b], Op + opoff[b], lane);
+      if (ph == 1)
+        hp_block(X, rows + rowoff[b], bsz[b], Op + opoff[b], lane);
+      else
+        hp_block_dual(X, rows + rowoff[b], bsz[b] >> 1, Op + opoff[b], lane);  // Re rows, then Im rows
     }
     __syncthreads();
   }
@@ -1504,13 +1587,13 @@ void helm_pas_tables(int P, const size_t* wv_off_w0, const size_t* wv_off_w1, co
       auto cr = [&](int n, int m) { return par ? od(n, m) : ev(n, m); };
       if (ph != 1) {
         const size_t* off = ph == 0 ? (par ? wv_off_w1 : wv_off_w0) : (par ? wv_off_v1 : wv_off_v0);
-        for (int n = par; n <= P; ++n)
-          for (int part = 0; part < 2; ++part) {  // Re rows, then Im rows, same operator
-            std::vector<int> b;
+        for (int n = par; n <= P; ++n) {  // one block per degree: Re rows, then Im rows, same operator
+          std::vector<int> b;
+          for (int part = 0; part < 2; ++part)
             for (int m = par; m <= n; ++m) b.push_back(2 * cr(n, m) + part);
-            blocks.push_back(b);
-            opo.push_back(int(off[n - par]));
-          }
+          blocks.push_back(b);
+          opo.push_back(int(off[n - par]));
+        }
       } else {
         for (int m = par; m <= P; ++m) {
           std::vector<int> b;
@@ -1534,9 +1617,9 @@ void helm_pas_tables(int P, const size_t* wv_off_w0, const size_t* wv_off_w1, co
       tab.insert(tab.end(), rows.begin(), rows.end());
       std::vector<int> order(nb);
       for (int i = 0; i < nb; ++i) order[i] = i;
-      auto cost = [&](int i) {
-        const int sz = int(blocks[i].size());
-        return long((sz + 7) / 8) * ((sz + 3) / 4);
+      auto cost = [&](int i) {  // DMMA fragments; a W / V block holds two row sets of half its size
+        const int sz = ph == 1 ? int(blocks[i].size()) : int(blocks[i].size()) / 2;
+        return long((sz + 7) / 8) * ((sz + 3) / 4) * (ph == 1 ? 1 : 2);
       };
       std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
       std::vector<std::vector<int>> wl(kHpW);
