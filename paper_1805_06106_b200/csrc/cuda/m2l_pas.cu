@@ -185,45 +185,49 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 // k >= S read the zero row), the DMMAs, and the rows written back.  Tile j's reads
 // feed its DMMAs, which precede its writes; other tiles touch other columns.
 template <int S, int BN, int ZR>
-__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, int lane, int nt) {
+__device__ __forceinline__ void pas_block(double* X, const int* rw, const double* Ob, int lane, int nt, bool dual) {
   constexpr int MT = (S + 7) / 8, KS = (S + 3) / 4;
   double a[MT][KS];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) a[mt][ks] = Ob[(mt * KS + ks) * 32 + lane];
-  int rb[KS], ro[MT];
-#pragma unroll
-  for (int ks = 0; ks < KS; ++ks) {
-    const int k = ks * 4 + (lane & 3);
-    const int t = k < S ? rw[k] : ZR * BN;  // row offset | swizzle << 16
-    rb[ks] = (t & 0xffff) + ((lane >> 2) ^ (t >> 16));
-  }
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int i = mt * 8 + (lane >> 2);
-    const int t = i < S ? rw[i] : -1;
-    ro[mt] = t < 0 ? -1 : (t & 0xffff) + (((lane & 3) * 2) ^ (t >> 16));
-  }
+  // a dual block (Z of order m >= 1) applies the same fragments to a second row set
 #pragma unroll 1
-  for (int j = 0; j < nt; ++j) {
-    double b[KS];
+  for (int part = 0; part < (dual ? 2 : 1); ++part, rw += S) {
+    int rb[KS], ro[MT];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) b[ks] = X[col_group<BN>(rb[ks], j)];
-    double acc[MT][2];
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + (lane & 3);
+      const int t = k < S ? rw[k] : ZR * BN;  // row offset | swizzle << 16
+      rb[ks] = (t & 0xffff) + ((lane >> 2) ^ (t >> 16));
+    }
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    for (int mt = 0; mt < MT; ++mt) {
+      const int i = mt * 8 + (lane >> 2);
+      const int t = i < S ? rw[i] : -1;
+      ro[mt] = t < 0 ? -1 : (t & 0xffff) + (((lane & 3) * 2) ^ (t >> 16));
+    }
+#pragma unroll 1
+    for (int j = 0; j < nt; ++j) {
+      double b[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
+      for (int ks = 0; ks < KS; ++ks) b[ks] = X[col_group<BN>(rb[ks], j)];
+      double acc[MT][2];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], a[mt][ks], b[ks]);
-    __syncwarp();
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-      if (ro[mt] >= 0) {
-        X[col_group<BN>(ro[mt], j)] = acc[mt][0];
-        X[col_group<BN>(ro[mt], j) ^ 1] = acc[mt][1];
-      }
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], a[mt][ks], b[ks]);
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        if (ro[mt] >= 0) {
+          X[col_group<BN>(ro[mt], j)] = acc[mt][0];
+          X[col_group<BN>(ro[mt], j) ^ 1] = acc[mt][1];
+        }
+    }
   }
 }
 
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(kNTh, 2)
       const int* wblk = woff + kWarps + 1;
 #define QBXG_PAS_CASE(S) \
   case S:                \
-    if (S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt); \
+    if (S <= kMaxBlock) pas_block<S, BN, NROW>(X, rw, Ob, lane, nt, dual); \
     break;
       const int i_end = woff[warp + 1];
 #pragma unroll 1
@@ -394,7 +398,8 @@ __global__ void __launch_bounds__(kNTh, 2)
         const int b = wblk[i];
         const int* rw = rows + rowoff[b];
         const double* Ob = Op + opoff[b];
-        switch (rowoff[b + 1] - rowoff[b]) {
+        const bool dual = ph == 1 && b > 0;  // Z of order m >= 1: Re rows, then Im rows
+        switch ((rowoff[b + 1] - rowoff[b]) >> (dual ? 1 : 0)) {
           QBXG_PAS_CASE(1) QBXG_PAS_CASE(2) QBXG_PAS_CASE(3) QBXG_PAS_CASE(4) QBXG_PAS_CASE(5) QBXG_PAS_CASE(6)
           QBXG_PAS_CASE(7) QBXG_PAS_CASE(8) QBXG_PAS_CASE(9) QBXG_PAS_CASE(10) QBXG_PAS_CASE(11)
           QBXG_PAS_CASE(12) QBXG_PAS_CASE(13) QBXG_PAS_CASE(14) QBXG_PAS_CASE(15) QBXG_PAS_CASE(16)
@@ -474,19 +479,30 @@ __global__ void __launch_bounds__(kNTh, 2)
 struct SubBlock {
   int part, a;
   std::vector<int> rows;
+  std::vector<int> rows2;  // Z phase, m >= 1: the Im rows that take the same operator (dual block)
 };
 std::vector<SubBlock> phase_subblocks(int p, int ph) {
   const int NR = hsize(p);
   auto re = [&](int n, int m) { return hidx(n, m); };
   auto im = [&](int n, int m) { return NR + n * (n - 1) / 2 + m - 1; };
   std::vector<SubBlock> out;
+  if (ph == 1) {
+    // Z_m is the same for the Re and the Im rows of order m: sub-block m >= 1 is dual (its
+    // operator fragments are loaded once and applied to both row sets); m = 0 has Re rows only
+    for (int a = 0; a <= p; ++a) {
+      SubBlock b{0, a, {}, {}};
+      for (int n = a; n <= p; ++n) {
+        b.rows.push_back(re(n, a));
+        if (a > 0) b.rows2.push_back(im(n, a));
+      }
+      out.push_back(b);
+    }
+    return out;
+  }
   for (int part = 0; part < 2; ++part)
     for (int a = part; a <= p; ++a) {
-      SubBlock b{part, a, {}};
-      if (ph != 1)
-        for (int m = part; m <= a; ++m) b.rows.push_back(part ? im(a, m) : re(a, m));
-      else
-        for (int n = a; n <= p; ++n) b.rows.push_back(part ? im(n, a) : re(n, a));
+      SubBlock b{part, a, {}, {}};
+      for (int m = part; m <= a; ++m) b.rows.push_back(part ? im(a, m) : re(a, m));
       out.push_back(b);
     }
   return out;
@@ -495,6 +511,7 @@ std::vector<SubBlock> phase_subblocks(int p, int ph) {
 // Merged blocks: sub-blocks placed block-diagonally in one operator when that costs no
 // more DMMA fragments than running them apart (the padding of a large block absorbs a
 // small one), so a phase is ~17 near-square blocks instead of 2p + 1 at p = 15.
+// (a sub-block without a second row set is never merged with dual ones)
 std::vector<std::vector<int>> merge_subblocks(const std::vector<SubBlock>& sb) {
   std::vector<int> order(sb.size());
   for (size_t i = 0; i < sb.size(); ++i) order[i] = int(i);
@@ -513,6 +530,7 @@ std::vector<std::vector<int>> merge_subblocks(const std::vector<SubBlock>& sb) {
       for (int j : order) {  // largest sub-block that fits for free
         if (used[j]) continue;
         const int u = int(sb[j].rows.size());
+        if (sb[j].rows2.empty() != sb[i].rows2.empty()) continue;
         if (s + u > kMaxBlock || pad_blk(s + u) > cost + pad_blk(u)) continue;
         used[j] = 1;
         gr.push_back(j);
@@ -549,19 +567,31 @@ PasLayout make_layout(int p) {
     L.hd.base[ph] = int(L.tab.size());
     std::vector<int> rowoff{0}, rows, sizes;
     int oo = 0;
+    std::vector<char> dual;
     for (const auto& gr : G) {
-      for (int i : gr) rows.insert(rows.end(), L.sub[ph][i].rows.begin(), L.sub[ph][i].rows.end());
+      int sz = 0;
+      for (int i : gr) {
+        rows.insert(rows.end(), L.sub[ph][i].rows.begin(), L.sub[ph][i].rows.end());
+        sz += int(L.sub[ph][i].rows.size());
+      }
+      // a dual block lists its second row set after the first (the kernel runs the block
+      // twice with the operator fragments in registers)
+      dual.push_back(!L.sub[ph][gr[0]].rows2.empty());
+      for (int i : gr) rows.insert(rows.end(), L.sub[ph][i].rows2.begin(), L.sub[ph][i].rows2.end());
       rowoff.push_back(int(rows.size()));
-      sizes.push_back(rowoff.back() - rowoff[rowoff.size() - 2]);
+      sizes.push_back(sz);
       L.opoff[ph].push_back(oo);
-      oo += pad_blk(sizes.back());
+      oo += pad_blk(sz);
     }
+    // the kernel tells dual blocks by position: Z phase, every block but the first
+    for (int b = 0; b < nblk; ++b)
+      if (bool(dual[b]) != (ph == 1 && b > 0)) throw std::logic_error("m2l_pas: unexpected dual block order");
     L.phase_size = std::max(L.phase_size, oo);
     // whole blocks per warp, longest processing time first; a block costs its DMMA
     // fragments plus a fixed latency share
     std::vector<int> order(nblk);
     for (int i = 0; i < nblk; ++i) order[i] = i;
-    auto cost = [&](int b) { return long(pad_blk(sizes[b])) + 96; };
+    auto cost = [&](int b) { return long(pad_blk(sizes[b])) * (dual[b] ? 2 : 1) + 96; };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
     std::vector<std::vector<int>> wl(kWarps);
     std::vector<long> load(kWarps, 0);
