@@ -279,7 +279,11 @@ int qbxg_create_sharded(const qbxg_config* cfg, const qbxg_geometry* geom, const
                         int32_t device, int32_t n_ranks, int32_t rank, qbxg_handle** out);
 /* phase 1: gather density, P2M, M2M of owned subtrees.
  * phase 2: M2M of straddling boxes, Stages 3-9 for owned boxes; potentials and
- *          centre coefficients of other ranks' targets are written as 0. */
+ *          centre coefficients of other ranks' targets are written as 0.
+ * Helmholtz handles take the complex interleaved DEVICE arrays of qbxg_apply_complex
+ * (weights [n_sources][2], dipoles [n_sources][3][2], potentials [n_targets][2],
+ * centre locals [n_centers][(p_qbx+1)^2][2]); the exchanged multipole rows are full
+ * complex tables, 2 (p_fmm+1)^2 doubles per box. */
 int qbxg_apply_phase(qbxg_handle* h, int32_t phase, const double* d_weights, const double* d_dipoles,
                      double* d_out_target_pot, double* d_out_center_coeffs, void* cuda_stream);
 /* Device multipole buffer (n_boxes rows of row_doubles, DFS order) and cuts
@@ -342,7 +346,7 @@ int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* w
                     const int32_t* association, int32_t p_qbx, double* out_pot);
 
 /* ---- Helmholtz FMM (cfg.kernel = QBXG_KERNEL_HELMHOLTZ_SL or _SL_DL,
- * cfg.helmholtz_k > 0, p_fmm <= 20, p_qbx <= 6, one GPU) ----------------------
+ * cfg.helmholtz_k > 0, p_fmm <= 20, p_qbx <= 6) ----------------------
  * Complex weights [n_sources][2] in, complex potentials [n_targets][2] out (caller
  * order), optional centre locals [n_centers][(p_qbx+1)^2][2] in the internal basis
  * L_n^m of  phi = sum L_n^m j_n(k|x-c|) Y_n^m(x-c)  (index n^2+n+m; orthonormal Y,
@@ -350,7 +354,10 @@ int qbxg_direct_qbx(int64_t n_sources, const double* source_pos, const double* w
  * same tree and lists as the Laplace path.  SL+DL: complex dipole moments
  * [n_sources][3][2] (m_x, m_y, m_z, each re, im) add m . grad_y G_k(x, y) -- e.g.
  * the Brakhage-Werner combination with w = -i eta q mu and
- * m = q mu n; dipoles_c must be NULL for the single layer. */
+ * m = q mu n; dipoles_c must be NULL for the single layer.  On a sharded handle
+ * (qbxg_create_sharded + qbxg_nccl_attach) every rank passes the whole density and
+ * receives the whole result: owned upward pass, multipole broadcast, downward pass
+ * for the rank's boxes, all-gather of the owned potentials / centre locals. */
 int qbxg_apply_complex(qbxg_handle* h, const double* weights_c, const double* dipoles_c_or_null,
                        double* out_target_pot_c, double* out_center_coeffs_c, qbxg_timings* timings);
 

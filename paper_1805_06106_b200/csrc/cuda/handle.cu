@@ -148,6 +148,8 @@ struct Handle {
   int2* h_m2m_pairs = nullptr;
   int2* h_l2l_pairs = nullptr;
   std::vector<int> h_m2m_off, h_l2l_off;  // (nlev x 8 + 1) offsets
+  int2* h_m2m_spairs = nullptr;           // sharded: M2M pairs into boxes whose subtree spans ranks
+  std::vector<int> h_m2m_soff;
   double2* h_cs = nullptr;                     // per operator e^{i m alpha}, m <= p (split form)
   int* h_ent_op = nullptr;                     // operator of every List-2 CSR entry (split form)
   double* h_zops = nullptr;   // per operator: Z blocks (fragment order)
@@ -491,6 +493,8 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.M = dalloc<double2>(O, size_t(nb) * HD.KP);
   HD.L = dalloc<double2>(O, size_t(nb) * HD.KP);
   HD.Lc = dalloc<double2>(O, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ);
+  // sharded: only the rank's centres are ever written; the others read as zero in the centre output
+  if (H.nranks > 1) QCK(cudaMemsetAsync(HD.Lc, 0, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ * sizeof(double2), s));
   HD.phi = dalloc<double2>(O, std::max<int64_t>(H.nconv, 1));
   HD.gaunt = dupload(O, helm_gaunt_table(p), s);
   dev::helm_upload_constants();
@@ -533,32 +537,38 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
              (V.box_center[3 * c + 2] > V.box_center[3 * par + 2] ? 1 : 0);
     };
     const auto& mk = H.mask;
-    std::vector<std::vector<int2>> m2m(size_t(H.nlev) * 8), l2l(size_t(H.nlev) * 8);
+    std::vector<std::vector<int2>> m2m(size_t(H.nlev) * 8), l2l(size_t(H.nlev) * 8), m2ms(size_t(H.nlev) * 8);
     for (int l = 0; l < H.nlev; ++l)
       for (int i = V.level_starts[l]; i < V.level_starts[l + 1]; ++i) {
         const int b = V.level_boxes[i];
+        // upward: boxes whose subtree is the rank's, and (after the exchange) those spanning ranks
         if (!(V.box_flags[b] & QBXG_BOX_LEAF) && (V.box_flags[b] & QBXG_BOX_HAS_SOURCES) &&
-            (mk[b] & QBXG_SHARD_SUBTREE))
+            (mk[b] & (QBXG_SHARD_SUBTREE | QBXG_SHARD_STRADDLE)))
           for (int k = V.child_starts[b]; k < V.child_starts[b + 1]; ++k) {
             const int c = V.children[k];
-            if (V.src_sub_count[c] > 0) m2m[size_t(l) * 8 + hoct(c, b)].push_back(make_int2(c, b));
+            if (V.src_sub_count[c] > 0)
+              ((mk[b] & QBXG_SHARD_SUBTREE) ? m2m : m2ms)[size_t(l) * 8 + hoct(c, b)].push_back(make_int2(c, b));
           }
         if (l > 0 && (V.box_flags[b] & (QBXG_BOX_TARGET | QBXG_BOX_TARGET_ANCESTOR)) && (mk[b] & QBXG_SHARD_DOWN)) {
           const int a = V.box_parent[b];
           l2l[size_t(l) * 8 + hoct(b, a)].push_back(make_int2(a, b));
         }
       }
-    std::vector<int2> pm, pl;
+    std::vector<int2> pm, pl, ps;
     H.h_m2m_off.assign(size_t(H.nlev) * 8 + 1, 0);
     H.h_l2l_off.assign(size_t(H.nlev) * 8 + 1, 0);
+    H.h_m2m_soff.assign(size_t(H.nlev) * 8 + 1, 0);
     for (size_t g = 0; g < m2m.size(); ++g) {
       pm.insert(pm.end(), m2m[g].begin(), m2m[g].end());
       H.h_m2m_off[g + 1] = int(pm.size());
+      ps.insert(ps.end(), m2ms[g].begin(), m2ms[g].end());
+      H.h_m2m_soff[g + 1] = int(ps.size());
       pl.insert(pl.end(), l2l[g].begin(), l2l[g].end());
       H.h_l2l_off[g + 1] = int(pl.size());
     }
     H.h_m2m_pairs = dupload(O, pm, s);
     H.h_l2l_pairs = dupload(O, pl, s);
+    if (!ps.empty()) H.h_m2m_spairs = dupload(O, ps, s);
     QCK(cudaStreamSynchronize(s));
   }
 
@@ -735,10 +745,13 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
 
 // One Helmholtz apply: d_wc complex weights (caller order, interleaved), d_pot
 // complex potentials (caller order), d_coeffs optional centre locals (caller order).
-void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot, double* d_coeffs, cudaStream_t s) {
+// phase bits as in run_device: 1 = density gather, P2M, M2M of the rank's subtrees;
+// 2 = M2M of straddling boxes (sharded), then Stages 3-9 for the rank's boxes.
+void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot, double* d_coeffs, cudaStream_t s,
+              int phase = 3) {
   dev::HelmData& HD = H.HD;
   auto& ev = H.ev;
-  int L = 0;
+  int L = (phase & 1) ? 0 : H.last_launches;
   const bool debug_sync = H.debug_sync;
   int stage_no = 0;
   auto chk = [&](int k) {
@@ -754,23 +767,35 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
       throw CudaError(std::string("CUDA error after Helmholtz launch group ") + std::to_string(stage_no) + ": " +
                       cudaGetErrorString(e));
   };
-  QCK(cudaEventRecord(ev[0], s));
-  if (HD.hmu && !d_muc) throw InvalidArgument("qbxg_apply_complex: Helmholtz SL+DL requires dipole moments");
-  if (!HD.hmu && d_muc) throw InvalidArgument("qbxg_apply_complex: dipoles given to a single-layer handle");
-  chk(dev::helm_gather(HD, H.ns, H.d_src_perm, d_wc, d_muc, s));
-  QCK(cudaMemsetAsync(HD.M, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
-  QCK(cudaMemsetAsync(HD.L, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
-  QCK(cudaMemsetAsync(HD.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double2), s));
-  QCK(cudaMemsetAsync(HD.bad, 0, sizeof(unsigned int), s));
-  QCK(cudaEventRecord(ev[1], s));
-  chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
-  QCK(cudaEventRecord(ev[2], s));
-  for (int l = H.nlev - 2; l >= 0; --l) {
-    for (int o = 0; o < 8; ++o) {  // octants in a fixed order: deterministic sums into the parents
-      const int a = H.h_m2m_off[size_t(l) * 8 + o], e = H.h_m2m_off[size_t(l) * 8 + o + 1];
-      chk(dev::helm_shift_pairs(HD, 0, H.h_m2m_pairs + a, e - a, H.h_ops_m2m[l] + size_t(o) * HD.KP * HD.KP, s));
+  if (phase & 1) {
+    QCK(cudaEventRecord(ev[0], s));
+    if (HD.hmu && !d_muc) throw InvalidArgument("qbxg_apply_complex: Helmholtz SL+DL requires dipole moments");
+    if (!HD.hmu && d_muc) throw InvalidArgument("qbxg_apply_complex: dipoles given to a single-layer handle");
+    chk(dev::helm_gather(HD, H.ns, H.d_src_perm, d_wc, d_muc, s));
+    QCK(cudaMemsetAsync(HD.M, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
+    QCK(cudaMemsetAsync(HD.L, 0, size_t(H.nb) * HD.KP * sizeof(double2), s));
+    QCK(cudaMemsetAsync(HD.phi, 0, size_t(std::max<int64_t>(H.nconv, 1)) * sizeof(double2), s));
+    QCK(cudaMemsetAsync(HD.bad, 0, sizeof(unsigned int), s));
+    QCK(cudaEventRecord(ev[1], s));
+    chk(dev::helm_p2m(HD, H.d_leaves, H.n_leaves, s));
+    QCK(cudaEventRecord(ev[2], s));
+    for (int l = H.nlev - 2; l >= 0; --l) {
+      for (int o = 0; o < 8; ++o) {  // octants in a fixed order: deterministic sums into the parents
+        const int a = H.h_m2m_off[size_t(l) * 8 + o], e = H.h_m2m_off[size_t(l) * 8 + o + 1];
+        chk(dev::helm_shift_pairs(HD, 0, H.h_m2m_pairs + a, e - a, H.h_ops_m2m[l] + size_t(o) * HD.KP * HD.KP, s));
+      }
     }
+    H.last_launches = L;
   }
+  if (!(phase & 2)) return;
+  // boxes whose subtree spans ranks: every rank recomputes them, children in the same
+  // octant order as the unsharded pass, once the owned multipoles have been exchanged
+  if (H.nranks > 1 && H.h_m2m_spairs)
+    for (int l = H.nlev - 2; l >= 0; --l)
+      for (int o = 0; o < 8; ++o) {
+        const int a = H.h_m2m_soff[size_t(l) * 8 + o], e = H.h_m2m_soff[size_t(l) * 8 + o + 1];
+        chk(dev::helm_shift_pairs(HD, 0, H.h_m2m_spairs + a, e - a, H.h_ops_m2m[l] + size_t(o) * HD.KP * HD.KP, s));
+      }
   QCK(cudaEventRecord(ev[3], s));
   chk(dev::helm_near(HD, H.d_near_boxes, H.n_ctr_boxes, s));
   chk(dev::helm_p2p(HD, H.d_tgt_boxes, H.n_tgt_boxes, s));
@@ -795,9 +820,21 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
   QCK(cudaEventRecord(ev[6], s));
   chk(dev::helm_ctr(HD, 0, HD.L, H.h_n_lctas, H.h_lctas, H.h_lctr, H.h_lctr, HD.Lc, 1, s));
   QCK(cudaEventRecord(ev[9], s));
+  if (H.nranks > 1)  // targets of other ranks stay zero until the result exchange
+    QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * 2 * sizeof(double), s));
   chk(dev::helm_eval(HD, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_tgt_boxes_eval,
                      H.d_tgt_boxes_eval, H.d_tgt_perm, d_pot, s));
+  // (sharded: the centre locals of other ranks' centres are zero from create on; nothing writes them)
   if (d_coeffs) chk(dev::helm_centre_out(HD, int(H.nc), H.d_ctr_perm, d_coeffs, s));
+  if (H.nranks > 1) {  // the rank's results into its segment of the gather buffers
+    const int64_t a = H.res_off[H.rank], e = H.res_off[H.rank + 1];
+    chk(dev::launch_pack(int(e - a), H.d_res_idx + a, 2, d_pot, H.d_res_buf + 2 * a, false, s));
+    if (d_coeffs) {
+      const int64_t ca = H.cres_off[H.rank], ce = H.cres_off[H.rank + 1];
+      chk(dev::launch_pack(int(ce - ca), H.d_cres_idx + ca, 2 * HD.KQ, d_coeffs, H.d_cres_buf + ca * 2 * HD.KQ, false,
+                           s));
+    }
+  }
   QCK(cudaEventRecord(ev[10], s));
   QCK(cudaGetLastError());
   H.timed_overlap = false;
@@ -822,7 +859,6 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL && cfg.kernel != QBXG_KERNEL_HELMHOLTZ_SL_DL)
     throw InvalidArgument("qbxg_create: unknown kernel");
   H.helm = cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL || cfg.kernel == QBXG_KERNEL_HELMHOLTZ_SL_DL;
-  if (H.helm && nranks > 1) throw InvalidArgument("qbxg_create: Helmholtz runs on one GPU in this build");
   if (H.helm && (cfg.p_fmm > 20 || cfg.p_qbx > 6))
     throw InvalidArgument("qbxg_create: Helmholtz supports p_fmm <= 20, p_qbx <= 6");
   if (H.helm && !(cfg.helmholtz_k > 0 && std::isfinite(cfg.helmholtz_k)))
@@ -1099,8 +1135,9 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
         throw InvalidArgument("qbxg_create_sharded: targets / centres not partitioned by the shard cuts");
       H.d_res_idx = dupload(O, ti, s);
       H.d_cres_idx = dupload(O, ci, s);
-      H.d_res_buf = dalloc<double>(O, std::max<int64_t>(H.nt, 1));
-      H.d_cres_buf = dalloc<double>(O, std::max<int64_t>(H.nc, 1) * 2 * D.kq);
+      // (Helmholtz: complex potentials, full (q+1)^2 tables of complex centre coefficients)
+      H.d_res_buf = dalloc<double>(O, std::max<int64_t>(H.nt, 1) * (H.helm ? 2 : 1));
+      H.d_cres_buf = dalloc<double>(O, std::max<int64_t>(H.nc, 1) * 2 * (H.helm ? (H.cfg.p_qbx + 1) * (H.cfg.p_qbx + 1) : D.kq));
       QCK(cudaStreamSynchronize(s));
     }
     {
@@ -1256,6 +1293,13 @@ Nccl& nccl() {
   return n;
 }
 
+// Box multipoles as rows of doubles (Laplace: half tables; Helmholtz: full complex tables)
+double* m_ptr(Handle& H) { return reinterpret_cast<double*>(H.helm ? H.HD.M : H.D.M); }
+size_t m_row(const Handle& H) { return size_t(2) * (H.helm ? H.HD.KP : H.D.kp); }
+// doubles per target potential / per centre in the result exchange
+int pot_w(const Handle& H) { return H.helm ? 2 : 1; }
+int coef_w(const Handle& H) { return 2 * (H.helm ? H.HD.KQ : H.D.kq); }
+
 void nck(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw NcclError(std::string(what) + ": " + nccl().GetErrorString(r));
 }
@@ -1265,12 +1309,12 @@ void nck(ncclResult_t r, const char* what) {
 void exchange_nccl(Handle& H, cudaStream_t s) {
   Nccl& n = nccl();
   auto comm = static_cast<ncclComm_t>(H.nccl_comm);
-  const size_t row = size_t(2) * H.D.kp;
+  const size_t row = m_row(H);
   nck(n.GroupStart(), "ncclGroupStart");
   for (int r = 0; r < H.nranks; ++r) {
     const size_t a = size_t(H.cuts[r]), b = size_t(H.cuts[r + 1]);
     if (b <= a) continue;
-    double* p = reinterpret_cast<double*>(H.D.M) + a * row;
+    double* p = m_ptr(H) + a * row;
     nck(n.Broadcast(p, p, (b - a) * row, ncclFloat64, r, comm, s), "ncclBroadcast");
   }
   nck(n.GroupEnd(), "ncclGroupEnd");
@@ -1378,11 +1422,13 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
 void exchange_results_nccl(Handle& H, double* d_pot, double* d_coeffs, cudaStream_t s) {
   Nccl& n = nccl();
   auto comm = static_cast<ncclComm_t>(H.nccl_comm);
-  const int w = 2 * H.D.kq;
+  const int w = coef_w(H), pw = pot_w(H);
   nck(n.GroupStart(), "ncclGroupStart");
   for (int r = 0; r < H.nranks; ++r) {
     const int64_t a = H.res_off[r], e = H.res_off[r + 1];
-    if (e > a) nck(n.Broadcast(H.d_res_buf + a, H.d_res_buf + a, size_t(e - a), ncclFloat64, r, comm, s), "ncclBroadcast");
+    if (e > a)
+      nck(n.Broadcast(H.d_res_buf + a * pw, H.d_res_buf + a * pw, size_t(e - a) * pw, ncclFloat64, r, comm, s),
+          "ncclBroadcast");
     if (d_coeffs) {
       const int64_t ca = H.cres_off[r], ce = H.cres_off[r + 1];
       if (ce > ca)
@@ -1391,7 +1437,7 @@ void exchange_results_nccl(Handle& H, double* d_pot, double* d_coeffs, cudaStrea
     }
   }
   nck(n.GroupEnd(), "ncclGroupEnd");
-  dev::launch_pack(int(H.nt), H.d_res_idx, 1, d_pot, H.d_res_buf, true, s);
+  dev::launch_pack(int(H.nt), H.d_res_idx, pw, d_pot, H.d_res_buf, true, s);
   if (d_coeffs) dev::launch_pack(int(H.nc), H.d_cres_idx, w, d_coeffs, H.d_cres_buf, true, s);
 }
 
@@ -1400,6 +1446,14 @@ void exchange_results_nccl(Handle& H, double* d_pot, double* d_coeffs, cudaStrea
 void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s) {
   if (H.nranks > 1 && !H.nccl_comm)
     throw InvalidArgument("sharded handle: attach NCCL (qbxg_nccl_attach) or drive qbxg_apply_phase");
+  if (H.helm) {  // complex interleaved arrays; no side stream
+    if (H.nranks == 1) return run_helm(H, d_w, d_mu, d_pot, d_coeffs, s);
+    run_helm(H, d_w, d_mu, d_pot, d_coeffs, s, 1);
+    exchange_nccl(H, s);
+    run_helm(H, d_w, d_mu, d_pot, d_coeffs, s, 2);
+    exchange_results_nccl(H, d_pot, d_coeffs, s);
+    return;
+  }
   if (H.nranks == 1) {
     run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 3, H.overlap ? NEAR_SIDE : NEAR_INLINE);
     return;
@@ -1620,10 +1674,12 @@ int qbxg_apply_phase(qbxg_handle* hp, int32_t phase, const double* d_weights, co
     if (phase == 1 && !d_weights) throw qbxg::InvalidArgument("qbxg_apply_phase: null weights");
     if (phase == 2 && !d_out_target_pot) throw qbxg::InvalidArgument("qbxg_apply_phase: null output");
     auto& H = hp->h;
-    if (H.helm) throw qbxg::InvalidArgument("qbxg_apply_phase: Helmholtz handle, use qbxg_apply_complex");
     QCK(cudaSetDevice(H.device));
     cudaStream_t s = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : H.stream;
-    qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, phase);
+    if (H.helm)  // complex interleaved device arrays (the layouts of qbxg_apply_complex)
+      qbxg::run_helm(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, phase);
+    else
+      qbxg::run_device(H, d_weights, d_dipoles, d_out_target_pot, d_out_center_coeffs, s, phase);
     QCK(cudaStreamSynchronize(s));
     if (phase == 2) qbxg::check_domain(H, s);
   });
@@ -1633,8 +1689,8 @@ int qbxg_multipole_buffer(qbxg_handle* hp, double** d_multipoles, int64_t* row_d
   return qbxg::guarded([&] {
     if (!hp || !d_multipoles || !row_doubles) throw qbxg::InvalidArgument("qbxg_multipole_buffer: null argument");
     auto& H = hp->h;
-    *d_multipoles = reinterpret_cast<double*>(H.D.M);
-    *row_doubles = int64_t(2) * H.D.kp;
+    *d_multipoles = qbxg::m_ptr(H);
+    *row_doubles = int64_t(qbxg::m_row(H));
     if (cuts) std::copy(H.cuts.begin(), H.cuts.end(), cuts);
   });
 }
@@ -1645,13 +1701,14 @@ int qbxg_exchange_local(qbxg_handle** hs, int32_t n) {
     for (int r = 0; r < n; ++r) {
       auto& src = hs[r]->h;
       if (src.nranks != n || src.rank != r) throw qbxg::InvalidArgument("qbxg_exchange_local: handles not rank-ordered");
-      const size_t row = size_t(2) * src.D.kp * sizeof(double);
+      const size_t row = qbxg::m_row(src);
       const size_t a = size_t(src.cuts[r]), b = size_t(src.cuts[r + 1]);
       for (int q = 0; q < n; ++q) {
         if (q == r || b <= a) continue;
         auto& dst = hs[q]->h;
-        QCK(cudaMemcpy(reinterpret_cast<char*>(dst.D.M) + a * row, reinterpret_cast<char*>(src.D.M) + a * row,
-                       (b - a) * row, cudaMemcpyDefault));
+        if (dst.helm != src.helm) throw qbxg::InvalidArgument("qbxg_exchange_local: mixed kernels");
+        QCK(cudaMemcpy(qbxg::m_ptr(dst) + a * row, qbxg::m_ptr(src) + a * row, (b - a) * row * sizeof(double),
+                       cudaMemcpyDefault));
       }
     }
   });
@@ -1661,17 +1718,19 @@ int qbxg_result_exchange_local(qbxg_handle** hs, int32_t n, double* const* d_pot
   return qbxg::guarded([&] {
     if (!hs || n < 1 || !d_pots) throw qbxg::InvalidArgument("qbxg_result_exchange_local: bad argument");
     for (int r = 0; r < n; ++r)
-      if (hs[r]->h.nranks != n || hs[r]->h.rank != r || hs[r]->h.helm)
+      if (hs[r]->h.nranks != n || hs[r]->h.rank != r || hs[r]->h.helm != hs[0]->h.helm)
         throw qbxg::InvalidArgument("qbxg_result_exchange_local: handles not rank-ordered");
     for (int r = 0; r < n; ++r) QCK(cudaStreamSynchronize(hs[r]->h.stream));
     for (int r = 0; r < n; ++r) {  // each rank's packed segment into every other rank's buffers
       auto& src = hs[r]->h;
-      const int w = 2 * src.D.kq;
+      const int w = qbxg::coef_w(src), pw = qbxg::pot_w(src);
       for (int q = 0; q < n; ++q) {
         if (q == r) continue;
         auto& dst = hs[q]->h;
         const int64_t a = src.res_off[r], e = src.res_off[r + 1];
-        if (e > a) QCK(cudaMemcpy(dst.d_res_buf + a, src.d_res_buf + a, size_t(e - a) * sizeof(double), cudaMemcpyDefault));
+        if (e > a)
+          QCK(cudaMemcpy(dst.d_res_buf + a * pw, src.d_res_buf + a * pw, size_t(e - a) * pw * sizeof(double),
+                         cudaMemcpyDefault));
         const int64_t ca = src.cres_off[r], ce = src.cres_off[r + 1];
         if (d_coeffs && ce > ca)
           QCK(cudaMemcpy(dst.d_cres_buf + ca * w, src.d_cres_buf + ca * w, size_t(ce - ca) * w * sizeof(double),
@@ -1680,9 +1739,9 @@ int qbxg_result_exchange_local(qbxg_handle** hs, int32_t n, double* const* d_pot
     }
     for (int r = 0; r < n; ++r) {
       auto& H = hs[r]->h;
-      qbxg::dev::launch_pack(int(H.nt), H.d_res_idx, 1, d_pots[r], H.d_res_buf, true, H.stream);
+      qbxg::dev::launch_pack(int(H.nt), H.d_res_idx, qbxg::pot_w(H), d_pots[r], H.d_res_buf, true, H.stream);
       if (d_coeffs && d_coeffs[r])
-        qbxg::dev::launch_pack(int(H.nc), H.d_cres_idx, 2 * H.D.kq, d_coeffs[r], H.d_cres_buf, true, H.stream);
+        qbxg::dev::launch_pack(int(H.nc), H.d_cres_idx, qbxg::coef_w(H), d_coeffs[r], H.d_cres_buf, true, H.stream);
       QCK(cudaStreamSynchronize(H.stream));
     }
   });
@@ -1842,7 +1901,8 @@ int qbxg_apply_complex(qbxg_handle* hp, const double* weights_c, const double* d
     QCK(cudaEventRecord(H.ev[11], s));
     QCK(cudaMemcpyAsync(H.d_wc, weights_c, 2 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
     if (dipoles_c) QCK(cudaMemcpyAsync(H.d_muc, dipoles_c, 6 * H.ns * sizeof(double), cudaMemcpyHostToDevice, s));
-    qbxg::run_helm(H, H.d_wc, dipoles_c ? H.d_muc : nullptr, H.d_potc, out_center_coeffs_c ? H.d_coeffc : nullptr, s);
+    // (sharded handles: owned upward pass, NCCL multipole exchange, downward pass, result all-gather)
+    qbxg::full_apply(H, H.d_wc, dipoles_c ? H.d_muc : nullptr, H.d_potc, out_center_coeffs_c ? H.d_coeffc : nullptr, s);
     QCK(cudaMemcpyAsync(out_target_pot_c, H.d_potc, 2 * H.nt * sizeof(double), cudaMemcpyDeviceToHost, s));
     const size_t cbytes = size_t(H.nc) * 2 * H.HD.KQ * sizeof(double);
     if (out_center_coeffs_c) QCK(cudaMemcpyAsync(out_center_coeffs_c, H.d_coeffc, cbytes, cudaMemcpyDeviceToHost, s));

@@ -108,3 +108,52 @@ def test_sharded_result_allgather_equals_single_bitwise(nranks):
         assert np.array_equal(cc[..., 0] + 1j * cc[..., 1], c1)
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_helmholtz_sharded_equals_single_bitwise(nranks, kernel):
+    """Helmholtz SL and SL+DL (complex128) over Morton shards: phases driven per rank with
+    complex device arrays, full complex multipole rows exchanged, the packed owned results
+    all-gathered -- every rank ends with the single-GPU result, bitwise."""
+    import torch
+    K = 3.0
+    g = api.config_geometry(2, level=2, n_volume_targets=2000)
+    cfg = api.FmmConfig(p_fmm=8, p_qbx=4, n_max=64, kernel=kernel, helmholtz_k=K)
+    plan = api.Plan(cfg, g)
+    rng = np.random.default_rng(11)
+    w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
+    mu = None
+    if kernel == 3:
+        mu = np.ascontiguousarray((w[:, None] * rng.standard_normal((g.n_sources, 3))).astype(np.complex128))
+    ref = api.FmmEngine(cfg, g, plan)
+    pot1, c1 = ref.apply_complex(w, mu, want_centers=True)
+    ref.close()
+    kq = (cfg.p_qbx + 1) ** 2
+    dev = torch.device("cuda", 0)
+    dw = torch.from_numpy(w.view(np.float64).copy()).to(dev)
+    dm = torch.from_numpy(mu.reshape(-1).view(np.float64).copy()).to(dev) if mu is not None else None
+    engines = [api.FmmEngine(cfg, g, plan, shard=(nranks, r)) for r in range(nranks)]
+    _, row, cuts = engines[0].multipole_buffer()
+    assert row == 2 * (cfg.p_fmm + 1) ** 2 and len(cuts) == nranks + 1
+    pots = [torch.empty(2 * g.n_targets, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    coefs = [torch.empty(2 * g.n_centers * kq, dtype=torch.float64, device=dev) for _ in range(nranks)]
+    mp = dm.data_ptr() if dm is not None else None
+    for e in engines:
+        e.apply_phase(1, dw.data_ptr(), mp, None)
+    api.exchange_local(engines)
+    for e, p, c in zip(engines, pots, coefs):
+        e.apply_phase(2, dw.data_ptr(), mp, p.data_ptr(), c.data_ptr())
+    torch.cuda.synchronize()
+    # before the result exchange: the ranks' outputs partition the result (zeros elsewhere)
+    psum = sum(p for p in pots).cpu().numpy().view(np.complex128)
+    nz = sum((p.view(-1, 2) != 0).any(dim=1).to(torch.int32) for p in pots).cpu().numpy()
+    assert nz.max() <= 1
+    assert np.array_equal(psum, pot1)
+    api.exchange_results_local(engines, [p.data_ptr() for p in pots], [c.data_ptr() for c in coefs])
+    torch.cuda.synchronize()
+    for p, c in zip(pots, coefs):
+        assert np.array_equal(p.cpu().numpy().view(np.complex128), pot1)
+        assert np.array_equal(c.cpu().numpy().view(np.complex128).reshape(g.n_centers, kq), c1)
+    for e in engines:
+        e.close()
