@@ -275,6 +275,8 @@ int qbxg_destroy(qbxg_handle* h);
  * qbxg_apply_device then need an NCCL communicator (qbxg_nccl_attach) and
  * return complete results on every rank.  Without NCCL, drive the phases and
  * the multipole exchange yourself: */
+/* (n_ranks = 1 is allowed: the handle then runs the same protocol -- packed results,
+ * NCCL broadcasts -- on a communicator of one rank; tests use it to exercise NCCL.) */
 int qbxg_create_sharded(const qbxg_config* cfg, const qbxg_geometry* geom, const qbxg_plan* plan,
                         int32_t device, int32_t n_ranks, int32_t rank, qbxg_handle** out);
 /* phase 1: gather density, P2M, M2M of owned subtrees.

@@ -123,6 +123,9 @@ struct Handle {
   std::vector<dev::ShiftLevel> m2m_straddle;  // per level, recomputed after the exchange
   // sharding: rank's role bits per box and the global cuts
   int nranks = 1, rank = 0;
+  // results packed per rank and gathered (sharded handles; also a one-rank handle made by
+  // qbxg_create_sharded, which runs the whole NCCL protocol on a communicator of one)
+  bool gather = false;
   std::vector<uint8_t> mask;
   std::vector<int32_t> cuts;
   int* d_eval_assoc = nullptr;   // owned associated targets (original index)
@@ -494,7 +497,7 @@ void helm_setup(Handle& H, const qbxg_plan_view& V, const std::vector<int64_t>& 
   HD.L = dalloc<double2>(O, size_t(nb) * HD.KP);
   HD.Lc = dalloc<double2>(O, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ);
   // sharded: only the rank's centres are ever written; the others read as zero in the centre output
-  if (H.nranks > 1) QCK(cudaMemsetAsync(HD.Lc, 0, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ * sizeof(double2), s));
+  if (H.gather) QCK(cudaMemsetAsync(HD.Lc, 0, size_t(std::max<int64_t>(H.nc, 1)) * HD.KQ * sizeof(double2), s));
   HD.phi = dalloc<double2>(O, std::max<int64_t>(H.nconv, 1));
   HD.gaunt = dupload(O, helm_gaunt_table(p), s);
   dev::helm_upload_constants();
@@ -820,13 +823,13 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
   QCK(cudaEventRecord(ev[6], s));
   chk(dev::helm_ctr(HD, 0, HD.L, H.h_n_lctas, H.h_lctas, H.h_lctr, H.h_lctr, HD.Lc, 1, s));
   QCK(cudaEventRecord(ev[9], s));
-  if (H.nranks > 1)  // targets of other ranks stay zero until the result exchange
+  if (H.gather)  // targets of other ranks stay zero until the result exchange
     QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * 2 * sizeof(double), s));
   chk(dev::helm_eval(HD, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_tgt_boxes_eval,
                      H.d_tgt_boxes_eval, H.d_tgt_perm, d_pot, s));
   // (sharded: the centre locals of other ranks' centres are zero from create on; nothing writes them)
   if (d_coeffs) chk(dev::helm_centre_out(HD, int(H.nc), H.d_ctr_perm, d_coeffs, s));
-  if (H.nranks > 1) {  // the rank's results into its segment of the gather buffers
+  if (H.gather) {  // the rank's results into its segment of the gather buffers
     const int64_t a = H.res_off[H.rank], e = H.res_off[H.rank + 1];
     chk(dev::launch_pack(int(e - a), H.d_res_idx + a, 2, d_pot, H.d_res_buf + 2 * a, false, s));
     if (d_coeffs) {
@@ -842,8 +845,9 @@ void run_helm(Handle& H, const double* d_wc, const double* d_muc, double* d_pot,
 }
 
 void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbxg_plan* plan, int device,
-            int nranks = 1, int rank = 0) {
+            int nranks = 1, int rank = 0, bool sharded = false) {
   check_device();
+  H.gather = sharded || nranks > 1;
   if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("qbxg_create: bad rank / n_ranks");
   {
     qbxg_plan_view V0;
@@ -1106,7 +1110,7 @@ void create(Handle& H, const qbxg_config& cfg, const qbxg_geometry& g, const qbx
       for (int j = 0; j < V.ctr_own_count[b]; ++j) fw.push_back(V.ctr_own_start[b] + j);
     H.d_ctr_box = dupload(O, cbox, s);
     H.d_flat_all = dupload(O, all, s);
-    if (nranks > 1) {
+    if (H.gather) {
       // result all-gather layout: rank-major segments of every rank's owned targets
       // (associated in target order, then conventional in box order) and centres
       auto owner = [&](int b) {
@@ -1394,14 +1398,14 @@ void run_device(Handle& H, const double* d_w, const double* d_mu, double* d_pot,
   H.timed_overlap = near == NEAR_SIDE;
   chk(dev::launch_l2qbxl3(D, H.d_flat_all, H.d_l3_ctas, H.n_l3_ctas, H.d_ctr_box, s));
   QCK(cudaEventRecord(ev[9], s));
-  if (H.nranks > 1) {  // targets / centres of other ranks stay zero until the result exchange
+  if (H.gather) {  // targets / centres of other ranks stay zero until the result exchange
     QCK(cudaMemsetAsync(d_pot, 0, size_t(std::max<int64_t>(H.nt, 1)) * sizeof(double), s));
     if (d_coeffs) QCK(cudaMemsetAsync(d_coeffs, 0, size_t(std::max<int64_t>(H.nc, 1)) * 2 * D.kq * sizeof(double), s));
   }
   chk(dev::launch_eval(D, H.n_eval_assoc, H.d_eval_assoc, H.d_tpos, H.d_assoc, H.d_ctr_sorted, H.n_eval_conv,
                        H.d_eval_conv, H.d_tgt_perm, H.d_tgt_box, d_pot, s));
   if (d_coeffs) chk(dev::launch_centre_out(D, H.n_own_ctr, H.d_flat_all, H.d_ctr_perm, d_coeffs, s));
-  if (H.nranks > 1) {  // the rank's results into its segment of the gather buffers
+  if (H.gather) {  // the rank's results into its segment of the gather buffers
     const int64_t a = H.res_off[H.rank], e = H.res_off[H.rank + 1];
     chk(dev::launch_pack(int(e - a), H.d_res_idx + a, 1, d_pot, H.d_res_buf + a, false, s));
     if (d_coeffs) {
@@ -1444,17 +1448,17 @@ void exchange_results_nccl(Handle& H, double* d_pot, double* d_coeffs, cudaStrea
 // One whole apply.  Sharded: owned upward pass (near field forked beside it), multipole
 // exchange (NCCL), straddling M2M, downward + QBX stages, result all-gather.
 void full_apply(Handle& H, const double* d_w, const double* d_mu, double* d_pot, double* d_coeffs, cudaStream_t s) {
-  if (H.nranks > 1 && !H.nccl_comm)
+  if (H.gather && !H.nccl_comm)
     throw InvalidArgument("sharded handle: attach NCCL (qbxg_nccl_attach) or drive qbxg_apply_phase");
   if (H.helm) {  // complex interleaved arrays; no side stream
-    if (H.nranks == 1) return run_helm(H, d_w, d_mu, d_pot, d_coeffs, s);
+    if (!H.gather) return run_helm(H, d_w, d_mu, d_pot, d_coeffs, s);
     run_helm(H, d_w, d_mu, d_pot, d_coeffs, s, 1);
     exchange_nccl(H, s);
     run_helm(H, d_w, d_mu, d_pot, d_coeffs, s, 2);
     exchange_results_nccl(H, d_pot, d_coeffs, s);
     return;
   }
-  if (H.nranks == 1) {
+  if (!H.gather) {
     run_device(H, d_w, d_mu, d_pot, d_coeffs, s, 3, H.overlap ? NEAR_SIDE : NEAR_INLINE);
     return;
   }
@@ -1505,7 +1509,7 @@ void batch_apply(Handle& H, int R, const double* d_w, const double* d_mu, double
   // density than the shared harmonic table plus one contraction per density (76.9 vs 81.6 ms
   // per density at config 1), so only the single layer is batched through the near field
   const int NR = D.dipole ? 1 : dev::near_batch_width(D.q);
-  if (H.nranks > 1 || NR < 2 || R < 2) {
+  if (H.gather || NR < 2 || R < 2) {
     for (int r = 0; r < R; ++r)
       full_apply(H, d_w + size_t(r) * H.ns, d_mu ? d_mu + size_t(r) * 3 * H.ns : nullptr, d_pot + size_t(r) * H.nt,
                  d_coeffs ? d_coeffs + size_t(r) * H.nc * 2 * D.kq : nullptr, s);
@@ -1658,7 +1662,7 @@ int qbxg_create_sharded(const qbxg_config* cfg, const qbxg_geometry* geom, const
     if (!cfg || !geom || !plan || !out) throw qbxg::InvalidArgument("qbxg_create_sharded: null argument");
     auto* h = new qbxg_handle;
     try {
-      qbxg::create(h->h, *cfg, *geom, plan, device, n_ranks, rank);
+      qbxg::create(h->h, *cfg, *geom, plan, device, n_ranks, rank, true);
     } catch (...) {
       delete h;
       throw;

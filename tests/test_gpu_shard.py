@@ -157,3 +157,37 @@ def test_helmholtz_sharded_equals_single_bitwise(nranks, kernel):
         assert np.array_equal(c.cpu().numpy().view(np.complex128).reshape(g.n_centers, kq), c1)
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("kernel", ["laplace_sl_dl", "helmholtz_sl_dl"])
+def test_nccl_protocol_on_a_communicator_of_one(kernel):
+    """The production multi-GPU path end to end through NCCL itself (libnccl loaded at run
+    time, ncclCommInitRank, the grouped in-place multipole broadcast, the grouped result
+    broadcasts and the scatter) on a communicator of one rank: a handle from
+    qbxg_create_sharded(n_ranks = 1) runs phase 1 -> exchange -> phase 2 -> result gather
+    inside qbxg_apply / qbxg_apply_complex.  Bitwise equal to the unsharded handle."""
+    if kernel == "laplace_sl_dl":
+        g = api.config_geometry(1, nu=48, nv=24)
+        cfg = api.config_fmm(1)
+        w, mu = g.weights(), g.dipoles()
+        run = lambda e: e.apply(w, mu, want_centers=True)
+    else:
+        g = api.config_geometry(3, level=2)
+        cfg = api.FmmConfig(p_fmm=8, p_qbx=4, n_max=64, kernel=3, helmholtz_k=3.0)
+        rng = np.random.default_rng(5)
+        w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
+        mu = np.ascontiguousarray(w[:, None] * rng.standard_normal((g.n_sources, 3)))
+        run = lambda e: e.apply_complex(w, mu, want_centers=True)
+    plan = api.Plan(cfg, g)
+    ref = api.FmmEngine(cfg, g, plan)
+    pot1, c1 = run(ref)
+    ref.close()
+    eng = api.FmmEngine(cfg, g, plan, shard=(1, 0))
+    with pytest.raises(ValueError, match="attach NCCL"):
+        run(eng)
+    eng.attach_nccl(api.FmmEngine.nccl_unique_id())
+    pot, c = run(eng)
+    pot2, _ = run(eng)
+    eng.close()
+    assert np.array_equal(pot, pot1) and np.array_equal(c, c1)
+    assert np.array_equal(pot2, pot1)
