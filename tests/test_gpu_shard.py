@@ -110,16 +110,18 @@ def test_sharded_result_allgather_equals_single_bitwise(nranks):
         e.close()
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
-@pytest.mark.parametrize("kernel", [2, 3])
-def test_helmholtz_sharded_equals_single_bitwise(nranks, kernel):
+@pytest.mark.parametrize("nranks,kernel,p,q,geo", [
+    (2, 2, 8, 4, "urchin_vol"), (3, 2, 8, 4, "urchin_vol"), (2, 3, 8, 4, "urchin_vol"), (3, 3, 8, 4, "urchin_vol"),
+    (2, 3, 20, 5, "sphere3")])  # the last: BASELINE config 3's orders on a level-3 sphere
+def test_helmholtz_sharded_equals_single_bitwise(nranks, kernel, p, q, geo):
     """Helmholtz SL and SL+DL (complex128) over Morton shards: phases driven per rank with
     complex device arrays, full complex multipole rows exchanged, the packed owned results
     all-gathered -- every rank ends with the single-GPU result, bitwise."""
     import torch
     K = 3.0
-    g = api.config_geometry(2, level=2, n_volume_targets=2000)
-    cfg = api.FmmConfig(p_fmm=8, p_qbx=4, n_max=64, kernel=kernel, helmholtz_k=K)
+    g = (api.config_geometry(2, level=2, n_volume_targets=2000) if geo == "urchin_vol"
+         else api.config_geometry(3, level=3))
+    cfg = api.FmmConfig(p_fmm=p, p_qbx=q, n_max=64, kernel=kernel, helmholtz_k=K)
     plan = api.Plan(cfg, g)
     rng = np.random.default_rng(11)
     w = g.quad_weight * (rng.uniform(-1, 1, g.n_sources) + 1j * rng.uniform(-1, 1, g.n_sources))
