@@ -1702,6 +1702,7 @@ int qbxg_multipole_buffer(qbxg_handle* hp, double** d_multipoles, int64_t* row_d
 int qbxg_exchange_local(qbxg_handle** hs, int32_t n) {
   return qbxg::guarded([&] {
     if (!hs || n < 1) throw qbxg::InvalidArgument("qbxg_exchange_local: bad argument");
+    QCK(cudaDeviceSynchronize());  // phase 1 of every rank complete, whatever stream it ran on
     for (int r = 0; r < n; ++r) {
       auto& src = hs[r]->h;
       if (src.nranks != n || src.rank != r) throw qbxg::InvalidArgument("qbxg_exchange_local: handles not rank-ordered");
@@ -1715,6 +1716,9 @@ int qbxg_exchange_local(qbxg_handle** hs, int32_t n) {
                        cudaMemcpyDefault));
       }
     }
+    // device-to-device cudaMemcpy does not wait on the host, and the handles' streams do
+    // not synchronise with the default stream: phase 2 must not start before the rows land
+    QCK(cudaDeviceSynchronize());
   });
 }
 
@@ -1741,6 +1745,7 @@ int qbxg_result_exchange_local(qbxg_handle** hs, int32_t n, double* const* d_pot
                          cudaMemcpyDefault));
       }
     }
+    QCK(cudaDeviceSynchronize());  // (device-to-device copies above: see qbxg_exchange_local)
     for (int r = 0; r < n; ++r) {
       auto& H = hs[r]->h;
       qbxg::dev::launch_pack(int(H.nt), H.d_res_idx, qbxg::pot_w(H), d_pots[r], H.d_res_buf, true, H.stream);

@@ -193,3 +193,37 @@ def test_nccl_protocol_on_a_communicator_of_one(kernel):
     eng.close()
     assert np.array_equal(pot, pot1) and np.array_equal(c, c1)
     assert np.array_equal(pot2, pot1)
+
+
+def test_sharded_full_config1_equals_single_bitwise():
+    """The bench workload (BASELINE config 1 at full size: 1,048,576 sources, 180,081 boxes)
+    over 4 emulated ranks: every rank ends with the single-GPU potentials, bitwise.  (At this
+    size the ~400 MB of exchanged multipole rows once exposed a race in the emulated exchange,
+    which copied device to device without waiting: qbxg_exchange_local now synchronises.)"""
+    import torch
+    g = api.config_geometry(1)
+    cfg = api.config_fmm(1)
+    plan = api.Plan(cfg, g)
+    w, mu = g.weights(), g.dipoles()
+    dev = torch.device("cuda", 0)
+    dw = torch.from_numpy(w).to(dev)
+    dm = torch.from_numpy(mu.reshape(-1)).to(dev)
+    p1 = torch.empty(g.n_targets, dtype=torch.float64, device=dev)
+    ref = api.FmmEngine(cfg, g, plan)
+    ref.apply_device(dw.data_ptr(), dm.data_ptr(), p1.data_ptr(), None, None)
+    torch.cuda.synchronize()
+    ref.close()
+    n = 4
+    engines = [api.FmmEngine(cfg, g, plan, shard=(n, r)) for r in range(n)]
+    pots = [torch.empty(g.n_targets, dtype=torch.float64, device=dev) for _ in range(n)]
+    for e in engines:
+        e.apply_phase(1, dw.data_ptr(), dm.data_ptr(), None)
+    api.exchange_local(engines)
+    for e, p in zip(engines, pots):
+        e.apply_phase(2, dw.data_ptr(), dm.data_ptr(), p.data_ptr(), None)
+    api.exchange_results_local(engines, [p.data_ptr() for p in pots], None)
+    torch.cuda.synchronize()
+    for p in pots:
+        assert torch.equal(p, p1)
+    for e in engines:
+        e.close()
