@@ -54,7 +54,15 @@ def main():
     pot1 = p1.cpu().numpy()
     ref.close()
 
-    engines = [api.FmmEngine(cfg, g, plan, shard=(n, r)) for r in range(n)]
+    engines, per_engine = [], 0
+    for r in range(n):  # bounded memory: stop before the next handle would not fit
+        free0 = torch.cuda.mem_get_info(dev)[0]
+        if per_engine and free0 < 1.3 * per_engine + (8 << 30):
+            print(json.dumps({"tool": "shard_times", "config": cid, "n_ranks": n, "skipped":
+                              f"handle {r} of {n} would not fit: {free0 >> 30} GiB free, {per_engine >> 30} GiB per handle"}))
+            return
+        engines.append(api.FmmEngine(cfg, g, plan, shard=(n, r)))
+        per_engine = max(per_engine, free0 - torch.cuda.mem_get_info(dev)[0])
     pots = [torch.empty(g.n_targets, dtype=torch.float64, device=dev) for _ in range(n)]
     _, row, cuts = engines[0].multipole_buffer()
     t = np.zeros((reps + 1, 2, n))
@@ -98,6 +106,7 @@ def main():
         "multipole_exchange_bytes_total": int(nb) * int(row) * 8,
         "result_gather_bytes_total": int(g.n_targets) * 8,
         "box_cuts": [int(c) for c in cuts],
+        "device_gib_per_handle": round(per_engine / 2**30, 1),
         "bitwise_equal_to_single": bool(same), "n_targets_differing": ndiff, "max_rel_diff": maxdiff,
         "note": ("ranks emulated one after another on one B200: per-rank kernel time only; the NCCL "
                  "exchanges (sizes above; 900 GB/s per direction over NVLink 5) are not timed"),
