@@ -60,7 +60,10 @@ __global__ void k_gather_batch(int ns, int R, const int* __restrict__ perm, cons
 
 // ---------------------------------------------------------------- P2M (Stage 2)
 // M~_n^m = sum_s w conj(R_n^m(u)) + conj(mu . grad R_n^m(u)) / h,  u = (s - c)/h
-constexpr int kP2MBatch = 16;
+#ifndef QBXG_P2M_BATCH
+#define QBXG_P2M_BATCH 16  // sources per table batch; config 1: 8 -> 1.61 ms, 16 -> 1.41, 32 -> 1.71
+#endif
+constexpr int kP2MBatch = QBXG_P2M_BATCH;
 
 __global__ void __launch_bounds__(256) k_p2m(DevData D, const int* __restrict__ boxes) {
   extern __shared__ double2 sm[];
