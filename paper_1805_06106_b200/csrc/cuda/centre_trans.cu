@@ -96,10 +96,10 @@ __global__ void k_pair_reduce(const int* __restrict__ centres, const int* __rest
 // per (N, K) every thread issues 2 x hsize(q) complex FMAs against warp-broadcast
 // shared reads, with R_N^K streamed from a register recurrence.
 template <int Q>
-#ifndef QBXG_L3_MINB
-#define QBXG_L3_MINB 1  // resident CTAs asked of ptxas: 1 -> 166 registers, 3 CTAs per SM, 4.03 ms at config 1; 4 -> 128 registers with spills, 4.50 ms
-#endif
-__global__ void __launch_bounds__(kL3Threads, QBXG_L3_MINB) k_l2qbxl3(DevData D, const int* __restrict__ items,
+// (166 registers, 3 CTAs per SM: 4.03 ms at config 1.  Measured and not kept: a minimum of
+// 4 resident CTAs -> 128 registers with spills, 4.50 ms; a minimum of 1 -> ptxas takes more
+// registers still, 4.88 ms.)
+__global__ void __launch_bounds__(kL3Threads) k_l2qbxl3(DevData D, const int* __restrict__ items,
                                                         const int2* __restrict__ ctas,
                                                         const int* __restrict__ ctr_box) {
   constexpr int KQ = hsize(Q);
